@@ -1,0 +1,166 @@
+/*
+ * katzb200 -- C-ABI of the B200-native bounded-Katz ranking engine.
+ *
+ * The reference (katzbounds, arxiv 1807.03847) is a pure-Python package; it
+ * has no FFI of its own.  These entry points are the ones its Python engine
+ * would bind to hand the hot path to native code: each one replaces the
+ * reference function named beside it (paths under
+ * /root/reference/pkg/src/katzbounds/).  All functions return a status code
+ * (KB_OK == 0); on failure kb_last_error() gives a message.  Plain pointers
+ * and sizes only -- no torch or CUDA types cross this boundary.
+ *
+ * Id spaces: every array that crosses the ABI is indexed by the caller's
+ * (original) node ids.  Internally the device relabels rows by descending
+ * out-degree; that is invisible here.
+ *
+ * Ownership: host arrays are borrowed for the duration of a call; device
+ * memory is owned by the handles and freed by the *_destroy calls.
+ * Threading: a kb_state is used by one thread at a time; a kb_graph may be
+ * shared by many states (read-only) except during kb_update_batch.
+ */
+#ifndef KATZB200_H
+#define KATZB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> katzbounds.errors classes (errors.py:9-58) */
+enum {
+    KB_OK = 0,
+    KB_EPARAM = 1,        /* ParameterError       errors.py:29 */
+    KB_ESTATE = 2,        /* StateError           errors.py:33 */
+    KB_ECONVERGENCE = 3,  /* ConvergenceError     errors.py:37-50 */
+    KB_ENUMERIC = 4,      /* NumericError         errors.py:57 */
+    KB_EBATCH = 5,        /* BatchPreconditionError errors.py:25 */
+    KB_ENODERANGE = 6,    /* NodeRangeError       errors.py:21 */
+    KB_ECUDA = 7,         /* device failure (no reference analogue) */
+    KB_ENOMEM = 8
+};
+
+/* Criterion kinds (engine.py:28-31) */
+enum { KB_RANKING = 0, KB_TOPK = 1, KB_SCORE = 2, KB_PAIR = 3 };
+
+/* vectors readable through kb_get_vector */
+enum { KB_VEC_LEVEL = 0, KB_VEC_KATZ = 1, KB_VEC_LOWER = 2, KB_VEC_UPPER = 3 };
+
+typedef struct kb_graph kb_graph;
+typedef struct kb_state kb_state;
+
+typedef struct {
+    int64_t n;                /* node_count                                  */
+    int64_t nnz;              /* arcs                                        */
+    int64_t max_out_degree;   /* Graph.max_out_degree  graph.py:154-158      */
+    int64_t nonisolated;      /* rows with out-degree > 0                    */
+    int64_t heavy_rows;       /* rows split into segments (deg > threshold)  */
+    int64_t segments;         /* virtual rows covering the heavy rows        */
+    int64_t slices;           /* 32-row SELL slices                          */
+    int64_t sell_elems;       /* stored column slots incl. padding           */
+    int64_t split_threshold;  /* rows longer than this are segmented         */
+    int64_t hot_size;         /* leading (hottest) x entries staged in smem  */
+    int64_t version;          /* bumped by kb_update_batch                   */
+    int64_t device_bytes;     /* device memory held by the graph             */
+} kb_graph_info;
+
+typedef struct {
+    int64_t r;                /* KatzState.r                                 */
+    int64_t active;           /* KatzState.active.size                       */
+    int64_t max_iterations;   /* KatzState.max_iterations                    */
+    int64_t levels_kept;      /* len(KatzState.levels)                       */
+    double  alpha, gamma, epsilon;
+    double  last_check_ms;    /* device time of the last kb_check            */
+    double  spmv_ms;          /* summed device time of the K1 launches       */
+    int64_t spmv_launches;    /* number of K1 iterations timed in spmv_ms    */
+} kb_state_info;
+
+typedef struct {
+    int64_t batch_size, seeds, visited, reactivated, resumed_iterations;
+    int64_t aborted_level;    /* -1 == None                                  */
+    int64_t n_level_sizes;
+    int64_t level_sizes[64];  /* UpdateStats.level_sizes (dynamic.py:35)     */
+} kb_update_stats;
+
+/* ---- library ---- */
+const char *kb_last_error(void);
+int kb_version(void);
+int kb_device_count(int *count);
+
+/* ---- measurement plumbing (bench.py): device-stream timer, kernel launch
+ * counter, page-locking of caller buffers for the host<->device copies */
+int kb_timer(int device, int op /* 0 start, 1 stop */, double *elapsed_ms);
+int kb_launch_count(int64_t *count);
+int kb_host_register(void *ptr, int64_t bytes);
+int kb_host_unregister(void *ptr);
+
+/* ---- graph ingest: replaces Graph.out_csr() + the scipy CSR the engine
+ * reads (graph.py:177-197) with a device-resident, degree-relabelled SELL-32
+ * layout.  indptr: n+1 int64, indices: nnz int32, each row sorted ascending.
+ * split_threshold <= 0 and hot_size < 0 select the defaults. */
+int kb_graph_create(int device, int64_t n, int64_t nnz, const int64_t *indptr,
+                    const int32_t *indices, int64_t split_threshold,
+                    int64_t hot_size, kb_graph **out);
+/* Device generators, bit-identical to katzbounds.generate (generate.py:38-103)
+ * loaded with undirected=True: R-MAT on n = 2^scale nodes from numpy's PCG64
+ * stream whose current state is pcg_state = {state_hi, state_lo, inc_hi,
+ * inc_lo} (np.random.default_rng(seed).bit_generator.state); a, ab, abc are
+ * the quadrant thresholds exactly as generate.py:73-74 evaluates them. */
+int kb_graph_create_rmat(int device, int scale, int64_t edge_factor,
+                         const uint64_t *pcg_state, double a, double ab,
+                         double abc, int64_t split_threshold, int64_t hot_size,
+                         kb_graph **out);
+int kb_graph_create_grid(int device, int64_t n, int64_t split_threshold,
+                         int64_t hot_size, kb_graph **out);
+/* the canonical CSR (original ids, rows ascending): n+1 / nnz entries */
+int kb_graph_get_csr(kb_graph *g, int64_t *indptr, int32_t *indices);
+int kb_graph_destroy(kb_graph *g);
+int kb_graph_info_get(const kb_graph *g, kb_graph_info *info);
+/* Graph.is_symmetric (graph.py:168-175), evaluated on the device */
+int kb_graph_is_symmetric(kb_graph *g, int *symmetric);
+
+/* ---- state: replaces engine.init (engine.py:248-283).  alpha/gamma/cap are
+ * computed by the caller with the reference's own expressions
+ * (engine.py:96-119, :286-293) so the device sees bit-identical inputs. */
+int kb_state_create(kb_graph *g, double alpha, double gamma, int undirected,
+                    int kind, double epsilon, int64_t k, int64_t u, int64_t v,
+                    int keep_all_levels, int64_t max_iterations,
+                    kb_state **out);
+int kb_state_destroy(kb_state *s);
+int kb_state_info_get(const kb_state *s, kb_state_info *info);
+int kb_state_set_max_iterations(kb_state *s, int64_t max_iterations);
+
+/* iterate_once (engine.py:296-319), `steps` times, no stopping test */
+int kb_iterate(kb_state *s, int64_t steps);
+/* check_converged (engine.py:333-379); may shrink the active set */
+int kb_check(kb_state *s, int *converged);
+/* run (engine.py:382-396) without the final ranking_result: iterate+check on
+ * the device until converged; KB_ECONVERGENCE at the cap (r, gap via info) */
+int kb_run(kb_state *s, int *converged);
+/* KatzState.gap (engine.py:172-174) */
+int kb_gap(kb_state *s, double *gap);
+/* epsilon_separated (engine.py:322-330) */
+int kb_epsilon_separated(kb_state *s, int64_t w, int64_t v, int *separated);
+
+/* ranking_result (engine.py:399-408) + separated_fraction (:411-427):
+ * order (n int64), lower/upper (n fp64, by node id), and the exact number of
+ * separated ordered pairs; any output pointer may be NULL. */
+int kb_result(kb_state *s, int64_t *order, double *lower, double *upper,
+              int64_t *separated_pairs);
+int kb_separated_pairs(kb_state *s, int64_t *separated_pairs);
+
+/* read KatzState vectors (by node id): levels[level], katz, lower, upper */
+int kb_get_vector(kb_state *s, int which, int64_t level, double *out);
+/* KatzState.active in its current order (node ids); `out` holds >= active */
+int kb_get_active(kb_state *s, int64_t *out);
+
+/* dynamic.update_batch (dynamic.py:126-211): arcs as (src,dst) int64 pairs,
+ * already validated by the caller against the host graph. */
+int kb_update_batch(kb_state *s, const int64_t *ins, int64_t n_ins,
+                    const int64_t *dels, int64_t n_dels, double theta,
+                    double new_gamma, kb_update_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KATZB200_H */

@@ -163,7 +163,19 @@ def rmat_packed(n: int, edge_factor: int = 8, seed: int = 0,
     w = lib().oracle_rmat_pairs(s >> 64, s & M, inc >> 64, inc & M, scale, m,
                                 a, ab, abc, t, _p(src), _p(dst), _p(packed))
     del src, dst
-    return np.unique(packed[:w])
+    return _sorted_unique(packed[:w])
+
+
+def _sorted_unique(a: np.ndarray) -> np.ndarray:
+    """np.unique (generate.py:80) as sort + mask: identical result; numpy
+    2.3's np.unique is pathologically slow on large int64 arrays here."""
+    a = np.sort(a)
+    if a.size:
+        keep = np.empty(a.size, dtype=bool)
+        keep[0] = True
+        np.not_equal(a[1:], a[:-1], out=keep[1:])
+        a = a[keep]
+    return a
 
 
 def rmat_graph(n: int, edge_factor: int = 8, seed: int = 0) -> CSRGraph:

@@ -1,0 +1,516 @@
+// The C-ABI (include/katzb200.h): handle management and the run loop.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "kb_internal.cuh"
+
+struct kb_graph {
+    kb::Graph g;
+};
+struct kb_state {
+    kb::State s;
+};
+
+namespace kb {
+
+static thread_local std::string t_err;
+static std::atomic<int64_t> g_launches{0};
+void note_launch(int64_t k) { g_launches += k; }
+int64_t launch_count() { return g_launches.load(); }
+void set_error(const std::string &msg) { t_err = msg; }
+
+cudaStream_t device_stream() {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!streams[dev]) {
+        cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    return streams[dev];
+}
+
+namespace {
+
+__global__ void k_fill(double *p, int64_t n, double v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_active_to_orig(const int32_t *act, int dense, int64_t m, const int32_t *perm,
+                                 int64_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) out[i] = perm[dense ? (int32_t)i : act[i]];
+}
+
+__global__ void k_sep_one(const double *lower, const double *upper, const int32_t *iperm,
+                          int64_t w, int64_t v, double eps, unsigned long long *out) {
+    out[0] = lower[iperm[w]] > __dsub_rn(upper[iperm[v]], eps);
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+template <typename F>
+int guarded(F &&f) {
+    try {
+        f();
+        return KB_OK;
+    } catch (const Error &e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        set_error("host allocation failed");
+        return KB_ENOMEM;
+    } catch (const std::exception &e) {
+        set_error(e.what());
+        return KB_ECUDA;
+    }
+}
+
+void use_device(int dev) { KB_CUDA(cudaSetDevice(dev)); }
+
+}  // namespace
+}  // namespace kb
+
+using namespace kb;
+
+extern "C" {
+
+static kb_graph *new_graph(int device, int64_t split_threshold, int64_t hot_size);
+
+const char *kb_last_error(void) { return t_err.c_str(); }
+
+int kb_version(void) { return 10000; }
+
+int kb_device_count(int *count) {
+    return guarded([&] { KB_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int kb_timer(int device, int op, double *elapsed_ms) {
+    return guarded([&] {
+        static cudaEvent_t ev[64][2];
+        static bool made[64];
+        KB_REQUIRE(device >= 0 && device < 64, KB_EPARAM, "bad device");
+        use_device(device);
+        if (!made[device]) {
+            KB_CUDA(cudaEventCreate(&ev[device][0]));
+            KB_CUDA(cudaEventCreate(&ev[device][1]));
+            made[device] = true;
+        }
+        cudaStream_t st = device_stream();
+        if (op == 0) {
+            KB_CUDA(cudaEventRecord(ev[device][0], st));
+        } else {
+            KB_CUDA(cudaEventRecord(ev[device][1], st));
+            KB_CUDA(cudaEventSynchronize(ev[device][1]));
+            float ms = 0;
+            KB_CUDA(cudaEventElapsedTime(&ms, ev[device][0], ev[device][1]));
+            if (elapsed_ms) *elapsed_ms = ms;
+        }
+    });
+}
+
+int kb_launch_count(int64_t *count) {
+    return guarded([&] {
+        KB_REQUIRE(count, KB_EPARAM, "NULL argument");
+        *count = launch_count();
+    });
+}
+
+int kb_host_register(void *ptr, int64_t bytes) {
+    return guarded([&] {
+        if (!ptr || bytes <= 0) return;
+        KB_CUDA(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault));
+    });
+}
+
+int kb_host_unregister(void *ptr) {
+    return guarded([&] {
+        if (ptr) KB_CUDA(cudaHostUnregister(ptr));
+    });
+}
+
+int kb_graph_create(int device, int64_t n, int64_t nnz, const int64_t *indptr,
+                    const int32_t *indices, int64_t split_threshold, int64_t hot_size,
+                    kb_graph **out) {
+    return guarded([&] {
+        KB_REQUIRE(out, KB_EPARAM, "out is NULL");
+        KB_REQUIRE(n >= 0 && n < ((int64_t)1 << 31), KB_ENODERANGE,
+                   "node ids must fit the 32-bit index type");
+        KB_REQUIRE(nnz >= 0 && nnz < ((int64_t)1 << 31) * 32, KB_EPARAM, "bad nnz");
+        KB_REQUIRE(indptr && (nnz == 0 || indices), KB_EPARAM, "NULL CSR arrays");
+        KB_REQUIRE(indptr[0] == 0 && indptr[n] == nnz, KB_EPARAM,
+                   "indptr must start at 0 and end at nnz");
+        kb_graph *h = new_graph(device, split_threshold, hot_size);
+        Graph &g = h->g;
+        g.n = n;
+        g.nnz = nnz;
+        try {
+            build_graph(g, indptr, indices);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+static kb_graph *new_graph(int device, int64_t split_threshold, int64_t hot_size) {
+    use_device(device);
+    auto *h = new kb_graph();
+    Graph &g = h->g;
+    g.device = device;
+    KB_CUDA(cudaDeviceGetAttribute(&g.sm_count, cudaDevAttrMultiProcessorCount, device));
+    g.stream = device_stream();
+    g.split = split_threshold > 0 ? split_threshold : 8192;
+    g.split = std::max<int64_t>(4, g.split & ~(int64_t)3);
+    g.hot = hot_size >= 0 ? hot_size : 24576;
+    return h;
+}
+
+int kb_graph_create_rmat(int device, int scale, int64_t edge_factor, const uint64_t *pcg_state,
+                         double a, double ab, double abc, int64_t split_threshold,
+                         int64_t hot_size, kb_graph **out) {
+    return guarded([&] {
+        KB_REQUIRE(out && pcg_state, KB_EPARAM, "NULL argument");
+        KB_REQUIRE(edge_factor >= 1, KB_EPARAM, "edge_factor must be >= 1");
+        kb_graph *h = new_graph(device, split_threshold, hot_size);
+        try {
+            Graph &g = h->g;
+            g.n = (int64_t)1 << scale;
+            rmat_device_csr(scale, edge_factor, pcg_state, a, ab, abc, g.indptr, g.indices,
+                            g.nnz);
+            g.symmetric = 1;
+            build_graph_device(g);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int kb_graph_create_grid(int device, int64_t n, int64_t split_threshold, int64_t hot_size,
+                         kb_graph **out) {
+    return guarded([&] {
+        KB_REQUIRE(out, KB_EPARAM, "NULL argument");
+        KB_REQUIRE(n >= 1 && n < ((int64_t)1 << 31), KB_EPARAM, "grid needs 1 <= n < 2^31");
+        kb_graph *h = new_graph(device, split_threshold, hot_size);
+        try {
+            Graph &g = h->g;
+            g.n = n;
+            grid_device_csr(n, g.indptr, g.indices, g.nnz);
+            g.symmetric = 1;
+            build_graph_device(g);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int kb_graph_get_csr(kb_graph *h, int64_t *indptr, int32_t *indices) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL graph");
+        Graph &g = h->g;
+        use_device(g.device);
+        if (indptr)
+            KB_CUDA(cudaMemcpyAsync(indptr, g.indptr.p, (g.n + 1) * sizeof(int64_t),
+                                    cudaMemcpyDeviceToHost, g.stream));
+        if (indices && g.nnz)
+            KB_CUDA(cudaMemcpyAsync(indices, g.indices.p, g.nnz * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, g.stream));
+        KB_CUDA(cudaStreamSynchronize(g.stream));
+    });
+}
+
+int kb_graph_destroy(kb_graph *h) {
+    return guarded([&] {
+        if (!h) return;
+        use_device(h->g.device);
+        KB_CUDA(cudaStreamSynchronize(h->g.stream));
+        delete h;
+    });
+}
+
+int kb_graph_info_get(const kb_graph *h, kb_graph_info *info) {
+    return guarded([&] {
+        KB_REQUIRE(h && info, KB_EPARAM, "NULL argument");
+        const Graph &g = h->g;
+        info->n = g.n;
+        info->nnz = g.nnz;
+        info->max_out_degree = g.max_deg;
+        info->nonisolated = g.nv;
+        info->heavy_rows = g.nh;
+        info->segments = g.sell.nseg;
+        info->slices = g.sell.nslices;
+        info->sell_elems = g.sell.elems;
+        info->split_threshold = g.split;
+        info->hot_size = std::min<int64_t>(g.hot, g.n);
+        info->version = g.version;
+        info->device_bytes = (int64_t)g.device_bytes();
+    });
+}
+
+int kb_graph_is_symmetric(kb_graph *h, int *symmetric) {
+    return guarded([&] {
+        KB_REQUIRE(h && symmetric, KB_EPARAM, "NULL argument");
+        use_device(h->g.device);
+        if (h->g.symmetric < 0) h->g.symmetric = graph_is_symmetric(h->g);
+        *symmetric = h->g.symmetric;
+    });
+}
+
+int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, int kind,
+                    double epsilon, int64_t k, int64_t u, int64_t v, int keep_all_levels,
+                    int64_t max_iterations, kb_state **out) {
+    return guarded([&] {
+        KB_REQUIRE(gh && out, KB_EPARAM, "NULL argument");
+        Graph &g = gh->g;
+        KB_REQUIRE(g.n >= 1, KB_EPARAM, "graph must have at least one node");
+        KB_REQUIRE(std::isfinite(alpha) && alpha > 0, KB_EPARAM, "alpha must be finite and > 0");
+        KB_REQUIRE(std::isfinite(epsilon) && epsilon > 0, KB_EPARAM,
+                   "epsilon must be finite and > 0");
+        KB_REQUIRE(kind >= KB_RANKING && kind <= KB_PAIR, KB_EPARAM, "unknown criterion kind");
+        KB_REQUIRE(kind != KB_TOPK || (k >= 1 && k <= g.n), KB_EPARAM, "bad k");
+        KB_REQUIRE(kind != KB_PAIR || (u >= 0 && v >= 0 && u < g.n && v < g.n && u != v),
+                   KB_EPARAM, "pair criterion names a node outside the graph");
+        KB_REQUIRE(max_iterations >= 1, KB_EPARAM, "max_iterations must be >= 1");
+        use_device(g.device);
+        auto *h = new kb_state();
+        State &s = h->s;
+        s.g = &g;
+        s.alpha = alpha;
+        s.gamma = gamma;
+        s.eps = epsilon;
+        s.undirected = undirected;
+        s.kind = kind;
+        s.k = k;
+        s.u = u;
+        s.v = v;
+        s.keep_all = keep_all_levels;
+        s.max_iter = max_iterations;
+        s.graph_version = g.version;
+        const int64_t n = g.n;
+        cudaStream_t st = g.stream;
+        s.levels.emplace_back();
+        s.levels.back().alloc(n + 1);
+        k_fill<<<nblk(n + 1, 256), 256, 0, st>>>(s.levels.back().p, n, 1.0); note_launch();  // engine.py:147
+        KB_CUDA(cudaMemsetAsync(s.levels.back().p + n, 0, sizeof(double), st));
+        s.katz.alloc(n + 1);
+        s.lower.alloc(n + 1);
+        s.upper.alloc(n + 1);
+        KB_CUDA(cudaMemsetAsync(s.katz.p, 0, (n + 1) * sizeof(double), st));   // :148
+        KB_CUDA(cudaMemsetAsync(s.lower.p, 0, (n + 1) * sizeof(double), st));  // :149
+        k_fill<<<nblk(n + 1, 256), 256, 0, st>>>(s.upper.p, n + 1, alpha * gamma); note_launch();  // :151
+        s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
+        s.act[0].alloc(n);
+        s.act[1].alloc(n);
+        s.act_dense = true;  // :152 arange(n), materialised on first check
+        s.m_host = n;
+        s.scratch_u64.alloc(1 << 16);
+        s.scratch_i32.alloc(1 << 16);
+        s.work_counter.alloc(1);
+        KB_CUDA(cudaMallocHost(&s.h_flags, 64 * sizeof(unsigned long long)));
+        KB_CUDA(cudaEventCreate(&s.ev0));
+        KB_CUDA(cudaEventCreate(&s.ev1));
+        KB_CUDA(cudaGetLastError());
+        KB_CUDA(cudaStreamSynchronize(st));
+        *out = h;
+    });
+}
+
+int kb_state_destroy(kb_state *h) {
+    return guarded([&] {
+        if (!h) return;
+        use_device(h->s.g->device);
+        KB_CUDA(cudaStreamSynchronize(h->s.g->stream));
+        if (h->s.h_flags) cudaFreeHost(h->s.h_flags);
+        if (h->s.ev0) cudaEventDestroy(h->s.ev0);
+        if (h->s.ev1) cudaEventDestroy(h->s.ev1);
+        for (cudaEvent_t e : h->s.k1_ev) cudaEventDestroy(e);
+        delete h;
+    });
+}
+
+int kb_state_info_get(const kb_state *h, kb_state_info *info) {
+    return guarded([&] {
+        KB_REQUIRE(h && info, KB_EPARAM, "NULL argument");
+        const State &s = h->s;
+        info->r = s.r;
+        info->active = s.m_host;
+        info->max_iterations = s.max_iter;
+        info->levels_kept = (int64_t)s.levels.size();
+        info->alpha = s.alpha;
+        info->gamma = s.gamma;
+        info->epsilon = s.eps;
+        info->last_check_ms = s.last_check_ms;
+        collect_k1_times(const_cast<State &>(s));
+        info->spmv_ms = s.spmv_ms;
+        info->spmv_launches = s.spmv_launches;
+    });
+}
+
+int kb_state_set_max_iterations(kb_state *h, int64_t m) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL state");
+        h->s.max_iter = m;
+    });
+}
+
+static void check_version(State &s) {
+    KB_REQUIRE(s.g->version == s.graph_version, KB_ESTATE,
+               "graph changed since init; static iteration would be unsound");
+}
+
+int kb_iterate(kb_state *h, int64_t steps) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL state");
+        State &s = h->s;
+        use_device(s.g->device);
+        check_version(s);
+        for (int64_t i = 0; i < steps; i++) launch_iterate(s, s.g->stream);
+        KB_CUDA(cudaGetLastError());
+    });
+}
+
+int kb_check(kb_state *h, int *converged) {
+    return guarded([&] {
+        KB_REQUIRE(h && converged, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        *converged = run_check(s, s.g->stream) ? 1 : 0;
+    });
+}
+
+int kb_run(kb_state *h, int *converged) {
+    return guarded([&] {
+        KB_REQUIRE(h && converged, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        *converged = 0;
+        for (;;) {
+            check_version(s);
+            launch_iterate(s, s.g->stream);
+            if (run_check(s, s.g->stream)) { *converged = 1; break; }
+            if (s.r >= s.max_iter) {
+                const double gap = run_gap(s, s.g->stream);
+                char buf[160];
+                snprintf(buf, sizeof buf,
+                         "stopping rule still unmet after %lld iterations (widest bound "
+                         "interval %.3e)", (long long)s.r, gap);
+                throw Error{KB_ECONVERGENCE, buf};
+            }
+        }
+    });
+}
+
+int kb_gap(kb_state *h, double *gap) {
+    return guarded([&] {
+        KB_REQUIRE(h && gap, KB_EPARAM, "NULL argument");
+        use_device(h->s.g->device);
+        *gap = run_gap(h->s, h->s.g->stream);
+    });
+}
+
+int kb_epsilon_separated(kb_state *h, int64_t w, int64_t v, int *sep) {
+    return guarded([&] {
+        KB_REQUIRE(h && sep, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        KB_REQUIRE(w >= 0 && w < s.g->n, KB_EPARAM, "node id outside graph");
+        KB_REQUIRE(v >= 0 && v < s.g->n, KB_EPARAM, "node id outside graph");
+        use_device(s.g->device);
+        cudaStream_t st = s.g->stream;
+        k_sep_one<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, s.g->iperm.p, w, v, s.eps,
+                                   s.scratch_u64.p); note_launch();
+        KB_CUDA(cudaMemcpyAsync(s.h_flags, s.scratch_u64.p, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        *sep = s.h_flags[0] != 0;
+    });
+}
+
+int kb_result(kb_state *h, int64_t *order, double *lower, double *upper, int64_t *pairs) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL state");
+        use_device(h->s.g->device);
+        run_result(h->s, h->s.g->stream, order, lower, upper, pairs);
+    });
+}
+
+int kb_separated_pairs(kb_state *h, int64_t *pairs) {
+    return guarded([&] {
+        KB_REQUIRE(h && pairs, KB_EPARAM, "NULL argument");
+        use_device(h->s.g->device);
+        run_result(h->s, h->s.g->stream, nullptr, nullptr, nullptr, pairs);
+    });
+}
+
+int kb_get_vector(kb_state *h, int which, int64_t level, double *out) {
+    return guarded([&] {
+        KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        const double *src = nullptr;
+        switch (which) {
+            case KB_VEC_LEVEL: {
+                const int64_t idx = level - s.level_base;
+                KB_REQUIRE(idx >= 0 && idx < (int64_t)s.levels.size(), KB_EPARAM,
+                           "level not retained");
+                src = s.levels[idx].p;
+                break;
+            }
+            case KB_VEC_KATZ: src = s.katz.p; break;
+            case KB_VEC_LOWER: src = s.lower.p; break;
+            case KB_VEC_UPPER: src = s.upper.p; break;
+            default: throw Error{KB_EPARAM, "unknown vector"};
+        }
+        cudaStream_t st = s.g->stream;
+        DBuf<double> tmp;
+        tmp.alloc(s.g->n);
+        gather_to_original(*s.g, src, tmp.p, st);
+        KB_CUDA(cudaMemcpyAsync(out, tmp.p, s.g->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kb_get_active(kb_state *h, int64_t *out) {
+    return guarded([&] {
+        KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        cudaStream_t st = s.g->stream;
+        const int64_t m = s.m_host;
+        if (!m) return;
+        DBuf<int64_t> tmp;
+        tmp.alloc(m);
+        k_active_to_orig<<<nblk(m, 256), 256, 0, st>>>(s.act[s.cur].p, s.act_dense, m,
+                                                       s.g->perm.p, tmp.p); note_launch();
+        KB_CUDA(cudaMemcpyAsync(out, tmp.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kb_update_batch(kb_state *h, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                    int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats) {
+    return guarded([&] {
+        (void)h; (void)ins; (void)n_ins; (void)dels; (void)n_dels; (void)theta;
+        (void)new_gamma; (void)stats;
+        throw Error{KB_ESTATE, "kb_update_batch: not built yet"};
+    });
+}
+
+}  // extern "C"

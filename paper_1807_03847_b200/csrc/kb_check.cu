@@ -1,0 +1,666 @@
+// K2: the stopping rule (check_converged, engine.py:333-379) on the device.
+//
+// TOPK (k <= KMAX): one cooperative kernel over the active set
+//   1. radix-select the k-th largest lower bound: 8 passes of 8-bit digits
+//      over the IEEE bits of lower (lower >= +0, so the bit pattern orders
+//      like the value); histograms are block-privatised in shared memory;
+//   2. ties at the cut are broken by the smallest original id (a 4-pass
+//      radix select on the id among the keys equal to the threshold) --
+//      numpy's argpartition (engine.py:359) breaks them arbitrarily;
+//   3. order-preserving compaction: the k winners go to a prefix buffer, the
+//      losers with fl(upper - eps) >= threshold survive (engine.py:368-373);
+// then a one-block kernel sorts the prefix by (-lower, id) in shared memory
+// (engine.py:365) and evaluates |active| > k and the adjacent separations
+// fl(upper[p_i] - eps) < lower[p_{i-1}] (engine.py:374-378).
+//
+// RANKING, or TOPK with k > KMAX: O(n) certificates first (SURVEY.md 7
+// "exact O(n) fast paths"), and a full stable radix sort by (-lower, id)
+// only when they cannot decide.
+// SCORE: max(upper-lower) < eps (:344-345).  PAIR: scalar test (:346-353).
+#include <cooperative_groups.h>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/block/block_reduce.cuh>
+
+#include <algorithm>
+
+#include "kb_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kb {
+
+namespace {
+
+constexpr int KMAX = 4096;
+constexpr int CHK_THREADS = 512;
+constexpr int NCAND = 8;
+
+__device__ __forceinline__ uint64_t key_of(const double *lower, int32_t id) {
+    return (uint64_t)__double_as_longlong(lower[id]);
+}
+
+struct TopkArgs {
+    const double *lower, *upper;
+    const int32_t *perm;
+    const int32_t *act_in;
+    int64_t m;
+    int dense;
+    int32_t *act_out;
+    int64_t k;
+    double eps;
+    unsigned int *hist;             // 12 * 256
+    unsigned long long *blk;        // 2 * gridDim
+    int32_t *prefix_buf;            // k
+    unsigned long long *out;        // [0]=new m, [1]=converged, [2]=#prefix
+};
+
+__global__ void __launch_bounds__(CHK_THREADS) k_topk_select(TopkArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned int sh[256];
+    __shared__ uint64_t s_sel[2];
+    __shared__ int64_t s_need;
+    const int64_t G = gridDim.x;
+    const int64_t chunk = (A.m + G - 1) / G;
+    const int64_t i0 = min(A.m, blockIdx.x * chunk), i1 = min(A.m, i0 + chunk);
+
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 12 * 256; i += blockDim.x) A.hist[i] = 0;
+    grid.sync();
+
+    // ---- 1. k-th largest key
+    uint64_t prefix = 0, mask = 0;
+    int64_t kk = A.k;
+    for (int p = 0; p < 8; p++) {
+        const int shift = 56 - 8 * p;
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = 0;
+        __syncthreads();
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+            const int32_t id = A.dense ? (int32_t)i : A.act_in[i];
+            const uint64_t key = key_of(A.lower, id);
+            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < 256; b += blockDim.x)
+            if (sh[b]) atomicAdd(&A.hist[p * 256 + b], sh[b]);
+        grid.sync();
+        if (threadIdx.x == 0) {
+            int64_t cum = 0;
+            int sel = 0;
+            for (int b = 255; b >= 0; b--) {
+                const int64_t c = A.hist[p * 256 + b];
+                if (cum + c >= kk) { sel = b; break; }
+                cum += c;
+            }
+            s_sel[0] = (uint64_t)sel;
+            s_need = kk - cum;
+        }
+        __syncthreads();
+        prefix |= s_sel[0] << shift;
+        mask |= (uint64_t)0xFF << shift;
+        kk = s_need;
+        __syncthreads();
+    }
+    const uint64_t kstar = prefix;
+    const int64_t count_eq = A.hist[7 * 256 + (int)(kstar & 255)];
+
+    // ---- 2. ties at the cut: the kk smallest original ids among key == kstar
+    uint32_t istar = 0xFFFFFFFFu;
+    if (kk < count_eq) {
+        uint32_t ipre = 0, imask = 0;
+        int64_t need = kk;
+        for (int p = 0; p < 4; p++) {
+            const int shift = 24 - 8 * p;
+            for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = 0;
+            __syncthreads();
+            for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+                const int32_t id = A.dense ? (int32_t)i : A.act_in[i];
+                if (key_of(A.lower, id) != kstar) continue;
+                const uint32_t o = (uint32_t)A.perm[id];
+                if ((o & imask) == ipre) atomicAdd(&sh[(o >> shift) & 255], 1u);
+            }
+            __syncthreads();
+            for (int b = threadIdx.x; b < 256; b += blockDim.x)
+                if (sh[b]) atomicAdd(&A.hist[(8 + p) * 256 + b], sh[b]);
+            grid.sync();
+            if (threadIdx.x == 0) {
+                int64_t cum = 0;
+                int sel = 255;
+                for (int b = 0; b < 256; b++) {
+                    const int64_t c = A.hist[(8 + p) * 256 + b];
+                    if (cum + c >= need) { sel = b; break; }
+                    cum += c;
+                }
+                s_sel[0] = (uint64_t)sel;
+                s_need = need - cum;
+            }
+            __syncthreads();
+            ipre |= (uint32_t)s_sel[0] << shift;
+            imask |= 0xFFu << shift;
+            need = s_need;
+            __syncthreads();
+        }
+        istar = ipre;
+    }
+    const double thr = __longlong_as_double((long long)kstar);
+
+    // ---- 3. order-preserving compaction
+    typedef cub::BlockScan<int, CHK_THREADS> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_tot[2];
+    auto classify = [&](int64_t i, int32_t &id, int &top, int &surv) {
+        top = surv = 0;
+        if (i >= i1) return;
+        id = A.dense ? (int32_t)i : A.act_in[i];
+        const uint64_t key = key_of(A.lower, id);
+        top = key > kstar || (key == kstar && (uint32_t)A.perm[id] <= istar);
+        if (!top) surv = __dsub_rn(A.upper[id], A.eps) >= thr;
+    };
+    {
+        unsigned long long nt = 0, ns = 0;
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+            int32_t id; int t, s;
+            classify(i, id, t, s);
+            nt += t; ns += s;
+        }
+        typedef cub::BlockReduce<unsigned long long, CHK_THREADS> Red;
+        __shared__ typename Red::TempStorage red_tmp;
+        unsigned long long a = Red(red_tmp).Sum(nt);
+        __syncthreads();
+        unsigned long long b = Red(red_tmp).Sum(ns);
+        if (threadIdx.x == 0) { A.blk[blockIdx.x] = a; A.blk[G + blockIdx.x] = b; }
+    }
+    grid.sync();
+    __shared__ unsigned long long s_off[2];
+    if (threadIdx.x == 0) {
+        unsigned long long ot = 0, os = 0, ts = 0;
+        for (int64_t b = 0; b < G; b++) {
+            if (b < blockIdx.x) { ot += A.blk[b]; os += A.blk[G + b]; }
+            ts += A.blk[G + b];
+        }
+        s_off[0] = ot;
+        s_off[1] = os;
+        if (blockIdx.x == 0) { A.out[0] = (unsigned long long)A.k + ts; A.out[2] = A.k; }
+    }
+    __syncthreads();
+    unsigned long long ot = s_off[0], os = s_off[1];
+    for (int64_t base = i0; base < i1; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        int32_t id = 0; int t, s;
+        classify(i, id, t, s);
+        int pt, ps;
+        Scan(scan_tmp).ExclusiveSum(t, pt, s_tot[0]);
+        __syncthreads();
+        Scan(scan_tmp).ExclusiveSum(s, ps, s_tot[1]);
+        __syncthreads();
+        if (t) A.prefix_buf[ot + pt] = id;
+        if (s) A.act_out[A.k + os + ps] = id;
+        ot += s_tot[0];
+        os += s_tot[1];
+        __syncthreads();
+    }
+}
+
+// Sort the prefix by (-lower, original id), write it to act_out[0..cnt), and
+// evaluate the stopping rule.  One block; cnt <= KMAX.
+__global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const double *upper,
+                                                      const int32_t *perm, const int32_t *src,
+                                                      int dense_src, int32_t *act_out,
+                                                      unsigned long long *out, double eps,
+                                                      int64_t k) {
+    extern __shared__ unsigned char smem[];
+    const int64_t cnt = (int64_t)out[2];
+    const int64_t mnew = (int64_t)out[0];
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    uint64_t *hi = (uint64_t *)smem;            // ~key  (ascending = lower desc)
+    uint32_t *lo = (uint32_t *)(hi + P);        // original id
+    int32_t *nid = (int32_t *)(lo + P);         // new id
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < cnt) {
+            const int32_t id = dense_src ? i : src[i];
+            hi[i] = ~key_of(lower, id);
+            lo[i] = (uint32_t)perm[id];
+            nid[i] = id;
+        } else {
+            hi[i] = ~0ull;
+            lo[i] = 0xFFFFFFFFu;
+            nid[i] = -1;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool gt = hi[i] > hi[j] || (hi[i] == hi[j] && lo[i] > lo[j]);
+                    if (gt == up) {
+                        uint64_t th = hi[i]; hi[i] = hi[j]; hi[j] = th;
+                        uint32_t tl = lo[i]; lo[i] = lo[j]; lo[j] = tl;
+                        int32_t tn = nid[i]; nid[i] = nid[j]; nid[j] = tn;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        act_out[i] = nid[i];
+        if (i >= 1 && !(__dsub_rn(upper[nid[i]], eps) < lower[nid[i - 1]])) bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) out[1] = (mnew <= k) && !bad;
+}
+
+// ---------------------------------------------------------------- reductions
+__global__ void k_gap(const double *lower, const double *upper, int64_t n,
+                      unsigned long long *out) {
+    typedef cub::BlockReduce<unsigned long long, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    unsigned long long best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = __dsub_rn(upper[i], lower[i]);
+        // map doubles to order-preserving unsigned keys (d may be -0/neg)
+        const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+        const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+        best = max(best, key);
+    }
+    best = Red(tmp).Reduce(best, cub::Max());
+    if (threadIdx.x == 0) atomicMax(out, best);
+}
+
+__global__ void k_pair(const double *lower, const double *upper, const int32_t *iperm,
+                       int64_t u, int64_t v, double eps, unsigned long long *out) {
+    const int32_t nu = iperm[u], nv = iperm[v];
+    const double lu = lower[nu], lv = lower[nv];
+    int64_t w, x;
+    int32_t nw, nx;
+    // (lu, -u) >= (lv, -v)  (engine.py:349)
+    if (lu > lv || (lu == lv && -u >= -v)) { w = u; x = v; nw = nu; nx = nv; }
+    else { w = v; x = u; nw = nv; nx = nu; }
+    (void)w; (void)x;
+    out[1] = lower[nw] > __dsub_rn(upper[nx], eps);
+}
+
+// ---------------------------------------------------------------- ranking
+// violators of the self test fl(upper[q]-eps) < lower[q]; count them and keep,
+// per block, the one with the widest excess (ties: smallest original id)
+struct Cand {
+    unsigned long long key;  // order-preserving bits of excess
+    int32_t id;              // new id
+};
+
+__device__ __forceinline__ unsigned long long ord_bits(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_rank_violators(const double *lower, const double *upper, const int32_t *perm,
+                                 const int32_t *act, int dense, int64_t m, double eps,
+                                 unsigned long long *count, unsigned long long *blk_key,
+                                 int32_t *blk_id) {
+    __shared__ unsigned long long sk[256];
+    __shared__ int32_t sid[256];
+    unsigned long long bk = 0, c = 0;
+    int32_t bid = -1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t q = dense ? (int32_t)i : act[i];
+        const double ex = __dsub_rn(__dsub_rn(upper[q], eps), lower[q]);
+        if (!(__dsub_rn(upper[q], eps) < lower[q])) {
+            c++;
+            const unsigned long long k = ord_bits(ex);
+            if (bid < 0 || k > bk || (k == bk && perm[q] < perm[bid])) { bk = k; bid = q; }
+        }
+    }
+    sk[threadIdx.x] = bk;
+    sid[threadIdx.x] = bid;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            const unsigned long long k2 = sk[threadIdx.x + s];
+            const int32_t i2 = sid[threadIdx.x + s];
+            const int32_t i1 = sid[threadIdx.x];
+            if (i2 >= 0 && (i1 < 0 || k2 > sk[threadIdx.x] ||
+                            (k2 == sk[threadIdx.x] && perm[i2] < perm[i1]))) {
+                sk[threadIdx.x] = k2;
+                sid[threadIdx.x] = i2;
+            }
+        }
+        __syncthreads();
+    }
+    typedef cub::BlockReduce<unsigned long long, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    unsigned long long tot = Red(tmp).Sum(c);
+    if (threadIdx.x == 0) {
+        if (tot) atomicAdd(count, tot);
+        blk_key[blockIdx.x] = sk[0];
+        blk_id[blockIdx.x] = sid[0];
+    }
+}
+
+// predecessor search for up to NCAND candidates: for each q the element x
+// ranked immediately before it in (-lower, id) order, i.e. the minimum of
+// (lower[x], -id[x]) over {x : (lower[x], -id[x]) > (lower[q], -id[q])}.
+// Packed into one 64-bit key per block-candidate for a min reduction:
+// we reduce on (lower bits, ~id) with atomicMin over two words via a
+// 128-bit emulation -- done here as per-block arrays + host-free final pass.
+__global__ void k_rank_pred(const double *lower, const int32_t *perm, const int32_t *act,
+                            int dense, int64_t m, const int32_t *cand, int ncand,
+                            unsigned long long *pred_key, unsigned int *pred_id) {
+    __shared__ uint64_t ck[NCAND];
+    __shared__ uint32_t co[NCAND];
+    if (threadIdx.x < ncand) {
+        ck[threadIdx.x] = key_of(lower, cand[threadIdx.x]);
+        co[threadIdx.x] = (uint32_t)perm[cand[threadIdx.x]];
+    }
+    __syncthreads();
+    uint64_t bk[NCAND];
+    uint32_t bo[NCAND];
+    for (int c = 0; c < NCAND; c++) { bk[c] = ~0ull; bo[c] = 0; }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t x = dense ? (int32_t)i : act[i];
+        const uint64_t kx = key_of(lower, x);
+        const uint32_t ox = (uint32_t)perm[x];
+        for (int c = 0; c < ncand; c++) {
+            // x ranked before q: kx > kq or (kx == kq and ox < oq)
+            const bool before = kx > ck[c] || (kx == ck[c] && ox < co[c]);
+            // keep the last-ranked such x: smallest kx, then largest ox
+            if (before && (kx < bk[c] || (kx == bk[c] && ox > bo[c]))) { bk[c] = kx; bo[c] = ox; }
+        }
+    }
+    // pack (key, ~id) ordering into a single comparison via two atomics:
+    // first atomicMin on the key, then (after a grid-wide pass) the id.  To
+    // stay single-pass we write per-thread winners to a block reduction.
+    __shared__ uint64_t rk[256];
+    __shared__ uint32_t ro[256];
+    for (int c = 0; c < ncand; c++) {
+        rk[threadIdx.x] = bk[c];
+        ro[threadIdx.x] = bo[c];
+        __syncthreads();
+        for (int s = 128; s > 0; s >>= 1) {
+            if (threadIdx.x < s) {
+                const uint64_t k2 = rk[threadIdx.x + s];
+                const uint32_t o2 = ro[threadIdx.x + s];
+                if (k2 < rk[threadIdx.x] || (k2 == rk[threadIdx.x] && o2 > ro[threadIdx.x])) {
+                    rk[threadIdx.x] = k2;
+                    ro[threadIdx.x] = o2;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            pred_key[blockIdx.x * NCAND + c] = rk[0];
+            pred_id[blockIdx.x * NCAND + c] = ro[0];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_orig_keys(const double *lower, const int32_t *iperm, const int32_t *act,
+                            int dense, int64_t m, uint32_t *okey, int32_t *nid) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    // dense: walk original ids in order; else the active new ids
+    if (dense) { okey[i] = (uint32_t)i; nid[i] = iperm[i]; }
+    else { nid[i] = act[i]; }
+}
+
+__global__ void k_perm_keys(const int32_t *perm, const int32_t *nid, int64_t m, uint32_t *okey) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    okey[i] = (uint32_t)perm[nid[i]];
+}
+
+__global__ void k_lower_keys(const double *lower, const int32_t *nid, int64_t m, uint64_t *key) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    key[i] = ~key_of(lower, nid[i]);
+}
+
+// after the (-lower, id) sort: keep the first k, and the rest whose
+// fl(upper - eps) >= lower of the k-th (engine.py:367-373); count adjacent
+// separation failures inside the prefix (engine.py:376-378)
+__global__ void k_cut_flags(const double *lower, const double *upper, const int32_t *order,
+                            int64_t m, int64_t k, double eps, unsigned char *flag,
+                            unsigned long long *bad) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t pk = (m < k ? m : k) - 1;
+    const double thr = lower[order[pk]];
+    if (i <= pk) {
+        flag[i] = 1;
+        if (i >= 1 && !(__dsub_rn(upper[order[i]], eps) < lower[order[i - 1]]))
+            atomicAdd(bad, 1ull);
+    } else {
+        flag[i] = __dsub_rn(upper[order[i]], eps) >= thr;
+    }
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+int coop_grid(int sm_count) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_topk_select,
+                                                              CHK_THREADS, 0));
+        per_sm = std::max(1, std::min(per_sm, 2));
+    }
+    return sm_count * per_sm;
+}
+
+void sync_read(State &s, cudaStream_t st, const unsigned long long *dev, int count) {
+    KB_CUDA(cudaMemcpyAsync(s.h_flags, dev, count * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+}
+
+// Generic rule by full sort: order the active set by (-lower, original id)
+// with two stable radix sorts, cut at k, compact the survivors in sorted
+// order.  Used for RANKING when the O(n) certificates cannot decide and for
+// TOPK with k > KMAX.
+bool sorted_check(State &s, cudaStream_t st, int64_t k) {
+    Graph &g = *s.g;
+    const int64_t m = s.m_host;
+    DBuf<uint32_t> ok_in, ok_out;
+    DBuf<int32_t> id_in, id_out;
+    DBuf<uint64_t> lk_in, lk_out;
+    ok_in.alloc(m); ok_out.alloc(m); id_in.alloc(m); id_out.alloc(m);
+    lk_in.alloc(m); lk_out.alloc(m);
+    const int32_t *act = s.act[s.cur].p;
+    k_orig_keys<<<nblk(m, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, act, s.act_dense, m,
+                                              ok_in.p, id_in.p); note_launch();
+    const int32_t *by_orig = id_in.p;
+    size_t tb = 0;
+    if (!s.act_dense) {
+        k_perm_keys<<<nblk(m, 256), 256, 0, st>>>(g.perm.p, id_in.p, m, ok_in.p); note_launch();
+        KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ok_in.p, ok_out.p, id_in.p,
+                                                id_out.p, (int)m, 0, 32, st));
+        ensure_cub_tmp(s, tb);
+        KB_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp.p, tb, ok_in.p, ok_out.p, id_in.p,
+                                                id_out.p, (int)m, 0, 32, st)); note_launch();
+        by_orig = id_out.p;
+    }
+    k_lower_keys<<<nblk(m, 256), 256, 0, st>>>(s.lower.p, by_orig, m, lk_in.p); note_launch();
+    int32_t *sorted = s.act_dense ? id_out.p : id_in.p;
+    tb = 0;
+    KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, lk_in.p, lk_out.p, by_orig, sorted,
+                                            (int)m, 0, 64, st));
+    ensure_cub_tmp(s, tb);
+    KB_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp.p, tb, lk_in.p, lk_out.p, by_orig, sorted,
+                                            (int)m, 0, 64, st)); note_launch();
+    unsigned char *flag = (unsigned char *)lk_in.p;  // reuse
+    unsigned long long *u = s.scratch_u64.p;          // [0]=bad, [1]=selected count
+    KB_CUDA(cudaMemsetAsync(u, 0, 2 * sizeof(unsigned long long), st));
+    k_cut_flags<<<nblk(m, 256), 256, 0, st>>>(s.lower.p, s.upper.p, sorted, m, k, s.eps, flag, u); note_launch();
+    const int nxt = s.cur ^ 1;
+    tb = 0;
+    KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, sorted, flag, s.act[nxt].p, u + 1, (int)m,
+                                       st));
+    ensure_cub_tmp(s, tb);
+    KB_CUDA(cub::DeviceSelect::Flagged(s.cub_tmp.p, tb, sorted, flag, s.act[nxt].p, u + 1,
+                                       (int)m, st)); note_launch();
+    sync_read(s, st, u, 2);
+    s.cur = nxt;
+    s.act_dense = false;
+    s.m_host = (int64_t)s.h_flags[1];
+    return s.m_host <= k && s.h_flags[0] == 0;
+}
+
+bool check_ranking(State &s, cudaStream_t st) {
+    Graph &g = *s.g;
+    const int64_t n = s.m_host;
+    const int32_t *act = s.act[s.cur].p;
+    const int dense = s.act_dense;
+    const int nb = 2 * g.sm_count;
+    unsigned long long *u = s.scratch_u64.p;     // [0]=count, [1..nb] block keys
+    int32_t *ids = s.scratch_i32.p;              // [0..nb) block ids, [nb..nb+8) cands
+    KB_CUDA(cudaMemsetAsync(u, 0, sizeof(unsigned long long), st));
+    k_rank_violators<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, s.eps,
+                                         u, u + 1, ids); note_launch();
+    // bring the per-block winners back and pick up to NCAND candidates
+    std::vector<unsigned long long> bk(nb + 1);
+    std::vector<int32_t> bid(nb);
+    KB_CUDA(cudaMemcpyAsync(bk.data(), u, (nb + 1) * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaMemcpyAsync(bid.data(), ids, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long nviol = bk[0];
+    if (nviol == 0) return true;  // every q clears itself, hence its predecessor
+    std::vector<std::pair<unsigned long long, int32_t>> c;
+    for (int b = 0; b < nb; b++)
+        if (bid[b] >= 0) c.push_back({bk[b + 1], bid[b]});
+    std::stable_sort(c.begin(), c.end(), [](auto &a, auto &b) { return a.first > b.first; });
+    if ((int)c.size() > NCAND) c.resize(NCAND);
+    const int nc = (int)c.size();
+    std::vector<int32_t> cand(nc);
+    for (int i = 0; i < nc; i++) cand[i] = c[i].second;
+    KB_CUDA(cudaMemcpyAsync(ids + nb, cand.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice,
+                            st));
+    unsigned long long *pk = u + 1 + nb;
+    unsigned int *po = (unsigned int *)(ids + nb + NCAND);
+    k_rank_pred<<<nb, 256, 0, st>>>(s.lower.p, g.perm.p, act, dense, n, ids + nb, nc, pk, po); note_launch();
+    std::vector<unsigned long long> hpk((size_t)nb * NCAND);
+    std::vector<unsigned int> hpo((size_t)nb * NCAND);
+    std::vector<double> uq(nc);
+    KB_CUDA(cudaMemcpyAsync(hpk.data(), pk, hpk.size() * 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaMemcpyAsync(hpo.data(), po, hpo.size() * 4, cudaMemcpyDeviceToHost, st));
+    for (int i = 0; i < nc; i++)
+        KB_CUDA(cudaMemcpyAsync(&uq[i], s.upper.p + cand[i], sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    // The comparisons below only *route* between the certificates and the
+    // full device sort; each is the same IEEE subtraction+compare the kernels
+    // perform.
+    unsigned long long resolved_ok = 0;
+    for (int i = 0; i < nc; i++) {
+        uint64_t bestk = ~0ull;
+        uint32_t besto = 0;
+        for (int b = 0; b < nb; b++) {
+            const uint64_t k2 = hpk[(size_t)b * NCAND + i];
+            const uint32_t o2 = hpo[(size_t)b * NCAND + i];
+            if (k2 < bestk || (k2 == bestk && o2 > besto)) { bestk = k2; besto = o2; }
+        }
+        if (bestk == ~0ull) { resolved_ok++; continue; }  // q is ranked first
+        double lp;
+        memcpy(&lp, &bestk, sizeof(double));
+        volatile double diff = uq[i] - s.eps;
+        if (!(diff < lp)) return false;  // certified: q is not separated
+        resolved_ok++;
+    }
+    if (resolved_ok == nviol) return true;  // every violator checked, all fine
+    return sorted_check(s, st, g.n);
+}
+
+}  // namespace
+
+void ensure_cub_tmp(State &s, size_t bytes) {
+    if (s.cub_tmp.n < bytes) s.cub_tmp.alloc(bytes);
+}
+
+double run_gap(State &s, cudaStream_t st) {
+    Graph &g = *s.g;
+    unsigned long long *u = s.scratch_u64.p;
+    KB_CUDA(cudaMemsetAsync(u, 0, sizeof(unsigned long long), st));
+    if (g.n)
+        k_gap<<<2 * g.sm_count, 256, 0, st>>>(s.lower.p, s.upper.p, g.n, u); note_launch();
+    sync_read(s, st, u, 1);
+    unsigned long long key = s.h_flags[0];
+    unsigned long long b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+    double d;
+    memcpy(&d, &b, sizeof(double));
+    return g.n ? d : 0.0;
+}
+
+bool run_check(State &s, cudaStream_t st) {
+    Graph &g = *s.g;
+    KB_REQUIRE(s.r >= 1, KB_ESTATE, "check_converged needs at least one iteration");
+    if (s.kind == KB_SCORE) return run_gap(s, st) < s.eps;
+    if (s.kind == KB_PAIR) {
+        k_pair<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, g.iperm.p, s.u, s.v, s.eps,
+                                s.scratch_u64.p); note_launch();
+        sync_read(s, st, s.scratch_u64.p, 2);
+        return s.h_flags[1] != 0;
+    }
+    const int64_t k = (s.kind == KB_RANKING) ? g.n : s.k;
+    const int64_t m = s.m_host;
+    if (s.kind == KB_RANKING) return check_ranking(s, st);
+    if (k > KMAX) return sorted_check(s, st, k);
+    unsigned long long *out = s.scratch_u64.p;  // [0..3)
+    const int nxt = s.cur ^ 1;
+    if (m <= k) {
+        // nothing to deactivate: sort the whole active set as the prefix
+        unsigned long long init[3] = {(unsigned long long)m, 0ull, (unsigned long long)m};
+        memcpy(s.h_flags, init, sizeof(init));
+        KB_CUDA(cudaMemcpyAsync(out, s.h_flags, sizeof(init), cudaMemcpyHostToDevice, st));
+        int P = 1;
+        while (P < m) P <<= 1;
+        const size_t smem = (size_t)P * 16;
+        KB_CUDA(cudaFuncSetAttribute(k_topk_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 1)));
+        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.perm.p, s.act[s.cur].p,
+                                             s.act_dense, s.act[nxt].p, out, s.eps, k); note_launch();
+        KB_CUDA(cudaGetLastError());
+    } else {
+        TopkArgs A;
+        A.lower = s.lower.p;
+        A.upper = s.upper.p;
+        A.perm = g.perm.p;
+        A.act_in = s.act[s.cur].p;
+        A.m = m;
+        A.dense = s.act_dense;
+        A.act_out = s.act[nxt].p;
+        A.k = k;
+        A.eps = s.eps;
+        A.hist = (unsigned int *)(s.scratch_u64.p + 8);
+        const int G = coop_grid(g.sm_count);
+        A.blk = s.scratch_u64.p + 8 + 12 * 256;
+        A.prefix_buf = s.scratch_i32.p;
+        A.out = out;
+        void *args[] = {&A};
+        KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
+        int P = 1;
+        while (P < k) P <<= 1;
+        const size_t smem = (size_t)P * 16;
+        KB_CUDA(cudaFuncSetAttribute(k_topk_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.perm.p, A.prefix_buf, 0,
+                                             s.act[nxt].p, out, s.eps, k); note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    sync_read(s, st, out, 3);
+    s.cur = nxt;
+    s.act_dense = false;
+    s.m_host = (int64_t)s.h_flags[0];
+    return s.h_flags[1] != 0;
+}
+
+}  // namespace kb

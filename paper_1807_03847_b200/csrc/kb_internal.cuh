@@ -1,0 +1,169 @@
+// Internal structures of the katzb200 engine (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/katzb200.h"
+
+namespace kb {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+#define KB_CUDA(call)                                                          \
+    do {                                                                       \
+        cudaError_t _e = (call);                                               \
+        if (_e != cudaSuccess)                                                 \
+            throw ::kb::Error{KB_ECUDA, std::string(#call) + ": " +            \
+                                            cudaGetErrorString(_e)};           \
+    } while (0)
+
+#define KB_REQUIRE(cond, code, msg)                                            \
+    do {                                                                       \
+        if (!(cond)) throw ::kb::Error{(code), (msg)};                         \
+    } while (0)
+
+// number of kernel launches issued by the library (bench.py gpu_launches)
+void note_launch(int64_t k = 1);
+int64_t launch_count();
+
+// ---------------------------------------------------------------- device buf
+// All device work of a process runs on one non-blocking stream per device;
+// buffers are stream-ordered allocations from the device mempool (release
+// threshold raised at first use), so per-iteration scratch costs no
+// cudaMalloc round trip.
+cudaStream_t device_stream();
+
+template <typename T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) count = 1;
+        KB_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), device_stream()));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, device_stream());
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---------------------------------------------------------------- layout
+// SELL-32 over "virtual rows":
+//   vr in [0, nseg)        : segments of heavy rows (deg > split), length <= split
+//   vr in [nseg, nvr)      : ordinary rows, new id = nh + (vr - nseg)
+// Rows are relabelled by descending out-degree (stable in the original id),
+// so new ids [0, nh) are the heavy rows, [0, nv) the rows with arcs and
+// [nv, n) the rows without.  Within a row the column order is the original
+// ascending-id order of graph.py:191-192, stored as *new* ids.
+// Slice s holds 32 consecutive virtual rows.  If its padded width w <= 4 the
+// slot of (step j, lane l) is cols[off + j*32 + l]; otherwise w % 4 == 0 and
+// the slot is cols[off + (j/4)*128 + l*4 + j%4] (one int4 per lane per 4
+// steps).
+struct Sell {
+    DBuf<int32_t> cols;
+    DBuf<int64_t> slice_off;
+    DBuf<int32_t> slice_w;
+    DBuf<int32_t> vlen;
+    int64_t nslices = 0, nvr = 0, nseg = 0, elems = 0;
+};
+
+struct Graph {
+    int device = 0;
+    int sm_count = 0;
+    int64_t n = 0, nnz = 0, nv = 0, nh = 0, max_deg = 0;
+    int64_t split = 0, hot = 0;
+    int64_t version = 1;
+    DBuf<int32_t> perm;    // new -> original id
+    DBuf<int32_t> iperm;   // original -> new id
+    DBuf<int32_t> deg;     // out-degree by new id
+    // canonical CSR (original ids, rows ascending) kept for the dynamic path
+    // and the symmetry test
+    DBuf<int64_t> indptr;
+    DBuf<int32_t> indices;
+    Sell sell;
+    // heavy-row combine: segments of heavy row h are seg_list[seg_ptr[h] ..
+    // seg_ptr[h+1]) in order (indices into the segment-sum buffer)
+    DBuf<int32_t> seg_ptr;
+    DBuf<int32_t> seg_list;
+    cudaStream_t stream = nullptr;
+    int symmetric = -1;  // cached result of kb_graph_is_symmetric
+    size_t device_bytes() const;
+};
+
+// ---------------------------------------------------------------- state
+struct State {
+    Graph *g = nullptr;
+    double alpha = 0, gamma = 0, eps = 0;
+    int undirected = 0, kind = 0, keep_all = 1;
+    int64_t k = 0, u = 0, v = 0;
+    int64_t r = 0, max_iter = 0;
+    int64_t graph_version = 0;
+    std::vector<DBuf<double>> levels;  // new-id space, n+1 slots each
+    int64_t level_base = 0;            // level index of levels[0]
+    DBuf<double> katz, lower, upper;   // new-id space
+    DBuf<double> seg_sum;
+    // active set (new ids) -- ping-pong buffers; count lives on the device
+    DBuf<int32_t> act[2];
+    int cur = 0;
+    bool act_dense = true;  // active == arange(n) (never materialised)
+    int64_t m_host = 0;     // |active| mirrored after each check
+    // device scratch for the checks
+    DBuf<unsigned long long> scratch_u64;
+    DBuf<int32_t> scratch_i32;
+    DBuf<double> scratch_f64;
+    DBuf<unsigned char> cub_tmp;
+    DBuf<unsigned long long> work_counter;
+    unsigned long long *h_flags = nullptr;  // pinned host mirror
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_check_ms = 0;
+    // K1 launch timing: event pairs recorded around each SpMV+bounds step
+    std::vector<cudaEvent_t> k1_ev;
+    size_t k1_used = 0, k1_read = 0;
+    double spmv_ms = 0;
+    int64_t spmv_launches = 0;
+    const double *x_level() const { return levels.back().p; }
+};
+
+// ---------------------------------------------------------------- kernels
+void launch_iterate(State &s, cudaStream_t st);
+void collect_k1_times(State &s);
+bool run_check(State &s, cudaStream_t st);      // returns converged
+double run_gap(State &s, cudaStream_t st);
+void run_result(State &s, cudaStream_t st, int64_t *order, double *lower,
+                double *upper, int64_t *pairs);
+void gather_to_original(const Graph &g, const double *src_new, double *dst_orig,
+                        cudaStream_t st);
+void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices);
+void build_graph_device(Graph &g);
+void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], double a,
+                     double ab, double abc, DBuf<int64_t> &indptr, DBuf<int32_t> &indices,
+                     int64_t &nnz_out);
+void grid_device_csr(int64_t n, DBuf<int64_t> &indptr, DBuf<int32_t> &indices,
+                     int64_t &nnz_out);
+int graph_is_symmetric(Graph &g);
+void ensure_cub_tmp(State &s, size_t bytes);
+
+}  // namespace kb

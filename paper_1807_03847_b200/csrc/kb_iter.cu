@@ -1,0 +1,264 @@
+// K1: fused walk-count SpMV + bound refresh (iterate_once, engine.py:296-319).
+//
+// One pull step  w_r(v) = alpha * sum_{u in N+(v)} w_{r-1}(u)  over the
+// SELL-32 layout of kb_ingest.cu, fused with
+//     katz += w; tail = alpha*w; lower = katz + tail (undirected) | katz;
+//     upper = katz + tail*gamma
+// in exactly numpy's operation order with every multiply and add rounded
+// separately (no FMA contraction: __dmul_rn/__dadd_rn), so every row whose
+// length is <= the split threshold is bit-identical to scipy's sequential
+// csr_matvec (each lane folds its own row in ascending original column
+// order).  Rows longer than the threshold are cut into fixed segments whose
+// partial sums are combined in segment order by k_heavy_combine: a
+// deterministic, hardware-independent order that differs from the pure
+// sequential sum only by rounding (<= ~1e-15 relative; north-star tolerance
+// 1e-12).
+//
+// Memory plan per iteration (C2: n=16.8M, nnz=521M):
+//   column stream  4 B/slot, read once, L1::no_allocate + L2::evict_first
+//   x = w_{r-1}    gathered; the `hot` leading entries (the highest-degree
+//                  vertices after relabelling) are staged in shared memory
+//                  once per CTA, the rest read through L1/L2
+//   katz r+w, w/lower/upper w  (coalesced: lanes own consecutive rows)
+#include "kb_internal.cuh"
+
+namespace kb {
+
+namespace {
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ int4 ld_stream_i4(const int32_t *p, uint64_t pol) {
+    int4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ int32_t ld_stream_i1(const int32_t *p, uint64_t pol) {
+    int32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+        : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream(double *p, double v) {
+    asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+struct IterArgs {
+    const int32_t *cols;
+    const int64_t *slice_off;
+    const int32_t *slice_w;
+    const int32_t *vlen;
+    int64_t nslices, nvr, nseg, nh;
+    const double *x;
+    double *w, *katz, *lower, *upper, *seg_sum;
+    double alpha, gamma;
+    int undirected;
+    int hot;
+    unsigned long long *counter;
+};
+
+__device__ __forceinline__ double fetch(const double *__restrict__ hot_s, int hot,
+                                        const double *__restrict__ x, int32_t c) {
+    return (c < hot) ? hot_s[c] : __ldg(x + c);
+}
+
+__device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s) {
+    const double w = __dmul_rn(A.alpha, s);          // engine.py:306
+    const double k = __dadd_rn(A.katz[v], w);        // :308
+    const double t = __dmul_rn(A.alpha, w);          // :309
+    A.katz[v] = k;
+    A.w[v] = w;                                      // :317
+    st_stream(A.lower + v, A.undirected ? __dadd_rn(k, t) : k);  // :313/:315
+    st_stream(A.upper + v, __dadd_rn(k, __dmul_rn(t, A.gamma)));  // :316
+}
+
+// Persistent kernel: each warp takes 32-row slices off a global counter.
+// Slices are ordered by descending length so the longest chains start first.
+__global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
+    extern __shared__ double hot_s[];
+    for (int i = threadIdx.x; i < A.hot; i += blockDim.x) hot_s[i] = A.x[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const double *__restrict__ x = A.x;
+    const uint64_t pol = evict_first_policy();
+    for (;;) {
+        unsigned long long s = 0;
+        if (lane == 0) s = atomicAdd(A.counter, 1ULL);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if ((int64_t)s >= A.nslices) break;
+        const int64_t vr = (int64_t)s * 32 + lane;
+        const int len = (vr < A.nvr) ? A.vlen[vr] : 0;
+        const int w = A.slice_w[s];
+        const int32_t *base = A.cols + A.slice_off[s];
+        double sum = 0.0;
+        if (w <= 4) {
+            for (int j = 0; j < w; j++) {
+                const int32_t c = ld_stream_i1(base + j * 32 + lane, pol);
+                if (j < len) sum = __dadd_rn(sum, fetch(hot_s, A.hot, x, c));
+            }
+        } else {
+            const int32_t *p = base + lane * 4;
+            const int w4 = w >> 2;
+            int j4 = 0;
+            for (; j4 + 2 <= w4; j4 += 2) {
+                const int4 ca = ld_stream_i4(p + (int64_t)j4 * 128, pol);
+                const int4 cb = ld_stream_i4(p + (int64_t)(j4 + 1) * 128, pol);
+                const int jb = j4 * 4;
+                double v[8];
+                v[0] = (jb + 0 < len) ? fetch(hot_s, A.hot, x, ca.x) : 0.0;
+                v[1] = (jb + 1 < len) ? fetch(hot_s, A.hot, x, ca.y) : 0.0;
+                v[2] = (jb + 2 < len) ? fetch(hot_s, A.hot, x, ca.z) : 0.0;
+                v[3] = (jb + 3 < len) ? fetch(hot_s, A.hot, x, ca.w) : 0.0;
+                v[4] = (jb + 4 < len) ? fetch(hot_s, A.hot, x, cb.x) : 0.0;
+                v[5] = (jb + 5 < len) ? fetch(hot_s, A.hot, x, cb.y) : 0.0;
+                v[6] = (jb + 6 < len) ? fetch(hot_s, A.hot, x, cb.z) : 0.0;
+                v[7] = (jb + 7 < len) ? fetch(hot_s, A.hot, x, cb.w) : 0.0;
+                // padding contributes +0.0, which leaves a non-negative sum
+                // bit-identical
+#pragma unroll
+                for (int q = 0; q < 8; q++) sum = __dadd_rn(sum, v[q]);
+            }
+            if (j4 < w4) {
+                const int4 ca = ld_stream_i4(p + (int64_t)j4 * 128, pol);
+                const int jb = j4 * 4;
+                double v[4];
+                v[0] = (jb + 0 < len) ? fetch(hot_s, A.hot, x, ca.x) : 0.0;
+                v[1] = (jb + 1 < len) ? fetch(hot_s, A.hot, x, ca.y) : 0.0;
+                v[2] = (jb + 2 < len) ? fetch(hot_s, A.hot, x, ca.z) : 0.0;
+                v[3] = (jb + 3 < len) ? fetch(hot_s, A.hot, x, ca.w) : 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; q++) sum = __dadd_rn(sum, v[q]);
+            }
+        }
+        if (vr < A.nvr) {
+            if (vr < A.nseg) A.seg_sum[vr] = sum;
+            else epilogue(A, A.nh + (vr - A.nseg), sum);
+        }
+    }
+}
+
+// heavy row h = combine its segment sums in segment order, then epilogue
+__global__ void k_heavy_combine(IterArgs A, const int32_t *seg_ptr,
+                                const int32_t *seg_list) {
+    int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h >= A.nh) return;
+    double s = 0.0;
+    for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++)
+        s = __dadd_rn(s, A.seg_sum[seg_list[q]]);
+    epilogue(A, h, s);
+}
+
+// rows without out-arcs: w = 0, katz unchanged (0), bounds collapse to katz
+__global__ void k_empty_rows(double *upper, double *lower, const double *katz,
+                             int64_t nv, int64_t n) {
+    int64_t i = nv + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    lower[i] = katz[i];
+    upper[i] = katz[i];
+}
+
+__global__ void k_gather(const int32_t *iperm, const double *src, double *dst,
+                         int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    dst[i] = src[iperm[i]];
+}
+
+}  // namespace
+
+void gather_to_original(const Graph &g, const double *src_new, double *dst_orig,
+                        cudaStream_t st) {
+    if (!g.n) return;
+    k_gather<<<(unsigned)((g.n + 255) / 256), 256, 0, st>>>(g.iperm.p, src_new,
+                                                           dst_orig, g.n); note_launch();
+    KB_CUDA(cudaGetLastError());
+}
+
+void collect_k1_times(State &s) {
+    for (; s.k1_read + 2 <= s.k1_used; s.k1_read += 2) {
+        float ms = 0;
+        KB_CUDA(cudaEventSynchronize(s.k1_ev[s.k1_read + 1]));
+        KB_CUDA(cudaEventElapsedTime(&ms, s.k1_ev[s.k1_read], s.k1_ev[s.k1_read + 1]));
+        s.spmv_ms += ms;
+        s.spmv_launches += 1;
+    }
+    if (s.k1_read == s.k1_used) s.k1_read = s.k1_used = 0;  // recycle the pool
+}
+
+void launch_iterate(State &s, cudaStream_t st) {
+    Graph &g = *s.g;
+    const int64_t n = g.n;
+    // new level buffer: rows without arcs stay exactly 0
+    DBuf<double> wnew;
+    wnew.alloc(n + 1);
+    KB_CUDA(cudaMemsetAsync(wnew.p + g.nv, 0, (n + 1 - g.nv) * sizeof(double), st));
+    IterArgs A;
+    A.cols = g.sell.cols.p;
+    A.slice_off = g.sell.slice_off.p;
+    A.slice_w = g.sell.slice_w.p;
+    A.vlen = g.sell.vlen.p;
+    A.nslices = g.sell.nslices;
+    A.nvr = g.sell.nvr;
+    A.nseg = g.sell.nseg;
+    A.nh = g.nh;
+    A.x = s.x_level();
+    A.w = wnew.p;
+    A.katz = s.katz.p;
+    A.lower = s.lower.p;
+    A.upper = s.upper.p;
+    A.seg_sum = s.seg_sum.p;
+    A.alpha = s.alpha;
+    A.gamma = s.gamma;
+    A.undirected = s.undirected;
+    A.hot = (int)std::min<int64_t>(g.hot, n);
+    A.counter = s.work_counter.p;
+    if (s.k1_used + 2 > s.k1_ev.size()) {
+        for (int q = 0; q < 2; q++) {
+            cudaEvent_t e;
+            KB_CUDA(cudaEventCreate(&e));
+            s.k1_ev.push_back(e);
+        }
+    }
+    KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used], st));
+    if (A.nslices) {
+        KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
+        const size_t smem = (size_t)A.hot * sizeof(double);
+        static bool attr_set = false;
+        if (!attr_set) {
+            KB_CUDA(cudaFuncSetAttribute(k_sell_iterate,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024));
+            attr_set = true;
+        }
+        k_sell_iterate<<<g.sm_count, 1024, smem, st>>>(A); note_launch();
+        KB_CUDA(cudaGetLastError());
+        if (g.nh) {
+            k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
+                A, g.seg_ptr.p, g.seg_list.p); note_launch();
+            KB_CUDA(cudaGetLastError());
+        }
+    }
+    KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used + 1], st));
+    s.k1_used += 2;
+    if (s.r == 0 && n > g.nv) {
+        k_empty_rows<<<(unsigned)((n - g.nv + 255) / 256), 256, 0, st>>>(
+            s.upper.p, s.lower.p, s.katz.p, g.nv, n); note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    s.levels.push_back(std::move(wnew));
+    s.r += 1;
+    if (!s.keep_all && s.levels.size() > 2) {
+        s.levels.erase(s.levels.begin());
+        s.level_base += 1;
+    }
+}
+
+}  // namespace kb

@@ -1,0 +1,228 @@
+"""CUDA path vs the CPU oracle and the reference's golden vectors (B200).
+
+Bar (north_star): identical certified order, iteration count and separated
+fraction; bounds bit-identical where every row sum is sequential (rows no
+longer than the split threshold -- all of them when the threshold is raised
+above deg_max), else within 1e-12 relative.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import katz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_1807_03847_b200")
+
+RTOL = 1e-12   # north_star: "bounds within a 1e-12 relative tolerance"
+
+
+def h16(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def to_graph(g0: O.CSRGraph) -> "P.Graph":
+    return P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+
+
+def crit(c):
+    kind = c["kind"]
+    if kind == "ranking":
+        return P.Criterion.ranking(c["epsilon"])
+    if kind == "topk":
+        return P.Criterion.top_k(c["k"], c["epsilon"])
+    if kind == "score":
+        return P.Criterion.score(c["epsilon"])
+    return P.Criterion.pair(c["u"], c["v"], c["epsilon"])
+
+
+def assert_same_active(mine, ref, lower, key):
+    mine, ref = np.sort(mine), np.sort(ref)
+    if np.array_equal(mine, ref):
+        return
+    assert mine.size == ref.size, key
+    np.testing.assert_array_equal(np.sort(lower[mine]), np.sort(lower[ref]), err_msg=key)
+
+
+def test_small_golden_cases_bitwise(golden_index, small_cases):
+    """Every small reference case: bitwise order/bounds/katz/levels/r."""
+    for c in golden_index["small"]:
+        key = c["key"]
+        e = small_cases[f"{c['graph']}/edges"]
+        g = P.Graph.from_edges(c["n"], e, undirected=False)
+        st = P.init(g, crit(c), undirected=c["undirected"])
+        assert st.alpha == c["alpha"] and st.gamma == c["gamma"], key
+        res = P.run(st, g)
+        assert res.iterations_used == c["r"], key
+        np.testing.assert_array_equal(res.order, small_cases[key + "/order"], err_msg=key)
+        np.testing.assert_array_equal(res.lower, small_cases[key + "/lower"], err_msg=key)
+        np.testing.assert_array_equal(res.upper, small_cases[key + "/upper"], err_msg=key)
+        np.testing.assert_array_equal(st.katz, small_cases[key + "/katz"], err_msg=key)
+        np.testing.assert_array_equal(np.stack(list(st.levels)),
+                                      small_cases[key + "/levels"], err_msg=key)
+        assert_same_active(st.active, small_cases[key + "/active"], res.lower, key)
+        assert res.separated_fraction == c["sepfrac"], key
+
+
+@pytest.fixture(scope="module")
+def c1():
+    g0 = O.rmat_graph(65536, edge_factor=16, seed=42)
+    return g0, to_graph(g0)
+
+
+def test_C1_exact_digests_without_split(golden_index, c1):
+    """Split threshold above deg_max: every row is one sequential sum, so the
+    device reproduces the reference's digests bit for bit."""
+    d = golden_index["digests"]["C1_topk100"]
+    g0, g = c1
+    dg = P.DeviceGraph(g0.indptr, g0.indices, split_threshold=1 << 20)
+    g._device = (g.version, dg)
+    st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
+    res = P.run(st, g)
+    g._device = None
+    assert res.iterations_used == d["r"]
+    assert res.separated_fraction == d["sepfrac"]
+    assert h16(res.order) == d["order"]
+    assert h16(res.lower) == d["lower"] and h16(res.upper) == d["upper"]
+    assert st.active.size == d["active"]
+
+
+def test_C1_default_split_within_tolerance(golden_index, c1):
+    d = golden_index["digests"]["C1_topk100"]
+    g0, g = c1
+    st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
+    info = st.device_graph.info()
+    assert info.heavy_rows == 1 and info.max_out_degree == 9648
+    res = P.run(st, g)
+    ost = O.OracleState(g0, O.Crit("topk", 1e-6, k=100))
+    ores = O.run(ost, g0)
+    assert res.iterations_used == ores.iterations_used == d["r"]
+    assert res.top(100) == d["top100"]
+    np.testing.assert_array_equal(res.order, ores.order)
+    np.testing.assert_allclose(res.lower, ores.lower, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(res.upper, ores.upper, rtol=RTOL, atol=0)
+    assert res.separated_fraction == d["sepfrac"]
+    assert sorted(st.active.tolist()) == sorted(ost.active.tolist())
+
+
+def test_fixture_eps_sweep(golden_index):
+    """Acceptance gate 08 on the ef8 fixture: r and separated fraction per eps."""
+    d = golden_index["digests"]
+    g0 = O.rmat_graph(65536, edge_factor=8, seed=42)
+    g = to_graph(g0)
+    for eps, r, frac in d["fixture_eps_sweep"]:
+        st = P.init(g, P.Criterion.ranking(eps), undirected=True)
+        res = P.run(st, g)
+        assert (res.iterations_used, res.separated_fraction) == (r, frac), eps
+
+
+def test_grid256_ranking_bitwise(golden_index):
+    """Exact interior ties: order decided by rounding, so only bit-exact
+    arithmetic reproduces it (SURVEY.md 8(c) parity fact 4)."""
+    d = golden_index["digests"]["grid256_ranking1e-9"]
+    g0 = O.grid_graph(256 * 256)
+    g = to_graph(g0)
+    st = P.init(g, P.Criterion.ranking(1e-9), undirected=True)
+    res = P.run(st, g)
+    assert res.iterations_used == d["r"] == 99
+    assert h16(res.order) == d["order"]
+    assert h16(res.lower) == d["lower"] and h16(res.upper) == d["upper"]
+    assert res.separated_fraction == d["sepfrac"]
+
+
+@pytest.mark.parametrize("split", [0, 64, 1 << 20])
+def test_rmat_s12_topk_vs_oracle(golden_index, split):
+    """Real Graph fixture of the golden set; segmentation thresholds vary."""
+    d = golden_index["digests"]["rmat_s12_seed3_topk50"]
+    g0 = O.rmat_graph(4096, edge_factor=16, seed=3)
+    g = to_graph(g0)
+    g._device = (g.version, P.DeviceGraph(g0.indptr, g0.indices, split_threshold=split))
+    st = P.init(g, P.Criterion.top_k(50, 1e-9), undirected=True)
+    res = P.run(st, g)
+    assert res.iterations_used == d["r"]
+    assert res.top(100) == d["top100"]
+    assert res.separated_fraction == d["sepfrac"]
+    if split == 1 << 20:
+        assert h16(res.lower) == d["lower"] and h16(res.upper) == d["upper"]
+        assert h16(res.order) == d["order"]
+    else:
+        ost = O.OracleState(g0, O.Crit("topk", 1e-9, k=50))
+        ores = O.run(ost, g0)
+        np.testing.assert_allclose(res.lower, ores.lower, rtol=RTOL, atol=0)
+        np.testing.assert_allclose(res.upper, ores.upper, rtol=RTOL, atol=0)
+
+
+def test_iterate_and_check_step_by_step():
+    """iterate_once/check_converged individually agree with the oracle at
+    every step, including the shrinking active set."""
+    g0 = O.rmat_graph(8192, edge_factor=16, seed=11)
+    g = to_graph(g0)
+    st = P.init(g, P.Criterion.top_k(20, 1e-8), undirected=True)
+    ost = O.OracleState(g0, O.Crit("topk", 1e-8, k=20))
+    for _ in range(12):
+        P.iterate_once(st, g)
+        O.iterate_once(ost, g0)
+        assert st.r == ost.r
+        np.testing.assert_allclose(st.levels[-1], ost.levels[-1], rtol=RTOL, atol=0)
+        np.testing.assert_allclose(st.katz, ost.katz, rtol=RTOL, atol=0)
+        done = P.check_converged(st)
+        odone = O.check_converged(ost)
+        assert done == odone
+        assert sorted(st.active.tolist()) == sorted(ost.active.tolist())
+        # the sorted prefix is identical and in the same order
+        k = min(20, st.active.size)
+        assert st.active[:k].tolist() == ost.active[:k].tolist()
+        if done:
+            break
+    assert done
+
+
+def test_directed_graph_and_pair_score():
+    rng = np.random.default_rng(4)
+    n = 3000
+    e = rng.integers(0, n, size=(20000, 2))
+    g = P.Graph.from_edges(n, e[e[:, 0] != e[:, 1]])
+    g0 = O.CSRGraph(n, *g.csr_arrays())
+    for c, oc in [(P.Criterion.score(1e-9), O.Crit("score", 1e-9)),
+                  (P.Criterion.pair(5, 17, 1e-7), O.Crit("pair", 1e-7, u=5, v=17)),
+                  (P.Criterion.ranking(1e-5), O.Crit("ranking", 1e-5))]:
+        st = P.init(g, c)
+        res = P.run(st, g)
+        ost = O.OracleState(g0, oc, undirected=False)
+        ores = O.run(ost, g0)
+        assert res.iterations_used == ores.iterations_used
+        np.testing.assert_array_equal(res.lower, ores.lower)
+        np.testing.assert_array_equal(res.upper, ores.upper)
+        np.testing.assert_array_equal(res.order, ores.order)
+        assert res.separated_fraction == ores.separated_fraction
+
+
+def test_device_symmetry_check():
+    g = P.Graph.from_edges(5, [(0, 1), (1, 2)], undirected=True)
+    assert P.device_graph(g).is_symmetric()
+    gd = P.Graph.from_edges(5, [(0, 1), (1, 2)])
+    assert not P.device_graph(gd).is_symmetric()
+
+
+def test_convergence_error_carries_iterations_and_gap():
+    g = P.Graph.from_edges(6, [(i, j) for i in range(6) for j in range(i + 1, 6)],
+                           undirected=True)
+    st = P.init(g, P.Criterion.score(1e-10), undirected=True, max_iterations=2)
+    with pytest.raises(P.ConvergenceError) as exc:
+        P.run(st, g)
+    assert exc.value.iterations == 2 and exc.value.gap > 1e-10
+
+
+def test_stale_graph_rejected():
+    g = P.Graph.from_edges(4, [(0, 1), (1, 2), (2, 3)], undirected=True)
+    st = P.init(g, P.Criterion.ranking(1e-6))
+    g.insert_arcs([(0, 2)])
+    with pytest.raises(P.StateError):
+        P.iterate_once(st, g)
+    st2 = P.init(g, P.Criterion.ranking(1e-6))
+    with pytest.raises(P.StateError):
+        P.check_converged(st2)
