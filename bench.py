@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""Benchmark: time to certified top-100 Katz ranking on R-MAT scale 24 (C2).
+
+Contract (one JSON line on rank 0):
+  step   = one certified run on the device-resident graph: init + run()
+           (iterate + device check until the top-100 is certified) +
+           ranking_result (order, bounds, separated fraction) kept on the
+           device.  value = seconds per step (lower is better).
+  e2e    = the same through the public API with HOST buffers: the canonical
+           CSR is uploaded from page-locked host memory (kb_graph_create:
+           H2D + device ingest), init + run, and the RankingResult arrays
+           (order, lower, upper) come back to the host.
+  roofline = the K1 SpMV+bounds kernel: algorithmic bytes per iteration
+           B_iter = 4*nnz + w_off*(n+1) + 48*n over its
+           average device duration (CUDA events on the library's stream).
+  cpu_baseline = the oracle port of the reference engine on this host's
+           cores, on a bounded sample (one iterate_once + check_converged on
+           the full C2 graph, plus ranking_result), projected to T_cert.
+  --impl reference: the reference's CPU implementation (the oracle port,
+           since the reference is Python and does not travel) on the same
+           config; each step = one iterate_once + check on the full graph.
+
+Inputs are larger than L2 (2.1 GB of column ids per iteration), so no L2
+flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "rmat-s24-ef16-topk100"
+METRIC = "time to certified top-100 Katz ranking (s); GTEPS/iter; HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 7:
+                for nm, val in zip(names, r[3:7]):
+                    if val.lower() == "active":
+                        reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def b_iter(n: int, nnz: int) -> int:
+    w_off = 4 if nnz < 2**31 else 8
+    return 4 * nnz + w_off * (n + 1) + 48 * n
+
+
+def cpu_leg(g0, k, eps, r_expected=None, reps=1):
+    """Oracle port on all host cores: one iterate+check on the full graph,
+    then ranking_result; returns (per-iteration seconds, result seconds)."""
+    from oracle import katz_oracle as O
+    threads = os.cpu_count() or 1
+    st = O.OracleState(g0, O.Crit("topk", eps, k=k), threads=threads)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.iterate_once(st, g0)
+        O.check_converged(st)
+        times.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    O.ranking_result(st)
+    t_res = time.perf_counter() - t0
+    return times, t_res, threads
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    from oracle import katz_oracle as O
+    n = 1 << a.scale
+    t0 = time.perf_counter()
+    g0 = O.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed)
+    t_gen = time.perf_counter() - t0
+    threads = os.cpu_count() or 1
+    # each step: one iterate_once + check_converged of the reference engine on
+    # the full graph; a fresh state every r_ref steps
+    r_ref = 7 if a.scale == 24 else None
+    st = O.OracleState(g0, O.Crit("topk", a.eps, k=a.k), threads=threads)
+    per = []
+    for i in range(a.warmup + a.steps):
+        if st.r >= 3:
+            st = O.OracleState(g0, O.Crit("topk", a.eps, k=a.k), threads=threads)
+        t0 = time.perf_counter()
+        O.iterate_once(st, g0)
+        O.check_converged(st)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            per.append(dt)
+    t0 = time.perf_counter()
+    O.ranking_result(st)
+    t_res = time.perf_counter() - t0
+    it = sum(per) / len(per)
+    r = r_ref or 7
+    value = r * it + t_res
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": it * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": n, "nnz": g0.nnz, "k": a.k, "eps": a.eps,
+                   "seed": a.seed, "r_assumed": r},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
+                         "sample": f"{a.steps} x (iterate_once+check_converged) on the full "
+                                   f"graph + 1 ranking_result; T_cert = r*iter + result"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gteps_per_iter": g0.nnz / it / 1e9, "generate_s": t_gen,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import numpy as np
+
+    import paper_1807_03847_b200 as P
+    from paper_1807_03847_b200 import _lib
+    from paper_1807_03847_b200 import generate as G
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    L = _lib.lib()
+    n = 1 << a.scale
+
+    t0 = time.perf_counter()
+    g = G.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed, device=device)
+    t_gen = time.perf_counter() - t0
+    info = g.device_graph.info()
+    nnz = int(info.nnz)
+    crit = P.Criterion.top_k(a.k, a.eps)
+
+    def step(keep_state=False):
+        st = P.init(g, crit, undirected=True, device=device)
+        out = P.engine.ctypes.c_int()
+        _lib.check(L.kb_run(st._h, P.engine.ctypes.byref(out)))
+        pairs = P.engine.ctypes.c_int64()
+        _lib.check(L.kb_result(st._h, None, None, None, P.engine.ctypes.byref(pairs)))
+        return st if keep_state else None
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        step()
+    lc0 = P.engine.ctypes.c_int64()
+    _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc0)))
+    states = []
+    barrier()
+    ms = P.engine.ctypes.c_double()
+    with ClockSampler(device) as clk:
+        _lib.check(L.kb_timer(device, 0, None))
+        for _ in range(a.steps):
+            states.append(step(keep_state=True))
+        _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms)))
+    lc1 = P.engine.ctypes.c_int64()
+    _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc1)))
+    elapsed_ms = ms.value
+    if dist is not None:
+        import torch
+        t = torch.tensor([elapsed_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / a.steps
+    st0 = states[0]
+    sinfo = st0._info()
+    r = int(sinfo.r)
+    spmv_ms, spmv_n = 0.0, 0
+    for s in states:
+        si = s._info()
+        spmv_ms += si.spmv_ms
+        spmv_n += si.spmv_launches
+    k1_ms = spmv_ms / max(1, spmv_n)
+    states = states[:1]
+    B = b_iter(n, nnz)
+    peak, peak_src = measured_peaks()
+    achieved = B / (k1_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("traffic_bytes_per_launch")
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        indptr, indices = g.csr_arrays()
+        indptr = np.ascontiguousarray(indptr)
+        indices = np.ascontiguousarray(indices)
+        _lib.check(L.kb_host_register(_lib.ptr(indptr), indptr.nbytes))
+        _lib.check(L.kb_host_register(_lib.ptr(indices), indices.nbytes))
+        order = np.empty(n, dtype=np.int64)
+        lo = np.empty(n, dtype=np.float64)
+        up = np.empty(n, dtype=np.float64)
+        for arr in (order, lo, up):
+            _lib.check(L.kb_host_register(_lib.ptr(arr), arr.nbytes))
+
+        def e2e_step():
+            dg = P.DeviceGraph(indptr, indices, device=device)
+            hg = G.DeviceResidentGraph(dg)
+            st = P.init(hg, crit, undirected=True, device=device)
+            out = P.engine.ctypes.c_int()
+            _lib.check(L.kb_run(st._h, P.engine.ctypes.byref(out)))
+            pairs = P.engine.ctypes.c_int64()
+            _lib.check(L.kb_result(st._h, _lib.ptr(order), _lib.ptr(lo), _lib.ptr(up),
+                                   P.engine.ctypes.byref(pairs)))
+            del st
+            dg.close()
+            return int(pairs.value)
+
+        e2e_step()
+        barrier()
+        _lib.check(L.kb_timer(device, 0, None))
+        t0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            e2e_step()
+        _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms)))
+        e2e_wall = (time.perf_counter() - t0) / a.e2e_steps
+        e2e = {"value": e2e_wall, "unit": "s",
+               "h2d_bytes_per_step": int(indptr.nbytes + indices.nbytes),
+               "d2h_bytes_per_step": int(order.nbytes + lo.nbytes + up.nbytes),
+               "device_ms_per_step": ms.value / a.e2e_steps,
+               "timing": "host wall clock around the public calls (each ends in a "
+                         "synchronising D2H copy)"}
+        for arr in (indptr, indices, order, lo, up):
+            L.kb_host_unregister(_lib.ptr(arr))
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        from oracle import katz_oracle as O
+        ip, ix = g.csr_arrays()
+        g0 = O.CSRGraph(n, ip, ix, symmetric=True)
+        it_times, t_res, threads = cpu_leg(g0, a.k, a.eps)
+        it = sum(it_times) / len(it_times)
+        cpu = {"value": r * it + t_res, "unit": "s", "cores": threads, "kind": "port",
+               "sample": f"1 x (iterate_once + check_converged) on the full C2 graph "
+                         f"({it:.2f}s) + ranking_result ({t_res:.2f}s); "
+                         f"T_cert projected as r*iter + result with r={r}"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC,
+            "value": ms_per_step / 1e3,
+            "unit": "s",
+            "n_gpus": world,
+            "steps": a.steps,
+            "warmup": a.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
+                       "seed": a.seed, "iterations": r,
+                       "max_out_degree": int(info.max_out_degree),
+                       "l2": "inputs larger than L2 (column stream 2.1 GB/iteration)",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "gteps_per_iter": nnz / (k1_ms * 1e-3) / 1e9,
+            "hbm_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_sell_iterate (+k_heavy_combine)",
+                         "bytes_per_launch": B, "avg_launch_ms": k1_ms,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(lc1.value - lc0.value),
+            "clocks": clocks,
+            "generate_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -43,6 +43,14 @@ cudaStream_t device_stream() {
     return streams[dev];
 }
 
+// page-locked mirror for small device->host reads; one per host thread, used
+// only inside a single synchronous API call
+unsigned long long *pinned_flags() {
+    static thread_local unsigned long long *p = nullptr;
+    if (!p) KB_CUDA(cudaMallocHost(&p, 64 * sizeof(unsigned long long)));
+    return p;
+}
+
 namespace {
 
 __global__ void k_fill(double *p, int64_t n, double v) {
@@ -325,7 +333,7 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.scratch_u64.alloc(1 << 16);
         s.scratch_i32.alloc(1 << 16);
         s.work_counter.alloc(1);
-        KB_CUDA(cudaMallocHost(&s.h_flags, 64 * sizeof(unsigned long long)));
+        s.h_flags = pinned_flags();
         KB_CUDA(cudaEventCreate(&s.ev0));
         KB_CUDA(cudaEventCreate(&s.ev1));
         KB_CUDA(cudaGetLastError());
@@ -339,7 +347,6 @@ int kb_state_destroy(kb_state *h) {
         if (!h) return;
         use_device(h->s.g->device);
         KB_CUDA(cudaStreamSynchronize(h->s.g->stream));
-        if (h->s.h_flags) cudaFreeHost(h->s.h_flags);
         if (h->s.ev0) cudaEventDestroy(h->s.ev0);
         if (h->s.ev1) cudaEventDestroy(h->s.ev1);
         for (cudaEvent_t e : h->s.k1_ev) cudaEventDestroy(e);
