@@ -91,6 +91,9 @@ int kb_device_count(int *count);
  * counter, page-locking of caller buffers for the host<->device copies */
 int kb_timer(int device, int op /* 0 start, 1 stop */, double *elapsed_ms);
 int kb_launch_count(int64_t *count);
+/* named tuning knobs of the kernels (e.g. "k1.depth", "k1.hot"); defaults
+ * apply when unset */
+int kb_tune(const char *name, int64_t value);
 int kb_host_register(void *ptr, int64_t bytes);
 int kb_host_unregister(void *ptr);
 

@@ -61,6 +61,7 @@ SIGNATURES = {
     "kb_device_count": (i32, [ctypes.POINTER(i32)]),
     "kb_timer": (i32, [i32, i32, ctypes.POINTER(dbl)]),
     "kb_launch_count": (i32, [ctypes.POINTER(i64)]),
+    "kb_tune": (i32, [ctypes.c_char_p, i64]),
     "kb_host_register": (i32, [vp, i64]),
     "kb_host_unregister": (i32, [vp]),
     "kb_graph_create": (i32, [i32, i64, i64, vp, vp, i64, i64, ctypes.POINTER(vp)]),

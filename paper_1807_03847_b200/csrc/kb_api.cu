@@ -8,6 +8,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "kb_internal.cuh"
 
@@ -22,6 +24,14 @@ namespace kb {
 
 static thread_local std::string t_err;
 static std::atomic<int64_t> g_launches{0};
+static std::mutex g_tune_mu;
+static std::vector<std::pair<std::string, int64_t>> g_tune;
+int64_t tune_get(const char *name, int64_t dflt) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    for (auto &kv : g_tune)
+        if (kv.first == name) return kv.second;
+    return dflt;
+}
 void note_launch(int64_t k) { g_launches += k; }
 int64_t launch_count() { return g_launches.load(); }
 void set_error(const std::string &msg) { t_err = msg; }
@@ -131,6 +141,16 @@ int kb_timer(int device, int op, double *elapsed_ms) {
     });
 }
 
+int kb_tune(const char *name, int64_t value) {
+    return guarded([&] {
+        KB_REQUIRE(name, KB_EPARAM, "NULL name");
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        for (auto &kv : g_tune)
+            if (kv.first == name) { kv.second = value; return; }
+        g_tune.emplace_back(name, value);
+    });
+}
+
 int kb_launch_count(int64_t *count) {
     return guarded([&] {
         KB_REQUIRE(count, KB_EPARAM, "NULL argument");
@@ -183,9 +203,9 @@ static kb_graph *new_graph(int device, int64_t split_threshold, int64_t hot_size
     g.device = device;
     KB_CUDA(cudaDeviceGetAttribute(&g.sm_count, cudaDevAttrMultiProcessorCount, device));
     g.stream = device_stream();
-    g.split = split_threshold > 0 ? split_threshold : 8192;
+    g.split = split_threshold > 0 ? split_threshold : 2048;
     g.split = std::max<int64_t>(4, g.split & ~(int64_t)3);
-    g.hot = hot_size >= 0 ? hot_size : 24576;
+    g.hot = hot_size >= 0 ? hot_size : 12288;
     return h;
 }
 

@@ -32,6 +32,9 @@ struct Error {
         if (!(cond)) throw ::kb::Error{(code), (msg)};                         \
     } while (0)
 
+// named tuning knobs (kb_tune); default when unset
+int64_t tune_get(const char *name, int64_t dflt);
+
 // number of kernel launches issued by the library (bench.py gpu_launches)
 void note_launch(int64_t k = 1);
 int64_t launch_count();

@@ -65,9 +65,22 @@ struct IterArgs {
     unsigned long long *counter;
 };
 
+// XL: 0 = ld.global.nc (read-only path, L1 allocate), 1 = ld.global.cg
+// (L2 only), 2 = ld.global.ca with an L2 evict_last hint
+template <int XL>
+__device__ __forceinline__ double ldx(const double *p) {
+    if (XL == 0) return __ldg(p);
+    double r;
+    if (XL == 1) asm("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    else asm("{ .reg .b64 pol; createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+             "  ld.global.nc.L2::cache_hint.f64 %0, [%1], pol; }" : "=d"(r) : "l"(p));
+    return r;
+}
+
+template <int XL>
 __device__ __forceinline__ double fetch(const double *__restrict__ hot_s, int hot,
                                         const double *__restrict__ x, int32_t c) {
-    return (c < hot) ? hot_s[c] : __ldg(x + c);
+    return (c < hot) ? hot_s[c] : ldx<XL>(x + c);
 }
 
 __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s) {
@@ -80,8 +93,24 @@ __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s)
     st_stream(A.upper + v, __dadd_rn(k, __dmul_rn(t, A.gamma)));  // :316
 }
 
+// Gather of one batch of 8 column slots (two int4 groups) of a lane's row;
+// slots at or beyond the row length read as +0.0 without touching memory.
+template <int XL>
+__device__ __forceinline__ void gather8(const double *__restrict__ hot_s, int hot,
+                                        const double *__restrict__ x, int4 ca, int4 cb,
+                                        int jb, int len, double v[8]) {
+    const int32_t c[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+        v[q] = (jb + q < len) ? fetch<XL>(hot_s, hot, x, c[q]) : 0.0;
+}
+
 // Persistent kernel: each warp takes 32-row slices off a global counter.
 // Slices are ordered by descending length so the longest chains start first.
+// DEPTH batches of 8 gathers per lane are kept in flight (software pipeline):
+// the loads of batch i+1..i+DEPTH-1 are issued before batch i is folded, so
+// the in-order dependent add chain never waits on a single batch's latency.
+template <int DEPTH, int XL>
 __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     extern __shared__ double hot_s[];
     for (int i = threadIdx.x; i < A.hot; i += blockDim.x) hot_s[i] = A.x[i];
@@ -89,6 +118,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     const int lane = threadIdx.x & 31;
     const double *__restrict__ x = A.x;
     const uint64_t pol = evict_first_policy();
+    const int4 zero4 = make_int4(0, 0, 0, 0);
     for (;;) {
         unsigned long long s = 0;
         if (lane == 0) s = atomicAdd(A.counter, 1ULL);
@@ -100,42 +130,45 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         const int32_t *base = A.cols + A.slice_off[s];
         double sum = 0.0;
         if (w <= 4) {
-            for (int j = 0; j < w; j++) {
-                const int32_t c = ld_stream_i1(base + j * 32 + lane, pol);
-                if (j < len) sum = __dadd_rn(sum, fetch(hot_s, A.hot, x, c));
-            }
+            int32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (j < w) c[j] = ld_stream_i1(base + j * 32 + lane, pol);
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (j < len) sum = __dadd_rn(sum, fetch<XL>(hot_s, A.hot, x, c[j]));
         } else {
             const int32_t *p = base + lane * 4;
-            const int w4 = w >> 2;
-            int j4 = 0;
-            for (; j4 + 2 <= w4; j4 += 2) {
-                const int4 ca = ld_stream_i4(p + (int64_t)j4 * 128, pol);
-                const int4 cb = ld_stream_i4(p + (int64_t)(j4 + 1) * 128, pol);
-                const int jb = j4 * 4;
-                double v[8];
-                v[0] = (jb + 0 < len) ? fetch(hot_s, A.hot, x, ca.x) : 0.0;
-                v[1] = (jb + 1 < len) ? fetch(hot_s, A.hot, x, ca.y) : 0.0;
-                v[2] = (jb + 2 < len) ? fetch(hot_s, A.hot, x, ca.z) : 0.0;
-                v[3] = (jb + 3 < len) ? fetch(hot_s, A.hot, x, ca.w) : 0.0;
-                v[4] = (jb + 4 < len) ? fetch(hot_s, A.hot, x, cb.x) : 0.0;
-                v[5] = (jb + 5 < len) ? fetch(hot_s, A.hot, x, cb.y) : 0.0;
-                v[6] = (jb + 6 < len) ? fetch(hot_s, A.hot, x, cb.z) : 0.0;
-                v[7] = (jb + 7 < len) ? fetch(hot_s, A.hot, x, cb.w) : 0.0;
-                // padding contributes +0.0, which leaves a non-negative sum
-                // bit-identical
+            const int w4 = w >> 2;             // int4 groups per lane
+            const int nb = (w4 + 1) >> 1;      // batches of 8 slots
+            double v[DEPTH][8];
 #pragma unroll
-                for (int q = 0; q < 8; q++) sum = __dadd_rn(sum, v[q]);
+            for (int d = 0; d < DEPTH; d++) {
+                if (d < nb) {
+                    const int g0 = 2 * d;
+                    const int4 ca = ld_stream_i4(p + (int64_t)g0 * 128, pol);
+                    const int4 cb = (g0 + 1 < w4) ? ld_stream_i4(p + (int64_t)(g0 + 1) * 128, pol)
+                                                  : zero4;
+                    gather8<XL>(hot_s, A.hot, x, ca, cb, g0 * 4, len, v[d]);
+                }
             }
-            if (j4 < w4) {
-                const int4 ca = ld_stream_i4(p + (int64_t)j4 * 128, pol);
-                const int jb = j4 * 4;
-                double v[4];
-                v[0] = (jb + 0 < len) ? fetch(hot_s, A.hot, x, ca.x) : 0.0;
-                v[1] = (jb + 1 < len) ? fetch(hot_s, A.hot, x, ca.y) : 0.0;
-                v[2] = (jb + 2 < len) ? fetch(hot_s, A.hot, x, ca.z) : 0.0;
-                v[3] = (jb + 3 < len) ? fetch(hot_s, A.hot, x, ca.w) : 0.0;
+            for (int b = 0; b < nb; b += DEPTH) {
 #pragma unroll
-                for (int q = 0; q < 4; q++) sum = __dadd_rn(sum, v[q]);
+                for (int d = 0; d < DEPTH; d++) {
+                    if (b + d < nb) {
+#pragma unroll
+                        for (int q = 0; q < 8; q++) sum = __dadd_rn(sum, v[d][q]);
+                        const int bn = b + d + DEPTH;  // refill this slot
+                        if (bn < nb) {
+                            const int g0 = 2 * bn;
+                            const int4 ca = ld_stream_i4(p + (int64_t)g0 * 128, pol);
+                            const int4 cb = (g0 + 1 < w4)
+                                                ? ld_stream_i4(p + (int64_t)(g0 + 1) * 128, pol)
+                                                : zero4;
+                            gather8<XL>(hot_s, A.hot, x, ca, cb, g0 * 4, len, v[d]);
+                        }
+                    }
+                }
             }
         }
         if (vr < A.nvr) {
@@ -218,7 +251,7 @@ void launch_iterate(State &s, cudaStream_t st) {
     A.alpha = s.alpha;
     A.gamma = s.gamma;
     A.undirected = s.undirected;
-    A.hot = (int)std::min<int64_t>(g.hot, n);
+    A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), n);
     A.counter = s.work_counter.p;
     if (s.k1_used + 2 > s.k1_ev.size()) {
         for (int q = 0; q < 2; q++) {
@@ -231,14 +264,17 @@ void launch_iterate(State &s, cudaStream_t st) {
     if (A.nslices) {
         KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
         const size_t smem = (size_t)A.hot * sizeof(double);
-        static bool attr_set = false;
-        if (!attr_set) {
-            KB_CUDA(cudaFuncSetAttribute(k_sell_iterate,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024));
-            attr_set = true;
-        }
-        k_sell_iterate<<<g.sm_count, 1024, smem, st>>>(A); note_launch();
+        const int depth = (int)tune_get("k1.depth", 1);
+        const int xl = (int)tune_get("k1.xload", 0);
+        const int threads = (int)tune_get("k1.threads", 1024);
+        const int ctas = (int)tune_get("k1.ctas_per_sm", 1);
+        auto kern = k_sell_iterate<2, 0>;
+        if (depth == 1) kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2> : k_sell_iterate<1, 0>;
+        else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
+        else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        kern<<<g.sm_count * ctas, threads, smem, st>>>(A); note_launch();
         KB_CUDA(cudaGetLastError());
         if (g.nh) {
             k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
