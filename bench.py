@@ -224,7 +224,7 @@ def main():
     k1_times = []
 
     def step():
-        st = P.init(g, crit, undirected=True, device=device)
+        st = P.init(g, crit, undirected=True, device=device, max_iterations=200)
         out = P.engine.ctypes.c_int()
         _lib.check(L.kb_run(st._h, P.engine.ctypes.byref(out)))
         pairs = P.engine.ctypes.c_int64()
@@ -287,7 +287,7 @@ def main():
         def e2e_step():
             dg = P.DeviceGraph(indptr, indices, device=device)
             hg = G.DeviceResidentGraph(dg)
-            st = P.init(hg, crit, undirected=True, device=device)
+            st = P.init(hg, crit, undirected=True, device=device, max_iterations=200)
             out = P.engine.ctypes.c_int()
             _lib.check(L.kb_run(st._h, P.engine.ctypes.byref(out)))
             pairs = P.engine.ctypes.c_int64()

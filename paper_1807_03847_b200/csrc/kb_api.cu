@@ -349,6 +349,11 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.act[0].alloc(n);
         s.act[1].alloc(n);
         s.act_dense = true;  // :152 arange(n), materialised on first check
+        s.tail_zero_from = g.nv;
+        s.cand.alloc(n);
+        s.stK.alloc(n);
+        s.stU.alloc(n);
+        s.stI.alloc(n);
         s.m_host = n;
         s.scratch_u64.alloc(1 << 16);
         s.scratch_i32.alloc(1 << 16);

@@ -21,6 +21,8 @@
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/device/device_partition.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <cub/block/block_reduce.cuh>
 
 #include <algorithm>
@@ -50,60 +52,172 @@ struct TopkArgs {
     int32_t *act_out;
     int64_t k;
     double eps;
-    unsigned int *hist;             // 12 * 256
-    unsigned long long *blk;        // 2 * gridDim
+    unsigned int *hist;             // HIST_WORDS
+    unsigned long long *blk;        // 2 * gridDim + 2
     int32_t *prefix_buf;            // k
+    int32_t *cand;                  // capacity m: positions matching the 24-bit prefix
+    uint64_t *stK;                  // staged keys / uppers / ids (non-dense sets)
+    double *stU;
+    int32_t *stI;
     unsigned long long *out;        // [0]=new m, [1]=converged, [2]=#prefix
 };
 
-__global__ void __launch_bounds__(CHK_THREADS) k_topk_select(TopkArgs A) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ unsigned int sh[256];
-    __shared__ uint64_t s_sel[2];
-    __shared__ int64_t s_need;
-    const int64_t G = gridDim.x;
-    const int64_t chunk = (A.m + G - 1) / G;
-    const int64_t i0 = min(A.m, blockIdx.x * chunk), i1 = min(A.m, i0 + chunk);
+// digit plan: two 12-bit digits over all elements, then the survivors of the
+// 24-bit prefix are compacted and five 8-bit digits finish on them; ties at
+// the cut take four 8-bit digits of the original id
+constexpr int HIST_WORDS = 2 * 4096 + 5 * 256 + 4 * 256;
 
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i < 12 * 256; i += blockDim.x) A.hist[i] = 0;
+// Shared-memory histogram increment with warp aggregation: lanes hitting the
+// same bin (common for the exponent digit) elect one leader that adds the
+// group's count, so a warp costs at most one atomic per distinct bin.
+__device__ __forceinline__ void hist_add(unsigned int *sh, unsigned bin, bool active) {
+    const unsigned mask = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const unsigned peers = __match_any_sync(mask, bin);
+    if ((threadIdx.x & 31) == (__ffs(peers) - 1)) atomicAdd(&sh[bin], __popc(peers));
+}
+
+// Find the bin where the running count (from the top, or from the bottom)
+// first reaches `need`; every block computes it identically from the global
+// histogram.  Block-parallel: bins are staged in shared memory and scanned
+// with cub::BlockScan over per-thread runs.
+__device__ __forceinline__ void select_digit(unsigned int *sh, const unsigned int *gh, int nbins,
+                                             int64_t &need, int &sel, bool from_top) {
+    typedef cub::BlockScan<unsigned long long, CHK_THREADS> BS;
+    __shared__ typename BS::TempStorage bs_tmp;
+    __shared__ unsigned long long s_res[2];
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) sh[b] = gh[b];
+    __syncthreads();
+    const int per = (nbins + CHK_THREADS - 1) / CHK_THREADS;
+    unsigned long long mine = 0;
+    for (int q = 0; q < per; q++) {
+        const int bp = threadIdx.x * per + q;  // position in scan order
+        if (bp < nbins) mine += sh[from_top ? nbins - 1 - bp : bp];
+    }
+    unsigned long long before;
+    BS(bs_tmp).ExclusiveSum(mine, before);
+    unsigned long long cum = before;
+    for (int q = 0; q < per; q++) {
+        const int bp = threadIdx.x * per + q;
+        if (bp >= nbins) break;
+        const int bin = from_top ? nbins - 1 - bp : bp;
+        const unsigned long long c = sh[bin];
+        if (cum < (unsigned long long)need && cum + c >= (unsigned long long)need) {
+            s_res[0] = (unsigned long long)bin;
+            s_res[1] = cum;
+        }
+        cum += c;
+    }
+    __syncthreads();
+    sel = (int)s_res[0];
+    need -= (int64_t)s_res[1];
+    __syncthreads();
+}
+
+constexpr int UNR = 4;  // elements per thread per tile (memory-level parallelism)
+
+__global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned int sh[4096];
+    const int64_t G = gridDim.x;
+    const int64_t TILE = (int64_t)CHK_THREADS * UNR;
+    const int64_t chunk = ((A.m + G - 1) / G + TILE - 1) / TILE * TILE;
+    const int64_t i0 = min(A.m, blockIdx.x * chunk), i1 = min(A.m, i0 + chunk);
+    unsigned long long *ncand = A.blk + 2 * G;
+    // Element views: dense -> lower/upper by position; otherwise the active
+    // ids are first staged into contiguous key/upper/id arrays so that every
+    // later pass streams instead of gathering.
+    const bool dense = A.dense;
+    auto id_at = [&](int64_t i) -> int32_t { return dense ? (int32_t)i : A.act_in[i]; };
+
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < HIST_WORDS; i += blockDim.x) A.hist[i] = 0;
+        if (threadIdx.x == 0) *ncand = 0;
+    }
     grid.sync();
 
-    // ---- 1. k-th largest key
+    // ---- 1a. two 12-bit digits over the whole active set
     uint64_t prefix = 0, mask = 0;
     int64_t kk = A.k;
-    for (int p = 0; p < 8; p++) {
-        const int shift = 56 - 8 * p;
+    for (int p = 0; p < 2; p++) {
+        const int shift = 52 - 12 * p;
+        unsigned int *gh = A.hist + p * 4096;
+        for (int b = threadIdx.x; b < 4096; b += blockDim.x) sh[b] = 0;
+        __syncthreads();
+        for (int64_t t = i0; t < i1; t += TILE) {
+            uint64_t key[UNR];
+#pragma unroll
+            for (int q = 0; q < UNR; q++) {
+                const int64_t i = t + q * CHK_THREADS + threadIdx.x;
+                key[q] = i < i1 ? key_of(A.lower, id_at(i)) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < UNR; q++) {
+                const int64_t i = t + q * CHK_THREADS + threadIdx.x;
+                const bool on = i < i1 && (key[q] & mask) == prefix;
+                hist_add(sh, (unsigned)((key[q] >> shift) & 4095), on);
+            }
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < 4096; b += blockDim.x)
+            if (sh[b]) atomicAdd(&gh[b], sh[b]);
+        grid.sync();
+        int sel;
+        select_digit(sh, gh, 4096, kk, sel, true);
+        prefix |= (uint64_t)sel << shift;
+        mask |= (uint64_t)0xFFF << shift;
+    }
+    // ---- 1b. compact the positions carrying the 24-bit prefix
+    for (int64_t t = i0; t < i1; t += TILE) {
+        uint64_t key[UNR];
+#pragma unroll
+        for (int q = 0; q < UNR; q++) {
+            const int64_t i = t + q * CHK_THREADS + threadIdx.x;
+            key[q] = i < i1 ? key_of(A.lower, id_at(i)) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < UNR; q++) {
+            const int64_t i = t + q * CHK_THREADS + threadIdx.x;
+            const bool on = i < i1 && (key[q] & mask) == prefix;
+            const unsigned bal = __ballot_sync(0xffffffffu, on);
+            if (bal) {
+                unsigned long long base = 0;
+                const int lane = threadIdx.x & 31;
+                if (lane == __ffs(bal) - 1) base = atomicAdd(ncand, (unsigned long long)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+                if (on) A.cand[base + __popc(bal & ((1u << lane) - 1))] = (int32_t)i;
+            }
+        }
+    }
+    grid.sync();
+    const int64_t nc = (int64_t)*ncand;
+    const int64_t cchunk = (nc + G - 1) / G;
+    const int64_t c0 = min(nc, blockIdx.x * cchunk), c1 = min(nc, c0 + cchunk);
+    // ---- 1c. five 8-bit digits over the candidates
+    for (int p = 0; p < 5; p++) {
+        const int shift = 32 - 8 * p;
+        unsigned int *gh = A.hist + 2 * 4096 + p * 256;
         for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = 0;
         __syncthreads();
-        for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-            const int32_t id = A.dense ? (int32_t)i : A.act_in[i];
-            const uint64_t key = key_of(A.lower, id);
-            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255], 1u);
+        for (int64_t i0w = c0; i0w < c1; i0w += blockDim.x) {
+            const int64_t i = i0w + threadIdx.x;
+            bool on = i < c1;
+            uint64_t key = 0;
+            if (on) key = key_of(A.lower, id_at(A.cand[i]));
+            on = on && (key & mask) == prefix;
+            hist_add(sh, (unsigned)((key >> shift) & 255), on);
         }
         __syncthreads();
         for (int b = threadIdx.x; b < 256; b += blockDim.x)
-            if (sh[b]) atomicAdd(&A.hist[p * 256 + b], sh[b]);
+            if (sh[b]) atomicAdd(&gh[b], sh[b]);
         grid.sync();
-        if (threadIdx.x == 0) {
-            int64_t cum = 0;
-            int sel = 0;
-            for (int b = 255; b >= 0; b--) {
-                const int64_t c = A.hist[p * 256 + b];
-                if (cum + c >= kk) { sel = b; break; }
-                cum += c;
-            }
-            s_sel[0] = (uint64_t)sel;
-            s_need = kk - cum;
-        }
-        __syncthreads();
-        prefix |= s_sel[0] << shift;
+        int sel;
+        select_digit(sh, gh, 256, kk, sel, true);
+        prefix |= (uint64_t)sel << shift;
         mask |= (uint64_t)0xFF << shift;
-        kk = s_need;
-        __syncthreads();
     }
     const uint64_t kstar = prefix;
-    const int64_t count_eq = A.hist[7 * 256 + (int)(kstar & 255)];
+    const int64_t count_eq = A.hist[2 * 4096 + 4 * 256 + (int)(kstar & 255)];
 
     // ---- 2. ties at the cut: the kk smallest original ids among key == kstar
     uint32_t istar = 0xFFFFFFFFu;
@@ -112,94 +226,63 @@ __global__ void __launch_bounds__(CHK_THREADS) k_topk_select(TopkArgs A) {
         int64_t need = kk;
         for (int p = 0; p < 4; p++) {
             const int shift = 24 - 8 * p;
+            unsigned int *gh = A.hist + 2 * 4096 + 5 * 256 + p * 256;
             for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = 0;
             __syncthreads();
-            for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-                const int32_t id = A.dense ? (int32_t)i : A.act_in[i];
-                if (key_of(A.lower, id) != kstar) continue;
-                const uint32_t o = (uint32_t)A.perm[id];
-                if ((o & imask) == ipre) atomicAdd(&sh[(o >> shift) & 255], 1u);
+            for (int64_t i0w = c0; i0w < c1; i0w += blockDim.x) {
+                const int64_t i = i0w + threadIdx.x;
+                bool on = i < c1;
+                uint32_t o = 0;
+                if (on) {
+                    const int32_t pos = A.cand[i];
+                    on = key_of(A.lower, id_at(pos)) == kstar;
+                    if (on) o = (uint32_t)A.perm[id_at(pos)];
+                }
+                on = on && (o & imask) == ipre;
+                hist_add(sh, (o >> shift) & 255, on);
             }
             __syncthreads();
             for (int b = threadIdx.x; b < 256; b += blockDim.x)
-                if (sh[b]) atomicAdd(&A.hist[(8 + p) * 256 + b], sh[b]);
+                if (sh[b]) atomicAdd(&gh[b], sh[b]);
             grid.sync();
-            if (threadIdx.x == 0) {
-                int64_t cum = 0;
-                int sel = 255;
-                for (int b = 0; b < 256; b++) {
-                    const int64_t c = A.hist[(8 + p) * 256 + b];
-                    if (cum + c >= need) { sel = b; break; }
-                    cum += c;
-                }
-                s_sel[0] = (uint64_t)sel;
-                s_need = need - cum;
-            }
-            __syncthreads();
-            ipre |= (uint32_t)s_sel[0] << shift;
+            int sel;
+            select_digit(sh, gh, 256, need, sel, false);
+            ipre |= (uint32_t)sel << shift;
             imask |= 0xFFu << shift;
-            need = s_need;
-            __syncthreads();
         }
         istar = ipre;
     }
-    const double thr = __longlong_as_double((long long)kstar);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.out[3] = kstar;
+        A.out[4] = istar;
+    }
+}
 
-    // ---- 3. order-preserving compaction
-    typedef cub::BlockScan<int, CHK_THREADS> Scan;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ int s_tot[2];
-    auto classify = [&](int64_t i, int32_t &id, int &top, int &surv) {
-        top = surv = 0;
-        if (i >= i1) return;
-        id = A.dense ? (int32_t)i : A.act_in[i];
-        const uint64_t key = key_of(A.lower, id);
-        top = key > kstar || (key == kstar && (uint32_t)A.perm[id] <= istar);
-        if (!top) surv = __dsub_rn(A.upper[id], A.eps) >= thr;
-    };
-    {
-        unsigned long long nt = 0, ns = 0;
-        for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-            int32_t id; int t, s;
-            classify(i, id, t, s);
-            nt += t; ns += s;
-        }
-        typedef cub::BlockReduce<unsigned long long, CHK_THREADS> Red;
-        __shared__ typename Red::TempStorage red_tmp;
-        unsigned long long a = Red(red_tmp).Sum(nt);
-        __syncthreads();
-        unsigned long long b = Red(red_tmp).Sum(ns);
-        if (threadIdx.x == 0) { A.blk[blockIdx.x] = a; A.blk[G + blockIdx.x] = b; }
+// Three-way split of the active set once the cut (kstar, istar) is known:
+// winners (the k best by (-lower, id)) and survivors (the rest with
+// fl(upper - eps) >= threshold, engine.py:368-373) in active-set order.
+struct IsWinner {
+    const double *lower;
+    const int32_t *perm;
+    const unsigned long long *cut;
+    __device__ bool operator()(int32_t id) const {
+        const uint64_t key = key_of(lower, id), kstar = cut[3];
+        return key > kstar || (key == kstar && (uint32_t)perm[id] <= (uint32_t)cut[4]);
     }
-    grid.sync();
-    __shared__ unsigned long long s_off[2];
-    if (threadIdx.x == 0) {
-        unsigned long long ot = 0, os = 0, ts = 0;
-        for (int64_t b = 0; b < G; b++) {
-            if (b < blockIdx.x) { ot += A.blk[b]; os += A.blk[G + b]; }
-            ts += A.blk[G + b];
-        }
-        s_off[0] = ot;
-        s_off[1] = os;
-        if (blockIdx.x == 0) { A.out[0] = (unsigned long long)A.k + ts; A.out[2] = A.k; }
+};
+struct IsSurvivor {
+    const double *lower, *upper;
+    const unsigned long long *cut;
+    double eps;
+    __device__ bool operator()(int32_t id) const {
+        const double thr = __longlong_as_double((long long)cut[3]);
+        return __dsub_rn(upper[id], eps) >= thr;
     }
-    __syncthreads();
-    unsigned long long ot = s_off[0], os = s_off[1];
-    for (int64_t base = i0; base < i1; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        int32_t id = 0; int t, s;
-        classify(i, id, t, s);
-        int pt, ps;
-        Scan(scan_tmp).ExclusiveSum(t, pt, s_tot[0]);
-        __syncthreads();
-        Scan(scan_tmp).ExclusiveSum(s, ps, s_tot[1]);
-        __syncthreads();
-        if (t) A.prefix_buf[ot + pt] = id;
-        if (s) A.act_out[A.k + os + ps] = id;
-        ot += s_tot[0];
-        os += s_tot[1];
-        __syncthreads();
-    }
+};
+
+__global__ void k_cut_counts(unsigned long long *out, int64_t k) {
+    out[0] = (unsigned long long)k + out[6];  // |active| after the cut
+    out[2] = (unsigned long long)k;           // winners in the prefix buffer
 }
 
 // Sort the prefix by (-lower, original id), write it to act_out[0..cnt), and
@@ -635,18 +718,45 @@ bool run_check(State &s, cudaStream_t st) {
         A.upper = s.upper.p;
         A.perm = g.perm.p;
         A.act_in = s.act[s.cur].p;
-        A.m = m;
+        // in the dense first check, rows without out-arcs (new ids >= nv) have
+        // lower == upper == 0 < every other lower: when k <= nv they can be
+        // neither winners nor survivors, so they are dropped unread
+        A.m = (s.act_dense && k <= s.tail_zero_from) ? s.tail_zero_from : m;
         A.dense = s.act_dense;
         A.act_out = s.act[nxt].p;
         A.k = k;
         A.eps = s.eps;
         A.hist = (unsigned int *)(s.scratch_u64.p + 8);
-        const int G = coop_grid(g.sm_count);
-        A.blk = s.scratch_u64.p + 8 + 12 * 256;
+        // small active sets run in one block (grid.sync degenerates)
+        const int G = (int)std::max<int64_t>(
+            1, std::min<int64_t>(coop_grid(g.sm_count), (A.m + 8191) / 8192));
+        A.blk = s.scratch_u64.p + 8 + HIST_WORDS;
         A.prefix_buf = s.scratch_i32.p;
+        A.cand = s.cand.p;
+        A.stK = s.stK.p;
+        A.stU = s.stU.p;
+        A.stI = s.stI.p;
         A.out = out;
         void *args[] = {&A};
         KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
+        note_launch();
+        IsWinner win{s.lower.p, g.perm.p, out};
+        IsSurvivor sur{s.lower.p, s.upper.p, out, s.eps};
+        unsigned long long *nsel = out + 5;  // [5]=winners, [6]=survivors
+        int32_t *unsel = s.stI.p;
+        size_t tb = 0;
+        auto run_part = [&](auto in) {
+            KB_CUDA(cub::DevicePartition::If(nullptr, tb, in, A.prefix_buf, s.act[nxt].p + k, unsel,
+                                             nsel, (int)A.m, win, sur, st));
+            ensure_cub_tmp(s, tb);
+            KB_CUDA(cub::DevicePartition::If(s.cub_tmp.p, tb, in, A.prefix_buf, s.act[nxt].p + k,
+                                             unsel, nsel, (int)A.m, win, sur, st));
+            note_launch();
+        };
+        if (A.dense) run_part(cub::CountingInputIterator<int32_t>(0));
+        else run_part((const int32_t *)s.act[s.cur].p);
+        k_cut_counts<<<1, 1, 0, st>>>(out, k);
+        note_launch();
         int P = 1;
         while (P < k) P <<= 1;
         const size_t smem = (size_t)P * 16;

@@ -132,6 +132,11 @@ struct State {
     DBuf<int32_t> act[2];
     int cur = 0;
     bool act_dense = true;  // active == arange(n) (never materialised)
+    int64_t tail_zero_from = 0;  // new ids >= this have lower == upper == 0
+    DBuf<int32_t> cand;          // selection candidates (capacity n)
+    DBuf<uint64_t> stK;          // staged keys/uppers/ids of the active set
+    DBuf<double> stU;
+    DBuf<int32_t> stI;
     int64_t m_host = 0;     // |active| mirrored after each check
     // device scratch for the checks
     DBuf<unsigned long long> scratch_u64;

@@ -40,22 +40,42 @@ __global__ void k_sort_keys(const double *lower, const int32_t *iperm, const int
 }
 
 // count_v = #{i < npos : sorted_desc[i] > upper[v]} where sorted_desc holds
-// ~keys; nodes with lower == 0 never exceed an upper bound (upper >= 0)
-__global__ void k_sep_pairs(const uint64_t *skeys, int64_t npos, const double *upper,
-                            int64_t n, unsigned long long *total) {
-    typedef cub::BlockReduce<unsigned long long, 256> Red;
+// ~keys.  Every 1024th key is staged in shared memory, so the search touches
+// global memory only inside one 1024-key window.  Nodes with upper == 0
+// (no out-arcs) count every positive lower bound without a search.
+constexpr int SEP_SAMPLES = 12288;  // 96 KB of shared memory
+
+__global__ void __launch_bounds__(512) k_sep_pairs(const uint64_t *skeys, int64_t npos,
+                                                   const double *upper, int64_t n,
+                                                   int64_t SEP_STRIDE,
+                                                   unsigned long long *total) {
+    extern __shared__ double samp[];
+    const int64_t ns = (npos + SEP_STRIDE - 1) / SEP_STRIDE;
+    for (int64_t t = threadIdx.x; t < ns; t += blockDim.x)
+        samp[t] = __longlong_as_double((long long)~skeys[t * SEP_STRIDE]);
+    __syncthreads();
+    typedef cub::BlockReduce<unsigned long long, 512> Red;
     __shared__ typename Red::TempStorage tmp;
     unsigned long long acc = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         const double u = upper[v];
-        int64_t lo = 0, hi = npos;  // first i with value <= u
+        if (u == 0.0) { acc += (unsigned long long)npos; continue; }
+        // sample level: first sample index t with samp[t] <= u
+        int64_t lo = 0, hi = ns;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
-            const double val = __longlong_as_double((long long)~skeys[mid]);
-            if (val > u) lo = mid + 1; else hi = mid;
+            if (samp[mid] > u) lo = mid + 1; else hi = mid;
         }
-        acc += (unsigned long long)lo;
+        // answer lies in ((lo-1)*S, lo*S]
+        int64_t a = lo == 0 ? 0 : (lo - 1) * SEP_STRIDE + 1;
+        int64_t b = lo * SEP_STRIDE < npos ? lo * SEP_STRIDE : npos;
+        while (a < b) {
+            const int64_t mid = (a + b) >> 1;
+            const double val = __longlong_as_double((long long)~skeys[mid]);
+            if (val > u) a = mid + 1; else b = mid;
+        }
+        acc += (unsigned long long)a;
     }
     acc = Red(tmp).Sum(acc);
     if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
@@ -105,8 +125,15 @@ void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, do
         KB_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp.p, tb, kin.p, kout.p, ids.p, order.p,
                                                 (int)npos, 0, 64, st)); note_launch();
     }
-    if (n >= 2)
-        k_sep_pairs<<<4 * g.sm_count, 256, 0, st>>>(kout.p, npos, s.upper.p, n, u + 2); note_launch();
+    if (n >= 2) {
+        int64_t stride = 1024;
+        while ((npos + stride - 1) / stride > SEP_SAMPLES) stride *= 2;
+        const size_t smem = SEP_SAMPLES * sizeof(double);
+        KB_CUDA(cudaFuncSetAttribute(k_sep_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        k_sep_pairs<<<2 * g.sm_count, 512, smem, st>>>(kout.p, npos, s.upper.p, n, stride, u + 2);
+        note_launch();
+    }
     if (h_order) {
         DBuf<int64_t> wide;
         wide.alloc(n);

@@ -96,7 +96,9 @@ def test_C1_default_split_within_tolerance(golden_index, c1):
     g0, g = c1
     st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
     info = st.device_graph.info()
-    assert info.heavy_rows == 1 and info.max_out_degree == 9648
+    deg = np.diff(g0.indptr)
+    assert info.heavy_rows == int((deg > info.split_threshold).sum()) >= 1
+    assert info.max_out_degree == 9648
     res = P.run(st, g)
     ost = O.OracleState(g0, O.Crit("topk", 1e-6, k=100))
     ores = O.run(ost, g0)
