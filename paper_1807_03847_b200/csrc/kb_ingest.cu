@@ -2,6 +2,7 @@
 // rows (replaces Graph.out_csr, graph.py:177-197).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <numeric>
@@ -103,6 +104,18 @@ __global__ void k_fill(const int64_t *indptr, const int32_t *indices,
                                : ((int64_t)(j >> 2) * 128 + lane * 4 + (j & 3));
         base[pos] = c;
     }
+}
+
+__global__ void k_arc_flags(const int64_t *indptr, int64_t n, unsigned char *fl, int32_t *iota) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    fl[v] = indptr[v + 1] > indptr[v];
+    iota[v] = (int32_t)v;
+}
+
+__global__ void k_flip(unsigned char *fl, int64_t n) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < n) fl[v] = !fl[v];
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -238,6 +251,31 @@ void build_graph_device(Graph &g) {
     KB_CUDA(cudaStreamSynchronize(st));
     tmp.release();
     sz.release();
+
+    // ---- original ids with / without out-arcs, ascending (for K3)
+    {
+        DBuf<unsigned char> fl;
+        DBuf<int32_t> iota;
+        DBuf<int64_t> cntp;
+        fl.alloc(n); iota.alloc(n); cntp.alloc(2);
+        k_arc_flags<<<blocks_for(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(g.indptr.p, n, fl.p, iota.p);
+        note_launch();
+        g.orig_pos.alloc(std::max<int64_t>(1, g.nv));
+        g.orig_zero.alloc(std::max<int64_t>(1, n - g.nv));
+        size_t tb = 0;
+        DBuf<unsigned char> t2;
+        // stable selection of both sides (DevicePartition would reverse the
+        // rejected side)
+        KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fl.p, g.orig_pos.p, cntp.p,
+                                           (int)n, st));
+        t2.alloc(tb);
+        KB_CUDA(cub::DeviceSelect::Flagged(t2.p, tb, iota.p, fl.p, g.orig_pos.p, cntp.p, (int)n,
+                                           st));
+        k_flip<<<blocks_for(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(fl.p, n);
+        KB_CUDA(cub::DeviceSelect::Flagged(t2.p, tb, iota.p, fl.p, g.orig_zero.p, cntp.p + 1,
+                                           (int)n, st));
+        note_launch(3);
+    }
 
     // ---- fill the column slots (relabelled, original per-row order)
     S.cols.alloc(S.elems + 4);

@@ -109,6 +109,8 @@ struct Graph {
     Sell sell;
     // heavy-row combine: segments of heavy row h are seg_list[seg_ptr[h] ..
     // seg_ptr[h+1]) in order (indices into the segment-sum buffer)
+    // original ids of the rows with / without out-arcs, ascending
+    DBuf<int32_t> orig_pos, orig_zero;
     DBuf<int32_t> seg_ptr;
     DBuf<int32_t> seg_list;
     cudaStream_t stream = nullptr;
@@ -133,6 +135,7 @@ struct State {
     int cur = 0;
     bool act_dense = true;  // active == arange(n) (never materialised)
     int64_t tail_zero_from = 0;  // new ids >= this have lower == upper == 0
+    bool zero_tail_exact = true; // and exactly those (no dynamic change yet)
     DBuf<int32_t> cand;          // selection candidates (capacity n)
     DBuf<uint64_t> stK;          // staged keys/uppers/ids of the active set
     DBuf<double> stU;

@@ -33,49 +33,48 @@ __global__ void k_pos_flags(const double *lower, const int32_t *iperm, int64_t n
 }
 
 __global__ void k_sort_keys(const double *lower, const int32_t *iperm, const int32_t *ids,
-                            int64_t npos, uint64_t *keys) {
+                            int64_t npos, uint64_t *keys, int32_t *nids) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= npos) return;
-    keys[i] = ~(uint64_t)__double_as_longlong(lower[iperm[ids[i]]]);
+    const int32_t v = iperm[ids[i]];
+    keys[i] = ~(uint64_t)__double_as_longlong(lower[v]);
+    nids[i] = v;
 }
 
-// count_v = #{i < npos : sorted_desc[i] > upper[v]} where sorted_desc holds
-// ~keys.  Every 1024th key is staged in shared memory, so the search touches
-// global memory only inside one 1024-key window.  Nodes with upper == 0
-// (no out-arcs) count every positive lower bound without a search.
-constexpr int SEP_SAMPLES = 12288;  // 96 KB of shared memory
+__global__ void k_new_to_orig(const int32_t *perm, const int32_t *nids, int64_t n, int32_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = perm[nids[i]];
+}
 
-__global__ void __launch_bounds__(512) k_sep_pairs(const uint64_t *skeys, int64_t npos,
-                                                   const double *upper, int64_t n,
-                                                   int64_t SEP_STRIDE,
-                                                   unsigned long long *total) {
-    extern __shared__ double samp[];
-    const int64_t ns = (npos + SEP_STRIDE - 1) / SEP_STRIDE;
-    for (int64_t t = threadIdx.x; t < ns; t += blockDim.x)
-        samp[t] = __longlong_as_double((long long)~skeys[t * SEP_STRIDE]);
-    __syncthreads();
-    typedef cub::BlockReduce<unsigned long long, 512> Red;
+// Separated pairs counted by rank: the node at rank t (descending lower) has
+// upper >= lower, so every w with lower[w] > upper[v] ranks before it and the
+// count is the first rank j <= t with sorted[j] <= upper[v].  Bounds are
+// tight, so j is found by galloping down from t inside a small window that
+// neighbouring threads share (coalesced, cache resident).
+__global__ void k_sep_pairs_rank(const uint64_t *skeys, const int32_t *snids, int64_t npos,
+                                 const double *upper, unsigned long long *total) {
+    typedef cub::BlockReduce<unsigned long long, 256> Red;
     __shared__ typename Red::TempStorage tmp;
     unsigned long long acc = 0;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        const double u = upper[v];
-        if (u == 0.0) { acc += (unsigned long long)npos; continue; }
-        // sample level: first sample index t with samp[t] <= u
-        int64_t lo = 0, hi = ns;
-        while (lo < hi) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < npos) {
+        const double u = upper[snids[t]];
+        auto val = [&](int64_t j) { return __longlong_as_double((long long)~skeys[j]); };
+        // invariant: val(hi) <= u ; find smallest j in [0, hi] with val(j) <= u
+        int64_t hi = t, step = 1, lo = t;
+        while (true) {
+            lo = hi - step;
+            if (lo < 0) { lo = -1; break; }
+            if (val(lo) > u) break;
+            hi = lo;
+            step <<= 1;
+        }
+        // val(lo) > u (or lo == -1), val(hi) <= u
+        while (hi - lo > 1) {
             const int64_t mid = (lo + hi) >> 1;
-            if (samp[mid] > u) lo = mid + 1; else hi = mid;
+            if (val(mid) > u) lo = mid; else hi = mid;
         }
-        // answer lies in ((lo-1)*S, lo*S]
-        int64_t a = lo == 0 ? 0 : (lo - 1) * SEP_STRIDE + 1;
-        int64_t b = lo * SEP_STRIDE < npos ? lo * SEP_STRIDE : npos;
-        while (a < b) {
-            const int64_t mid = (a + b) >> 1;
-            const double val = __longlong_as_double((long long)~skeys[mid]);
-            if (val > u) a = mid + 1; else b = mid;
-        }
-        acc += (unsigned long long)a;
+        acc = (unsigned long long)hi;
     }
     acc = Red(tmp).Sum(acc);
     if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
@@ -88,50 +87,87 @@ __global__ void k_widen(const int32_t *src, int64_t n, int64_t *dst) {
 
 }  // namespace
 
+// positive-bound nodes by ascending original id, and the rest: from the
+// flags of the current lower bounds (generic) -- or, when the state knows
+// that exactly the rows with out-arcs are positive (static runs), from the
+// lists precomputed at ingest (Graph::orig_pos / orig_zero)
+static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_t *zero_out,
+                           int64_t &npos) {
+    Graph &g = *s.g;
+    const int64_t n = g.n;
+    if (s.zero_tail_exact && g.orig_pos.p) {
+        npos = g.nv;
+        KB_CUDA(cudaMemcpyAsync(ids.p, g.orig_pos.p, npos * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, st));
+        if (n > npos)
+            KB_CUDA(cudaMemcpyAsync(zero_out, g.orig_zero.p, (n - npos) * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    DBuf<unsigned char> fpos, fzero;
+    DBuf<int32_t> iota;
+    fpos.alloc(n); fzero.alloc(n); iota.alloc(n);
+    unsigned long long *u = s.scratch_u64.p + 16;
+    KB_CUDA(cudaMemsetAsync(u, 0, 2 * sizeof(unsigned long long), st));
+    k_pos_flags<<<nblk(n, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, n, fpos.p, fzero.p, iota.p);
+    note_launch();
+    size_t tb = 0;
+    KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fpos.p, ids.p, u, (int)n, st));
+    ensure_cub_tmp(s, tb);
+    KB_CUDA(cub::DeviceSelect::Flagged(s.cub_tmp.p, tb, iota.p, fpos.p, ids.p, u, (int)n, st));
+    note_launch();
+    unsigned long long hcnt = 0;
+    KB_CUDA(cudaMemcpyAsync(&hcnt, u, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    npos = (int64_t)hcnt;
+    tb = 0;
+    KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fzero.p, zero_out, u + 1, (int)n, st));
+    ensure_cub_tmp(s, tb);
+    KB_CUDA(cub::DeviceSelect::Flagged(s.cub_tmp.p, tb, iota.p, fzero.p, zero_out, u + 1, (int)n,
+                                       st));
+    note_launch();
+}
+
 void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, double *h_upper,
                 int64_t *h_pairs) {
     Graph &g = *s.g;
     const int64_t n = g.n;
     KB_REQUIRE(s.r >= 1, KB_ESTATE, "separated_fraction needs at least one iteration");
-    DBuf<unsigned char> fpos, fzero;
-    DBuf<int32_t> iota, ids, order;
+    DBuf<int32_t> ids, order, nids, snids;
     DBuf<uint64_t> kin, kout;
-    fpos.alloc(n); fzero.alloc(n); iota.alloc(n); ids.alloc(n); order.alloc(n);
-    unsigned long long *u = s.scratch_u64.p;  // [0]=npos, [1]=nzero, [2]=pairs
-    KB_CUDA(cudaMemsetAsync(u, 0, 3 * sizeof(unsigned long long), st));
-    k_pos_flags<<<nblk(n, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, n, fpos.p, fzero.p, iota.p); note_launch();
-    size_t tb = 0;
-    KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fpos.p, ids.p, u, (int)n, st));
-    ensure_cub_tmp(s, tb);
-    KB_CUDA(cub::DeviceSelect::Flagged(s.cub_tmp.p, tb, iota.p, fpos.p, ids.p, u, (int)n, st)); note_launch();
-    unsigned long long hcnt[1];
-    KB_CUDA(cudaMemcpyAsync(hcnt, u, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    const int64_t npos = (int64_t)hcnt[0];
-    // zero-bound nodes go last, in id order
-    tb = 0;
-    KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fzero.p, order.p + npos, u + 1,
-                                       (int)n, st));
-    ensure_cub_tmp(s, tb);
-    KB_CUDA(cub::DeviceSelect::Flagged(s.cub_tmp.p, tb, iota.p, fzero.p, order.p + npos, u + 1,
-                                       (int)n, st)); note_launch();
-    kin.alloc(npos); kout.alloc(npos);
+    ids.alloc(n); order.alloc(n);
+    int64_t npos = 0;
+    split_positive(s, st, ids, order.p, npos);  // zero part lands at order[0..)
+    // shift the zero part behind the positive one
+    DBuf<int32_t> zero_part;
+    if (n > npos) {
+        zero_part.alloc(n - npos);
+        KB_CUDA(cudaMemcpyAsync(zero_part.p, order.p, (n - npos) * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, st));
+    }
+    unsigned long long *u = s.scratch_u64.p;  // [2]=pairs
+    KB_CUDA(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), st));
+    kin.alloc(npos); kout.alloc(npos); nids.alloc(npos); snids.alloc(npos);
     if (npos) {
-        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, ids.p, npos, kin.p); note_launch();
-        tb = 0;
-        KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.p, kout.p, ids.p, order.p,
+        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, ids.p, npos, kin.p,
+                                                     nids.p);
+        note_launch();
+        size_t tb = 0;
+        KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.p, kout.p, nids.p, snids.p,
                                                 (int)npos, 0, 64, st));
         ensure_cub_tmp(s, tb);
-        KB_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp.p, tb, kin.p, kout.p, ids.p, order.p,
-                                                (int)npos, 0, 64, st)); note_launch();
+        KB_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp.p, tb, kin.p, kout.p, nids.p, snids.p,
+                                                (int)npos, 0, 64, st));
+        note_launch();
+        k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order.p);
+        note_launch();
     }
-    if (n >= 2) {
-        int64_t stride = 1024;
-        while ((npos + stride - 1) / stride > SEP_SAMPLES) stride *= 2;
-        const size_t smem = SEP_SAMPLES * sizeof(double);
-        KB_CUDA(cudaFuncSetAttribute(k_sep_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        k_sep_pairs<<<2 * g.sm_count, 512, smem, st>>>(kout.p, npos, s.upper.p, n, stride, u + 2);
+    if (n > npos)
+        KB_CUDA(cudaMemcpyAsync(order.p + npos, zero_part.p, (n - npos) * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, st));
+    if (n >= 2 && npos) {
+        k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(kout.p, snids.p, npos, s.upper.p,
+                                                          u + 2);
         note_launch();
     }
     if (h_order) {
@@ -158,6 +194,8 @@ void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, do
     unsigned long long pairs = 0;
     KB_CUDA(cudaMemcpyAsync(&pairs, u + 2, sizeof(pairs), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
+    // zero-bound nodes have upper == 0: every positive lower separates them
+    pairs += (unsigned long long)(n - npos) * (unsigned long long)npos;
     if (h_pairs) *h_pairs = (int64_t)pairs;
 }
 
