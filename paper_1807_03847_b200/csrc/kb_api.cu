@@ -256,11 +256,20 @@ int kb_graph_get_csr(kb_graph *h, int64_t *indptr, int32_t *indices) {
         KB_REQUIRE(h, KB_EPARAM, "NULL graph");
         Graph &g = h->g;
         use_device(g.device);
+        DBuf<int64_t> cip;
+        DBuf<int32_t> cix;
+        const int64_t *ip = g.indptr.p;
+        const int32_t *ix = g.indices.p;
+        if (g.slack) {  // compact the CSR-with-slack first
+            compact_csr(g, cip, cix);
+            ip = cip.p;
+            ix = cix.p;
+        }
         if (indptr)
-            KB_CUDA(cudaMemcpyAsync(indptr, g.indptr.p, (g.n + 1) * sizeof(int64_t),
+            KB_CUDA(cudaMemcpyAsync(indptr, ip, (g.n + 1) * sizeof(int64_t),
                                     cudaMemcpyDeviceToHost, g.stream));
         if (indices && g.nnz)
-            KB_CUDA(cudaMemcpyAsync(indices, g.indices.p, g.nnz * sizeof(int32_t),
+            KB_CUDA(cudaMemcpyAsync(indices, ix, g.nnz * sizeof(int32_t),
                                     cudaMemcpyDeviceToHost, g.stream));
         KB_CUDA(cudaStreamSynchronize(g.stream));
     });
@@ -349,7 +358,8 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.act[0].alloc(n);
         s.act[1].alloc(n);
         s.act_dense = true;  // :152 arange(n), materialised on first check
-        s.tail_zero_from = g.nv;
+        s.tail_zero_from = g.mutated ? n : g.nv;
+        s.zero_tail_exact = !g.mutated;
         s.cand.alloc(n);
         s.stK.alloc(n);
         s.stU.alloc(n);
@@ -539,9 +549,15 @@ int kb_get_active(kb_state *h, int64_t *out) {
 int kb_update_batch(kb_state *h, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                     int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats) {
     return guarded([&] {
-        (void)h; (void)ins; (void)n_ins; (void)dels; (void)n_dels; (void)theta;
-        (void)new_gamma; (void)stats;
-        throw Error{KB_ESTATE, "kb_update_batch: not built yet"};
+        KB_REQUIRE(h && stats, KB_EPARAM, "NULL argument");
+        KB_REQUIRE((n_ins == 0 || ins) && (n_dels == 0 || dels), KB_EPARAM, "NULL arc array");
+        State &s = h->s;
+        use_device(s.g->device);
+        for (int64_t i = 0; i < 2 * n_ins; i++)
+            KB_REQUIRE(ins[i] >= 0 && ins[i] < s.g->n, KB_ENODERANGE, "node id outside graph");
+        for (int64_t i = 0; i < 2 * n_dels; i++)
+            KB_REQUIRE(dels[i] >= 0 && dels[i] < s.g->n, KB_ENODERANGE, "node id outside graph");
+        update_batch(s, ins, n_ins, dels, n_dels, theta, new_gamma, stats);
     });
 }
 

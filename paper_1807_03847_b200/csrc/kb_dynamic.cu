@@ -1,0 +1,680 @@
+// K4: dynamic edge-batch update (dynamic.update_batch, dynamic.py:126-211).
+//
+// 1. The batch is applied to the device CSR-with-slack in place: every edited
+//    row is rebuilt by one warp as (old row - deletions) merged with the
+//    sorted insertions.  Rows whose capacity would overflow trigger one
+//    re-spread of the whole CSR with fresh slack.
+// 2. Levels 1..r are repaired on the post-batch graph.  The rows recomputed
+//    at level i are R_i = seeds U in-neighbours of the rows whose level i-1
+//    changed bit-wise -- the reference's affected-set growth
+//    (dynamic.py:94-103) -- so UpdateStats follow it.  Each row is recomputed
+//    by pull with exactly K1's summation order (sequential per row, or per
+//    split-sized segment combined in order), so repaired levels are
+//    bit-identical to a fresh static run.  Past theta*n affected nodes the
+//    remaining levels are recomputed whole with K1 (dynamic.py:78-88).
+// 3. katz is re-summed from the stored levels in order, the bounds are
+//    refreshed under the new tail factor (dynamic.py:181-187), nodes that may
+//    contend again are reactivated (:190-197), and the run resumes (:203-210).
+#include <cub/block/block_reduce.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kb_internal.cuh"
+
+namespace kb {
+
+namespace {
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+template <typename F>
+void cub_run(F &&f) {
+    size_t tb = 0;
+    KB_CUDA(f(nullptr, tb));
+    DBuf<unsigned char> tmp;
+    tmp.alloc(tb);
+    KB_CUDA(f(tmp.p, tb));
+    note_launch();
+}
+
+// ---------------------------------------------------------------- slack CSR
+
+__global__ void k_capacity(const int32_t *rlen, const int32_t *extra, int64_t n, int64_t *cap) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v > n) return;
+    if (v == n) { cap[v] = 0; return; }
+    const int64_t need = (int64_t)rlen[v] + (extra ? extra[v] : 0);
+    cap[v] = need + max((int64_t)2, need / 8);
+}
+
+__global__ void k_copy_rows(const int64_t *old_ip, const int32_t *old_ix, const int32_t *rlen,
+                            int64_t n, const int64_t *new_ip, int32_t *new_ix) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int64_t a = old_ip[warp], b = new_ip[warp];
+    for (int64_t j = lane; j < rlen[warp]; j += 32) new_ix[b + j] = old_ix[a + j];
+}
+
+__global__ void k_compact_len(const int32_t *rlen, int64_t n, int64_t *len) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v > n) return;
+    len[v] = v < n ? rlen[v] : 0;
+}
+
+// Rebuild the slack layout: capacity = len (+extra) + max(2, len/8).
+void respread(Graph &g, const int32_t *extra) {
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n;
+    DBuf<int64_t> cap, nip;
+    cap.alloc(n + 1);
+    nip.alloc(n + 1);
+    k_capacity<<<nblk(n + 1, 256), 256, 0, st>>>(g.rlen.p, extra, n, cap.p);
+    note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, cap.p, nip.p, (int)(n + 1), st);
+    });
+    int64_t total = 0;
+    KB_CUDA(cudaMemcpyAsync(&total, nip.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    DBuf<int32_t> nix;
+    nix.alloc(std::max<int64_t>(1, total));
+    k_copy_rows<<<nblk(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.indices.p, g.rlen.p, n, nip.p,
+                                                   nix.p);
+    note_launch();
+    g.indptr = std::move(nip);
+    g.indices = std::move(nix);
+    g.slack = true;
+}
+
+// ---------------------------------------------------------------- batch edits
+
+// Edited row e: original id rows[e], deletions del[dptr[e]..dptr[e+1]),
+// insertions ins[iptr[e]..iptr[e+1]) (both ascending).  One warp per row
+// writes the merged row to tmp[toff[e] ..) and then back in place.
+__device__ __forceinline__ int64_t lower_bound32(const int32_t *a, int64_t n, int32_t x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dptr,
+                              const int32_t *del, const int64_t *iptr, const int32_t *ins,
+                              const int64_t *toff, int32_t *tmp, const int64_t *indptr,
+                              int32_t *indices, int32_t *rlen) {
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= ne) return;
+    const int32_t v = rows[e];
+    const int32_t *row = indices + indptr[v];
+    const int64_t L = rlen[v];
+    const int32_t *D = del + dptr[e];
+    const int64_t nd = dptr[e + 1] - dptr[e];
+    const int32_t *I = ins + iptr[e];
+    const int64_t ni = iptr[e + 1] - iptr[e];
+    int32_t *out = tmp + toff[e];
+    for (int64_t j = lane; j < L; j += 32) {
+        const int32_t c = row[j];
+        const int64_t dl = lower_bound32(D, nd, c);
+        if (dl < nd && D[dl] == c) continue;  // deleted
+        out[j - dl + lower_bound32(I, ni, c)] = c;
+    }
+    for (int64_t q = lane; q < ni; q += 32) {
+        const int32_t t = I[q];
+        out[lower_bound32(row, L, t) - lower_bound32(D, nd, t) + q] = t;
+    }
+    __syncwarp();
+    const int64_t nl = L - nd + ni;
+    for (int64_t j = lane; j < nl; j += 32) indices[indptr[v] + j] = out[j];
+    __syncwarp();
+    if (lane == 0) rlen[v] = (int32_t)nl;
+}
+
+__global__ void k_gather_len(const int32_t *rlen, const int64_t *indptr, const int32_t *rows,
+                             int64_t ne, int64_t *len_cap) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const int32_t v = rows[e];
+    len_cap[2 * e] = rlen[v];
+    len_cap[2 * e + 1] = indptr[v + 1] - indptr[v];
+}
+
+// ---------------------------------------------------------------- transpose
+
+__global__ void k_arc_keys_t(const int64_t *indptr, const int32_t *indices, const int32_t *rlen,
+                             int64_t n, const int64_t *cidx, uint64_t *keys) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int64_t base = cidx[warp];
+    for (int64_t j = lane; j < rlen[warp]; j += 32)
+        keys[base + j] = ((uint64_t)(uint32_t)indices[indptr[warp] + j] << 32) | (uint32_t)warp;
+}
+
+__global__ void k_row_count_t(const uint64_t *keys, int64_t m, int64_t n, int64_t *ip) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v > n) return;
+    const uint64_t target = (uint64_t)v << 32;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    ip[v] = lo;
+}
+
+__global__ void k_low32(const uint64_t *keys, int64_t m, int32_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) out[i] = (int32_t)(keys[i] & 0xffffffffu);
+}
+
+// ---------------------------------------------------------------- frontier
+
+// add the rows of `list` to R (deduplicated with a per-level stamp)
+__global__ void k_mark_list(const int32_t *list, int64_t m, int32_t *stamp, int32_t level,
+                            int32_t *R, unsigned long long *rcount, unsigned char *touched) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int32_t v = list[i];
+    if (atomicExch(&stamp[v], level) != level) {
+        R[atomicAdd(rcount, 1ull)] = v;
+        touched[v] = 1;
+    }
+}
+
+// cumulative affected set: byte flags, count of first-time insertions
+__global__ void k_affect(const int32_t *list, int64_t m, unsigned int *aff_words,
+                         unsigned long long *affcount) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int32_t v = list[i];
+    const unsigned bit = 1u << (v & 31);
+    if (!(atomicOr(&aff_words[v >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
+}
+
+// in-neighbours of the changed rows (new ids) -> R (stamped) and affected
+__global__ void k_expand(const int32_t *changed, int64_t nc, const int64_t *in_ip,
+                         const int32_t *in_len, const int32_t *in_ix, const int32_t *perm,
+                         const int32_t *iperm, int32_t *stamp, int32_t level, int32_t *R,
+                         unsigned long long *rcount, unsigned int *aff_words,
+                         unsigned long long *affcount, unsigned char *touched) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nc) return;
+    const int32_t o = perm[changed[warp]];
+    const int64_t a = in_ip[o];
+    const int64_t L = in_len ? in_len[o] : in_ip[o + 1] - a;
+    for (int64_t j = lane; j < L; j += 32) {
+        const int32_t u = iperm[in_ix[a + j]];
+        const unsigned bit = 1u << (u & 31);
+        if (!(atomicOr(&aff_words[u >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
+        if (atomicExch(&stamp[u], level) != level) {
+            R[atomicAdd(rcount, 1ull)] = u;
+            touched[u] = 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- recompute
+
+// w_level[v] = alpha * sum_{c in row(v)} x[iperm[c]] with K1's order: one
+// sequential chain per row of length <= split, else split-sized segments
+// summed sequentially and combined in segment order.  One warp per row.
+__global__ void k_recompute(const int32_t *R, int64_t nr, const int32_t *perm,
+                            const int32_t *iperm, const int64_t *indptr, const int32_t *rlen,
+                            const int32_t *indices, const double *x, double *w, double alpha,
+                            int64_t split, int32_t *changed, unsigned long long *nchanged) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nr) return;
+    const int32_t v = R[warp];
+    const int32_t o = perm[v];
+    const int32_t *row = indices + indptr[o];
+    const int64_t L = rlen[o];
+    double s = 0.0;
+    if (L <= split) {
+        // lanes gather 32 consecutive slots; lane 0 folds them in order
+        for (int64_t base = 0; base < L; base += 32) {
+            const int64_t j = base + lane;
+            const double val = j < L ? x[iperm[row[j]]] : 0.0;
+            const int cnt = (int)min((int64_t)32, L - base);
+            for (int q = 0; q < cnt; q++) {
+                const double t = __shfl_sync(0xffffffffu, val, q);
+                if (lane == 0) s = __dadd_rn(s, t);
+            }
+        }
+    } else {
+        const int64_t nseg = (L + split - 1) / split;
+        for (int64_t g0 = 0; g0 < nseg; g0 += 32) {
+            const int64_t sg = g0 + lane;
+            double ss = 0.0;
+            if (sg < nseg) {
+                const int64_t a = sg * split, b = min(L, a + split);
+                for (int64_t j = a; j < b; j++) ss = __dadd_rn(ss, x[iperm[row[j]]]);
+            }
+            const int cnt = (int)min((int64_t)32, nseg - g0);
+            for (int q = 0; q < cnt; q++) {
+                const double t = __shfl_sync(0xffffffffu, ss, q);
+                if (lane == 0) s = __dadd_rn(s, t);
+            }
+        }
+    }
+    if (lane == 0) {
+        const double nw = __dmul_rn(alpha, s);
+        const double old = w[v];
+        if (__double_as_longlong(nw) != __double_as_longlong(old)) {
+            changed[atomicAdd(nchanged, 1ull)] = v;
+            w[v] = nw;
+        }
+    }
+}
+
+// katz[v] = ((0 + w_1) + w_2) + ... + w_r, the static accumulation order
+__global__ void k_katz_rows(const int32_t *rows, int64_t m, const double *const *levels, int r,
+                            double *katz) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t v = rows ? rows[i] : i;
+    double k = 0.0;
+    for (int l = 1; l <= r; l++) k = __dadd_rn(k, levels[l][v]);
+    katz[v] = k;
+}
+
+__global__ void k_bounds_rows(const int32_t *rows, int64_t m, const double *katz,
+                              const double *wr, double alpha, double gamma, int undirected,
+                              double *lower, double *upper) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t v = rows ? rows[i] : i;
+    const double k = katz[v];
+    const double t = __dmul_rn(alpha, wr[v]);                 // dynamic.py:182
+    lower[v] = undirected ? __dadd_rn(k, t) : k;             // :183-186
+    upper[v] = __dadd_rn(k, __dmul_rn(t, gamma));            // :187
+}
+
+__global__ void k_flags_from_list(const int32_t *list, int64_t m, unsigned char *flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) flag[list[i]] = 1;
+}
+
+__global__ void k_min_lower(const int32_t *act, int64_t m, const double *lower,
+                            unsigned long long *out) {
+    typedef cub::BlockReduce<unsigned long long, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    unsigned long long best = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        // lower >= +0: the IEEE bits order like the values
+        best = min(best, (unsigned long long)__double_as_longlong(lower[act[i]]));
+    }
+    best = Red(tmp).Reduce(best, cub::Min());
+    if (threadIdx.x == 0) atomicMin(out, best);
+}
+
+// reactivation flags by original id: not active and fl(upper) >= floor
+__global__ void k_reactivate_flags(const int32_t *iperm, int64_t n, const unsigned char *inact,
+                                   const double *upper, const unsigned long long *minbits,
+                                   double eps, unsigned char *flag) {
+    int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    const int32_t v = iperm[o];
+    const double floor = __dsub_rn(__longlong_as_double((long long)*minbits), eps);
+    flag[o] = !inact[v] && upper[v] >= floor;
+}
+
+}  // namespace
+
+void compact_csr(Graph &g, DBuf<int64_t> &ip, DBuf<int32_t> &ix) {
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n;
+    DBuf<int64_t> len;
+    len.alloc(n + 1);
+    ip.alloc(n + 1);
+    k_compact_len<<<nblk(n + 1, 256), 256, 0, st>>>(g.rlen.p, n, len.p);
+    note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, len.p, ip.p, (int)(n + 1), st);
+    });
+    ix.alloc(std::max<int64_t>(1, g.nnz));
+    k_copy_rows<<<nblk(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.indices.p, g.rlen.p, n, ip.p,
+                                                   ix.p);
+    note_launch();
+    KB_CUDA(cudaStreamSynchronize(st));
+}
+
+// in-neighbour CSR of the current arc set (original ids; rows ascending)
+static void build_transpose(Graph &g, DBuf<int64_t> &tip, DBuf<int32_t> &tix) {
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n, m = g.nnz;
+    DBuf<int64_t> cip;
+    DBuf<int32_t> cix;
+    compact_csr(g, cip, cix);
+    DBuf<uint64_t> keys, skeys;
+    keys.alloc(std::max<int64_t>(1, m));
+    skeys.alloc(std::max<int64_t>(1, m));
+    k_arc_keys_t<<<nblk(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.indices.p, g.rlen.p, n, cip.p,
+                                                    keys.p);
+    note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, keys.p, skeys.p, (int)m, 0, 64, st);
+    });
+    tip.alloc(n + 1);
+    tix.alloc(std::max<int64_t>(1, m));
+    k_row_count_t<<<nblk(n + 1, 256), 256, 0, st>>>(skeys.p, m, n, tip.p);
+    k_low32<<<nblk(m, 256), 256, 0, st>>>(skeys.p, m, tix.p);
+    note_launch(2);
+    KB_CUDA(cudaStreamSynchronize(st));
+}
+
+void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                          int64_t n_dels) {
+    cudaStream_t st = g.stream;
+    // group the edits by source row (host; batches are small)
+    struct Edit { int32_t src, dst; int kind; };  // kind 0 = delete, 1 = insert
+    std::vector<Edit> ed;
+    ed.reserve(n_ins + n_dels);
+    for (int64_t i = 0; i < n_dels; i++) ed.push_back({(int32_t)dels[2 * i], (int32_t)dels[2 * i + 1], 0});
+    for (int64_t i = 0; i < n_ins; i++) ed.push_back({(int32_t)ins[2 * i], (int32_t)ins[2 * i + 1], 1});
+    if (ed.empty()) return;
+    std::sort(ed.begin(), ed.end(), [](const Edit &a, const Edit &b) {
+        return a.src != b.src ? a.src < b.src : (a.kind != b.kind ? a.kind < b.kind : a.dst < b.dst);
+    });
+    std::vector<int32_t> rows, dl, il;
+    std::vector<int64_t> dptr{0}, iptr{0};
+    for (size_t i = 0; i < ed.size();) {
+        size_t j = i;
+        rows.push_back(ed[i].src);
+        while (j < ed.size() && ed[j].src == ed[i].src) {
+            (ed[j].kind ? il : dl).push_back(ed[j].dst);
+            j++;
+        }
+        dptr.push_back((int64_t)dl.size());
+        iptr.push_back((int64_t)il.size());
+        i = j;
+    }
+    const int64_t ne = (int64_t)rows.size();
+    DBuf<int32_t> drows, ddel, dins;
+    DBuf<int64_t> ddptr, diptr, lc;
+    drows.alloc(ne); ddel.alloc(std::max<size_t>(1, dl.size()));
+    dins.alloc(std::max<size_t>(1, il.size())); ddptr.alloc(ne + 1); diptr.alloc(ne + 1);
+    lc.alloc(2 * ne);
+    KB_CUDA(cudaMemcpyAsync(drows.p, rows.data(), ne * 4, cudaMemcpyHostToDevice, st));
+    if (!dl.empty()) KB_CUDA(cudaMemcpyAsync(ddel.p, dl.data(), dl.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!il.empty()) KB_CUDA(cudaMemcpyAsync(dins.p, il.data(), il.size() * 4, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemcpyAsync(ddptr.p, dptr.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemcpyAsync(diptr.p, iptr.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
+    // capacity check (slack CSR); re-spread once if any edited row overflows
+    if (!g.slack) respread(g, nullptr);
+    k_gather_len<<<nblk(ne, 256), 256, 0, st>>>(g.rlen.p, g.indptr.p, drows.p, ne, lc.p);
+    note_launch();
+    std::vector<int64_t> hlc(2 * ne);
+    KB_CUDA(cudaMemcpyAsync(hlc.data(), lc.p, 2 * ne * 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    bool overflow = false;
+    std::vector<int64_t> toff(ne + 1, 0);
+    for (int64_t e = 0; e < ne; e++) {
+        const int64_t nl = hlc[2 * e] - (dptr[e + 1] - dptr[e]) + (iptr[e + 1] - iptr[e]);
+        if (nl > hlc[2 * e + 1]) overflow = true;
+        toff[e + 1] = toff[e] + std::max<int64_t>(nl, hlc[2 * e]);
+    }
+    if (overflow) {
+        std::vector<int32_t> extra(g.n, 0);
+        for (int64_t e = 0; e < ne; e++) extra[rows[e]] = (int32_t)(iptr[e + 1] - iptr[e]);
+        DBuf<int32_t> dex;
+        dex.alloc(g.n);
+        KB_CUDA(cudaMemcpyAsync(dex.p, extra.data(), g.n * 4, cudaMemcpyHostToDevice, st));
+        respread(g, dex.p);
+        KB_CUDA(cudaStreamSynchronize(st));
+    }
+    DBuf<int64_t> dtoff;
+    DBuf<int32_t> tmp;
+    dtoff.alloc(ne + 1);
+    tmp.alloc(std::max<int64_t>(1, toff[ne]));
+    KB_CUDA(cudaMemcpyAsync(dtoff.p, toff.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
+    k_apply_edits<<<nblk(ne * 32, 256), 256, 0, st>>>(drows.p, ne, ddptr.p, ddel.p, diptr.p,
+                                                       dins.p, dtoff.p, tmp.p, g.indptr.p,
+                                                       g.indices.p, g.rlen.p);
+    note_launch();
+    KB_CUDA(cudaGetLastError());
+    KB_CUDA(cudaStreamSynchronize(st));
+    g.nnz += n_ins - n_dels;
+    g.sell_dirty = true;
+    g.mutated = true;
+    g.version += 1;
+}
+
+void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                  int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats) {
+    Graph &g = *s.g;
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n;
+    KB_REQUIRE(s.keep_all, KB_ESTATE, "dynamic updates need keep_all_levels=True");
+    KB_REQUIRE(s.r >= 1, KB_ESTATE, "run the static engine before applying updates");
+    KB_REQUIRE(g.version == s.graph_version, KB_ESTATE,
+               "state does not belong to this graph revision");
+    KB_REQUIRE(theta >= 0.0 && theta <= 1.0, KB_EPARAM, "theta must be in [0, 1]");
+    kb_update_stats st_out{};
+    st_out.batch_size = n_ins + n_dels;
+    st_out.aborted_level = -1;
+
+    // seeds (sources) and targets, as new ids
+    std::vector<int32_t> seeds_o, targets_o;
+    for (int64_t i = 0; i < n_ins; i++) { seeds_o.push_back((int32_t)ins[2 * i]); targets_o.push_back((int32_t)ins[2 * i + 1]); }
+    for (int64_t i = 0; i < n_dels; i++) { seeds_o.push_back((int32_t)dels[2 * i]); targets_o.push_back((int32_t)dels[2 * i + 1]); }
+    std::sort(seeds_o.begin(), seeds_o.end());
+    seeds_o.erase(std::unique(seeds_o.begin(), seeds_o.end()), seeds_o.end());
+    std::sort(targets_o.begin(), targets_o.end());
+    targets_o.erase(std::unique(targets_o.begin(), targets_o.end()), targets_o.end());
+    st_out.seeds = (int64_t)seeds_o.size();
+    std::vector<int32_t> hiperm(n);
+    KB_CUDA(cudaMemcpyAsync(hiperm.data(), g.iperm.p, n * 4, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> seeds(seeds_o.size()), targets(targets_o.size());
+    for (size_t i = 0; i < seeds_o.size(); i++) seeds[i] = hiperm[seeds_o[i]];
+    for (size_t i = 0; i < targets_o.size(); i++) targets[i] = hiperm[targets_o[i]];
+
+    // 1. the post-batch arc set on the device
+    const bool was_sym = g.symmetric == 1;
+    apply_batch_to_graph(g, ins, n_ins, dels, n_dels);
+    if (!(was_sym && s.undirected)) g.symmetric = -1;
+    // in-neighbours: the CSR itself when undirected (symmetric), else a transpose
+    DBuf<int64_t> tip;
+    DBuf<int32_t> tix;
+    const int64_t *in_ip = g.indptr.p;
+    const int32_t *in_len = g.rlen.p;
+    const int32_t *in_ix = g.indices.p;
+    if (!s.undirected) {
+        build_transpose(g, tip, tix);
+        in_ip = tip.p;
+        in_len = nullptr;
+        in_ix = tix.p;
+    }
+
+    // 2. level repair
+    DBuf<int32_t> stamp, R, C, dseeds;
+    DBuf<unsigned int> aff;
+    DBuf<unsigned char> touched;
+    DBuf<unsigned long long> cnt;  // [0]=|R|, [1]=|changed|, [2]=|affected|
+    stamp.alloc(n); R.alloc(n); C.alloc(n); aff.alloc((n + 31) / 32 + 1); touched.alloc(n);
+    cnt.alloc(4);
+    dseeds.alloc(std::max<size_t>(1, seeds.size()));
+    KB_CUDA(cudaMemsetAsync(stamp.p, 0xff, n * 4, st));
+    KB_CUDA(cudaMemsetAsync(aff.p, 0, ((n + 31) / 32 + 1) * 4, st));
+    KB_CUDA(cudaMemsetAsync(touched.p, 0, n, st));
+    KB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * 8, st));
+    if (!seeds.empty())
+        KB_CUDA(cudaMemcpyAsync(dseeds.p, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice, st));
+    const int64_t ns = (int64_t)seeds.size();
+    if (ns) {
+        k_affect<<<nblk(ns, 256), 256, 0, st>>>(dseeds.p, ns, aff.p, cnt.p + 2);
+        note_launch();
+    }
+    int64_t affected = ns;
+    bool aborted = false;
+    int64_t nchanged = 0;
+    for (int64_t level = 1; level <= s.r; level++) {
+        double *w_prev = s.levels[level - 1 - s.level_base].p;
+        double *w_cur = s.levels[level - s.level_base].p;
+        if (aborted || (double)affected > theta * (double)n) {  // dynamic.py:58-60, :78
+            if (!aborted) {
+                aborted = true;
+                st_out.aborted_level = level;
+            }
+            run_spmv(s, st, w_prev, w_cur, true);
+            KB_CUDA(cudaStreamSynchronize(st));
+            continue;
+        }
+        if (st_out.n_level_sizes < 64) st_out.level_sizes[st_out.n_level_sizes++] = affected;
+        // R_level = seeds U in-neighbours(changed at level-1)
+        KB_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * 8, st));
+        if (ns) {
+            k_mark_list<<<nblk(ns, 256), 256, 0, st>>>(dseeds.p, ns, stamp.p, (int32_t)level,
+                                                       R.p, cnt.p, touched.p);
+            note_launch();
+        }
+        if (nchanged) {
+            k_expand<<<nblk(nchanged * 32, 256), 256, 0, st>>>(
+                C.p, nchanged, in_ip, in_len, in_ix, g.perm.p, g.iperm.p, stamp.p, (int32_t)level,
+                R.p, cnt.p, aff.p, cnt.p + 2, touched.p);
+            note_launch();
+        }
+        unsigned long long hc[3];
+        KB_CUDA(cudaMemcpyAsync(hc, cnt.p, 3 * 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        const int64_t nr = (int64_t)hc[0];
+        affected = (int64_t)hc[2];
+        // recompute R at this level; the changed list feeds the next level
+        KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
+        if (nr) {
+            k_recompute<<<nblk(nr * 32, 256), 256, 0, st>>>(
+                R.p, nr, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p, w_prev, w_cur,
+                s.alpha, g.split, C.p, cnt.p + 1);
+            note_launch();
+        }
+        unsigned long long hchg = 0;
+        KB_CUDA(cudaMemcpyAsync(&hchg, cnt.p + 1, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        nchanged = (int64_t)hchg;
+    }
+    // visited = |affected U targets| (dynamic.py:176)
+    {
+        DBuf<int32_t> dt;
+        dt.alloc(std::max<size_t>(1, targets.size()));
+        if (!targets.empty()) {
+            KB_CUDA(cudaMemcpyAsync(dt.p, targets.data(), targets.size() * 4,
+                                    cudaMemcpyHostToDevice, st));
+            k_affect<<<nblk((int64_t)targets.size(), 256), 256, 0, st>>>(
+                dt.p, (int64_t)targets.size(), aff.p, cnt.p + 2);
+            note_launch();
+        }
+        unsigned long long ha = 0;
+        KB_CUDA(cudaMemcpyAsync(&ha, cnt.p + 2, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        st_out.visited = (int64_t)ha;
+    }
+
+    // 3. katz and bounds (dynamic.py:181-187)
+    std::vector<const double *> hl(s.r + 1);
+    for (int64_t l = 0; l <= s.r; l++) hl[l] = s.levels[l - s.level_base].p;
+    DBuf<const double *> dl;
+    dl.alloc(s.r + 1);
+    KB_CUDA(cudaMemcpyAsync(dl.p, hl.data(), (s.r + 1) * sizeof(double *), cudaMemcpyHostToDevice,
+                            st));
+    const bool gamma_changed = new_gamma != s.gamma;
+    s.gamma = new_gamma;
+    const double *wr = s.levels[s.r - s.level_base].p;
+    if (aborted) {
+        k_katz_rows<<<nblk(n, 256), 256, 0, st>>>(nullptr, n, dl.p, (int)s.r, s.katz.p);
+        k_bounds_rows<<<nblk(n, 256), 256, 0, st>>>(nullptr, n, s.katz.p, wr, s.alpha, s.gamma,
+                                                    s.undirected, s.lower.p, s.upper.p);
+        note_launch(2);
+    } else {
+        DBuf<int32_t> tl, iota;
+        DBuf<int64_t> tn;
+        tl.alloc(n); iota.alloc(n); tn.alloc(1);
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, cub::CountingInputIterator<int32_t>(0),
+                                              touched.p, tl.p, tn.p, (int)n, st);
+        });
+        int64_t ntouch = 0;
+        KB_CUDA(cudaMemcpyAsync(&ntouch, tn.p, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        if (ntouch) {
+            k_katz_rows<<<nblk(ntouch, 256), 256, 0, st>>>(tl.p, ntouch, dl.p, (int)s.r, s.katz.p);
+            note_launch();
+        }
+        if (gamma_changed) {
+            k_bounds_rows<<<nblk(n, 256), 256, 0, st>>>(nullptr, n, s.katz.p, wr, s.alpha,
+                                                        s.gamma, s.undirected, s.lower.p,
+                                                        s.upper.p);
+            note_launch();
+        } else if (ntouch) {
+            k_bounds_rows<<<nblk(ntouch, 256), 256, 0, st>>>(tl.p, ntouch, s.katz.p, wr, s.alpha,
+                                                             s.gamma, s.undirected, s.lower.p,
+                                                             s.upper.p);
+            note_launch();
+        }
+    }
+    KB_CUDA(cudaGetLastError());
+
+    // 4. reactivation (dynamic.py:190-197)
+    if ((s.kind == KB_RANKING || s.kind == KB_TOPK) && !s.act_dense && s.m_host < n) {
+        const int64_t m = s.m_host;
+        DBuf<unsigned char> inact, flag;
+        DBuf<unsigned long long> mn;
+        DBuf<int64_t> nb;
+        inact.alloc(n); flag.alloc(n); mn.alloc(1); nb.alloc(1);
+        KB_CUDA(cudaMemsetAsync(inact.p, 0, n, st));
+        KB_CUDA(cudaMemsetAsync(mn.p, 0xff, 8, st));
+        if (m) {
+            k_flags_from_list<<<nblk(m, 256), 256, 0, st>>>(s.act[s.cur].p, m, inact.p);
+            k_min_lower<<<2 * g.sm_count, 256, 0, st>>>(s.act[s.cur].p, m, s.lower.p, mn.p);
+            note_launch(2);
+        }
+        k_reactivate_flags<<<nblk(n, 256), 256, 0, st>>>(g.iperm.p, n, inact.p, s.upper.p, mn.p,
+                                                        s.eps, flag.p);
+        note_launch();
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, g.iperm.p, flag.p, s.act[s.cur].p + m, nb.p,
+                                              (int)n, st);
+        });
+        int64_t back = 0;
+        KB_CUDA(cudaMemcpyAsync(&back, nb.p, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        s.m_host = m + back;
+        st_out.reactivated = back;
+    }
+
+    // 5. the relabelling is no longer degree-sorted: no static shortcuts
+    s.zero_tail_exact = false;
+    s.tail_zero_from = n;
+    s.graph_version = g.version;
+
+    // 6. resume (dynamic.py:203-210)
+    for (;;) {
+        if (run_check(s, st)) break;
+        if (s.r >= s.max_iter) {
+            *stats = st_out;
+            const double gap = run_gap(s, st);
+            char buf[160];
+            snprintf(buf, sizeof buf,
+                     "stopping rule unmet after resuming to %lld iterations (gap %.3e)",
+                     (long long)s.r, gap);
+            throw Error{KB_ECONVERGENCE, buf};
+        }
+        launch_iterate(s, st);
+        st_out.resumed_iterations++;
+    }
+    *stats = st_out;
+}
+
+}  // namespace kb

@@ -1,5 +1,12 @@
-// Graph ingest: canonical host CSR -> device SELL-32 over degree-relabelled
-// rows (replaces Graph.out_csr, graph.py:177-197).
+// Graph ingest: canonical CSR -> device SELL-32 over degree-relabelled rows
+// (replaces Graph.out_csr, graph.py:177-197).
+//
+// The canonical CSR is kept on the device as a CSR-with-slack: row v owns
+// the slots [indptr[v], indptr[v+1]) of `indices` and uses the first rlen[v]
+// of them, ascending.  A fresh graph is compact (capacity == length); the
+// first dynamic batch spreads it out with per-row slack (kb_dynamic.cu).
+// The SELL layout K1 reads is (re)built from it by build_sell().
+#include <cub/block/block_reduce.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -12,29 +19,38 @@
 namespace kb {
 
 size_t Graph::device_bytes() const {
-    return perm.bytes() + iperm.bytes() + deg.bytes() + indptr.bytes() +
+    return perm.bytes() + iperm.bytes() + deg.bytes() + indptr.bytes() + rlen.bytes() +
            indices.bytes() + sell.cols.bytes() + sell.slice_off.bytes() +
-           sell.slice_w.bytes() + sell.vlen.bytes() + seg_ptr.bytes() +
-           seg_list.bytes();
+           sell.slice_w.bytes() + sell.vlen.bytes() + seg_ptr.bytes() + seg_list.bytes() +
+           hrow.bytes() + vrow.bytes() + zrows.bytes() + orig_pos.bytes() + orig_zero.bytes();
 }
 
 namespace {
 
-__global__ void k_degree(const int64_t *indptr, int64_t n, uint32_t *key,
-                         int32_t *ids) {
+inline unsigned blocks_for(int64_t n, int t) {
+    return (unsigned)std::max<int64_t>(1, (n + t - 1) / t);
+}
+
+__global__ void k_rlen_compact(const int64_t *indptr, int64_t n, int32_t *rlen) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < n) rlen[v] = (int32_t)(indptr[v + 1] - indptr[v]);
+}
+
+__global__ void k_degree_key(const int32_t *rlen, int64_t n, uint32_t *key, int32_t *ids) {
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
-    int64_t d = indptr[v + 1] - indptr[v];
-    key[v] = 0xFFFFFFFFu - (uint32_t)d;  // ascending key == descending degree
+    key[v] = 0xFFFFFFFFu - (uint32_t)rlen[v];  // ascending key == descending degree
     ids[v] = (int32_t)v;
 }
 
-__global__ void k_finish_perm(const uint32_t *skey, const int32_t *perm,
-                              int64_t n, int32_t *iperm, int32_t *sdeg) {
+__global__ void k_invert(const int32_t *perm, int64_t n, int32_t *iperm) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    iperm[perm[i]] = (int32_t)i;
-    sdeg[i] = (int32_t)(0xFFFFFFFFu - skey[i]);
+    if (i < n) iperm[perm[i]] = (int32_t)i;
+}
+
+__global__ void k_len_by_new(const int32_t *rlen, const int32_t *perm, int64_t n, int32_t *deg) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) deg[i] = rlen[perm[i]];
 }
 
 // first index in the descending array whose value <= bound
@@ -47,18 +63,46 @@ __device__ int64_t first_le(const int32_t *a, int64_t n, int64_t bound) {
     return lo;
 }
 
-__global__ void k_counts(const int32_t *sdeg, int64_t n, int64_t split,
-                         int64_t *out) {
-    out[0] = first_le(sdeg, n, 0);      // nv: rows with arcs
-    out[1] = first_le(sdeg, n, split);  // nh: rows longer than split
-    out[2] = n ? sdeg[0] : 0;
+__global__ void k_counts(const int32_t *sdeg, int64_t n, int64_t split, int64_t *out) {
+    out[0] = first_le(sdeg, n, 0);      // rows with arcs
+    out[1] = first_le(sdeg, n, split);  // rows longer than split
 }
 
-__global__ void k_vlen_tail(const int32_t *sdeg, int64_t nh, int64_t nv,
-                            int64_t nseg, int32_t *vlen) {
+__global__ void k_max(const int32_t *a, int64_t n, unsigned long long *out) {
+    typedef cub::BlockReduce<int, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    int m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, a[i]);
+    m = Red(tmp).Reduce(m, cub::Max());
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)m);
+}
+
+// classify rows by new id: heavy (len > split), normal (0 < len <= split), empty
+__global__ void k_row_class(const int32_t *deg, int64_t n, int64_t split, unsigned char *heavy,
+                            unsigned char *normal, unsigned char *zero, int32_t *iota,
+                            uint32_t *key) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int d = deg[v];
+    heavy[v] = d > split;
+    normal[v] = d > 0 && d <= split;
+    zero[v] = d == 0;
+    iota[v] = (int32_t)v;
+    key[v] = 0xFFFFFFFFu - (uint32_t)d;
+}
+
+__global__ void k_gather_keys(const uint32_t *key, const int32_t *ids, int64_t m, uint32_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= nv - nh) return;
-    vlen[nseg + i] = sdeg[nh + i];
+    if (i < m) out[i] = key[ids[i]];
+}
+
+__global__ void k_vlen_normal(const int32_t *deg, const int32_t *vrow, int64_t nh, int64_t nnorm,
+                              int64_t nseg, int32_t *vlen) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nnorm) return;
+    vlen[nseg + i] = deg[vrow ? vrow[i] : nh + i];
 }
 
 __global__ void k_slice_width(const int32_t *vlen, int64_t nvr, int64_t nslices,
@@ -76,12 +120,11 @@ __global__ void k_slice_width(const int32_t *vlen, int64_t nvr, int64_t nslices,
 }
 
 // one warp per slice: lane l copies virtual row s*32+l into its column slots
-__global__ void k_fill(const int64_t *indptr, const int32_t *indices,
-                       const int32_t *perm, const int32_t *iperm,
-                       const int32_t *vlen, const int32_t *seg_row,
-                       const int32_t *seg_start, const int32_t *slice_w,
-                       const int64_t *slice_off, int64_t nslices, int64_t nvr,
-                       int64_t nseg, int64_t nh, int32_t *cols) {
+__global__ void k_fill(const int64_t *indptr, const int32_t *indices, const int32_t *perm,
+                       const int32_t *iperm, const int32_t *vlen, const int32_t *seg_row,
+                       const int32_t *seg_start, const int32_t *hrow, const int32_t *vrow,
+                       const int32_t *slice_w, const int64_t *slice_off, int64_t nslices,
+                       int64_t nvr, int64_t nseg, int64_t nh, int32_t *cols) {
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= nslices) return;
@@ -92,8 +135,13 @@ __global__ void k_fill(const int64_t *indptr, const int32_t *indices,
     if (vr < nvr) {
         len = vlen[vr];
         int64_t row_new, start = 0;
-        if (vr < nseg) { row_new = seg_row[vr]; start = seg_start[vr]; }
-        else row_new = nh + (vr - nseg);
+        if (vr < nseg) {
+            const int32_t h = seg_row[vr];
+            row_new = hrow ? hrow[h] : h;
+            start = seg_start[vr];
+        } else {
+            row_new = vrow ? vrow[vr - nseg] : nh + (vr - nseg);
+        }
         src = indptr[perm[row_new]] + start;
     }
     int w = slice_w[s];
@@ -106,10 +154,10 @@ __global__ void k_fill(const int64_t *indptr, const int32_t *indices,
     }
 }
 
-__global__ void k_arc_flags(const int64_t *indptr, int64_t n, unsigned char *fl, int32_t *iota) {
+__global__ void k_arc_flags(const int32_t *rlen, int64_t n, unsigned char *fl, int32_t *iota) {
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
-    fl[v] = indptr[v + 1] > indptr[v];
+    fl[v] = rlen[v] > 0;
     iota[v] = (int32_t)v;
 }
 
@@ -118,67 +166,119 @@ __global__ void k_flip(unsigned char *fl, int64_t n) {
     if (v < n) fl[v] = !fl[v];
 }
 
-inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+template <typename F>
+void cub_run(F &&f) {
+    size_t tb = 0;
+    KB_CUDA(f(nullptr, tb));
+    DBuf<unsigned char> tmp;
+    tmp.alloc(tb);
+    KB_CUDA(f(tmp.p, tb));
+    note_launch();
+}
 
 }  // namespace
 
-void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
-    cudaStream_t st = g.stream;
-    g.indptr.alloc(g.n + 1);
-    g.indices.alloc(g.nnz);
-    KB_CUDA(cudaMemcpyAsync(g.indptr.p, h_indptr, (g.n + 1) * sizeof(int64_t),
-                            cudaMemcpyHostToDevice, st));
-    if (g.nnz)
-        KB_CUDA(cudaMemcpyAsync(g.indices.p, h_indices, g.nnz * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
-    build_graph_device(g);
-}
-
-// g.indptr / g.indices already hold the canonical CSR on the device
-void build_graph_device(Graph &g) {
+// Virtual rows, slices and column slots for the current arc set under the
+// current relabelling.  `fresh` means perm sorts rows by descending length,
+// so heavy / normal / empty rows are the contiguous new-id ranges
+// [0,nh) / [nh,nv) / [nv,n) and no explicit row maps are needed.
+void build_sell(Graph &g, bool fresh) {
     cudaStream_t st = g.stream;
     const int64_t n = g.n;
-
-    // ---- relabel rows by descending degree (stable radix sort on ~deg)
-    DBuf<uint32_t> key_in, key_out;
-    DBuf<int32_t> id_in;
-    key_in.alloc(n); key_out.alloc(n); id_in.alloc(n);
-    g.perm.alloc(n); g.iperm.alloc(n); g.deg.alloc(n);
-    if (n) k_degree<<<blocks_for(n, 256), 256, 0, st>>>(g.indptr.p, n, key_in.p, id_in.p); note_launch();
-    KB_CUDA(cudaGetLastError());
-    size_t tmp_bytes = 0;
-    KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key_in.p, key_out.p,
-                                            id_in.p, g.perm.p, (int)n, 0, 32, st));
-    DBuf<unsigned char> tmp;
-    tmp.alloc(tmp_bytes);
-    KB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key_in.p, key_out.p,
-                                            id_in.p, g.perm.p, (int)n, 0, 32, st)); note_launch();
-    if (n) k_finish_perm<<<blocks_for(n, 256), 256, 0, st>>>(key_out.p, g.perm.p, n,
-                                                            g.iperm.p, g.deg.p); note_launch();
-    KB_CUDA(cudaGetLastError());
-    key_in.release(); key_out.release(); id_in.release(); tmp.release();
-
-    DBuf<int64_t> cnt;
-    cnt.alloc(3);
-    k_counts<<<1, 1, 0, st>>>(g.deg.p, n, g.split, cnt.p); note_launch();
-    int64_t hc[3];
-    KB_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    g.nv = hc[0];
-    g.nh = hc[1];
-    g.max_deg = hc[2];
+    if (!g.deg.p) g.deg.alloc(n);
+    if (n) k_len_by_new<<<blocks_for(n, 256), 256, 0, st>>>(g.rlen.p, g.perm.p, n, g.deg.p);
+    note_launch();
+    g.hrow.release();
+    g.vrow.release();
+    g.zrows.release();
+    g.implicit_rows = fresh;
+    {
+        DBuf<unsigned long long> mx;
+        mx.alloc(1);
+        KB_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), st));
+        k_max<<<2 * std::max(1, g.sm_count), 256, 0, st>>>(g.deg.p, n, mx.p);
+        note_launch();
+        unsigned long long hm = 0;
+        KB_CUDA(cudaMemcpyAsync(&hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        g.max_deg = (int64_t)hm;
+    }
+    if (fresh) {
+        DBuf<int64_t> cnt;
+        cnt.alloc(2);
+        k_counts<<<1, 1, 0, st>>>(g.deg.p, n, g.split, cnt.p);
+        note_launch();
+        int64_t hc[2];
+        KB_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        g.nv = hc[0];
+        g.nh = hc[1];
+        g.nzero = n - g.nv;
+    } else {
+        DBuf<unsigned char> fh, fn, fz;
+        DBuf<int32_t> iota, sel;
+        DBuf<uint32_t> key, k2, k3;
+        DBuf<int64_t> cnt;
+        fh.alloc(n); fn.alloc(n); fz.alloc(n); iota.alloc(n); key.alloc(n); cnt.alloc(3);
+        k_row_class<<<blocks_for(n, 256), 256, 0, st>>>(g.deg.p, n, g.split, fh.p, fn.p, fz.p,
+                                                       iota.p, key.p);
+        note_launch();
+        g.hrow.alloc(n); g.zrows.alloc(n); sel.alloc(n);
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, iota.p, fh.p, g.hrow.p, cnt.p, (int)n, st);
+        });
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, iota.p, fn.p, sel.p, cnt.p + 1, (int)n, st);
+        });
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, iota.p, fz.p, g.zrows.p, cnt.p + 2, (int)n,
+                                              st);
+        });
+        int64_t hc[3];
+        KB_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        g.nh = hc[0];
+        const int64_t nnorm = hc[1];
+        g.nzero = hc[2];
+        g.nv = g.nh + nnorm;
+        // normal rows by descending length (stable in the new id) for balance
+        g.vrow.alloc(std::max<int64_t>(1, nnorm));
+        k2.alloc(std::max<int64_t>(1, nnorm));
+        k3.alloc(std::max<int64_t>(1, nnorm));
+        if (nnorm) {
+            k_gather_keys<<<blocks_for(nnorm, 256), 256, 0, st>>>(key.p, sel.p, nnorm, k2.p);
+            note_launch();
+            cub_run([&](void *t, size_t &b) {
+                return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k3.p, sel.p, g.vrow.p,
+                                                       (int)nnorm, 0, 32, st);
+            });
+        }
+    }
     g.hot = std::min<int64_t>(g.hot, g.n);
 
     // ---- heavy rows -> segments (host plan; nh is small)
     std::vector<int32_t> hdeg(g.nh);
-    if (g.nh)
-        KB_CUDA(cudaMemcpy(hdeg.data(), g.deg.p, g.nh * sizeof(int32_t),
-                           cudaMemcpyDeviceToHost));
+    if (g.nh) {
+        if (fresh) {
+            KB_CUDA(cudaMemcpyAsync(hdeg.data(), g.deg.p, g.nh * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, st));
+        } else {
+            DBuf<int32_t> hd;
+            hd.alloc(g.nh);
+            k_gather_keys<<<blocks_for(g.nh, 256), 256, 0, st>>>(
+                (const uint32_t *)g.deg.p, g.hrow.p, g.nh, (uint32_t *)hd.p);
+            note_launch();
+            KB_CUDA(cudaMemcpyAsync(hdeg.data(), hd.p, g.nh * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaStreamSynchronize(st));
+        }
+        KB_CUDA(cudaStreamSynchronize(st));
+    }
     std::vector<int32_t> seg_row, seg_start, seg_len;
     std::vector<std::vector<int32_t>> row_segs(g.nh);
     const int64_t T = g.split;
     for (int64_t h = 0; h < g.nh; h++) {  // full segments, row by row
-        int64_t full = hdeg[h] / T;
+        const int64_t full = hdeg[h] / T;
         for (int64_t q = 0; q < full; q++) {
             row_segs[h].push_back((int32_t)seg_row.size());
             seg_row.push_back((int32_t)h);
@@ -226,31 +326,83 @@ void build_graph_device(Graph &g) {
         KB_CUDA(cudaMemcpyAsync(S.vlen.p, seg_len.data(), S.nseg * sizeof(int32_t),
                                 cudaMemcpyHostToDevice, st));
     }
-    if (g.nv > g.nh)
-        k_vlen_tail<<<blocks_for(g.nv - g.nh, 256), 256, 0, st>>>(g.deg.p, g.nh, g.nv,
-                                                                 S.nseg, S.vlen.p); note_launch();
-    KB_CUDA(cudaGetLastError());
+    const int64_t nnorm = g.nv - g.nh;
+    if (nnorm) {
+        k_vlen_normal<<<blocks_for(nnorm, 256), 256, 0, st>>>(g.deg.p, g.vrow.p, g.nh, nnorm,
+                                                             S.nseg, S.vlen.p);
+        note_launch();
+    }
 
     // ---- slice widths and offsets
     S.slice_w.alloc(S.nslices);
     S.slice_off.alloc(S.nslices + 1);
     DBuf<int64_t> sz;
     sz.alloc(S.nslices + 1);
-    if (S.nslices)
+    if (S.nslices) {
         k_slice_width<<<blocks_for(S.nslices, 256), 256, 0, st>>>(S.vlen.p, S.nvr, S.nslices,
-                                                                 S.slice_w.p, sz.p); note_launch();
+                                                                 S.slice_w.p, sz.p);
+        note_launch();
+    }
     KB_CUDA(cudaMemsetAsync(sz.p + S.nslices, 0, sizeof(int64_t), st));
-    tmp_bytes = 0;
-    KB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sz.p, S.slice_off.p,
-                                          (int)(S.nslices + 1), st));
-    tmp.alloc(tmp_bytes);
-    KB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, sz.p, S.slice_off.p,
-                                          (int)(S.nslices + 1), st)); note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, sz.p, S.slice_off.p, (int)(S.nslices + 1), st);
+    });
     KB_CUDA(cudaMemcpyAsync(&S.elems, S.slice_off.p + S.nslices, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    tmp.release();
     sz.release();
+
+    // ---- fill the column slots (relabelled, original per-row order)
+    S.cols.alloc(S.elems + 4);
+    if (S.nslices) {
+        const int64_t threads = S.nslices * 32;
+        k_fill<<<blocks_for(threads, 256), 256, 0, st>>>(
+            g.indptr.p, g.indices.p, g.perm.p, g.iperm.p, S.vlen.p, d_seg_row.p, d_seg_start.p,
+            g.hrow.p, g.vrow.p, S.slice_w.p, S.slice_off.p, S.nslices, S.nvr, S.nseg, g.nh,
+            S.cols.p);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    KB_CUDA(cudaStreamSynchronize(st));
+    g.sell_dirty = false;
+}
+
+void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
+    cudaStream_t st = g.stream;
+    g.indptr.alloc(g.n + 1);
+    g.indices.alloc(g.nnz);
+    KB_CUDA(cudaMemcpyAsync(g.indptr.p, h_indptr, (g.n + 1) * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, st));
+    if (g.nnz)
+        KB_CUDA(cudaMemcpyAsync(g.indices.p, h_indices, g.nnz * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, st));
+    build_graph_device(g);
+}
+
+// g.indptr / g.indices hold a compact canonical CSR on the device
+void build_graph_device(Graph &g) {
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n;
+    g.rlen.alloc(n);
+    if (n) k_rlen_compact<<<blocks_for(n, 256), 256, 0, st>>>(g.indptr.p, n, g.rlen.p);
+    note_launch();
+
+    // ---- relabel rows by descending degree (stable radix sort on ~deg)
+    {
+        DBuf<uint32_t> key_in, key_out;
+        DBuf<int32_t> id_in;
+        key_in.alloc(n); key_out.alloc(n); id_in.alloc(n);
+        g.perm.alloc(n); g.iperm.alloc(n);
+        if (n) k_degree_key<<<blocks_for(n, 256), 256, 0, st>>>(g.rlen.p, n, key_in.p, id_in.p);
+        note_launch();
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, key_in.p, key_out.p, id_in.p, g.perm.p,
+                                                   (int)n, 0, 32, st);
+        });
+        if (n) k_invert<<<blocks_for(n, 256), 256, 0, st>>>(g.perm.p, n, g.iperm.p);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
 
     // ---- original ids with / without out-arcs, ascending (for K3)
     {
@@ -258,54 +410,41 @@ void build_graph_device(Graph &g) {
         DBuf<int32_t> iota;
         DBuf<int64_t> cntp;
         fl.alloc(n); iota.alloc(n); cntp.alloc(2);
-        k_arc_flags<<<blocks_for(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(g.indptr.p, n, fl.p, iota.p);
+        k_arc_flags<<<blocks_for(n, 256), 256, 0, st>>>(g.rlen.p, n, fl.p, iota.p);
         note_launch();
-        g.orig_pos.alloc(std::max<int64_t>(1, g.nv));
-        g.orig_zero.alloc(std::max<int64_t>(1, n - g.nv));
-        size_t tb = 0;
-        DBuf<unsigned char> t2;
-        // stable selection of both sides (DevicePartition would reverse the
-        // rejected side)
-        KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fl.p, g.orig_pos.p, cntp.p,
-                                           (int)n, st));
-        t2.alloc(tb);
-        KB_CUDA(cub::DeviceSelect::Flagged(t2.p, tb, iota.p, fl.p, g.orig_pos.p, cntp.p, (int)n,
-                                           st));
-        k_flip<<<blocks_for(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(fl.p, n);
-        KB_CUDA(cub::DeviceSelect::Flagged(t2.p, tb, iota.p, fl.p, g.orig_zero.p, cntp.p + 1,
-                                           (int)n, st));
-        note_launch(3);
+        g.orig_pos.alloc(n);
+        g.orig_zero.alloc(n);
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, iota.p, fl.p, g.orig_pos.p, cntp.p, (int)n,
+                                              st);
+        });
+        k_flip<<<blocks_for(n, 256), 256, 0, st>>>(fl.p, n);
+        note_launch();
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, iota.p, fl.p, g.orig_zero.p, cntp.p + 1,
+                                              (int)n, st);
+        });
     }
-
-    // ---- fill the column slots (relabelled, original per-row order)
-    S.cols.alloc(S.elems + 4);
-    if (S.nslices) {
-        int64_t threads = S.nslices * 32;
-        k_fill<<<blocks_for(threads, 256), 256, 0, st>>>(
-            g.indptr.p, g.indices.p, g.perm.p, g.iperm.p, S.vlen.p, d_seg_row.p,
-            d_seg_start.p, S.slice_w.p, S.slice_off.p, S.nslices, S.nvr, S.nseg,
-            g.nh, S.cols.p); note_launch();
-        KB_CUDA(cudaGetLastError());
-    }
-    KB_CUDA(cudaStreamSynchronize(st));
+    build_sell(g, true);
 }
 
 namespace {
 // arc (u, v) needs u in row v; rows are sorted, so a binary search per arc
-__global__ void k_symmetric(const int64_t *indptr, const int32_t *indices, int64_t n,
-                            unsigned long long *bad) {
+__global__ void k_symmetric(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
+                            int64_t n, unsigned long long *bad) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= n) return;
     const int64_t u = warp;
-    for (int64_t e = indptr[u] + lane; e < indptr[u + 1]; e += 32) {
+    for (int64_t e = indptr[u] + lane; e < indptr[u] + rlen[u]; e += 32) {
         const int64_t v = indices[e];
-        int64_t lo = indptr[v], hi = indptr[v + 1];
+        int64_t lo = indptr[v], hi = indptr[v] + rlen[v];
+        const int64_t end = hi;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
             if (indices[mid] < u) lo = mid + 1; else hi = mid;
         }
-        if (lo >= indptr[v + 1] || indices[lo] != u) { atomicAdd(bad, 1ull); return; }
+        if (lo >= end || indices[lo] != u) { atomicAdd(bad, 1ull); return; }
     }
 }
 }  // namespace
@@ -315,8 +454,9 @@ int graph_is_symmetric(Graph &g) {
     bad.alloc(1);
     KB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), g.stream));
     if (g.n)
-        k_symmetric<<<blocks_for(g.n * 32, 256), 256, 0, g.stream>>>(g.indptr.p, g.indices.p,
-                                                                      g.n, bad.p); note_launch();
+        k_symmetric<<<blocks_for(g.n * 32, 256), 256, 0, g.stream>>>(g.indptr.p, g.rlen.p,
+                                                                      g.indices.p, g.n, bad.p);
+    note_launch();
     KB_CUDA(cudaGetLastError());
     unsigned long long h = 0;
     KB_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, g.stream));

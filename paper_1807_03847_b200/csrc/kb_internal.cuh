@@ -96,16 +96,25 @@ struct Sell {
 struct Graph {
     int device = 0;
     int sm_count = 0;
-    int64_t n = 0, nnz = 0, nv = 0, nh = 0, max_deg = 0;
+    int64_t n = 0, nnz = 0, nv = 0, nh = 0, nzero = 0, max_deg = 0;
     int64_t split = 0, hot = 0;
     int64_t version = 1;
     DBuf<int32_t> perm;    // new -> original id
     DBuf<int32_t> iperm;   // original -> new id
     DBuf<int32_t> deg;     // out-degree by new id
-    // canonical CSR (original ids, rows ascending) kept for the dynamic path
-    // and the symmetry test
+    // canonical CSR-with-slack (original ids, rows ascending): row v owns
+    // indices[indptr[v] .. indptr[v+1]) and uses the first rlen[v] slots
     DBuf<int64_t> indptr;
     DBuf<int32_t> indices;
+    DBuf<int32_t> rlen;
+    bool slack = false;      // indptr spreads rows apart (after an update)
+    // row maps of the SELL layout; empty while implicit_rows (fresh
+    // relabelling: heavy [0,nh), normal [nh,nv), empty [nv,n))
+    bool implicit_rows = true;
+    bool sell_dirty = false; // arcs changed since the SELL build
+    bool mutated = false;    // a batch was applied: the relabelling is no longer
+                             // degree-sorted and empty rows are not a tail
+    DBuf<int32_t> hrow, vrow, zrows;
     Sell sell;
     // heavy-row combine: segments of heavy row h are seg_list[seg_ptr[h] ..
     // seg_ptr[h+1]) in order (indices into the segment-sum buffer)
@@ -160,6 +169,7 @@ struct State {
 
 // ---------------------------------------------------------------- kernels
 void launch_iterate(State &s, cudaStream_t st);
+void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only);
 void collect_k1_times(State &s);
 bool run_check(State &s, cudaStream_t st);      // returns converged
 double run_gap(State &s, cudaStream_t st);
@@ -169,6 +179,10 @@ void gather_to_original(const Graph &g, const double *src_new, double *dst_orig,
                         cudaStream_t st);
 void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices);
 void build_graph_device(Graph &g);
+void build_sell(Graph &g, bool fresh);
+void compact_csr(Graph &g, DBuf<int64_t> &indptr, DBuf<int32_t> &indices);
+void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                  int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats);
 void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], double a,
                      double ab, double abc, DBuf<int64_t> &indptr, DBuf<int32_t> &indices,
                      int64_t &nnz_out);

@@ -61,6 +61,8 @@ struct IterArgs {
     double *w, *katz, *lower, *upper, *seg_sum;
     double alpha, gamma;
     int undirected;
+    int level_only;                 // write w only (dynamic level repair)
+    const int32_t *hrow, *vrow;     // explicit row maps (nullptr: implicit)
     int hot;
     unsigned long long *counter;
 };
@@ -85,6 +87,10 @@ __device__ __forceinline__ double fetch(const double *__restrict__ hot_s, int ho
 
 __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s) {
     const double w = __dmul_rn(A.alpha, s);          // engine.py:306
+    if (A.level_only) {
+        A.w[v] = w;
+        return;
+    }
     const double k = __dadd_rn(A.katz[v], w);        // :308
     const double t = __dmul_rn(A.alpha, w);          // :309
     A.katz[v] = k;
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         }
         if (vr < A.nvr) {
             if (vr < A.nseg) A.seg_sum[vr] = sum;
-            else epilogue(A, A.nh + (vr - A.nseg), sum);
+            else epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), sum);
         }
     }
 }
@@ -186,7 +192,7 @@ __global__ void k_heavy_combine(IterArgs A, const int32_t *seg_ptr,
     double s = 0.0;
     for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++)
         s = __dadd_rn(s, A.seg_sum[seg_list[q]]);
-    epilogue(A, h, s);
+    epilogue(A, A.hrow ? A.hrow[h] : h, s);
 }
 
 // rows without out-arcs: w = 0, katz unchanged (0), bounds collapse to katz
@@ -196,6 +202,19 @@ __global__ void k_empty_rows(double *upper, double *lower, const double *katz,
     if (i >= n) return;
     lower[i] = katz[i];
     upper[i] = katz[i];
+}
+
+// explicit empty rows (after updates): w = 0 and the bounds collapse to katz
+__global__ void k_zero_rows(const int32_t *zrows, int64_t nz, double *w, double *lower,
+                            double *upper, const double *katz, int level_only) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nz) return;
+    const int32_t v = zrows[i];
+    w[v] = 0.0;
+    if (!level_only) {
+        lower[v] = katz[v];
+        upper[v] = katz[v];
+    }
 }
 
 __global__ void k_gather(const int32_t *iperm, const double *src, double *dst,
@@ -226,13 +245,12 @@ void collect_k1_times(State &s) {
     if (s.k1_read == s.k1_used) s.k1_read = s.k1_used = 0;  // recycle the pool
 }
 
-void launch_iterate(State &s, cudaStream_t st) {
+// One SpMV step w = alpha * A x (+ the fused bound refresh unless
+// level_only) over the current SELL layout.
+void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only) {
     Graph &g = *s.g;
     const int64_t n = g.n;
-    // new level buffer: rows without arcs stay exactly 0
-    DBuf<double> wnew;
-    wnew.alloc(n + 1);
-    KB_CUDA(cudaMemsetAsync(wnew.p + g.nv, 0, (n + 1 - g.nv) * sizeof(double), st));
+    if (g.sell_dirty) build_sell(g, false);
     IterArgs A;
     A.cols = g.sell.cols.p;
     A.slice_off = g.sell.slice_off.p;
@@ -242,8 +260,8 @@ void launch_iterate(State &s, cudaStream_t st) {
     A.nvr = g.sell.nvr;
     A.nseg = g.sell.nseg;
     A.nh = g.nh;
-    A.x = s.x_level();
-    A.w = wnew.p;
+    A.x = x;
+    A.w = w;
     A.katz = s.katz.p;
     A.lower = s.lower.p;
     A.upper = s.upper.p;
@@ -251,8 +269,21 @@ void launch_iterate(State &s, cudaStream_t st) {
     A.alpha = s.alpha;
     A.gamma = s.gamma;
     A.undirected = s.undirected;
+    A.level_only = level_only;
+    A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
+    A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
     A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), n);
     A.counter = s.work_counter.p;
+    if (s.seg_sum.n < (size_t)std::max<int64_t>(1, g.sell.nseg)) {
+        s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
+        A.seg_sum = s.seg_sum.p;
+    }
+    if (g.implicit_rows) {
+        // rows without arcs: w = 0 (bounds collapse once, see k_empty_rows)
+        KB_CUDA(cudaMemsetAsync(w + g.nv, 0, (n + 1 - g.nv) * sizeof(double), st));
+    } else {
+        KB_CUDA(cudaMemsetAsync(w + n, 0, sizeof(double), st));
+    }
     if (s.k1_used + 2 > s.k1_ev.size()) {
         for (int q = 0; q < 2; q++) {
             cudaEvent_t e;
@@ -278,13 +309,27 @@ void launch_iterate(State &s, cudaStream_t st) {
         KB_CUDA(cudaGetLastError());
         if (g.nh) {
             k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
-                A, g.seg_ptr.p, g.seg_list.p); note_launch();
+                A, g.hrow.p ? g.seg_ptr.p : g.seg_ptr.p, g.seg_list.p); note_launch();
             KB_CUDA(cudaGetLastError());
         }
     }
+    if (!g.implicit_rows && g.nzero) {
+        k_zero_rows<<<(unsigned)((g.nzero + 255) / 256), 256, 0, st>>>(
+            g.zrows.p, g.nzero, w, s.lower.p, s.upper.p, s.katz.p, level_only);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
     KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used + 1], st));
-    s.k1_used += 2;
-    if (s.r == 0 && n > g.nv) {
+    if (!level_only) s.k1_used += 2;
+}
+
+void launch_iterate(State &s, cudaStream_t st) {
+    Graph &g = *s.g;
+    const int64_t n = g.n;
+    DBuf<double> wnew;
+    wnew.alloc(n + 1);
+    run_spmv(s, st, s.x_level(), wnew.p, false);
+    if (s.r == 0 && g.implicit_rows && n > g.nv) {
         k_empty_rows<<<(unsigned)((n - g.nv + 255) / 256), 256, 0, st>>>(
             s.upper.p, s.lower.p, s.katz.p, g.nv, n); note_launch();
         KB_CUDA(cudaGetLastError());

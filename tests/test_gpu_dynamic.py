@@ -1,0 +1,288 @@
+"""Dynamic updates (K4) on the device vs the reference's golden sequences,
+a fresh static recompute, and the reference suite's behavioural rules
+(pkg/tests/test_dynamic.py restated)."""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle import katz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_1807_03847_b200")
+
+REL = 1e-12
+
+
+def fresh_to_depth(g, st):
+    """Static state on g's current arcs, iterated to st.r (test_dynamic.py:18-24)."""
+    other = P.init(g, st.criterion, alpha=st.alpha, undirected=st.undirected,
+                   max_iterations=max(st.r, 1))
+    for _ in range(st.r):
+        P.iterate_once(other, g)
+    return other
+
+
+def assert_state_matches(st, fresh, rel=REL):
+    assert len(st.levels) == len(fresh.levels)
+    for mine, theirs in zip(st.levels, fresh.levels):
+        np.testing.assert_allclose(mine, theirs, rtol=rel, atol=rel)
+    np.testing.assert_allclose(st.katz, fresh.katz, rtol=rel, atol=rel)
+    np.testing.assert_allclose(st.lower, fresh.lower, rtol=rel, atol=rel)
+    np.testing.assert_allclose(st.upper, fresh.upper, rtol=rel, atol=rel)
+
+
+def er(n, p, seed, undirected=True):
+    rng = random.Random(seed)
+    e = []
+    for i in range(n):
+        for j in range(i + 1 if undirected else 0, n):
+            if i != j and rng.random() < p:
+                e.append((i, j))
+    return P.Graph.from_edges(n, e, undirected=undirected)
+
+
+def random_batch(g, rng, max_ops=5, undirected=False):
+    n = g.node_count
+    present = list(g.arcs())
+    if undirected:
+        present = [(u, v) for u, v in present if u < v]
+    rng.shuffle(present)
+    dels = present[:rng.randint(0, min(max_ops, len(present)))]
+    ins = []
+    want = rng.randint(0, max_ops)
+    tries = 0
+    while len(ins) < want and tries < 50 * max_ops:
+        tries += 1
+        u, v = rng.randrange(n), rng.randrange(n)
+        if u == v or g.has_arc(u, v) or (u, v) in ins:
+            continue
+        if undirected:
+            u, v = min(u, v), max(u, v)
+            if (u, v) in ins:
+                continue
+        ins.append((u, v))
+    if undirected:
+        dels = [a for uv in dels for a in (uv, uv[::-1])]
+        ins = [a for uv in ins for a in (uv, uv[::-1])]
+    return P.EdgeBatch(insertions=ins, deletions=dels)
+
+
+def test_golden_dynamic_sequences(golden_index, dynamic_cases):
+    """The reference's own update sequences: states within 1e-12 of its
+    delta-propagated values, bit-identical to a fresh static recompute, and
+    the same UpdateStats."""
+    for c in golden_index["dynamic"]:
+        name = c["name"]
+        g = P.Graph.from_edges(c["n"], dynamic_cases[f"{name}/edges0"])
+        kind = c["kind"]
+        crit = {"ranking": P.Criterion.ranking(c["epsilon"]),
+                "score": P.Criterion.score(c["epsilon"]),
+                "topk": P.Criterion.top_k(c["k"] or 1, c["epsilon"])}[kind]
+        st = P.init(g, crit, alpha=c["alpha"], undirected=c["undirected"])
+        P.run(st, g)
+        for i, step in enumerate(c["steps"]):
+            p = f"{name}/b{i}"
+            batch = P.EdgeBatch(insertions=[tuple(x) for x in dynamic_cases[p + "/ins"].tolist()],
+                                deletions=[tuple(x) for x in dynamic_cases[p + "/del"].tolist()])
+            P.update_batch(st, g, batch, theta=c["theta"])
+            assert st.r == step["r"], p
+            np.testing.assert_allclose(st.katz, dynamic_cases[p + "/katz"], rtol=REL, atol=1e-13)
+            np.testing.assert_allclose(st.lower, dynamic_cases[p + "/lower"], rtol=REL, atol=1e-13)
+            np.testing.assert_allclose(st.upper, dynamic_cases[p + "/upper"], rtol=REL, atol=1e-13)
+            fresh = fresh_to_depth(g, st)
+            np.testing.assert_array_equal(st.katz, fresh.katz, err_msg=p)
+            np.testing.assert_array_equal(st.lower, fresh.lower, err_msg=p)
+            np.testing.assert_array_equal(st.upper, fresh.upper, err_msg=p)
+            s = st.last_update_stats
+            assert s.seeds == step["seeds"], p
+            assert s.aborted_level == step["aborted_level"], p
+            assert s.level_sizes == step["level_sizes"], p
+            assert s.visited == step["visited"], p
+            assert s.reactivated == step["reactivated"], p
+            assert s.resumed_iterations == step["resumed_iterations"], p
+            assert st.gamma == step["gamma"], p
+
+
+def test_single_insertion_and_deletion_match_fresh():
+    g = P.Graph.from_edges(6, [(i, i + 1) for i in range(5)], undirected=True)
+    st = P.init(g, P.Criterion.ranking(1e-8), alpha=0.2, undirected=True)
+    P.run(st, g)
+    P.update_batch(st, g, P.EdgeBatch(insertions=[(0, 3), (3, 0)]), theta=1.0)
+    assert_state_matches(st, fresh_to_depth(g, st))
+    g2 = P.Graph.from_edges(8, [(i, (i + 1) % 8) for i in range(8)], undirected=True)
+    st2 = P.init(g2, P.Criterion.ranking(1e-8), alpha=0.2, undirected=True)
+    P.run(st2, g2)
+    P.update_batch(st2, g2, P.EdgeBatch(deletions=[(2, 3), (3, 2)]), theta=1.0)
+    assert_state_matches(st2, fresh_to_depth(g2, st2))
+
+
+def test_directed_mixed_and_random_streams():
+    g = er(40, 0.08, 13, undirected=False)
+    st = P.init(g, P.Criterion.score(1e-9), alpha=0.05)
+    P.run(st, g)
+    rng = random.Random(99)
+    P.update_batch(st, g, random_batch(g, rng, max_ops=6), theta=1.0)
+    assert_state_matches(st, fresh_to_depth(g, st))
+    rng = random.Random(7)
+    g = er(35, 0.1, 2)
+    st = P.init(g, P.Criterion.ranking(1e-7), alpha=0.02, undirected=True)
+    P.run(st, g)
+    for _ in range(8):
+        P.update_batch(st, g, random_batch(g, rng, max_ops=4, undirected=True), theta=1.0)
+        assert_state_matches(st, fresh_to_depth(g, st))
+        assert P.check_converged(st)
+
+
+def test_theta_zero_forces_full_recompute_and_routes_agree():
+    g = P.Graph.from_edges(12, [(i, (i + 1) % 12) for i in range(12)], undirected=True)
+    st = P.init(g, P.Criterion.score(1e-8), alpha=0.2, undirected=True)
+    P.run(st, g)
+    P.update_batch(st, g, P.EdgeBatch(insertions=[(0, 6), (6, 0)]), theta=0.0)
+    s = st.last_update_stats
+    assert s.aborted_level == 1 and s.level_sizes == []
+    assert_state_matches(st, fresh_to_depth(g, st))
+    g1, g2 = er(30, 0.1, 5), er(30, 0.1, 5)
+    ins = [(0, 17), (17, 0)] if not g1.has_arc(0, 17) else next(
+        [(u, v), (v, u)] for u in range(30) for v in range(u + 1, 30) if not g1.has_arc(u, v))
+    dele = next([(u, v), (v, u)] for u, v in sorted(g1.arcs()) if u < v and (u, v) != ins[0])
+    b = P.EdgeBatch(insertions=ins, deletions=dele)
+    s1 = P.init(g1, P.Criterion.score(1e-9), alpha=0.05, undirected=True)
+    s2 = P.init(g2, P.Criterion.score(1e-9), alpha=0.05, undirected=True)
+    P.run(s1, g1)
+    P.run(s2, g2)
+    P.update_batch(s1, g1, b, theta=1.0)
+    P.update_batch(s2, g2, b, theta=0.0)
+    assert s1.last_update_stats.aborted_level is None
+    assert s2.last_update_stats.aborted_level == 1
+    np.testing.assert_array_equal(s1.katz, s2.katz)
+    np.testing.assert_array_equal(s1.lower, s2.lower)
+    np.testing.assert_array_equal(s1.upper, s2.upper)
+
+
+def test_insert_then_delete_restores_levels():
+    e = []
+    for r in range(5):
+        for c in range(5):
+            v = r * 5 + c
+            if c + 1 < 5:
+                e.append((v, v + 1))
+            if r + 1 < 5:
+                e.append((v, v + 5))
+    g = P.Graph.from_edges(25, e, undirected=True)
+    st = P.init(g, P.Criterion.score(1e-9), alpha=0.1, undirected=True)
+    P.run(st, g)
+    levels0 = [lvl.copy() for lvl in st.levels]
+    arc = [(0, 6), (6, 0)]
+    P.update_batch(st, g, P.EdgeBatch(insertions=arc), theta=1.0)
+    P.update_batch(st, g, P.EdgeBatch(deletions=arc), theta=1.0)
+    assert len(st.levels) >= len(levels0)
+    for mine, orig in zip(st.levels, levels0):
+        np.testing.assert_allclose(mine, orig, rtol=1e-12, atol=1e-14)
+    assert_state_matches(st, fresh_to_depth(g, st))
+
+
+def test_empty_batch_is_a_noop():
+    g = P.Graph.from_edges(10, [(0, i) for i in range(1, 10)], undirected=True)
+    st = P.init(g, P.Criterion.top_k(3, 1e-7), undirected=True)
+    P.run(st, g)
+    lo, up = st.lower.copy(), st.upper.copy()
+    P.update_batch(st, g, P.EdgeBatch())
+    np.testing.assert_array_equal(st.lower, lo)
+    np.testing.assert_array_equal(st.upper, up)
+    assert P.check_converged(st)
+
+
+def test_guards():
+    g = P.Graph.from_edges(4, [(0, 1), (1, 2), (2, 3)], undirected=True)
+    st = P.init(g, P.Criterion.ranking(1e-6), undirected=True)
+    P.run(st, g)
+    arcs_before = set(g.arcs())
+    with pytest.raises(P.ParameterError):   # alpha admission before mutation
+        P.update_batch(st, g, P.EdgeBatch(insertions=[(1, 3), (3, 1)]))
+    assert set(g.arcs()) == arcs_before and P.check_converged(st)
+    c6 = lambda: P.Graph.from_edges(6, [(i, (i + 1) % 6) for i in range(6)], undirected=True)
+    g = c6()
+    st = P.init(g, P.Criterion.ranking(1e-6), alpha=0.2, undirected=True)
+    P.run(st, g)
+    with pytest.raises(P.ParameterError):
+        P.update_batch(st, g, P.EdgeBatch(insertions=[(0, 3)]))
+    with pytest.raises(P.ParameterError):
+        P.update_batch(st, g, P.EdgeBatch(), theta=1.5)
+    with pytest.raises(P.BatchPreconditionError):
+        P.update_batch(st, g, P.EdgeBatch(deletions=[(0, 3), (3, 0)]))
+    g.insert_arcs([(0, 3), (3, 0)])
+    with pytest.raises(P.StateError):
+        P.update_batch(st, g, P.EdgeBatch())
+    g = c6()
+    st = P.init(g, P.Criterion.ranking(1e-6), alpha=0.2, undirected=True, keep_all_levels=False)
+    P.run(st, g)
+    with pytest.raises(P.StateError):
+        P.update_batch(st, g, P.EdgeBatch())
+
+
+def test_topk_reactivates_displaced_nodes():
+    edges = [(0, i) for i in range(1, 12)] + [(12, 13), (13, 14), (12, 14)]
+    g = P.Graph.from_edges(15, edges, undirected=True)
+    st = P.init(g, P.Criterion.top_k(2, 1e-6), alpha=0.05, undirected=True)
+    P.run(st, g)
+    assert st.active.size < 15
+    dels = []
+    for leaf in range(4, 12):
+        dels += [(0, leaf), (leaf, 0)]
+    P.update_batch(st, g, P.EdgeBatch(deletions=dels), theta=1.0)
+    assert st.last_update_stats.reactivated > 0
+    assert P.check_converged(st)
+    fresh = P.init(g, P.Criterion.top_k(2, 1e-6), alpha=0.05, undirected=True)
+    assert P.ranking_result(st).top(2) == P.run(fresh, g).top(2)
+
+
+def test_locality_and_level_growth():
+    e = [(i, i + 1) for i in range(29)]
+    g = P.Graph.from_edges(30, e, undirected=True)
+    st = P.init(g, P.Criterion.score(0.5), alpha=0.3, undirected=True)
+    P.run(st, g)
+    P.update_batch(st, g, P.EdgeBatch(deletions=[(10, 11), (11, 10)]), theta=1.0)
+    sizes = st.last_update_stats.level_sizes
+    assert sizes[0] == 2
+    for a, b in zip(sizes, sizes[1:]):
+        assert b - a <= 2
+
+
+@pytest.mark.parametrize("nb", [100, 1000])
+def test_rmat_s16_batches_match_static_recompute(nb):
+    """C5 in miniature: insertion batches on R-MAT s16 ef16 vs a static run
+    on the post-batch graph (same r, order, top-100; bounds 1e-12)."""
+    g0 = O.rmat_graph(65536, edge_factor=16, seed=42)
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
+    P.run(st, g)
+    deg = np.diff(g0.indptr)
+    dmax = int(deg.max())
+    rng = np.random.default_rng(7)
+    ins = set()
+    while len(ins) < nb:
+        u, v = (int(x) for x in rng.integers(0, 65536, 2))
+        if u == v:
+            continue
+        u, v = min(u, v), max(u, v)
+        if (u, v) in ins or g.has_arc(u, v) or deg[u] + 1 >= dmax or deg[v] + 1 >= dmax:
+            continue
+        ins.add((u, v))
+    arcs = [a for uv in sorted(ins) for a in (uv, uv[::-1])]
+    P.update_batch(st, g, P.EdgeBatch(insertions=arcs))
+    res = P.ranking_result(st)
+    assert P.check_converged(st)
+    same_depth = fresh_to_depth(g, st)
+    np.testing.assert_allclose(st.lower, same_depth.lower, rtol=REL, atol=0)
+    np.testing.assert_allclose(st.upper, same_depth.upper, rtol=REL, atol=0)
+    fres = P.run(P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True), g)
+    assert res.top(100) == fres.top(100)
+    # the oracle on the post-batch arcs agrees on the certified top-100
+    ip, ix = g.csr_arrays()
+    og = O.CSRGraph(65536, ip, ix, symmetric=True)
+    ores = O.run(O.OracleState(og, O.Crit("topk", 1e-6, k=100)), og)
+    assert ores.top(100) == fres.top(100)
