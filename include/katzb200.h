@@ -117,6 +117,18 @@ int kb_graph_create_grid(int device, int64_t n, int64_t split_threshold,
                          int64_t hot_size, kb_graph **out);
 /* the canonical CSR (original ids, rows ascending): n+1 / nnz entries */
 int kb_graph_get_csr(kb_graph *g, int64_t *indptr, int32_t *indices);
+/* Graph.has_arc / validate_batch presence test (graph.py:207-220), batched:
+ * arcs = m (src,dst) int64 pairs, present = m bytes */
+int kb_graph_has_arcs(kb_graph *g, const int64_t *arcs, int64_t m, uint8_t *present);
+/* max out-degree after applying a batch (dynamic.py:151-157), on the device */
+int kb_graph_max_degree_after(kb_graph *g, const int64_t *ins, int64_t n_ins,
+                              const int64_t *dels, int64_t n_dels, int64_t *max_degree);
+/* Graph.out_degrees (graph.py:160-161): n int64 */
+int kb_graph_out_degrees(kb_graph *g, int64_t *out);
+/* Graph.apply_batch (graph.py:201-205) without a state: the device
+ * CSR-with-slack is edited in place (the caller validated the batch) */
+int kb_graph_apply_batch(kb_graph *g, const int64_t *ins, int64_t n_ins,
+                         const int64_t *dels, int64_t n_dels);
 int kb_graph_destroy(kb_graph *g);
 int kb_graph_info_get(const kb_graph *g, kb_graph_info *info);
 /* Graph.is_symmetric (graph.py:168-175), evaluated on the device */

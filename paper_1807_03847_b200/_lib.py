@@ -69,6 +69,10 @@ SIGNATURES = {
                                    ctypes.POINTER(vp)]),
     "kb_graph_create_grid": (i32, [i32, i64, i64, i64, ctypes.POINTER(vp)]),
     "kb_graph_get_csr": (i32, [vp, vp, vp]),
+    "kb_graph_has_arcs": (i32, [vp, vp, i64, vp]),
+    "kb_graph_max_degree_after": (i32, [vp, vp, i64, vp, i64, ctypes.POINTER(i64)]),
+    "kb_graph_out_degrees": (i32, [vp, vp]),
+    "kb_graph_apply_batch": (i32, [vp, vp, i64, vp, i64]),
     "kb_graph_destroy": (i32, [vp]),
     "kb_graph_info_get": (i32, [vp, ctypes.POINTER(GraphInfo)]),
     "kb_graph_is_symmetric": (i32, [vp, ctypes.POINTER(i32)]),

@@ -275,6 +275,49 @@ int kb_graph_get_csr(kb_graph *h, int64_t *indptr, int32_t *indices) {
     });
 }
 
+int kb_graph_has_arcs(kb_graph *h, const int64_t *arcs, int64_t m, uint8_t *present) {
+    return guarded([&] {
+        KB_REQUIRE(h && (m == 0 || (arcs && present)), KB_EPARAM, "NULL argument");
+        Graph &g = h->g;
+        for (int64_t i = 0; i < 2 * m; i++)
+            KB_REQUIRE(arcs[i] >= 0 && arcs[i] < g.n, KB_ENODERANGE, "node id outside graph");
+        use_device(g.device);
+        graph_has_arcs(g, arcs, m, present);
+    });
+}
+
+int kb_graph_max_degree_after(kb_graph *h, const int64_t *ins, int64_t n_ins,
+                              const int64_t *dels, int64_t n_dels, int64_t *out) {
+    return guarded([&] {
+        KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
+        use_device(h->g.device);
+        *out = graph_max_degree_after(h->g, ins, n_ins, dels, n_dels);
+    });
+}
+
+int kb_graph_out_degrees(kb_graph *h, int64_t *out) {
+    return guarded([&] {
+        KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
+        use_device(h->g.device);
+        graph_out_degrees(h->g, out);
+    });
+}
+
+int kb_graph_apply_batch(kb_graph *h, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                         int64_t n_dels) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL graph");
+        Graph &g = h->g;
+        for (int64_t i = 0; i < 2 * n_ins; i++)
+            KB_REQUIRE(ins[i] >= 0 && ins[i] < g.n, KB_ENODERANGE, "node id outside graph");
+        for (int64_t i = 0; i < 2 * n_dels; i++)
+            KB_REQUIRE(dels[i] >= 0 && dels[i] < g.n, KB_ENODERANGE, "node id outside graph");
+        use_device(g.device);
+        apply_batch_to_graph(g, ins, n_ins, dels, n_dels);
+        g.symmetric = -1;
+    });
+}
+
 int kb_graph_destroy(kb_graph *h) {
     return guarded([&] {
         if (!h) return;

@@ -331,7 +331,96 @@ __global__ void k_reactivate_flags(const int32_t *iperm, int64_t n, const unsign
     flag[o] = !inact[v] && upper[v] >= floor;
 }
 
+__global__ void k_has_arcs(const int64_t *arcs, int64_t m, const int64_t *indptr,
+                           const int32_t *rlen, const int32_t *indices, unsigned char *present) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t u = arcs[2 * i], v = arcs[2 * i + 1];
+    const int32_t *row = indices + indptr[u];
+    const int64_t L = rlen[u];
+    const int64_t p = lower_bound32(row, L, (int32_t)v);
+    present[i] = p < L && row[p] == v;
+}
+
+__global__ void k_deg_delta(const int64_t *arcs, int64_t m, int delta, int32_t *deg) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) atomicAdd(&deg[arcs[2 * i]], delta);
+}
+
+__global__ void k_max_i32(const int32_t *a, int64_t n, unsigned long long *out) {
+    typedef cub::BlockReduce<int, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    int m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, a[i]);
+    m = Red(tmp).Reduce(m, cub::Max());
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)m);
+}
+
+__global__ void k_widen_i32(const int32_t *a, int64_t n, int64_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = a[i];
+}
+
 }  // namespace
+
+void graph_has_arcs(Graph &g, const int64_t *h_arcs, int64_t m, unsigned char *h_present) {
+    cudaStream_t st = g.stream;
+    if (m <= 0) return;
+    DBuf<int64_t> a;
+    DBuf<unsigned char> pr;
+    a.alloc(2 * m);
+    pr.alloc(m);
+    KB_CUDA(cudaMemcpyAsync(a.p, h_arcs, 2 * m * 8, cudaMemcpyHostToDevice, st));
+    k_has_arcs<<<nblk(m, 256), 256, 0, st>>>(a.p, m, g.indptr.p, g.rlen.p, g.indices.p, pr.p);
+    note_launch();
+    KB_CUDA(cudaMemcpyAsync(h_present, pr.p, m, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+}
+
+int64_t graph_max_degree_after(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                               int64_t n_dels) {
+    cudaStream_t st = g.stream;
+    DBuf<int32_t> deg;
+    DBuf<int64_t> a;
+    DBuf<unsigned long long> mx;
+    deg.alloc(g.n);
+    mx.alloc(1);
+    KB_CUDA(cudaMemcpyAsync(deg.p, g.rlen.p, g.n * 4, cudaMemcpyDeviceToDevice, st));
+    KB_CUDA(cudaMemsetAsync(mx.p, 0, 8, st));
+    const int64_t m = std::max(n_ins, n_dels);
+    a.alloc(std::max<int64_t>(1, 2 * m));
+    if (n_ins) {
+        KB_CUDA(cudaMemcpyAsync(a.p, ins, 2 * n_ins * 8, cudaMemcpyHostToDevice, st));
+        k_deg_delta<<<nblk(n_ins, 256), 256, 0, st>>>(a.p, n_ins, 1, deg.p);
+        note_launch();
+    }
+    if (n_dels) {
+        KB_CUDA(cudaStreamSynchronize(st));
+        KB_CUDA(cudaMemcpyAsync(a.p, dels, 2 * n_dels * 8, cudaMemcpyHostToDevice, st));
+        k_deg_delta<<<nblk(n_dels, 256), 256, 0, st>>>(a.p, n_dels, -1, deg.p);
+        note_launch();
+    }
+    if (g.n) {
+        k_max_i32<<<2 * std::max(1, g.sm_count), 256, 0, st>>>(deg.p, g.n, mx.p);
+        note_launch();
+    }
+    unsigned long long h = 0;
+    KB_CUDA(cudaMemcpyAsync(&h, mx.p, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    return (int64_t)h;
+}
+
+void graph_out_degrees(Graph &g, int64_t *h_out) {
+    cudaStream_t st = g.stream;
+    DBuf<int64_t> w;
+    w.alloc(std::max<int64_t>(1, g.n));
+    if (g.n) k_widen_i32<<<nblk(g.n, 256), 256, 0, st>>>(g.rlen.p, g.n, w.p);
+    note_launch();
+    KB_CUDA(cudaMemcpyAsync(h_out, w.p, g.n * 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+}
 
 void compact_csr(Graph &g, DBuf<int64_t> &ip, DBuf<int32_t> &ix) {
     cudaStream_t st = g.stream;

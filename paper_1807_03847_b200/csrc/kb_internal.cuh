@@ -181,6 +181,12 @@ void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices);
 void build_graph_device(Graph &g);
 void build_sell(Graph &g, bool fresh);
 void compact_csr(Graph &g, DBuf<int64_t> &indptr, DBuf<int32_t> &indices);
+void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                          int64_t n_dels);
+void graph_has_arcs(Graph &g, const int64_t *arcs, int64_t m, unsigned char *present);
+int64_t graph_max_degree_after(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                               int64_t n_dels);
+void graph_out_degrees(Graph &g, int64_t *out);
 void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                   int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats);
 void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], double a,

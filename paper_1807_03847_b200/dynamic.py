@@ -58,7 +58,8 @@ def update_batch(state: KatzState, g, batch: EdgeBatch, *, theta: float = 0.5) -
         raise ParameterError(
             "state is in undirected mode; batch must contain both "
             "directions of every edge")
-    new_max = _post_batch_max_degree(g, batch)
+    new_max = (g.max_degree_after(batch) if hasattr(g, "max_degree_after")
+               else _post_batch_max_degree(g, batch))
     if new_max > 0 and state.alpha >= 1.0 / new_max:
         raise ParameterError(
             f"batch raises max out-degree to {new_max}; alpha={state.alpha} "
@@ -75,13 +76,19 @@ def update_batch(state: KatzState, g, batch: EdgeBatch, *, theta: float = 0.5) -
     # the host graph follows the device (deletions then insertions,
     # dynamic.py:170, :199) whether or not the resume converged
     if st in (_lib.KB_OK, _lib.KB_ECONVERGENCE):
-        g.remove_arcs(batch.deletions, _validated=True)
-        g.insert_arcs(batch.insertions, _validated=True)
+        if hasattr(g, "_note_device_update"):
+            g._note_device_update()          # the device copy is the graph
+        else:
+            g.remove_arcs(batch.deletions, _validated=True)
+            g.insert_arcs(batch.insertions, _validated=True)
         state.graph_version = g.version
         state.set_gamma(new_gamma)
         dg = state.device_graph
         if hasattr(g, "_device"):
             g._device = (g.version, dg)
+        else:
+            from .engine import _FOREIGN_CACHE
+            _FOREIGN_CACHE.insert(0, (g, g.version, dg))
         stats = UpdateStats(
             batch_size=int(stats_c.batch_size), seeds=int(stats_c.seeds),
             visited=int(stats_c.visited),

@@ -14,29 +14,83 @@ import numpy as np
 
 from . import _lib
 from .engine import DeviceGraph
-from .errors import ParameterError
+from .errors import BatchPreconditionError, NodeRangeError, ParameterError
+from .graph import EdgeBatch
 
 
 class DeviceResidentGraph:
-    """node_count / version / max_out_degree() / is_symmetric() / out_csr()
-    over a device graph (graph.py:80-255 surface, read-only)."""
+    """A graph whose arcs live only in HBM, with the reference's Graph surface
+    (graph.py:80-255): node_count, arc_count, version, has_arc, out_degrees,
+    max_out_degree, is_symmetric, out_csr, in_neighbors, validate_batch,
+    insert_arcs, remove_arcs, apply_batch.  Mutations edit the device
+    CSR-with-slack in place; nothing is mirrored on the host."""
 
     def __init__(self, dg: DeviceGraph):
         self._dg = dg
         info = dg.info()
         self.node_count = int(info.n)
-        self.arc_count = int(info.nnz)
-        self._max = int(info.max_out_degree)
-        self.version = 1
-        self._device = (self.version, dg)
+        self._version = 1
+        self._device = (self._version, dg)
+        self._csr = None
+
+    @property
+    def version(self) -> int:
+        return self._version
+
+    def _bump(self):
+        self._version += 1
+        self._device = (self._version, self._dg)
         self._csr = None
 
     @property
     def device_graph(self) -> DeviceGraph:
         return self._dg
 
+    @property
+    def arc_count(self) -> int:
+        return int(self._dg.info().nnz)
+
+    def _check_node(self, v: int) -> None:
+        if not 0 <= v < self.node_count:
+            raise NodeRangeError(f"node id {v} outside universe [0, {self.node_count})")
+
+    def _arcs(self, arcs) -> np.ndarray:
+        a = np.ascontiguousarray(np.asarray(arcs, dtype=np.int64).reshape(-1, 2))
+        if a.size:
+            bad = (a < 0) | (a >= self.node_count)
+            if bad.any():
+                self._check_node(int(a[bad][0]))
+        return a
+
+    def _present(self, a: np.ndarray) -> np.ndarray:
+        out = np.zeros(a.shape[0], dtype=np.uint8)
+        if a.shape[0]:
+            _lib.check(_lib.lib().kb_graph_has_arcs(self._dg.handle, _lib.ptr(a), a.shape[0],
+                                                    _lib.ptr(out)))
+        return out.astype(bool)
+
+    def has_arc(self, u: int, v: int) -> bool:
+        self._check_node(u)
+        self._check_node(v)
+        return bool(self._present(self._arcs([(u, v)]))[0])
+
     def max_out_degree(self) -> int:
-        return self._max
+        return self.max_degree_after(EdgeBatch())
+
+    def max_degree_after(self, batch: EdgeBatch) -> int:
+        """dynamic.py:151-157 evaluated on the device."""
+        i = self._arcs(batch.insertions)
+        d = self._arcs(batch.deletions)
+        out = ctypes.c_int64()
+        _lib.check(_lib.lib().kb_graph_max_degree_after(self._dg.handle, _lib.ptr(i), i.shape[0],
+                                                        _lib.ptr(d), d.shape[0],
+                                                        ctypes.byref(out)))
+        return int(out.value)
+
+    def out_degrees(self) -> np.ndarray:
+        out = np.empty(self.node_count, dtype=np.int64)
+        _lib.check(_lib.lib().kb_graph_out_degrees(self._dg.handle, _lib.ptr(out)))
+        return out
 
     def is_symmetric(self) -> bool:
         return self._dg.is_symmetric()
@@ -50,14 +104,69 @@ class DeviceResidentGraph:
             self._csr = (indptr, indices)
         return self._csr
 
-    def out_degrees(self) -> np.ndarray:
-        return np.diff(self.csr_arrays()[0])
+    def out_neighbors(self, v: int):
+        self._check_node(v)
+        ip, ix = self.csr_arrays()
+        return iter(ix[ip[v]:ip[v + 1]].tolist())
+
+    def in_neighbors(self, v: int):
+        self._check_node(v)
+        ip, ix = self.csr_arrays()
+        rows = np.repeat(np.arange(self.node_count), np.diff(ip))
+        return iter(rows[ix == v].tolist())
+
+    def arcs(self):
+        ip, ix = self.csr_arrays()
+        for u in range(self.node_count):
+            for v in ix[ip[u]:ip[u + 1]].tolist():
+                yield (u, v)
 
     def out_csr(self):
         from scipy import sparse
         ip, ix = self.csr_arrays()
         return sparse.csr_matrix((np.ones(ix.size), ix, ip),
                                  shape=(self.node_count, self.node_count))
+
+    # ---- mutation (graph.py:201-237)
+    def validate_batch(self, batch: EdgeBatch) -> None:
+        batch.validate_shape()
+        i = self._arcs(batch.insertions)
+        d = self._arcs(batch.deletions)
+        pi, pd = self._present(i), self._present(d)
+        if pi.any():
+            u, v = batch.insertions[int(np.argmax(pi))]
+            raise BatchPreconditionError(f"cannot insert arc ({u}, {v}): already present")
+        if not pd.all():
+            u, v = batch.deletions[int(np.argmin(pd))]
+            raise BatchPreconditionError(f"cannot delete arc ({u}, {v}): not present")
+
+    def _apply(self, ins, dels):
+        i, d = self._arcs(ins), self._arcs(dels)
+        _lib.check(_lib.lib().kb_graph_apply_batch(self._dg.handle, _lib.ptr(i), i.shape[0],
+                                                   _lib.ptr(d), d.shape[0]))
+
+    def apply_batch(self, batch: EdgeBatch) -> None:
+        self.validate_batch(batch)
+        self.remove_arcs(batch.deletions, _validated=True)
+        self.insert_arcs(batch.insertions, _validated=True)
+
+    def insert_arcs(self, arcs, _validated: bool = False) -> None:
+        if not _validated:
+            self.validate_batch(EdgeBatch(insertions=list(arcs)))
+        self._apply(arcs, [])
+        self._bump()
+
+    def remove_arcs(self, arcs, _validated: bool = False) -> None:
+        if not _validated:
+            self.validate_batch(EdgeBatch(deletions=list(arcs)))
+        self._apply([], arcs)
+        self._bump()
+
+    def _note_device_update(self) -> None:
+        """update_batch already edited the device arcs: deletions then
+        insertions, two version bumps (dynamic.py:170, :199)."""
+        self._bump()
+        self._bump()
 
 
 def _wrap(h, device) -> DeviceGraph:

@@ -267,8 +267,8 @@ class Graph:
         if not _validated:
             self.validate_batch(EdgeBatch(insertions=list(arcs)))
         if len(arcs):
-            k = np.array([u * self._n + v for u, v in arcs], dtype=np.int64)
-            self._keys = np.union1d(self._keys, k)
+            k = np.sort(np.array([u * self._n + v for u, v in arcs], dtype=np.int64))
+            self._keys = np.insert(self._keys, np.searchsorted(self._keys, k), k)
         self._version += 1
 
     def remove_arcs(self, arcs: Sequence[Arc], _validated: bool = False) -> None:
@@ -276,7 +276,7 @@ class Graph:
             self.validate_batch(EdgeBatch(deletions=list(arcs)))
         if len(arcs):
             k = np.array([u * self._n + v for u, v in arcs], dtype=np.int64)
-            self._keys = np.setdiff1d(self._keys, k, assume_unique=True)
+            self._keys = np.delete(self._keys, np.searchsorted(self._keys, k))
         self._version += 1
 
     def __repr__(self) -> str:
