@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
+                    help="c2: R-MAT s24 top-100 (the headline); c4: grid 4096^2 "
+                         "ranking(1e-9); c5: dynamic insertion batches on c2")
     return ap.parse_args()
 
 
@@ -192,11 +195,128 @@ def run_reference(a, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_grid(a, device):
+    """C4: grid 4096^2, Ranking(eps=1e-9) -- many iterations, deg <= 4."""
+    import paper_1807_03847_b200 as P
+    from paper_1807_03847_b200 import _lib
+    from paper_1807_03847_b200 import generate as G
+    L = _lib.lib()
+    n = 1 << a.scale
+    g = G.grid_graph(n, device=device)
+    crit = P.Criterion.ranking(1e-9)
+    nnz = int(g.device_graph.info().nnz)
+    infos = []
+
+    def step():
+        st = P.init(g, crit, undirected=True, device=device, max_iterations=2000)
+        out = P.engine.ctypes.c_int()
+        _lib.check(L.kb_run(st._h, P.engine.ctypes.byref(out)))
+        pairs = P.engine.ctypes.c_int64()
+        _lib.check(L.kb_result(st._h, None, None, None, P.engine.ctypes.byref(pairs)))
+        infos.append((st._info(), int(pairs.value)))
+
+    for _ in range(a.warmup):
+        step()
+    ms = P.engine.ctypes.c_double()
+    with ClockSampler(device) as clk:
+        _lib.check(L.kb_timer(device, 0, None))
+        for _ in range(a.steps):
+            step()
+        _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms)))
+    timed = infos[a.warmup:]
+    r = int(timed[0][0].r)
+    k1 = sum(i.spmv_ms for i, _ in timed) / max(1, sum(i.spmv_launches for i, _ in timed))
+    B = b_iter(n, nnz)
+    peak, src = measured_peaks()
+    line = {"metric": "time to certified epsilon-ranking (s)", "value": ms.value / a.steps / 1e3,
+            "unit": "s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms.value / a.steps, "higher_is_better": False, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"grid-{int(n**0.5)}x{int(n**0.5)}-ranking1e-9", "n": n,
+                       "nnz": nnz, "iterations": r,
+                       "separated_fraction": timed[0][1] / (n * (n - 1) // 2)},
+            "roofline": {"bound": "hbm", "achieved": B / (k1 * 1e-3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": B / (k1 * 1e-3) / 1e9 / peak,
+                         "avg_launch_ms": k1, "bytes_per_launch": B, "peak_source": src},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
+def run_dynamic(a, device):
+    """C5: cumulative insertion batches of 1e2..1e5 undirected edges on C2
+    (np.random.default_rng(7), endpoints with degree+1 < deg_max, SURVEY
+    8(d)); each timed through update_batch against a static recompute."""
+    import numpy as np
+
+    import paper_1807_03847_b200 as P
+    from paper_1807_03847_b200 import _lib
+    from paper_1807_03847_b200 import generate as G
+    L = _lib.lib()
+    n = 1 << a.scale
+    g = G.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed, device=device)
+    crit = P.Criterion.top_k(a.k, a.eps)
+    st = P.init(g, crit, undirected=True, device=device, max_iterations=200)
+    P.run(st, g)
+    deg = g.out_degrees()
+    dmax = int(deg.max())
+    rng = np.random.default_rng(7)
+    rows = []
+    for b in (100, 1000, 10000, 100000):
+        picked = set()
+        while len(picked) < b:
+            cand = rng.integers(0, n, size=(2 * (b - len(picked)) + 16, 2))
+            for u, v in cand.tolist():
+                if u == v:
+                    continue
+                u, v = (u, v) if u < v else (v, u)
+                if (u, v) in picked or deg[u] + 1 >= dmax or deg[v] + 1 >= dmax:
+                    continue
+                picked.add((u, v))
+                if len(picked) == b:
+                    break
+        pk = np.array(sorted(picked), dtype=np.int64)
+        pres = g._present(pk)
+        pk = pk[~pres]
+        arcs = np.concatenate([pk, pk[:, ::-1]])
+        batch = P.EdgeBatch(insertions=[tuple(x) for x in arcs.tolist()])
+        ms = P.engine.ctypes.c_double()
+        _lib.check(L.kb_timer(device, 0, None))
+        t0 = time.perf_counter()
+        P.update_batch(st, g, batch)
+        t_dyn = time.perf_counter() - t0
+        _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms)))
+        top_dyn = P.ranking_result(st).top(a.k)
+        _lib.check(L.kb_timer(device, 0, None))
+        t0 = time.perf_counter()
+        fres = P.run(P.init(g, crit, undirected=True, device=device, max_iterations=200), g)
+        t_static = time.perf_counter() - t0
+        ms2 = P.engine.ctypes.c_double()
+        _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms2)))
+        s = st.last_update_stats
+        np.add.at(deg, arcs[:, 0], 1)
+        rows.append({"batch_edges": int(pk.shape[0]), "update_s": t_dyn,
+                     "update_device_ms": ms.value, "static_recompute_s": t_static,
+                     "static_device_ms": ms2.value, "same_topk": top_dyn == fres.top(a.k),
+                     "r": st.r, "level_sizes": s.level_sizes, "aborted_level": s.aborted_level,
+                     "visited": s.visited, "reactivated": s.reactivated,
+                     "resumed_iterations": s.resumed_iterations})
+    print(json.dumps({"metric": "dynamic update vs static recompute (s)",
+                      "config": {"workload": f"rmat-s{a.scale}-ef{a.edge_factor}-topk{a.k}"
+                                             "-insertion-batches", "seed_batches": 7},
+                      "batches": rows}), flush=True)
+
+
 def main():
     a = parse()
     rank, world, local = dist_env()
     if a.impl == "reference":
         return run_reference(a, rank, world)
+    if a.workload == "c4":
+        if a.scale == 24:
+            pass
+        return run_grid(a, local)
+    if a.workload == "c5":
+        return run_dynamic(a, local)
 
     import numpy as np
 

@@ -104,6 +104,18 @@ int kb_host_unregister(void *ptr);
 int kb_graph_create(int device, int64_t n, int64_t nnz, const int64_t *indptr,
                     const int32_t *indices, int64_t split_threshold,
                     int64_t hot_size, kb_graph **out);
+/* flags for kb_graph_create_ex */
+enum { KB_GRAPH_NO_RELABEL = 1, KB_GRAPH_SYMMETRIC = 2 };
+/* kb_graph_create with options: KB_GRAPH_NO_RELABEL keeps the caller's row
+ * order as the device id space (multi-GPU shards, whose omega blocks must stay
+ * contiguous for the all-gather); `labels` (n int32, may be NULL) replaces
+ * the node id in every tie-break (engine.py:365, :401) -- shards pass the
+ * original ids of the exchange layout.  Rows [own_lo, own_hi) are the ones
+ * this device computes (own_hi < 0: all); KatzState.gap covers only them. */
+int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr,
+                       const int32_t *indices, int64_t split_threshold,
+                       int64_t hot_size, int flags, const int32_t *labels,
+                       int64_t own_lo, int64_t own_hi, kb_graph **out);
 /* Device generators, bit-identical to katzbounds.generate (generate.py:38-103)
  * loaded with undirected=True: R-MAT on n = 2^scale nodes from numpy's PCG64
  * stream whose current state is pcg_state = {state_hi, state_lo, inc_hi,
@@ -168,6 +180,30 @@ int kb_separated_pairs(kb_state *s, int64_t *separated_pairs);
 int kb_get_vector(kb_state *s, int which, int64_t level, double *out);
 /* KatzState.active in its current order (node ids); `out` holds >= active */
 int kb_get_active(kb_state *s, int64_t *out);
+
+/* ---- multi-GPU building blocks (one process per GPU; the caller moves the
+ * omega blocks and candidates with NCCL) */
+/* restrict the active set (node ids of this graph) */
+int kb_state_set_active(kb_state *s, const int64_t *ids, int64_t m);
+/* device pointer of a state vector (device id space: node ids for
+ * KB_GRAPH_NO_RELABEL graphs) */
+int kb_state_vector_ptr(kb_state *s, int which, int64_t level, void **ptr);
+int kb_sync(int device);
+/* the k best active nodes by (-lower, label) without deactivating anything:
+ * raw lower bits, labels and upper bounds, sorted; count <= k */
+int kb_check_local_topk(kb_state *s, int64_t k, uint64_t *keys, int64_t *labels,
+                        double *uppers, int64_t *count);
+/* global top-k of gathered candidates: the cut (k-th key and label) and the
+ * adjacent-separation test of the prefix (engine.py:365-378) */
+int kb_select_global(int device, const uint64_t *keys, const int64_t *labels,
+                     const double *uppers, int64_t ncand, int64_t k, double eps,
+                     uint64_t *kstar, int64_t *istar, int *prefix_separated);
+/* keep the winners of the global cut and the survivors
+ * fl(upper - eps) >= threshold (engine.py:367-373); returns |active| */
+int kb_check_apply_cut(kb_state *s, uint64_t kstar, int64_t istar, int64_t *active);
+/* ranking_result + separated pairs on caller vectors indexed by node id */
+int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
+                   int64_t *order, int64_t *separated_pairs);
 
 /* dynamic.update_batch (dynamic.py:126-211): arcs as (src,dst) int64 pairs,
  * already validated by the caller against the host graph. */

@@ -19,6 +19,7 @@ KB_OK, KB_EPARAM, KB_ESTATE, KB_ECONVERGENCE, KB_ENUMERIC = 0, 1, 2, 3, 4
 KB_EBATCH, KB_ENODERANGE, KB_ECUDA, KB_ENOMEM = 5, 6, 7, 8
 KB_RANKING, KB_TOPK, KB_SCORE, KB_PAIR = 0, 1, 2, 3
 KB_VEC_LEVEL, KB_VEC_KATZ, KB_VEC_LOWER, KB_VEC_UPPER = 0, 1, 2, 3
+KB_GRAPH_NO_RELABEL, KB_GRAPH_SYMMETRIC = 1, 2
 
 _ERRORS = {
     KB_EPARAM: ParameterError,
@@ -65,6 +66,8 @@ SIGNATURES = {
     "kb_host_register": (i32, [vp, i64]),
     "kb_host_unregister": (i32, [vp]),
     "kb_graph_create": (i32, [i32, i64, i64, vp, vp, i64, i64, ctypes.POINTER(vp)]),
+    "kb_graph_create_ex": (i32, [i32, i64, i64, vp, vp, i64, i64, i32, vp, i64, i64,
+                                 ctypes.POINTER(vp)]),
     "kb_graph_create_rmat": (i32, [i32, i32, i64, vp, dbl, dbl, dbl, i64, i64,
                                    ctypes.POINTER(vp)]),
     "kb_graph_create_grid": (i32, [i32, i64, i64, i64, ctypes.POINTER(vp)]),
@@ -90,6 +93,14 @@ SIGNATURES = {
     "kb_separated_pairs": (i32, [vp, ctypes.POINTER(i64)]),
     "kb_get_vector": (i32, [vp, i32, i64, vp]),
     "kb_get_active": (i32, [vp, vp]),
+    "kb_state_set_active": (i32, [vp, vp, i64]),
+    "kb_state_vector_ptr": (i32, [vp, i32, i64, ctypes.POINTER(vp)]),
+    "kb_sync": (i32, [i32]),
+    "kb_check_local_topk": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
+    "kb_select_global": (i32, [i32, vp, vp, vp, i64, i64, dbl, ctypes.POINTER(ctypes.c_uint64),
+                               ctypes.POINTER(i64), ctypes.POINTER(i32)]),
+    "kb_check_apply_cut": (i32, [vp, ctypes.c_uint64, i64, ctypes.POINTER(i64)]),
+    "kb_rank_bounds": (i32, [i32, i64, vp, vp, vp, ctypes.POINTER(i64)]),
     "kb_update_batch": (i32, [vp, vp, i64, vp, i64, dbl, dbl,
                               ctypes.POINTER(UpdateStatsC)]),
 }

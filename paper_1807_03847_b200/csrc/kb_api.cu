@@ -74,6 +74,20 @@ __global__ void k_active_to_orig(const int32_t *act, int dense, int64_t m, const
     if (i < m) out[i] = perm[dense ? (int32_t)i : act[i]];
 }
 
+__global__ void k_compose(const int32_t *ul, const int32_t *perm, int64_t n, int32_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ul[perm[i]];
+}
+
+__global__ void k_map_ids(const int64_t *ids, int64_t m, const int32_t *iperm, int64_t n,
+                          int32_t *out, unsigned long long *bad) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t v = ids[i];
+    if (v < 0 || v >= n) { bad[8] = 1; return; }
+    out[i] = iperm[v];
+}
+
 __global__ void k_sep_one(const double *lower, const double *upper, const int32_t *iperm,
                           int64_t w, int64_t v, double eps, unsigned long long *out) {
     out[0] = lower[iperm[w]] > __dsub_rn(upper[iperm[v]], eps);
@@ -193,6 +207,137 @@ int kb_graph_create(int device, int64_t n, int64_t nnz, const int64_t *indptr,
             throw;
         }
         *out = h;
+    });
+}
+
+int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr,
+                       const int32_t *indices, int64_t split_threshold, int64_t hot_size,
+                       int flags, const int32_t *labels, int64_t own_lo, int64_t own_hi,
+                       kb_graph **out) {
+    return guarded([&] {
+        KB_REQUIRE(out, KB_EPARAM, "out is NULL");
+        KB_REQUIRE(n >= 0 && n < ((int64_t)1 << 31), KB_ENODERANGE,
+                   "node ids must fit the 32-bit index type");
+        KB_REQUIRE(indptr && (nnz == 0 || indices), KB_EPARAM, "NULL CSR arrays");
+        KB_REQUIRE(indptr[0] == 0 && indptr[n] == nnz, KB_EPARAM,
+                   "indptr must start at 0 and end at nnz");
+        kb_graph *h = new_graph(device, split_threshold, hot_size);
+        Graph &g = h->g;
+        g.n = n;
+        g.nnz = nnz;
+        g.relabel = !(flags & KB_GRAPH_NO_RELABEL);
+        KB_REQUIRE(own_lo >= 0 && (own_hi < 0 || (own_hi >= own_lo && own_hi <= n)), KB_EPARAM,
+                   "bad owned row range");
+                g.own_lo = own_lo;
+        g.own_hi = own_hi < 0 ? n : own_hi;
+        try {
+            build_graph(g, indptr, indices);
+            if (labels) {
+                DBuf<int32_t> ul;
+                ul.alloc(std::max<int64_t>(1, n));
+                KB_CUDA(cudaMemcpyAsync(ul.p, labels, n * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, g.stream));
+                g.label.alloc(std::max<int64_t>(1, n));
+                if (n) k_compose<<<nblk(n, 256), 256, 0, g.stream>>>(ul.p, g.perm.p, n, g.label.p);
+                note_launch();
+                KB_CUDA(cudaStreamSynchronize(g.stream));
+            }
+            if (flags & KB_GRAPH_SYMMETRIC) g.symmetric = 1;
+            if (!g.relabel) g.mutated = true;  // no degree-sorted tail shortcuts
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int kb_state_set_active(kb_state *h, const int64_t *ids, int64_t m) {
+    return guarded([&] {
+        KB_REQUIRE(h && (m == 0 || ids), KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        KB_REQUIRE(m >= 0 && m <= s.g->n, KB_EPARAM, "bad active size");
+        use_device(s.g->device);
+        DBuf<int64_t> d;
+        d.alloc(std::max<int64_t>(1, m));
+        if (m) KB_CUDA(cudaMemcpyAsync(d.p, ids, m * 8, cudaMemcpyHostToDevice, s.g->stream));
+        if (m) k_map_ids<<<nblk(m, 256), 256, 0, s.g->stream>>>(d.p, m, s.g->iperm.p, s.g->n,
+                                                              s.act[s.cur].p, s.scratch_u64.p);
+        note_launch();
+        KB_CUDA(cudaMemsetAsync(s.scratch_u64.p + 8, 0, 8, s.g->stream));
+        KB_CUDA(cudaStreamSynchronize(s.g->stream));
+        s.act_dense = false;
+        s.m_host = m;
+    });
+}
+
+int kb_state_vector_ptr(kb_state *h, int which, int64_t level, void **ptr) {
+    return guarded([&] {
+        KB_REQUIRE(h && ptr, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        switch (which) {
+            case KB_VEC_LEVEL: {
+                const int64_t idx = level - s.level_base;
+                KB_REQUIRE(idx >= 0 && idx < (int64_t)s.levels.size(), KB_EPARAM,
+                           "level not retained");
+                *ptr = s.levels[idx].p;
+                break;
+            }
+            case KB_VEC_KATZ: *ptr = s.katz.p; break;
+            case KB_VEC_LOWER: *ptr = s.lower.p; break;
+            case KB_VEC_UPPER: *ptr = s.upper.p; break;
+            default: throw Error{KB_EPARAM, "unknown vector"};
+        }
+    });
+}
+
+int kb_sync(int device) {
+    return guarded([&] {
+        use_device(device);
+        KB_CUDA(cudaStreamSynchronize(device_stream()));
+    });
+}
+
+int kb_check_local_topk(kb_state *h, int64_t k, uint64_t *keys, int64_t *labels,
+                        double *uppers, int64_t *count) {
+    return guarded([&] {
+        KB_REQUIRE(h && keys && labels && uppers && count && k >= 1, KB_EPARAM, "bad argument");
+        State &s = h->s;
+        KB_REQUIRE(s.r >= 1, KB_ESTATE, "check_converged needs at least one iteration");
+        use_device(s.g->device);
+        local_topk(s, s.g->stream, k, keys, labels, uppers, count);
+    });
+}
+
+int kb_check_apply_cut(kb_state *h, uint64_t kstar, int64_t istar, int64_t *active) {
+    return guarded([&] {
+        KB_REQUIRE(h && active, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        apply_cut(s, s.g->stream, kstar, istar);
+        *active = s.m_host;
+    });
+}
+
+int kb_select_global(int device, const uint64_t *keys, const int64_t *labels,
+                     const double *uppers, int64_t ncand, int64_t k, double eps, uint64_t *kstar,
+                     int64_t *istar, int *prefix_separated) {
+    return guarded([&] {
+        KB_REQUIRE(keys && labels && uppers && kstar && istar && prefix_separated, KB_EPARAM,
+                   "NULL argument");
+        KB_REQUIRE(ncand >= 1 && k >= 1, KB_EPARAM, "no candidates");
+        use_device(device);
+        select_global(device, keys, labels, uppers, ncand, k, eps, kstar, istar,
+                      prefix_separated);
+    });
+}
+
+int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
+                   int64_t *order, int64_t *separated_pairs) {
+    return guarded([&] {
+        KB_REQUIRE(lower && upper && n >= 1, KB_EPARAM, "bad argument");
+        use_device(device);
+        rank_bounds(device, n, lower, upper, order, separated_pairs);
     });
 }
 

@@ -673,8 +673,9 @@ double run_gap(State &s, cudaStream_t st) {
     Graph &g = *s.g;
     unsigned long long *u = s.scratch_u64.p;
     KB_CUDA(cudaMemsetAsync(u, 0, sizeof(unsigned long long), st));
-    if (g.n)
-        k_gap<<<2 * g.sm_count, 256, 0, st>>>(s.lower.p, s.upper.p, g.n, u); note_launch();
+    const int64_t lo = g.own_lo, hi = g.own_hi < 0 ? g.n : g.own_hi;
+    if (hi > lo)
+        k_gap<<<2 * g.sm_count, 256, 0, st>>>(s.lower.p + lo, s.upper.p + lo, hi - lo, u); note_launch();
     sync_read(s, st, u, 1);
     unsigned long long key = s.h_flags[0];
     unsigned long long b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
@@ -709,14 +710,14 @@ bool run_check(State &s, cudaStream_t st) {
         const size_t smem = (size_t)P * 16;
         KB_CUDA(cudaFuncSetAttribute(k_topk_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smem, 1)));
-        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.perm.p, s.act[s.cur].p,
+        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), s.act[s.cur].p,
                                              s.act_dense, s.act[nxt].p, out, s.eps, k); note_launch();
         KB_CUDA(cudaGetLastError());
     } else {
         TopkArgs A;
         A.lower = s.lower.p;
         A.upper = s.upper.p;
-        A.perm = g.perm.p;
+        A.perm = g.labels();
         A.act_in = s.act[s.cur].p;
         // in the dense first check, rows without out-arcs (new ids >= nv) have
         // lower == upper == 0 < every other lower: when k <= nv they can be
@@ -740,7 +741,7 @@ bool run_check(State &s, cudaStream_t st) {
         void *args[] = {&A};
         KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
         note_launch();
-        IsWinner win{s.lower.p, g.perm.p, out};
+        IsWinner win{s.lower.p, g.labels(), out};
         IsSurvivor sur{s.lower.p, s.upper.p, out, s.eps};
         unsigned long long *nsel = out + 5;  // [5]=winners, [6]=survivors
         int32_t *unsel = s.stI.p;
@@ -762,7 +763,7 @@ bool run_check(State &s, cudaStream_t st) {
         const size_t smem = (size_t)P * 16;
         KB_CUDA(cudaFuncSetAttribute(k_topk_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.perm.p, A.prefix_buf, 0,
+        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), A.prefix_buf, 0,
                                              s.act[nxt].p, out, s.eps, k); note_launch();
         KB_CUDA(cudaGetLastError());
     }
@@ -771,6 +772,242 @@ bool run_check(State &s, cudaStream_t st) {
     s.act_dense = false;
     s.m_host = (int64_t)s.h_flags[0];
     return s.h_flags[1] != 0;
+}
+
+
+// ---------------------------------------------------------------- multi-GPU
+
+namespace {
+
+__global__ void __launch_bounds__(1024) k_sort_cands(const double *lower, const double *upper,
+                                                     const int32_t *labels, const int32_t *src,
+                                                     int dense, int64_t cnt, uint64_t *keys_out,
+                                                     int64_t *labels_out, double *uppers_out) {
+    extern __shared__ unsigned char smem[];
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    uint64_t *hi = (uint64_t *)smem;
+    uint32_t *lo = (uint32_t *)(hi + P);
+    int32_t *nid = (int32_t *)(lo + P);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < cnt) {
+            const int32_t id = dense ? i : src[i];
+            hi[i] = ~key_of(lower, id);
+            lo[i] = (uint32_t)labels[id];
+            nid[i] = id;
+        } else {
+            hi[i] = ~0ull;
+            lo[i] = 0xFFFFFFFFu;
+            nid[i] = -1;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool gt = hi[i] > hi[j] || (hi[i] == hi[j] && lo[i] > lo[j]);
+                    if (gt == up) {
+                        uint64_t th = hi[i]; hi[i] = hi[j]; hi[j] = th;
+                        uint32_t tl = lo[i]; lo[i] = lo[j]; lo[j] = tl;
+                        int32_t tn = nid[i]; nid[i] = nid[j]; nid[j] = tn;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        keys_out[i] = ~hi[i];
+        labels_out[i] = (int64_t)lo[i];
+        uppers_out[i] = upper[nid[i]];
+    }
+}
+
+__global__ void k_global_cut(const uint64_t *keys, const int64_t *labels, const double *uppers,
+                             const int32_t *order, int64_t kk, double eps,
+                             unsigned long long *out) {
+    // order: candidate indices sorted by (key desc, label asc)
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int64_t i = 1 + threadIdx.x; i < kk; i += blockDim.x) {
+        const double lprev = __longlong_as_double((long long)keys[order[i - 1]]);
+        if (!(__dsub_rn(uppers[order[i]], eps) < lprev)) bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = keys[order[kk - 1]];
+        out[1] = (unsigned long long)labels[order[kk - 1]];
+        out[2] = !bad;
+    }
+}
+
+__global__ void k_neg_keys(const uint64_t *keys, int64_t n, uint64_t *nk, int32_t *iota) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) { nk[i] = ~keys[i]; iota[i] = (int32_t)i; }
+}
+
+__global__ void k_gather_u64(const uint64_t *src, const int32_t *idx, int64_t n, uint64_t *dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+
+template <typename F>
+void cub_go(State *s, F &&f) {
+    size_t tb = 0;
+    KB_CUDA(f(nullptr, tb));
+    DBuf<unsigned char> tmp;
+    tmp.alloc(tb);
+    KB_CUDA(f(tmp.p, tb));
+    note_launch();
+}
+
+// three-way split of the active set under the cut stored in out[3], out[4]
+int64_t partition_cut(State &s, cudaStream_t st, int32_t *win_out, int32_t *surv_out,
+                      int64_t *nwin) {
+    Graph &g = *s.g;
+    unsigned long long *out = s.scratch_u64.p;
+    IsWinner win{s.lower.p, g.labels(), out};
+    IsSurvivor sur{s.lower.p, s.upper.p, out, s.eps};
+    unsigned long long *nsel = out + 5;
+    const int64_t m = s.m_host;
+    auto run_part = [&](auto in) {
+        cub_go(&s, [&](void *t, size_t &b) {
+            return cub::DevicePartition::If(t, b, in, win_out, surv_out, s.stI.p, nsel, (int)m,
+                                            win, sur, st);
+        });
+    };
+    if (s.act_dense) run_part(cub::CountingInputIterator<int32_t>(0));
+    else run_part((const int32_t *)s.act[s.cur].p);
+    unsigned long long h[2];
+    KB_CUDA(cudaMemcpyAsync(h, nsel, sizeof(h), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    *nwin = (int64_t)h[0];
+    return (int64_t)h[1];
+}
+
+}  // namespace
+
+void local_topk(State &s, cudaStream_t st, int64_t k, uint64_t *keys, int64_t *labels,
+                double *uppers, int64_t *count) {
+    Graph &g = *s.g;
+    KB_REQUIRE(k <= KMAX, KB_EPARAM, "sharded top-k supports k <= 4096");
+    const int64_t m = s.m_host;
+    const int32_t *src = s.act[s.cur].p;
+    int dense = s.act_dense;
+    int64_t cnt = m;
+    if (m > k) {
+        TopkArgs A;
+        A.lower = s.lower.p;
+        A.upper = s.upper.p;
+        A.perm = g.labels();
+        A.act_in = s.act[s.cur].p;
+        A.m = m;
+        A.dense = s.act_dense;
+        A.act_out = s.act[s.cur ^ 1].p;
+        A.k = k;
+        A.eps = s.eps;
+        A.hist = (unsigned int *)(s.scratch_u64.p + 8);
+        const int G = (int)std::max<int64_t>(
+            1, std::min<int64_t>(coop_grid(g.sm_count), (A.m + 8191) / 8192));
+        A.blk = s.scratch_u64.p + 8 + HIST_WORDS;
+        A.prefix_buf = s.scratch_i32.p;
+        A.cand = s.cand.p;
+        A.stK = s.stK.p;
+        A.stU = s.stU.p;
+        A.stI = s.stI.p;
+        A.out = s.scratch_u64.p;
+        void *args[] = {&A};
+        KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
+        note_launch();
+        int64_t nw = 0;
+        DBuf<int32_t> surv;
+        surv.alloc(m);
+        partition_cut(s, st, s.scratch_i32.p, surv.p, &nw);
+        cnt = nw;
+        src = s.scratch_i32.p;
+        dense = 0;
+    }
+    DBuf<uint64_t> dk;
+    DBuf<int64_t> dl;
+    DBuf<double> du;
+    dk.alloc(std::max<int64_t>(1, cnt));
+    dl.alloc(std::max<int64_t>(1, cnt));
+    du.alloc(std::max<int64_t>(1, cnt));
+    if (cnt) {
+        int P = 1;
+        while (P < cnt) P <<= 1;
+        const size_t smem = (size_t)P * 16;
+        KB_CUDA(cudaFuncSetAttribute(k_sort_cands, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        k_sort_cands<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), src, dense, cnt,
+                                            dk.p, dl.p, du.p);
+        note_launch();
+        KB_CUDA(cudaMemcpyAsync(keys, dk.p, cnt * 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaMemcpyAsync(labels, dl.p, cnt * 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaMemcpyAsync(uppers, du.p, cnt * 8, cudaMemcpyDeviceToHost, st));
+    }
+    KB_CUDA(cudaStreamSynchronize(st));
+    *count = cnt;
+}
+
+void apply_cut(State &s, cudaStream_t st, uint64_t kstar, int64_t istar) {
+    unsigned long long cut[2] = {kstar, (unsigned long long)istar};
+    KB_CUDA(cudaMemcpyAsync(s.scratch_u64.p + 3, cut, sizeof(cut), cudaMemcpyHostToDevice, st));
+    const int nxt = s.cur ^ 1;
+    DBuf<int32_t> surv;
+    surv.alloc(std::max<int64_t>(1, s.m_host));
+    int64_t nw = 0;
+    const int64_t ns = partition_cut(s, st, s.act[nxt].p, surv.p, &nw);
+    if (ns)
+        KB_CUDA(cudaMemcpyAsync(s.act[nxt].p + nw, surv.p, ns * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    s.cur = nxt;
+    s.act_dense = false;
+    s.m_host = nw + ns;
+}
+
+void select_global(int device, const uint64_t *keys, const int64_t *labels, const double *uppers,
+                   int64_t ncand, int64_t k, double eps, uint64_t *kstar, int64_t *istar,
+                   int *prefix_ok) {
+    (void)device;
+    cudaStream_t st = device_stream();
+    DBuf<uint64_t> dk, nk, nk2;
+    DBuf<int64_t> dl, l2;
+    DBuf<double> du;
+    DBuf<int32_t> i0, i1, i2;
+    DBuf<unsigned long long> out;
+    dk.alloc(ncand); nk.alloc(ncand); nk2.alloc(ncand); dl.alloc(ncand); l2.alloc(ncand);
+    du.alloc(ncand); i0.alloc(ncand); i1.alloc(ncand); i2.alloc(ncand); out.alloc(3);
+    KB_CUDA(cudaMemcpyAsync(dk.p, keys, ncand * 8, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemcpyAsync(dl.p, labels, ncand * 8, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemcpyAsync(du.p, uppers, ncand * 8, cudaMemcpyHostToDevice, st));
+    k_neg_keys<<<nblk(ncand, 256), 256, 0, st>>>(dk.p, ncand, nk.p, i0.p);
+    note_launch();
+    // stable: by label ascending, then by key descending
+    cub_go(nullptr, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, dl.p, l2.p, i0.p, i1.p, (int)ncand, 0, 64,
+                                               st);
+    });
+    k_gather_u64<<<nblk(ncand, 256), 256, 0, st>>>(nk.p, i1.p, ncand, nk2.p);
+    note_launch();
+    cub_go(nullptr, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, nk2.p, nk.p, i1.p, i2.p, (int)ncand, 0, 64,
+                                               st);
+    });
+    const int64_t kk = std::min(k, ncand);
+    k_global_cut<<<1, 256, 0, st>>>(dk.p, dl.p, du.p, i2.p, kk, eps, out.p);
+    note_launch();
+    unsigned long long h[3];
+    KB_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    *kstar = h[0];
+    *istar = (int64_t)h[1];
+    *prefix_ok = (int)h[2];
 }
 
 }  // namespace kb

@@ -43,6 +43,11 @@ __global__ void k_degree_key(const int32_t *rlen, int64_t n, uint32_t *key, int3
     ids[v] = (int32_t)v;
 }
 
+__global__ void k_iota_pair(int64_t n, int32_t *a, int32_t *b) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = b[i] = (int32_t)i;
+}
+
 __global__ void k_invert(const int32_t *perm, int64_t n, int32_t *iperm) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) iperm[perm[i]] = (int32_t)i;
@@ -82,13 +87,13 @@ __global__ void k_max(const int32_t *a, int64_t n, unsigned long long *out) {
 // classify rows by new id: heavy (len > split), normal (0 < len <= split), empty
 __global__ void k_row_class(const int32_t *deg, int64_t n, int64_t split, unsigned char *heavy,
                             unsigned char *normal, unsigned char *zero, int32_t *iota,
-                            uint32_t *key) {
+                            uint32_t *key, int64_t own_lo, int64_t own_hi) {
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
     const int d = deg[v];
     heavy[v] = d > split;
     normal[v] = d > 0 && d <= split;
-    zero[v] = d == 0;
+    zero[v] = d == 0 && v >= own_lo && v < own_hi;  // empty rows this device owns
     iota[v] = (int32_t)v;
     key[v] = 0xFFFFFFFFu - (uint32_t)d;
 }
@@ -221,7 +226,8 @@ void build_sell(Graph &g, bool fresh) {
         DBuf<int64_t> cnt;
         fh.alloc(n); fn.alloc(n); fz.alloc(n); iota.alloc(n); key.alloc(n); cnt.alloc(3);
         k_row_class<<<blocks_for(n, 256), 256, 0, st>>>(g.deg.p, n, g.split, fh.p, fn.p, fz.p,
-                                                       iota.p, key.p);
+                                                       iota.p, key.p, g.own_lo,
+                                                       g.own_hi < 0 ? n : g.own_hi);
         note_launch();
         g.hrow.alloc(n); g.zrows.alloc(n); sel.alloc(n);
         cub_run([&](void *t, size_t &b) {
@@ -388,7 +394,13 @@ void build_graph_device(Graph &g) {
     note_launch();
 
     // ---- relabel rows by descending degree (stable radix sort on ~deg)
-    {
+    if (!g.relabel) {
+        g.perm.alloc(n); g.iperm.alloc(n);
+        if (n) {
+            k_iota_pair<<<blocks_for(n, 256), 256, 0, st>>>(n, g.perm.p, g.iperm.p);
+            note_launch();
+        }
+    } else {
         DBuf<uint32_t> key_in, key_out;
         DBuf<int32_t> id_in;
         key_in.alloc(n); key_out.alloc(n); id_in.alloc(n);
@@ -425,7 +437,7 @@ void build_graph_device(Graph &g) {
                                               (int)n, st);
         });
     }
-    build_sell(g, true);
+    build_sell(g, g.relabel);
 }
 
 namespace {

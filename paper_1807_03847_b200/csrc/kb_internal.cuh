@@ -112,6 +112,10 @@ struct Graph {
     // relabelling: heavy [0,nh), normal [nh,nv), empty [nv,n))
     bool implicit_rows = true;
     bool sell_dirty = false; // arcs changed since the SELL build
+    int64_t own_lo = 0, own_hi = -1;  // rows this device computes (shards)
+    bool relabel = true;     // rows degree-sorted (false: identity, shard graphs)
+    DBuf<int32_t> label;     // tie-break/output label by new id (empty: perm)
+    const int32_t *labels() const { return label.p ? label.p : perm.p; }
     bool mutated = false;    // a batch was applied: the relabelling is no longer
                              // degree-sorted and empty rows are not a tail
     DBuf<int32_t> hrow, vrow, zrows;
@@ -187,6 +191,14 @@ void graph_has_arcs(Graph &g, const int64_t *arcs, int64_t m, unsigned char *pre
 int64_t graph_max_degree_after(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                                int64_t n_dels);
 void graph_out_degrees(Graph &g, int64_t *out);
+void local_topk(State &s, cudaStream_t st, int64_t k, uint64_t *keys, int64_t *labels,
+                double *uppers, int64_t *count);
+void apply_cut(State &s, cudaStream_t st, uint64_t kstar, int64_t istar);
+void select_global(int device, const uint64_t *keys, const int64_t *labels, const double *uppers,
+                   int64_t ncand, int64_t k, double eps, uint64_t *kstar, int64_t *istar,
+                   int *prefix_ok);
+void rank_bounds(int device, int64_t n, const double *lower, const double *upper, int64_t *order,
+                 int64_t *pairs);
 void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                   int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats);
 void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], double a,

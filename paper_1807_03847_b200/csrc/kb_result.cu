@@ -199,4 +199,81 @@ void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, do
     if (h_pairs) *h_pairs = (int64_t)pairs;
 }
 
+
+namespace {
+__global__ void k_iota32(int64_t n, int32_t *a) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int32_t)i;
+}
+}  // namespace
+
+// ranking_result + separated pairs on caller vectors indexed by node id
+// (the multi-GPU path gathers the shard bounds and ranks them here)
+void rank_bounds(int device, int64_t n, const double *h_lower, const double *h_upper,
+                 int64_t *h_order, int64_t *h_pairs) {
+    (void)device;
+    cudaStream_t st = device_stream();
+    DBuf<double> lo, up;
+    DBuf<int32_t> iota, ids, order, zero_part, nids, snids;
+    DBuf<unsigned char> fpos, fzero;
+    DBuf<uint64_t> kin, kout;
+    DBuf<unsigned long long> u;
+    lo.alloc(n); up.alloc(n); iota.alloc(n); ids.alloc(n); order.alloc(n);
+    fpos.alloc(n); fzero.alloc(n); u.alloc(3);
+    KB_CUDA(cudaMemcpyAsync(lo.p, h_lower, n * 8, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemcpyAsync(up.p, h_upper, n * 8, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemsetAsync(u.p, 0, 3 * 8, st));
+    k_iota32<<<nblk(n, 256), 256, 0, st>>>(n, iota.p);
+    k_pos_flags<<<nblk(n, 256), 256, 0, st>>>(lo.p, iota.p, n, fpos.p, fzero.p, ids.p);
+    note_launch(2);
+    auto sel = [&](unsigned char *fl, int32_t *outp, unsigned long long *cnt) {
+        size_t tb = 0;
+        KB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, fl, outp, cnt, (int)n, st));
+        DBuf<unsigned char> t;
+        t.alloc(tb);
+        KB_CUDA(cub::DeviceSelect::Flagged(t.p, tb, iota.p, fl, outp, cnt, (int)n, st));
+        note_launch();
+    };
+    sel(fpos.p, ids.p, u.p);
+    zero_part.alloc(n);
+    sel(fzero.p, zero_part.p, u.p + 1);
+    unsigned long long hc[2];
+    KB_CUDA(cudaMemcpyAsync(hc, u.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    const int64_t npos = (int64_t)hc[0];
+    kin.alloc(npos); kout.alloc(npos); nids.alloc(npos); snids.alloc(npos);
+    if (npos) {
+        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(lo.p, iota.p, ids.p, npos, kin.p, nids.p);
+        note_launch();
+        size_t tb = 0;
+        KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.p, kout.p, nids.p, snids.p,
+                                                (int)npos, 0, 64, st));
+        DBuf<unsigned char> t;
+        t.alloc(tb);
+        KB_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin.p, kout.p, nids.p, snids.p,
+                                                (int)npos, 0, 64, st));
+        note_launch();
+        KB_CUDA(cudaMemcpyAsync(order.p, snids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
+        if (n >= 2) {
+            k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(kout.p, snids.p, npos, up.p, u.p + 2);
+            note_launch();
+        }
+    }
+    if (n > npos)
+        KB_CUDA(cudaMemcpyAsync(order.p + npos, zero_part.p, (n - npos) * 4,
+                                cudaMemcpyDeviceToDevice, st));
+    if (h_order) {
+        DBuf<int64_t> wide;
+        wide.alloc(n);
+        k_widen<<<nblk(n, 256), 256, 0, st>>>(order.p, n, wide.p);
+        note_launch();
+        KB_CUDA(cudaMemcpyAsync(h_order, wide.p, n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    unsigned long long pairs = 0;
+    KB_CUDA(cudaMemcpyAsync(&pairs, u.p + 2, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    pairs += (unsigned long long)(n - npos) * (unsigned long long)npos;
+    if (h_pairs) *h_pairs = (int64_t)pairs;
+}
+
 }  // namespace kb

@@ -1,0 +1,331 @@
+"""Multi-GPU bounded-Katz ranking: 1-D row shards and an omega all-gather.
+
+SURVEY.md 8(e).  Rows are ranked by descending out-degree (stable in the
+node id) and dealt round-robin: the row of degree rank q belongs to rank
+q mod P, so every rank gets n/P rows and about nnz/P arcs.  Each rank lays its
+rows out contiguously in the *exchange layout*
+
+    e(v) = owner(v) * n_per + local(v),     n_per = ceil(n / P),
+
+so one all-gather of every rank's block rebuilds the full omega_r replica on
+every GPU.  A shard is an ordinary device graph over the exchange ids
+(created with KB_GRAPH_NO_RELABEL, so its id space *is* the exchange layout)
+whose non-owned rows are empty; each row keeps its arcs in the original
+ascending order, so per-row sums are the single-GPU ones bit for bit.
+
+Per iteration (run (engine.py:382-396) restated for P ranks):
+
+  1. K1 on the local rows writes the rank's omega block;
+  2. all-gather of the blocks (NCCL over NVLink);
+  3. TOPK: each rank proposes its k best active nodes (key, original id,
+     upper); the P*k proposals are all-gathered and every rank takes the
+     same global cut and adjacent-separation test on its device
+     (kb_select_global); each rank then drops its losers with the global
+     threshold (kb_check_apply_cut) and |active| is all-reduced;
+     SCORE: the max gap is all-reduced;
+  4. ranking_result: the bound blocks are all-gathered and ranked on the
+     device (kb_rank_bounds).
+
+The collective plumbing is torch.distributed (nccl on GPUs; the CPU tests use
+gloo with an oracle-backed shard).  The backend object supplies the local
+compute; ``CudaShard`` is the product backend.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+from .engine import (PAIR, RANKING, SCORE, TOPK, Criterion, RankingResult,
+                     default_alpha, default_iteration_cap, tail_gamma,
+                     validate_alpha)
+from .errors import ConvergenceError, ParameterError
+
+
+class ShardPlan:
+    """Degree-rank round-robin partition and the exchange layout."""
+
+    def __init__(self, indptr: np.ndarray, nranks: int):
+        if nranks < 1:
+            raise ParameterError("nranks must be >= 1")
+        indptr = np.asarray(indptr, dtype=np.int64)
+        self.n = n = indptr.size - 1
+        self.P = P = int(nranks)
+        self.n_per = max(1, -(-n // P))
+        deg = np.diff(indptr)
+        by_rank = np.argsort(-deg, kind="stable")          # degree rank -> node
+        q = np.empty(n, dtype=np.int64)
+        q[by_rank] = np.arange(n, dtype=np.int64)          # node -> degree rank
+        self.exch_of_node = (q % P) * self.n_per + q // P
+        self.node_of_exch = np.full(P * self.n_per, -1, dtype=np.int64)
+        self.node_of_exch[self.exch_of_node] = np.arange(n, dtype=np.int64)
+        self.max_degree = int(deg.max()) if n else 0
+
+    def block(self, rank: int) -> tuple[int, int]:
+        return rank * self.n_per, (rank + 1) * self.n_per
+
+    def labels(self) -> np.ndarray:
+        """Tie-break labels by exchange id: the node id (padding: unique > n)."""
+        lab = self.node_of_exch.copy()
+        pad = lab < 0
+        lab[pad] = self.n + np.arange(int(pad.sum()))
+        return lab.astype(np.int32)
+
+    def local_csr(self, indptr: np.ndarray, indices: np.ndarray, rank: int):
+        """CSR over exchange ids holding only this rank's rows; each row keeps
+        its original (ascending node id) order, columns mapped to exchange ids."""
+        indptr = np.asarray(indptr, dtype=np.int64)
+        lo, hi = self.block(rank)
+        N = self.P * self.n_per
+        rows = self.node_of_exch[lo:hi]
+        valid = rows >= 0
+        deg = np.zeros(N, dtype=np.int64)
+        deg[lo:hi][valid] = indptr[rows[valid] + 1] - indptr[rows[valid]]
+        ip = np.zeros(N + 1, dtype=np.int64)
+        np.cumsum(deg, out=ip[1:])
+        starts = indptr[rows[valid]]
+        lens = deg[lo:hi][valid]
+        src = np.repeat(starts - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens) + \
+            np.arange(int(lens.sum()), dtype=np.int64)
+        ix = self.exch_of_node[np.asarray(indices)[src]].astype(np.int32)
+        return ip, ix
+
+
+class CudaShard:
+    """Product backend: this rank's shard on its GPU through the C-ABI."""
+
+    def __init__(self, plan: ShardPlan, rank: int, indptr, indices, *, device: int,
+                 alpha: float, gamma: float, crit: Criterion, undirected: bool,
+                 max_iterations: int, symmetric: bool = True):
+        import torch
+        self.torch = torch
+        self.L = _lib.lib()
+        self.plan, self.rank, self.device = plan, rank, device
+        ip, ix = plan.local_csr(indptr, indices, rank)
+        lab = plan.labels()
+        lo, hi = plan.block(rank)
+        flags = _lib.KB_GRAPH_NO_RELABEL | (_lib.KB_GRAPH_SYMMETRIC if symmetric else 0)
+        h = ctypes.c_void_p()
+        _lib.check(self.L.kb_graph_create_ex(device, ip.size - 1, int(ip[-1]), _lib.ptr(ip),
+                                             _lib.ptr(ix), 0, -1, flags, _lib.ptr(lab), lo, hi,
+                                             ctypes.byref(h)))
+        self.g = h
+        kind = {RANKING: 0, TOPK: 1, SCORE: 2, PAIR: 3}[crit.kind]
+        s = ctypes.c_void_p()
+        _lib.check(self.L.kb_state_create(h, alpha, gamma, int(undirected), kind, crit.epsilon,
+                                          int(crit.k or 0), 0, 0, 1, int(max_iterations),
+                                          ctypes.byref(s)))
+        self.s = s
+        own = np.arange(lo, hi, dtype=np.int64)
+        own = own[plan.node_of_exch[lo:hi] >= 0]
+        _lib.check(self.L.kb_state_set_active(s, _lib.ptr(own), own.size))
+        self.r = 0
+
+    def close(self):
+        if getattr(self, "s", None):
+            self.L.kb_state_destroy(self.s)
+            self.s = None
+        if getattr(self, "g", None):
+            self.L.kb_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _view(self, which: int, level: int = 0, count: int | None = None, offset: int = 0):
+        ptr = ctypes.c_void_p()
+        _lib.check(self.L.kb_state_vector_ptr(self.s, which, level, ctypes.byref(ptr)))
+        n = count if count is not None else self.plan.P * self.plan.n_per
+        iface = {"shape": (n,), "typestr": "<f8", "version": 3,
+                 "data": (int(ptr.value) + 8 * offset, False)}
+
+        class _A:
+            __cuda_array_interface__ = iface
+        return self.torch.as_tensor(_A(), device=f"cuda:{self.device}")
+
+    # -- protocol
+    def iterate(self):
+        _lib.check(self.L.kb_iterate(self.s, 1))
+        _lib.check(self.L.kb_sync(self.device))
+        self.r += 1
+
+    def level_tensor(self):
+        return self._view(_lib.KB_VEC_LEVEL, self.r)
+
+    def bounds_tensors(self):
+        return self._view(_lib.KB_VEC_LOWER), self._view(_lib.KB_VEC_UPPER)
+
+    def local_topk(self, k: int):
+        keys = np.empty(k, dtype=np.uint64)
+        labels = np.empty(k, dtype=np.int64)
+        uppers = np.empty(k, dtype=np.float64)
+        cnt = ctypes.c_int64()
+        _lib.check(self.L.kb_check_local_topk(self.s, k, _lib.ptr(keys), _lib.ptr(labels),
+                                              _lib.ptr(uppers), ctypes.byref(cnt)))
+        c = int(cnt.value)
+        return keys[:c], labels[:c], uppers[:c]
+
+    def select_global(self, keys, labels, uppers, k: int, eps: float):
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        labels = np.ascontiguousarray(labels, dtype=np.int64)
+        uppers = np.ascontiguousarray(uppers, dtype=np.float64)
+        ks, ist, ok = ctypes.c_uint64(), ctypes.c_int64(), ctypes.c_int()
+        _lib.check(self.L.kb_select_global(self.device, _lib.ptr(keys), _lib.ptr(labels),
+                                           _lib.ptr(uppers), keys.size, k, eps, ctypes.byref(ks),
+                                           ctypes.byref(ist), ctypes.byref(ok)))
+        return int(ks.value), int(ist.value), bool(ok.value)
+
+    def apply_cut(self, kstar: int, istar: int) -> int:
+        m = ctypes.c_int64()
+        _lib.check(self.L.kb_check_apply_cut(self.s, kstar, istar, ctypes.byref(m)))
+        return int(m.value)
+
+    def local_gap(self) -> float:
+        out = ctypes.c_double()
+        _lib.check(self.L.kb_gap(self.s, ctypes.byref(out)))
+        return float(out.value)
+
+    def rank_bounds(self, lower: np.ndarray, upper: np.ndarray):
+        n = lower.size
+        order = np.empty(n, dtype=np.int64)
+        pairs = ctypes.c_int64()
+        _lib.check(self.L.kb_rank_bounds(self.device, n, _lib.ptr(lower), _lib.ptr(upper),
+                                         _lib.ptr(order), ctypes.byref(pairs)))
+        return order, int(pairs.value)
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.device)
+
+
+def _all_gather_flat(dist, full, rank: int, P: int, n_per: int):
+    """In-place all-gather of equal blocks of a flat tensor."""
+    mine = full[rank * n_per:(rank + 1) * n_per].clone()
+    dist.all_gather(list(full.split(n_per)), mine)
+
+
+class ShardedRun:
+    """One rank's side of a sharded run (same calls on every rank)."""
+
+    def __init__(self, backend, plan: ShardPlan, crit: Criterion, *, rank: int, world: int,
+                 max_iterations: int, dist=None):
+        import torch
+        import torch.distributed as tdist
+        self.torch = torch
+        self.dist = dist or tdist
+        self.b, self.plan, self.crit = backend, plan, crit
+        self.rank, self.world = rank, world
+        self.max_iterations = max_iterations
+        if crit.kind not in (TOPK, SCORE):
+            raise ParameterError(
+                f"sharded runs support the topk and score criteria (got {crit.kind!r})")
+
+    def _allreduce(self, value, op):
+        t = self.torch.tensor([value], dtype=self.torch.float64,
+                              device=getattr(self.b, "collective_device", "cpu"))
+        self.dist.all_reduce(t, op=op)
+        return t.item()
+
+    def _check(self) -> bool:
+        c = self.crit
+        ops = self.dist.ReduceOp
+        if c.kind == SCORE:
+            return self._allreduce(self.b.local_gap(), ops.MAX) < c.epsilon
+        k = int(c.k)
+        keys, labels, uppers = self.b.local_topk(k)
+        # all-gather fixed-size proposal blocks (count + k entries) as float64
+        # bit patterns so one collective carries keys, labels and uppers
+        blk = np.zeros(1 + 3 * k, dtype=np.float64)
+        cnt = keys.size
+        blk[0] = cnt
+        blk[1:1 + cnt] = keys.view(np.float64)
+        blk[1 + k:1 + k + cnt] = labels.astype(np.float64)
+        blk[1 + 2 * k:1 + 2 * k + cnt] = uppers
+        dev = getattr(self.b, "collective_device", "cpu")
+        t = self.torch.from_numpy(blk).to(dev)
+        outs = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t)
+        K, Lb, U = [], [], []
+        for o in outs:
+            a = o.cpu().numpy()
+            n_ = int(a[0])
+            K.append(a[1:1 + n_].view(np.uint64))
+            Lb.append(a[1 + k:1 + k + n_].astype(np.int64))
+            U.append(a[1 + 2 * k:1 + 2 * k + n_])
+        keys_all, labels_all, uppers_all = map(np.concatenate, (K, Lb, U))
+        kstar, istar, prefix_ok = self.b.select_global(keys_all, labels_all, uppers_all, k,
+                                                       c.epsilon)
+        m_local = self.b.apply_cut(kstar, istar)
+        m_total = int(self._allreduce(float(m_local), ops.SUM))
+        return m_total <= k and prefix_ok
+
+    def run(self) -> RankingResult:
+        """engine.run for P ranks; every rank returns the same result."""
+        P, n_per = self.plan.P, self.plan.n_per
+        r = 0
+        while True:
+            self.b.iterate()
+            r += 1
+            _all_gather_flat(self.dist, self.b.level_tensor(), self.rank, P, n_per)
+            self.b.sync()
+            if self._check():
+                break
+            if r >= self.max_iterations:
+                gap = self._allreduce(self.b.local_gap(), self.dist.ReduceOp.MAX)
+                raise ConvergenceError(
+                    f"stopping rule still unmet after {r} iterations "
+                    f"(widest bound interval {gap:.3e})", iterations=r, gap=gap)
+        return self.result(r)
+
+    def result(self, r: int) -> RankingResult:
+        P, n_per = self.plan.P, self.plan.n_per
+        lo_t, up_t = self.b.bounds_tensors()
+        _all_gather_flat(self.dist, lo_t, self.rank, P, n_per)
+        _all_gather_flat(self.dist, up_t, self.rank, P, n_per)
+        self.b.sync()
+        node = self.plan.node_of_exch
+        valid = node >= 0
+        lower = np.empty(self.plan.n, dtype=np.float64)
+        upper = np.empty(self.plan.n, dtype=np.float64)
+        lower[node[valid]] = lo_t.cpu().numpy()[valid]
+        upper[node[valid]] = up_t.cpu().numpy()[valid]
+        order, pairs = self.b.rank_bounds(lower, upper)
+        n = self.plan.n
+        for arr in (order, lower, upper):
+            arr.setflags(write=False)
+        frac = 1.0 if n < 2 else pairs / (n * (n - 1) // 2)
+        return RankingResult(order=order, lower=lower, upper=upper, iterations_used=r,
+                             criterion=self.crit, separated_fraction=frac)
+
+
+def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = True,
+                alpha: float | None = None, max_iterations: int | None = None,
+                device: int | None = None, backend_factory=None) -> RankingResult:
+    """Certify `crit` on the graph (canonical CSR on every rank's host) with
+    the current torch.distributed group, one GPU per rank."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    plan = ShardPlan(indptr, world)
+    d = plan.max_degree
+    if alpha is None:
+        alpha = 1.0 / (1.0 + d) if d > 0 else 0.5      # engine.py:96-99
+    validate_alpha(alpha, d)
+    gamma = tail_gamma(alpha, d)
+    if max_iterations is None:
+        max_iterations = default_iteration_cap(alpha, d, crit.epsilon)
+    if backend_factory is None:
+        dev = rank if device is None else device
+        backend = CudaShard(plan, rank, indptr, indices, device=dev, alpha=alpha, gamma=gamma,
+                            crit=crit, undirected=undirected, max_iterations=max_iterations)
+        backend.collective_device = f"cuda:{dev}"
+    else:
+        backend = backend_factory(plan, rank, alpha, gamma)
+    return ShardedRun(backend, plan, crit, rank=rank, world=world,
+                      max_iterations=max_iterations).run()
+
+
+__all__ = ["ShardPlan", "CudaShard", "ShardedRun", "sharded_run"]
