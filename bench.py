@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded multi-GPU path even at one rank")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
                     help="c2: R-MAT s24 top-100 (the headline); c4: grid 4096^2 "
                          "ranking(1e-9); c5: dynamic insertion batches on c2")
@@ -306,6 +308,84 @@ def run_dynamic(a, device):
                       "batches": rows}), flush=True)
 
 
+def run_sharded(a, rank, world, local):
+    """C2 on N GPUs: rows sharded by degree rank, omega all-gathered with NCCL
+    every iteration (paper_1807_03847_b200.distributed).  Strong scaling: the
+    same graph at every N."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1807_03847_b200 as P
+    from paper_1807_03847_b200 import _lib
+    from paper_1807_03847_b200 import distributed as D
+    from paper_1807_03847_b200 import generate as G
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29577")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.lib()
+    n = 1 << a.scale
+    t0 = time.perf_counter()
+    gfull = G.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed, device=local)
+    ip, ix = gfull.csr_arrays()
+    gfull.device_graph.close()
+    plan = D.ShardPlan(ip, world)
+    crit = P.Criterion.top_k(a.k, a.eps)
+    d = plan.max_degree
+    alpha = 1.0 / (1.0 + d)
+    gamma = P.tail_gamma(alpha, d)
+    shard = D.CudaShard(plan, rank, ip, ix, device=local, alpha=alpha, gamma=gamma, crit=crit,
+                        undirected=True, max_iterations=200)
+    shard.collective_device = f"cuda:{local}"
+    nnz = int(ip[-1])
+    del ix
+    t_setup = time.perf_counter() - t0
+
+    def step():
+        shard.reset(alpha=alpha, gamma=gamma, crit=crit, undirected=True, max_iterations=200)
+        return D.ShardedRun(shard, plan, crit, rank=rank, world=world,
+                            max_iterations=200).run()
+
+    for _ in range(a.warmup):
+        res = step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = P.engine.ctypes.c_double()
+    lc0 = P.engine.ctypes.c_int64()
+    _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc0)))
+    with ClockSampler(local) as clk:
+        _lib.check(L.kb_timer(local, 0, None))
+        for _ in range(a.steps):
+            res = step()
+        torch.cuda.synchronize()
+        _lib.check(L.kb_timer(local, 1, P.engine.ctypes.byref(ms)))
+    lc1 = P.engine.ctypes.c_int64()
+    _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc1)))
+    t = torch.tensor([ms.value], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / a.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
+                       "seed": a.seed, "iterations": res.iterations_used,
+                       "parallelism": f"row-shard{world} + NCCL omega all-gather",
+                       "top10": res.top(10)},
+            "gteps_per_iter": nnz * res.iterations_used / (ms_step * 1e-3) / 1e9,
+            "gpu_launches": int(lc1.value - lc0.value), "clocks": clk.summary(),
+            "setup_s": t_setup, "e2e": None, "cpu_baseline": None,
+            "roofline": None}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     a = parse()
     rank, world, local = dist_env()
@@ -317,6 +397,8 @@ def main():
         return run_grid(a, local)
     if a.workload == "c5":
         return run_dynamic(a, local)
+    if world > 1 or a.sharded:
+        return run_sharded(a, rank, world, local)
 
     import numpy as np
 

@@ -154,8 +154,7 @@ void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], do
     KB_REQUIRE(scale >= 1 && scale <= 30, KB_EPARAM, "rmat scale must be in [1, 30]");
     const int64_t n = (int64_t)1 << scale;
     const int64_t m = n * edge_factor;
-    KB_REQUIRE(m < ((int64_t)1 << 31), KB_EPARAM,
-               "rmat: n*edge_factor must stay below 2^31 samples per generation");
+    KB_REQUIRE(m <= ((int64_t)1 << 33), KB_EPARAM, "rmat: n*edge_factor too large");
     const u128 inc = mk(state[2], state[3]);
     u128 JA, JC;
     pcg_jump((u128)m, inc, JA, JC);
@@ -173,12 +172,12 @@ void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], do
     // valid keys are < n*n - 1; the loop sentinel ~0 has all low 2*scale bits
     // set, so sorting only those bits still puts it last
     cub_call([&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, keys.p, keys2.p, (int)m, 0, 2 * scale, st);
+        return cub::DeviceRadixSort::SortKeys(t, b, keys.p, keys2.p, m, 0, 2 * scale, st);
     }, st);
     DBuf<int64_t> cnt;
     cnt.alloc(1);
     cub_call([&](void *t, size_t &b) {
-        return cub::DeviceSelect::Unique(t, b, keys2.p, keys.p, cnt.p, (int)m, st);
+        return cub::DeviceSelect::Unique(t, b, keys2.p, keys.p, cnt.p, m, st);
     }, st);
     int64_t nu = 0;
     KB_CUDA(cudaMemcpyAsync(&nu, cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -196,7 +195,7 @@ void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], do
     DBuf<uint64_t> keys_b;
     keys_b.alloc(ne);
     cub_call([&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, keys2.p, keys_b.p, (int)ne, 0, 2 * scale, st);
+        return cub::DeviceRadixSort::SortKeys(t, b, keys2.p, keys_b.p, ne, 0, 2 * scale, st);
     }, st);
     keys2.release();
     DBuf<int64_t> sa, sb, deg;

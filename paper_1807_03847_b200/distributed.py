@@ -112,14 +112,24 @@ class CudaShard:
                                              _lib.ptr(ix), 0, -1, flags, _lib.ptr(lab), lo, hi,
                                              ctypes.byref(h)))
         self.g = h
+        self.reset(alpha=alpha, gamma=gamma, crit=crit, undirected=undirected,
+                   max_iterations=max_iterations)
+
+    def reset(self, *, alpha: float, gamma: float, crit: Criterion, undirected: bool,
+              max_iterations: int):
+        """A fresh state (engine.init) on the resident shard graph."""
+        if getattr(self, "s", None):
+            self.L.kb_state_destroy(self.s)
+            self.s = None
         kind = {RANKING: 0, TOPK: 1, SCORE: 2, PAIR: 3}[crit.kind]
         s = ctypes.c_void_p()
-        _lib.check(self.L.kb_state_create(h, alpha, gamma, int(undirected), kind, crit.epsilon,
-                                          int(crit.k or 0), 0, 0, 1, int(max_iterations),
-                                          ctypes.byref(s)))
+        _lib.check(self.L.kb_state_create(self.g, alpha, gamma, int(undirected), kind,
+                                          crit.epsilon, int(crit.k or 0), 0, 0, 1,
+                                          int(max_iterations), ctypes.byref(s)))
         self.s = s
+        lo, hi = self.plan.block(self.rank)
         own = np.arange(lo, hi, dtype=np.int64)
-        own = own[plan.node_of_exch[lo:hi] >= 0]
+        own = own[self.plan.node_of_exch[lo:hi] >= 0]
         _lib.check(self.L.kb_state_set_active(s, _lib.ptr(own), own.size))
         self.r = 0
 
