@@ -37,6 +37,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "rmat-s24-ef16-topk100"
+
+
+def workload_name(a):
+    return f"rmat-s{a.scale}-ef{a.edge_factor}-topk{a.k}"
 METRIC = "time to certified top-100 Katz ranking (s); GTEPS/iter; HBM GB/s vs peak"
 
 
@@ -186,7 +190,7 @@ def run_reference(a, rank, world):
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": it * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": n, "nnz": g0.nnz, "k": a.k, "eps": a.eps,
+        "config": {"workload": workload_name(a), "n": n, "nnz": g0.nnz, "k": a.k, "eps": a.eps,
                    "seed": a.seed, "r_assumed": r},
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
                          "sample": f"{a.steps} x (iterate_once+check_converged) on the full "
@@ -236,7 +240,8 @@ def run_grid(a, device):
             "data": "synthetic",
             "config": {"workload": f"grid-{int(n**0.5)}x{int(n**0.5)}-ranking1e-9", "n": n,
                        "nnz": nnz, "iterations": r,
-                       "separated_fraction": timed[0][1] / (n * (n - 1) // 2)},
+                       "separated_fraction": timed[0][1] / (n * (n - 1) // 2),
+                       "full_sort_checks": int(timed[0][0].check_full_sorts)},
             "roofline": {"bound": "hbm", "achieved": B / (k1 * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": B / (k1 * 1e-3) / 1e9 / peak,
                          "avg_launch_ms": k1, "bytes_per_launch": B, "peak_source": src},
@@ -374,7 +379,7 @@ def run_sharded(a, rank, world, local):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
+            "config": {"workload": workload_name(a), "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
                        "seed": a.seed, "iterations": res.iterations_used,
                        "parallelism": f"row-shard{world} + NCCL omega all-gather",
                        "top10": res.top(10)},
@@ -468,7 +473,7 @@ def main():
     achieved = B / (k1_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and a.scale == 24 and a.edge_factor == 16:
         with open(prof) as fh:
             traffic = json.load(fh).get("traffic_bytes_per_launch")
 
@@ -544,8 +549,8 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
-                       "seed": a.seed, "iterations": r,
+            "config": {"workload": workload_name(a), "n": n, "nnz": nnz, "k": a.k,
+                       "eps": a.eps, "seed": a.seed, "iterations": r,
                        "max_out_degree": int(info.max_out_degree),
                        "l2": "inputs larger than L2 (column stream 2.1 GB/iteration)",
                        "parallelism": "replicas" if world > 1 else "single"},

@@ -73,6 +73,7 @@ typedef struct {
     double  last_check_ms;    /* device time of the last kb_check            */
     double  spmv_ms;          /* summed device time of the K1 launches       */
     int64_t spmv_launches;    /* number of K1 iterations timed in spmv_ms    */
+    int64_t check_full_sorts; /* ranking checks that needed the full sort    */
 } kb_state_info;
 
 typedef struct {

@@ -45,7 +45,7 @@ class StateInfo(ctypes.Structure):
     _fields_ = [("r", i64), ("active", i64), ("max_iterations", i64),
                 ("levels_kept", i64), ("alpha", dbl), ("gamma", dbl),
                 ("epsilon", dbl), ("last_check_ms", dbl), ("spmv_ms", dbl),
-                ("spmv_launches", i64)]
+                ("spmv_launches", i64), ("check_full_sorts", i64)]
 
 
 class UpdateStatsC(ctypes.Structure):

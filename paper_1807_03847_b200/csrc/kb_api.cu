@@ -592,6 +592,7 @@ int kb_state_info_get(const kb_state *h, kb_state_info *info) {
         collect_k1_times(const_cast<State &>(s));
         info->spmv_ms = s.spmv_ms;
         info->spmv_launches = s.spmv_launches;
+        info->check_full_sorts = s.check_full_sorts;
     });
 }
 

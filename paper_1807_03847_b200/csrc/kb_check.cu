@@ -552,6 +552,7 @@ void sync_read(State &s, cudaStream_t st, const unsigned long long *dev, int cou
 // TOPK with k > KMAX.
 bool sorted_check(State &s, cudaStream_t st, int64_t k) {
     Graph &g = *s.g;
+    s.check_full_sorts++;
     const int64_t m = s.m_host;
     DBuf<uint32_t> ok_in, ok_out;
     DBuf<int32_t> id_in, id_out;

@@ -168,6 +168,7 @@ struct State {
     size_t k1_used = 0, k1_read = 0;
     double spmv_ms = 0;
     int64_t spmv_launches = 0;
+    int64_t check_full_sorts = 0;   // RANKING checks the certificates could not decide
     const double *x_level() const { return levels.back().p; }
 };
 
