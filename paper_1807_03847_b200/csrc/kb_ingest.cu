@@ -355,6 +355,16 @@ void build_sell(Graph &g, bool fresh) {
     });
     KB_CUDA(cudaMemcpyAsync(&S.elems, S.slice_off.p + S.nslices, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));
+    {   // narrow tail: K1 takes those slices four at a time
+        std::vector<int32_t> hw(S.nslices);
+        if (S.nslices)
+            KB_CUDA(cudaMemcpyAsync(hw.data(), S.slice_w.p, S.nslices * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        int64_t t = S.nslices;
+        while (t > 0 && hw[t - 1] <= 4) t--;
+        S.nwide = t;
+    }
     KB_CUDA(cudaStreamSynchronize(st));
     sz.release();
 

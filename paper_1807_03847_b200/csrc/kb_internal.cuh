@@ -91,6 +91,7 @@ struct Sell {
     DBuf<int32_t> slice_w;
     DBuf<int32_t> vlen;
     int64_t nslices = 0, nvr = 0, nseg = 0, elems = 0;
+    int64_t nwide = 0;  // slices [nwide, nslices) all have width <= 4
 };
 
 struct Graph {

@@ -57,6 +57,7 @@ struct IterArgs {
     const int32_t *slice_w;
     const int32_t *vlen;
     int64_t nslices, nvr, nseg, nh;
+    int64_t nwide;                  // slices >= nwide are narrow: 4 per grab
     const double *x;
     double *w, *katz, *lower, *upper, *seg_sum;
     double alpha, gamma;
@@ -111,6 +112,21 @@ __device__ __forceinline__ void gather8(const double *__restrict__ hot_s, int ho
         v[q] = (jb + q < len) ? fetch<XL>(hot_s, hot, x, c[q]) : 0.0;
 }
 
+// epilogue with katz already loaded (narrow-slice path)
+__device__ __forceinline__ void epilogue_k(const IterArgs &A, int64_t v, double s, double kv) {
+    const double w = __dmul_rn(A.alpha, s);
+    if (A.level_only) {
+        A.w[v] = w;
+        return;
+    }
+    const double k = __dadd_rn(kv, w);
+    const double t = __dmul_rn(A.alpha, w);
+    A.katz[v] = k;
+    A.w[v] = w;
+    st_stream(A.lower + v, A.undirected ? __dadd_rn(k, t) : k);
+    st_stream(A.upper + v, __dadd_rn(k, __dmul_rn(t, A.gamma)));
+}
+
 // Persistent kernel: each warp takes 32-row slices off a global counter.
 // Slices are ordered by descending length so the longest chains start first.
 // DEPTH batches of 8 gathers per lane are kept in flight (software pipeline):
@@ -125,11 +141,59 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     const double *__restrict__ x = A.x;
     const uint64_t pol = evict_first_policy();
     const int4 zero4 = make_int4(0, 0, 0, 0);
+    const int64_t nwide_grabs = A.nwide;
+    const int64_t grabs = A.nwide + (A.nslices - A.nwide + 3) / 4;
     for (;;) {
-        unsigned long long s = 0;
-        if (lane == 0) s = atomicAdd(A.counter, 1ULL);
-        s = __shfl_sync(0xffffffffu, s, 0);
-        if ((int64_t)s >= A.nslices) break;
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(A.counter, 1ULL);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if ((int64_t)c >= grabs) break;
+        if ((int64_t)c >= nwide_grabs) {
+            // four narrow slices (width <= 4) at once: their loads overlap
+            const int64_t s0 = A.nwide + ((int64_t)c - nwide_grabs) * 4;
+            int len[4], w[4];
+            const int32_t *base[4];
+            int64_t row[4];
+            double kz[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int64_t sq = s0 + q;
+                const int64_t vq = sq * 32 + lane;
+                const bool ok = sq < A.nslices && vq < A.nvr;
+                len[q] = ok ? A.vlen[vq] : 0;
+                w[q] = sq < A.nslices ? A.slice_w[sq] : 0;
+                base[q] = A.cols + (sq < A.nslices ? A.slice_off[sq] : 0);
+                row[q] = -1;
+                if (ok && vq >= A.nseg)
+                    row[q] = A.vrow ? A.vrow[vq - A.nseg] : A.nh + (vq - A.nseg);
+                kz[q] = (row[q] >= 0 && !A.level_only) ? A.katz[row[q]] : 0.0;
+            }
+            int32_t cc[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    cc[q][j] = (j < w[q]) ? ld_stream_i1(base[q] + j * 32 + lane, pol) : 0;
+            double v[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    v[q][j] = (j < len[q]) ? fetch<XL>(hot_s, A.hot, x, cc[q][j]) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                double sum = 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; j++) sum = __dadd_rn(sum, v[q][j]);
+                const int64_t vq = (s0 + q) * 32 + lane;
+                if (s0 + q < A.nslices && vq < A.nvr) {
+                    if (vq < A.nseg) A.seg_sum[vq] = sum;
+                    else epilogue_k(A, row[q], sum, kz[q]);
+                }
+            }
+            continue;
+        }
+        const int64_t s = (int64_t)c;
         const int64_t vr = (int64_t)s * 32 + lane;
         const int len = (vr < A.nvr) ? A.vlen[vr] : 0;
         const int w = A.slice_w[s];
@@ -271,6 +335,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     A.nvr = g.sell.nvr;
     A.nseg = g.sell.nseg;
     A.nh = g.nh;
+    A.nwide = tune_get("k1.narrow4", 1) ? g.sell.nwide : g.sell.nslices;
     A.x = x;
     A.w = w;
     A.katz = s.katz.p;
@@ -302,38 +367,40 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
             s.k1_ev.push_back(e);
         }
     }
-    KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used], st));
     const bool ones = !s.levels.empty() && s.level_base == 0 && x == s.levels[0].p &&
                       tune_get("k1.ones_shortcut", 1);
+    // host-side setup first, so the events bracket only device work
+    const int depth = (int)tune_get("k1.depth", 1);
+    const int xl = (int)tune_get("k1.xload", 0);
+    const int threads = (int)tune_get("k1.threads", 1024);
+    const int ctas = (int)tune_get("k1.ctas_per_sm", 1);
+    auto kern = k_sell_iterate<2, 0>;
+    if (depth == 1) kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2> : k_sell_iterate<1, 0>;
+    else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
+    else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
+    static bool attr_done[64][9] = {};
+    const int kid = (depth - 1) * 3 + xl;
+    if (!attr_done[g.device][kid]) {
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr_done[g.device][kid] = true;
+    }
+    const size_t smem = (size_t)A.hot * sizeof(double);
+    if (A.nslices && !ones)
+        KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
+    KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used], st));
     if (A.nslices && ones) {
         k_ones_step<<<(unsigned)((A.nvr + 255) / 256), 256, 0, st>>>(A);
         note_launch();
         KB_CUDA(cudaGetLastError());
-        if (g.nh) {
-            k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
-                A, g.seg_ptr.p, g.seg_list.p); note_launch();
-            KB_CUDA(cudaGetLastError());
-        }
     } else if (A.nslices) {
-        KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
-        const size_t smem = (size_t)A.hot * sizeof(double);
-        const int depth = (int)tune_get("k1.depth", 1);
-        const int xl = (int)tune_get("k1.xload", 0);
-        const int threads = (int)tune_get("k1.threads", 1024);
-        const int ctas = (int)tune_get("k1.ctas_per_sm", 1);
-        auto kern = k_sell_iterate<2, 0>;
-        if (depth == 1) kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2> : k_sell_iterate<1, 0>;
-        else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
-        else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
-        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
         kern<<<g.sm_count * ctas, threads, smem, st>>>(A); note_launch();
         KB_CUDA(cudaGetLastError());
-        if (g.nh) {
-            k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
-                A, g.seg_ptr.p, g.seg_list.p); note_launch();
-            KB_CUDA(cudaGetLastError());
-        }
+    }
+    if (A.nslices && g.nh) {
+        k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
+            A, g.seg_ptr.p, g.seg_list.p); note_launch();
+        KB_CUDA(cudaGetLastError());
     }
     if (!g.implicit_rows && g.nzero) {
         k_zero_rows<<<(unsigned)((g.nzero + 255) / 256), 256, 0, st>>>(
