@@ -393,14 +393,32 @@ __global__ void k_rank_violators(const double *lower, const double *upper, const
     __shared__ int32_t sid[256];
     unsigned long long bk = 0, c = 0;
     int32_t bid = -1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t q = dense ? (int32_t)i : act[i];
-        const double ex = __dsub_rn(__dsub_rn(upper[q], eps), lower[q]);
-        if (!(__dsub_rn(upper[q], eps) < lower[q])) {
-            c++;
-            const unsigned long long k = ord_bits(ex);
-            if (bid < 0 || k > bk || (k == bk && perm[q] < perm[bid])) { bk = k; bid = q; }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < m; i0 += 4 * stride) {
+        int32_t q[4];
+        double lo[4], up[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int64_t i = i0 + t * stride;
+            q[t] = i < m ? (dense ? (int32_t)i : act[i]) : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            lo[t] = q[t] >= 0 ? lower[q[t]] : 0.0;
+            up[t] = q[t] >= 0 ? upper[q[t]] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            if (q[t] < 0) continue;
+            const double um = __dsub_rn(up[t], eps);
+            if (!(um < lo[t])) {
+                c++;
+                const unsigned long long k = ord_bits(__dsub_rn(um, lo[t]));
+                if (bid < 0 || k > bk || (k == bk && perm[q[t]] < perm[bid])) {
+                    bk = k;
+                    bid = q[t];
+                }
+            }
         }
     }
     sk[threadIdx.x] = bk;
@@ -436,8 +454,10 @@ __global__ void k_rank_violators(const double *lower, const double *upper, const
 // we reduce on (lower bits, ~id) with atomicMin over two words via a
 // 128-bit emulation -- done here as per-block arrays + host-free final pass.
 __global__ void k_rank_pred(const double *lower, const int32_t *perm, const int32_t *act,
-                            int dense, int64_t m, const int32_t *cand, int ncand,
+                            int dense, int64_t m, const int32_t *cand, int ncand_max,
+                            const unsigned long long *meta,
                             unsigned long long *pred_key, unsigned int *pred_id) {
+    const int ncand = meta ? (int)min((unsigned long long)ncand_max, *meta) : ncand_max;
     __shared__ uint64_t ck[NCAND];
     __shared__ uint32_t co[NCAND];
     if (threadIdx.x < ncand) {
@@ -448,16 +468,42 @@ __global__ void k_rank_pred(const double *lower, const int32_t *perm, const int3
     uint64_t bk[NCAND];
     uint32_t bo[NCAND];
     for (int c = 0; c < NCAND; c++) { bk[c] = ~0ull; bo[c] = 0; }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t x = dense ? (int32_t)i : act[i];
-        const uint64_t kx = key_of(lower, x);
-        const uint32_t ox = (uint32_t)perm[x];
-        for (int c = 0; c < ncand; c++) {
-            // x ranked before q: kx > kq or (kx == kq and ox < oq)
-            const bool before = kx > ck[c] || (kx == ck[c] && ox < co[c]);
-            // keep the last-ranked such x: smallest kx, then largest ox
-            if (before && (kx < bk[c] || (kx == bk[c] && ox > bo[c]))) { bk[c] = kx; bo[c] = ox; }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < m; i0 += 4 * stride) {
+        int32_t xs[4];
+        uint64_t ks[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int64_t i = i0 + t * stride;
+            xs[t] = i < m ? (dense ? (int32_t)i : act[i]) : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; t++) ks[t] = xs[t] >= 0 ? key_of(lower, xs[t]) : 0;
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            if (xs[t] < 0) continue;
+            const uint64_t kx = ks[t];
+            uint32_t ox = 0;
+            bool have_ox = false;
+            for (int c = 0; c < ncand; c++) {
+                // x ranked before q: kx > kq or (kx == kq and ox < oq); the
+                // label is only read on key ties
+                bool before = kx > ck[c];
+                if (!before && kx == ck[c]) {
+                    if (!have_ox) { ox = (uint32_t)perm[xs[t]]; have_ox = true; }
+                    before = ox < co[c];
+                }
+                if (!before) continue;
+                // keep the last-ranked such x: smallest kx, then largest ox
+                if (kx < bk[c]) {
+                    if (!have_ox) { ox = (uint32_t)perm[xs[t]]; have_ox = true; }
+                    bk[c] = kx;
+                    bo[c] = ox;
+                } else if (kx == bk[c]) {
+                    if (!have_ox) { ox = (uint32_t)perm[xs[t]]; have_ox = true; }
+                    if (ox > bo[c]) bo[c] = ox;
+                }
+            }
         }
     }
     // pack (key, ~id) ordering into a single comparison via two atomics:
@@ -599,68 +645,133 @@ bool sorted_check(State &s, cudaStream_t st, int64_t k) {
     return s.m_host <= k && s.h_flags[0] == 0;
 }
 
+// candidates: the NCAND block winners with the widest excess (ties: the
+// smaller label), chosen identically on the device by NCAND rounds of a
+// block-wide arg-max
+__global__ void __launch_bounds__(256) k_pick_cands(const unsigned long long *blk_key,
+                                                    const int32_t *blk_id, int nb,
+                                                    const int32_t *perm, int32_t *cand,
+                                                    unsigned long long *meta) {
+    __shared__ unsigned long long rk[256];
+    __shared__ int32_t rb[256];
+    __shared__ int32_t chosen[NCAND];
+    int nc = 0;
+    for (int round = 0; round < NCAND; round++) {
+        unsigned long long bk = 0;
+        int32_t bb = -1;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            const int32_t id = blk_id[b];
+            if (id < 0) continue;
+            bool taken = false;
+            for (int t = 0; t < nc; t++) taken |= chosen[t] == b;
+            if (taken) continue;
+            const unsigned long long k = blk_key[b];
+            if (bb < 0 || k > bk || (k == bk && perm[id] < perm[blk_id[bb]])) { bk = k; bb = b; }
+        }
+        rk[threadIdx.x] = bk;
+        rb[threadIdx.x] = bb;
+        __syncthreads();
+        for (int sft = 128; sft > 0; sft >>= 1) {
+            if (threadIdx.x < sft) {
+                const int32_t b2 = rb[threadIdx.x + sft], b1 = rb[threadIdx.x];
+                const unsigned long long k2 = rk[threadIdx.x + sft];
+                if (b2 >= 0 && (b1 < 0 || k2 > rk[threadIdx.x] ||
+                                (k2 == rk[threadIdx.x] && perm[blk_id[b2]] < perm[blk_id[b1]]))) {
+                    rk[threadIdx.x] = k2;
+                    rb[threadIdx.x] = b2;
+                }
+            }
+            __syncthreads();
+        }
+        const int32_t win = rb[0];
+        __syncthreads();
+        if (win < 0) break;
+        if (threadIdx.x == 0) {
+            chosen[nc] = win;
+            cand[nc] = blk_id[win];
+        }
+        nc++;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) meta[0] = (unsigned long long)nc;
+}
+
+// per candidate: the exact predecessor over all blocks, then the verdict
+// out[0]: 0 converged, 1 certified not converged, 2 undecided
+__global__ void __launch_bounds__(256) k_rank_decide(
+    const unsigned long long *count, const unsigned long long *meta, const int32_t *cand,
+    const unsigned long long *pred_key, const unsigned int *pred_id, int nb,
+    const double *upper, double eps, unsigned long long *out) {
+    __shared__ uint64_t rk[256];
+    __shared__ uint32_t ro[256];
+    __shared__ int s_bad, s_ok;
+    const unsigned long long nviol = *count;
+    if (nviol == 0) {
+        if (threadIdx.x == 0) out[0] = 0;
+        return;
+    }
+    const int nc = (int)min((unsigned long long)NCAND, meta[0]);
+    if (threadIdx.x == 0) { s_bad = 0; s_ok = 0; }
+    __syncthreads();
+    for (int c = 0; c < nc; c++) {
+        uint64_t bestk = ~0ull;
+        uint32_t besto = 0;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            const uint64_t k2 = pred_key[(size_t)b * NCAND + c];
+            const uint32_t o2 = pred_id[(size_t)b * NCAND + c];
+            if (k2 < bestk || (k2 == bestk && o2 > besto)) { bestk = k2; besto = o2; }
+        }
+        rk[threadIdx.x] = bestk;
+        ro[threadIdx.x] = besto;
+        __syncthreads();
+        for (int sft = 128; sft > 0; sft >>= 1) {
+            if (threadIdx.x < sft) {
+                const uint64_t k2 = rk[threadIdx.x + sft];
+                const uint32_t o2 = ro[threadIdx.x + sft];
+                if (k2 < rk[threadIdx.x] || (k2 == rk[threadIdx.x] && o2 > ro[threadIdx.x])) {
+                    rk[threadIdx.x] = k2;
+                    ro[threadIdx.x] = o2;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            if (rk[0] == ~0ull) s_ok++;  // q is ranked first
+            else if (!(__dsub_rn(upper[cand[c]], eps) < __longlong_as_double((long long)rk[0])))
+                s_bad = 1;
+            else s_ok++;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        out[0] = s_bad ? 1 : ((unsigned long long)s_ok == nviol ? 0 : 2);
+}
+
 bool check_ranking(State &s, cudaStream_t st) {
     Graph &g = *s.g;
     const int64_t n = s.m_host;
     const int32_t *act = s.act[s.cur].p;
     const int dense = s.act_dense;
-    const int nb = 2 * g.sm_count;
-    unsigned long long *u = s.scratch_u64.p;     // [0]=count, [1..nb] block keys
-    int32_t *ids = s.scratch_i32.p;              // [0..nb) block ids, [nb..nb+8) cands
-    KB_CUDA(cudaMemsetAsync(u, 0, sizeof(unsigned long long), st));
+    const int nb = 16 * g.sm_count;
+    unsigned long long *u = s.scratch_u64.p;   // [0]=count [1]=ncand [2]=verdict [4..) blocks
+    unsigned long long *bkey = u + 4;
+    unsigned long long *pk = bkey + nb;
+    int32_t *ids = s.scratch_i32.p;            // [0..nb) block ids, [nb..nb+8) candidates
+    int32_t *cand = ids + nb;
+    unsigned int *po = (unsigned int *)(cand + NCAND);
+    KB_CUDA(cudaMemsetAsync(u, 0, 4 * sizeof(unsigned long long), st));
     k_rank_violators<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, s.eps,
-                                         u, u + 1, ids); note_launch();
-    // bring the per-block winners back and pick up to NCAND candidates
-    std::vector<unsigned long long> bk(nb + 1);
-    std::vector<int32_t> bid(nb);
-    KB_CUDA(cudaMemcpyAsync(bk.data(), u, (nb + 1) * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaMemcpyAsync(bid.data(), ids, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    const unsigned long long nviol = bk[0];
-    if (nviol == 0) return true;  // every q clears itself, hence its predecessor
-    std::vector<std::pair<unsigned long long, int32_t>> c;
-    for (int b = 0; b < nb; b++)
-        if (bid[b] >= 0) c.push_back({bk[b + 1], bid[b]});
-    std::stable_sort(c.begin(), c.end(), [](auto &a, auto &b) { return a.first > b.first; });
-    if ((int)c.size() > NCAND) c.resize(NCAND);
-    const int nc = (int)c.size();
-    std::vector<int32_t> cand(nc);
-    for (int i = 0; i < nc; i++) cand[i] = c[i].second;
-    KB_CUDA(cudaMemcpyAsync(ids + nb, cand.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice,
-                            st));
-    unsigned long long *pk = u + 1 + nb;
-    unsigned int *po = (unsigned int *)(ids + nb + NCAND);
-    k_rank_pred<<<nb, 256, 0, st>>>(s.lower.p, g.perm.p, act, dense, n, ids + nb, nc, pk, po); note_launch();
-    std::vector<unsigned long long> hpk((size_t)nb * NCAND);
-    std::vector<unsigned int> hpo((size_t)nb * NCAND);
-    std::vector<double> uq(nc);
-    KB_CUDA(cudaMemcpyAsync(hpk.data(), pk, hpk.size() * 8, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaMemcpyAsync(hpo.data(), po, hpo.size() * 4, cudaMemcpyDeviceToHost, st));
-    for (int i = 0; i < nc; i++)
-        KB_CUDA(cudaMemcpyAsync(&uq[i], s.upper.p + cand[i], sizeof(double),
-                                cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    // The comparisons below only *route* between the certificates and the
-    // full device sort; each is the same IEEE subtraction+compare the kernels
-    // perform.
-    unsigned long long resolved_ok = 0;
-    for (int i = 0; i < nc; i++) {
-        uint64_t bestk = ~0ull;
-        uint32_t besto = 0;
-        for (int b = 0; b < nb; b++) {
-            const uint64_t k2 = hpk[(size_t)b * NCAND + i];
-            const uint32_t o2 = hpo[(size_t)b * NCAND + i];
-            if (k2 < bestk || (k2 == bestk && o2 > besto)) { bestk = k2; besto = o2; }
-        }
-        if (bestk == ~0ull) { resolved_ok++; continue; }  // q is ranked first
-        double lp;
-        memcpy(&lp, &bestk, sizeof(double));
-        volatile double diff = uq[i] - s.eps;
-        if (!(diff < lp)) return false;  // certified: q is not separated
-        resolved_ok++;
-    }
-    if (resolved_ok == nviol) return true;  // every violator checked, all fine
+                                         u, bkey, ids);
+    k_pick_cands<<<1, 256, 0, st>>>(bkey, ids, nb, g.perm.p, cand, u + 1);
+    k_rank_pred<<<nb, 256, 0, st>>>(s.lower.p, g.perm.p, act, dense, n, cand, NCAND, u + 1, pk,
+                                    po);
+    k_rank_decide<<<1, 256, 0, st>>>(u, u + 1, cand, pk, po, nb, s.upper.p, s.eps, u + 2);
+    note_launch(4);
+    KB_CUDA(cudaGetLastError());
+    sync_read(s, st, u + 2, 1);
+    const unsigned long long verdict = s.h_flags[0];
+    if (verdict == 0) return true;
+    if (verdict == 1) return false;
     return sorted_check(s, st, g.n);
 }
 
