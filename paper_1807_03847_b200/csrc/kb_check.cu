@@ -385,7 +385,7 @@ __device__ __forceinline__ unsigned long long ord_bits(double d) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void k_rank_violators(const double *lower, const double *upper, const int32_t *perm,
+__global__ void __launch_bounds__(256, 4) k_rank_violators(const double *lower, const double *upper, const int32_t *perm,
                                  const int32_t *act, int dense, int64_t m, double eps,
                                  unsigned long long *count, unsigned long long *blk_key,
                                  int32_t *blk_id) {
@@ -453,20 +453,36 @@ __global__ void k_rank_violators(const double *lower, const double *upper, const
 // Packed into one 64-bit key per block-candidate for a min reduction:
 // we reduce on (lower bits, ~id) with atomicMin over two words via a
 // 128-bit emulation -- done here as per-block arrays + host-free final pass.
-__global__ void k_rank_pred(const double *lower, const int32_t *perm, const int32_t *act,
-                            int dense, int64_t m, const int32_t *cand, int ncand_max,
-                            const unsigned long long *meta,
-                            unsigned long long *pred_key, unsigned int *pred_id) {
+__global__ void __launch_bounds__(256, 4) k_rank_pred(const double *lower, const int32_t *perm,
+                                                     const int32_t *act, int dense, int64_t m,
+                                                     const int32_t *cand, int ncand_max,
+                                                     const unsigned long long *meta,
+                                                     unsigned long long *pred_key,
+                                                     unsigned int *pred_id) {
     const int ncand = meta ? (int)min((unsigned long long)ncand_max, *meta) : ncand_max;
+    // candidates sorted by rank order R = (lower, -label) ascending; sidx maps
+    // back to the caller's candidate slot
     __shared__ uint64_t ck[NCAND];
     __shared__ uint32_t co[NCAND];
-    if (threadIdx.x < ncand) {
-        ck[threadIdx.x] = key_of(lower, cand[threadIdx.x]);
-        co[threadIdx.x] = (uint32_t)perm[cand[threadIdx.x]];
+    __shared__ int sidx[NCAND];
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < ncand; c++) {
+            const uint64_t k = key_of(lower, cand[c]);
+            const uint32_t o = (uint32_t)perm[cand[c]];
+            int p = c;
+            while (p > 0 && (ck[p - 1] > k || (ck[p - 1] == k && co[p - 1] < o))) {
+                ck[p] = ck[p - 1]; co[p] = co[p - 1]; sidx[p] = sidx[p - 1];
+                p--;
+            }
+            ck[p] = k; co[p] = o; sidx[p] = c;
+        }
     }
     __syncthreads();
+    // x can only be the predecessor of the highest-ranked-below candidate:
+    // every candidate is itself an element, so it pre-empts x for the rest
     uint64_t bk[NCAND];
     uint32_t bo[NCAND];
+#pragma unroll
     for (int c = 0; c < NCAND; c++) { bk[c] = ~0ull; bo[c] = 0; }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < m; i0 += 4 * stride) {
@@ -483,42 +499,37 @@ __global__ void k_rank_pred(const double *lower, const int32_t *perm, const int3
         for (int t = 0; t < 4; t++) {
             if (xs[t] < 0) continue;
             const uint64_t kx = ks[t];
+            if (ncand == 0 || kx < ck[0]) continue;   // below every candidate
             uint32_t ox = 0;
-            bool have_ox = false;
-            for (int c = 0; c < ncand; c++) {
-                // x ranked before q: kx > kq or (kx == kq and ox < oq); the
-                // label is only read on key ties
-                bool before = kx > ck[c];
-                if (!before && kx == ck[c]) {
-                    if (!have_ox) { ox = (uint32_t)perm[xs[t]]; have_ox = true; }
-                    before = ox < co[c];
+            bool have = false;
+            int js = -1;
+            for (int j = ncand - 1; j >= 0; j--) {
+                bool before = kx > ck[j];
+                if (!before && kx == ck[j]) {
+                    if (!have) { ox = (uint32_t)perm[xs[t]]; have = true; }
+                    before = ox < co[j];
                 }
-                if (!before) continue;
-                // keep the last-ranked such x: smallest kx, then largest ox
-                if (kx < bk[c]) {
-                    if (!have_ox) { ox = (uint32_t)perm[xs[t]]; have_ox = true; }
-                    bk[c] = kx;
-                    bo[c] = ox;
-                } else if (kx == bk[c]) {
-                    if (!have_ox) { ox = (uint32_t)perm[xs[t]]; have_ox = true; }
-                    if (ox > bo[c]) bo[c] = ox;
-                }
+                if (before) { js = j; break; }
             }
+            if (js < 0) continue;
+            if (!have) { ox = (uint32_t)perm[xs[t]]; have = true; }
+#pragma unroll
+            for (int c = 0; c < NCAND; c++)
+                if (c == js && (kx < bk[c] || (kx == bk[c] && ox > bo[c]))) { bk[c] = kx; bo[c] = ox; }
         }
     }
-    // pack (key, ~id) ordering into a single comparison via two atomics:
-    // first atomicMin on the key, then (after a grid-wide pass) the id.  To
-    // stay single-pass we write per-thread winners to a block reduction.
     __shared__ uint64_t rk[256];
     __shared__ uint32_t ro[256];
-    for (int c = 0; c < ncand; c++) {
+#pragma unroll
+    for (int c = 0; c < NCAND; c++) {
+        if (c >= ncand) break;
         rk[threadIdx.x] = bk[c];
         ro[threadIdx.x] = bo[c];
         __syncthreads();
-        for (int s = 128; s > 0; s >>= 1) {
-            if (threadIdx.x < s) {
-                const uint64_t k2 = rk[threadIdx.x + s];
-                const uint32_t o2 = ro[threadIdx.x + s];
+        for (int sft = 128; sft > 0; sft >>= 1) {
+            if (threadIdx.x < sft) {
+                const uint64_t k2 = rk[threadIdx.x + sft];
+                const uint32_t o2 = ro[threadIdx.x + sft];
                 if (k2 < rk[threadIdx.x] || (k2 == rk[threadIdx.x] && o2 > ro[threadIdx.x])) {
                     rk[threadIdx.x] = k2;
                     ro[threadIdx.x] = o2;
@@ -527,8 +538,8 @@ __global__ void k_rank_pred(const double *lower, const int32_t *perm, const int3
             __syncthreads();
         }
         if (threadIdx.x == 0) {
-            pred_key[blockIdx.x * NCAND + c] = rk[0];
-            pred_id[blockIdx.x * NCAND + c] = ro[0];
+            pred_key[blockIdx.x * NCAND + sidx[c]] = rk[0];
+            pred_id[blockIdx.x * NCAND + sidx[c]] = ro[0];
         }
         __syncthreads();
     }
@@ -752,7 +763,7 @@ bool check_ranking(State &s, cudaStream_t st) {
     const int64_t n = s.m_host;
     const int32_t *act = s.act[s.cur].p;
     const int dense = s.act_dense;
-    const int nb = 16 * g.sm_count;
+    const int nb = 8 * g.sm_count;
     unsigned long long *u = s.scratch_u64.p;   // [0]=count [1]=ncand [2]=verdict [4..) blocks
     unsigned long long *bkey = u + 4;
     unsigned long long *pk = bkey + nb;
