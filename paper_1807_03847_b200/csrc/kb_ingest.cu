@@ -450,39 +450,79 @@ void build_graph_device(Graph &g) {
     build_sell(g, g.relabel);
 }
 
+
 namespace {
-// arc (u, v) needs u in row v; rows are sorted, so a binary search per arc
-__global__ void k_symmetric(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
-                            int64_t n, unsigned long long *bad) {
+__global__ void k_arc_keys_fwd_rev(const int64_t *indptr, const int32_t *rlen,
+                                   const int32_t *indices, int64_t n, const int64_t *cidx,
+                                   int shift, uint64_t *rev) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= n) return;
-    const int64_t u = warp;
-    for (int64_t e = indptr[u] + lane; e < indptr[u] + rlen[u]; e += 32) {
-        const int64_t v = indices[e];
-        int64_t lo = indptr[v], hi = indptr[v] + rlen[v];
-        const int64_t end = hi;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (indices[mid] < u) lo = mid + 1; else hi = mid;
-        }
-        if (lo >= end || indices[lo] != u) { atomicAdd(bad, 1ull); return; }
+    const int64_t base = cidx[warp];
+    for (int64_t j = lane; j < rlen[warp]; j += 32)
+        rev[base + j] = ((uint64_t)(uint32_t)indices[indptr[warp] + j] << shift) | (uint64_t)warp;
+}
+
+// forward key of slot i (rows ascending, columns ascending within a row) vs
+// the i-th smallest reversed key
+__global__ void k_compare_fwd(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
+                              int64_t n, const int64_t *cidx, int shift, const uint64_t *rev,
+                              unsigned long long *bad) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int64_t base = cidx[warp];
+    for (int64_t j = lane; j < rlen[warp]; j += 32) {
+        const uint64_t f = ((uint64_t)warp << shift) | (uint64_t)(uint32_t)indices[indptr[warp] + j];
+        if (rev[base + j] != f) { atomicAdd(bad, 1ull); return; }
     }
+}
+
+__global__ void k_compact_lens(const int32_t *rlen, int64_t n, int64_t *len) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v > n) return;
+    len[v] = v < n ? rlen[v] : 0;
 }
 }  // namespace
 
+// Graph.is_symmetric (graph.py:168-175): the arc set equals its reversal.
+// The forward keys u*2^s+v are already sorted (canonical CSR), so the set is
+// symmetric iff the sorted reversed keys v*2^s+u match them one for one.
 int graph_is_symmetric(Graph &g) {
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n, m = g.nnz;
+    if (m == 0) return 1;
+    int shift = 1;
+    while (((int64_t)1 << shift) < n) shift++;
+    DBuf<int64_t> len, cidx;
+    len.alloc(n + 1);
+    cidx.alloc(n + 1);
+    k_compact_lens<<<blocks_for(n + 1, 256), 256, 0, st>>>(g.rlen.p, n, len.p);
+    note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, len.p, cidx.p, (int)(n + 1), st);
+    });
+    DBuf<uint64_t> rev, srev;
+    rev.alloc(m);
+    srev.alloc(m);
+    k_arc_keys_fwd_rev<<<blocks_for(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p,
+                                                                g.indices.p, n, cidx.p, shift,
+                                                                rev.p);
+    note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, rev.p, srev.p, m, 0, 2 * shift, st);
+    });
+    rev.release();
     DBuf<unsigned long long> bad;
     bad.alloc(1);
-    KB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), g.stream));
-    if (g.n)
-        k_symmetric<<<blocks_for(g.n * 32, 256), 256, 0, g.stream>>>(g.indptr.p, g.rlen.p,
-                                                                      g.indices.p, g.n, bad.p);
+    KB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), st));
+    k_compare_fwd<<<blocks_for(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p, n,
+                                                           cidx.p, shift, srev.p, bad.p);
     note_launch();
     KB_CUDA(cudaGetLastError());
     unsigned long long h = 0;
-    KB_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, g.stream));
-    KB_CUDA(cudaStreamSynchronize(g.stream));
+    KB_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
     return h == 0;
 }
 
