@@ -23,6 +23,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "kb_internal.cuh"
@@ -137,6 +140,11 @@ __global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dp
     for (int64_t j = lane; j < nl; j += 32) indices[indptr[v] + j] = out[j];
     __syncwarp();
     if (lane == 0) rlen[v] = (int32_t)nl;
+}
+
+__global__ void k_scatter_extra(const int32_t *rows, const int32_t *x, int64_t ne, int32_t *dst) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < ne) dst[rows[e]] = x[e];
 }
 
 __global__ void k_gather_len(const int32_t *rlen, const int64_t *indptr, const int32_t *rows,
@@ -301,6 +309,38 @@ __global__ void k_bounds_rows(const int32_t *rows, int64_t m, const double *katz
     upper[v] = __dadd_rn(k, __dmul_rn(t, gamma));            // :187
 }
 
+// u joins the affected set when any of its out-neighbours changed
+__global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
+                              const int32_t *iperm, int64_t n, const unsigned char *chg,
+                              unsigned int *aff_words, unsigned long long *affcount) {
+    int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    const int32_t u = iperm[o];
+    const unsigned bit = 1u << (u & 31);
+    if (aff_words[u >> 5] & bit) return;
+    const int32_t *row = indices + indptr[o];
+    const int32_t L = rlen[o];
+    for (int32_t j = 0; j < L; j++) {
+        if (chg[iperm[row[j]]]) {
+            if (!(atomicOr(&aff_words[u >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
+            return;
+        }
+    }
+}
+
+__global__ void k_diff_changed(const double *old, const double *nw, int64_t n, int32_t *changed,
+                               unsigned long long *count) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    if (__double_as_longlong(old[v]) != __double_as_longlong(nw[v]))
+        changed[atomicAdd(count, 1ull)] = (int32_t)v;
+}
+
+__global__ void k_map_new(const int32_t *orig, int64_t m, const int32_t *iperm, int32_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) out[i] = iperm[orig[i]];
+}
+
 __global__ void k_flags_from_list(const int32_t *list, int64_t m, unsigned char *flag) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < m) flag[list[i]] = 1;
@@ -362,6 +402,23 @@ __global__ void k_widen_i32(const int32_t *a, int64_t n, int64_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = a[i];
 }
+
+struct PhaseTrace {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    cudaStream_t st;
+    explicit PhaseTrace(cudaStream_t s) : on(getenv("KB_TRACE") != nullptr), st(s) {
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[kb] %-28s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 }  // namespace
 
@@ -474,6 +531,7 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
     for (int64_t i = 0; i < n_dels; i++) ed.push_back({(int32_t)dels[2 * i], (int32_t)dels[2 * i + 1], 0});
     for (int64_t i = 0; i < n_ins; i++) ed.push_back({(int32_t)ins[2 * i], (int32_t)ins[2 * i + 1], 1});
     if (ed.empty()) return;
+    PhaseTrace tr(st);
     std::sort(ed.begin(), ed.end(), [](const Edit &a, const Edit &b) {
         return a.src != b.src ? a.src < b.src : (a.kind != b.kind ? a.kind < b.kind : a.dst < b.dst);
     });
@@ -491,6 +549,7 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
         i = j;
     }
     const int64_t ne = (int64_t)rows.size();
+    tr.mark("  host group edits");
     DBuf<int32_t> drows, ddel, dins;
     DBuf<int64_t> ddptr, diptr, lc;
     drows.alloc(ne); ddel.alloc(std::max<size_t>(1, dl.size()));
@@ -515,14 +574,20 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
         if (nl > hlc[2 * e + 1]) overflow = true;
         toff[e + 1] = toff[e] + std::max<int64_t>(nl, hlc[2 * e]);
     }
+    tr.mark("  capacity check");
     if (overflow) {
-        std::vector<int32_t> extra(g.n, 0);
-        for (int64_t e = 0; e < ne; e++) extra[rows[e]] = (int32_t)(iptr[e + 1] - iptr[e]);
-        DBuf<int32_t> dex;
+        std::vector<int32_t> extra(ne);
+        for (int64_t e = 0; e < ne; e++) extra[e] = (int32_t)(iptr[e + 1] - iptr[e]);
+        DBuf<int32_t> dex, dx;
         dex.alloc(g.n);
-        KB_CUDA(cudaMemcpyAsync(dex.p, extra.data(), g.n * 4, cudaMemcpyHostToDevice, st));
+        dx.alloc(ne);
+        KB_CUDA(cudaMemsetAsync(dex.p, 0, g.n * 4, st));
+        KB_CUDA(cudaMemcpyAsync(dx.p, extra.data(), ne * 4, cudaMemcpyHostToDevice, st));
+        k_scatter_extra<<<nblk(ne, 256), 256, 0, st>>>(drows.p, dx.p, ne, dex.p);
+        note_launch();
         respread(g, dex.p);
         KB_CUDA(cudaStreamSynchronize(st));
+        tr.mark("  respread");
     }
     DBuf<int64_t> dtoff;
     DBuf<int32_t> tmp;
@@ -535,8 +600,10 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
     note_launch();
     KB_CUDA(cudaGetLastError());
     KB_CUDA(cudaStreamSynchronize(st));
+    tr.mark("  edit rows");
     g.nnz += n_ins - n_dels;
-    g.sell_dirty = true;
+    patch_sell(g, drows.p, ne);
+    tr.mark("  patch SELL");
     g.mutated = true;
     g.version += 1;
 }
@@ -564,16 +631,31 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     std::sort(targets_o.begin(), targets_o.end());
     targets_o.erase(std::unique(targets_o.begin(), targets_o.end()), targets_o.end());
     st_out.seeds = (int64_t)seeds_o.size();
-    std::vector<int32_t> hiperm(n);
-    KB_CUDA(cudaMemcpyAsync(hiperm.data(), g.iperm.p, n * 4, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
+    // seeds and targets as new ids (mapped on the device)
     std::vector<int32_t> seeds(seeds_o.size()), targets(targets_o.size());
-    for (size_t i = 0; i < seeds_o.size(); i++) seeds[i] = hiperm[seeds_o[i]];
-    for (size_t i = 0; i < targets_o.size(); i++) targets[i] = hiperm[targets_o[i]];
+    {
+        DBuf<int32_t> a, b;
+        const int64_t m1 = (int64_t)seeds_o.size(), m2 = (int64_t)targets_o.size();
+        a.alloc(std::max<int64_t>(1, m1 + m2));
+        b.alloc(std::max<int64_t>(1, m1 + m2));
+        if (m1) KB_CUDA(cudaMemcpyAsync(a.p, seeds_o.data(), m1 * 4, cudaMemcpyHostToDevice, st));
+        if (m2)
+            KB_CUDA(cudaMemcpyAsync(a.p + m1, targets_o.data(), m2 * 4, cudaMemcpyHostToDevice, st));
+        if (m1 + m2) {
+            k_map_new<<<nblk(m1 + m2, 256), 256, 0, st>>>(a.p, m1 + m2, g.iperm.p, b.p);
+            note_launch();
+        }
+        if (m1) KB_CUDA(cudaMemcpyAsync(seeds.data(), b.p, m1 * 4, cudaMemcpyDeviceToHost, st));
+        if (m2)
+            KB_CUDA(cudaMemcpyAsync(targets.data(), b.p + m1, m2 * 4, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    }
 
+    PhaseTrace tr(st);
     // 1. the post-batch arc set on the device
     const bool was_sym = g.symmetric == 1;
     apply_batch_to_graph(g, ins, n_ins, dels, n_dels);
+    tr.mark("apply batch");
     if (!(was_sym && s.undirected)) g.symmetric = -1;
     // in-neighbours: the CSR itself when undirected (symmetric), else a transpose
     DBuf<int64_t> tip;
@@ -609,6 +691,9 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     }
     int64_t affected = ns;
     bool aborted = false;
+    bool all_touched = false;
+    DBuf<unsigned char> chg;
+    chg.alloc(n);
     int64_t nchanged = 0;
     for (int64_t level = 1; level <= s.r; level++) {
         double *w_prev = s.levels[level - 1 - s.level_base].p;
@@ -620,9 +705,37 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             }
             run_spmv(s, st, w_prev, w_cur, true);
             KB_CUDA(cudaStreamSynchronize(st));
+            tr.mark("level (full K1)");
             continue;
         }
         if (st_out.n_level_sizes < 64) st_out.level_sizes[st_out.n_level_sizes++] = affected;
+        if (nchanged > n / 256) {
+            // Dense level: the expansion would reach most rows, so recompute
+            // the whole level with K1 (identical bits for every row) and
+            // find the changed rows by comparison.  The affected set grows by
+            // the in-neighbours of the previous changed rows, found by a pull
+            // over every row's out-arcs (u in N-(v) <=> v in N+(u)).
+            KB_CUDA(cudaMemsetAsync(chg.p, 0, n, st));
+            k_flags_from_list<<<nblk(nchanged, 256), 256, 0, st>>>(C.p, nchanged, chg.p);
+            k_pull_affect<<<nblk(n, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p,
+                                                        g.iperm.p, n, chg.p, aff.p, cnt.p + 2);
+            note_launch(2);
+            DBuf<double> fresh;
+            fresh.alloc(n + 1);
+            run_spmv(s, st, w_prev, fresh.p, true);
+            KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
+            k_diff_changed<<<nblk(n, 256), 256, 0, st>>>(w_cur, fresh.p, n, C.p, cnt.p + 1);
+            note_launch();
+            std::swap(s.levels[level - s.level_base], fresh);
+            unsigned long long hc[3];
+            KB_CUDA(cudaMemcpyAsync(hc, cnt.p, 3 * 8, cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaStreamSynchronize(st));
+            nchanged = (int64_t)hc[1];
+            affected = (int64_t)hc[2];
+            all_touched = true;
+            tr.mark("level (dense repair)");
+            continue;
+        }
         // R_level = seeds U in-neighbours(changed at level-1)
         KB_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * 8, st));
         if (ns) {
@@ -641,6 +754,24 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         KB_CUDA(cudaStreamSynchronize(st));
         const int64_t nr = (int64_t)hc[0];
         affected = (int64_t)hc[2];
+        if (nr > n / 64) {
+            // a wide frontier: one K1 level (same bits) is cheaper than a
+            // warp per row; the changed rows come from the comparison
+            DBuf<double> fresh;
+            fresh.alloc(n + 1);
+            run_spmv(s, st, w_prev, fresh.p, true);
+            KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
+            k_diff_changed<<<nblk(n, 256), 256, 0, st>>>(w_cur, fresh.p, n, C.p, cnt.p + 1);
+            note_launch();
+            std::swap(s.levels[level - s.level_base], fresh);
+            unsigned long long hchg = 0;
+            KB_CUDA(cudaMemcpyAsync(&hchg, cnt.p + 1, 8, cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaStreamSynchronize(st));
+            nchanged = (int64_t)hchg;
+            all_touched = true;
+            tr.mark("level (wide frontier)");
+            continue;
+        }
         // recompute R at this level; the changed list feeds the next level
         KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
         if (nr) {
@@ -653,6 +784,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         KB_CUDA(cudaMemcpyAsync(&hchg, cnt.p + 1, 8, cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaStreamSynchronize(st));
         nchanged = (int64_t)hchg;
+        tr.mark("level (local repair)");
     }
     // visited = |affected U targets| (dynamic.py:176)
     {
@@ -671,6 +803,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         st_out.visited = (int64_t)ha;
     }
 
+    tr.mark("visited count");
     // 3. katz and bounds (dynamic.py:181-187)
     std::vector<const double *> hl(s.r + 1);
     for (int64_t l = 0; l <= s.r; l++) hl[l] = s.levels[l - s.level_base].p;
@@ -681,7 +814,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     const bool gamma_changed = new_gamma != s.gamma;
     s.gamma = new_gamma;
     const double *wr = s.levels[s.r - s.level_base].p;
-    if (aborted) {
+    if (aborted || all_touched) {
         k_katz_rows<<<nblk(n, 256), 256, 0, st>>>(nullptr, n, dl.p, (int)s.r, s.katz.p);
         k_bounds_rows<<<nblk(n, 256), 256, 0, st>>>(nullptr, n, s.katz.p, wr, s.alpha, s.gamma,
                                                     s.undirected, s.lower.p, s.upper.p);
@@ -715,6 +848,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     }
     KB_CUDA(cudaGetLastError());
 
+    tr.mark("katz + bounds");
     // 4. reactivation (dynamic.py:190-197)
     if ((s.kind == KB_RANKING || s.kind == KB_TOPK) && !s.act_dense && s.m_host < n) {
         const int64_t m = s.m_host;
@@ -748,6 +882,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     s.tail_zero_from = n;
     s.graph_version = g.version;
 
+    tr.mark("reactivation");
     // 6. resume (dynamic.py:203-210)
     for (;;) {
         if (run_check(s, st)) break;
@@ -763,6 +898,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         launch_iterate(s, st);
         st_out.resumed_iterations++;
     }
+    tr.mark("resume (checks)");
     *stats = st_out;
 }
 

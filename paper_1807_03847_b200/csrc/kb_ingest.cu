@@ -159,6 +159,57 @@ __global__ void k_fill(const int64_t *indptr, const int32_t *indices, const int3
     }
 }
 
+__global__ void k_rev_normal(const int32_t *vrow, int64_t nh, int64_t nnorm, int64_t nseg,
+                             int32_t *vr_of_row) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nnorm) vr_of_row[vrow ? vrow[i] : nh + i] = (int32_t)(nseg + i);
+}
+
+__global__ void k_rev_heavy(const int32_t *hrow, int64_t nh, int32_t *h_of_row) {
+    int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h < nh) h_of_row[hrow ? hrow[h] : h] = (int32_t)h;
+}
+
+// One thread per edited row (original id): rewrite its SELL lane in place
+// when the new length fits the slice, else turn it into an overflow row
+// (its SELL lane / segments contribute 0 and the overflow pass recomputes it)
+__global__ void k_patch_rows(const int32_t *rows_orig, int64_t ne, const int32_t *iperm,
+                             const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
+                             const int32_t *vr_of_row, const int32_t *h_of_row,
+                             const int32_t *seg_ptr, const int32_t *seg_list,
+                             const int32_t *slice_w, const int64_t *slice_off, int32_t *vlen,
+                             int32_t *cols, int32_t *ovf_flag, int32_t *ovf,
+                             unsigned long long *ovf_count) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const int32_t o = rows_orig[e];
+    const int32_t v = iperm[o];
+    if (ovf_flag[v]) return;  // already recomputed from the canonical CSR
+    const int32_t len = rlen[o];
+    const int32_t vr = vr_of_row[v];
+    if (vr >= 0) {
+        const int64_t s = vr >> 5;
+        const int lane = vr & 31;
+        const int w = slice_w[s];
+        if (len <= w) {
+            int32_t *base = cols + slice_off[s];
+            const int32_t *row = indices + indptr[o];
+            for (int j = 0; j < len; j++) {
+                const int64_t pos = (w <= 4) ? ((int64_t)j * 32 + lane)
+                                             : ((int64_t)(j >> 2) * 128 + lane * 4 + (j & 3));
+                base[pos] = iperm[row[j]];
+            }
+            vlen[vr] = len;
+            return;
+        }
+        vlen[vr] = 0;
+    } else if (h_of_row[v] >= 0) {
+        const int32_t h = h_of_row[v];
+        for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++) vlen[seg_list[q]] = 0;
+    }
+    if (atomicExch(&ovf_flag[v], 1) == 0) ovf[atomicAdd(ovf_count, 1ull)] = v;
+}
+
 __global__ void k_arc_flags(const int32_t *rlen, int64_t n, unsigned char *fl, int32_t *iota) {
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
@@ -379,8 +430,54 @@ void build_sell(Graph &g, bool fresh) {
         note_launch();
         KB_CUDA(cudaGetLastError());
     }
+    // reverse maps for in-place patching by dynamic batches
+    g.vr_of_row.alloc(std::max<int64_t>(1, n));
+    g.h_of_row.alloc(std::max<int64_t>(1, n));
+    KB_CUDA(cudaMemsetAsync(g.vr_of_row.p, 0xff, std::max<int64_t>(1, n) * 4, st));
+    KB_CUDA(cudaMemsetAsync(g.h_of_row.p, 0xff, std::max<int64_t>(1, n) * 4, st));
+    if (g.nv > g.nh) {
+        k_rev_normal<<<blocks_for(g.nv - g.nh, 256), 256, 0, st>>>(g.vrow.p, g.nh, g.nv - g.nh,
+                                                                  S.nseg, g.vr_of_row.p);
+        note_launch();
+    }
+    if (g.nh) {
+        k_rev_heavy<<<blocks_for(g.nh, 256), 256, 0, st>>>(g.hrow.p, g.nh, g.h_of_row.p);
+        note_launch();
+    }
+    g.ovf.release();
+    g.ovf_flag.release();
+    g.n_ovf = 0;
     KB_CUDA(cudaStreamSynchronize(st));
     g.sell_dirty = false;
+}
+
+// Apply the per-row effects of a batch to the SELL layout (after the
+// canonical CSR was edited).  Too many overflow rows -> full rebuild later.
+void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne) {
+    cudaStream_t st = g.stream;
+    if (g.sell_dirty || ne == 0) return;
+    const int64_t n = g.n;
+    if (!g.ovf.p) {
+        g.ovf.alloc(std::max<int64_t>(1, n));
+        g.ovf_flag.alloc(std::max<int64_t>(1, n));
+        g.ovf_count.alloc(1);
+        KB_CUDA(cudaMemsetAsync(g.ovf_flag.p, 0, std::max<int64_t>(1, n) * 4, st));
+        KB_CUDA(cudaMemsetAsync(g.ovf_count.p, 0, 8, st));
+    }
+    Sell &S = g.sell;
+    k_patch_rows<<<blocks_for(ne, 128), 128, 0, st>>>(
+        rows_orig, ne, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p, g.vr_of_row.p,
+        g.h_of_row.p, g.seg_ptr.p, g.seg_list.p, S.slice_w.p, S.slice_off.p, S.vlen.p, S.cols.p,
+        g.ovf_flag.p, g.ovf.p, g.ovf_count.p);
+    note_launch();
+    KB_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    KB_CUDA(cudaMemcpyAsync(&h, g.ovf_count.p, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    g.n_ovf = (int64_t)h;
+    // the overflow pass is a warp per row: past a few percent of the rows a
+    // rebuild of the layout is cheaper
+    if (g.n_ovf > std::max<int64_t>(4096, g.nv / 32)) g.sell_dirty = true;
 }
 
 void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {

@@ -120,6 +120,13 @@ struct Graph {
     bool mutated = false;    // a batch was applied: the relabelling is no longer
                              // degree-sorted and empty rows are not a tail
     DBuf<int32_t> hrow, vrow, zrows;
+    // dynamic patching of the SELL layout: new id -> normal virtual row /
+    // heavy index (-1 if none); rows that no longer fit their slice are
+    // "overflow" rows recomputed from the canonical CSR after K1
+    DBuf<int32_t> vr_of_row, h_of_row;
+    DBuf<int32_t> ovf, ovf_flag;
+    DBuf<unsigned long long> ovf_count;
+    int64_t n_ovf = 0;
     Sell sell;
     // heavy-row combine: segments of heavy row h are seg_list[seg_ptr[h] ..
     // seg_ptr[h+1]) in order (indices into the segment-sum buffer)
@@ -187,6 +194,7 @@ void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices);
 void build_graph_device(Graph &g);
 void build_sell(Graph &g, bool fresh);
 void compact_csr(Graph &g, DBuf<int64_t> &indptr, DBuf<int32_t> &indices);
+void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne);
 void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                           int64_t n_dels);
 void graph_has_arcs(Graph &g, const int64_t *arcs, int64_t m, unsigned char *present);

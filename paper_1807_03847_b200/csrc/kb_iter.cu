@@ -279,6 +279,51 @@ __global__ void k_empty_rows(double *upper, double *lower, const double *katz,
     upper[i] = katz[i];
 }
 
+// Overflow rows (dynamic batches that outgrew their SELL lane): recomputed
+// from the canonical CSR with K1's summation order -- one sequential chain,
+// or split-sized segments combined in order -- after K1 left them at +0.
+// One warp per row.
+__global__ void k_ovf_rows(IterArgs A, const int32_t *rows, int64_t nr, const int32_t *perm,
+                           const int32_t *iperm, const int64_t *indptr, const int32_t *rlen,
+                           const int32_t *indices, int64_t split) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nr) return;
+    const int32_t v = rows[warp];
+    const int32_t o = perm[v];
+    const int32_t *row = indices + indptr[o];
+    const int64_t L = rlen[o];
+    const double *__restrict__ x = A.x;
+    double s = 0.0;
+    if (L <= split) {
+        for (int64_t base = 0; base < L; base += 32) {
+            const int64_t j = base + lane;
+            const double val = j < L ? x[iperm[row[j]]] : 0.0;
+            const int cnt = (int)min((int64_t)32, L - base);
+            for (int q = 0; q < cnt; q++) {
+                const double t = __shfl_sync(0xffffffffu, val, q);
+                if (lane == 0) s = __dadd_rn(s, t);
+            }
+        }
+    } else {
+        const int64_t nseg = (L + split - 1) / split;
+        for (int64_t g0 = 0; g0 < nseg; g0 += 32) {
+            const int64_t sg = g0 + lane;
+            double ss = 0.0;
+            if (sg < nseg) {
+                const int64_t a = sg * split, b = min(L, a + split);
+                for (int64_t j = a; j < b; j++) ss = __dadd_rn(ss, x[iperm[row[j]]]);
+            }
+            const int cnt = (int)min((int64_t)32, nseg - g0);
+            for (int q = 0; q < cnt; q++) {
+                const double t = __shfl_sync(0xffffffffu, ss, q);
+                if (lane == 0) s = __dadd_rn(s, t);
+            }
+        }
+    }
+    if (lane == 0) epilogue(A, v, s);
+}
+
 // explicit empty rows (after updates): w = 0 and the bounds collapse to katz
 __global__ void k_zero_rows(const int32_t *zrows, int64_t nz, double *w, double *lower,
                             double *upper, const double *katz, int level_only) {
@@ -408,6 +453,19 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         note_launch();
         KB_CUDA(cudaGetLastError());
     }
+    if (g.implicit_rows && s.r == 0 && !level_only && n > g.nv) {
+        // rows without arcs: bounds collapse to katz (= 0) after the first step
+        k_empty_rows<<<(unsigned)((n - g.nv + 255) / 256), 256, 0, st>>>(
+            s.upper.p, s.lower.p, s.katz.p, g.nv, n); note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    if (g.n_ovf) {
+        k_ovf_rows<<<(unsigned)((g.n_ovf * 32 + 255) / 256), 256, 0, st>>>(
+            A, g.ovf.p, g.n_ovf, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p,
+            g.split);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
     KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used + 1], st));
     // the gather-free first step is not a K1 launch: keep it out of the
     // K1 timing (bench roofline) but count it in the run
@@ -420,11 +478,6 @@ void launch_iterate(State &s, cudaStream_t st) {
     DBuf<double> wnew;
     wnew.alloc(n + 1);
     run_spmv(s, st, s.x_level(), wnew.p, false);
-    if (s.r == 0 && g.implicit_rows && n > g.nv) {
-        k_empty_rows<<<(unsigned)((n - g.nv + 255) / 256), 256, 0, st>>>(
-            s.upper.p, s.lower.p, s.katz.p, g.nv, n); note_launch();
-        KB_CUDA(cudaGetLastError());
-    }
     s.levels.push_back(std::move(wnew));
     s.r += 1;
     if (!s.keep_all && s.levels.size() > 2) {
