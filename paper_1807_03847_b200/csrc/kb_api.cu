@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -97,11 +99,21 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (
 
 template <typename F>
 int guarded(F &&f) {
+    // a non-sticky error left by an earlier failed runtime call (for example
+    // a destructor running during interpreter teardown) must not surface in
+    // this call's cudaPeekAtLastError checks (CUB)
+    {
+        const cudaError_t stale = cudaGetLastError();
+        if (stale != cudaSuccess && getenv("KB_TRACE"))
+            fprintf(stderr, "[kb] stale CUDA error before API call: %s (last message: %s)\n",
+                    cudaGetErrorString(stale), t_err.c_str());
+    }
     try {
         f();
         return KB_OK;
     } catch (const Error &e) {
         set_error(e.msg);
+        (void)cudaGetLastError();
         return e.code;
     } catch (const std::bad_alloc &) {
         set_error("host allocation failed");
@@ -569,6 +581,8 @@ int kb_state_destroy(kb_state *h) {
     return guarded([&] {
         if (!h) return;
         use_device(h->s.g->device);
+        // a state must not outlive its graph (the Python layer holds the
+        // DeviceGraph); sync before the buffers go back to the pool
         KB_CUDA(cudaStreamSynchronize(h->s.g->stream));
         if (h->s.ev0) cudaEventDestroy(h->s.ev0);
         if (h->s.ev1) cudaEventDestroy(h->s.ev1);
