@@ -549,78 +549,99 @@ void build_graph_device(Graph &g) {
 
 
 namespace {
-__global__ void k_arc_keys_fwd_rev(const int64_t *indptr, const int32_t *rlen,
-                                   const int32_t *indices, int64_t n, const int64_t *cidx,
-                                   int shift, uint64_t *rev) {
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n) return;
-    const int64_t base = cidx[warp];
-    for (int64_t j = lane; j < rlen[warp]; j += 32)
-        rev[base + j] = ((uint64_t)(uint32_t)indices[indptr[warp] + j] << shift) | (uint64_t)warp;
+// per row u: arcs to smaller ids (lower triangle) and to larger ids (upper)
+__global__ void k_tri_counts(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
+                             int64_t n, int64_t *lo_cnt, int64_t *hi_cnt) {
+    int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (u > n) return;
+    if (u == n) { lo_cnt[u] = hi_cnt[u] = 0; return; }
+    const int32_t *row = indices + indptr[u];
+    const int64_t L = rlen[u];
+    int64_t a = 0, b = L;  // first slot with col >= u
+    while (a < b) { const int64_t m = (a + b) >> 1; if (row[m] < u) a = m + 1; else b = m; }
+    const int64_t lo = a;
+    const int64_t self = (lo < L && row[lo] == u) ? 1 : 0;
+    lo_cnt[u] = lo;
+    hi_cnt[u] = L - lo - self;
 }
 
-// forward key of slot i (rows ascending, columns ascending within a row) vs
-// the i-th smallest reversed key
-__global__ void k_compare_fwd(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
-                              int64_t n, const int64_t *cidx, int shift, const uint64_t *rev,
-                              unsigned long long *bad) {
+// forward upper-triangle keys u<<s|v (already in sorted order) and reversed
+// lower-triangle keys v<<s|u (to be sorted); one warp per row
+__global__ void k_tri_keys(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
+                           int64_t n, const int64_t *lo_off, const int64_t *hi_off,
+                           const int64_t *lo_cnt, int shift, uint64_t *fwd, uint64_t *rev) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= n) return;
-    const int64_t base = cidx[warp];
-    for (int64_t j = lane; j < rlen[warp]; j += 32) {
-        const uint64_t f = ((uint64_t)warp << shift) | (uint64_t)(uint32_t)indices[indptr[warp] + j];
-        if (rev[base + j] != f) { atomicAdd(bad, 1ull); return; }
+    const int64_t u = warp;
+    const int32_t *row = indices + indptr[u];
+    const int64_t L = rlen[u], nlo = lo_cnt[u];
+    for (int64_t j = lane; j < L; j += 32) {
+        const int64_t v = row[j];
+        if (j < nlo) rev[lo_off[u] + j] = ((uint64_t)v << shift) | (uint64_t)u;
+        else if (v > u) {
+            const int64_t self = (nlo < L && row[nlo] == u) ? 1 : 0;
+            fwd[hi_off[u] + (j - nlo - self)] = ((uint64_t)u << shift) | (uint64_t)v;
+        }
     }
 }
 
-__global__ void k_compact_lens(const int32_t *rlen, int64_t n, int64_t *len) {
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v > n) return;
-    len[v] = v < n ? rlen[v] : 0;
+__global__ void k_equal_u64(const uint64_t *a, const uint64_t *b, int64_t m,
+                            unsigned long long *bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (a[i] != b[i]) { atomicAdd(bad, 1ull); return; }
 }
 }  // namespace
 
 // Graph.is_symmetric (graph.py:168-175): the arc set equals its reversal.
-// The forward keys u*2^s+v are already sorted (canonical CSR), so the set is
-// symmetric iff the sorted reversed keys v*2^s+u match them one for one.
+// Self-loops are their own reversal; every arc u->v with u < v must be
+// matched by v->u.  The upper-triangle keys u*2^s+v come out of the
+// canonical CSR already sorted, so the set is symmetric iff the sorted
+// reversed lower-triangle keys match them one for one (half the arcs sorted).
 int graph_is_symmetric(Graph &g) {
     cudaStream_t st = g.stream;
     const int64_t n = g.n, m = g.nnz;
     if (m == 0) return 1;
     int shift = 1;
     while (((int64_t)1 << shift) < n) shift++;
-    DBuf<int64_t> len, cidx;
-    len.alloc(n + 1);
-    cidx.alloc(n + 1);
-    k_compact_lens<<<blocks_for(n + 1, 256), 256, 0, st>>>(g.rlen.p, n, len.p);
+    DBuf<int64_t> lo_cnt, hi_cnt, lo_off, hi_off;
+    lo_cnt.alloc(n + 1); hi_cnt.alloc(n + 1); lo_off.alloc(n + 1); hi_off.alloc(n + 1);
+    k_tri_counts<<<blocks_for(n + 1, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p, n,
+                                                        lo_cnt.p, hi_cnt.p);
     note_launch();
     cub_run([&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, len.p, cidx.p, (int)(n + 1), st);
+        return cub::DeviceScan::ExclusiveSum(t, b, lo_cnt.p, lo_off.p, (int)(n + 1), st);
     });
-    DBuf<uint64_t> rev, srev;
-    rev.alloc(m);
-    srev.alloc(m);
-    k_arc_keys_fwd_rev<<<blocks_for(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p,
-                                                                g.indices.p, n, cidx.p, shift,
-                                                                rev.p);
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, hi_cnt.p, hi_off.p, (int)(n + 1), st);
+    });
+    int64_t tot[2];
+    KB_CUDA(cudaMemcpyAsync(&tot[0], lo_off.p + n, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaMemcpyAsync(&tot[1], hi_off.p + n, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    if (tot[0] != tot[1]) return 0;
+    const int64_t h = tot[0];
+    if (h == 0) return 1;
+    DBuf<uint64_t> fwd, rev, srev;
+    fwd.alloc(h); rev.alloc(h); srev.alloc(h);
+    k_tri_keys<<<blocks_for(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p, n,
+                                                        lo_off.p, hi_off.p, lo_cnt.p, shift,
+                                                        fwd.p, rev.p);
     note_launch();
     cub_run([&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, rev.p, srev.p, m, 0, 2 * shift, st);
+        return cub::DeviceRadixSort::SortKeys(t, b, rev.p, srev.p, h, 0, 2 * shift, st);
     });
-    rev.release();
     DBuf<unsigned long long> bad;
     bad.alloc(1);
     KB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), st));
-    k_compare_fwd<<<blocks_for(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p, n,
-                                                           cidx.p, shift, srev.p, bad.p);
+    k_equal_u64<<<4 * std::max(1, g.sm_count), 256, 0, st>>>(fwd.p, srev.p, h, bad.p);
     note_launch();
     KB_CUDA(cudaGetLastError());
-    unsigned long long h = 0;
-    KB_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    unsigned long long hb = 0;
+    KB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    return h == 0;
+    return hb == 0;
 }
 
 }  // namespace kb

@@ -85,3 +85,27 @@ def test_device_resident_graph_dynamic_matches_host_graph():
     with pytest.raises(P.BatchPreconditionError):
         gd.validate_batch(P.EdgeBatch(deletions=[present[0]]))
     assert gd.max_out_degree() == gh.max_out_degree()
+
+
+def test_device_symmetry_check_cases():
+    cases = [
+        ([(0, 1), (1, 0), (2, 2)], True),           # self-loop is its own reverse
+        ([(0, 1), (1, 0), (1, 2)], False),
+        ([(0, 2), (2, 0), (1, 2), (2, 1), (3, 3)], True),
+        ([(3, 0), (0, 3), (2, 0)], False),
+        ([], True),
+    ]
+    for arcs, sym in cases:
+        g = P.Graph.from_edges(5, arcs)
+        assert P.device_graph(g).is_symmetric() == sym, arcs
+        assert g.is_symmetric() == sym
+    gr = G.rmat_graph(1 << 14, edge_factor=16, seed=1)
+    ip, ix = gr.csr_arrays()
+    assert P.DeviceGraph(ip, ix).is_symmetric()
+    row = ix[ip[5]:ip[6]].copy()
+    cand = [c for c in range(1 << 14) if c != 5 and c not in set(row.tolist())]
+    ix2 = ix.copy()
+    row[-1] = max(cand) if max(cand) > row[-2] else row[-1]
+    ix2[ip[5]:ip[6]] = np.sort(row)
+    if not np.array_equal(ix2, ix):
+        assert not P.DeviceGraph(ip, ix2).is_symmetric()

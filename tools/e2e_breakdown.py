@@ -12,7 +12,10 @@ ip, ix = np.ascontiguousarray(ip), np.ascontiguousarray(ix)
 L.kb_host_register(_lib.ptr(ip), ip.nbytes)
 L.kb_host_register(_lib.ptr(ix), ix.nbytes)
 crit = P.Criterion.top_k(100, 1e-6)
-for rep in range(3):
+import torch
+for rep in range(int(os.environ.get("REPS", "3"))):
+    free, total = torch.cuda.mem_get_info(0)
+    print(f"rep {rep}: device free {free/2**30:.1f} GiB of {total/2**30:.1f}", flush=True)
     t = [time.perf_counter()]
     dg = P.DeviceGraph(ip, ix); t.append(time.perf_counter())
     hg = G.DeviceResidentGraph(dg); t.append(time.perf_counter())
