@@ -206,6 +206,12 @@ int kb_check_apply_cut(kb_state *s, uint64_t kstar, int64_t istar, int64_t *acti
 int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
                    int64_t *order, int64_t *separated_pairs);
 
+/* ranking_result of a sharded run: the state's lower/upper hold all shards'
+ * blocks (exchange layout, after the all-gather) and the graph labels map
+ * exchange ids to the n node ids; outputs by node id, any may be NULL */
+int kb_rank_gathered(kb_state *s, int64_t n, int64_t *order, double *lower,
+                     double *upper, int64_t *separated_pairs);
+
 /* dynamic.update_batch (dynamic.py:126-211): arcs as (src,dst) int64 pairs,
  * already validated by the caller against the host graph. */
 int kb_update_batch(kb_state *s, const int64_t *ins, int64_t n_ins,

@@ -101,6 +101,7 @@ SIGNATURES = {
                                ctypes.POINTER(i64), ctypes.POINTER(i32)]),
     "kb_check_apply_cut": (i32, [vp, ctypes.c_uint64, i64, ctypes.POINTER(i64)]),
     "kb_rank_bounds": (i32, [i32, i64, vp, vp, vp, ctypes.POINTER(i64)]),
+    "kb_rank_gathered": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
     "kb_update_batch": (i32, [vp, vp, i64, vp, i64, dbl, dbl,
                               ctypes.POINTER(UpdateStatsC)]),
 }

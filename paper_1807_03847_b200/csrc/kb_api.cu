@@ -353,6 +353,15 @@ int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upp
     });
 }
 
+int kb_rank_gathered(kb_state *h, int64_t n, int64_t *order, double *lower, double *upper,
+                     int64_t *separated_pairs) {
+    return guarded([&] {
+        KB_REQUIRE(h && n >= 1, KB_EPARAM, "bad argument");
+        use_device(h->s.g->device);
+        rank_gathered(h->s, n, order, lower, upper, separated_pairs);
+    });
+}
+
 static kb_graph *new_graph(int device, int64_t split_threshold, int64_t hot_size) {
     use_device(device);
     auto *h = new kb_graph();

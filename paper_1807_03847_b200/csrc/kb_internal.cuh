@@ -207,6 +207,8 @@ void apply_cut(State &s, cudaStream_t st, uint64_t kstar, int64_t istar);
 void select_global(int device, const uint64_t *keys, const int64_t *labels, const double *uppers,
                    int64_t ncand, int64_t k, double eps, uint64_t *kstar, int64_t *istar,
                    int *prefix_ok);
+void rank_gathered(State &s, int64_t n, int64_t *order, double *lower, double *upper,
+                   int64_t *pairs);
 void rank_bounds(int device, int64_t n, const double *lower, const double *upper, int64_t *order,
                  int64_t *pairs);
 void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,

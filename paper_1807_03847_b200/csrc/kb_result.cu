@@ -228,22 +228,30 @@ __global__ void k_iota32(int64_t n, int32_t *a) {
 
 // ranking_result + separated pairs on caller vectors indexed by node id
 // (the multi-GPU path gathers the shard bounds and ranks them here)
-void rank_bounds(int device, int64_t n, const double *h_lower, const double *h_upper,
-                 int64_t *h_order, int64_t *h_pairs) {
-    (void)device;
-    cudaStream_t st = device_stream();
-    DBuf<double> lo, up;
+namespace {
+__global__ void k_scatter_by_label(const double *lo_x, const double *up_x, const int32_t *label,
+                                   int64_t N, int64_t n, double *lo, double *up) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= N) return;
+    const int32_t v = label[e];
+    if (v >= 0 && v < n) {
+        lo[v] = lo_x[e];
+        up[v] = up_x[e];
+    }
+}
+}  // namespace
+
+// ranking_result + separated pairs on device vectors indexed by node id
+static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const double *up,
+                             int64_t *h_order, int64_t *h_pairs) {
     DBuf<int32_t> iota, ids, order, zero_part, nids, snids;
     DBuf<unsigned char> fpos, fzero;
     DBuf<uint64_t> kin, kout;
     DBuf<unsigned long long> u;
-    lo.alloc(n); up.alloc(n); iota.alloc(n); ids.alloc(n); order.alloc(n);
-    fpos.alloc(n); fzero.alloc(n); u.alloc(3);
-    KB_CUDA(cudaMemcpyAsync(lo.p, h_lower, n * 8, cudaMemcpyHostToDevice, st));
-    KB_CUDA(cudaMemcpyAsync(up.p, h_upper, n * 8, cudaMemcpyHostToDevice, st));
+    iota.alloc(n); ids.alloc(n); order.alloc(n); fpos.alloc(n); fzero.alloc(n); u.alloc(3);
     KB_CUDA(cudaMemsetAsync(u.p, 0, 3 * 8, st));
     k_iota32<<<nblk(n, 256), 256, 0, st>>>(n, iota.p);
-    k_pos_flags<<<nblk(n, 256), 256, 0, st>>>(lo.p, iota.p, n, fpos.p, fzero.p, ids.p);
+    k_pos_flags<<<nblk(n, 256), 256, 0, st>>>(lo, iota.p, n, fpos.p, fzero.p, ids.p);
     note_launch(2);
     auto sel = [&](unsigned char *fl, int32_t *outp, unsigned long long *cnt) {
         size_t tb = 0;
@@ -262,12 +270,12 @@ void rank_bounds(int device, int64_t n, const double *h_lower, const double *h_u
     const int64_t npos = (int64_t)hc[0];
     kin.alloc(npos); kout.alloc(npos); nids.alloc(npos); snids.alloc(npos);
     if (npos) {
-        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(lo.p, iota.p, ids.p, npos, kin.p, nids.p);
+        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(lo, iota.p, ids.p, npos, kin.p, nids.p);
         note_launch();
         sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
         KB_CUDA(cudaMemcpyAsync(order.p, snids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
         if (n >= 2) {
-            k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(kout.p, snids.p, npos, up.p, u.p + 2);
+            k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(kout.p, snids.p, npos, up, u.p + 2);
             note_launch();
         }
     }
@@ -286,6 +294,34 @@ void rank_bounds(int device, int64_t n, const double *h_lower, const double *h_u
     KB_CUDA(cudaStreamSynchronize(st));
     pairs += (unsigned long long)(n - npos) * (unsigned long long)npos;
     if (h_pairs) *h_pairs = (int64_t)pairs;
+}
+
+void rank_bounds(int device, int64_t n, const double *h_lower, const double *h_upper,
+                 int64_t *h_order, int64_t *h_pairs) {
+    (void)device;
+    cudaStream_t st = device_stream();
+    DBuf<double> lo, up;
+    lo.alloc(n); up.alloc(n);
+    KB_CUDA(cudaMemcpyAsync(lo.p, h_lower, n * 8, cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemcpyAsync(up.p, h_upper, n * 8, cudaMemcpyHostToDevice, st));
+    rank_bounds_core(st, n, lo.p, up.p, h_order, h_pairs);
+}
+
+// The multi-GPU result: the state's lower/upper hold every shard's block
+// (exchange layout) after the all-gather; the graph labels map exchange ids
+// to node ids (>= n: padding).  Everything stays on the device.
+void rank_gathered(State &s, int64_t n, int64_t *h_order, double *h_lower, double *h_upper,
+                   int64_t *h_pairs) {
+    Graph &g = *s.g;
+    cudaStream_t st = g.stream;
+    DBuf<double> lo, up;
+    lo.alloc(n); up.alloc(n);
+    k_scatter_by_label<<<nblk(g.n, 256), 256, 0, st>>>(s.lower.p, s.upper.p, g.labels(), g.n, n,
+                                                      lo.p, up.p);
+    note_launch();
+    if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, st));
+    rank_bounds_core(st, n, lo.p, up.p, h_order, h_pairs);
 }
 
 }  // namespace kb

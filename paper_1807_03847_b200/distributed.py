@@ -208,14 +208,35 @@ class CudaShard:
                                          _lib.ptr(order), ctypes.byref(pairs)))
         return order, int(pairs.value)
 
+    def rank_gathered(self, host: bool = True):
+        """ranking_result of the gathered bounds, on the device: the state's
+        lower/upper hold every block (exchange layout) and the graph labels
+        map exchange ids to node ids (kb_rank_gathered).  host=False computes
+        the order and pair count without copying the vectors back."""
+        n = self.plan.n
+        pairs = ctypes.c_int64()
+        if not host:
+            _lib.check(self.L.kb_rank_gathered(self.s, n, None, None, None, ctypes.byref(pairs)))
+            return None, None, None, int(pairs.value)
+        order = np.empty(n, dtype=np.int64)
+        lower = np.empty(n, dtype=np.float64)
+        upper = np.empty(n, dtype=np.float64)
+        _lib.check(self.L.kb_rank_gathered(self.s, n, _lib.ptr(order), _lib.ptr(lower),
+                                           _lib.ptr(upper), ctypes.byref(pairs)))
+        return order, lower, upper, int(pairs.value)
+
     def sync(self):
         self.torch.cuda.synchronize(self.device)
 
 
 def _all_gather_flat(dist, full, rank: int, P: int, n_per: int):
-    """In-place all-gather of equal blocks of a flat tensor."""
-    mine = full[rank * n_per:(rank + 1) * n_per].clone()
-    dist.all_gather(list(full.split(n_per)), mine)
+    """In-place all-gather of equal blocks of a flat tensor (one collective
+    into the full buffer; the own block is staged because NCCL's in-place
+    form needs the input to alias the output slot exactly)."""
+    if P == 1:
+        return
+    mine = full[rank * n_per:(rank + 1) * n_per]
+    dist.all_gather_into_tensor(full, mine)
 
 
 class ShardedRun:
@@ -273,8 +294,10 @@ class ShardedRun:
         m_total = int(self._allreduce(float(m_local), ops.SUM))
         return m_total <= k and prefix_ok
 
-    def run(self) -> RankingResult:
-        """engine.run for P ranks; every rank returns the same result."""
+    def run(self, host_result: bool = True):
+        """engine.run for P ranks; every rank returns the same result.
+        host_result=False leaves the ranked vectors on the device and
+        returns (iterations, separated pairs) (bench timing)."""
         P, n_per = self.plan.P, self.plan.n_per
         r = 0
         while True:
@@ -289,21 +312,17 @@ class ShardedRun:
                 raise ConvergenceError(
                     f"stopping rule still unmet after {r} iterations "
                     f"(widest bound interval {gap:.3e})", iterations=r, gap=gap)
-        return self.result(r)
+        return self.result(r, host_result)
 
-    def result(self, r: int) -> RankingResult:
+    def result(self, r: int, host: bool = True):
         P, n_per = self.plan.P, self.plan.n_per
         lo_t, up_t = self.b.bounds_tensors()
         _all_gather_flat(self.dist, lo_t, self.rank, P, n_per)
         _all_gather_flat(self.dist, up_t, self.rank, P, n_per)
         self.b.sync()
-        node = self.plan.node_of_exch
-        valid = node >= 0
-        lower = np.empty(self.plan.n, dtype=np.float64)
-        upper = np.empty(self.plan.n, dtype=np.float64)
-        lower[node[valid]] = lo_t.cpu().numpy()[valid]
-        upper[node[valid]] = up_t.cpu().numpy()[valid]
-        order, pairs = self.b.rank_bounds(lower, upper)
+        order, lower, upper, pairs = self.b.rank_gathered(host)
+        if not host:
+            return r, pairs
         n = self.plan.n
         for arr in (order, lower, upper):
             arr.setflags(write=False)

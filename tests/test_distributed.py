@@ -87,9 +87,15 @@ class OracleShard:
     def bounds_tensors(self):
         return torch.from_numpy(self.lower), torch.from_numpy(self.upper)
 
-    def rank_bounds(self, lower, upper):
+    def rank_gathered(self, host=True):
+        node = self.plan.node_of_exch
+        valid = node >= 0
+        lower = np.empty(self.plan.n)
+        upper = np.empty(self.plan.n)
+        lower[node[valid]] = self.lower[valid]
+        upper[node[valid]] = self.upper[valid]
         order = np.lexsort((np.arange(lower.size), -lower))
-        return order, O.separated_pairs(lower, upper)
+        return order, lower, upper, O.separated_pairs(lower, upper)
 
 
 def _free_port():

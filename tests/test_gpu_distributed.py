@@ -68,6 +68,19 @@ def _lockstep(g0, crit, world):
         lower[node[a:b][sel]] = lo[rk][0][a:b].cpu().numpy()[sel]
         upper[node[a:b][sel]] = lo[rk][1][a:b].cpu().numpy()[sel]
     order, pairs = shards[0].rank_bounds(lower, upper)
+    # the device result path: gather every block into shard 0's bounds
+    lo0, up0 = lo[0]
+    for rk in range(1, world):
+        a, b = plan.block(rk)
+        lo0[a:b].copy_(lo[rk][0][a:b])
+        up0[a:b].copy_(lo[rk][1][a:b])
+    torch.cuda.synchronize()
+    o2, l2, u2, p2 = shards[0].rank_gathered()
+    np.testing.assert_array_equal(o2, order)
+    np.testing.assert_array_equal(l2, lower)
+    np.testing.assert_array_equal(u2, upper)
+    assert p2 == pairs
+    assert shards[0].rank_gathered(host=False)[3] == pairs
     for s in shards:
         s.close()
     return r, order, lower, upper, pairs
