@@ -186,6 +186,9 @@ int kb_get_active(kb_state *s, int64_t *out);
  * omega blocks and candidates with NCCL) */
 /* restrict the active set (node ids of this graph) */
 int kb_state_set_active(kb_state *s, const int64_t *ids, int64_t m);
+/* the same for the contiguous internal id range [lo, hi) of a
+ * KB_GRAPH_NO_RELABEL graph (a shard's owned rows), without a host list */
+int kb_state_set_active_range(kb_state *s, int64_t lo, int64_t hi);
 /* device pointer of a state vector (device id space: node ids for
  * KB_GRAPH_NO_RELABEL graphs) */
 int kb_state_vector_ptr(kb_state *s, int which, int64_t level, void **ptr);
@@ -205,6 +208,23 @@ int kb_check_apply_cut(kb_state *s, uint64_t kstar, int64_t istar, int64_t *acti
 /* ranking_result + separated pairs on caller vectors indexed by node id */
 int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
                    int64_t *order, int64_t *separated_pairs);
+
+/* the library's stream on `device` (every call above is ordered on it; a
+ * caller running collectives on the same stream needs no host sync) */
+int kb_stream(int device, void **stream);
+
+/* device-resident sharded TOPK check (no host copies; all async on the
+ * library stream).  propose: this rank's k best active nodes into a device
+ * block of 1 + 3k 64-bit words [count, lower bit keys, labels, uppers].
+ * cut: from the nblocks all-gathered blocks, the global k-th cut and the
+ * adjacent-separation test; splits the local active set (winners, then
+ * survivors) and writes word[0] = word[1] = new local count, word[2] =
+ * prefix ok.  commit: the new local count, read back by the caller after
+ * all-reducing word[0] (required before the next propose/cut). */
+int kb_shard_propose(kb_state *s, int64_t k, void *block);
+int kb_shard_cut(kb_state *s, const void *blocks, int64_t nblocks, int64_t k,
+                 void *word);
+int kb_shard_commit(kb_state *s, int64_t active);
 
 /* ranking_result of a sharded run: the state's lower/upper hold all shards'
  * blocks (exchange layout, after the all-gather) and the graph labels map

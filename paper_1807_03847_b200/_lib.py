@@ -94,6 +94,7 @@ SIGNATURES = {
     "kb_get_vector": (i32, [vp, i32, i64, vp]),
     "kb_get_active": (i32, [vp, vp]),
     "kb_state_set_active": (i32, [vp, vp, i64]),
+    "kb_state_set_active_range": (i32, [vp, i64, i64]),
     "kb_state_vector_ptr": (i32, [vp, i32, i64, ctypes.POINTER(vp)]),
     "kb_sync": (i32, [i32]),
     "kb_check_local_topk": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
@@ -101,6 +102,10 @@ SIGNATURES = {
                                ctypes.POINTER(i64), ctypes.POINTER(i32)]),
     "kb_check_apply_cut": (i32, [vp, ctypes.c_uint64, i64, ctypes.POINTER(i64)]),
     "kb_rank_bounds": (i32, [i32, i64, vp, vp, vp, ctypes.POINTER(i64)]),
+    "kb_stream": (i32, [i32, ctypes.POINTER(vp)]),
+    "kb_shard_propose": (i32, [vp, i64, vp]),
+    "kb_shard_cut": (i32, [vp, vp, i64, i64, vp]),
+    "kb_shard_commit": (i32, [vp, i64]),
     "kb_rank_gathered": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
     "kb_update_batch": (i32, [vp, vp, i64, vp, i64, dbl, dbl,
                               ctypes.POINTER(UpdateStatsC)]),

@@ -90,6 +90,11 @@ __global__ void k_map_ids(const int64_t *ids, int64_t m, const int32_t *iperm, i
     out[i] = iperm[v];
 }
 
+__global__ void k_range32(int64_t lo, int64_t m, int32_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) out[i] = (int32_t)(lo + i);
+}
+
 __global__ void k_sep_one(const double *lower, const double *upper, const int32_t *iperm,
                           int64_t w, int64_t v, double eps, unsigned long long *out) {
     out[0] = lower[iperm[w]] > __dsub_rn(upper[iperm[v]], eps);
@@ -270,14 +275,37 @@ int kb_state_set_active(kb_state *h, const int64_t *ids, int64_t m) {
         State &s = h->s;
         KB_REQUIRE(m >= 0 && m <= s.g->n, KB_EPARAM, "bad active size");
         use_device(s.g->device);
+        cudaStream_t st = s.g->stream;
         DBuf<int64_t> d;
         d.alloc(std::max<int64_t>(1, m));
-        if (m) KB_CUDA(cudaMemcpyAsync(d.p, ids, m * 8, cudaMemcpyHostToDevice, s.g->stream));
-        if (m) k_map_ids<<<nblk(m, 256), 256, 0, s.g->stream>>>(d.p, m, s.g->iperm.p, s.g->n,
-                                                              s.act[s.cur].p, s.scratch_u64.p);
-        note_launch();
-        KB_CUDA(cudaMemsetAsync(s.scratch_u64.p + 8, 0, 8, s.g->stream));
-        KB_CUDA(cudaStreamSynchronize(s.g->stream));
+        KB_CUDA(cudaMemsetAsync(s.scratch_u64.p + 8, 0, 8, st));
+        if (m) {
+            KB_CUDA(cudaMemcpyAsync(d.p, ids, m * 8, cudaMemcpyHostToDevice, st));
+            k_map_ids<<<nblk(m, 256), 256, 0, st>>>(d.p, m, s.g->iperm.p, s.g->n, s.act[s.cur].p,
+                                                    s.scratch_u64.p);
+            note_launch();
+        }
+        unsigned long long bad = 0;
+        KB_CUDA(cudaMemcpyAsync(&bad, s.scratch_u64.p + 8, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        KB_REQUIRE(!bad, KB_EPARAM, "active id out of range");
+        s.act_dense = false;
+        s.m_host = m;
+    });
+}
+
+int kb_state_set_active_range(kb_state *h, int64_t lo, int64_t hi) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        KB_REQUIRE(0 <= lo && lo <= hi && hi <= s.g->n, KB_EPARAM, "bad active range");
+        KB_REQUIRE(!s.g->relabel, KB_EPARAM, "active ranges need a KB_GRAPH_NO_RELABEL graph");
+        use_device(s.g->device);
+        const int64_t m = hi - lo;
+        if (m) {
+            k_range32<<<nblk(m, 256), 256, 0, s.g->stream>>>(lo, m, s.act[s.cur].p);
+            note_launch();
+        }
         s.act_dense = false;
         s.m_host = m;
     });
@@ -350,6 +378,40 @@ int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upp
         KB_REQUIRE(lower && upper && n >= 1, KB_EPARAM, "bad argument");
         use_device(device);
         rank_bounds(device, n, lower, upper, order, separated_pairs);
+    });
+}
+
+int kb_stream(int device, void **stream) {
+    return guarded([&] {
+        KB_REQUIRE(stream, KB_EPARAM, "NULL argument");
+        use_device(device);
+        *stream = (void *)device_stream();
+    });
+}
+
+int kb_shard_propose(kb_state *h, int64_t k, void *block) {
+    return guarded([&] {
+        KB_REQUIRE(h && block, KB_EPARAM, "NULL argument");
+        use_device(h->s.g->device);
+        shard_propose(h->s, h->s.g->stream, k, (unsigned long long *)block);
+        KB_CUDA(cudaGetLastError());
+    });
+}
+
+int kb_shard_cut(kb_state *h, const void *blocks, int64_t nblocks, int64_t k, void *word) {
+    return guarded([&] {
+        KB_REQUIRE(h && blocks && word, KB_EPARAM, "NULL argument");
+        use_device(h->s.g->device);
+        shard_cut(h->s, h->s.g->stream, (const unsigned long long *)blocks, nblocks, k,
+                  (long long *)word);
+        KB_CUDA(cudaGetLastError());
+    });
+}
+
+int kb_shard_commit(kb_state *h, int64_t active) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL state");
+        shard_commit(h->s, active);
     });
 }
 

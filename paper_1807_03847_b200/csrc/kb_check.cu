@@ -905,8 +905,10 @@ namespace {
 __global__ void __launch_bounds__(1024) k_sort_cands(const double *lower, const double *upper,
                                                      const int32_t *labels, const int32_t *src,
                                                      int dense, int64_t cnt, uint64_t *keys_out,
-                                                     int64_t *labels_out, double *uppers_out) {
+                                                     int64_t *labels_out, double *uppers_out,
+                                                     unsigned long long *count_out) {
     extern __shared__ unsigned char smem[];
+    if (count_out && threadIdx.x == 0) *count_out = (unsigned long long)cnt;
     int P = 1;
     while (P < cnt) P <<= 1;
     uint64_t *hi = (uint64_t *)smem;
@@ -1067,7 +1069,7 @@ void local_topk(State &s, cudaStream_t st, int64_t k, uint64_t *keys, int64_t *l
         KB_CUDA(cudaFuncSetAttribute(k_sort_cands, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         k_sort_cands<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), src, dense, cnt,
-                                            dk.p, dl.p, du.p);
+                                            dk.p, dl.p, du.p, nullptr);
         note_launch();
         KB_CUDA(cudaMemcpyAsync(keys, dk.p, cnt * 8, cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaMemcpyAsync(labels, dl.p, cnt * 8, cudaMemcpyDeviceToHost, st));
@@ -1131,6 +1133,200 @@ void select_global(int device, const uint64_t *keys, const int64_t *labels, cons
     *kstar = h[0];
     *istar = (int64_t)h[1];
     *prefix_ok = (int)h[2];
+}
+
+// ------------------------------------------- device-resident shard protocol
+//
+// The TOPK check of a sharded run without host round trips: every rank
+// writes its k proposals into a fixed-size device block, the blocks are
+// all-gathered by NCCL on the same stream, every rank derives the same
+// global cut on its device and splits its active set; only the new local
+// count leaves the device (after the count all-reduce).  Block layout, in
+// 64-bit words: [count, keys[k], labels[k], uppers[k] (f64 bits)].
+
+namespace {
+
+__global__ void k_unpack_blocks(const unsigned long long *blocks, int64_t P, int64_t k,
+                                uint64_t *keys, int64_t *labels, double *uppers, uint64_t *nk,
+                                int32_t *iota) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P * k) return;
+    const int64_t b = i / k, j = i - b * k;
+    const unsigned long long *blk = blocks + b * (1 + 3 * k);
+    uint64_t key = 0;
+    int64_t lab = INT64_MAX;  // padding sorts after every real candidate
+    double up = 0.0;
+    if (j < (int64_t)blk[0]) {
+        key = blk[1 + j];
+        lab = (int64_t)blk[1 + k + j];
+        up = __longlong_as_double((long long)blk[1 + 2 * k + j]);
+    }
+    keys[i] = key;
+    labels[i] = lab;
+    uppers[i] = up;
+    nk[i] = ~key;
+    iota[i] = (int32_t)i;
+}
+
+// the global cut (k-th of the merged proposals) and the adjacent-separation
+// test of the merged top-k prefix; cut[3], cut[4] feed IsWinner/IsSurvivor
+__global__ void k_global_cut_dev(const uint64_t *keys, const int64_t *labels,
+                                 const double *uppers, const int32_t *order,
+                                 const unsigned long long *blocks, int64_t P, int64_t k,
+                                 double eps, unsigned long long *cut) {
+    __shared__ int bad;
+    __shared__ int64_t kk;
+    if (threadIdx.x == 0) {
+        bad = 0;
+        int64_t tot = 0;
+        for (int64_t b = 0; b < P; b++) tot += (int64_t)blocks[b * (1 + 3 * k)];
+        kk = tot < k ? tot : k;
+    }
+    __syncthreads();
+    for (int64_t i = 1 + threadIdx.x; i < kk; i += blockDim.x) {
+        const double lprev = __longlong_as_double((long long)keys[order[i - 1]]);
+        if (!(__dsub_rn(uppers[order[i]], eps) < lprev)) bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (kk == 0) {  // no active node anywhere: nothing wins or survives
+            cut[3] = ~0ull;
+            cut[4] = 0;
+        } else {
+            cut[3] = keys[order[kk - 1]];
+            cut[4] = (unsigned long long)labels[order[kk - 1]];
+        }
+        cut[7] = !bad;
+    }
+}
+
+// winners stay first, survivors follow; word = [m_local, m_local, prefix_ok]
+__global__ void k_append_survivors(const int32_t *surv, const unsigned long long *cut,
+                                   int32_t *act, long long *word) {
+    const unsigned long long nw = cut[5], ns = cut[6];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < (int64_t)ns) act[nw + i] = surv[i];
+    if (i == 0) {
+        word[0] = (long long)(nw + ns);
+        word[1] = (long long)(nw + ns);
+        word[2] = (long long)cut[7];
+    }
+}
+
+}  // namespace
+
+void shard_propose(State &s, cudaStream_t st, int64_t k, unsigned long long *blk) {
+    Graph &g = *s.g;
+    KB_REQUIRE(k >= 1 && k <= KMAX, KB_EPARAM, "sharded top-k supports 1 <= k <= 4096");
+    KB_REQUIRE(s.m_host >= 0, KB_ESTATE, "active count pending: kb_shard_commit first");
+    const int64_t m = s.m_host;
+    const int32_t *src = s.act[s.cur].p;
+    int dense = s.act_dense;
+    const int64_t cnt = std::min(m, k);
+    if (m > k) {
+        TopkArgs A;
+        A.lower = s.lower.p;
+        A.upper = s.upper.p;
+        A.perm = g.labels();
+        A.act_in = s.act[s.cur].p;
+        A.m = m;
+        A.dense = s.act_dense;
+        A.act_out = s.act[s.cur ^ 1].p;
+        A.k = k;
+        A.eps = s.eps;
+        A.hist = (unsigned int *)(s.scratch_u64.p + 8);
+        const int G = (int)std::max<int64_t>(
+            1, std::min<int64_t>(coop_grid(g.sm_count), (A.m + 8191) / 8192));
+        A.blk = s.scratch_u64.p + 8 + HIST_WORDS;
+        A.prefix_buf = s.scratch_i32.p;
+        A.cand = s.cand.p;
+        A.stK = s.stK.p;
+        A.stU = s.stU.p;
+        A.stI = s.stI.p;
+        A.out = s.scratch_u64.p;
+        void *args[] = {&A};
+        KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
+        note_launch();
+        // exactly k winners (labels are unique), so the count is known here
+        IsWinner win{s.lower.p, g.labels(), s.scratch_u64.p};
+        unsigned long long *nsel = s.scratch_u64.p + 5;
+        auto sel = [&](auto in) {
+            cub_go(&s, [&](void *t, size_t &b) {
+                return cub::DeviceSelect::If(t, b, in, s.scratch_i32.p, nsel, (int)m, win, st);
+            });
+        };
+        if (s.act_dense) sel(cub::CountingInputIterator<int32_t>(0));
+        else sel((const int32_t *)s.act[s.cur].p);
+        src = s.scratch_i32.p;
+        dense = 0;
+    }
+    int P = 1;
+    while (P < std::max<int64_t>(1, cnt)) P <<= 1;
+    const size_t smem = (size_t)P * 16;
+    KB_CUDA(cudaFuncSetAttribute(k_sort_cands, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_sort_cands<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), src, dense, cnt,
+                                        (uint64_t *)(blk + 1), (int64_t *)(blk + 1 + k),
+                                        (double *)(blk + 1 + 2 * k), blk);
+    note_launch();
+}
+
+void shard_cut(State &s, cudaStream_t st, const unsigned long long *blocks, int64_t P, int64_t k,
+               long long *word) {
+    KB_REQUIRE(P >= 1 && k >= 1 && k <= KMAX, KB_EPARAM, "bad proposal blocks");
+    KB_REQUIRE(s.m_host >= 0, KB_ESTATE, "active count pending: kb_shard_commit first");
+    const int64_t nc = P * k;
+    DBuf<uint64_t> dk, nk, nk2;
+    DBuf<int64_t> dl, l2;
+    DBuf<double> du;
+    DBuf<int32_t> i0, i1, i2, surv;
+    dk.alloc(nc); nk.alloc(nc); nk2.alloc(nc); dl.alloc(nc); l2.alloc(nc);
+    du.alloc(nc); i0.alloc(nc); i1.alloc(nc); i2.alloc(nc);
+    k_unpack_blocks<<<nblk(nc, 256), 256, 0, st>>>(blocks, P, k, dk.p, dl.p, du.p, nk.p, i0.p);
+    note_launch();
+    // (key desc, label asc): stable sort by label, then by inverted key
+    cub_go(nullptr, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, dl.p, l2.p, i0.p, i1.p, (int)nc, 0, 64, st);
+    });
+    k_gather_u64<<<nblk(nc, 256), 256, 0, st>>>(nk.p, i1.p, nc, nk2.p);
+    note_launch();
+    cub_go(nullptr, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, nk2.p, nk.p, i1.p, i2.p, (int)nc, 0, 64, st);
+    });
+    unsigned long long *cut = s.scratch_u64.p;
+    k_global_cut_dev<<<1, 256, 0, st>>>(dk.p, dl.p, du.p, i2.p, blocks, P, k, s.eps, cut);
+    note_launch();
+    // three-way split of the local active set under the global cut
+    Graph &g = *s.g;
+    const int64_t m = s.m_host;
+    const int nxt = s.cur ^ 1;
+    surv.alloc(std::max<int64_t>(1, m));
+    IsWinner win{s.lower.p, g.labels(), cut};
+    IsSurvivor sur{s.lower.p, s.upper.p, cut, s.eps};
+    if (m) {
+        auto part = [&](auto in) {
+            cub_go(&s, [&](void *t, size_t &b) {
+                return cub::DevicePartition::If(t, b, in, s.act[nxt].p, surv.p, s.stI.p, cut + 5,
+                                                (int)m, win, sur, st);
+            });
+        };
+        if (s.act_dense) part(cub::CountingInputIterator<int32_t>(0));
+        else part((const int32_t *)s.act[s.cur].p);
+    } else {
+        KB_CUDA(cudaMemsetAsync(cut + 5, 0, 16, st));
+    }
+    k_append_survivors<<<nblk(std::max<int64_t>(1, m), 256), 256, 0, st>>>(surv.p, cut,
+                                                                          s.act[nxt].p, word);
+    note_launch();
+    s.cur = nxt;
+    s.act_dense = false;
+    s.m_host = -1;  // known after the count all-reduce: kb_shard_commit
+}
+
+void shard_commit(State &s, int64_t m) {
+    KB_REQUIRE(s.m_host < 0, KB_ESTATE, "no cut pending");
+    KB_REQUIRE(m >= 0 && m <= s.g->n, KB_EPARAM, "bad active count");
+    s.m_host = m;
 }
 
 }  // namespace kb

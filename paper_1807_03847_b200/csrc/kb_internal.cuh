@@ -207,6 +207,10 @@ void apply_cut(State &s, cudaStream_t st, uint64_t kstar, int64_t istar);
 void select_global(int device, const uint64_t *keys, const int64_t *labels, const double *uppers,
                    int64_t ncand, int64_t k, double eps, uint64_t *kstar, int64_t *istar,
                    int *prefix_ok);
+void shard_propose(State &s, cudaStream_t st, int64_t k, unsigned long long *blk);
+void shard_cut(State &s, cudaStream_t st, const unsigned long long *blocks, int64_t P, int64_t k,
+               long long *word);
+void shard_commit(State &s, int64_t m);
 void rank_gathered(State &s, int64_t n, int64_t *order, double *lower, double *upper,
                    int64_t *pairs);
 void rank_bounds(int device, int64_t n, const double *lower, const double *upper, int64_t *order,

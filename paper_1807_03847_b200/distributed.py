@@ -66,6 +66,11 @@ class ShardPlan:
     def block(self, rank: int) -> tuple[int, int]:
         return rank * self.n_per, (rank + 1) * self.n_per
 
+    def owned(self, rank: int) -> int:
+        """Rows rank owns: degree ranks q = rank (mod P) below n, laid out at
+        the head of its block (the padding is the block's tail)."""
+        return max(0, -(-(self.n - rank) // self.P))
+
     def labels(self) -> np.ndarray:
         """Tie-break labels by exchange id: the node id (padding: unique > n)."""
         lab = self.node_of_exch.copy()
@@ -127,10 +132,8 @@ class CudaShard:
                                           crit.epsilon, int(crit.k or 0), 0, 0, 1,
                                           int(max_iterations), ctypes.byref(s)))
         self.s = s
-        lo, hi = self.plan.block(self.rank)
-        own = np.arange(lo, hi, dtype=np.int64)
-        own = own[self.plan.node_of_exch[lo:hi] >= 0]
-        _lib.check(self.L.kb_state_set_active(s, _lib.ptr(own), own.size))
+        lo, _ = self.plan.block(self.rank)
+        _lib.check(self.L.kb_state_set_active_range(s, lo, lo + self.plan.owned(self.rank)))
         self.r = 0
 
     def close(self):
@@ -159,10 +162,31 @@ class CudaShard:
         return self.torch.as_tensor(_A(), device=f"cuda:{self.device}")
 
     # -- protocol
+    def stream_context(self):
+        """Run the collectives on the library's stream, so NCCL orders after
+        the kernels that produce their inputs without a host sync."""
+        if getattr(self, "_stream", None) is None:
+            p = ctypes.c_void_p()
+            _lib.check(self.L.kb_stream(self.device, ctypes.byref(p)))
+            self._stream = self.torch.cuda.ExternalStream(int(p.value or 0),
+                                                          device=f"cuda:{self.device}")
+        return self.torch.cuda.stream(self._stream)
+
+    def new_buffer(self, words: int):
+        return self.torch.zeros(words, dtype=self.torch.int64, device=f"cuda:{self.device}")
+
     def iterate(self):
         _lib.check(self.L.kb_iterate(self.s, 1))
-        _lib.check(self.L.kb_sync(self.device))
         self.r += 1
+
+    def propose(self, k: int, block):
+        _lib.check(self.L.kb_shard_propose(self.s, k, block.data_ptr()))
+
+    def cut(self, blocks, nblocks: int, k: int, word):
+        _lib.check(self.L.kb_shard_cut(self.s, blocks.data_ptr(), nblocks, k, word.data_ptr()))
+
+    def commit(self, active: int):
+        _lib.check(self.L.kb_shard_commit(self.s, active))
 
     def level_tensor(self):
         return self._view(_lib.KB_VEC_LEVEL, self.r)
@@ -266,45 +290,37 @@ class ShardedRun:
         ops = self.dist.ReduceOp
         if c.kind == SCORE:
             return self._allreduce(self.b.local_gap(), ops.MAX) < c.epsilon
+        # TOPK: fixed-size proposal blocks (count + k keys, labels, uppers as
+        # 64-bit words) all-gathered on the device; every rank takes the same
+        # global cut; |active| is all-reduced; one host read per check
         k = int(c.k)
-        keys, labels, uppers = self.b.local_topk(k)
-        # all-gather fixed-size proposal blocks (count + k entries) as float64
-        # bit patterns so one collective carries keys, labels and uppers
-        blk = np.zeros(1 + 3 * k, dtype=np.float64)
-        cnt = keys.size
-        blk[0] = cnt
-        blk[1:1 + cnt] = keys.view(np.float64)
-        blk[1 + k:1 + k + cnt] = labels.astype(np.float64)
-        blk[1 + 2 * k:1 + 2 * k + cnt] = uppers
-        dev = getattr(self.b, "collective_device", "cpu")
-        t = self.torch.from_numpy(blk).to(dev)
-        outs = [self.torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t)
-        K, Lb, U = [], [], []
-        for o in outs:
-            a = o.cpu().numpy()
-            n_ = int(a[0])
-            K.append(a[1:1 + n_].view(np.uint64))
-            Lb.append(a[1 + k:1 + k + n_].astype(np.int64))
-            U.append(a[1 + 2 * k:1 + 2 * k + n_])
-        keys_all, labels_all, uppers_all = map(np.concatenate, (K, Lb, U))
-        kstar, istar, prefix_ok = self.b.select_global(keys_all, labels_all, uppers_all, k,
-                                                       c.epsilon)
-        m_local = self.b.apply_cut(kstar, istar)
-        m_total = int(self._allreduce(float(m_local), ops.SUM))
-        return m_total <= k and prefix_ok
+        if self._blocks is None:
+            self._blk = self.b.new_buffer(1 + 3 * k)
+            self._blocks = self.b.new_buffer(self.world * (1 + 3 * k))
+            self._word = self.b.new_buffer(3)
+        self.b.propose(k, self._blk)
+        self.dist.all_gather_into_tensor(self._blocks, self._blk)
+        self.b.cut(self._blocks, self.world, k, self._word)
+        self.dist.all_reduce(self._word[0:1], op=ops.SUM)
+        m_total, m_local, ok = (int(v) for v in self._word.tolist())
+        self.b.commit(m_local)
+        return m_total <= k and bool(ok)
 
     def run(self, host_result: bool = True):
         """engine.run for P ranks; every rank returns the same result.
         host_result=False leaves the ranked vectors on the device and
         returns (iterations, separated pairs) (bench timing)."""
+        with self.b.stream_context():
+            return self._run(host_result)
+
+    def _run(self, host_result):
         P, n_per = self.plan.P, self.plan.n_per
+        self._blocks = None
         r = 0
         while True:
             self.b.iterate()
             r += 1
             _all_gather_flat(self.dist, self.b.level_tensor(), self.rank, P, n_per)
-            self.b.sync()
             if self._check():
                 break
             if r >= self.max_iterations:
@@ -319,7 +335,6 @@ class ShardedRun:
         lo_t, up_t = self.b.bounds_tensors()
         _all_gather_flat(self.dist, lo_t, self.rank, P, n_per)
         _all_gather_flat(self.dist, up_t, self.rank, P, n_per)
-        self.b.sync()
         order, lower, upper, pairs = self.b.rank_gathered(host)
         if not host:
             return r, pairs

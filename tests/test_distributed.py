@@ -6,6 +6,7 @@ the C-ABI).  A sharded run must reproduce the single-process oracle bit for
 bit: same r, order, bounds and separated fraction."""
 from __future__ import annotations
 
+import contextlib
 import os
 import socket
 
@@ -79,6 +80,35 @@ class OracleShard:
         surv = ~win & (self.upper[a] - self.eps >= thr)
         self.active = np.concatenate([a[win], a[surv]])
         return int(self.active.size)
+
+    # the device-resident protocol, on CPU tensors (gloo)
+    def stream_context(self):
+        return contextlib.nullcontext()
+
+    def new_buffer(self, words):
+        return torch.zeros(words, dtype=torch.int64)
+
+    def propose(self, k, block):
+        keys, labels, uppers = self.local_topk(k)
+        b = block.numpy()
+        b[:] = 0
+        c = keys.size
+        b[0] = c
+        b[1:1 + c] = keys.view(np.int64)
+        b[1 + k:1 + k + c] = labels
+        b[1 + 2 * k:1 + 2 * k + c] = uppers.view(np.int64)
+
+    def cut(self, blocks, nblocks, k, word):
+        a = blocks.numpy().reshape(nblocks, 1 + 3 * k)
+        K = np.concatenate([r[1:1 + r[0]].view(np.uint64) for r in a])
+        L = np.concatenate([r[1 + k:1 + k + r[0]] for r in a])
+        U = np.concatenate([r[1 + 2 * k:1 + 2 * k + r[0]].view(np.float64) for r in a])
+        kstar, istar, ok = self.select_global(K, L, U, k, self.eps)
+        m = self.apply_cut(kstar, istar)
+        word[:] = torch.tensor([m, m, int(ok)])
+
+    def commit(self, m):
+        assert m == self.active.size
 
     def local_gap(self):
         b = slice(self.lo, self.hi)
@@ -174,6 +204,11 @@ def test_shard_plan_balances_and_is_a_bijection():
         # round-robin by degree rank: SURVEY.md 8(e) measured 1.003-1.006 at s22;
         # at this small scale single hubs weigh more
         assert loads.max() / loads.mean() < 1.05
+        for rk in range(P):
+            a, b = plan.block(rk)
+            own = plan.owned(rk)
+            assert np.all(plan.node_of_exch[a:a + own] >= 0)
+            assert np.all(plan.node_of_exch[a + own:b] < 0)
         ip, ix = plan.local_csr(g.indptr, g.indices, 1)
         lo, hi = plan.block(1)
         assert ip[lo] == 0 and ip[-1] == ip[hi]

@@ -19,7 +19,7 @@ torch = pytest.importorskip("torch")
 from paper_1807_03847_b200 import distributed as D  # noqa: E402
 
 
-def _lockstep(g0, crit, world):
+def _lockstep(g0, crit, world, protocol="device"):
     plan = D.ShardPlan(g0.indptr, world)
     d = plan.max_degree
     alpha = 1.0 / (1.0 + d)
@@ -33,6 +33,7 @@ def _lockstep(g0, crit, world):
     while True:
         for s in shards:
             s.iterate()
+        torch.cuda.synchronize()
         r += 1
         lv = [s.level_tensor() for s in shards]
         for rk in range(world):               # all-gather by device copies
@@ -43,6 +44,24 @@ def _lockstep(g0, crit, world):
         torch.cuda.synchronize()
         if crit.kind == "score":
             done = max(s.local_gap() for s in shards) < crit.epsilon
+        elif protocol == "device":
+            k = int(crit.k)
+            blks = [s.new_buffer(1 + 3 * k) for s in shards]
+            words = [s.new_buffer(3) for s in shards]
+            torch.cuda.synchronize()
+            for s, b in zip(shards, blks):
+                s.propose(k, b)
+            torch.cuda.synchronize()
+            allb = torch.cat(blks)
+            torch.cuda.synchronize()
+            for s, w in zip(shards, words):
+                s.cut(allb, world, k, w)
+            torch.cuda.synchronize()
+            ws = [w.tolist() for w in words]
+            assert len({w[2] for w in ws}) == 1
+            for s, w in zip(shards, ws):
+                s.commit(w[1])
+            done = sum(w[0] for w in ws) <= k and bool(ws[0][2])
         else:
             k = int(crit.k)
             props = [s.local_topk(k) for s in shards]
@@ -86,11 +105,12 @@ def _lockstep(g0, crit, world):
     return r, order, lower, upper, pairs
 
 
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_cuda_shards_equal_single_gpu(world):
+@pytest.mark.parametrize("world,protocol", [(1, "device"), (2, "device"), (3, "device"),
+                                            (2, "host")])
+def test_cuda_shards_equal_single_gpu(world, protocol):
     g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
     crit = P.Criterion.top_k(100, 1e-6)
-    r, order, lower, upper, pairs = _lockstep(g0, crit, world)
+    r, order, lower, upper, pairs = _lockstep(g0, crit, world, protocol)
     g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
     res = P.run(P.init(g, crit, undirected=True), g)
     assert r == res.iterations_used
