@@ -209,6 +209,18 @@ int kb_check_apply_cut(kb_state *s, uint64_t kstar, int64_t istar, int64_t *acti
 int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
                    int64_t *order, int64_t *separated_pairs);
 
+/* baselines.foster (baselines.py:36-68): c <- alpha*A*c + 1 from ones until
+ * max|change| < tol; values = c - 1 by original id (n doubles).  At the cap:
+ * KB_ECONVERGENCE with values/iterations/residual holding the partial. */
+int kb_foster(kb_graph *g, double alpha, double tol, int64_t max_iter,
+              double *values, int64_t *iterations, double *residual);
+
+/* baselines.cg_katz (baselines.py:71-129): CG on (I - alpha*A) z = 1 from
+ * z = 1; values = alpha*A*z.  KB_ENUMERIC on breakdown, KB_ECONVERGENCE at
+ * the cap (values = the partial).  The caller checks symmetry. */
+int kb_cg_katz(kb_graph *g, double alpha, double residual_tol, int64_t max_iter,
+               double *values, int64_t *iterations, double *residual);
+
 /* the library's stream on `device` (every call above is ordered on it; a
  * caller running collectives on the same stream needs no host sync) */
 int kb_stream(int device, void **stream);

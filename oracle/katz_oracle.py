@@ -536,3 +536,139 @@ def update_batch(st: OracleState, g: AdjGraph, insertions, deletions,
         stats.resumed_iterations += 1
     st.last_update_stats = stats
     return stats
+
+
+# ---------------------------------------------------------------- baselines
+# Restatement of baselines.py:36-154 and cli.py:349-386 (the paper's
+# comparison methods and the ranking-agreement measure).
+
+class OracleBaselineError(Exception):
+    """kind: 'convergence' | 'numeric' | 'not_applicable' | 'parameter'."""
+
+    def __init__(self, kind, partial=None, iterations=None):
+        super().__init__(kind)
+        self.kind, self.partial, self.iterations = kind, partial, iterations
+
+
+@dataclass
+class OracleScores:
+    method: str
+    values: np.ndarray
+    iterations: int | None = None
+    residual: float | None = None
+
+    def ranking(self) -> np.ndarray:                       # baselines.py:30-33
+        n = len(self.values)
+        return np.lexsort((np.arange(n), -self.values))
+
+
+def _baseline_alpha(g: CSRGraph, alpha):
+    d = g.max_out_degree()
+    if alpha is None:
+        alpha = default_alpha(d)                            # engine.py:96-99
+    if alpha <= 0 or (d > 0 and alpha >= 1.0 / d) or (d == 0 and alpha >= 1.0):
+        raise OracleBaselineError("parameter")              # engine.py:102-113
+    return alpha
+
+
+def foster(g: CSRGraph, alpha=None, tol=1e-9, max_iter=1000) -> OracleScores:
+    """baselines.py:36-68: c <- alpha*A*c + 1 until max|change| < tol."""
+    alpha = _baseline_alpha(g, alpha)
+    if not tol > 0 or max_iter < 1:
+        raise OracleBaselineError("parameter")
+    c = np.ones(g.node_count, dtype=np.float64)
+    delta = np.inf
+    for it in range(1, max_iter + 1):
+        nxt = alpha * csr_matvec(g, c) + 1.0                # :58
+        delta = float(np.max(np.abs(nxt - c))) if len(c) else 0.0
+        c = nxt
+        if delta < tol:
+            return OracleScores("foster", c - 1.0, iterations=it, residual=delta)
+    raise OracleBaselineError("convergence",
+                              OracleScores("foster", c - 1.0, max_iter, delta), max_iter)
+
+
+def cg_katz(g: CSRGraph, alpha=None, residual_tol=1e-15, max_iter=None) -> OracleScores:
+    """baselines.py:71-129: plain CG on (I - alpha*A) z = 1 from z = 1."""
+    alpha = _baseline_alpha(g, alpha)
+    if not residual_tol > 0:
+        raise OracleBaselineError("parameter")
+    if not g.is_symmetric():
+        raise OracleBaselineError("not_applicable")
+    n = g.node_count
+    if max_iter is None:
+        max_iter = 10 * n + 100
+
+    def system(v):
+        return v - alpha * csr_matvec(g, v)
+
+    b = np.ones(n)
+    x = np.ones(n)
+    r = b - system(x)
+    rs = float(r @ r)
+    it = 0
+    if np.sqrt(rs) >= residual_tol:
+        p = r.copy()
+        while it < max_iter:
+            Ap = system(p)
+            denom = float(p @ Ap)
+            if denom <= 0.0 or not np.isfinite(denom):
+                raise OracleBaselineError("numeric")
+            step = rs / denom
+            x += step * p
+            r -= step * Ap
+            rs_next = float(r @ r)
+            it += 1
+            if np.sqrt(rs_next) < residual_tol:
+                rs = rs_next
+                break
+            p = r + (rs_next / rs) * p
+            rs = rs_next
+        else:
+            raise OracleBaselineError(
+                "convergence", OracleScores("cg", alpha * csr_matvec(g, x), it,
+                                            float(np.sqrt(rs))), it)
+    return OracleScores("cg", alpha * csr_matvec(g, x), iterations=it,
+                        residual=float(np.sqrt(rs)))
+
+
+def dense_oracle(g: CSRGraph, alpha=None) -> OracleScores:
+    """baselines.py:132-154: LU solve of (I - alpha*A) z = 1; alpha*A*z."""
+    if g.node_count > 2000:
+        raise OracleBaselineError("parameter")
+    alpha = _baseline_alpha(g, alpha)
+    A = np.zeros((g.node_count, g.node_count))
+    for v in range(g.node_count):
+        A[v, g.indices[g.indptr[v]:g.indptr[v + 1]]] = 1.0
+    z = np.linalg.solve(np.eye(g.node_count) - alpha * A, np.ones(g.node_count))
+    return OracleScores("dense", alpha * (A @ z))
+
+
+def inversions(seq: np.ndarray) -> int:
+    """Pairs i < j with seq[i] > seq[j] (cli.py:363-386 counts the same by
+    merge sort); here a Fenwick tree over the values 0..n-1."""
+    seq = np.asarray(seq, dtype=np.int64)
+    n = seq.size
+    tree = np.zeros(n + 1, dtype=np.int64)
+    inv = 0
+    for i in range(n - 1, -1, -1):           # count smaller values to the right
+        j = int(seq[i])
+        while j > 0:
+            inv += int(tree[j])
+            j -= j & -j
+        j = int(seq[i]) + 1
+        while j <= n:
+            tree[j] += 1
+            j += j & -j
+    return inv
+
+
+def concordant_fraction(order_a, order_b) -> float:
+    """cli.py:349-360."""
+    n = len(order_a)
+    if n < 2:
+        return 1.0
+    pos = np.empty(n, dtype=np.int64)
+    pos[np.asarray(order_a)] = np.arange(n)
+    seq = pos[np.asarray(order_b)]
+    return 1.0 - inversions(seq) / (n * (n - 1) // 2)

@@ -381,6 +381,34 @@ int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upp
     });
 }
 
+int kb_foster(kb_graph *gh, double alpha, double tol, int64_t max_iter, double *values,
+              int64_t *iterations, double *residual) {
+    return guarded([&] {
+        KB_REQUIRE(gh && values && iterations && residual, KB_EPARAM, "NULL argument");
+        KB_REQUIRE(std::isfinite(alpha) && alpha > 0, KB_EPARAM, "alpha must be finite and > 0");
+        KB_REQUIRE(tol > 0, KB_EPARAM, "tol must be > 0");
+        KB_REQUIRE(max_iter >= 1, KB_EPARAM, "max_iter must be >= 1");
+        use_device(gh->g.device);
+        const bool ok = foster(gh->g, alpha, tol, max_iter, values, iterations, residual);
+        KB_REQUIRE(ok, KB_ECONVERGENCE, "foster did not reach tol within max_iter iterations");
+    });
+}
+
+int kb_cg_katz(kb_graph *gh, double alpha, double residual_tol, int64_t max_iter,
+               double *values, int64_t *iterations, double *residual) {
+    return guarded([&] {
+        KB_REQUIRE(gh && values && iterations && residual, KB_EPARAM, "NULL argument");
+        KB_REQUIRE(std::isfinite(alpha) && alpha > 0, KB_EPARAM, "alpha must be finite and > 0");
+        KB_REQUIRE(residual_tol > 0, KB_EPARAM, "residual_tol must be > 0");
+        KB_REQUIRE(max_iter >= 0, KB_EPARAM, "max_iter must be >= 0");
+        use_device(gh->g.device);
+        const int st = cg_katz(gh->g, alpha, residual_tol, max_iter, values, iterations,
+                               residual);
+        KB_REQUIRE(st != 2, KB_ENUMERIC, "conjugate gradient broke down (non-positive curvature)");
+        KB_REQUIRE(st == 0, KB_ECONVERGENCE, "cg residual still above residual_tol");
+    });
+}
+
 int kb_stream(int device, void **stream) {
     return guarded([&] {
         KB_REQUIRE(stream, KB_EPARAM, "NULL argument");

@@ -207,6 +207,10 @@ void apply_cut(State &s, cudaStream_t st, uint64_t kstar, int64_t istar);
 void select_global(int device, const uint64_t *keys, const int64_t *labels, const double *uppers,
                    int64_t ncand, int64_t k, double eps, uint64_t *kstar, int64_t *istar,
                    int *prefix_ok);
+bool foster(Graph &g, double alpha, double tol, int64_t max_iter, double *h_values,
+            int64_t *iterations, double *residual);
+int cg_katz(Graph &g, double alpha, double residual_tol, int64_t max_iter, double *h_values,
+            int64_t *iterations, double *residual);
 void shard_propose(State &s, cudaStream_t st, int64_t k, unsigned long long *blk);
 void shard_cut(State &s, cudaStream_t st, const unsigned long long *blocks, int64_t P, int64_t k,
                long long *word);
