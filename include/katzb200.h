@@ -221,6 +221,13 @@ int kb_foster(kb_graph *g, double alpha, double tol, int64_t max_iter,
 int kb_cg_katz(kb_graph *g, double alpha, double residual_tol, int64_t max_iter,
                double *values, int64_t *iterations, double *residual);
 
+/* cli.concordant_fraction (cli.py:349-386): the number of node pairs the two
+ * rankings (permutations of 0..n-1, host arrays) order differently;
+ * concordant fraction = 1 - inversions / (n(n-1)/2).  KB_EPARAM unless both
+ * are permutations. */
+int kb_ranking_inversions(int device, int64_t n, const int64_t *order_a,
+                          const int64_t *order_b, int64_t *inversions);
+
 /* the library's stream on `device` (every call above is ordered on it; a
  * caller running collectives on the same stream needs no host sync) */
 int kb_stream(int device, void **stream);

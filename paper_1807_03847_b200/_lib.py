@@ -104,6 +104,7 @@ SIGNATURES = {
     "kb_rank_bounds": (i32, [i32, i64, vp, vp, vp, ctypes.POINTER(i64)]),
     "kb_foster": (i32, [vp, dbl, dbl, i64, vp, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
     "kb_cg_katz": (i32, [vp, dbl, dbl, i64, vp, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
+    "kb_ranking_inversions": (i32, [i32, i64, vp, vp, ctypes.POINTER(i64)]),
     "kb_stream": (i32, [i32, ctypes.POINTER(vp)]),
     "kb_shard_propose": (i32, [vp, i64, vp]),
     "kb_shard_cut": (i32, [vp, vp, i64, i64, vp]),

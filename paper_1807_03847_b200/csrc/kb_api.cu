@@ -409,6 +409,16 @@ int kb_cg_katz(kb_graph *gh, double alpha, double residual_tol, int64_t max_iter
     });
 }
 
+int kb_ranking_inversions(int device, int64_t n, const int64_t *order_a,
+                          const int64_t *order_b, int64_t *inversions) {
+    return guarded([&] {
+        KB_REQUIRE(inversions && n >= 0 && (n == 0 || (order_a && order_b)), KB_EPARAM,
+                   "NULL argument");
+        use_device(device);
+        *inversions = count_inversions(order_a, order_b, n);
+    });
+}
+
 int kb_stream(int device, void **stream) {
     return guarded([&] {
         KB_REQUIRE(stream, KB_EPARAM, "NULL argument");

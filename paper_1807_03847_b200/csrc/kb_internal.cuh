@@ -207,6 +207,7 @@ void apply_cut(State &s, cudaStream_t st, uint64_t kstar, int64_t istar);
 void select_global(int device, const uint64_t *keys, const int64_t *labels, const double *uppers,
                    int64_t ncand, int64_t k, double eps, uint64_t *kstar, int64_t *istar,
                    int *prefix_ok);
+int64_t count_inversions(const int64_t *h_order_a, const int64_t *h_order_b, int64_t n);
 bool foster(Graph &g, double alpha, double tol, int64_t max_iter, double *h_values,
             int64_t *iterations, double *residual);
 int cg_katz(Graph &g, double alpha, double residual_tol, int64_t max_iter, double *h_values,

@@ -111,9 +111,37 @@ def main():
         arrays[f"conc{i}/c"] = c
         conc.append(dict(key=f"conc{i}", n=n, ab=concordant_fraction(a, b),
                          ac=concordant_fraction(a, c), aa=concordant_fraction(a, a)))
+    # the compare command's JSON report and a static CSV, via the reference
+    # CLI itself (cli.py:293-346, reports.py)
+    import tempfile
+    from katzbounds import cli
+    from katzbounds import reports as R
+    from katzbounds.graph import dumps_edge_list
+    reports = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for name in ("grid7x7", "er60_1", "star50"):
+            g = G[name]
+            path = os.path.join(tmp, f"{name}.txt")
+            with open(path, "w") as fh:
+                fh.write(dumps_edge_list(g.node_count, sorted(
+                    (u, v) for u, v in g.arcs() if u < v)))
+            out = os.path.join(tmp, f"{name}.json")
+            assert cli.main(["compare", path, "--undirected", "--out-file", out]) == 0
+            csv_out = os.path.join(tmp, f"{name}.csv")
+            assert cli.main(["static", path, "--undirected", "--out", "csv",
+                             "--out-file", csv_out]) == 0
+            with open(out) as fh, open(csv_out) as fc:
+                reports.append(dict(graph=name, n=g.node_count, compare_json=fh.read(),
+                                    static_csv=fc.read()))
+    sample = {"a": 1.0, "b": 0.1, "c": -0.0, "d": float("nan"), "e": float("inf"),
+              "f": 1e-300, "g": 123456789012345678, "h": [], "i": {}, "j": [1, 2.5, None, True],
+              "k": {"x": "q\"uote", "y": [{"z": 3}]}, "l": 2.0 ** 70}
+    samples = dict(json=R.dumps_json(sample), json4=R.dumps_json(sample, indent=4),
+                   floats=[R.format_float(x) for x in (1.0, 0.1, 1e22, 1e-7, 123.0, 2.0 ** 60)])
     np.savez_compressed(os.path.join(HERE, "baselines_cases.npz"), **arrays)
     with open(os.path.join(HERE, "baselines.json"), "w") as fh:
-        json.dump(dict(cases=index, concordant=conc), fh, indent=1)
+        json.dump(dict(cases=index, concordant=conc, reports=reports, samples=samples), fh,
+                  indent=1)
     print("cases", len(index), "concordant", len(conc))
 
 
