@@ -48,6 +48,7 @@ enum { KB_VEC_LEVEL = 0, KB_VEC_KATZ = 1, KB_VEC_LOWER = 2, KB_VEC_UPPER = 3 };
 
 typedef struct kb_graph kb_graph;
 typedef struct kb_state kb_state;
+typedef struct kb_text kb_text;
 
 typedef struct {
     int64_t n;                /* node_count                                  */
@@ -208,6 +209,27 @@ int kb_check_apply_cut(kb_state *s, uint64_t kstar, int64_t istar, int64_t *acti
 /* ranking_result + separated pairs on caller vectors indexed by node id */
 int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
                    int64_t *order, int64_t *separated_pairs);
+
+/* graph.load_edge_list (graph.py:260-320) / dynamic.load_batches
+ * (dynamic.py:216-253), parsed on the device.  scan: copies `bytes` to the
+ * device, splits lines at '\n' and classifies each one; info[0..4] =
+ * lines, arc lines, anomaly lines, first arc line (-1: none), max arc id.
+ * Anomalies (anything outside the plain ASCII grammar, and every "NODES"
+ * line) are for the caller to re-read with the reference's exact rules:
+ * candidates writes (line index, byte start, byte end) triples in line
+ * order.  lines copies the per-line class (edges: 0 skip, 1 arc, 2 header,
+ * 3 anomaly; batches: 0 separator, 1 insert, 4 delete, 3 anomaly) and ids.
+ * create_text builds the canonical CSR of the arc lines plus `n_extra`
+ * caller-resolved (u, v) pairs over [0, n), with reversals if undirected. */
+int kb_text_scan(int device, const void *bytes, int64_t nbytes, int batches,
+                 kb_text **out, int64_t *info);
+int kb_text_candidates(kb_text *t, int64_t *lines);
+int kb_text_lines(kb_text *t, uint8_t *kind, int32_t *u, int32_t *v);
+int kb_text_destroy(kb_text *t);
+int kb_graph_create_text(kb_text *t, int64_t n, int undirected,
+                         const int64_t *extra_arcs, int64_t n_extra,
+                         int64_t split_threshold, int64_t hot_size,
+                         kb_graph **out);
 
 /* baselines.foster (baselines.py:36-68): c <- alpha*A*c + 1 from ones until
  * max|change| < tol; values = c - 1 by original id (n doubles).  At the cap:

@@ -102,6 +102,11 @@ SIGNATURES = {
                                ctypes.POINTER(i64), ctypes.POINTER(i32)]),
     "kb_check_apply_cut": (i32, [vp, ctypes.c_uint64, i64, ctypes.POINTER(i64)]),
     "kb_rank_bounds": (i32, [i32, i64, vp, vp, vp, ctypes.POINTER(i64)]),
+    "kb_text_scan": (i32, [i32, vp, i64, i32, ctypes.POINTER(vp), vp]),
+    "kb_text_candidates": (i32, [vp, vp]),
+    "kb_text_lines": (i32, [vp, vp, vp, vp]),
+    "kb_text_destroy": (i32, [vp]),
+    "kb_graph_create_text": (i32, [vp, i64, i32, vp, i64, i64, i64, ctypes.POINTER(vp)]),
     "kb_foster": (i32, [vp, dbl, dbl, i64, vp, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
     "kb_cg_katz": (i32, [vp, dbl, dbl, i64, vp, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
     "kb_ranking_inversions": (i32, [i32, i64, vp, vp, ctypes.POINTER(i64)]),

@@ -21,6 +21,9 @@ struct kb_graph {
 struct kb_state {
     kb::State s;
 };
+struct kb_text {
+    kb::TextScan t;
+};
 
 namespace kb {
 
@@ -488,6 +491,76 @@ int kb_graph_create_rmat(int device, int scale, int64_t edge_factor, const uint6
             rmat_device_csr(scale, edge_factor, pcg_state, a, ab, abc, g.indptr, g.indices,
                             g.nnz);
             g.symmetric = 1;
+            build_graph_device(g);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int kb_text_scan(int device, const void *bytes, int64_t nbytes, int batches, kb_text **out,
+                 int64_t *info) {
+    return guarded([&] {
+        KB_REQUIRE(out && info && nbytes >= 0 && (nbytes == 0 || bytes), KB_EPARAM,
+                   "NULL argument");
+        use_device(device);
+        auto *t = new kb_text();
+        try {
+            t->t.device = device;
+            text_scan(t->t, (const char *)bytes, nbytes, batches ? 1 : 0);
+        } catch (...) {
+            delete t;
+            throw;
+        }
+        const TextScan &s = t->t;
+        info[0] = s.n_lines;
+        info[1] = s.n_arcs;
+        info[2] = s.n_cand;
+        info[3] = s.first_arc_line;
+        info[4] = s.max_id;
+        *out = t;
+    });
+}
+
+int kb_text_candidates(kb_text *t, int64_t *lines) {
+    return guarded([&] {
+        KB_REQUIRE(t && (lines || !t->t.n_cand), KB_EPARAM, "NULL argument");
+        use_device(t->t.device);
+        text_candidates(t->t, lines);
+    });
+}
+
+int kb_text_lines(kb_text *t, uint8_t *kind, int32_t *u, int32_t *v) {
+    return guarded([&] {
+        KB_REQUIRE(t, KB_EPARAM, "NULL argument");
+        use_device(t->t.device);
+        text_lines(t->t, kind, u, v);
+    });
+}
+
+int kb_text_destroy(kb_text *t) {
+    return guarded([&] {
+        if (!t) return;
+        use_device(t->t.device);
+        delete t;
+    });
+}
+
+int kb_graph_create_text(kb_text *t, int64_t n, int undirected, const int64_t *extra_arcs,
+                         int64_t n_extra, int64_t split_threshold, int64_t hot_size,
+                         kb_graph **out) {
+    return guarded([&] {
+        KB_REQUIRE(t && out && n_extra >= 0 && (n_extra == 0 || extra_arcs), KB_EPARAM,
+                   "NULL argument");
+        KB_REQUIRE(n >= 1, KB_EPARAM, "graph must have at least one node");
+        kb_graph *h = new_graph(t->t.device, split_threshold, hot_size);
+        try {
+            Graph &g = h->g;
+            g.n = n;
+            text_csr(t->t, n, undirected, extra_arcs, n_extra, g.indptr, g.indices, g.nnz);
+            g.symmetric = undirected ? 1 : -1;
             build_graph_device(g);
         } catch (...) {
             delete h;

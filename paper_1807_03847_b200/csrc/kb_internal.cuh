@@ -180,7 +180,25 @@ struct State {
     const double *x_level() const { return levels.back().p; }
 };
 
+// A scanned text file (kb_text.cu): bytes, newline offsets, per-line class
+// and ids, anomaly lines and arc lines (indices, ascending)
+struct TextScan {
+    int device = 0;
+    int batches = 0;
+    int64_t nbytes = 0, n_nl = 0, n_lines = 0, n_cand = 0, n_arcs = 0;
+    int64_t first_arc_line = -1, max_id = -1;
+    DBuf<char> buf;
+    DBuf<int64_t> nl, cand, arcs;
+    DBuf<uint8_t> kind;
+    DBuf<int32_t> u, v;
+};
+
 // ---------------------------------------------------------------- kernels
+void text_scan(TextScan &t, const char *h_bytes, int64_t nbytes, int batches);
+void text_candidates(TextScan &t, int64_t *h_out);
+void text_lines(TextScan &t, uint8_t *h_kind, int32_t *h_u, int32_t *h_v);
+void text_csr(TextScan &t, int64_t n, int undirected, const int64_t *h_extra, int64_t n_extra,
+              DBuf<int64_t> &indptr, DBuf<int32_t> &indices, int64_t &nnz);
 void launch_iterate(State &s, cudaStream_t st);
 void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only);
 void collect_k1_times(State &s);
