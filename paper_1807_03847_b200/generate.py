@@ -217,3 +217,52 @@ def grid_graph(n: int, *, device: int = 0, split_threshold: int = 0,
     _lib.check(_lib.lib().kb_graph_create_grid(device, n, split_threshold, hot_size,
                                                ctypes.byref(h)))
     return DeviceResidentGraph(_wrap(h, device))
+
+
+MODELS = ("complete", "star", "path", "grid", "rmat")
+
+
+def _need(cond: bool, message: str) -> None:
+    if not cond:
+        raise ParameterError(message)
+
+
+def _upper_pairs(g: DeviceResidentGraph) -> np.ndarray:
+    """(u, v) with u < v of a symmetric device graph, in (u, v) order."""
+    ip, ix = g.csr_arrays()
+    rows = np.repeat(np.arange(g.node_count, dtype=np.int64), np.diff(ip))
+    keep = rows < ix
+    return np.stack([rows[keep], ix[keep].astype(np.int64)], axis=1)
+
+
+def generate(model: str, n: int, *, seed: int = 0, edge_factor: int = 8,
+             as_array: bool = False, device: int = 0):
+    """generate.py:89-103: the undirected edge pairs (u < v) of a benchmark
+    instance, in the reference's order.  rmat and grid come from the device
+    generators (bit-identical replays); as_array=True returns an (m, 2)
+    int64 array instead of a list of tuples."""
+    if model == "complete":
+        _need(n >= 1, f"complete model needs >= 1 node, got {n}")
+        iu = np.triu_indices(n, 1)
+        e = np.stack([iu[0], iu[1]], axis=1).astype(np.int64)
+    elif model == "star":
+        _need(n >= 1, f"star model needs >= 1 node, got {n}")
+        e = np.stack([np.zeros(n - 1, dtype=np.int64), np.arange(1, n, dtype=np.int64)], axis=1)
+    elif model == "path":
+        _need(n >= 1, f"path model needs >= 1 node, got {n}")
+        a = np.arange(n - 1, dtype=np.int64)
+        e = np.stack([a, a + 1], axis=1)
+    elif model == "grid":
+        _need(n >= 1, f"grid model needs >= 1 node, got {n}")
+        e = _upper_pairs(grid_graph(n, device=device)) if n > 1 else np.zeros((0, 2), np.int64)
+    elif model == "rmat":
+        _need(n >= 2 and (n & (n - 1)) == 0,
+              f"rmat model needs a power-of-two node count >= 2, got {n}")
+        _need(edge_factor >= 1, f"edge_factor must be >= 1, got {edge_factor}")
+        e = _upper_pairs(rmat_graph(n, edge_factor=edge_factor, seed=seed, device=device))
+    else:
+        raise ParameterError(f"unknown model {model!r}; choose one of {', '.join(MODELS)}")
+    e = e.reshape(-1, 2)
+    if as_array:
+        return e
+    return list(zip(e[:, 0].tolist(), e[:, 1].tolist()))

@@ -151,6 +151,18 @@ def main():
                         "indptr_sum": int(np.asarray(ip, dtype=np.int64).sum()),
                         "indices_sum": int(np.asarray(g.out_csr().indices,
                                                       dtype=np.int64).sum())}
+    # generate() (generate.py:89-103): edge-list digests
+    import hashlib
+    gen = []
+    for model, n, kw in [("grid", 1, {}), ("grid", 2, {}), ("grid", 3, {}), ("grid", 10, {}),
+                         ("grid", 17, {}), ("grid", 1000, {}), ("rmat", 2, {}),
+                         ("rmat", 1024, {}), ("rmat", 4096, dict(seed=3, edge_factor=16)),
+                         ("rmat", 1 << 15, dict(seed=42, edge_factor=16)),
+                         ("star", 7, {}), ("path", 5, {}), ("complete", 6, {})]:
+        e = np.asarray(K.generate(model, n, **kw), dtype=np.int64).reshape(-1, 2)
+        gen.append(dict(model=model, n=n, kw=kw, m=int(e.shape[0]),
+                        sha=hashlib.sha256(e.tobytes()).hexdigest()[:16]))
+    out["generate"] = gen
     with open(os.path.join(HERE, "textio.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print("edges", len(out["edges"]), "batches", len(out["batches"]))

@@ -108,3 +108,17 @@ def test_large_generated_edge_list_roundtrip(tmp_path):
     ip2, ix2 = h.csr_arrays()
     np.testing.assert_array_equal(ip2, ip)
     np.testing.assert_array_equal(ix2, ix)
+
+
+def test_generate_matches_reference_digests(tio):
+    import hashlib
+    for rec in tio["generate"]:
+        e = P.generate(rec["model"], rec["n"], as_array=True, **rec["kw"])
+        assert e.shape[0] == rec["m"], rec
+        assert hashlib.sha256(np.ascontiguousarray(e, dtype=np.int64).tobytes()).hexdigest()[:16] \
+            == rec["sha"], rec
+    assert P.generate("star", 4) == [(0, 1), (0, 2), (0, 3)]
+    with pytest.raises(P.ParameterError):
+        P.generate("rmat", 3)
+    with pytest.raises(P.ParameterError):
+        P.generate("nope", 3)
