@@ -205,7 +205,7 @@ def run_grid(a, device):
     """C4: grid 4096^2, Ranking(eps=1e-9) -- many iterations, deg <= 4."""
     import paper_1807_03847_b200 as P
     from paper_1807_03847_b200 import _lib
-    from paper_1807_03847_b200 import generate as G
+    from paper_1807_03847_b200 import generators as G
     L = _lib.lib()
     n = 1 << a.scale
     g = G.grid_graph(n, device=device)
@@ -257,7 +257,7 @@ def run_dynamic(a, device):
 
     import paper_1807_03847_b200 as P
     from paper_1807_03847_b200 import _lib
-    from paper_1807_03847_b200 import generate as G
+    from paper_1807_03847_b200 import generators as G
     L = _lib.lib()
     n = 1 << a.scale
     g = G.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed, device=device)
@@ -324,7 +324,7 @@ def run_sharded(a, rank, world, local):
     import paper_1807_03847_b200 as P
     from paper_1807_03847_b200 import _lib
     from paper_1807_03847_b200 import distributed as D
-    from paper_1807_03847_b200 import generate as G
+    from paper_1807_03847_b200 import generators as G
     torch.cuda.set_device(local)
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -412,7 +412,7 @@ def main():
 
     import paper_1807_03847_b200 as P
     from paper_1807_03847_b200 import _lib
-    from paper_1807_03847_b200 import generate as G
+    from paper_1807_03847_b200 import generators as G
 
     dist = None
     if world > 1:

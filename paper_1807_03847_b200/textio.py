@@ -187,7 +187,7 @@ def load_edge_list(source, undirected: bool = False, *, device: int = 0,
         if scan is not None:
             scan.close()
         src.close()
-    from .generate import DeviceResidentGraph, _wrap
+    from .generators import DeviceResidentGraph, _wrap
     dg = _wrap(h, device)
     if resident:
         g = DeviceResidentGraph(dg)

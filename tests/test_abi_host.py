@@ -135,7 +135,7 @@ def test_graph_mutation_and_batch_rules():
 
 
 def test_generator_pcg_state_and_thresholds():
-    from paper_1807_03847_b200 import generate as G
+    from paper_1807_03847_b200 import generators as G
     st = G.pcg64_state(42)
     ref = np.random.default_rng(42).bit_generator.state["state"]
     assert (int(st[0]) << 64 | int(st[1])) == int(ref["state"])

@@ -11,7 +11,7 @@ from oracle import katz_oracle as O
 pytestmark = pytest.mark.gpu
 
 P = pytest.importorskip("paper_1807_03847_b200")
-from paper_1807_03847_b200 import generate as G  # noqa: E402
+from paper_1807_03847_b200 import generators as G  # noqa: E402
 
 
 def h16(a) -> str:

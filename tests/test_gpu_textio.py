@@ -96,7 +96,7 @@ def test_snap_like_file_and_engine_reuse(tio, tmp_path):
 
 def test_large_generated_edge_list_roundtrip(tmp_path):
     """dumps_edge_list -> load_edge_list on an R-MAT s16 graph (1.8M arcs)."""
-    from paper_1807_03847_b200 import generate as G
+    from paper_1807_03847_b200 import generators as G
     g = G.rmat_graph(1 << 16, edge_factor=16, seed=42)
     ip, ix = g.csr_arrays()
     rows = np.repeat(np.arange(g.node_count), np.diff(ip))

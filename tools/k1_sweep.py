@@ -15,7 +15,7 @@ import numpy as np  # noqa: E402
 
 import paper_1807_03847_b200 as P  # noqa: E402
 from paper_1807_03847_b200 import _lib  # noqa: E402
-from paper_1807_03847_b200 import generate as G  # noqa: E402
+from paper_1807_03847_b200 import generators as G  # noqa: E402
 
 
 def main():

@@ -18,7 +18,7 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1807_03847_b200 as P  # noqa: E402
 from paper_1807_03847_b200 import distributed as D  # noqa: E402
-from paper_1807_03847_b200 import generate as G  # noqa: E402
+from paper_1807_03847_b200 import generators as G  # noqa: E402
 
 SCALE = int(os.environ.get("SCALE", "24"))
 
