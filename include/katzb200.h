@@ -250,6 +250,14 @@ int kb_cg_katz(kb_graph *g, double alpha, double residual_tol, int64_t max_iter,
 int kb_ranking_inversions(int device, int64_t n, const int64_t *order_a,
                           const int64_t *order_b, int64_t *inversions);
 
+/* device memory held by the library: info[0..3] = stream-ordered pool
+ * (buffers < 64 MiB) reserved bytes, reserved high-water mark, used bytes,
+ * used high-water mark; info[4..5] = bytes held in large cached blocks
+ * (>= 64 MiB, cudaMalloc'd, reused best-fit) and the part in use.  reserve
+ * grows the pool by one allocation of `bytes` returned to it at once. */
+int kb_pool_info(int device, int64_t *info);
+int kb_pool_reserve(int device, int64_t bytes);
+
 /* the library's stream on `device` (every call above is ordered on it; a
  * caller running collectives on the same stream needs no host sync) */
 int kb_stream(int device, void **stream);

@@ -15,6 +15,9 @@
 
 #include "kb_internal.cuh"
 
+#include <map>
+#include <unordered_map>
+
 struct kb_graph {
     kb::Graph g;
 };
@@ -56,6 +59,106 @@ cudaStream_t device_stream() {
         }
     }
     return streams[dev];
+}
+
+namespace {
+struct BigCache {
+    std::multimap<size_t, void *> idle;      // size -> block
+    std::unordered_map<void *, size_t> live;
+    size_t held = 0;                          // bytes in live + idle blocks
+};
+std::mutex g_big_mu;
+BigCache g_big[64];
+
+int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+void flush_idle(BigCache &c) {
+    if (c.idle.empty()) return;
+    cudaStreamSynchronize(device_stream());
+    for (auto &kv : c.idle) {
+        cudaFree(kv.second);
+        c.held -= kv.first;
+    }
+    c.idle.clear();
+}
+}  // namespace
+
+void *dev_alloc(size_t bytes) {
+    cudaStream_t st = device_stream();
+    void *p = nullptr;
+    if (bytes < BIG_ALLOC) {
+        KB_CUDA(cudaMallocAsync(&p, bytes, st));
+        return p;
+    }
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    BigCache &c = g_big[cur_device()];
+    // best fit among idle blocks, wasting at most a quarter of the block
+    auto it = c.idle.lower_bound(bytes);
+    if (it != c.idle.end() && it->first - bytes <= it->first / 4) {
+        p = it->second;
+        c.live[p] = it->first;
+        c.idle.erase(it);
+        return p;
+    }
+    const size_t sz = (bytes + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e == cudaErrorMemoryAllocation) {
+        (void)cudaGetLastError();
+        flush_idle(c);                        // give cached blocks back and retry
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cur_device()) == cudaSuccess)
+            cudaMemPoolTrimTo(pool, 0);
+        e = cudaMalloc(&p, sz);
+    }
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error{e == cudaErrorMemoryAllocation ? KB_ENOMEM : KB_ECUDA,
+                    std::string("device allocation of ") + std::to_string(sz) + " bytes: " +
+                        cudaGetErrorString(e)};
+    }
+    c.live[p] = sz;
+    c.held += sz;
+    return p;
+}
+
+void dev_free(void *p, size_t bytes) {
+    if (!p) return;
+    if (bytes < BIG_ALLOC) {
+        cudaFreeAsync(p, device_stream());
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    BigCache &c = g_big[cur_device()];
+    auto it = c.live.find(p);
+    if (it == c.live.end()) {
+        cudaFreeAsync(p, device_stream());
+        return;
+    }
+    c.idle.emplace(it->second, p);            // reused in stream order
+    c.live.erase(it);
+}
+
+void dev_mem_info(int64_t info[6]) {
+    cudaMemPool_t pool;
+    KB_CUDA(cudaDeviceGetDefaultMemPool(&pool, cur_device()));
+    const cudaMemPoolAttr at[4] = {cudaMemPoolAttrReservedMemCurrent,
+                                   cudaMemPoolAttrReservedMemHigh,
+                                   cudaMemPoolAttrUsedMemCurrent, cudaMemPoolAttrUsedMemHigh};
+    for (int i = 0; i < 4; i++) {
+        uint64_t v = 0;
+        KB_CUDA(cudaMemPoolGetAttribute(pool, at[i], &v));
+        info[i] = (int64_t)v;
+    }
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    BigCache &c = g_big[cur_device()];
+    size_t live = 0;
+    for (auto &kv : c.live) live += kv.second;
+    info[4] = (int64_t)c.held;
+    info[5] = (int64_t)live;
 }
 
 // page-locked mirror for small device->host reads; one per host thread, used
@@ -419,6 +522,28 @@ int kb_ranking_inversions(int device, int64_t n, const int64_t *order_a,
                    "NULL argument");
         use_device(device);
         *inversions = count_inversions(order_a, order_b, n);
+    });
+}
+
+int kb_pool_info(int device, int64_t *info) {
+    return guarded([&] {
+        KB_REQUIRE(info, KB_EPARAM, "NULL argument");
+        use_device(device);
+        (void)device_stream();
+        dev_mem_info(info);
+    });
+}
+
+int kb_pool_reserve(int device, int64_t bytes) {
+    return guarded([&] {
+        KB_REQUIRE(bytes >= 0, KB_EPARAM, "bad size");
+        use_device(device);
+        cudaStream_t st = device_stream();
+        if (!bytes) return;
+        void *p = nullptr;
+        KB_CUDA(cudaMallocAsync(&p, (size_t)bytes, st));
+        KB_CUDA(cudaFreeAsync(p, st));
+        KB_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -56,14 +56,112 @@ __global__ void k_capacity(const int32_t *rlen, const int32_t *extra, int64_t n,
     cap[v] = need + max((int64_t)2, need / 8);
 }
 
-__global__ void k_copy_rows(const int64_t *old_ip, const int32_t *old_ix, const int32_t *rlen,
-                            int64_t n, const int64_t *new_ip, int32_t *new_ix) {
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n) return;
-    const int64_t a = old_ip[warp], b = new_ip[warp];
-    for (int64_t j = lane; j < rlen[warp]; j += 32) new_ix[b + j] = old_ix[a + j];
+__global__ void k_cap32(const int64_t *cap, int64_t n, int32_t *rcap) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < n) rcap[v] = (int32_t)min(cap[v], (int64_t)INT32_MAX);
 }
+
+// move row rows[e] (old content, rlen slots) to new_start[e], capacity new_cap[e]
+__global__ void k_relocate(const int32_t *rows, const int64_t *new_start,
+                           const int32_t *new_cap, int64_t ne, int64_t *indptr,
+                           const int32_t *rlen, int32_t *rcap, int32_t *indices) {
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= ne) return;
+    const int32_t v = rows[e];
+    const int64_t a = indptr[v], b = new_start[e];
+    const int64_t L = rlen[v];
+    for (int64_t j = lane; j < L; j += 32) indices[b + j] = indices[a + j];
+    __syncwarp();
+    if (lane == 0) {
+        indptr[v] = b;
+        rcap[v] = new_cap[e];
+    }
+}
+
+// Row copy old -> new layout.  Short rows: a block takes 256 consecutive
+// rows, scans their lengths in shared memory and copies the concatenated
+// elements with every thread busy (a warp per row would idle most lanes on
+// R-MAT's ~30-arc rows).  Rows longer than LONG_ROW get a block each.
+constexpr int COPY_ROWS = 256;
+constexpr int LONG_ROW = 1024;
+
+__global__ void __launch_bounds__(COPY_ROWS) k_copy_short(const int64_t *old_ip,
+                                                          const int32_t *old_ix,
+                                                          const int32_t *rlen, int64_t n,
+                                                          const int64_t *new_ip,
+                                                          int32_t *new_ix) {
+    __shared__ int64_t a[COPY_ROWS], b[COPY_ROWS];
+    __shared__ int off[COPY_ROWS + 1];
+    const int64_t r0 = (int64_t)blockIdx.x * COPY_ROWS;
+    const int t = threadIdx.x;
+    int len = 0;
+    if (r0 + t < n) {
+        len = rlen[r0 + t];
+        if (len > LONG_ROW) len = 0;
+        a[t] = old_ip[r0 + t];
+        b[t] = new_ip[r0 + t];
+    }
+    // exclusive scan of the lengths (block-wide, Hillis-Steele in smem)
+    off[t + 1] = len;
+    if (t == 0) off[0] = 0;
+    __syncthreads();
+    for (int d = 1; d < COPY_ROWS; d <<= 1) {
+        const int v = (t + 1 > d) ? off[t + 1 - d] : 0;
+        __syncthreads();
+        off[t + 1] += v;
+        __syncthreads();
+    }
+    const int total = off[COPY_ROWS];
+    for (int e = t; e < total; e += COPY_ROWS) {
+        int lo = 0, hi = COPY_ROWS;              // last row with off[row] <= e
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= e) lo = mid; else hi = mid;
+        }
+        const int k = e - off[lo];
+        new_ix[b[lo] + k] = old_ix[a[lo] + k];
+    }
+}
+
+__global__ void k_copy_long(const int32_t *rows, const int64_t *old_ip, const int32_t *old_ix,
+                            const int32_t *rlen, const int64_t *new_ip, int32_t *new_ix) {
+    const int32_t r = rows[blockIdx.x];
+    const int64_t L = rlen[r], a = old_ip[r], b = new_ip[r];
+    for (int64_t j = threadIdx.x; j < L; j += blockDim.x) new_ix[b + j] = old_ix[a + j];
+}
+
+struct IsLongRow {
+    const int32_t *rlen;
+    __device__ bool operator()(int32_t r) const { return rlen[r] > LONG_ROW; }
+};
+
+}  // namespace
+
+static void copy_rows(const int64_t *old_ip, const int32_t *old_ix, const int32_t *rlen, int64_t n,
+               const int64_t *new_ip, int32_t *new_ix, cudaStream_t st) {
+    if (n <= 0) return;
+    k_copy_short<<<nblk(n, COPY_ROWS), COPY_ROWS, 0, st>>>(old_ip, old_ix, rlen, n, new_ip,
+                                                         new_ix);
+    note_launch();
+    DBuf<int32_t> longs;
+    DBuf<int64_t> cnt;
+    longs.alloc(n);
+    cnt.alloc(1);
+    cub::CountingInputIterator<int32_t> it(0);
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, it, longs.p, cnt.p, (int)n, IsLongRow{rlen}, st);
+    });
+    int64_t nl = 0;
+    KB_CUDA(cudaMemcpyAsync(&nl, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    if (nl) {
+        k_copy_long<<<(unsigned)nl, 256, 0, st>>>(longs.p, old_ip, old_ix, rlen, new_ip, new_ix);
+        note_launch();
+    }
+}
+
+namespace {
 
 __global__ void k_compact_len(const int32_t *rlen, int64_t n, int64_t *len) {
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -86,15 +184,30 @@ void respread(Graph &g, const int32_t *extra) {
     int64_t total = 0;
     KB_CUDA(cudaMemcpyAsync(&total, nip.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
+    // reserve tail room for rows that later outgrow their slack (relocated
+    // there instead of re-spreading the whole graph)
+    const int64_t room = std::max<int64_t>(total / 16, (int64_t)1 << 20);
     DBuf<int32_t> nix;
-    nix.alloc(std::max<int64_t>(1, total));
-    k_copy_rows<<<nblk(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.indices.p, g.rlen.p, n, nip.p,
-                                                   nix.p);
+    nix.alloc(total + room);
+    copy_rows(g.indptr.p, g.indices.p, g.rlen.p, n, nip.p, nix.p, st);
+    g.rcap.alloc(std::max<int64_t>(1, n));
+    k_cap32<<<nblk(n, 256), 256, 0, st>>>(cap.p, n, g.rcap.p);
     note_launch();
     g.indptr = std::move(nip);
     g.indices = std::move(nix);
+    g.tail = total;
     g.slack = true;
 }
+
+}  // namespace
+
+// the slack layout the dynamic path edits in place, built once at ingest so
+// the first update does not re-spread (and regrow the memory pool) inside it
+void make_slack(Graph &g) {
+    if (!g.slack) respread(g, nullptr);
+}
+
+namespace {
 
 // ---------------------------------------------------------------- batch edits
 
@@ -147,13 +260,13 @@ __global__ void k_scatter_extra(const int32_t *rows, const int32_t *x, int64_t n
     if (e < ne) dst[rows[e]] = x[e];
 }
 
-__global__ void k_gather_len(const int32_t *rlen, const int64_t *indptr, const int32_t *rows,
+__global__ void k_gather_len(const int32_t *rlen, const int32_t *rcap, const int32_t *rows,
                              int64_t ne, int64_t *len_cap) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= ne) return;
     const int32_t v = rows[e];
     len_cap[2 * e] = rlen[v];
-    len_cap[2 * e + 1] = indptr[v + 1] - indptr[v];
+    len_cap[2 * e + 1] = rcap[v];
 }
 
 // ---------------------------------------------------------------- transpose
@@ -230,6 +343,21 @@ __global__ void k_expand(const int32_t *changed, int64_t nc, const int64_t *in_i
             touched[u] = 1;
         }
     }
+}
+
+// total in-degree of the changed rows: the work an expansion would do
+__global__ void k_work_sum(const int32_t *changed, int64_t nc, const int64_t *in_ip,
+                           const int32_t *in_len, const int32_t *perm,
+                           unsigned long long *work) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long w = 0;
+    if (i < nc) {
+        const int32_t o = perm[changed[i]];
+        w = (unsigned long long)(in_len ? in_len[o] : in_ip[o + 1] - in_ip[o]);
+    }
+#pragma unroll
+    for (int k = 16; k; k >>= 1) w += __shfl_down_sync(0xffffffffu, w, k);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(work, w);
 }
 
 // ---------------------------------------------------------------- recompute
@@ -491,9 +619,7 @@ void compact_csr(Graph &g, DBuf<int64_t> &ip, DBuf<int32_t> &ix) {
         return cub::DeviceScan::ExclusiveSum(t, b, len.p, ip.p, (int)(n + 1), st);
     });
     ix.alloc(std::max<int64_t>(1, g.nnz));
-    k_copy_rows<<<nblk(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.indices.p, g.rlen.p, n, ip.p,
-                                                   ix.p);
-    note_launch();
+    copy_rows(g.indptr.p, g.indices.p, g.rlen.p, n, ip.p, ix.p, st);
     KB_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -525,25 +651,26 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
                           int64_t n_dels) {
     cudaStream_t st = g.stream;
     // group the edits by source row (host; batches are small)
-    struct Edit { int32_t src, dst; int kind; };  // kind 0 = delete, 1 = insert
-    std::vector<Edit> ed;
+    // one 64-bit key per edit: src | kind (0 delete, 1 insert) | dst, so a
+    // plain integer sort groups by row with deletions first, dsts ascending
+    std::vector<uint64_t> ed;
     ed.reserve(n_ins + n_dels);
-    for (int64_t i = 0; i < n_dels; i++) ed.push_back({(int32_t)dels[2 * i], (int32_t)dels[2 * i + 1], 0});
-    for (int64_t i = 0; i < n_ins; i++) ed.push_back({(int32_t)ins[2 * i], (int32_t)ins[2 * i + 1], 1});
+    for (int64_t i = 0; i < n_dels; i++)
+        ed.push_back(((uint64_t)(uint32_t)dels[2 * i] << 33) | (uint32_t)dels[2 * i + 1]);
+    for (int64_t i = 0; i < n_ins; i++)
+        ed.push_back(((uint64_t)(uint32_t)ins[2 * i] << 33) | (1ull << 32) |
+                     (uint32_t)ins[2 * i + 1]);
     if (ed.empty()) return;
     PhaseTrace tr(st);
-    std::sort(ed.begin(), ed.end(), [](const Edit &a, const Edit &b) {
-        return a.src != b.src ? a.src < b.src : (a.kind != b.kind ? a.kind < b.kind : a.dst < b.dst);
-    });
+    std::sort(ed.begin(), ed.end());
     std::vector<int32_t> rows, dl, il;
     std::vector<int64_t> dptr{0}, iptr{0};
     for (size_t i = 0; i < ed.size();) {
+        const uint64_t src = ed[i] >> 33;
         size_t j = i;
-        rows.push_back(ed[i].src);
-        while (j < ed.size() && ed[j].src == ed[i].src) {
-            (ed[j].kind ? il : dl).push_back(ed[j].dst);
-            j++;
-        }
+        rows.push_back((int32_t)src);
+        for (; j < ed.size() && (ed[j] >> 33) == src; j++)
+            ((ed[j] >> 32) & 1 ? il : dl).push_back((int32_t)(uint32_t)ed[j]);
         dptr.push_back((int64_t)dl.size());
         iptr.push_back((int64_t)il.size());
         i = j;
@@ -562,20 +689,43 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
     KB_CUDA(cudaMemcpyAsync(diptr.p, iptr.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
     // capacity check (slack CSR); re-spread once if any edited row overflows
     if (!g.slack) respread(g, nullptr);
-    k_gather_len<<<nblk(ne, 256), 256, 0, st>>>(g.rlen.p, g.indptr.p, drows.p, ne, lc.p);
+    k_gather_len<<<nblk(ne, 256), 256, 0, st>>>(g.rlen.p, g.rcap.p, drows.p, ne, lc.p);
     note_launch();
     std::vector<int64_t> hlc(2 * ne);
     KB_CUDA(cudaMemcpyAsync(hlc.data(), lc.p, 2 * ne * 8, cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    bool overflow = false;
     std::vector<int64_t> toff(ne + 1, 0);
+    std::vector<int32_t> ov_rows, ov_cap;
+    std::vector<int64_t> ov_start;
+    int64_t need = 0;
     for (int64_t e = 0; e < ne; e++) {
         const int64_t nl = hlc[2 * e] - (dptr[e + 1] - dptr[e]) + (iptr[e + 1] - iptr[e]);
-        if (nl > hlc[2 * e + 1]) overflow = true;
+        if (nl > hlc[2 * e + 1]) {            // outgrows its slack: relocate
+            const int64_t cap = nl + std::max<int64_t>(2, nl / 8);
+            ov_rows.push_back(rows[e]);
+            ov_cap.push_back((int32_t)cap);
+            ov_start.push_back(g.tail + need);
+            need += cap;
+        }
         toff[e + 1] = toff[e] + std::max<int64_t>(nl, hlc[2 * e]);
     }
     tr.mark("  capacity check");
-    if (overflow) {
+    if (!ov_rows.empty() && g.tail + need <= (int64_t)g.indices.n) {
+        const int64_t no = (int64_t)ov_rows.size();
+        DBuf<int32_t> r, c;
+        DBuf<int64_t> b;
+        r.alloc(no); c.alloc(no); b.alloc(no);
+        KB_CUDA(cudaMemcpyAsync(r.p, ov_rows.data(), no * 4, cudaMemcpyHostToDevice, st));
+        KB_CUDA(cudaMemcpyAsync(c.p, ov_cap.data(), no * 4, cudaMemcpyHostToDevice, st));
+        KB_CUDA(cudaMemcpyAsync(b.p, ov_start.data(), no * 8, cudaMemcpyHostToDevice, st));
+        k_relocate<<<nblk(no * 32, 256), 256, 0, st>>>(r.p, b.p, c.p, no, g.indptr.p, g.rlen.p,
+                                                      g.rcap.p, g.indices.p);
+        note_launch();
+        KB_CUDA(cudaStreamSynchronize(st));
+        g.tail += need;
+        tr.mark("  relocate rows");
+    } else if (!ov_rows.empty()) {
+        // the tail is full: re-spread everything (with fresh tail room)
         std::vector<int32_t> extra(ne);
         for (int64_t e = 0; e < ne; e++) extra[e] = (int32_t)(iptr[e + 1] - iptr[e]);
         DBuf<int32_t> dex, dx;
@@ -709,7 +859,20 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             continue;
         }
         if (st_out.n_level_sizes < 64) st_out.level_sizes[st_out.n_level_sizes++] = affected;
-        if (nchanged > n / 256) {
+        bool dense = nchanged > n / 256;
+        if (!dense && nchanged) {
+            // a few hubs can carry most of the arcs: decide by the expansion's
+            // arc count (a warp per changed row would serialise on them)
+            KB_CUDA(cudaMemsetAsync(cnt.p + 3, 0, 8, st));
+            k_work_sum<<<nblk(nchanged, 256), 256, 0, st>>>(C.p, nchanged, in_ip, in_len,
+                                                            g.perm.p, cnt.p + 3);
+            note_launch();
+            unsigned long long work = 0;
+            KB_CUDA(cudaMemcpyAsync(&work, cnt.p + 3, 8, cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaStreamSynchronize(st));
+            dense = (int64_t)work > std::max<int64_t>(g.nnz / 64, 1 << 20);
+        }
+        if (dense) {
             // Dense level: the expansion would reach most rows, so recompute
             // the whole level with K1 (identical bits for every row) and
             // find the changed rows by comparison.  The affected set grows by

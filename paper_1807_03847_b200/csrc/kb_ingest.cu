@@ -545,6 +545,7 @@ void build_graph_device(Graph &g) {
         });
     }
     build_sell(g, g.relabel);
+    make_slack(g);
 }
 
 

@@ -40,11 +40,20 @@ void note_launch(int64_t k = 1);
 int64_t launch_count();
 
 // ---------------------------------------------------------------- device buf
-// All device work of a process runs on one non-blocking stream per device;
-// buffers are stream-ordered allocations from the device mempool (release
-// threshold raised at first use), so per-iteration scratch costs no
-// cudaMalloc round trip.
+// All device work of a process runs on one non-blocking stream per device.
+// Buffers come from dev_alloc: below BIG_ALLOC bytes, stream-ordered
+// allocations from the device mempool (release threshold raised at first
+// use, so per-iteration scratch costs no cudaMalloc round trip); from
+// BIG_ALLOC up, cudaMalloc'd blocks kept in a per-device best-fit cache.
+// Measured on B200 (tools/micro/alloc_bench.cu): growing the mempool costs
+// 40-140 ms per GB-sized request and a fragmented pool 1.4 s for 3 GB,
+// against 3-15 ms for cudaMalloc; cached blocks are reused in stream order
+// (one stream per device), so reuse needs no synchronisation.
 cudaStream_t device_stream();
+constexpr size_t BIG_ALLOC = (size_t)64 << 20;
+void *dev_alloc(size_t bytes);
+void dev_free(void *p, size_t bytes);
+void dev_mem_info(int64_t info[6]);
 
 template <typename T>
 struct DBuf {
@@ -62,11 +71,11 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         if (count == 0) count = 1;
-        KB_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), device_stream()));
+        p = (T *)dev_alloc(count * sizeof(T));
         n = count;
     }
     void release() {
-        if (p) cudaFreeAsync(p, device_stream());
+        if (p) dev_free(p, n * sizeof(T));
         p = nullptr;
         n = 0;
     }
@@ -103,12 +112,17 @@ struct Graph {
     DBuf<int32_t> perm;    // new -> original id
     DBuf<int32_t> iperm;   // original -> new id
     DBuf<int32_t> deg;     // out-degree by new id
-    // canonical CSR-with-slack (original ids, rows ascending): row v owns
-    // indices[indptr[v] .. indptr[v+1]) and uses the first rlen[v] slots
+    // canonical CSR-with-slack (original ids, rows ascending): row v starts
+    // at indices[indptr[v]] and uses the first rlen[v] slots.  Compact as
+    // built (capacity = indptr[v+1] - indptr[v]); after the first update
+    // (slack) capacities live in rcap and rows may be relocated to the
+    // reserved tail [tail, indices.n) when a batch outgrows them
     DBuf<int64_t> indptr;
     DBuf<int32_t> indices;
     DBuf<int32_t> rlen;
-    bool slack = false;      // indptr spreads rows apart (after an update)
+    DBuf<int32_t> rcap;
+    int64_t tail = 0;
+    bool slack = false;      // rcap/tail valid (after an update)
     // row maps of the SELL layout; empty while implicit_rows (fresh
     // relabelling: heavy [0,nh), normal [nh,nv), empty [nv,n))
     bool implicit_rows = true;
@@ -211,6 +225,7 @@ void gather_to_original(const Graph &g, const double *src_new, double *dst_orig,
 void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices);
 void build_graph_device(Graph &g);
 void build_sell(Graph &g, bool fresh);
+void make_slack(Graph &g);
 void compact_csr(Graph &g, DBuf<int64_t> &indptr, DBuf<int32_t> &indices);
 void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne);
 void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,

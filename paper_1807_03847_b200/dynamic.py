@@ -66,8 +66,7 @@ def update_batch(state: KatzState, g, batch: EdgeBatch, *, theta: float = 0.5) -
             f"would leave the walk series divergent")
     new_gamma = tail_gamma(state.alpha, new_max)
 
-    ins = np.array(batch.insertions, dtype=np.int64).reshape(-1, 2)
-    dels = np.array(batch.deletions, dtype=np.int64).reshape(-1, 2)
+    ins, dels = (np.ascontiguousarray(a) for a in batch.arrays())
     stats_c = _lib.UpdateStatsC()
     state._touch()
     st = state._L.kb_update_batch(state._h, _lib.ptr(ins), ins.shape[0],

@@ -79,8 +79,7 @@ class DeviceResidentGraph:
 
     def max_degree_after(self, batch: EdgeBatch) -> int:
         """dynamic.py:151-157 evaluated on the device."""
-        i = self._arcs(batch.insertions)
-        d = self._arcs(batch.deletions)
+        i, d = (self._arcs(a) for a in batch.arrays())
         out = ctypes.c_int64()
         _lib.check(_lib.lib().kb_graph_max_degree_after(self._dg.handle, _lib.ptr(i), i.shape[0],
                                                         _lib.ptr(d), d.shape[0],
@@ -130,8 +129,7 @@ class DeviceResidentGraph:
     # ---- mutation (graph.py:201-237)
     def validate_batch(self, batch: EdgeBatch) -> None:
         batch.validate_shape()
-        i = self._arcs(batch.insertions)
-        d = self._arcs(batch.deletions)
+        i, d = (self._arcs(a) for a in batch.arrays())
         pi, pd = self._present(i), self._present(d)
         if pi.any():
             u, v = batch.insertions[int(np.argmax(pi))]

@@ -16,6 +16,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Iterable, Iterator, Sequence
 
+import itertools
+
 import numpy as np
 
 from .errors import BatchPreconditionError, NodeRangeError
@@ -35,8 +37,39 @@ class EdgeBatch:
         self.insertions = [(int(u), int(v)) for u, v in self.insertions]
         self.deletions = [(int(u), int(v)) for u, v in self.deletions]
 
+    def arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        """(insertions, deletions) as (m, 2) int64 arrays, cached per list
+        object and length (the lists are the batch's public state)."""
+        key = (id(self.insertions), len(self.insertions), id(self.deletions),
+               len(self.deletions))
+        cached = self.__dict__.get("_arr")
+        if cached is None or cached[0] != key:
+            i, d = (np.fromiter(itertools.chain.from_iterable(x), dtype=np.int64,
+                                count=2 * len(x)).reshape(-1, 2)
+                    for x in (self.insertions, self.deletions))
+            cached = (key, i, d)
+            self.__dict__["_arr"] = cached
+        return cached[1], cached[2]
+
+    def _keys(self):
+        """u << 32 | v keys when every id fits 31 bits, else None."""
+        try:
+            i, d = self.arrays()
+        except OverflowError:
+            return None
+        for a in (i, d):
+            if a.size and (a.min() < 0 or a.max() > MAX_NODE_ID):
+                return None
+        return (i[:, 0] << 32) | i[:, 1], (d[:, 0] << 32) | d[:, 1]
+
     def validate_shape(self) -> None:
         """Duplicates and overlap (graph.py:46-59)."""
+        k = self._keys()
+        if k is not None:           # vectorised test; messages from the exact path
+            ki, kd = np.sort(k[0]), np.sort(k[1])
+            if not ((ki[1:] == ki[:-1]).any() or (kd[1:] == kd[:-1]).any() or
+                    np.intersect1d(ki, kd, assume_unique=True).size):
+                return
         ins, dels = set(self.insertions), set(self.deletions)
         if len(ins) != len(self.insertions):
             raise BatchPreconditionError(
@@ -51,6 +84,12 @@ class EdgeBatch:
 
     def is_symmetric(self) -> bool:
         """Both lists closed under reversal (graph.py:61-65)."""
+        k = self._keys()
+        if k is not None:
+            # reversal is a bijection, so "closed under it" = equal key sets
+            return all(np.array_equal(sorted_unique(a),
+                                      sorted_unique(((a & 0xFFFFFFFF) << 32) | (a >> 32)))
+                       for a in k)
         ins, dels = set(self.insertions), set(self.deletions)
         return all((v, u) in ins for u, v in ins) and \
             all((v, u) in dels for u, v in dels)
@@ -241,23 +280,28 @@ class Graph:
     def validate_batch(self, batch: EdgeBatch) -> None:
         """graph.py:207-220."""
         batch.validate_shape()
-        for u, v in batch.insertions:
-            self._check_node(u)
-            self._check_node(v)
-        for u, v in batch.deletions:
-            self._check_node(u)
-            self._check_node(v)
+        try:
+            ia, da = batch.arrays()
+        except OverflowError:
+            ia = da = None
+        if ia is None:
+            for u, v in batch.insertions + batch.deletions:
+                self._check_node(u)
+                self._check_node(v)
+        else:
+            for a in (ia, da):      # first offending id in (u, v) order
+                bad = (a < 0) | (a >= self._n)
+                if bad.any():
+                    self._check_node(int(a[bad][0]))
         n = self._n
         if batch.insertions:
-            k = np.array([u * n + v for u, v in batch.insertions], dtype=np.int64)
-            present = self._has_keys(k)
+            present = self._has_keys(ia[:, 0] * n + ia[:, 1])
             if present.any():
                 u, v = batch.insertions[int(np.argmax(present))]
                 raise BatchPreconditionError(
                     f"cannot insert arc ({u}, {v}): already present")
         if batch.deletions:
-            k = np.array([u * n + v for u, v in batch.deletions], dtype=np.int64)
-            present = self._has_keys(k)
+            present = self._has_keys(da[:, 0] * n + da[:, 1])
             if not present.all():
                 u, v = batch.deletions[int(np.argmin(present))]
                 raise BatchPreconditionError(
