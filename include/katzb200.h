@@ -49,6 +49,7 @@ enum { KB_VEC_LEVEL = 0, KB_VEC_KATZ = 1, KB_VEC_LOWER = 2, KB_VEC_UPPER = 3 };
 typedef struct kb_graph kb_graph;
 typedef struct kb_state kb_state;
 typedef struct kb_text kb_text;
+typedef struct kb_ranking kb_ranking;
 
 typedef struct {
     int64_t n;                /* node_count                                  */
@@ -249,6 +250,15 @@ int kb_cg_katz(kb_graph *g, double alpha, double residual_tol, int64_t max_iter,
  * are permutations. */
 int kb_ranking_inversions(int device, int64_t n, const int64_t *order_a,
                           const int64_t *order_b, int64_t *inversions);
+
+/* engine.ranking_result kept on the device (engine.py:399-408): a snapshot
+ * of order (int64 original ids, rank order), lower and upper (by original
+ * id) plus the exact separated-pair count; read copies any slice (which: 0
+ * order, 1 lower, 2 upper; 8-byte elements) to the host, so a caller that
+ * needs only the top k copies k entries. */
+int kb_ranking_snapshot(kb_state *s, kb_ranking **out, int64_t *separated_pairs);
+int kb_ranking_read(kb_ranking *r, int which, int64_t offset, int64_t count, void *host);
+int kb_ranking_destroy(kb_ranking *r);
 
 /* device memory held by the library: info[0..3] = stream-ordered pool
  * (buffers < 64 MiB) reserved bytes, reserved high-water mark, used bytes,

@@ -110,6 +110,9 @@ SIGNATURES = {
     "kb_foster": (i32, [vp, dbl, dbl, i64, vp, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
     "kb_cg_katz": (i32, [vp, dbl, dbl, i64, vp, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
     "kb_ranking_inversions": (i32, [i32, i64, vp, vp, ctypes.POINTER(i64)]),
+    "kb_ranking_snapshot": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]),
+    "kb_ranking_read": (i32, [vp, i32, i64, i64, vp]),
+    "kb_ranking_destroy": (i32, [vp]),
     "kb_pool_info": (i32, [i32, vp]),
     "kb_pool_reserve": (i32, [i32, i64]),
     "kb_stream": (i32, [i32, ctypes.POINTER(vp)]),

@@ -27,6 +27,12 @@ struct kb_state {
 struct kb_text {
     kb::TextScan t;
 };
+struct kb_ranking {
+    int device = 0;
+    int64_t n = 0;
+    kb::DBuf<int64_t> order;
+    kb::DBuf<double> lower, upper;
+};
 
 namespace kb {
 
@@ -544,6 +550,49 @@ int kb_pool_reserve(int device, int64_t bytes) {
         KB_CUDA(cudaMallocAsync(&p, (size_t)bytes, st));
         KB_CUDA(cudaFreeAsync(p, st));
         KB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kb_ranking_snapshot(kb_state *h, kb_ranking **out, int64_t *separated_pairs) {
+    return guarded([&] {
+        KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        auto *r = new kb_ranking();
+        try {
+            r->device = s.g->device;
+            r->n = s.g->n;
+            result_device(s, s.g->stream, &r->order, &r->lower, &r->upper, separated_pairs);
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        *out = r;
+    });
+}
+
+int kb_ranking_read(kb_ranking *r, int which, int64_t offset, int64_t count, void *host) {
+    return guarded([&] {
+        KB_REQUIRE(r && (host || !count), KB_EPARAM, "NULL argument");
+        KB_REQUIRE(which >= 0 && which <= 2, KB_EPARAM, "which: 0 order, 1 lower, 2 upper");
+        KB_REQUIRE(offset >= 0 && count >= 0 && offset + count <= r->n, KB_EPARAM,
+                   "range outside the result");
+        use_device(r->device);
+        if (!count) return;
+        const void *src = which == 0 ? (const void *)(r->order.p + offset)
+                        : which == 1 ? (const void *)(r->lower.p + offset)
+                                     : (const void *)(r->upper.p + offset);
+        cudaStream_t st = device_stream();
+        KB_CUDA(cudaMemcpyAsync(host, src, count * 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kb_ranking_destroy(kb_ranking *r) {
+    return guarded([&] {
+        if (!r) return;
+        use_device(r->device);
+        delete r;
     });
 }
 

@@ -218,6 +218,8 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
 void collect_k1_times(State &s);
 bool run_check(State &s, cudaStream_t st);      // returns converged
 double run_gap(State &s, cudaStream_t st);
+void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
+                   DBuf<double> *upper, int64_t *h_pairs);
 void run_result(State &s, cudaStream_t st, int64_t *order, double *lower,
                 double *upper, int64_t *pairs);
 void gather_to_original(const Graph &g, const double *src_new, double *dst_orig,

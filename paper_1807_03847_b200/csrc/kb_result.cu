@@ -153,8 +153,10 @@ static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_
     note_launch();
 }
 
-void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, double *h_upper,
-                int64_t *h_pairs) {
+// ranking_result on the device: order (int64 original ids), lower and upper
+// by original id, and the exact separated-pair count
+void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
+                   DBuf<double> *upper, int64_t *h_pairs) {
     Graph &g = *s.g;
     const int64_t n = g.n;
     KB_REQUIRE(s.r >= 1, KB_ESTATE, "separated_fraction needs at least one iteration");
@@ -189,26 +191,17 @@ void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, do
                                                           u + 2);
         note_launch();
     }
-    if (h_order) {
-        DBuf<int64_t> wide;
-        wide.alloc(n);
-        k_widen<<<nblk(n, 256), 256, 0, st>>>(order.p, n, wide.p); note_launch();
-        KB_CUDA(cudaMemcpyAsync(h_order, wide.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        KB_CUDA(cudaStreamSynchronize(st));
+    if (order64) {
+        order64->alloc(n);
+        k_widen<<<nblk(n, 256), 256, 0, st>>>(order.p, n, order64->p); note_launch();
     }
-    if (h_lower || h_upper) {
-        DBuf<double> tmpv;
-        tmpv.alloc(n);
-        if (h_lower) {
-            gather_to_original(g, s.lower.p, tmpv.p, st);
-            KB_CUDA(cudaMemcpyAsync(h_lower, tmpv.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-            KB_CUDA(cudaStreamSynchronize(st));
-        }
-        if (h_upper) {
-            gather_to_original(g, s.upper.p, tmpv.p, st);
-            KB_CUDA(cudaMemcpyAsync(h_upper, tmpv.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-            KB_CUDA(cudaStreamSynchronize(st));
-        }
+    if (lower) {
+        lower->alloc(n);
+        gather_to_original(g, s.lower.p, lower->p, st);
+    }
+    if (upper) {
+        upper->alloc(n);
+        gather_to_original(g, s.upper.p, upper->p, st);
     }
     unsigned long long pairs = 0;
     KB_CUDA(cudaMemcpyAsync(&pairs, u + 2, sizeof(pairs), cudaMemcpyDeviceToHost, st));
@@ -216,6 +209,19 @@ void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, do
     // zero-bound nodes have upper == 0: every positive lower separates them
     pairs += (unsigned long long)(n - npos) * (unsigned long long)npos;
     if (h_pairs) *h_pairs = (int64_t)pairs;
+}
+
+void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, double *h_upper,
+                int64_t *h_pairs) {
+    const int64_t n = s.g->n;
+    DBuf<int64_t> o;
+    DBuf<double> lo, up;
+    result_device(s, st, h_order ? &o : nullptr, h_lower ? &lo : nullptr,
+                  h_upper ? &up : nullptr, h_pairs);
+    if (h_order) KB_CUDA(cudaMemcpyAsync(h_order, o.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
 }
 
 

@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import math
-from dataclasses import dataclass, replace
+from dataclasses import FrozenInstanceError, dataclass, replace
 
 import numpy as np
 
@@ -351,22 +351,100 @@ class KatzState:
 
 # ---------------------------------------------------------------- results
 
-@dataclass(frozen=True)
-class RankingResult:
-    """Immutable outcome of a converged run (engine.py:224-243)."""
+class _DeviceRanking:
+    """A kb_ranking snapshot: the ranked vectors left in HBM until read."""
 
-    order: np.ndarray
-    lower: np.ndarray
-    upper: np.ndarray
-    iterations_used: int
-    criterion: Criterion
-    separated_fraction: float
+    def __init__(self, h, n: int):
+        self._h, self.n, self._L = h, n, _lib.lib()
+
+    def read(self, which: int, start: int, stop: int) -> np.ndarray:
+        out = np.empty(max(0, stop - start), dtype=np.int64 if which == 0 else np.float64)
+        if out.size:
+            _lib.check(self._L.kb_ranking_read(self._h, which, start, out.size, _lib.ptr(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._L.kb_ranking_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+class RankingResult:
+    """Immutable outcome of a converged run (engine.py:224-243).
+
+    Same fields and methods as the reference's frozen dataclass.  A result
+    made by ranking_result keeps its vectors on the device and copies each
+    one to the host the first time it is touched; ``top(k)`` and
+    ``bounds(v)`` copy only what they return.  Materialised arrays are
+    read-only, as in the reference."""
+
+    __slots__ = ("_order", "_lower", "_upper", "iterations_used", "criterion",
+                 "separated_fraction", "_dev")
+
+    def __init__(self, order=None, lower=None, upper=None, iterations_used: int = 0,
+                 criterion: Criterion | None = None, separated_fraction: float = 0.0, *,
+                 _device: _DeviceRanking | None = None):
+        set_ = object.__setattr__
+        set_(self, "_order", order)
+        set_(self, "_lower", lower)
+        set_(self, "_upper", upper)
+        set_(self, "iterations_used", iterations_used)
+        set_(self, "criterion", criterion)
+        set_(self, "separated_fraction", separated_fraction)
+        set_(self, "_dev", _device)
+
+    def __setattr__(self, name, value):
+        raise FrozenInstanceError(f"cannot assign to field {name!r}")
+
+    def __delattr__(self, name):
+        raise FrozenInstanceError(f"cannot delete field {name!r}")
+
+    def _field(self, slot: str, which: int) -> np.ndarray:
+        arr = object.__getattribute__(self, slot)
+        if arr is None:
+            dev = self._dev
+            arr = dev.read(which, 0, dev.n)
+            arr.setflags(write=False)
+            object.__setattr__(self, slot, arr)
+            if all(object.__getattribute__(self, x) is not None
+                   for x in ("_order", "_lower", "_upper")):
+                object.__setattr__(self, "_dev", None)   # all on the host: free HBM
+        return arr
+
+    @property
+    def order(self) -> np.ndarray:
+        return self._field("_order", 0)
+
+    @property
+    def lower(self) -> np.ndarray:
+        return self._field("_lower", 1)
+
+    @property
+    def upper(self) -> np.ndarray:
+        return self._field("_upper", 2)
 
     def bounds(self, v: int) -> tuple[float, float]:
+        if self._lower is None and self._dev is not None:
+            v = int(v)
+            if not -self._dev.n <= v < self._dev.n:
+                raise IndexError(f"index {v} is out of bounds for axis 0 with size {self._dev.n}")
+            v %= self._dev.n
+            return (float(self._dev.read(1, v, v + 1)[0]), float(self._dev.read(2, v, v + 1)[0]))
         return float(self.lower[v]), float(self.upper[v])
 
     def top(self, k: int) -> list[int]:
+        if self._order is None and self._dev is not None:
+            n = self._dev.n
+            stop = max(0, min(int(k), n)) if k >= 0 else max(0, n + int(k))
+            return [int(v) for v in self._dev.read(0, 0, stop)]
         return [int(v) for v in self.order[:k]]
+
+    def __repr__(self) -> str:
+        return (f"RankingResult(iterations_used={self.iterations_used}, "
+                f"criterion={self.criterion!r}, separated_fraction={self.separated_fraction!r})")
 
 
 # ---------------------------------------------------------------- operations
@@ -458,18 +536,12 @@ def ranking_result(state: KatzState) -> RankingResult:
     n = state.n
     if state.r < 1:
         raise StateError("separated_fraction needs at least one iteration")
-    order = np.empty(n, dtype=np.int64)
-    lower = np.empty(n, dtype=np.float64)
-    upper = np.empty(n, dtype=np.float64)
     pairs = ctypes.c_int64()
-    _lib.check(state._L.kb_result(state._h, _lib.ptr(order), _lib.ptr(lower),
-                                  _lib.ptr(upper), ctypes.byref(pairs)))
-    for arr in (order, lower, upper):
-        arr.setflags(write=False)
+    h = ctypes.c_void_p()
+    _lib.check(state._L.kb_ranking_snapshot(state._h, ctypes.byref(h), ctypes.byref(pairs)))
     frac = 1.0 if n < 2 else int(pairs.value) / (n * (n - 1) // 2)
-    return RankingResult(order=order, lower=lower, upper=upper,
-                         iterations_used=state.r, criterion=state.criterion,
-                         separated_fraction=frac)
+    return RankingResult(iterations_used=state.r, criterion=state.criterion,
+                         separated_fraction=frac, _device=_DeviceRanking(h, n))
 
 
 def separated_fraction(state: KatzState) -> float:

@@ -3,7 +3,7 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1807_03847_b200 as P
-from paper_1807_03847_b200 import _lib, generate as G
+from paper_1807_03847_b200 import _lib, generators as G
 
 L = _lib.lib()
 g = G.rmat_graph(1 << 24, edge_factor=16, seed=42)
