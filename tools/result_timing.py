@@ -2,7 +2,7 @@
 import ctypes, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1807_03847_b200 as P
-from paper_1807_03847_b200 import _lib, generate as G
+from paper_1807_03847_b200 import _lib, generators as G
 
 L = _lib.lib()
 knob = os.environ.get("KNOB", "k3.split_sort").encode()
