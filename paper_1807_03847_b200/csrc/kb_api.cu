@@ -357,8 +357,20 @@ int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr
         g.relabel = !(flags & KB_GRAPH_NO_RELABEL);
         KB_REQUIRE(own_lo >= 0 && (own_hi < 0 || (own_hi >= own_lo && own_hi <= n)), KB_EPARAM,
                    "bad owned row range");
-                g.own_lo = own_lo;
+        g.own_lo = own_lo;
         g.own_hi = own_hi < 0 ? n : own_hi;
+        {
+            // a shard of an exchange layout with 2^k-id blocks: K1 keeps the
+            // head of every block (the top hubs of each rank) in shared memory
+            const int64_t B = g.own_hi - g.own_lo;
+            if (!g.relabel && B > 0 && (B & (B - 1)) == 0 && n % B == 0 && own_lo % B == 0 &&
+                n / B > 1) {
+                int sh = 0;
+                while (((int64_t)1 << sh) < B) sh++;
+                g.hot_shift = sh;
+                g.hot_per = std::max<int64_t>(1, g.hot / (n / B));
+            }
+        }
         try {
             build_graph(g, indptr, indices);
             if (labels) {

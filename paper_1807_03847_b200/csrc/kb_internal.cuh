@@ -108,6 +108,10 @@ struct Graph {
     int sm_count = 0;
     int64_t n = 0, nnz = 0, nv = 0, nh = 0, nzero = 0, max_deg = 0;
     int64_t split = 0, hot = 0;
+    // sharded graphs (KB_GRAPH_NO_RELABEL with an owned block of 2^k ids):
+    // K1's shared-memory hot set takes the first hot_per ids of each block
+    int64_t hot_per = 0;
+    int hot_shift = 0;
     int64_t version = 1;
     DBuf<int32_t> perm;    // new -> original id
     DBuf<int32_t> iperm;   // original -> new id

@@ -65,7 +65,15 @@ struct IterArgs {
     int level_only;                 // write w only (dynamic level repair)
     const int32_t *hrow, *vrow;     // explicit row maps (nullptr: implicit)
     int hot;
+    // sharded graphs: the hot set is the head of every rank's block of the
+    // exchange layout (hot_per entries each, blocks of 2^hot_shift ids)
+    int hot_per, hot_shift;
     unsigned long long *counter;
+};
+
+struct HotMap {
+    int hot, per, shift;
+    uint32_t mask;
 };
 
 // XL: 0 = ld.global.nc (read-only path, L1 allocate), 1 = ld.global.cg
@@ -80,10 +88,12 @@ __device__ __forceinline__ double ldx(const double *p) {
     return r;
 }
 
-template <int XL>
-__device__ __forceinline__ double fetch(const double *__restrict__ hot_s, int hot,
+template <int XL, bool ST>
+__device__ __forceinline__ double fetch(const double *__restrict__ hot_s, const HotMap &hm,
                                         const double *__restrict__ x, int32_t c) {
-    return (c < hot) ? hot_s[c] : ldx<XL>(x + c);
+    if (!ST) return (c < hm.hot) ? hot_s[c] : ldx<XL>(x + c);
+    const int j = (int)((uint32_t)c & hm.mask);
+    return (j < hm.per) ? hot_s[(c >> hm.shift) * hm.per + j] : ldx<XL>(x + c);
 }
 
 __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s) {
@@ -102,14 +112,14 @@ __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s)
 
 // Gather of one batch of 8 column slots (two int4 groups) of a lane's row;
 // slots at or beyond the row length read as +0.0 without touching memory.
-template <int XL>
-__device__ __forceinline__ void gather8(const double *__restrict__ hot_s, int hot,
+template <int XL, bool ST>
+__device__ __forceinline__ void gather8(const double *__restrict__ hot_s, const HotMap &hm,
                                         const double *__restrict__ x, int4 ca, int4 cb,
                                         int jb, int len, double v[8]) {
     const int32_t c[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
     for (int q = 0; q < 8; q++)
-        v[q] = (jb + q < len) ? fetch<XL>(hot_s, hot, x, c[q]) : 0.0;
+        v[q] = (jb + q < len) ? fetch<XL, ST>(hot_s, hm, x, c[q]) : 0.0;
 }
 
 // epilogue with katz already loaded (narrow-slice path)
@@ -132,10 +142,18 @@ __device__ __forceinline__ void epilogue_k(const IterArgs &A, int64_t v, double 
 // DEPTH batches of 8 gathers per lane are kept in flight (software pipeline):
 // the loads of batch i+1..i+DEPTH-1 are issued before batch i is folded, so
 // the in-order dependent add chain never waits on a single batch's latency.
-template <int DEPTH, int XL>
+template <int DEPTH, int XL, bool ST = false>
 __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     extern __shared__ double hot_s[];
-    for (int i = threadIdx.x; i < A.hot; i += blockDim.x) hot_s[i] = A.x[i];
+    const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u};
+    if (ST) {
+        for (int i = threadIdx.x; i < A.hot; i += blockDim.x) {
+            const int r = i / A.hot_per, j = i - r * A.hot_per;
+            hot_s[i] = A.x[((int64_t)r << A.hot_shift) + j];
+        }
+    } else {
+        for (int i = threadIdx.x; i < A.hot; i += blockDim.x) hot_s[i] = A.x[i];
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const double *__restrict__ x = A.x;
@@ -179,7 +197,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
             for (int q = 0; q < 4; q++)
 #pragma unroll
                 for (int j = 0; j < 4; j++)
-                    v[q][j] = (j < len[q]) ? fetch<XL>(hot_s, A.hot, x, cc[q][j]) : 0.0;
+                    v[q][j] = (j < len[q]) ? fetch<XL, ST>(hot_s, hm, x, cc[q][j]) : 0.0;
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 double sum = 0.0;
@@ -206,7 +224,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
                 if (j < w) c[j] = ld_stream_i1(base + j * 32 + lane, pol);
 #pragma unroll
             for (int j = 0; j < 4; j++)
-                if (j < len) sum = __dadd_rn(sum, fetch<XL>(hot_s, A.hot, x, c[j]));
+                if (j < len) sum = __dadd_rn(sum, fetch<XL, ST>(hot_s, hm, x, c[j]));
         } else {
             const int32_t *p = base + lane * 4;
             const int w4 = w >> 2;             // int4 groups per lane
@@ -219,7 +237,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
                     const int4 ca = ld_stream_i4(p + (int64_t)g0 * 128, pol);
                     const int4 cb = (g0 + 1 < w4) ? ld_stream_i4(p + (int64_t)(g0 + 1) * 128, pol)
                                                   : zero4;
-                    gather8<XL>(hot_s, A.hot, x, ca, cb, g0 * 4, len, v[d]);
+                    gather8<XL, ST>(hot_s, hm, x, ca, cb, g0 * 4, len, v[d]);
                 }
             }
             for (int b = 0; b < nb; b += DEPTH) {
@@ -235,7 +253,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
                             const int4 cb = (g0 + 1 < w4)
                                                 ? ld_stream_i4(p + (int64_t)(g0 + 1) * 128, pol)
                                                 : zero4;
-                            gather8<XL>(hot_s, A.hot, x, ca, cb, g0 * 4, len, v[d]);
+                            gather8<XL, ST>(hot_s, hm, x, ca, cb, g0 * 4, len, v[d]);
                         }
                     }
                 }
@@ -394,6 +412,15 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
     A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
     A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), n);
+    A.hot_per = 0;
+    A.hot_shift = 0;
+    const bool strided = g.hot_per > 0 && tune_get("k1.shard_hot", 1);
+    if (strided) {
+        const int64_t P = n >> g.hot_shift;
+        A.hot_per = (int)std::min<int64_t>(g.hot_per, (int64_t)1 << g.hot_shift);
+        A.hot_shift = g.hot_shift;
+        A.hot = (int)(A.hot_per * P);
+    }
     A.counter = s.work_counter.p;
     if (s.seg_sum.n < (size_t)std::max<int64_t>(1, g.sell.nseg)) {
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
@@ -423,8 +450,9 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     if (depth == 1) kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2> : k_sell_iterate<1, 0>;
     else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
     else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
-    static bool attr_done[64][9] = {};
-    const int kid = (depth - 1) * 3 + xl;
+    if (strided) kern = k_sell_iterate<1, 0, true>;
+    static bool attr_done[64][10] = {};
+    const int kid = strided ? 9 : (depth - 1) * 3 + xl;
     if (!attr_done[g.device][kid]) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));

@@ -103,7 +103,7 @@ class CudaShard:
 
     def __init__(self, plan: ShardPlan, rank: int, indptr, indices, *, device: int,
                  alpha: float, gamma: float, crit: Criterion, undirected: bool,
-                 max_iterations: int, symmetric: bool = True):
+                 max_iterations: int, symmetric: bool = True, split_threshold: int = 0):
         import torch
         self.torch = torch
         self.L = _lib.lib()
@@ -113,9 +113,13 @@ class CudaShard:
         lo, hi = plan.block(rank)
         flags = _lib.KB_GRAPH_NO_RELABEL | (_lib.KB_GRAPH_SYMMETRIC if symmetric else 0)
         h = ctypes.c_void_p()
+        if split_threshold <= 0:
+            # segment long rows finer as the per-rank work shrinks, so one
+            # lane's sequential chain never sets the kernel's tail
+            split_threshold = max(512, 2048 // plan.P)
         _lib.check(self.L.kb_graph_create_ex(device, ip.size - 1, int(ip[-1]), _lib.ptr(ip),
-                                             _lib.ptr(ix), 0, -1, flags, _lib.ptr(lab), lo, hi,
-                                             ctypes.byref(h)))
+                                             _lib.ptr(ix), split_threshold, -1, flags,
+                                             _lib.ptr(lab), lo, hi, ctypes.byref(h)))
         self.g = h
         self.reset(alpha=alpha, gamma=gamma, crit=crit, undirected=undirected,
                    max_iterations=max_iterations)
