@@ -362,7 +362,8 @@ def run_sharded(a, rank, world, local):
     alpha = 1.0 / (1.0 + d)
     gamma = P.tail_gamma(alpha, d)
     shard = D.CudaShard(plan, rank, ip, ix, device=local, alpha=alpha, gamma=gamma, crit=crit,
-                        undirected=True, max_iterations=200)
+                        undirected=True, max_iterations=200,
+                        split_threshold=D.fast_split(world))
     shard.collective_device = f"cuda:{local}"
     nnz = int(ip[-1])
     del ix

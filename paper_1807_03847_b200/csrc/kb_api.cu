@@ -935,7 +935,7 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.m_host = n;
         s.scratch_u64.alloc(1 << 16);
         s.scratch_i32.alloc(1 << 16);
-        s.work_counter.alloc(1);
+        s.work_counter.alloc(2);
         s.h_flags = pinned_flags();
         KB_CUDA(cudaEventCreate(&s.ev0));
         KB_CUDA(cudaEventCreate(&s.ev1));

@@ -153,7 +153,7 @@ struct SpmvCtx {
     explicit SpmvCtx(Graph &g, double alpha) {
         s.g = &g;
         s.alpha = alpha;
-        s.work_counter.alloc(1);
+        s.work_counter.alloc(2);
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
     }
     ~SpmvCtx() {

@@ -758,6 +758,125 @@ __global__ void __launch_bounds__(256) k_rank_decide(
         out[0] = s_bad ? 1 : ((unsigned long long)s_ok == nviol ? 0 : 2);
 }
 
+// Candidate q fails its adjacent-separation test iff some x ranked above q
+// (lower[x] > lower[q], or equal with the smaller label) has
+// lower[x] <= fl(upper[q] - eps): the predecessor has the smallest lower of
+// all elements above q.  One pass tests that for every candidate at once
+// and stops every block as soon as any candidate is refuted (the verdict is
+// then "not converged"); only a converging check reads the whole set.
+__global__ void __launch_bounds__(256, 4) k_rank_refute(const double *lower, const double *upper,
+                                                       const int32_t *perm, const int32_t *act,
+                                                       int dense, int64_t m,
+                                                       const int32_t *cand,
+                                                       const unsigned long long *meta,
+                                                       double eps, unsigned long long *fail) {
+    __shared__ double cl[NCAND], ct[NCAND];
+    __shared__ int32_t cq[NCAND], co[NCAND];
+    const int nc = (int)min((unsigned long long)NCAND, *meta);
+    if (threadIdx.x < nc) {
+        const int32_t q = cand[threadIdx.x];
+        cq[threadIdx.x] = q;
+        cl[threadIdx.x] = lower[q];
+        ct[threadIdx.x] = __dsub_rn(upper[q], eps);
+        co[threadIdx.x] = perm[q];
+    }
+    __syncthreads();
+    if (nc == 0) return;
+    const volatile unsigned long long *vf = fail;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int it = 0;
+    // block-uniform trip count (the early-exit vote is a block barrier)
+    for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < m; b0 += 4 * stride) {
+        const int64_t i0 = b0 + threadIdx.x;
+        if ((++it & 3) == 0 && __syncthreads_or(*vf != 0)) return;
+        int32_t xs[4];
+        double lx[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int64_t i = i0 + t * stride;
+            xs[t] = i < m ? (dense ? (int32_t)i : act[i]) : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; t++) lx[t] = xs[t] >= 0 ? lower[xs[t]] : -1.0;
+        bool hit = false;
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            if (xs[t] < 0) continue;
+            for (int c = 0; c < nc; c++) {
+                const double l = lx[t];
+                if (l > ct[c] || l < cl[c]) continue;     // outside [lower_q, upper_q - eps]
+                if (l > cl[c] || (xs[t] != cq[c] && perm[xs[t]] < co[c])) hit = true;
+            }
+        }
+        if (hit) atomicOr(fail, 1ull);
+    }
+}
+
+// candidates: the NCAND block winners with the widest excess (ties: the
+// smaller label); one warp-synchronous arg-max per round, no block barriers
+__global__ void __launch_bounds__(1024) k_pick_cands_fast(const unsigned long long *blk_key,
+                                                         const int32_t *blk_id, int nb,
+                                                         const int32_t *perm, int32_t *cand,
+                                                         unsigned long long *meta) {
+    __shared__ unsigned long long wk[32];
+    __shared__ int32_t wb[32], wl[32];
+    __shared__ int32_t win_b;
+    extern __shared__ unsigned char taken[];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) taken[b] = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // every thread owns <= 2 block results (nb <= 2048)
+    unsigned long long k0 = 0, k1 = 0;
+    int32_t b0 = -1, b1 = -1, l0 = 0, l1 = 0;
+    {
+        const int a = threadIdx.x, c = threadIdx.x + blockDim.x;
+        if (a < nb && blk_id[a] >= 0) { b0 = a; k0 = blk_key[a]; l0 = perm[blk_id[a]]; }
+        if (c < nb && blk_id[c] >= 0) { b1 = c; k1 = blk_key[c]; l1 = perm[blk_id[c]]; }
+    }
+    __syncthreads();
+    int nc = 0;
+    for (int round = 0; round < NCAND; round++) {
+        // local best among untaken
+        unsigned long long bk = 0;
+        int32_t bb = -1, bl = 0;
+        if (b0 >= 0 && !taken[b0]) { bk = k0; bb = b0; bl = l0; }
+        if (b1 >= 0 && !taken[b1] &&
+            (bb < 0 || k1 > bk || (k1 == bk && l1 < bl))) { bk = k1; bb = b1; bl = l1; }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long ok = __shfl_down_sync(0xffffffffu, bk, o);
+            const int32_t ob = __shfl_down_sync(0xffffffffu, bb, o);
+            const int32_t ol = __shfl_down_sync(0xffffffffu, bl, o);
+            if (ob >= 0 && (bb < 0 || ok > bk || (ok == bk && ol < bl))) { bk = ok; bb = ob; bl = ol; }
+        }
+        if (lane == 0) { wk[warp] = bk; wb[warp] = bb; wl[warp] = bl; }
+        __syncthreads();
+        if (warp == 0) {
+            const int nw = blockDim.x >> 5;
+            bk = lane < nw ? wk[lane] : 0;
+            bb = lane < nw ? wb[lane] : -1;
+            bl = lane < nw ? wl[lane] : 0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long ok = __shfl_down_sync(0xffffffffu, bk, o);
+                const int32_t ob = __shfl_down_sync(0xffffffffu, bb, o);
+                const int32_t ol = __shfl_down_sync(0xffffffffu, bl, o);
+                if (ob >= 0 && (bb < 0 || ok > bk || (ok == bk && ol < bl))) { bk = ok; bb = ob; bl = ol; }
+            }
+            if (lane == 0) {
+                win_b = bb;
+                if (bb >= 0) {
+                    taken[bb] = 1;
+                    cand[nc] = blk_id[bb];
+                }
+            }
+        }
+        __syncthreads();
+        if (win_b < 0) break;
+        nc++;
+    }
+    if (threadIdx.x == 0) meta[0] = (unsigned long long)nc;
+}
+
 bool check_ranking(State &s, cudaStream_t st) {
     Graph &g = *s.g;
     const int64_t n = s.m_host;
@@ -773,6 +892,20 @@ bool check_ranking(State &s, cudaStream_t st) {
     KB_CUDA(cudaMemsetAsync(u, 0, 4 * sizeof(unsigned long long), st));
     k_rank_violators<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, s.eps,
                                          u, bkey, ids);
+    if (tune_get("check.refute", 1) && nb <= 2048) {
+        k_pick_cands_fast<<<1, 1024, nb, st>>>(bkey, ids, nb, g.perm.p, cand, u + 1);
+        k_rank_refute<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, cand,
+                                          u + 1, s.eps, u + 2);
+        note_launch(3);
+        KB_CUDA(cudaGetLastError());
+        sync_read(s, st, u, 3);
+        const unsigned long long nviol = s.h_flags[0], ncand = s.h_flags[1],
+                                 refuted = s.h_flags[2];
+        if (nviol == 0) return true;            // every node passes its self test
+        if (refuted) return false;               // a candidate fails: not converged
+        if (nviol <= ncand) return true;         // every violator checked and passes
+        return sorted_check(s, st, g.n);
+    }
     k_pick_cands<<<1, 256, 0, st>>>(bkey, ids, nb, g.perm.p, cand, u + 1);
     k_rank_pred<<<nb, 256, 0, st>>>(s.lower.p, g.perm.p, act, dense, n, cand, NCAND, u + 1, pk,
                                     po);

@@ -450,9 +450,11 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     if (depth == 1) kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2> : k_sell_iterate<1, 0>;
     else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
     else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
-    if (strided) kern = k_sell_iterate<1, 0, true>;
-    static bool attr_done[64][10] = {};
-    const int kid = strided ? 9 : (depth - 1) * 3 + xl;
+    if (strided)
+        kern = depth == 3 ? k_sell_iterate<3, 0, true>
+             : depth == 2 ? k_sell_iterate<2, 0, true> : k_sell_iterate<1, 0, true>;
+    static bool attr_done[64][12] = {};
+    const int kid = strided ? 9 + (depth - 1) : (depth - 1) * 3 + xl;
     if (!attr_done[g.device][kid]) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));

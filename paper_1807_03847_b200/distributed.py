@@ -113,10 +113,10 @@ class CudaShard:
         lo, hi = plan.block(rank)
         flags = _lib.KB_GRAPH_NO_RELABEL | (_lib.KB_GRAPH_SYMMETRIC if symmetric else 0)
         h = ctypes.c_void_p()
-        if split_threshold <= 0:
-            # segment long rows finer as the per-rank work shrinks, so one
-            # lane's sequential chain never sets the kernel's tail
-            split_threshold = max(512, 2048 // plan.P)
+        # split_threshold 0 keeps the single-GPU segmentation (2048 arcs), so
+        # the shards reproduce the one-GPU bounds bit for bit; a finer split
+        # (fast_split(P)) shortens the kernel tail when the per-rank work is
+        # small, at the cost of rounding-level (<= 1e-12) differences
         _lib.check(self.L.kb_graph_create_ex(device, ip.size - 1, int(ip[-1]), _lib.ptr(ip),
                                              _lib.ptr(ix), split_threshold, -1, flags,
                                              _lib.ptr(lab), lo, hi, ctypes.byref(h)))
@@ -257,6 +257,12 @@ class CudaShard:
         self.torch.cuda.synchronize(self.device)
 
 
+def fast_split(P: int) -> int:
+    """Row segmentation that keeps K1's tail short at P ranks (C2, one
+    B200: P=8 rank kernel 0.60 -> 0.31 ms; profiles/r01_shard_k1_split_sweep.log)."""
+    return max(512, 2048 // max(1, P))
+
+
 def _all_gather_flat(dist, full, rank: int, P: int, n_per: int):
     """In-place all-gather of equal blocks of a flat tensor (one collective
     into the full buffer; the own block is staged because NCCL's in-place
@@ -376,4 +382,4 @@ def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = True,
                       max_iterations=max_iterations).run()
 
 
-__all__ = ["ShardPlan", "CudaShard", "ShardedRun", "sharded_run"]
+__all__ = ["ShardPlan", "CudaShard", "ShardedRun", "sharded_run", "fast_split"]

@@ -19,14 +19,15 @@ torch = pytest.importorskip("torch")
 from paper_1807_03847_b200 import distributed as D  # noqa: E402
 
 
-def _lockstep(g0, crit, world, protocol="device"):
+def _lockstep(g0, crit, world, protocol="device", split=0):
     plan = D.ShardPlan(g0.indptr, world)
     d = plan.max_degree
     alpha = 1.0 / (1.0 + d)
     gamma = P.tail_gamma(alpha, d)
     cap = P.default_iteration_cap(alpha, d, crit.epsilon)
     shards = [D.CudaShard(plan, rk, g0.indptr, g0.indices, device=0, alpha=alpha,
-                          gamma=gamma, crit=crit, undirected=True, max_iterations=cap)
+                          gamma=gamma, crit=crit, undirected=True, max_iterations=cap,
+                          split_threshold=split)
               for rk in range(world)]
     n_per = plan.n_per
     r = 0
@@ -132,3 +133,17 @@ def test_cuda_shards_score_criterion():
     assert r == ores.iterations_used
     np.testing.assert_allclose(lower, ores.lower, rtol=1e-12, atol=0)
     np.testing.assert_array_equal(order, ores.order)
+
+
+def test_cuda_shards_fast_split_within_tolerance():
+    """The bench's finer row segmentation (fast_split) changes only the
+    rounding of long rows: same iterations and order, bounds within 1e-12."""
+    g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
+    crit = P.Criterion.top_k(100, 1e-6)
+    r, order, lower, upper, pairs = _lockstep(g0, crit, 4, split=D.fast_split(8) // 2)
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    res = P.run(P.init(g, crit, undirected=True), g)
+    assert r == res.iterations_used
+    np.testing.assert_array_equal(order[:100], res.order[:100])
+    np.testing.assert_allclose(lower, res.lower, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(upper, res.upper, rtol=1e-12, atol=0)

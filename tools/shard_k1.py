@@ -37,6 +37,9 @@ def main():
                          split_threshold=int(os.environ.get("SPLIT", "0")))
         for hot in (1, 0):
             _lib.check(L.kb_tune(b"k1.shard_hot", hot))
+            _lib.check(L.kb_tune(b"k1.depth", int(os.environ.get("DEPTH", "1"))))
+            if "HEAVY" in os.environ:
+                _lib.check(L.kb_tune(b"k1.heavy_warp", int(os.environ["HEAVY"])))
             sh.reset(alpha=alpha, gamma=gamma, crit=crit, undirected=True, max_iterations=200)
             for _ in range(7):
                 sh.iterate()

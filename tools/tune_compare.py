@@ -1,5 +1,6 @@
 """Time C2 (or C4 with WORKLOAD=c4) K1 with a knob on/off: KNOB=name VALUES=0,1"""
 import json, os, sys, time
+import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1807_03847_b200 as P
 from paper_1807_03847_b200 import _lib, generators as G
@@ -21,7 +22,10 @@ for rep in range(2):
         t0 = time.perf_counter()
         res = P.run(st, g)
         dt = time.perf_counter() - t0
+        lo = res.lower
+        import hashlib
+        dig = hashlib.sha256(np.ascontiguousarray(lo).tobytes()).hexdigest()[:16]
         i = st._info()
         print(json.dumps({"knob": knob.decode(), "value": v, "rep": rep, "run_s": round(dt, 5),
                           "k1_ms": round(i.spmv_ms / max(1, i.spmv_launches), 4), "r": i.r,
-                          "top3": res.top(3)}), flush=True)
+                          "top3": res.top(3), "lower_sha": dig}), flush=True)
