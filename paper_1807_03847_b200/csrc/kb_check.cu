@@ -769,7 +769,8 @@ __global__ void __launch_bounds__(256, 4) k_rank_refute(const double *lower, con
                                                        int dense, int64_t m,
                                                        const int32_t *cand,
                                                        const unsigned long long *meta,
-                                                       double eps, unsigned long long *fail) {
+                                                       double eps, unsigned long long *fail,
+                                                       unsigned long long *pair) {
     __shared__ double cl[NCAND], ct[NCAND];
     __shared__ int32_t cq[NCAND], co[NCAND];
     const int nc = (int)min((unsigned long long)NCAND, *meta);
@@ -799,17 +800,32 @@ __global__ void __launch_bounds__(256, 4) k_rank_refute(const double *lower, con
 #pragma unroll
         for (int t = 0; t < 4; t++) lx[t] = xs[t] >= 0 ? lower[xs[t]] : -1.0;
         bool hit = false;
+        unsigned long long rec = 0;
 #pragma unroll
         for (int t = 0; t < 4; t++) {
             if (xs[t] < 0) continue;
             for (int c = 0; c < nc; c++) {
                 const double l = lx[t];
                 if (l > ct[c] || l < cl[c]) continue;     // outside [lower_q, upper_q - eps]
-                if (l > cl[c] || (xs[t] != cq[c] && perm[xs[t]] < co[c])) hit = true;
+                if (l > cl[c] || (xs[t] != cq[c] && perm[xs[t]] < co[c])) {
+                    hit = true;
+                    rec = ((unsigned long long)(uint32_t)cq[c] << 32) | (uint32_t)xs[t];
+                }
             }
         }
-        if (hit) atomicOr(fail, 1ull);
+        if (hit) {
+            atomicOr(fail, 1ull);
+            atomicCAS(pair, ~0ull, rec);
+        }
     }
+}
+
+// does the cached pair (q, x) still refute q's adjacent-separation test?
+__global__ void k_pair_refutes(const double *lower, const double *upper, const int32_t *perm,
+                               int32_t q, int32_t x, double eps, unsigned long long *out) {
+    const double lq = lower[q], lx = lower[x];
+    const bool above = lx > lq || (lx == lq && perm[x] < perm[q]);
+    out[0] = (above && lx <= __dsub_rn(upper[q], eps)) ? 1ull : 0ull;
 }
 
 // candidates: the NCAND block winners with the widest excess (ties: the
@@ -889,20 +905,34 @@ bool check_ranking(State &s, cudaStream_t st) {
     int32_t *ids = s.scratch_i32.p;            // [0..nb) block ids, [nb..nb+8) candidates
     int32_t *cand = ids + nb;
     unsigned int *po = (unsigned int *)(cand + NCAND);
+    if (s.rk_q >= 0 && tune_get("check.pair_cache", 1)) {
+        k_pair_refutes<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, s.rk_q, s.rk_x, s.eps, u);
+        note_launch();
+        sync_read(s, st, u, 1);
+        if (s.h_flags[0]) return false;          // still refuted: not converged
+        s.rk_q = s.rk_x = -1;
+    }
     KB_CUDA(cudaMemsetAsync(u, 0, 4 * sizeof(unsigned long long), st));
+    KB_CUDA(cudaMemsetAsync(u + 3, 0xff, sizeof(unsigned long long), st));   // refuting pair
     k_rank_violators<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, s.eps,
                                          u, bkey, ids);
     if (tune_get("check.refute", 1) && nb <= 2048) {
         k_pick_cands_fast<<<1, 1024, nb, st>>>(bkey, ids, nb, g.perm.p, cand, u + 1);
         k_rank_refute<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, cand,
-                                          u + 1, s.eps, u + 2);
+                                          u + 1, s.eps, u + 2, u + 3);
         note_launch(3);
         KB_CUDA(cudaGetLastError());
-        sync_read(s, st, u, 3);
+        sync_read(s, st, u, 4);
         const unsigned long long nviol = s.h_flags[0], ncand = s.h_flags[1],
                                  refuted = s.h_flags[2];
         if (nviol == 0) return true;            // every node passes its self test
-        if (refuted) return false;               // a candidate fails: not converged
+        if (refuted) {                           // a candidate fails: not converged
+            if (s.h_flags[3] != ~0ull) {
+                s.rk_q = (int32_t)(s.h_flags[3] >> 32);
+                s.rk_x = (int32_t)(uint32_t)s.h_flags[3];
+            }
+            return false;
+        }
         if (nviol <= ncand) return true;         // every violator checked and passes
         return sorted_check(s, st, g.n);
     }

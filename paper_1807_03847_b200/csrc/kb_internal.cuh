@@ -195,6 +195,10 @@ struct State {
     double spmv_ms = 0;
     int64_t spmv_launches = 0;
     int64_t check_full_sorts = 0;   // RANKING checks the certificates could not decide
+    // RANKING: the last refuting pair (q, x): x ranked above q with
+    // lower[x] <= fl(upper[q] - eps); while it still refutes, a check is
+    // "not converged" without a pass over the set
+    int32_t rk_q = -1, rk_x = -1;
     const double *x_level() const { return levels.back().p; }
 };
 
