@@ -142,6 +142,54 @@ __device__ __forceinline__ void epilogue_k(const IterArgs &A, int64_t v, double 
 // DEPTH batches of 8 gathers per lane are kept in flight (software pipeline):
 // the loads of batch i+1..i+DEPTH-1 are issued before batch i is folded, so
 // the in-order dependent add chain never waits on a single batch's latency.
+// four narrow slices (width <= 4) from slice s0 on, folded per lane
+template <int XL, bool ST, int Q = 4>
+__device__ __forceinline__ void narrow_group(const IterArgs &A, int64_t s0, int lane,
+                                             const double *__restrict__ hot_s,
+                                             const HotMap &hm, const double *__restrict__ x,
+                                             uint64_t pol) {
+    int len[Q], w[Q];
+    const int32_t *base[Q];
+    int64_t row[Q];
+    double kz[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        const int64_t sq = s0 + q;
+        const int64_t vq = sq * 32 + lane;
+        const bool ok = sq < A.nslices && vq < A.nvr;
+        len[q] = ok ? A.vlen[vq] : 0;
+        w[q] = sq < A.nslices ? A.slice_w[sq] : 0;
+        base[q] = A.cols + (sq < A.nslices ? A.slice_off[sq] : 0);
+        row[q] = -1;
+        if (ok && vq >= A.nseg)
+            row[q] = A.vrow ? A.vrow[vq - A.nseg] : A.nh + (vq - A.nseg);
+        kz[q] = (row[q] >= 0 && !A.level_only) ? A.katz[row[q]] : 0.0;
+    }
+    int32_t cc[Q][4];
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            cc[q][j] = (j < w[q]) ? ld_stream_i1(base[q] + j * 32 + lane, pol) : 0;
+    double v[Q][4];
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            v[q][j] = (j < len[q]) ? fetch<XL, ST>(hot_s, hm, x, cc[q][j]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) sum = __dadd_rn(sum, v[q][j]);
+        const int64_t vq = (s0 + q) * 32 + lane;
+        if (s0 + q < A.nslices && vq < A.nvr) {
+            if (vq < A.nseg) A.seg_sum[vq] = sum;
+            else epilogue_k(A, row[q], sum, kz[q]);
+        }
+    }
+}
+
 template <int DEPTH, int XL, bool ST = false>
 __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     extern __shared__ double hot_s[];
@@ -168,47 +216,8 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         if ((int64_t)c >= grabs) break;
         if ((int64_t)c >= nwide_grabs) {
             // four narrow slices (width <= 4) at once: their loads overlap
-            const int64_t s0 = A.nwide + ((int64_t)c - nwide_grabs) * 4;
-            int len[4], w[4];
-            const int32_t *base[4];
-            int64_t row[4];
-            double kz[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const int64_t sq = s0 + q;
-                const int64_t vq = sq * 32 + lane;
-                const bool ok = sq < A.nslices && vq < A.nvr;
-                len[q] = ok ? A.vlen[vq] : 0;
-                w[q] = sq < A.nslices ? A.slice_w[sq] : 0;
-                base[q] = A.cols + (sq < A.nslices ? A.slice_off[sq] : 0);
-                row[q] = -1;
-                if (ok && vq >= A.nseg)
-                    row[q] = A.vrow ? A.vrow[vq - A.nseg] : A.nh + (vq - A.nseg);
-                kz[q] = (row[q] >= 0 && !A.level_only) ? A.katz[row[q]] : 0.0;
-            }
-            int32_t cc[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-#pragma unroll
-                for (int j = 0; j < 4; j++)
-                    cc[q][j] = (j < w[q]) ? ld_stream_i1(base[q] + j * 32 + lane, pol) : 0;
-            double v[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-#pragma unroll
-                for (int j = 0; j < 4; j++)
-                    v[q][j] = (j < len[q]) ? fetch<XL, ST>(hot_s, hm, x, cc[q][j]) : 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                double sum = 0.0;
-#pragma unroll
-                for (int j = 0; j < 4; j++) sum = __dadd_rn(sum, v[q][j]);
-                const int64_t vq = (s0 + q) * 32 + lane;
-                if (s0 + q < A.nslices && vq < A.nvr) {
-                    if (vq < A.nseg) A.seg_sum[vq] = sum;
-                    else epilogue_k(A, row[q], sum, kz[q]);
-                }
-            }
+            narrow_group<XL, ST>(A, A.nwide + ((int64_t)c - nwide_grabs) * 4, lane, hot_s, hm,
+                                 x, pol);
             continue;
         }
         const int64_t s = (int64_t)c;
@@ -264,6 +273,21 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
             else epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), sum);
         }
     }
+}
+
+// Graphs whose slices are all narrow (width <= 4: grids, meshes): no hot
+// set, fewer registers, two CTAs per SM and a static slice-group schedule,
+// so twice the warps keep loads in flight (K1 on C4 is latency-bound).
+template <int Q>
+__global__ void __launch_bounds__(1024, 2) k_sell_narrow(IterArgs A) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol = evict_first_policy();
+    const HotMap hm{0, 0, 0, 0u};
+    const int64_t groups = (A.nslices + Q - 1) / Q;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t gi = wid; gi < groups; gi += nw)
+        narrow_group<0, false, Q>(A, gi * Q, lane, nullptr, hm, A.x, pol);
 }
 
 // First iteration: x = levels[0] = ones, so every sequential row (or segment)
@@ -466,6 +490,11 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used], st));
     if (A.nslices && ones) {
         k_ones_step<<<(unsigned)((A.nvr + 255) / 256), 256, 0, st>>>(A);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    } else if (A.nslices && g.sell.nwide == 0 && A.nseg == 0 && tune_get("k1.narrow_kernel", 1)) {
+        if (tune_get("k1.narrow_q", 2) == 4) k_sell_narrow<4><<<g.sm_count * 2, 1024, 0, st>>>(A);
+        else k_sell_narrow<2><<<g.sm_count * 2, 1024, 0, st>>>(A);
         note_launch();
         KB_CUDA(cudaGetLastError());
     } else if (A.nslices) {
