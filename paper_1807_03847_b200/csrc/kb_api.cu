@@ -936,6 +936,9 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.scratch_u64.alloc(1 << 16);
         s.scratch_i32.alloc(1 << 16);
         s.work_counter.alloc(2);
+        s.abort_flag.alloc(1);
+        KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
+        KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
         s.h_flags = pinned_flags();
         KB_CUDA(cudaEventCreate(&s.ev0));
         KB_CUDA(cudaEventCreate(&s.ev1));
@@ -954,6 +957,7 @@ int kb_state_destroy(kb_state *h) {
         KB_CUDA(cudaStreamSynchronize(h->s.g->stream));
         if (h->s.ev0) cudaEventDestroy(h->s.ev0);
         if (h->s.ev1) cudaEventDestroy(h->s.ev1);
+        if (h->s.chk_ev) cudaEventDestroy(h->s.chk_ev);
         for (cudaEvent_t e : h->s.k1_ev) cudaEventDestroy(e);
         delete h;
     });
@@ -1016,6 +1020,44 @@ int kb_run(kb_state *h, int *converged) {
         State &s = h->s;
         use_device(s.g->device);
         *converged = 0;
+        cudaStream_t st = s.g->stream;
+        // TOPK: queue K1 of r+1 behind check r, so the GPU does not idle
+        // through the check's host read; that K1 exits at once on the device
+        // if check r converged, and the host then rolls the level back
+        const bool spec = s.kind == KB_TOPK && s.k <= 4096 && s.keep_all &&
+                          tune_get("run.speculate", 1);
+        if (spec) {
+            check_version(s);
+            launch_iterate(s, st);
+            for (;;) {
+                const int nxt = topk_check_enqueue(s, st);
+                const bool ahead = s.r < s.max_iter;
+                if (ahead) {
+                    s.spec_abort = true;
+                    launch_iterate(s, st);
+                    s.spec_abort = false;
+                }
+                KB_CUDA(cudaEventSynchronize(s.chk_ev));
+                if (topk_check_finish(s, nxt)) {
+                    if (ahead) {                      // the queued K1 did nothing
+                        s.levels.pop_back();
+                        s.r -= 1;
+                        if (s.k1_used >= 2) s.k1_used -= 2;
+                    }
+                    *converged = 1;
+                    break;
+                }
+                if (!ahead) {
+                    const double gap = run_gap(s, st);
+                    char buf[160];
+                    snprintf(buf, sizeof buf,
+                             "stopping rule still unmet after %lld iterations (widest bound "
+                             "interval %.3e)", (long long)s.r, gap);
+                    throw Error{KB_ECONVERGENCE, buf};
+                }
+            }
+            return;
+        }
         for (;;) {
             check_version(s);
             launch_iterate(s, s.g->stream);

@@ -981,9 +981,23 @@ bool run_check(State &s, cudaStream_t st) {
         return s.h_flags[1] != 0;
     }
     const int64_t k = (s.kind == KB_RANKING) ? g.n : s.k;
-    const int64_t m = s.m_host;
     if (s.kind == KB_RANKING) return check_ranking(s, st);
     if (k > KMAX) return sorted_check(s, st, k);
+    const int nxt = topk_check_enqueue(s, st);
+    KB_CUDA(cudaEventSynchronize(s.chk_ev));
+    return topk_check_finish(s, nxt);
+}
+
+namespace {
+__global__ void k_publish(const unsigned long long *src, unsigned long long *dst) {
+    *dst = *src;
+}
+}  // namespace
+
+int topk_check_enqueue(State &s, cudaStream_t st) {
+    Graph &g = *s.g;
+    const int64_t k = s.k;
+    const int64_t m = s.m_host;
     unsigned long long *out = s.scratch_u64.p;  // [0..3)
     const int nxt = s.cur ^ 1;
     if (m <= k) {
@@ -1053,7 +1067,17 @@ bool run_check(State &s, cudaStream_t st) {
                                              s.act[nxt].p, out, s.eps, k); note_launch();
         KB_CUDA(cudaGetLastError());
     }
-    sync_read(s, st, out, 3);
+    // publish the verdict for a speculative K1 queued behind, then the one
+    // host read of this check
+    k_publish<<<1, 1, 0, st>>>(out + 1, s.abort_flag.p);
+    note_launch();
+    KB_CUDA(cudaMemcpyAsync(s.h_flags, out, 3 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaEventRecord(s.chk_ev, st));
+    return nxt;
+}
+
+bool topk_check_finish(State &s, int nxt) {
     s.cur = nxt;
     s.act_dense = false;
     s.m_host = (int64_t)s.h_flags[0];

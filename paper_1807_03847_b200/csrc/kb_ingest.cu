@@ -7,7 +7,7 @@
 // first dynamic batch spreads it out with per-row slack (kb_dynamic.cu).
 // The SELL layout K1 reads is (re)built from it by build_sell().
 #include <cub/block/block_reduce.cuh>
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/cub.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
@@ -566,33 +566,124 @@ __global__ void k_tri_counts(const int64_t *indptr, const int32_t *rlen, const i
     hi_cnt[u] = L - lo - self;
 }
 
-// forward upper-triangle keys u<<s|v (already in sorted order) and reversed
-// lower-triangle keys v<<s|u (to be sorted); one warp per row
-__global__ void k_tri_keys(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
-                           int64_t n, const int64_t *lo_off, const int64_t *hi_off,
-                           const int64_t *lo_cnt, int shift, uint64_t *fwd, uint64_t *rev) {
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n) return;
-    const int64_t u = warp;
-    const int32_t *row = indices + indptr[u];
-    const int64_t L = rlen[u], nlo = lo_cnt[u];
-    for (int64_t j = lane; j < L; j += 32) {
-        const int64_t v = row[j];
-        if (j < nlo) rev[lo_off[u] + j] = ((uint64_t)v << shift) | (uint64_t)u;
-        else if (v > u) {
-            const int64_t self = (nlo < L && row[nlo] == u) ? 1 : 0;
-            fwd[hi_off[u] + (j - nlo - self)] = ((uint64_t)u << shift) | (uint64_t)v;
+// Arcs of a row range, with every lane busy: a block takes SEG_ROWS rows,
+// scans the per-row counts in shared memory and strides over the
+// concatenated arcs; rows with more than SEG_LONG arcs are skipped here and
+// get a block each (k_*_long).  part(u) = (first slot, count) of the arcs
+// of row u the kernel visits.
+constexpr int SEG_ROWS = 256;
+constexpr int SEG_LONG = 1024;
+
+template <typename Part, typename Visit>
+__device__ __forceinline__ void seg_rows(int64_t n, Part part, Visit visit) {
+    __shared__ int off[SEG_ROWS + 1];
+    __shared__ int64_t first[SEG_ROWS];
+    const int64_t r0 = (int64_t)blockIdx.x * SEG_ROWS;
+    const int t = threadIdx.x;
+    int cnt = 0;
+    if (r0 + t < n) {
+        int64_t f, c;
+        part(r0 + t, f, c);
+        first[t] = f;
+        cnt = c > SEG_LONG ? 0 : (int)c;
+    }
+    off[t + 1] = cnt;
+    if (t == 0) off[0] = 0;
+    __syncthreads();
+    for (int d = 1; d < SEG_ROWS; d <<= 1) {
+        const int v = (t + 1 > d) ? off[t + 1 - d] : 0;
+        __syncthreads();
+        off[t + 1] += v;
+        __syncthreads();
+    }
+    const int total = off[SEG_ROWS];
+    for (int e = t; e < total; e += SEG_ROWS) {
+        int lo = 0, hi = SEG_ROWS;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= e) lo = mid; else hi = mid;
         }
+        visit(r0 + lo, first[lo], e - off[lo]);
     }
 }
 
-__global__ void k_equal_u64(const uint64_t *a, const uint64_t *b, int64_t m,
-                            unsigned long long *bad) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x)
-        if (a[i] != b[i]) { atomicAdd(bad, 1ull); return; }
+// lower-triangle arcs u -> v (v < u) as (key v, value u), written in row
+// order at lo_off[u]: a stable sort by v then lists each v's u ascending
+struct LowerPart {
+    const int64_t *lo_cnt;
+    __device__ void operator()(int64_t u, int64_t &f, int64_t &c) const { f = 0; c = lo_cnt[u]; }
+};
+
+__global__ void __launch_bounds__(SEG_ROWS) k_tri_pairs(const int64_t *indptr,
+                                                        const int32_t *indices, int64_t n,
+                                                        const int64_t *lo_off,
+                                                        const int64_t *lo_cnt, uint32_t *key,
+                                                        int32_t *val) {
+    seg_rows(n, LowerPart{lo_cnt}, [&](int64_t u, int64_t, int j) {
+        const int64_t o = lo_off[u] + j;
+        key[o] = (uint32_t)indices[indptr[u] + j];
+        val[o] = (int32_t)u;
+    });
 }
+
+__global__ void k_tri_pairs_long(const int32_t *rows, const int64_t *indptr,
+                                 const int32_t *indices, const int64_t *lo_off,
+                                 const int64_t *lo_cnt, uint32_t *key, int32_t *val) {
+    const int64_t u = rows[blockIdx.x];
+    const int64_t c = lo_cnt[u];
+    for (int64_t j = threadIdx.x; j < c; j += blockDim.x) {
+        key[lo_off[u] + j] = (uint32_t)indices[indptr[u] + j];
+        val[lo_off[u] + j] = (int32_t)u;
+    }
+}
+
+// upper-triangle arcs v -> w (w > v) in row order must equal the sorted
+// reversed lower arcs one for one
+struct UpperPart {
+    const int64_t *lo_cnt, *hi_cnt;
+    const int32_t *rlen;
+    __device__ void operator()(int64_t v, int64_t &f, int64_t &c) const {
+        c = hi_cnt[v];
+        f = rlen[v] - c;          // the upper part is the row's tail
+    }
+};
+
+__global__ void __launch_bounds__(SEG_ROWS) k_tri_match(const int64_t *indptr,
+                                                        const int32_t *rlen,
+                                                        const int32_t *indices, int64_t n,
+                                                        const int64_t *hi_off,
+                                                        const int64_t *lo_cnt,
+                                                        const int64_t *hi_cnt,
+                                                        const uint32_t *skey,
+                                                        const int32_t *sval,
+                                                        unsigned long long *bad) {
+    bool b = false;
+    seg_rows(n, UpperPart{lo_cnt, hi_cnt, rlen}, [&](int64_t v, int64_t f, int j) {
+        const int64_t o = hi_off[v] + j;
+        b |= skey[o] != (uint32_t)v || sval[o] != indices[indptr[v] + f + j];
+    });
+    if (b) atomicOr(bad, 1ull);
+}
+
+__global__ void k_tri_match_long(const int32_t *rows, const int64_t *indptr,
+                                 const int32_t *rlen, const int32_t *indices,
+                                 const int64_t *hi_off, const int64_t *hi_cnt,
+                                 const uint32_t *skey, const int32_t *sval,
+                                 unsigned long long *bad) {
+    const int64_t v = rows[blockIdx.x];
+    const int64_t c = hi_cnt[v], f = rlen[v] - c;
+    bool b = false;
+    for (int64_t j = threadIdx.x; j < c; j += blockDim.x) {
+        const int64_t o = hi_off[v] + j;
+        b |= skey[o] != (uint32_t)v || sval[o] != indices[indptr[v] + f + j];
+    }
+    if (b) atomicOr(bad, 1ull);
+}
+
+struct LongOf {
+    const int64_t *cnt;
+    __device__ bool operator()(int32_t r) const { return cnt[r] > SEG_LONG; }
+};
 }  // namespace
 
 // Graph.is_symmetric (graph.py:168-175): the arc set equals its reversal.
@@ -624,20 +715,51 @@ int graph_is_symmetric(Graph &g) {
     if (tot[0] != tot[1]) return 0;
     const int64_t h = tot[0];
     if (h == 0) return 1;
-    DBuf<uint64_t> fwd, rev, srev;
-    fwd.alloc(h); rev.alloc(h); srev.alloc(h);
-    k_tri_keys<<<blocks_for(n * 32, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p, n,
-                                                        lo_off.p, hi_off.p, lo_cnt.p, shift,
-                                                        fwd.p, rev.p);
+    // (v, u) pairs of the lower triangle in row order, stably sorted by v
+    // alone (the u's of each v stay ascending): 32-bit keys, 4 passes at
+    // most instead of a 64-bit (v, u) key sort
+    DBuf<uint32_t> key, skey;
+    DBuf<int32_t> val, sval, longs;
+    DBuf<int64_t> nlong;
+    key.alloc(h); skey.alloc(h); val.alloc(h); sval.alloc(h); longs.alloc(n); nlong.alloc(2);
+    k_tri_pairs<<<blocks_for(n, SEG_ROWS), SEG_ROWS, 0, st>>>(g.indptr.p, g.indices.p, n,
+                                                             lo_off.p, lo_cnt.p, key.p, val.p);
     note_launch();
+    cub::CountingInputIterator<int32_t> it(0);
     cub_run([&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, rev.p, srev.p, h, 0, 2 * shift, st);
+        return cub::DeviceSelect::If(t, b, it, longs.p, nlong.p, (int)n, LongOf{lo_cnt.p}, st);
+    });
+    int64_t nl = 0;
+    KB_CUDA(cudaMemcpyAsync(&nl, nlong.p, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    if (nl) {
+        k_tri_pairs_long<<<(unsigned)nl, 256, 0, st>>>(longs.p, g.indptr.p, g.indices.p,
+                                                        lo_off.p, lo_cnt.p, key.p, val.p);
+        note_launch();
+    }
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, key.p, skey.p, val.p, sval.p, h, 0, shift,
+                                               st);
     });
     DBuf<unsigned long long> bad;
     bad.alloc(1);
     KB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), st));
-    k_equal_u64<<<4 * std::max(1, g.sm_count), 256, 0, st>>>(fwd.p, srev.p, h, bad.p);
+    k_tri_match<<<blocks_for(n, SEG_ROWS), SEG_ROWS, 0, st>>>(
+        g.indptr.p, g.rlen.p, g.indices.p, n, hi_off.p, lo_cnt.p, hi_cnt.p, skey.p, sval.p,
+        bad.p);
     note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, it, longs.p, nlong.p + 1, (int)n, LongOf{hi_cnt.p},
+                                     st);
+    });
+    KB_CUDA(cudaMemcpyAsync(&nl, nlong.p + 1, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    if (nl) {
+        k_tri_match_long<<<(unsigned)nl, 256, 0, st>>>(longs.p, g.indptr.p, g.rlen.p,
+                                                        g.indices.p, hi_off.p, hi_cnt.p, skey.p,
+                                                        sval.p, bad.p);
+        note_launch();
+    }
     KB_CUDA(cudaGetLastError());
     unsigned long long hb = 0;
     KB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));

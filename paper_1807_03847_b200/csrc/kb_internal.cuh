@@ -199,6 +199,11 @@ struct State {
     // lower[x] <= fl(upper[q] - eps); while it still refutes, a check is
     // "not converged" without a pass over the set
     int32_t rk_q = -1, rk_x = -1;
+    // speculative iteration (TOPK runs): K1 of r+1 is queued behind check r
+    // and exits at once if that check converged (abort_flag, set on device)
+    DBuf<unsigned long long> abort_flag;
+    bool spec_abort = false;
+    cudaEvent_t chk_ev = nullptr;
     const double *x_level() const { return levels.back().p; }
 };
 
@@ -225,6 +230,11 @@ void launch_iterate(State &s, cudaStream_t st);
 void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only);
 void collect_k1_times(State &s);
 bool run_check(State &s, cudaStream_t st);      // returns converged
+// TOPK check split around its one host read: enqueue (kernels, publish the
+// verdict to abort_flag, D2H into h_flags, record chk_ev) / finish (after
+// chk_ev: adopt the new active set, return converged); -1: not applicable
+int topk_check_enqueue(State &s, cudaStream_t st);
+bool topk_check_finish(State &s, int nxt);
 double run_gap(State &s, cudaStream_t st);
 void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
                    DBuf<double> *upper, int64_t *h_pairs);

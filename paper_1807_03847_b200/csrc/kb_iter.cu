@@ -69,7 +69,12 @@ struct IterArgs {
     // exchange layout (hot_per entries each, blocks of 2^hot_shift ids)
     int hot_per, hot_shift;
     unsigned long long *counter;
+    const unsigned long long *abort;  // speculative launch: exit if set
 };
+
+__device__ __forceinline__ bool aborted(const IterArgs &A) {
+    return A.abort && *(const volatile unsigned long long *)A.abort != 0;
+}
 
 struct HotMap {
     int hot, per, shift;
@@ -192,6 +197,7 @@ __device__ __forceinline__ void narrow_group(const IterArgs &A, int64_t s0, int 
 
 template <int DEPTH, int XL, bool ST = false>
 __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
+    if (aborted(A)) return;
     extern __shared__ double hot_s[];
     const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u};
     if (ST) {
@@ -280,6 +286,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
 // so twice the warps keep loads in flight (K1 on C4 is latency-bound).
 template <int Q>
 __global__ void __launch_bounds__(1024, 2) k_sell_narrow(IterArgs A) {
+    if (aborted(A)) return;
     const int lane = threadIdx.x & 31;
     const uint64_t pol = evict_first_policy();
     const HotMap hm{0, 0, 0, 0u};
@@ -305,7 +312,7 @@ __global__ void k_ones_step(IterArgs A) {
 __global__ void k_heavy_combine(IterArgs A, const int32_t *seg_ptr,
                                 const int32_t *seg_list) {
     int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (h >= A.nh) return;
+    if (h >= A.nh || aborted(A)) return;
     double s = 0.0;
     for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++)
         s = __dadd_rn(s, A.seg_sum[seg_list[q]]);
@@ -328,6 +335,7 @@ __global__ void k_empty_rows(double *upper, double *lower, const double *katz,
 __global__ void k_ovf_rows(IterArgs A, const int32_t *rows, int64_t nr, const int32_t *perm,
                            const int32_t *iperm, const int64_t *indptr, const int32_t *rlen,
                            const int32_t *indices, int64_t split) {
+    if (aborted(A)) return;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= nr) return;
@@ -446,6 +454,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         A.hot = (int)(A.hot_per * P);
     }
     A.counter = s.work_counter.p;
+    A.abort = s.spec_abort ? s.abort_flag.p : nullptr;
     if (s.seg_sum.n < (size_t)std::max<int64_t>(1, g.sell.nseg)) {
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
         A.seg_sum = s.seg_sum.p;
