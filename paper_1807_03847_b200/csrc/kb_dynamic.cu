@@ -169,11 +169,17 @@ __global__ void k_compact_len(const int32_t *rlen, int64_t n, int64_t *len) {
     len[v] = v < n ? rlen[v] : 0;
 }
 
-// Rebuild the slack layout: capacity = len (+extra) + max(2, len/8).
-void respread(Graph &g, const int32_t *extra) {
+}  // namespace
+
+// The slack layout for the current row lengths (+extra): capacity = len
+// (+extra) + max(2, len/8), row starts nip, the column array nix with 1/16
+// tail room (rows that later outgrow their slack are relocated there instead
+// of re-spreading the whole graph) and g.rcap.  Rows are not copied.
+void slack_layout(Graph &g, const int32_t *extra, DBuf<int64_t> &nip, DBuf<int32_t> &nix,
+                  int64_t &total) {
     cudaStream_t st = g.stream;
     const int64_t n = g.n;
-    DBuf<int64_t> cap, nip;
+    DBuf<int64_t> cap;
     cap.alloc(n + 1);
     nip.alloc(n + 1);
     k_capacity<<<nblk(n + 1, 256), 256, 0, st>>>(g.rlen.p, extra, n, cap.p);
@@ -181,18 +187,25 @@ void respread(Graph &g, const int32_t *extra) {
     cub_run([&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, cap.p, nip.p, (int)(n + 1), st);
     });
-    int64_t total = 0;
+    total = 0;
     KB_CUDA(cudaMemcpyAsync(&total, nip.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    // reserve tail room for rows that later outgrow their slack (relocated
-    // there instead of re-spreading the whole graph)
     const int64_t room = std::max<int64_t>(total / 16, (int64_t)1 << 20);
-    DBuf<int32_t> nix;
     nix.alloc(total + room);
-    copy_rows(g.indptr.p, g.indices.p, g.rlen.p, n, nip.p, nix.p, st);
     g.rcap.alloc(std::max<int64_t>(1, n));
     k_cap32<<<nblk(n, 256), 256, 0, st>>>(cap.p, n, g.rcap.p);
     note_launch();
+}
+
+namespace {
+
+// Rebuild the slack layout and copy every row into it.
+void respread(Graph &g, const int32_t *extra) {
+    DBuf<int64_t> nip;
+    DBuf<int32_t> nix;
+    int64_t total = 0;
+    slack_layout(g, extra, nip, nix, total);
+    copy_rows(g.indptr.p, g.indices.p, g.rlen.p, g.n, nip.p, nix.p, g.stream);
     g.indptr = std::move(nip);
     g.indices = std::move(nix);
     g.tail = total;
@@ -530,23 +543,6 @@ __global__ void k_widen_i32(const int32_t *a, int64_t n, int64_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = a[i];
 }
-
-struct PhaseTrace {
-    bool on;
-    std::chrono::steady_clock::time_point t0;
-    cudaStream_t st;
-    explicit PhaseTrace(cudaStream_t s) : on(getenv("KB_TRACE") != nullptr), st(s) {
-        t0 = std::chrono::steady_clock::now();
-    }
-    void mark(const char *what) {
-        if (!on) return;
-        cudaStreamSynchronize(st);
-        auto t1 = std::chrono::steady_clock::now();
-        fprintf(stderr, "[kb] %-28s %9.3f ms\n", what,
-                std::chrono::duration<double, std::milli>(t1 - t0).count());
-        t0 = t1;
-    }
-};
 
 }  // namespace
 

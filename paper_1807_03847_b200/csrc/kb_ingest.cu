@@ -11,7 +11,13 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <cub/iterator/counting_input_iterator.cuh>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <numeric>
 
 #include "kb_internal.cuh"
@@ -232,14 +238,69 @@ void cub_run(F &&f) {
     note_launch();
 }
 
+// heavy row h: full[h] segments of T arcs plus one partial one if deg % T;
+// the sort key orders partial segments by descending remainder (T: none)
+__global__ void k_seg_counts(const int32_t *hdeg, int64_t nh, int64_t T, int32_t *full,
+                             int32_t *tot, uint32_t *pkey, int32_t *hid) {
+    int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h > nh) return;
+    if (h == nh) { full[h] = tot[h] = 0; return; }
+    const int64_t d = hdeg[h], f = d / T, r = d % T;
+    full[h] = (int32_t)f;
+    tot[h] = (int32_t)(f + (r ? 1 : 0));
+    pkey[h] = (uint32_t)(r ? T - r : T);
+    hid[h] = (int32_t)h;
+}
+
+// partial segment ids follow the F full ones in sorted (remainder) order
+__global__ void k_seg_rank(const int32_t *hid_sorted, const uint32_t *key_sorted, int64_t nh,
+                           int64_t T, const int32_t *fstart, int32_t *pid) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nh && key_sorted[i] < (uint32_t)T) pid[hid_sorted[i]] = fstart[nh] + (int32_t)i;
+}
+
+__global__ void k_seg_fill(const int32_t *hdeg, int64_t nh, int64_t T, const int32_t *fstart,
+                           const int32_t *seg_ptr, const int32_t *pid, int32_t *seg_row,
+                           int32_t *seg_start, int32_t *seg_len, int32_t *seg_list) {
+    int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h >= nh) return;
+    const int64_t d = hdeg[h], f = d / T, r = d % T;
+    for (int64_t q = 0; q < f; q++) {
+        const int32_t sid = fstart[h] + (int32_t)q;
+        seg_row[sid] = (int32_t)h;
+        seg_start[sid] = (int32_t)(q * T);
+        seg_len[sid] = (int32_t)T;
+        seg_list[seg_ptr[h] + q] = sid;
+    }
+    if (r) {
+        const int32_t sid = pid[h];
+        seg_row[sid] = (int32_t)h;
+        seg_start[sid] = (int32_t)(f * T);
+        seg_len[sid] = (int32_t)r;
+        seg_list[seg_ptr[h] + f] = sid;
+    }
+}
+
+// 1 + the last slice wider than 4 (0 if none)
+__global__ void k_last_wide(const int32_t *slice_w, int64_t nslices, unsigned long long *out) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool wide = s < nslices && slice_w[s] > 4;
+    if (__any_sync(0xffffffffu, wide)) {
+        unsigned long long v = wide ? (unsigned long long)(s + 1) : 0ull;
+        for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if ((threadIdx.x & 31) == 0) atomicMax(out, v);
+    }
+}
+
 }  // namespace
 
 // Virtual rows, slices and column slots for the current arc set under the
 // current relabelling.  `fresh` means perm sorts rows by descending length,
 // so heavy / normal / empty rows are the contiguous new-id ranges
 // [0,nh) / [nh,nv) / [nv,n) and no explicit row maps are needed.
-void build_sell(Graph &g, bool fresh) {
+void build_sell(Graph &g, bool fresh, bool fill) {
     cudaStream_t st = g.stream;
+    PhaseTrace tr(st);
     const int64_t n = g.n;
     if (!g.deg.p) g.deg.alloc(n);
     if (n) k_len_by_new<<<blocks_for(n, 256), 256, 0, st>>>(g.rlen.p, g.perm.p, n, g.deg.p);
@@ -312,77 +373,72 @@ void build_sell(Graph &g, bool fresh) {
         }
     }
     g.hot = std::min<int64_t>(g.hot, g.n);
+    tr.mark("  sell: row classes");
 
-    // ---- heavy rows -> segments (host plan; nh is small)
-    std::vector<int32_t> hdeg(g.nh);
-    if (g.nh) {
-        if (fresh) {
-            KB_CUDA(cudaMemcpyAsync(hdeg.data(), g.deg.p, g.nh * sizeof(int32_t),
-                                    cudaMemcpyDeviceToHost, st));
-        } else {
-            DBuf<int32_t> hd;
-            hd.alloc(g.nh);
-            k_gather_keys<<<blocks_for(g.nh, 256), 256, 0, st>>>(
-                (const uint32_t *)g.deg.p, g.hrow.p, g.nh, (uint32_t *)hd.p);
-            note_launch();
-            KB_CUDA(cudaMemcpyAsync(hdeg.data(), hd.p, g.nh * sizeof(int32_t),
-                                    cudaMemcpyDeviceToHost, st));
-            KB_CUDA(cudaStreamSynchronize(st));
-        }
-        KB_CUDA(cudaStreamSynchronize(st));
-    }
-    std::vector<int32_t> seg_row, seg_start, seg_len;
-    std::vector<std::vector<int32_t>> row_segs(g.nh);
+    // ---- heavy rows -> segments, planned on the device (no host round trip
+    // while a pipelined upload holds the copy engine).  Full segments come
+    // first, row by row; then one partial segment per row with a remainder,
+    // longest remainder first (stable in h), so the long chains start early.
     const int64_t T = g.split;
-    for (int64_t h = 0; h < g.nh; h++) {  // full segments, row by row
-        const int64_t full = hdeg[h] / T;
-        for (int64_t q = 0; q < full; q++) {
-            row_segs[h].push_back((int32_t)seg_row.size());
-            seg_row.push_back((int32_t)h);
-            seg_start.push_back((int32_t)(q * T));
-            seg_len.push_back((int32_t)T);
-        }
-    }
-    std::vector<int64_t> partial;
-    for (int64_t h = 0; h < g.nh; h++)
-        if (hdeg[h] % T) partial.push_back(h);
-    std::stable_sort(partial.begin(), partial.end(), [&](int64_t a, int64_t b) {
-        return hdeg[a] % T > hdeg[b] % T;
-    });
-    for (int64_t h : partial) {
-        row_segs[h].push_back((int32_t)seg_row.size());
-        seg_row.push_back((int32_t)h);
-        seg_start.push_back((int32_t)((hdeg[h] / T) * T));
-        seg_len.push_back((int32_t)(hdeg[h] % T));
-    }
-    std::vector<int32_t> sptr(g.nh + 1, 0), slist;
-    for (int64_t h = 0; h < g.nh; h++) {
-        for (int32_t x : row_segs[h]) slist.push_back(x);
-        sptr[h + 1] = (int32_t)slist.size();
-    }
     Sell &S = g.sell;
-    S.nseg = (int64_t)seg_row.size();
-    S.nvr = S.nseg + (g.nv - g.nh);
-    S.nslices = (S.nvr + 31) / 32;
-    g.seg_ptr.alloc(g.nh + 1);
-    g.seg_list.alloc(std::max<size_t>(1, slist.size()));
-    KB_CUDA(cudaMemcpyAsync(g.seg_ptr.p, sptr.data(), sptr.size() * sizeof(int32_t),
-                            cudaMemcpyHostToDevice, st));
-    if (!slist.empty())
-        KB_CUDA(cudaMemcpyAsync(g.seg_list.p, slist.data(), slist.size() * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
     DBuf<int32_t> d_seg_row, d_seg_start;
-    d_seg_row.alloc(std::max<size_t>(1, seg_row.size()));
-    d_seg_start.alloc(std::max<size_t>(1, seg_row.size()));
-    S.vlen.alloc(S.nvr);
-    if (S.nseg) {
-        KB_CUDA(cudaMemcpyAsync(d_seg_row.p, seg_row.data(), S.nseg * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
-        KB_CUDA(cudaMemcpyAsync(d_seg_start.p, seg_start.data(), S.nseg * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
-        KB_CUDA(cudaMemcpyAsync(S.vlen.p, seg_len.data(), S.nseg * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
+    g.seg_ptr.alloc(g.nh + 1);
+    if (g.nh) {
+        const int64_t nh = g.nh;
+        DBuf<int32_t> hdeg, full, tot, fstart, hid, hid2, pid;
+        DBuf<uint32_t> pkey, pkey2;
+        const int32_t *hd = g.deg.p;
+        if (!fresh) {
+            hdeg.alloc(nh);
+            k_gather_keys<<<blocks_for(nh, 256), 256, 0, st>>>(
+                (const uint32_t *)g.deg.p, g.hrow.p, nh, (uint32_t *)hdeg.p);
+            note_launch();
+            hd = hdeg.p;
+        }
+        full.alloc(nh + 1); tot.alloc(nh + 1); fstart.alloc(nh + 1);
+        hid.alloc(nh); hid2.alloc(nh); pid.alloc(nh); pkey.alloc(nh); pkey2.alloc(nh);
+        k_seg_counts<<<blocks_for(nh + 1, 256), 256, 0, st>>>(hd, nh, T, full.p, tot.p, pkey.p,
+                                                             hid.p);
+        note_launch();
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, full.p, fstart.p, (int)(nh + 1), st);
+        });
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, tot.p, g.seg_ptr.p, (int)(nh + 1), st);
+        });
+        int bits = 1;
+        while (((int64_t)1 << bits) <= T) bits++;
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, pkey.p, pkey2.p, hid.p, hid2.p, (int)nh,
+                                                   0, bits, st);
+        });
+        int32_t ns = 0;
+        KB_CUDA(cudaMemcpyAsync(&ns, g.seg_ptr.p + nh, sizeof(ns), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        S.nseg = ns;
+        g.seg_list.alloc(std::max<int64_t>(1, ns));
+        d_seg_row.alloc(std::max<int64_t>(1, ns));
+        d_seg_start.alloc(std::max<int64_t>(1, ns));
+        S.nvr = S.nseg + (g.nv - g.nh);
+        S.vlen.alloc(S.nvr);
+        k_seg_rank<<<blocks_for(nh, 256), 256, 0, st>>>(hid2.p, pkey2.p, nh, T, fstart.p, pid.p);
+        note_launch();
+        k_seg_fill<<<blocks_for(nh, 128), 128, 0, st>>>(hd, nh, T, fstart.p, g.seg_ptr.p, pid.p,
+                                                        d_seg_row.p, d_seg_start.p, S.vlen.p,
+                                                        g.seg_list.p);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    } else {
+        KB_CUDA(cudaMemsetAsync(g.seg_ptr.p, 0, sizeof(int32_t), st));
+        S.nseg = 0;
+        g.seg_list.alloc(1);
+        d_seg_row.alloc(1);
+        d_seg_start.alloc(1);
+        S.nvr = g.nv - g.nh;
+        S.vlen.alloc(S.nvr);
     }
+    S.nslices = (S.nvr + 31) / 32;
+    tr.mark("  sell: segment plan");
     const int64_t nnorm = g.nv - g.nh;
     if (nnorm) {
         k_vlen_normal<<<blocks_for(nnorm, 256), 256, 0, st>>>(g.deg.p, g.vrow.p, g.nh, nnorm,
@@ -407,21 +463,29 @@ void build_sell(Graph &g, bool fresh) {
     KB_CUDA(cudaMemcpyAsync(&S.elems, S.slice_off.p + S.nslices, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));
     {   // narrow tail: K1 takes those slices four at a time
-        std::vector<int32_t> hw(S.nslices);
-        if (S.nslices)
-            KB_CUDA(cudaMemcpyAsync(hw.data(), S.slice_w.p, S.nslices * sizeof(int32_t),
-                                    cudaMemcpyDeviceToHost, st));
+        DBuf<unsigned long long> lw;
+        lw.alloc(1);
+        KB_CUDA(cudaMemsetAsync(lw.p, 0, sizeof(unsigned long long), st));
+        if (S.nslices) {
+            k_last_wide<<<blocks_for(S.nslices, 256), 256, 0, st>>>(S.slice_w.p, S.nslices, lw.p);
+            note_launch();
+        }
+        unsigned long long h = 0;
+        KB_CUDA(cudaMemcpyAsync(&h, lw.p, sizeof(h), cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaStreamSynchronize(st));
-        int64_t t = S.nslices;
-        while (t > 0 && hw[t - 1] <= 4) t--;
-        S.nwide = t;
+        S.nwide = (int64_t)h;
     }
     KB_CUDA(cudaStreamSynchronize(st));
     sz.release();
+    tr.mark("  sell: slice widths");
 
     // ---- fill the column slots (relabelled, original per-row order)
     S.cols.alloc(S.elems + 4);
-    if (S.nslices) {
+    if (!fill) {
+        // filled row by row as the arcs arrive (pipelined ingest); slots past
+        // a row's length read as column 0 like k_fill's padding
+        KB_CUDA(cudaMemsetAsync(S.cols.p, 0, S.cols.bytes(), st));
+    } else if (S.nslices) {
         const int64_t threads = S.nslices * 32;
         k_fill<<<blocks_for(threads, 256), 256, 0, st>>>(
             g.indptr.p, g.indices.p, g.perm.p, g.iperm.p, S.vlen.p, d_seg_row.p, d_seg_start.p,
@@ -430,6 +494,7 @@ void build_sell(Graph &g, bool fresh) {
         note_launch();
         KB_CUDA(cudaGetLastError());
     }
+    tr.mark("  sell: cols");
     // reverse maps for in-place patching by dynamic batches
     g.vr_of_row.alloc(std::max<int64_t>(1, n));
     g.h_of_row.alloc(std::max<int64_t>(1, n));
@@ -480,20 +545,9 @@ void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne) {
     if (g.n_ovf > std::max<int64_t>(4096, g.nv / 32)) g.sell_dirty = true;
 }
 
-void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
-    cudaStream_t st = g.stream;
-    g.indptr.alloc(g.n + 1);
-    g.indices.alloc(g.nnz);
-    KB_CUDA(cudaMemcpyAsync(g.indptr.p, h_indptr, (g.n + 1) * sizeof(int64_t),
-                            cudaMemcpyHostToDevice, st));
-    if (g.nnz)
-        KB_CUDA(cudaMemcpyAsync(g.indices.p, h_indices, g.nnz * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
-    build_graph_device(g);
-}
-
-// g.indptr / g.indices hold a compact canonical CSR on the device
-void build_graph_device(Graph &g) {
+// Row lengths, the degree relabelling and the original-id lists K3 uses:
+// everything that depends on g.indptr alone.
+static void build_rows(Graph &g) {
     cudaStream_t st = g.stream;
     const int64_t n = g.n;
     g.rlen.alloc(n);
@@ -544,227 +598,560 @@ void build_graph_device(Graph &g) {
                                               (int)n, st);
         });
     }
+}
+
+// g.indptr / g.indices hold a compact canonical CSR on the device
+void build_graph_device(Graph &g) {
+    build_rows(g);
     build_sell(g, g.relabel);
     make_slack(g);
 }
 
 
 namespace {
-// per row u: arcs to smaller ids (lower triangle) and to larger ids (upper)
-__global__ void k_tri_counts(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
-                             int64_t n, int64_t *lo_cnt, int64_t *hi_cnt) {
-    int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (u > n) return;
-    if (u == n) { lo_cnt[u] = hi_cnt[u] = 0; return; }
-    const int32_t *row = indices + indptr[u];
-    const int64_t L = rlen[u];
-    int64_t a = 0, b = L;  // first slot with col >= u
-    while (a < b) { const int64_t m = (a + b) >> 1; if (row[m] < u) a = m + 1; else b = m; }
-    const int64_t lo = a;
-    const int64_t self = (lo < L && row[lo] == u) ? 1 : 0;
-    lo_cnt[u] = lo;
-    hi_cnt[u] = L - lo - self;
+
+// ---------------------------------------------------------------- row passes
+// Per-arc work over a range of rows of a CSR (row starts ip, lengths rl,
+// columns ix).  Rows of at most LONG_ARCS arcs are taken TILE_ROWS at a time
+// by one block that scans their lengths and strides over the concatenated
+// arcs with every thread busy (R-MAT rows average ~30 arcs); longer rows get
+// a block each from a host-side list.
+constexpr int TILE_ROWS = 256;
+constexpr int LONG_ARCS = 256;   // tiles stay balanced: <= 64K arcs each
+
+enum : int { OP_VALIDATE = 1, OP_COPY = 2, OP_FILL = 4, OP_SCATTER = 8, OP_ORDER = 16 };
+enum : unsigned long long { F_ASYM = 1, F_INVALID = 2 };
+
+struct RowOps {
+    const int64_t *ip;
+    const int32_t *rl;
+    const int32_t *ix;
+    int64_t n;
+    int ops;
+    unsigned long long *flags;
+    // symmetry buckets: lower arc u -> v (v < u) goes to bkt[ip[v] + k] with
+    // k < rl[v] taken from fill[v]
+    unsigned int *fill;
+    int32_t *bkt;
+    // slack copy: row u to nix[nip[u] ..)
+    const int64_t *nip;
+    int32_t *nix;
+    // SELL fill (the plan of build_sell)
+    const int32_t *iperm, *vr_of_row, *h_of_row, *seg_ptr, *seg_list, *slice_w;
+    const int64_t *slice_off;
+    int32_t *cols;
+    int64_t split;
+};
+
+struct RowCtx {
+    int64_t first, dst, base;
+    int w, lane, h;
+};
+
+__device__ __forceinline__ void row_ctx(const RowOps &A, int64_t u, RowCtx &c) {
+    c.first = A.ip[u];
+    c.dst = (A.ops & OP_COPY) ? A.nip[u] : 0;
+    c.h = -1;
+    c.base = 0;
+    c.w = 0;
+    c.lane = 0;
+    if (A.ops & OP_FILL) {
+        const int32_t v = A.iperm[u];
+        const int32_t vr = A.vr_of_row[v];
+        if (vr >= 0) {
+            const int64_t s = vr >> 5;
+            c.base = A.slice_off[s];
+            c.w = A.slice_w[s];
+            c.lane = vr & 31;
+        } else {
+            c.h = A.h_of_row[v];
+        }
+    }
 }
 
-// Arcs of a row range, with every lane busy: a block takes SEG_ROWS rows,
-// scans the per-row counts in shared memory and strides over the
-// concatenated arcs; rows with more than SEG_LONG arcs are skipped here and
-// get a block each (k_*_long).  part(u) = (first slot, count) of the arcs
-// of row u the kernel visits.
-constexpr int SEG_ROWS = 256;
-constexpr int SEG_LONG = 1024;
+__device__ __forceinline__ int64_t sell_pos(int w, int lane, int64_t j) {
+    return (w <= 4) ? j * 32 + lane : (j >> 2) * 128 + lane * 4 + (j & 3);
+}
 
-template <typename Part, typename Visit>
-__device__ __forceinline__ void seg_rows(int64_t n, Part part, Visit visit) {
-    __shared__ int off[SEG_ROWS + 1];
-    __shared__ int64_t first[SEG_ROWS];
-    const int64_t r0 = (int64_t)blockIdx.x * SEG_ROWS;
+// arc j of row u: validate, copy to the slack layout, place the relabelled
+// column in its SELL slot, drop the reversed lower arc into its bucket
+__device__ __forceinline__ void arc_ops(const RowOps &A, int64_t u, const RowCtx &c, int64_t j,
+                                        bool &asym, bool &bad) {
+    const int32_t col = A.ix[c.first + j];
+    const bool in_range = col >= 0 && (int64_t)col < A.n;
+    if (A.ops & OP_VALIDATE) {
+        if (!in_range || ((A.ops & OP_ORDER) && j > 0 && A.ix[c.first + j - 1] >= col))
+            bad = true;
+    }
+    if (A.ops & OP_COPY) A.nix[c.dst + j] = col;
+    if (!in_range) return;
+    if (A.ops & OP_FILL) {
+        const int32_t nc = A.iperm[col];
+        if (c.h < 0) {
+            A.cols[c.base + sell_pos(c.w, c.lane, j)] = nc;
+        } else {
+            const int64_t q = j / A.split;
+            const int32_t vr = A.seg_list[A.seg_ptr[c.h] + q];
+            const int64_t s = vr >> 5;
+            A.cols[A.slice_off[s] + sell_pos(A.slice_w[s], vr & 31, j - q * A.split)] = nc;
+        }
+    }
+    if ((A.ops & OP_SCATTER) && (int64_t)col < u) {
+        const unsigned k = atomicAdd(A.fill + col, 1u);
+        if (k < (unsigned)A.rl[col]) A.bkt[A.ip[col] + k] = (int32_t)u;
+        else asym = true;  // more reversed arcs than the row has slots
+    }
+}
+
+__device__ __forceinline__ void raise_flags(const RowOps &A, bool asym, bool bad) {
+    const unsigned long long f = (asym ? F_ASYM : 0ull) | (bad ? F_INVALID : 0ull);
+    if (__any_sync(0xffffffffu, f != 0)) {
+        if (f) atomicOr(A.flags, f);
+    }
+}
+
+// index in the block's exclusive offsets of the row holding element e
+__device__ __forceinline__ int tile_row(const int *off, int e) {
+    int lo = 0, hi = TILE_ROWS;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= e) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(TILE_ROWS) k_rows_tile(RowOps A, int64_t a, int64_t b) {
+    typedef cub::BlockScan<int, TILE_ROWS> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int off[TILE_ROWS + 1];
+    __shared__ RowCtx ctx[TILE_ROWS];
+    const int64_t r0 = a + (int64_t)blockIdx.x * TILE_ROWS;
     const int t = threadIdx.x;
     int cnt = 0;
-    if (r0 + t < n) {
-        int64_t f, c;
-        part(r0 + t, f, c);
-        first[t] = f;
-        cnt = c > SEG_LONG ? 0 : (int)c;
-    }
-    off[t + 1] = cnt;
-    if (t == 0) off[0] = 0;
-    __syncthreads();
-    for (int d = 1; d < SEG_ROWS; d <<= 1) {
-        const int v = (t + 1 > d) ? off[t + 1 - d] : 0;
-        __syncthreads();
-        off[t + 1] += v;
-        __syncthreads();
-    }
-    const int total = off[SEG_ROWS];
-    for (int e = t; e < total; e += SEG_ROWS) {
-        int lo = 0, hi = SEG_ROWS;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (off[mid] <= e) lo = mid; else hi = mid;
+    if (r0 + t < b) {
+        const int L = A.rl[r0 + t];
+        if (L <= LONG_ARCS) {
+            cnt = L;
+            row_ctx(A, r0 + t, ctx[t]);
         }
-        visit(r0 + lo, first[lo], e - off[lo]);
     }
+    int ex, total;
+    Scan(tmp).ExclusiveSum(cnt, ex, total);
+    off[t] = ex;
+    if (t == 0) off[TILE_ROWS] = total;
+    __syncthreads();
+    bool asym = false, bad = false;
+    for (int e = t; e < total; e += TILE_ROWS) {
+        const int lo = tile_row(off, e);
+        arc_ops(A, r0 + lo, ctx[lo], e - off[lo], asym, bad);
+    }
+    raise_flags(A, asym, bad);
 }
 
-// lower-triangle arcs u -> v (v < u) as (key v, value u), written in row
-// order at lo_off[u]: a stable sort by v then lists each v's u ascending
-struct LowerPart {
-    const int64_t *lo_cnt;
-    __device__ void operator()(int64_t u, int64_t &f, int64_t &c) const { f = 0; c = lo_cnt[u]; }
+// long rows are cut into items of LONG_ITEM arcs (row, first arc), so a hub
+// row spreads over many blocks instead of serialising the pass's tail
+constexpr int LONG_ITEM = 2048;
+
+__global__ void k_rows_long(RowOps A, const int32_t *item_row, const int32_t *item_j0) {
+    __shared__ RowCtx c;
+    const int64_t u = item_row[blockIdx.x];
+    if (threadIdx.x == 0) row_ctx(A, u, c);
+    __syncthreads();
+    const int64_t j0 = item_j0[blockIdx.x];
+    const int64_t j1 = min((int64_t)A.rl[u], j0 + LONG_ITEM);
+    bool asym = false, bad = false;
+    for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) arc_ops(A, u, c, j, asym, bad);
+    raise_flags(A, asym, bad);
+}
+
+// first index of the ascending row with a column > v
+__device__ __forceinline__ int64_t upper_start(const int32_t *row, int64_t L, int64_t v) {
+    int64_t lo = 0, hi = L;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)row[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ bool contains(const int32_t *a, int64_t n, int32_t x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && a[lo] == x;
+}
+
+// Row v's bucket holds the sources u > v of the arcs u -> v.  The arc set is
+// symmetric iff for every v the bucket has exactly as many entries as v has
+// upper arcs v -> w (w > v) and each entry is one of those w: the entries
+// are distinct (one per row u, rows strictly ascending), so the bucket then
+// equals the upper part and every arc has its reversal.
+__global__ void __launch_bounds__(TILE_ROWS) k_verify_tile(RowOps A, int64_t a, int64_t b) {
+    typedef cub::BlockScan<int, TILE_ROWS> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int off[TILE_ROWS + 1];
+    __shared__ int64_t first[TILE_ROWS], up[TILE_ROWS];
+    __shared__ int hi_n[TILE_ROWS];
+    const int64_t r0 = a + (int64_t)blockIdx.x * TILE_ROWS;
+    const int t = threadIdx.x;
+    int cnt = 0;
+    bool asym = false;
+    if (r0 + t < b) {
+        const int64_t v = r0 + t;
+        const int64_t L = A.rl[v];
+        const int64_t f = A.ip[v];
+        const int64_t u0 = upper_start(A.ix + f, L, v);
+        const unsigned got = A.fill[v];
+        if ((int64_t)got != L - u0) asym = true;
+        first[t] = f;
+        up[t] = f + u0;
+        hi_n[t] = (int)(L - u0);
+        if (L <= LONG_ARCS && !asym) cnt = (int)(L - u0);
+    }
+    int ex, total;
+    Scan(tmp).ExclusiveSum(cnt, ex, total);
+    off[t] = ex;
+    if (t == 0) off[TILE_ROWS] = total;
+    __syncthreads();
+    for (int e = t; e < total; e += TILE_ROWS) {
+        const int lo = tile_row(off, e);
+        const int32_t u = A.bkt[first[lo] + (e - off[lo])];
+        if (!contains(A.ix + up[lo], hi_n[lo], u)) asym = true;
+    }
+    raise_flags(A, asym, false);
+}
+
+// A long row's buckets are checked against a sample of its upper part in
+// shared memory (every stride-th column, at most VSAMPLES of them): each
+// search is a shared-memory bisection plus one short window in global
+// memory instead of ~19 dependent loads through L2.
+constexpr int VSAMPLES = 4096;
+
+__global__ void __launch_bounds__(256) k_verify_long(RowOps A, const int32_t *item_row,
+                                                     const int32_t *item_j0) {
+    __shared__ int64_t u0s;
+    __shared__ int32_t samp[VSAMPLES];
+    const int64_t v = item_row[blockIdx.x];
+    const int64_t L = A.rl[v], f = A.ip[v];
+    if (threadIdx.x == 0) u0s = upper_start(A.ix + f, L, v);
+    __syncthreads();
+    const int64_t u0 = u0s, hn = L - u0;
+    if ((int64_t)A.fill[v] != hn) return;  // k_verify_tile flagged the row
+    const int32_t *U = A.ix + f + u0;
+    const int64_t stride = (hn + VSAMPLES - 1) / VSAMPLES;
+    const int ns = (int)((hn + stride - 1) / stride);
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) samp[i] = U[i * stride];
+    __syncthreads();
+    const int64_t e0 = item_j0[blockIdx.x], e1 = min(hn, e0 + LONG_ITEM);
+    bool asym = false;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const int32_t x = A.bkt[f + e];
+        int lo = 0, hi = ns;  // first sample > x
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (samp[mid] <= x) lo = mid + 1; else hi = mid;
+        }
+        if (lo == 0) { asym = true; continue; }  // below every upper column
+        const int64_t w0 = (int64_t)(lo - 1) * stride;
+        if (!contains(U + w0, min(stride, hn - w0), x)) asym = true;
+    }
+    raise_flags(A, asym, false);
+}
+
+struct LongRow {
+    const int32_t *rl;
+    __device__ bool operator()(int32_t r) const { return rl[r] > LONG_ARCS; }
 };
 
-__global__ void __launch_bounds__(SEG_ROWS) k_tri_pairs(const int64_t *indptr,
-                                                        const int32_t *indices, int64_t n,
-                                                        const int64_t *lo_off,
-                                                        const int64_t *lo_cnt, uint32_t *key,
-                                                        int32_t *val) {
-    seg_rows(n, LowerPart{lo_cnt}, [&](int64_t u, int64_t, int j) {
-        const int64_t o = lo_off[u] + j;
-        key[o] = (uint32_t)indices[indptr[u] + j];
-        val[o] = (int32_t)u;
-    });
+__global__ void k_item_counts(const int32_t *len, int64_t m, int32_t *cnt) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) cnt[i] = (len[i] + LONG_ITEM - 1) / LONG_ITEM;
+    else if (i == m) cnt[i] = 0;
 }
 
-__global__ void k_tri_pairs_long(const int32_t *rows, const int64_t *indptr,
-                                 const int32_t *indices, const int64_t *lo_off,
-                                 const int64_t *lo_cnt, uint32_t *key, int32_t *val) {
-    const int64_t u = rows[blockIdx.x];
-    const int64_t c = lo_cnt[u];
-    for (int64_t j = threadIdx.x; j < c; j += blockDim.x) {
-        key[lo_off[u] + j] = (uint32_t)indices[indptr[u] + j];
-        val[lo_off[u] + j] = (int32_t)u;
+__global__ void k_item_fill(const int32_t *rows, const int32_t *len, const int32_t *pre,
+                            int64_t m, int32_t *item_row, int32_t *item_j0) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    for (int32_t k = 0, j = 0; j < len[i]; k++, j += LONG_ITEM) {
+        item_row[pre[i] + k] = rows[i];
+        item_j0[pre[i] + k] = j;
     }
 }
 
-// upper-triangle arcs v -> w (w > v) in row order must equal the sorted
-// reversed lower arcs one for one
-struct UpperPart {
-    const int64_t *lo_cnt, *hi_cnt;
-    const int32_t *rlen;
-    __device__ void operator()(int64_t v, int64_t &f, int64_t &c) const {
-        c = hi_cnt[v];
-        f = rlen[v] - c;          // the upper part is the row's tail
+// Work items of the rows of rl longer than LONG_ARCS, ascending by row:
+// (row, first arc) every LONG_ITEM arcs.  Host copy of the item rows for the
+// per-chunk ranges, device copies for the kernels.
+struct LongItems {
+    std::vector<int32_t> row;      // host, ascending
+    DBuf<int32_t> d_row, d_j0;
+    void build(const int32_t *rl, int64_t n, cudaStream_t st) {
+        DBuf<int32_t> d, len;
+        DBuf<int64_t> cnt;
+        d.alloc(std::max<int64_t>(1, n));
+        cnt.alloc(1);
+        cub::CountingInputIterator<int32_t> it(0);
+        cub_run([&](void *t, size_t &b) {
+            return cub::DeviceSelect::If(t, b, it, d.p, cnt.p, (int)n, LongRow{rl}, st);
+        });
+        int64_t m = 0;
+        KB_CUDA(cudaMemcpyAsync(&m, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> rows(m), lens(m);
+        if (m) {
+            len.alloc(m);
+            k_gather_keys<<<blocks_for(m, 256), 256, 0, st>>>((const uint32_t *)rl, d.p, m,
+                                                              (uint32_t *)len.p);
+            note_launch();
+            KB_CUDA(cudaMemcpyAsync(rows.data(), d.p, m * 4, cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaMemcpyAsync(lens.data(), len.p, m * 4, cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaStreamSynchronize(st));
+        }
+        // host mirror of the item rows (for the per-chunk ranges); the device
+        // arrays are written by a kernel, so nothing is uploaded
+        row.clear();
+        for (int64_t i = 0; i < m; i++)
+            for (int64_t j = 0; j < lens[i]; j += LONG_ITEM) row.push_back(rows[i]);
+        const int64_t ni = (int64_t)row.size();
+        d_row.alloc(std::max<int64_t>(1, ni));
+        d_j0.alloc(std::max<int64_t>(1, ni));
+        if (ni) {
+            DBuf<int32_t> cnt_i, pre;
+            cnt_i.alloc(m + 1);
+            pre.alloc(m + 1);
+            k_item_counts<<<blocks_for(m + 1, 256), 256, 0, st>>>(len.p, m, cnt_i.p);
+            note_launch();
+            cub_run([&](void *t, size_t &b) {
+                return cub::DeviceScan::ExclusiveSum(t, b, cnt_i.p, pre.p, (int)(m + 1), st);
+            });
+            k_item_fill<<<blocks_for(m, 128), 128, 0, st>>>(d.p, len.p, pre.p, m, d_row.p,
+                                                            d_j0.p);
+            note_launch();
+            KB_CUDA(cudaGetLastError());
+            KB_CUDA(cudaStreamSynchronize(st));
+        }
     }
 };
 
-__global__ void __launch_bounds__(SEG_ROWS) k_tri_match(const int64_t *indptr,
-                                                        const int32_t *rlen,
-                                                        const int32_t *indices, int64_t n,
-                                                        const int64_t *hi_off,
-                                                        const int64_t *lo_cnt,
-                                                        const int64_t *hi_cnt,
-                                                        const uint32_t *skey,
-                                                        const int32_t *sval,
-                                                        unsigned long long *bad) {
-    bool b = false;
-    seg_rows(n, UpperPart{lo_cnt, hi_cnt, rlen}, [&](int64_t v, int64_t f, int j) {
-        const int64_t o = hi_off[v] + j;
-        b |= skey[o] != (uint32_t)v || sval[o] != indices[indptr[v] + f + j];
-    });
-    if (b) atomicOr(bad, 1ull);
-}
-
-__global__ void k_tri_match_long(const int32_t *rows, const int64_t *indptr,
-                                 const int32_t *rlen, const int32_t *indices,
-                                 const int64_t *hi_off, const int64_t *hi_cnt,
-                                 const uint32_t *skey, const int32_t *sval,
-                                 unsigned long long *bad) {
-    const int64_t v = rows[blockIdx.x];
-    const int64_t c = hi_cnt[v], f = rlen[v] - c;
-    bool b = false;
-    for (int64_t j = threadIdx.x; j < c; j += blockDim.x) {
-        const int64_t o = hi_off[v] + j;
-        b |= skey[o] != (uint32_t)v || sval[o] != indices[indptr[v] + f + j];
-    }
-    if (b) atomicOr(bad, 1ull);
-}
-
-struct LongOf {
-    const int64_t *cnt;
-    __device__ bool operator()(int32_t r) const { return cnt[r] > SEG_LONG; }
-};
-}  // namespace
-
-// Graph.is_symmetric (graph.py:168-175): the arc set equals its reversal.
-// Self-loops are their own reversal; every arc u->v with u < v must be
-// matched by v->u.  The upper-triangle keys u*2^s+v come out of the
-// canonical CSR already sorted, so the set is symmetric iff the sorted
-// reversed lower-triangle keys match them one for one (half the arcs sorted).
-int graph_is_symmetric(Graph &g) {
-    cudaStream_t st = g.stream;
-    const int64_t n = g.n, m = g.nnz;
-    if (m == 0) return 1;
-    int shift = 1;
-    while (((int64_t)1 << shift) < n) shift++;
-    DBuf<int64_t> lo_cnt, hi_cnt, lo_off, hi_off;
-    lo_cnt.alloc(n + 1); hi_cnt.alloc(n + 1); lo_off.alloc(n + 1); hi_off.alloc(n + 1);
-    k_tri_counts<<<blocks_for(n + 1, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p, n,
-                                                        lo_cnt.p, hi_cnt.p);
+// one pass (arc ops or bucket verification) over rows [a, b)
+void rows_pass(const RowOps &A, bool verify, int64_t a, int64_t b, const LongItems &li,
+               cudaStream_t st) {
+    if (b <= a) return;
+    if (verify) k_verify_tile<<<blocks_for(b - a, TILE_ROWS), TILE_ROWS, 0, st>>>(A, a, b);
+    else k_rows_tile<<<blocks_for(b - a, TILE_ROWS), TILE_ROWS, 0, st>>>(A, a, b);
     note_launch();
-    cub_run([&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, lo_cnt.p, lo_off.p, (int)(n + 1), st);
-    });
-    cub_run([&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, hi_cnt.p, hi_off.p, (int)(n + 1), st);
-    });
-    int64_t tot[2];
-    KB_CUDA(cudaMemcpyAsync(&tot[0], lo_off.p + n, 8, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaMemcpyAsync(&tot[1], hi_off.p + n, 8, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    if (tot[0] != tot[1]) return 0;
-    const int64_t h = tot[0];
-    if (h == 0) return 1;
-    // (v, u) pairs of the lower triangle in row order, stably sorted by v
-    // alone (the u's of each v stay ascending): 32-bit keys, 4 passes at
-    // most instead of a 64-bit (v, u) key sort
-    DBuf<uint32_t> key, skey;
-    DBuf<int32_t> val, sval, longs;
-    DBuf<int64_t> nlong;
-    key.alloc(h); skey.alloc(h); val.alloc(h); sval.alloc(h); longs.alloc(n); nlong.alloc(2);
-    k_tri_pairs<<<blocks_for(n, SEG_ROWS), SEG_ROWS, 0, st>>>(g.indptr.p, g.indices.p, n,
-                                                             lo_off.p, lo_cnt.p, key.p, val.p);
-    note_launch();
-    cub::CountingInputIterator<int32_t> it(0);
-    cub_run([&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, it, longs.p, nlong.p, (int)n, LongOf{lo_cnt.p}, st);
-    });
-    int64_t nl = 0;
-    KB_CUDA(cudaMemcpyAsync(&nl, nlong.p, 8, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    if (nl) {
-        k_tri_pairs_long<<<(unsigned)nl, 256, 0, st>>>(longs.p, g.indptr.p, g.indices.p,
-                                                        lo_off.p, lo_cnt.p, key.p, val.p);
-        note_launch();
-    }
-    cub_run([&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, key.p, skey.p, val.p, sval.p, h, 0, shift,
-                                               st);
-    });
-    DBuf<unsigned long long> bad;
-    bad.alloc(1);
-    KB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), st));
-    k_tri_match<<<blocks_for(n, SEG_ROWS), SEG_ROWS, 0, st>>>(
-        g.indptr.p, g.rlen.p, g.indices.p, n, hi_off.p, lo_cnt.p, hi_cnt.p, skey.p, sval.p,
-        bad.p);
-    note_launch();
-    cub_run([&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, it, longs.p, nlong.p + 1, (int)n, LongOf{hi_cnt.p},
-                                     st);
-    });
-    KB_CUDA(cudaMemcpyAsync(&nl, nlong.p + 1, 8, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    if (nl) {
-        k_tri_match_long<<<(unsigned)nl, 256, 0, st>>>(longs.p, g.indptr.p, g.rlen.p,
-                                                        g.indices.p, hi_off.p, hi_cnt.p, skey.p,
-                                                        sval.p, bad.p);
+    const auto &R = li.row;
+    const int64_t la = std::lower_bound(R.begin(), R.end(), (int32_t)a) - R.begin();
+    const int64_t lb = std::lower_bound(R.begin(), R.end(),
+                                        (int32_t)std::min<int64_t>(b, INT32_MAX)) - R.begin();
+    if (lb > la) {
+        if (verify) k_verify_long<<<(unsigned)(lb - la), 256, 0, st>>>(A, li.d_row.p + la,
+                                                                        li.d_j0.p + la);
+        else k_rows_long<<<(unsigned)(lb - la), 256, 0, st>>>(A, li.d_row.p + la,
+                                                              li.d_j0.p + la);
         note_launch();
     }
     KB_CUDA(cudaGetLastError());
-    unsigned long long hb = 0;
-    KB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+}
+
+cudaStream_t copy_stream() {
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    KB_CUDA(cudaGetDevice(&dev));
+    if (!streams[dev]) KB_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    return streams[dev];
+}
+
+}  // namespace
+
+// Graph.is_symmetric (graph.py:168-175): the arc set equals its reversal.
+// Every lower arc u -> v (v < u) is dropped into v's bucket (k_rows_tile,
+// OP_SCATTER); then each bucket must equal v's upper part (k_verify_*).
+// Works on the CSR-with-slack as it stands (row starts + lengths).
+int graph_is_symmetric(Graph &g) {
+    cudaStream_t st = g.stream;
+    const int64_t n = g.n;
+    if (n == 0 || g.indices.n == 0) return 1;
+    DBuf<unsigned int> fill;
+    DBuf<int32_t> bkt;
+    DBuf<unsigned long long> flags;
+    fill.alloc(n);
+    bkt.alloc(g.indices.n);
+    flags.alloc(1);
+    KB_CUDA(cudaMemsetAsync(fill.p, 0, n * sizeof(unsigned int), st));
+    KB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(unsigned long long), st));
+    LongItems li;
+    li.build(g.rlen.p, n, st);
+    RowOps A{};
+    A.ip = g.indptr.p;
+    A.rl = g.rlen.p;
+    A.ix = g.indices.p;
+    A.n = n;
+    A.ops = OP_SCATTER;
+    A.flags = flags.p;
+    A.fill = fill.p;
+    A.bkt = bkt.p;
+    rows_pass(A, false, 0, n, li, st);
+    rows_pass(A, true, 0, n, li, st);
+    unsigned long long hf = 0;
+    KB_CUDA(cudaMemcpyAsync(&hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    return hb == 0;
+    return (hf & F_ASYM) ? 0 : 1;
+}
+
+// Ingest of a host CSR, pipelined with its upload.  indptr goes first; the
+// relabelling, the SELL plan and the slack layout need only the row lengths
+// and are computed while the columns stream in.  The columns arrive in
+// chunks of whole rows, highest rows first, on a copy stream; as each chunk
+// lands, one pass validates it (ids in range, rows strictly ascending),
+// copies it into the slack layout, writes its SELL slots and drops its lower
+// arcs into the symmetry buckets, and a second pass verifies the buckets of
+// its rows -- complete, because every row above it has arrived.  The upload
+// is the bound (2.2 GB at C2); the graph and its symmetry flag are ready
+// one chunk after the last byte lands.
+void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
+    cudaStream_t st = g.stream;
+    cudaStream_t cs = copy_stream();
+    const int64_t n = g.n, nnz = g.nnz;
+    g.indptr.alloc(n + 1);
+    DBuf<int32_t> stage;  // the compact columns as uploaded
+    stage.alloc(nnz);
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, h_indices) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    // chunks of whole rows, ~chunk_arcs arcs each, processed from the top
+    // rows down; the last ones (the bottom rows, processed after the final
+    // byte lands) shrink geometrically so little work trails the upload
+    const int64_t C = std::max<int64_t>(1, tune_get("ingest.chunk_arcs", (int64_t)1 << 25));
+    std::vector<int64_t> rb{n};   // descending row boundaries
+    while (rb.back() > 0) {
+        const int64_t hi = rb.back(), arcs_left = h_indptr[hi];
+        const int64_t size = arcs_left > 2 * C ? C : std::max<int64_t>(C / 16, arcs_left / 2);
+        int64_t r = std::lower_bound(h_indptr, h_indptr + hi + 1, arcs_left - size) - h_indptr;
+        r = std::max<int64_t>(0, std::min<int64_t>(r, hi - 1));
+        rb.push_back(r);
+    }
+    std::reverse(rb.begin(), rb.end());   // ascending: chunk c = [rb[c], rb[c+1])
+    const int nch = (int)rb.size() - 1;
+    const bool trace = getenv("KB_TRACE") != nullptr;
+    std::vector<cudaEvent_t> ev(nch + 2), tev(trace ? nch : 0);
+    cudaEvent_t tev0 = nullptr;
+    for (auto &e : ev)
+        KB_CUDA(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+    for (auto &e : tev) KB_CUDA(cudaEventCreate(&e));
+    if (trace) KB_CUDA(cudaEventCreate(&tev0));
+    auto cleanup = [&] {
+        cudaStreamSynchronize(cs);
+        for (auto &e : ev) cudaEventDestroy(e);
+        for (auto &e : tev) cudaEventDestroy(e);
+        if (tev0) cudaEventDestroy(tev0);
+    };
+    auto copy_chunk = [&](int c) {
+        const int64_t a = h_indptr[rb[c]], b = h_indptr[rb[c + 1]];
+        if (b > a)
+            KB_CUDA(cudaMemcpyAsync(stage.p + a, h_indices + a, (b - a) * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, cs));
+        KB_CUDA(cudaEventRecord(ev[c], cs));
+    };
+    try {
+        // the buffers may be recycled blocks still in use by queued work
+        KB_CUDA(cudaEventRecord(ev[nch], st));
+        KB_CUDA(cudaStreamWaitEvent(cs, ev[nch], 0));
+        if (trace) KB_CUDA(cudaEventRecord(tev0, cs));
+        KB_CUDA(cudaMemcpyAsync(g.indptr.p, h_indptr, (n + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, cs));
+        KB_CUDA(cudaEventRecord(ev[nch + 1], cs));
+        if (pinned)
+            for (int c = nch - 1; c >= 0; c--) copy_chunk(c);
+        KB_CUDA(cudaStreamWaitEvent(st, ev[nch + 1], 0));
+
+        const auto h0 = std::chrono::steady_clock::now();
+        auto mark = [&](const char *what) {
+            if (!trace) return;
+            KB_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr, "[ingest]   %s at %.2f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+        };
+        build_rows(g);
+        mark("rows");
+        build_sell(g, g.relabel, false);
+        mark("sell plan");
+        DBuf<int64_t> nip;
+        DBuf<int32_t> nix, bkt;
+        int64_t total = 0;
+        slack_layout(g, nullptr, nip, nix, total);
+        mark("slack layout");
+        DBuf<unsigned int> fill;
+        DBuf<unsigned long long> flags;
+        fill.alloc(n);
+        bkt.alloc(nnz);
+        flags.alloc(1);
+        KB_CUDA(cudaMemsetAsync(fill.p, 0, std::max<int64_t>(1, n) * sizeof(unsigned int), st));
+        KB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(unsigned long long), st));
+        LongItems li;
+        li.build(g.rlen.p, n, st);
+
+        if (trace) {
+            KB_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr, "[ingest] plan (rows, SELL plan, slack layout, long items): %.2f ms host\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+        }
+        RowOps A{};
+        A.ip = g.indptr.p;
+        A.rl = g.rlen.p;
+        A.ix = stage.p;
+        A.n = n;
+        // shard graphs (no relabelling) keep their rows in original-id order
+        // over exchange ids: ranges are checked, order and symmetry are not
+        A.ops = OP_VALIDATE | OP_COPY | OP_FILL | (g.relabel ? OP_SCATTER | OP_ORDER : 0);
+        A.flags = flags.p;
+        A.fill = fill.p;
+        A.bkt = bkt.p;
+        A.nip = nip.p;
+        A.nix = nix.p;
+        A.iperm = g.iperm.p;
+        A.vr_of_row = g.vr_of_row.p;
+        A.h_of_row = g.h_of_row.p;
+        A.seg_ptr = g.seg_ptr.p;
+        A.seg_list = g.seg_list.p;
+        A.slice_w = g.sell.slice_w.p;
+        A.slice_off = g.sell.slice_off.p;
+        A.cols = g.sell.cols.p;
+        A.split = g.split;
+        for (int c = nch - 1; c >= 0; c--) {
+            if (!pinned) copy_chunk(c);
+            KB_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
+            rows_pass(A, false, rb[c], rb[c + 1], li, st);
+            if (A.ops & OP_SCATTER) rows_pass(A, true, rb[c], rb[c + 1], li, st);
+            if (trace) KB_CUDA(cudaEventRecord(tev[c], st));
+        }
+        unsigned long long hf = 0;
+        KB_CUDA(cudaMemcpyAsync(&hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        KB_REQUIRE(!(hf & F_INVALID), KB_EPARAM,
+                   "indices: every row must be strictly ascending with ids in [0, n)");
+        g.symmetric = !(A.ops & OP_SCATTER) ? -1 : (hf & F_ASYM) ? 0 : 1;
+        if (trace) {
+            float t0 = 0, t1 = 0;
+            for (int c = nch - 1; c >= 0; c--) {
+                KB_CUDA(cudaEventElapsedTime(&t0, tev0, ev[c]));
+                KB_CUDA(cudaEventElapsedTime(&t1, tev0, tev[c]));
+                fprintf(stderr, "[ingest] chunk %d rows [%lld, %lld): copied %.2f ms, done %.2f ms\n",
+                        c, (long long)rb[c], (long long)rb[c + 1], t0, t1);
+            }
+        }
+        g.indptr = std::move(nip);
+        g.indices = std::move(nix);
+        g.tail = total;
+        g.slack = true;
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
 }
 
 }  // namespace kb

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -38,6 +41,24 @@ int64_t tune_get(const char *name, int64_t dflt);
 // number of kernel launches issued by the library (bench.py gpu_launches)
 void note_launch(int64_t k = 1);
 int64_t launch_count();
+
+// KB_TRACE=1: host-side phase times (syncing the stream at each mark)
+struct PhaseTrace {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    cudaStream_t st;
+    explicit PhaseTrace(cudaStream_t s) : on(getenv("KB_TRACE") != nullptr), st(s) {
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[kb] %-28s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 // ---------------------------------------------------------------- device buf
 // All device work of a process runs on one non-blocking stream per device.
@@ -244,8 +265,10 @@ void gather_to_original(const Graph &g, const double *src_new, double *dst_orig,
                         cudaStream_t st);
 void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices);
 void build_graph_device(Graph &g);
-void build_sell(Graph &g, bool fresh);
+void build_sell(Graph &g, bool fresh, bool fill = true);
 void make_slack(Graph &g);
+void slack_layout(Graph &g, const int32_t *extra, DBuf<int64_t> &nip, DBuf<int32_t> &nix,
+                  int64_t &total);
 void compact_csr(Graph &g, DBuf<int64_t> &indptr, DBuf<int32_t> &indices);
 void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne);
 void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
