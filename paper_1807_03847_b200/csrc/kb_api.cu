@@ -67,6 +67,18 @@ cudaStream_t device_stream() {
     return streams[dev];
 }
 
+// A second non-blocking stream per device for bulk host<->device copies that
+// overlap the device stream's kernels (pipelined ingest, result download).
+cudaStream_t copy_stream() {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!streams[dev]) KB_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    return streams[dev];
+}
+
 namespace {
 struct BigCache {
     std::multimap<size_t, void *> idle;      // size -> block

@@ -956,14 +956,6 @@ void rows_pass(const RowOps &A, bool verify, int64_t a, int64_t b, const LongIte
     KB_CUDA(cudaGetLastError());
 }
 
-cudaStream_t copy_stream() {
-    static cudaStream_t streams[64] = {};
-    int dev = 0;
-    KB_CUDA(cudaGetDevice(&dev));
-    if (!streams[dev]) KB_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-    return streams[dev];
-}
-
 }  // namespace
 
 // Graph.is_symmetric (graph.py:168-175): the arc set equals its reversal.

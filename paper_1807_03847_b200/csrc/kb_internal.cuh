@@ -71,6 +71,7 @@ struct PhaseTrace {
 // against 3-15 ms for cudaMalloc; cached blocks are reused in stream order
 // (one stream per device), so reuse needs no synchronisation.
 cudaStream_t device_stream();
+cudaStream_t copy_stream();
 constexpr size_t BIG_ALLOC = (size_t)64 << 20;
 void *dev_alloc(size_t bytes);
 void dev_free(void *p, size_t bytes);

@@ -211,19 +211,61 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
     if (h_pairs) *h_pairs = (int64_t)pairs;
 }
 
+static bool host_pinned(const void *p) {
+    cudaPointerAttributes a{};
+    const bool ok = p && cudaPointerGetAttributes(&a, p) == cudaSuccess &&
+                    a.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    return ok;
+}
+
+// ranking_result to host arrays.  With page-locked destinations the bound
+// vectors are gathered first and downloaded on the copy stream while the
+// order is sorted on the device stream.
 void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, double *h_upper,
                 int64_t *h_pairs) {
     const int64_t n = s.g->n;
     DBuf<int64_t> o;
     DBuf<double> lo, up;
-    result_device(s, st, h_order ? &o : nullptr, h_lower ? &lo : nullptr,
-                  h_upper ? &up : nullptr, h_pairs);
-    if (h_order) KB_CUDA(cudaMemcpyAsync(h_order, o.p, n * 8, cudaMemcpyDeviceToHost, st));
-    if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, st));
-    if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
+    const bool early = (h_lower || h_upper) && (!h_lower || host_pinned(h_lower)) &&
+                       (!h_upper || host_pinned(h_upper));
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev = nullptr;
+    if (early) {
+        cs = copy_stream();
+        if (h_lower) {
+            lo.alloc(n);
+            gather_to_original(*s.g, s.lower.p, lo.p, st);
+        }
+        if (h_upper) {
+            up.alloc(n);
+            gather_to_original(*s.g, s.upper.p, up.p, st);
+        }
+        KB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        KB_CUDA(cudaEventRecord(ev, st));
+        KB_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, cs));
+        if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, cs));
+    }
+    try {
+        result_device(s, st, h_order ? &o : nullptr, (h_lower && !early) ? &lo : nullptr,
+                      (h_upper && !early) ? &up : nullptr, h_pairs);
+        if (h_order) KB_CUDA(cudaMemcpyAsync(h_order, o.p, n * 8, cudaMemcpyDeviceToHost, st));
+        if (!early) {
+            if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, st));
+            if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, st));
+        }
+        KB_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        if (cs) cudaStreamSynchronize(cs);
+        if (ev) cudaEventDestroy(ev);
+        throw;
+    }
+    if (cs) {
+        KB_CUDA(cudaStreamSynchronize(cs));
+        KB_CUDA(cudaEventDestroy(ev));
+    }
 }
-
 
 namespace {
 __global__ void k_iota32(int64_t n, int32_t *a) {
