@@ -240,8 +240,8 @@ __global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dp
                               const int32_t *del, const int64_t *iptr, const int32_t *ins,
                               const int64_t *toff, int32_t *tmp, const int64_t *indptr,
                               int32_t *indices, int32_t *rlen) {
-    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int64_t e = blockIdx.x;  // a block per edited row (hub rows are long)
+    const int t = threadIdx.x, nt = blockDim.x;
     if (e >= ne) return;
     const int32_t v = rows[e];
     const int32_t *row = indices + indptr[v];
@@ -251,21 +251,20 @@ __global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dp
     const int32_t *I = ins + iptr[e];
     const int64_t ni = iptr[e + 1] - iptr[e];
     int32_t *out = tmp + toff[e];
-    for (int64_t j = lane; j < L; j += 32) {
+    for (int64_t j = t; j < L; j += nt) {
         const int32_t c = row[j];
         const int64_t dl = lower_bound32(D, nd, c);
         if (dl < nd && D[dl] == c) continue;  // deleted
         out[j - dl + lower_bound32(I, ni, c)] = c;
     }
-    for (int64_t q = lane; q < ni; q += 32) {
-        const int32_t t = I[q];
-        out[lower_bound32(row, L, t) - lower_bound32(D, nd, t) + q] = t;
+    for (int64_t q = t; q < ni; q += nt) {
+        const int32_t x = I[q];
+        out[lower_bound32(row, L, x) - lower_bound32(D, nd, x) + q] = x;
     }
-    __syncwarp();
+    __syncthreads();
     const int64_t nl = L - nd + ni;
-    for (int64_t j = lane; j < nl; j += 32) indices[indptr[v] + j] = out[j];
-    __syncwarp();
-    if (lane == 0) rlen[v] = (int32_t)nl;
+    for (int64_t j = t; j < nl; j += nt) indices[indptr[v] + j] = out[j];
+    if (t == 0) rlen[v] = (int32_t)nl;
 }
 
 __global__ void k_scatter_extra(const int32_t *rows, const int32_t *x, int64_t ne, int32_t *dst) {
@@ -451,8 +450,10 @@ __global__ void k_bounds_rows(const int32_t *rows, int64_t m, const double *katz
 }
 
 // u joins the affected set when any of its out-neighbours changed
+// rows (original id o) with a changed out-neighbour join the affected set;
+// chg_bits marks the changed rows by original id (2 MB at C2: L2-resident)
 __global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const int32_t *indices,
-                              const int32_t *iperm, int64_t n, const unsigned char *chg,
+                              const int32_t *iperm, int64_t n, const unsigned int *chg_bits,
                               unsigned int *aff_words, unsigned long long *affcount) {
     int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (o >= n) return;
@@ -462,7 +463,8 @@ __global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const 
     const int32_t *row = indices + indptr[o];
     const int32_t L = rlen[o];
     for (int32_t j = 0; j < L; j++) {
-        if (chg[iperm[row[j]]]) {
+        const int32_t c = __ldg(row + j);
+        if ((__ldg(chg_bits + (c >> 5)) >> (c & 31)) & 1u) {
             if (!(atomicOr(&aff_words[u >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
             return;
         }
@@ -471,10 +473,15 @@ __global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const 
 
 __global__ void k_diff_changed(const double *old, const double *nw, int64_t n, int32_t *changed,
                                unsigned long long *count) {
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    if (__double_as_longlong(old[v]) != __double_as_longlong(nw[v]))
-        changed[atomicAdd(count, 1ull)] = (int32_t)v;
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool c = v < n && __double_as_longlong(old[v]) != __double_as_longlong(nw[v]);
+    const unsigned m = __ballot_sync(0xffffffffu, c);   // one atomic per warp
+    if (!m) return;
+    const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+    unsigned long long b = 0;
+    if (lane == lead) b = atomicAdd(count, (unsigned long long)__popc(m));
+    b = __shfl_sync(0xffffffffu, b, lead);
+    if (c) changed[b + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
 }
 
 __global__ void k_map_new(const int32_t *orig, int64_t m, const int32_t *iperm, int32_t *out) {
@@ -485,6 +492,16 @@ __global__ void k_map_new(const int32_t *orig, int64_t m, const int32_t *iperm, 
 __global__ void k_flags_from_list(const int32_t *list, int64_t m, unsigned char *flag) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < m) flag[list[i]] = 1;
+}
+
+// bitmap by original id of a list of new ids
+__global__ void k_bits_from_list(const int32_t *list, int64_t m, const int32_t *perm,
+                                 unsigned int *bits) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) {
+        const int32_t o = perm[list[i]];
+        atomicOr(bits + (o >> 5), 1u << (o & 31));
+    }
 }
 
 __global__ void k_min_lower(const int32_t *act, int64_t m, const double *lower,
@@ -658,7 +675,20 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
                      (uint32_t)ins[2 * i + 1]);
     if (ed.empty()) return;
     PhaseTrace tr(st);
-    std::sort(ed.begin(), ed.end());
+    if (ed.size() < 4096) {
+        std::sort(ed.begin(), ed.end());
+    } else {  // large batches: radix sort on the device
+        const int64_t m = (int64_t)ed.size();
+        DBuf<uint64_t> a, b;
+        a.alloc(m);
+        b.alloc(m);
+        KB_CUDA(cudaMemcpyAsync(a.p, ed.data(), m * 8, cudaMemcpyHostToDevice, st));
+        cub_run([&](void *t, size_t &bb) {
+            return cub::DeviceRadixSort::SortKeys(t, bb, a.p, b.p, (int)m, 0, 64, st);
+        });
+        KB_CUDA(cudaMemcpyAsync(ed.data(), b.p, m * 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    }
     std::vector<int32_t> rows, dl, il;
     std::vector<int64_t> dptr{0}, iptr{0};
     for (size_t i = 0; i < ed.size();) {
@@ -740,7 +770,7 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
     dtoff.alloc(ne + 1);
     tmp.alloc(std::max<int64_t>(1, toff[ne]));
     KB_CUDA(cudaMemcpyAsync(dtoff.p, toff.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
-    k_apply_edits<<<nblk(ne * 32, 256), 256, 0, st>>>(drows.p, ne, ddptr.p, ddel.p, diptr.p,
+    k_apply_edits<<<(unsigned)ne, 128, 0, st>>>(drows.p, ne, ddptr.p, ddel.p, diptr.p,
                                                        dins.p, dtoff.p, tmp.p, g.indptr.p,
                                                        g.indices.p, g.rlen.p);
     note_launch();
@@ -838,8 +868,8 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     int64_t affected = ns;
     bool aborted = false;
     bool all_touched = false;
-    DBuf<unsigned char> chg;
-    chg.alloc(n);
+    DBuf<unsigned int> chg_bits;
+    chg_bits.alloc((n + 31) / 32 + 1);
     int64_t nchanged = 0;
     for (int64_t level = 1; level <= s.r; level++) {
         double *w_prev = s.levels[level - 1 - s.level_base].p;
@@ -874,10 +904,12 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             // find the changed rows by comparison.  The affected set grows by
             // the in-neighbours of the previous changed rows, found by a pull
             // over every row's out-arcs (u in N-(v) <=> v in N+(u)).
-            KB_CUDA(cudaMemsetAsync(chg.p, 0, n, st));
-            k_flags_from_list<<<nblk(nchanged, 256), 256, 0, st>>>(C.p, nchanged, chg.p);
+            KB_CUDA(cudaMemsetAsync(chg_bits.p, 0, chg_bits.bytes(), st));
+            k_bits_from_list<<<nblk(nchanged, 256), 256, 0, st>>>(C.p, nchanged, g.perm.p,
+                                                                  chg_bits.p);
             k_pull_affect<<<nblk(n, 256), 256, 0, st>>>(g.indptr.p, g.rlen.p, g.indices.p,
-                                                        g.iperm.p, n, chg.p, aff.p, cnt.p + 2);
+                                                        g.iperm.p, n, chg_bits.p, aff.p,
+                                                        cnt.p + 2);
             note_launch(2);
             DBuf<double> fresh;
             fresh.alloc(n + 1);
