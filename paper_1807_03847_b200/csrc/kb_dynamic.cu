@@ -380,7 +380,9 @@ __global__ void k_work_sum(const int32_t *changed, int64_t nc, const int64_t *in
 __global__ void k_recompute(const int32_t *R, int64_t nr, const int32_t *perm,
                             const int32_t *iperm, const int64_t *indptr, const int32_t *rlen,
                             const int32_t *indices, const double *x, double *w, double alpha,
-                            int64_t split, int32_t *changed, unsigned long long *nchanged) {
+                            int64_t split, int32_t *changed, unsigned long long *nchanged,
+                            const int32_t *h_of_row, const int32_t *ovf_flag,
+                            int32_t *heavy_out, unsigned long long *nheavy) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= nr) return;
@@ -388,6 +390,11 @@ __global__ void k_recompute(const int32_t *R, int64_t nr, const int32_t *perm,
     const int32_t o = perm[v];
     const int32_t *row = indices + indptr[o];
     const int64_t L = rlen[o];
+    if (heavy_out && L > split && h_of_row[v] >= 0 && !(ovf_flag && ovf_flag[v])) {
+        // a heavy row with current SELL segments: k_heavy_rows_fold
+        if (lane == 0) heavy_out[atomicAdd(nheavy, 1ull)] = v;
+        return;
+    }
     double s = 0.0;
     if (L <= split) {
         // lanes gather 32 consecutive slots; lane 0 folds them in order
@@ -420,6 +427,79 @@ __global__ void k_recompute(const int32_t *R, int64_t nr, const int32_t *perm,
         const double nw = __dmul_rn(alpha, s);
         const double old = w[v];
         if (__double_as_longlong(nw) != __double_as_longlong(old)) {
+            changed[atomicAdd(nchanged, 1ull)] = v;
+            w[v] = nw;
+        }
+    }
+}
+
+// Heavy rows of a sparse level, recomputed from their SELL segments with
+// K1's own folds (each lane one segment, ascending slots, gathers issued 16
+// ahead) and k_heavy_combine's segment order, so the bits are K1's.  A block
+// per row: a hub's ~200 segments fold in parallel instead of one warp
+// walking them.
+__global__ void __launch_bounds__(256) k_heavy_rows_fold(
+    const int32_t *rows, const double *x, double *w, double alpha, const int32_t *h_of_row,
+    const int32_t *seg_ptr, const int32_t *seg_list, const int64_t *slice_off,
+    const int32_t *slice_w, const int32_t *vlen, const int32_t *cols, int32_t *changed,
+    unsigned long long *nchanged) {
+    __shared__ double part[256];
+    const int32_t v = rows[blockIdx.x];
+    const int32_t h = h_of_row[v];
+    const int q0 = seg_ptr[h], nq = seg_ptr[h + 1] - q0;
+    double s = 0.0;  // thread 0's running row sum
+    for (int b = 0; b < nq; b += blockDim.x) {
+        const int q = b + threadIdx.x;
+        double ss = 0.0;
+        if (q < nq) {
+            const int32_t vr = seg_list[q0 + q];
+            const int64_t sl = vr >> 5;
+            const int ln = vr & 31;
+            const int len = vlen[vr];
+            const int32_t *p = cols + slice_off[sl] + ln * 4;
+            (void)slice_w;
+            // batches of 32 slots: the next batch's column groups are loaded
+            // before this batch's gathers are folded
+            int4 cn[8];
+#pragma unroll
+            for (int g4 = 0; g4 < 8; g4++)
+                cn[g4] = (g4 * 4 < len) ? *(const int4 *)(p + (int64_t)g4 * 128)
+                                        : make_int4(0, 0, 0, 0);
+            for (int j0 = 0; j0 < len; j0 += 32) {
+                int4 c[8];
+#pragma unroll
+                for (int g4 = 0; g4 < 8; g4++) c[g4] = cn[g4];
+#pragma unroll
+                for (int g4 = 0; g4 < 8; g4++) {
+                    const int j = j0 + 32 + g4 * 4;
+                    cn[g4] = (j < len) ? *(const int4 *)(p + (int64_t)(j >> 2) * 128)
+                                       : make_int4(0, 0, 0, 0);
+                }
+                double t[32];
+#pragma unroll
+                for (int g4 = 0; g4 < 8; g4++) {
+                    const int j = j0 + g4 * 4;
+                    t[g4 * 4 + 0] = j + 0 < len ? x[c[g4].x] : 0.0;
+                    t[g4 * 4 + 1] = j + 1 < len ? x[c[g4].y] : 0.0;
+                    t[g4 * 4 + 2] = j + 2 < len ? x[c[g4].z] : 0.0;
+                    t[g4 * 4 + 3] = j + 3 < len ? x[c[g4].w] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 32; u++)
+                    if (j0 + u < len) ss = __dadd_rn(ss, t[u]);
+            }
+        }
+        part[threadIdx.x] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int cnt = min((int)blockDim.x, nq - b);
+            for (int u = 0; u < cnt; u++) s = __dadd_rn(s, part[u]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double nw = __dmul_rn(alpha, s);
+        if (__double_as_longlong(nw) != __double_as_longlong(w[v])) {
             changed[atomicAdd(nchanged, 1ull)] = v;
             w[v] = nw;
         }
@@ -469,19 +549,6 @@ __global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const 
             return;
         }
     }
-}
-
-__global__ void k_diff_changed(const double *old, const double *nw, int64_t n, int32_t *changed,
-                               unsigned long long *count) {
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool c = v < n && __double_as_longlong(old[v]) != __double_as_longlong(nw[v]);
-    const unsigned m = __ballot_sync(0xffffffffu, c);   // one atomic per warp
-    if (!m) return;
-    const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
-    unsigned long long b = 0;
-    if (lane == lead) b = atomicAdd(count, (unsigned long long)__popc(m));
-    b = __shfl_sync(0xffffffffu, b, lead);
-    if (c) changed[b + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
 }
 
 __global__ void k_map_new(const int32_t *orig, int64_t m, const int32_t *iperm, int32_t *out) {
@@ -784,6 +851,45 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
     g.version += 1;
 }
 
+namespace {
+struct BitsDiffer {
+    const double *a, *b;
+    __device__ bool operator()(int32_t v) const {
+        return __double_as_longlong(a[v]) != __double_as_longlong(b[v]);
+    }
+};
+}  // namespace
+
+// rows whose value differs bit-wise, ascending, and their count (a device
+// select: one decoupled-lookback pass instead of an atomic per warp)
+static void diff_changed(const double *old, const double *nw, int64_t n, int32_t *changed,
+                         unsigned long long *count, cudaStream_t st) {
+    DBuf<int64_t> c64;
+    c64.alloc(1);
+    cub::CountingInputIterator<int32_t> it(0);
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, it, changed, c64.p, (int)n, BitsDiffer{old, nw}, st);
+    });
+    KB_CUDA(cudaMemcpyAsync(count, c64.p, 8, cudaMemcpyDeviceToDevice, st));
+}
+
+// ascending node ids (>= 0): two 16-bit LSD counting passes (batches of
+// 1e5 edges carry 2e5 ids; std::sort took ~5 ms per list here)
+static void sort_ids(std::vector<int32_t> &a) {
+    if (a.size() < 2048) {
+        std::sort(a.begin(), a.end());
+        return;
+    }
+    std::vector<int32_t> b(a.size());
+    for (int sh = 0; sh < 32; sh += 16) {
+        std::vector<size_t> cnt(65537, 0);
+        for (int32_t x : a) cnt[(((uint32_t)x >> sh) & 0xffffu) + 1]++;
+        for (size_t d = 1; d < cnt.size(); d++) cnt[d] += cnt[d - 1];
+        for (int32_t x : a) b[cnt[((uint32_t)x >> sh) & 0xffffu]++] = x;
+        a.swap(b);
+    }
+}
+
 void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                   int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats) {
     Graph &g = *s.g;
@@ -802,9 +908,9 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     std::vector<int32_t> seeds_o, targets_o;
     for (int64_t i = 0; i < n_ins; i++) { seeds_o.push_back((int32_t)ins[2 * i]); targets_o.push_back((int32_t)ins[2 * i + 1]); }
     for (int64_t i = 0; i < n_dels; i++) { seeds_o.push_back((int32_t)dels[2 * i]); targets_o.push_back((int32_t)dels[2 * i + 1]); }
-    std::sort(seeds_o.begin(), seeds_o.end());
+    sort_ids(seeds_o);
     seeds_o.erase(std::unique(seeds_o.begin(), seeds_o.end()), seeds_o.end());
-    std::sort(targets_o.begin(), targets_o.end());
+    sort_ids(targets_o);
     targets_o.erase(std::unique(targets_o.begin(), targets_o.end()), targets_o.end());
     st_out.seeds = (int64_t)seeds_o.size();
     // seeds and targets as new ids (mapped on the device)
@@ -847,11 +953,11 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     }
 
     // 2. level repair
-    DBuf<int32_t> stamp, R, C, dseeds;
+    DBuf<int32_t> stamp, R, C, dseeds, HR;
     DBuf<unsigned int> aff;
     DBuf<unsigned char> touched;
     DBuf<unsigned long long> cnt;  // [0]=|R|, [1]=|changed|, [2]=|affected|
-    stamp.alloc(n); R.alloc(n); C.alloc(n); aff.alloc((n + 31) / 32 + 1); touched.alloc(n);
+    stamp.alloc(n); R.alloc(n); C.alloc(n); HR.alloc(std::max<int64_t>(1, g.nh)); aff.alloc((n + 31) / 32 + 1); touched.alloc(n);
     cnt.alloc(4);
     dseeds.alloc(std::max<size_t>(1, seeds.size()));
     KB_CUDA(cudaMemsetAsync(stamp.p, 0xff, n * 4, st));
@@ -914,9 +1020,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             DBuf<double> fresh;
             fresh.alloc(n + 1);
             run_spmv(s, st, w_prev, fresh.p, true);
-            KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
-            k_diff_changed<<<nblk(n, 256), 256, 0, st>>>(w_cur, fresh.p, n, C.p, cnt.p + 1);
-            note_launch();
+            diff_changed(w_cur, fresh.p, n, C.p, cnt.p + 1, st);
             std::swap(s.levels[level - s.level_base], fresh);
             unsigned long long hc[3];
             KB_CUDA(cudaMemcpyAsync(hc, cnt.p, 3 * 8, cudaMemcpyDeviceToHost, st));
@@ -951,9 +1055,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             DBuf<double> fresh;
             fresh.alloc(n + 1);
             run_spmv(s, st, w_prev, fresh.p, true);
-            KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
-            k_diff_changed<<<nblk(n, 256), 256, 0, st>>>(w_cur, fresh.p, n, C.p, cnt.p + 1);
-            note_launch();
+            diff_changed(w_cur, fresh.p, n, C.p, cnt.p + 1, st);
             std::swap(s.levels[level - s.level_base], fresh);
             unsigned long long hchg = 0;
             KB_CUDA(cudaMemcpyAsync(&hchg, cnt.p + 1, 8, cudaMemcpyDeviceToHost, st));
@@ -966,10 +1068,26 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         // recompute R at this level; the changed list feeds the next level
         KB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
         if (nr) {
+            // heavy rows fold their SELL segments (only while the layout is current)
+            const bool seg_ok = !g.sell_dirty && g.nh > 0 && g.sell.nseg > 0;
+            KB_CUDA(cudaMemsetAsync(cnt.p + 3, 0, 8, st));
             k_recompute<<<nblk(nr * 32, 256), 256, 0, st>>>(
                 R.p, nr, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p, w_prev, w_cur,
-                s.alpha, g.split, C.p, cnt.p + 1);
+                s.alpha, g.split, C.p, cnt.p + 1, g.h_of_row.p, g.ovf_flag.p,
+                seg_ok ? HR.p : nullptr, cnt.p + 3);
             note_launch();
+            if (seg_ok) {
+                unsigned long long hh = 0;
+                KB_CUDA(cudaMemcpyAsync(&hh, cnt.p + 3, 8, cudaMemcpyDeviceToHost, st));
+                KB_CUDA(cudaStreamSynchronize(st));
+                if (hh) {
+                    k_heavy_rows_fold<<<(unsigned)hh, 256, 0, st>>>(
+                        HR.p, w_prev, w_cur, s.alpha, g.h_of_row.p, g.seg_ptr.p, g.seg_list.p,
+                        g.sell.slice_off.p, g.sell.slice_w.p, g.sell.vlen.p, g.sell.cols.p, C.p,
+                        cnt.p + 1);
+                    note_launch();
+                }
+            }
         }
         unsigned long long hchg = 0;
         KB_CUDA(cudaMemcpyAsync(&hchg, cnt.p + 1, 8, cudaMemcpyDeviceToHost, st));

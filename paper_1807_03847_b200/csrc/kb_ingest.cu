@@ -185,8 +185,11 @@ __global__ void k_patch_rows(const int32_t *rows_orig, int64_t ne, const int32_t
                              const int32_t *seg_ptr, const int32_t *seg_list,
                              const int32_t *slice_w, const int64_t *slice_off, int32_t *vlen,
                              int32_t *cols, int32_t *ovf_flag, int32_t *ovf,
-                             unsigned long long *ovf_count) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                             unsigned long long *ovf_count, int64_t split, int32_t *heavy,
+                             unsigned long long *heavy_count) {
+    // a warp per edited row: the lanes rewrite a fitting row's slots
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (e >= ne) return;
     const int32_t o = rows_orig[e];
     const int32_t v = iperm[o];
@@ -195,25 +198,67 @@ __global__ void k_patch_rows(const int32_t *rows_orig, int64_t ne, const int32_t
     const int32_t vr = vr_of_row[v];
     if (vr >= 0) {
         const int64_t s = vr >> 5;
-        const int lane = vr & 31;
+        const int sl = vr & 31;
         const int w = slice_w[s];
         if (len <= w) {
             int32_t *base = cols + slice_off[s];
             const int32_t *row = indices + indptr[o];
-            for (int j = 0; j < len; j++) {
-                const int64_t pos = (w <= 4) ? ((int64_t)j * 32 + lane)
-                                             : ((int64_t)(j >> 2) * 128 + lane * 4 + (j & 3));
+            for (int j = lane; j < len; j += 32) {
+                const int64_t pos = (w <= 4) ? ((int64_t)j * 32 + sl)
+                                             : ((int64_t)(j >> 2) * 128 + sl * 4 + (j & 3));
                 base[pos] = iperm[row[j]];
             }
-            vlen[vr] = len;
+            if (lane == 0) vlen[vr] = len;
             return;
         }
-        vlen[vr] = 0;
+        if (lane == 0) vlen[vr] = 0;
     } else if (h_of_row[v] >= 0) {
+        // a heavy row keeps its segments while the count of full ones is
+        // unchanged and the remainder fits the partial segment's lane (or
+        // is 0): k_patch_heavy rewrites them in place
         const int32_t h = h_of_row[v];
-        for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++) vlen[seg_list[q]] = 0;
+        const int q0 = seg_ptr[h], nq = seg_ptr[h + 1] - q0;
+        const int32_t last = seg_list[q0 + nq - 1];
+        const int F = vlen[last] < split ? nq - 1 : nq;
+        const int64_t rem = (int64_t)len - (int64_t)F * split;
+        bool fits = false;
+        if (rem >= 0 && rem < split)
+            fits = (nq == F + 1) ? rem <= slice_w[last >> 5] : rem == 0;
+        if (fits) {
+            if (lane == 0) heavy[atomicAdd(heavy_count, 1ull)] = v;
+            return;
+        }
+        for (int q = q0 + lane; q < q0 + nq; q += 32) vlen[seg_list[q]] = 0;
     }
-    if (atomicExch(&ovf_flag[v], 1) == 0) ovf[atomicAdd(ovf_count, 1ull)] = v;
+    if (lane == 0 && atomicExch(&ovf_flag[v], 1) == 0) ovf[atomicAdd(ovf_count, 1ull)] = v;
+}
+
+// rewrite the SELL segments of an edited heavy row (new id rows[blockIdx.x])
+__global__ void k_patch_heavy(const int32_t *rows, const int32_t *perm, const int64_t *indptr,
+                              const int32_t *rlen, const int32_t *indices, const int32_t *iperm,
+                              const int32_t *h_of_row, const int32_t *seg_ptr,
+                              const int32_t *seg_list, const int32_t *slice_w,
+                              const int64_t *slice_off, int64_t split, int32_t *vlen,
+                              int32_t *cols) {
+    const int32_t v = rows[blockIdx.x];
+    const int32_t o = perm[v];
+    const int32_t h = h_of_row[v];
+    const int q0 = seg_ptr[h], nq = seg_ptr[h + 1] - q0;
+    const int32_t *row = indices + indptr[o];
+    const int64_t L = rlen[o];
+    for (int64_t j = threadIdx.x; j < L; j += blockDim.x) {
+        const int64_t q = j / split, jj = j - q * split;
+        const int32_t vr = seg_list[q0 + q];
+        const int64_t s = vr >> 5;
+        const int ln = vr & 31;
+        const int w = slice_w[s];
+        const int64_t pos = (w <= 4) ? jj * 32 + ln : (jj >> 2) * 128 + ln * 4 + (jj & 3);
+        cols[slice_off[s] + pos] = iperm[row[j]];
+    }
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        const int64_t a = (int64_t)q * split;
+        vlen[seg_list[q0 + q]] = (int32_t)(L > a ? min(split, L - a) : 0);
+    }
 }
 
 __global__ void k_arc_flags(const int32_t *rlen, int64_t n, unsigned char *fl, int32_t *iota) {
@@ -530,16 +575,29 @@ void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne) {
         KB_CUDA(cudaMemsetAsync(g.ovf_count.p, 0, 8, st));
     }
     Sell &S = g.sell;
-    k_patch_rows<<<blocks_for(ne, 128), 128, 0, st>>>(
+    DBuf<int32_t> hv;                 // edited heavy rows patched in place
+    DBuf<unsigned long long> hc;
+    hv.alloc(std::max<int64_t>(1, std::min<int64_t>(ne, g.nh)));
+    hc.alloc(1);
+    KB_CUDA(cudaMemsetAsync(hc.p, 0, 8, st));
+    k_patch_rows<<<blocks_for(ne * 32, 256), 256, 0, st>>>(
         rows_orig, ne, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p, g.vr_of_row.p,
         g.h_of_row.p, g.seg_ptr.p, g.seg_list.p, S.slice_w.p, S.slice_off.p, S.vlen.p, S.cols.p,
-        g.ovf_flag.p, g.ovf.p, g.ovf_count.p);
+        g.ovf_flag.p, g.ovf.p, g.ovf_count.p, g.split, hv.p, hc.p);
     note_launch();
     KB_CUDA(cudaGetLastError());
-    unsigned long long h = 0;
-    KB_CUDA(cudaMemcpyAsync(&h, g.ovf_count.p, 8, cudaMemcpyDeviceToHost, st));
+    unsigned long long h[2] = {0, 0};
+    KB_CUDA(cudaMemcpyAsync(&h[0], g.ovf_count.p, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaMemcpyAsync(&h[1], hc.p, 8, cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    g.n_ovf = (int64_t)h;
+    g.n_ovf = (int64_t)h[0];
+    if (h[1]) {
+        k_patch_heavy<<<(unsigned)h[1], 256, 0, st>>>(
+            hv.p, g.perm.p, g.indptr.p, g.rlen.p, g.indices.p, g.iperm.p, g.h_of_row.p,
+            g.seg_ptr.p, g.seg_list.p, S.slice_w.p, S.slice_off.p, g.split, S.vlen.p, S.cols.p);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
     // the overflow pass is a warp per row: past a few percent of the rows a
     // rebuild of the layout is cheaper
     if (g.n_ovf > std::max<int64_t>(4096, g.nv / 32)) g.sell_dirty = true;
