@@ -311,12 +311,18 @@ def run_dynamic(a, device):
         t_dyn = time.perf_counter() - t0
         _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms)))
         top_dyn = P.ranking_result(st).top(a.k)
-        _lib.check(L.kb_timer(device, 0, None))
-        t0 = time.perf_counter()
-        fres = P.run(P.init(g, crit, undirected=True, device=device, max_iterations=200), g)
-        t_static = time.perf_counter() - t0
-        ms2 = P.engine.ctypes.c_double()
-        _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms2)))
+        # static recompute on the post-batch graph, best of two (the first
+        # can include one-off allocations)
+        t_static, ms2 = None, P.engine.ctypes.c_double()
+        for _rep in range(2):
+            _lib.check(L.kb_timer(device, 0, None))
+            t0 = time.perf_counter()
+            fres = P.run(P.init(g, crit, undirected=True, device=device, max_iterations=200), g)
+            t1 = time.perf_counter() - t0
+            m = P.engine.ctypes.c_double()
+            _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(m)))
+            if t_static is None or t1 < t_static:
+                t_static, ms2 = t1, m
         s = st.last_update_stats
         np.add.at(deg, arcs[:, 0], 1)
         rows.append({"batch_edges": int(pk.shape[0]), "update_s": t_dyn,

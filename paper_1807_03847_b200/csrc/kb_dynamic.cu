@@ -506,6 +506,35 @@ __global__ void __launch_bounds__(256) k_heavy_rows_fold(
     }
 }
 
+// heavy row rows[i] = its segment sums combined in order (warp per row)
+__global__ void k_heavy_finish(const int32_t *rows, int64_t m, double *w, double alpha,
+                               const int32_t *h_of_row, const int32_t *seg_ptr,
+                               const int32_t *seg_list, const double *seg_sum,
+                               int32_t *changed, unsigned long long *nchanged) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= m) return;
+    const int32_t v = rows[i];
+    const int32_t h = h_of_row[v];
+    const int q0 = seg_ptr[h], q1 = seg_ptr[h + 1];
+    double s = 0.0;
+    for (int b = q0; b < q1; b += 32) {
+        const double val = (b + lane < q1) ? seg_sum[seg_list[b + lane]] : 0.0;
+        const int cnt = min(32, q1 - b);
+        for (int q = 0; q < cnt; q++) {
+            const double t = __shfl_sync(0xffffffffu, val, q);
+            if (lane == 0) s = __dadd_rn(s, t);
+        }
+    }
+    if (lane == 0) {
+        const double nw = __dmul_rn(alpha, s);
+        if (__double_as_longlong(nw) != __double_as_longlong(w[v])) {
+            changed[atomicAdd(nchanged, 1ull)] = v;
+            w[v] = nw;
+        }
+    }
+}
+
 // katz[v] = ((0 + w_1) + w_2) + ... + w_r, the static accumulation order
 __global__ void k_katz_rows(const int32_t *rows, int64_t m, const double *const *levels, int r,
                             double *katz) {
@@ -1080,7 +1109,15 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
                 unsigned long long hh = 0;
                 KB_CUDA(cudaMemcpyAsync(&hh, cnt.p + 3, 8, cudaMemcpyDeviceToHost, st));
                 KB_CUDA(cudaStreamSynchronize(st));
-                if (hh) {
+                if ((int64_t)hh > tune_get("dyn.heavy_dense", 256)) {
+                    // many heavy rows: all segment sums by K1 (~45% of a
+                    // level), then each listed row combined and compared
+                    run_segments(s, st, w_prev);
+                    k_heavy_finish<<<nblk((int64_t)hh * 32, 256), 256, 0, st>>>(
+                        HR.p, (int64_t)hh, w_cur, s.alpha, g.h_of_row.p, g.seg_ptr.p,
+                        g.seg_list.p, s.seg_sum.p, C.p, cnt.p + 1);
+                    note_launch();
+                } else if (hh) {
                     k_heavy_rows_fold<<<(unsigned)hh, 256, 0, st>>>(
                         HR.p, w_prev, w_cur, s.alpha, g.h_of_row.p, g.seg_ptr.p, g.seg_list.p,
                         g.sell.slice_off.p, g.sell.slice_w.p, g.sell.vlen.p, g.sell.cols.p, C.p,

@@ -251,6 +251,7 @@ void text_csr(TextScan &t, int64_t n, int undirected, const int64_t *h_extra, in
 void launch_iterate(State &s, cudaStream_t st);
 void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only);
 void collect_k1_times(State &s);
+void run_segments(State &s, cudaStream_t st, const double *x);
 bool run_check(State &s, cudaStream_t st);      // returns converged
 // TOPK check split around its one host read: enqueue (kernels, publish the
 // verdict to abort_flag, D2H into h_flags, record chk_ev) / finish (after

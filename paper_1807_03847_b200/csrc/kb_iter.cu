@@ -63,6 +63,7 @@ struct IterArgs {
     double alpha, gamma;
     int undirected;
     int level_only;                 // write w only (dynamic level repair)
+    int seg_only;                   // heavy-row segment sums only (no row epilogue)
     const int32_t *hrow, *vrow;     // explicit row maps (nullptr: implicit)
     int hot;
     // sharded graphs: the hot set is the head of every rank's block of the
@@ -190,7 +191,7 @@ __device__ __forceinline__ void narrow_group(const IterArgs &A, int64_t s0, int 
         const int64_t vq = (s0 + q) * 32 + lane;
         if (s0 + q < A.nslices && vq < A.nvr) {
             if (vq < A.nseg) A.seg_sum[vq] = sum;
-            else epilogue_k(A, row[q], sum, kz[q]);
+            else if (!A.seg_only) epilogue_k(A, row[q], sum, kz[q]);
         }
     }
 }
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         }
         if (vr < A.nvr) {
             if (vr < A.nseg) A.seg_sum[vr] = sum;
-            else epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), sum);
+            else if (!A.seg_only) epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), sum);
         }
     }
 }
@@ -441,6 +442,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     A.gamma = s.gamma;
     A.undirected = s.undirected;
     A.level_only = level_only;
+    A.seg_only = 0;
     A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
     A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
     A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), n);
@@ -538,6 +540,46 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     // the gather-free first step is not a K1 launch: keep it out of the
     // K1 timing (bench roofline) but count it in the run
     if (!level_only && !ones) s.k1_used += 2;
+}
+
+// The heavy-row segment sums alone (seg_sum, K1's folds) over the slices
+// that hold segments -- the dynamic path's dense recompute of heavy rows.
+void run_segments(State &s, cudaStream_t st, const double *x) {
+    Graph &g = *s.g;
+    if (g.sell_dirty || g.sell.nseg == 0) return;
+    IterArgs A{};
+    A.cols = g.sell.cols.p;
+    A.slice_off = g.sell.slice_off.p;
+    A.slice_w = g.sell.slice_w.p;
+    A.vlen = g.sell.vlen.p;
+    A.nslices = (g.sell.nseg + 31) / 32;
+    A.nvr = g.sell.nvr;
+    A.nseg = g.sell.nseg;
+    A.nh = g.nh;
+    A.nwide = std::min<int64_t>(g.sell.nwide, A.nslices);
+    A.x = x;
+    A.seg_sum = s.seg_sum.p;
+    A.level_only = 1;
+    A.seg_only = 1;
+    A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
+    A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
+    A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), g.n);
+    A.counter = s.work_counter.p;
+    if (s.seg_sum.n < (size_t)std::max<int64_t>(1, g.sell.nseg)) {
+        s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
+        A.seg_sum = s.seg_sum.p;
+    }
+    auto kern = k_sell_iterate<1, 0>;
+    static bool attr_done[64] = {};
+    if (!attr_done[g.device]) {
+        KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr_done[g.device] = true;
+    }
+    KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
+    kern<<<g.sm_count, 1024, (size_t)A.hot * sizeof(double), st>>>(A);
+    note_launch();
+    KB_CUDA(cudaGetLastError());
 }
 
 void launch_iterate(State &s, cudaStream_t st) {

@@ -286,3 +286,44 @@ def test_rmat_s16_batches_match_static_recompute(nb):
     og = O.CSRGraph(65536, ip, ix, symmetric=True)
     ores = O.run(O.OracleState(og, O.Crit("topk", 1e-6, k=100)), og)
     assert ores.top(100) == fres.top(100)
+
+
+@pytest.mark.parametrize("heavy_dense", [0, 10**9])
+def test_heavy_row_repair_routes_bitwise(heavy_dense):
+    """Heavy rows (> split arcs) of a sparse level are re-folded from their
+    SELL segments -- per row (k_heavy_rows_fold) or all at once through K1
+    (run_segments + k_heavy_finish); both give a fresh static run's bits.
+    The batch also edits heavy rows (patched in place)."""
+    from paper_1807_03847_b200 import _lib
+    L = _lib.lib()
+    _lib.check(L.kb_tune(b"dyn.heavy_dense", heavy_dense))
+    try:
+        g0 = O.rmat_graph(65536, edge_factor=16, seed=42)
+        g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+        st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
+        P.run(st, g)
+        deg = np.diff(g0.indptr)
+        heavy = np.nonzero((deg > 2048) & (deg + 1 < deg.max()))[0]
+        assert heavy.size > 0
+        rng = np.random.default_rng(11)
+        ins = set()
+        for h in heavy[:8]:               # edit some heavy rows directly
+            while True:
+                v = int(rng.integers(0, 65536))
+                if v != h and not g.has_arc(int(h), v) and deg[v] + 1 < deg.max():
+                    ins.add((min(int(h), v), max(int(h), v)))
+                    break
+        while len(ins) < 600:
+            u, v = (int(x) for x in rng.integers(0, 65536, 2))
+            if u == v or g.has_arc(u, v) or max(deg[u], deg[v]) + 1 >= deg.max():
+                continue
+            ins.add((min(u, v), max(u, v)))
+        arcs = [a for uv in sorted(ins) for a in (uv, uv[::-1])]
+        P.update_batch(st, g, P.EdgeBatch(insertions=arcs))
+        fresh = fresh_to_depth(g, st)
+        for mine, theirs in zip(st.levels, fresh.levels):
+            np.testing.assert_array_equal(mine, theirs)
+        np.testing.assert_array_equal(st.lower, fresh.lower)
+        np.testing.assert_array_equal(st.upper, fresh.upper)
+    finally:
+        _lib.check(L.kb_tune(b"dyn.heavy_dense", 256))
