@@ -367,9 +367,11 @@ def run_sharded(a, rank, world, local):
     d = plan.max_degree
     alpha = 1.0 / (1.0 + d)
     gamma = P.tail_gamma(alpha, d)
-    shard = D.CudaShard(plan, rank, ip, ix, device=local, alpha=alpha, gamma=gamma, crit=crit,
-                        undirected=True, max_iterations=200,
-                        split_threshold=D.fast_split(world))
+    lcsr = tuple(np.ascontiguousarray(x) for x in plan.local_csr(ip, ix, rank))
+    shard_nnz = int(lcsr[0][-1])
+    shard = D.CudaShard(plan, rank, ip, ix, device=local, alpha=alpha, gamma=gamma,
+                        crit=crit, undirected=True, max_iterations=200,
+                        split_threshold=D.fast_split(world), local_csr=lcsr)
     shard.collective_device = f"cuda:{local}"
     nnz = int(ip[-1])
     del ix
@@ -398,9 +400,60 @@ def run_sharded(a, rank, world, local):
     assert r_it == res.iterations_used
     lc1 = P.engine.ctypes.c_int64()
     _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc1)))
+    k1_ms, k1_n = shard.k1_times()       # K1 launches of the last timed step
     t = torch.tensor([ms.value], device=f"cuda:{local}", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / a.steps
+
+    # roofline of this rank's K1 (its rows: n_per, its arcs)
+    nnz_r = int(shard_nnz)
+    w_off = 4 if nnz_r < 2**31 else 8
+    b_rank = 4 * nnz_r + w_off * (plan.n_per + 1) + 48 * plan.n_per
+    k1_avg = k1_ms / max(1, k1_n)
+    peak, peak_src = measured_peaks()
+    ach = b_rank / (k1_avg * 1e-3) / 1e9 if k1_avg > 0 else 0.0
+    roof = torch.tensor([ach, k1_avg], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(roof, op=dist.ReduceOp.MIN)   # the slowest rank's kernel
+
+    # e2e through the public API: this rank's host CSR shard (page-locked)
+    # -> CudaShard (upload + ingest) -> sharded run -> RankingResult on host
+    e2e = None
+    if not a.no_e2e:
+        res_out = (np.empty(n, dtype=np.int64), np.empty(n, dtype=np.float64),
+                   np.empty(n, dtype=np.float64))
+        for arr in lcsr + res_out:
+            _lib.check(L.kb_host_register(_lib.ptr(arr), arr.nbytes))
+
+        def e2e_step():
+            sh = D.CudaShard(plan, rank, None, None, device=local, alpha=alpha, gamma=gamma,
+                             crit=crit, undirected=True, max_iterations=200,
+                             split_threshold=D.fast_split(world), local_csr=lcsr)
+            sh.collective_device = f"cuda:{local}"
+            out = D.ShardedRun(sh, plan, crit, rank=rank, world=world,
+                               max_iterations=200).run(host_result=True, out=res_out)
+            sh.close()
+            return out
+
+        e2e_step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        wall = torch.tensor([(time.perf_counter() - t0) / a.e2e_steps], device=f"cuda:{local}",
+                            dtype=torch.float64)
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        hb = torch.tensor([float(lcsr[0].nbytes + lcsr[1].nbytes)], device=f"cuda:{local}",
+                          dtype=torch.float64)
+        dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(wall.item()), "unit": "s",
+               "h2d_bytes_per_step": int(hb.item()),
+               "d2h_bytes_per_step": int(world * n * 24),
+               "timing": "host wall clock, max over ranks; each rank uploads its row shard "
+                         "from page-locked memory and every rank receives the ranked result"}
+        for arr in lcsr + res_out:
+            L.kb_host_unregister(_lib.ptr(arr))
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
@@ -413,8 +466,12 @@ def run_sharded(a, rank, world, local):
                        "top10": res.top(10)},
             "gteps_per_iter": nnz * res.iterations_used / (ms_step * 1e-3) / 1e9,
             "gpu_launches": int(lc1.value - lc0.value), "clocks": clk.summary(),
-            "setup_s": t_setup, "e2e": None, "cpu_baseline": None,
-            "roofline": None}), flush=True)
+            "setup_s": t_setup, "e2e": e2e, "cpu_baseline": None,
+            "roofline": {"bound": "hbm", "achieved": float(roof[0].item()), "peak": peak,
+                         "unit": "GB/s", "frac": float(roof[0].item()) / peak, "traffic": None,
+                         "kernel": "k_sell_iterate (+k_heavy_combine), per rank, slowest rank",
+                         "bytes_per_launch": int(b_rank), "avg_launch_ms": float(roof[1].item()),
+                         "peak_source": peak_src}}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

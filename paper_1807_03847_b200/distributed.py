@@ -72,11 +72,16 @@ class ShardPlan:
         return max(0, -(-(self.n - rank) // self.P))
 
     def labels(self) -> np.ndarray:
-        """Tie-break labels by exchange id: the node id (padding: unique > n)."""
+        """Tie-break labels by exchange id: the node id (padding: unique > n).
+        Computed once per plan."""
+        cached = getattr(self, "_labels", None)
+        if cached is not None:
+            return cached
         lab = self.node_of_exch.copy()
         pad = lab < 0
         lab[pad] = self.n + np.arange(int(pad.sum()))
-        return lab.astype(np.int32)
+        self._labels = lab.astype(np.int32)
+        return self._labels
 
     def local_csr(self, indptr: np.ndarray, indices: np.ndarray, rank: int):
         """CSR over exchange ids holding only this rank's rows; each row keeps
@@ -103,12 +108,14 @@ class CudaShard:
 
     def __init__(self, plan: ShardPlan, rank: int, indptr, indices, *, device: int,
                  alpha: float, gamma: float, crit: Criterion, undirected: bool,
-                 max_iterations: int, symmetric: bool = True, split_threshold: int = 0):
+                 max_iterations: int, symmetric: bool = True, split_threshold: int = 0,
+                 local_csr=None):
         import torch
         self.torch = torch
         self.L = _lib.lib()
         self.plan, self.rank, self.device = plan, rank, device
-        ip, ix = plan.local_csr(indptr, indices, rank)
+        # local_csr: this rank's plan.local_csr(...) computed ahead (bench e2e)
+        ip, ix = local_csr if local_csr is not None else plan.local_csr(indptr, indices, rank)
         lab = plan.labels()
         lo, hi = plan.block(rank)
         flags = _lib.KB_GRAPH_NO_RELABEL | (_lib.KB_GRAPH_SYMMETRIC if symmetric else 0)
@@ -236,7 +243,7 @@ class CudaShard:
                                          _lib.ptr(order), ctypes.byref(pairs)))
         return order, int(pairs.value)
 
-    def rank_gathered(self, host: bool = True):
+    def rank_gathered(self, host: bool = True, out=None):
         """ranking_result of the gathered bounds, on the device: the state's
         lower/upper hold every block (exchange layout) and the graph labels
         map exchange ids to node ids (kb_rank_gathered).  host=False computes
@@ -246,15 +253,24 @@ class CudaShard:
         if not host:
             _lib.check(self.L.kb_rank_gathered(self.s, n, None, None, None, ctypes.byref(pairs)))
             return None, None, None, int(pairs.value)
-        order = np.empty(n, dtype=np.int64)
-        lower = np.empty(n, dtype=np.float64)
-        upper = np.empty(n, dtype=np.float64)
+        if out is not None:          # caller-provided (e.g. page-locked) arrays
+            order, lower, upper = out
+        else:
+            order = np.empty(n, dtype=np.int64)
+            lower = np.empty(n, dtype=np.float64)
+            upper = np.empty(n, dtype=np.float64)
         _lib.check(self.L.kb_rank_gathered(self.s, n, _lib.ptr(order), _lib.ptr(lower),
                                            _lib.ptr(upper), ctypes.byref(pairs)))
         return order, lower, upper, int(pairs.value)
 
     def sync(self):
         self.torch.cuda.synchronize(self.device)
+
+    def k1_times(self):
+        """(K1 device ms summed, launches) of the current state."""
+        info = _lib.StateInfo()
+        _lib.check(self.L.kb_state_info_get(self.s, ctypes.byref(info)))
+        return float(info.spmv_ms), int(info.spmv_launches)
 
 
 def fast_split(P: int) -> int:
@@ -316,14 +332,14 @@ class ShardedRun:
         self.b.commit(m_local)
         return m_total <= k and bool(ok)
 
-    def run(self, host_result: bool = True):
+    def run(self, host_result: bool = True, out=None):
         """engine.run for P ranks; every rank returns the same result.
         host_result=False leaves the ranked vectors on the device and
         returns (iterations, separated pairs) (bench timing)."""
         with self.b.stream_context():
-            return self._run(host_result)
+            return self._run(host_result, out)
 
-    def _run(self, host_result):
+    def _run(self, host_result, out=None):
         P, n_per = self.plan.P, self.plan.n_per
         self._blocks = None
         r = 0
@@ -338,14 +354,15 @@ class ShardedRun:
                 raise ConvergenceError(
                     f"stopping rule still unmet after {r} iterations "
                     f"(widest bound interval {gap:.3e})", iterations=r, gap=gap)
-        return self.result(r, host_result)
+        return self.result(r, host_result, out)
 
-    def result(self, r: int, host: bool = True):
+    def result(self, r: int, host: bool = True, out=None):
         P, n_per = self.plan.P, self.plan.n_per
         lo_t, up_t = self.b.bounds_tensors()
         _all_gather_flat(self.dist, lo_t, self.rank, P, n_per)
         _all_gather_flat(self.dist, up_t, self.rank, P, n_per)
-        order, lower, upper, pairs = self.b.rank_gathered(host)
+        order, lower, upper, pairs = (self.b.rank_gathered(host, out=out) if out is not None
+                                      else self.b.rank_gathered(host))
         if not host:
             return r, pairs
         n = self.plan.n
