@@ -656,6 +656,18 @@ bool sorted_check(State &s, cudaStream_t st, int64_t k) {
     return s.m_host <= k && s.h_flags[0] == 0;
 }
 
+// the cached pair test for a speculative run: out[0] = refutes; the queued
+// K1 of the next level runs only if it does (abort = !refutes)
+__global__ void k_pair_refutes_pub(const double *lower, const double *upper, const int32_t *perm,
+                                   int32_t q, int32_t x, double eps, unsigned long long *out,
+                                   unsigned long long *abort) {
+    const double lq = lower[q], lx = lower[x];
+    const bool above = lx > lq || (lx == lq && perm[x] < perm[q]);
+    const bool ref = above && lx <= __dsub_rn(upper[q], eps);
+    out[0] = ref ? 1ull : 0ull;
+    abort[0] = ref ? 0ull : 1ull;
+}
+
 // candidates: the NCAND block winners with the widest excess (ties: the
 // smaller label), chosen identically on the device by NCAND rounds of a
 // block-wide arg-max
@@ -813,9 +825,12 @@ __global__ void __launch_bounds__(256, 4) k_rank_refute(const double *lower, con
                 }
             }
         }
-        if (hit) {
+        // one atomic pair per warp (a refuted check on a graph with many
+        // exact ties, e.g. the grid, has a hit in almost every lane)
+        const unsigned hm = __ballot_sync(0xffffffffu, hit);
+        if (hm && (threadIdx.x & 31) == __ffs(hm) - 1) {
             atomicOr(fail, 1ull);
-            atomicCAS(pair, ~0ull, rec);
+            if (*(volatile unsigned long long *)pair == ~0ull) atomicCAS(pair, ~0ull, rec);
         }
     }
 }
@@ -968,6 +983,23 @@ double run_gap(State &s, cudaStream_t st) {
     double d;
     memcpy(&d, &b, sizeof(double));
     return g.n ? d : 0.0;
+}
+
+// RANKING with a cached refuting pair: enqueue its test, publish the abort
+// flag for a speculative K1 and start the 8-byte read into h_flags[0]
+// (complete at chk_ev).  false: no pair cached.
+bool ranking_pair_enqueue(State &s, cudaStream_t st) {
+    if (s.rk_q < 0 || !tune_get("check.pair_cache", 1)) return false;
+    Graph &g = *s.g;
+    if (!s.abort_flag.p) s.abort_flag.alloc(1);
+    if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
+    k_pair_refutes_pub<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, s.rk_q, s.rk_x, s.eps,
+                                        s.scratch_u64.p, s.abort_flag.p);
+    note_launch();
+    KB_CUDA(cudaGetLastError());
+    KB_CUDA(cudaMemcpyAsync(s.h_flags, s.scratch_u64.p, 8, cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaEventRecord(s.chk_ev, st));
+    return true;
 }
 
 bool run_check(State &s, cudaStream_t st) {

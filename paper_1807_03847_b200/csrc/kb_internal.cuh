@@ -258,6 +258,7 @@ bool run_check(State &s, cudaStream_t st);      // returns converged
 // chk_ev: adopt the new active set, return converged); -1: not applicable
 int topk_check_enqueue(State &s, cudaStream_t st);
 bool topk_check_finish(State &s, int nxt);
+bool ranking_pair_enqueue(State &s, cudaStream_t st);
 double run_gap(State &s, cudaStream_t st);
 void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
                    DBuf<double> *upper, int64_t *h_pairs);
