@@ -1078,6 +1078,15 @@ int kb_run(kb_state *h, int *converged) {
                                tune_get("run.speculate", 1);
         if (spec_rank) {
             check_version(s);
+            s.lazy_bounds = tune_get("k1.lazy_bounds", 1) != 0;
+            struct Restore {   // bounds are materialized however the loop ends
+                State &s;
+                cudaStream_t st;
+                ~Restore() {
+                    s.lazy_bounds = false;
+                    try { materialize_bounds(s, st); } catch (...) {}
+                }
+            } restore{s, st};
             launch_iterate(s, st);
             for (;;) {
                 if (ranking_pair_enqueue(s, st)) {
@@ -1090,6 +1099,7 @@ int kb_run(kb_state *h, int *converged) {
                     KB_CUDA(cudaEventSynchronize(s.chk_ev));
                     if (s.h_flags[0]) {              // still refuted: not converged
                         if (ahead) continue;         // the queued K1 was the next level
+                        materialize_bounds(s, st);
                         const double gap = run_gap(s, st);
                         char buf[160];
                         snprintf(buf, sizeof buf,
@@ -1104,6 +1114,7 @@ int kb_run(kb_state *h, int *converged) {
                     }
                     s.rk_q = s.rk_x = -1;
                 }
+                materialize_bounds(s, st);
                 if (run_check(s, st)) { *converged = 1; break; }
                 if (s.r >= s.max_iter) {
                     const double gap = run_gap(s, st);

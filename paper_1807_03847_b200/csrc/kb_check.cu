@@ -658,12 +658,17 @@ bool sorted_check(State &s, cudaStream_t st, int64_t k) {
 
 // the cached pair test for a speculative run: out[0] = refutes; the queued
 // K1 of the next level runs only if it does (abort = !refutes)
-__global__ void k_pair_refutes_pub(const double *lower, const double *upper, const int32_t *perm,
-                                   int32_t q, int32_t x, double eps, unsigned long long *out,
+__global__ void k_pair_refutes_pub(const double *katz, const double *w, double alpha, double gamma,
+                                   int undirected, const int32_t *perm, int32_t q, int32_t x,
+                                   double eps, unsigned long long *out,
                                    unsigned long long *abort) {
-    const double lq = lower[q], lx = lower[x];
+    // the two nodes' bounds from katz and the level, as the K1 epilogue forms them
+    const double tq = __dmul_rn(alpha, w[q]), tx = __dmul_rn(alpha, w[x]);
+    const double lq = undirected ? __dadd_rn(katz[q], tq) : katz[q];
+    const double lx = undirected ? __dadd_rn(katz[x], tx) : katz[x];
+    const double uq = __dadd_rn(katz[q], __dmul_rn(tq, gamma));
     const bool above = lx > lq || (lx == lq && perm[x] < perm[q]);
-    const bool ref = above && lx <= __dsub_rn(upper[q], eps);
+    const bool ref = above && lx <= __dsub_rn(uq, eps);
     out[0] = ref ? 1ull : 0ull;
     abort[0] = ref ? 0ull : 1ull;
 }
@@ -993,8 +998,9 @@ bool ranking_pair_enqueue(State &s, cudaStream_t st) {
     Graph &g = *s.g;
     if (!s.abort_flag.p) s.abort_flag.alloc(1);
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
-    k_pair_refutes_pub<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, s.rk_q, s.rk_x, s.eps,
-                                        s.scratch_u64.p, s.abort_flag.p);
+    k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma, s.undirected,
+                                        g.perm.p, s.rk_q, s.rk_x, s.eps, s.scratch_u64.p,
+                                        s.abort_flag.p);
     note_launch();
     KB_CUDA(cudaGetLastError());
     KB_CUDA(cudaMemcpyAsync(s.h_flags, s.scratch_u64.p, 8, cudaMemcpyDeviceToHost, st));

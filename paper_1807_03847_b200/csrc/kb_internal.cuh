@@ -225,6 +225,10 @@ struct State {
     // and exits at once if that check converged (abort_flag, set on device)
     DBuf<unsigned long long> abort_flag;
     bool spec_abort = false;
+    // RANKING runs skip the per-iteration lower/upper stores (K1 writes w and
+    // katz only); materialize_bounds recomputes them, bit for bit, before
+    // anything reads them
+    bool lazy_bounds = false, bounds_stale = false;
     cudaEvent_t chk_ev = nullptr;
     const double *x_level() const { return levels.back().p; }
 };
@@ -251,6 +255,7 @@ void text_csr(TextScan &t, int64_t n, int undirected, const int64_t *h_extra, in
 void launch_iterate(State &s, cudaStream_t st);
 void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only);
 void collect_k1_times(State &s);
+void materialize_bounds(State &s, cudaStream_t st);
 void run_segments(State &s, cudaStream_t st, const double *x);
 bool run_check(State &s, cudaStream_t st);      // returns converged
 // TOPK check split around its one host read: enqueue (kernels, publish the

@@ -64,6 +64,7 @@ struct IterArgs {
     int undirected;
     int level_only;                 // write w only (dynamic level repair)
     int seg_only;                   // heavy-row segment sums only (no row epilogue)
+    int lazy_bounds;                // leave lower/upper to materialize_bounds
     const int32_t *hrow, *vrow;     // explicit row maps (nullptr: implicit)
     int hot;
     // sharded graphs: the hot set is the head of every rank's block of the
@@ -112,6 +113,7 @@ __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s)
     const double t = __dmul_rn(A.alpha, w);          // :309
     A.katz[v] = k;
     A.w[v] = w;                                      // :317
+    if (A.lazy_bounds) return;
     st_stream(A.lower + v, A.undirected ? __dadd_rn(k, t) : k);  // :313/:315
     st_stream(A.upper + v, __dadd_rn(k, __dmul_rn(t, A.gamma)));  // :316
 }
@@ -139,6 +141,7 @@ __device__ __forceinline__ void epilogue_k(const IterArgs &A, int64_t v, double 
     const double t = __dmul_rn(A.alpha, w);
     A.katz[v] = k;
     A.w[v] = w;
+    if (A.lazy_bounds) return;
     st_stream(A.lower + v, A.undirected ? __dadd_rn(k, t) : k);
     st_stream(A.upper + v, __dadd_rn(k, __dmul_rn(t, A.gamma)));
 }
@@ -457,6 +460,8 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     }
     A.counter = s.work_counter.p;
     A.abort = s.spec_abort ? s.abort_flag.p : nullptr;
+    A.lazy_bounds = (s.lazy_bounds && !level_only) ? 1 : 0;
+    if (A.lazy_bounds) s.bounds_stale = true;
     if (s.seg_sum.n < (size_t)std::max<int64_t>(1, g.sell.nseg)) {
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
         A.seg_sum = s.seg_sum.p;
@@ -561,6 +566,7 @@ void run_segments(State &s, cudaStream_t st, const double *x) {
     A.seg_sum = s.seg_sum.p;
     A.level_only = 1;
     A.seg_only = 1;
+    A.lazy_bounds = 0;
     A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
     A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
     A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), g.n);
@@ -580,6 +586,30 @@ void run_segments(State &s, cudaStream_t st, const double *x) {
     kern<<<g.sm_count, 1024, (size_t)A.hot * sizeof(double), st>>>(A);
     note_launch();
     KB_CUDA(cudaGetLastError());
+}
+
+// lower/upper of every row from katz and the last level, with the epilogue's
+// exact operations (engine.py:309-316): the bits K1 would have stored
+__global__ void k_bounds_from(const double *katz, const double *w, int64_t n, double alpha,
+                              double gamma, int undirected, double *lower, double *upper) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const double k = katz[v];
+    const double t = __dmul_rn(alpha, w[v]);
+    lower[v] = undirected ? __dadd_rn(k, t) : k;
+    upper[v] = __dadd_rn(k, __dmul_rn(t, gamma));
+}
+
+void materialize_bounds(State &s, cudaStream_t st) {
+    if (!s.bounds_stale) return;
+    const int64_t n = s.g->n;
+    if (n) {
+        k_bounds_from<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            s.katz.p, s.x_level(), n, s.alpha, s.gamma, s.undirected, s.lower.p, s.upper.p);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    s.bounds_stale = false;
 }
 
 void launch_iterate(State &s, cudaStream_t st) {
