@@ -102,7 +102,10 @@ int kb_host_unregister(void *ptr);
 
 /* ---- graph ingest: replaces Graph.out_csr() + the scipy CSR the engine
  * reads (graph.py:177-197) with a device-resident, degree-relabelled SELL-32
- * layout.  indptr: n+1 int64, indices: nnz int32, each row sorted ascending.
+ * layout.  indptr: n+1 int64, indices: nnz int32, each row strictly
+ * ascending with ids in [0, n) (checked: KB_EPARAM otherwise).  The columns
+ * are uploaded in row chunks and laid out while later chunks are in flight;
+ * the symmetry flag (kb_graph_is_symmetric) is decided in the same pass.
  * split_threshold <= 0 and hot_size < 0 select the defaults. */
 int kb_graph_create(int device, int64_t n, int64_t nnz, const int64_t *indptr,
                     const int32_t *indices, int64_t split_threshold,
