@@ -373,9 +373,13 @@ def run_sharded(a, rank, world, local):
     gamma = P.tail_gamma(alpha, d)
     lcsr = tuple(np.ascontiguousarray(x) for x in plan.local_csr(ip, ix, rank))
     shard_nnz = int(lcsr[0][-1])
-    shard = D.CudaShard(plan, rank, ip, ix, device=local, alpha=alpha, gamma=gamma,
-                        crit=crit, undirected=True, max_iterations=200,
-                        split_threshold=D.fast_split(world), local_csr=lcsr)
+    fused = os.environ.get("KB_FUSED_EXCHANGE", "1") == "1"
+
+    def make_shard(fz):
+        return D.CudaShard(plan, rank, None, None, device=local, alpha=alpha, gamma=gamma,
+                           crit=crit, undirected=True, max_iterations=200,
+                           split_threshold=D.fast_split(world), local_csr=lcsr, fused=fz)
+    shard, exch_mode = D.connect_shard(make_shard, dist, rank, world, f"cuda:{local}", fused)
     shard.collective_device = f"cuda:{local}"
     nnz = int(ip[-1])
     del ix
@@ -429,9 +433,8 @@ def run_sharded(a, rank, world, local):
             _lib.check(L.kb_host_register(_lib.ptr(arr), arr.nbytes))
 
         def e2e_step():
-            sh = D.CudaShard(plan, rank, None, None, device=local, alpha=alpha, gamma=gamma,
-                             crit=crit, undirected=True, max_iterations=200,
-                             split_threshold=D.fast_split(world), local_csr=lcsr)
+            sh, _ = D.connect_shard(make_shard, dist, rank, world, f"cuda:{local}",
+                                    exch_mode.startswith("fused"))
             sh.collective_device = f"cuda:{local}"
             out = D.ShardedRun(sh, plan, crit, rank=rank, world=world,
                                max_iterations=200).run(host_result=True, out=res_out)
@@ -466,7 +469,7 @@ def run_sharded(a, rank, world, local):
             "data": "synthetic",
             "config": {"workload": workload_name(a), "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
                        "seed": a.seed, "iterations": res.iterations_used,
-                       "parallelism": f"row-shard{world} + NCCL omega all-gather",
+                       "parallelism": f"row-shard{world}, omega exchange: {exch_mode}",
                        "top10": res.top(10)},
             "gteps_per_iter": nnz * res.iterations_used / (ms_step * 1e-3) / 1e9,
             "gpu_launches": int(lc1.value - lc0.value), "clocks": clk.summary(),

@@ -210,6 +210,21 @@ int kb_select_global(int device, const uint64_t *keys, const int64_t *labels,
 /* keep the winners of the global cut and the survivors
  * fl(upper - eps) >= threshold (engine.py:367-373); returns |active| */
 int kb_check_apply_cut(kb_state *s, uint64_t kstar, int64_t istar, int64_t *active);
+/* Fused omega exchange (B200-native replacement of the per-iteration
+ * all-gather).  A shard graph owns two full-length level
+ * buffers (parity 0/1, cudaMalloc'd); each rank registers the other ranks'
+ * buffers of each parity -- by CUDA IPC handle across processes or by device
+ * pointer within one -- and K1's epilogue stores every owned row's w into
+ * all of them over NVLink while it computes, followed by a system-scope
+ * fence.  The caller's per-check collectives order the ranks' iterations.
+ * A state using it keeps two levels (keep_levels = 0). */
+int kb_graph_exchange_alloc(kb_graph *g);
+int kb_graph_exchange_ptr(kb_graph *g, int parity, void **ptr);
+/* 64-byte cudaIpcMemHandle_t of this rank's buffer */
+int kb_graph_exchange_handle(kb_graph *g, int parity, void *handle);
+/* a peer's buffer of `parity`: IPC handle (opened here) or a device pointer */
+int kb_graph_exchange_add_peer(kb_graph *g, int parity, const void *handle, void *ptr);
+int kb_state_exchange(kb_state *s, int on);
 /* ranking_result + separated pairs on caller vectors indexed by node id */
 int kb_rank_bounds(int device, int64_t n, const double *lower, const double *upper,
                    int64_t *order, int64_t *separated_pairs);

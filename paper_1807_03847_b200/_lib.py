@@ -120,6 +120,11 @@ SIGNATURES = {
     "kb_shard_cut": (i32, [vp, vp, i64, i64, vp]),
     "kb_shard_commit": (i32, [vp, i64]),
     "kb_rank_gathered": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
+    "kb_graph_exchange_alloc": (i32, [vp]),
+    "kb_graph_exchange_ptr": (i32, [vp, i32, ctypes.POINTER(vp)]),
+    "kb_graph_exchange_handle": (i32, [vp, i32, vp]),
+    "kb_graph_exchange_add_peer": (i32, [vp, i32, vp, vp]),
+    "kb_state_exchange": (i32, [vp, i32]),
     "kb_update_batch": (i32, [vp, vp, i64, vp, i64, dbl, dbl,
                               ctypes.POINTER(UpdateStatsC)]),
 }

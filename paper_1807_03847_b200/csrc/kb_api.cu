@@ -855,6 +855,76 @@ int kb_graph_apply_batch(kb_graph *h, const int64_t *ins, int64_t n_ins, const i
     });
 }
 
+// ---- fused omega exchange for shards (replaces the per-iteration NCCL
+// all-gather of SURVEY.md 8(e) with K1-epilogue stores over NVLink)
+int kb_graph_exchange_alloc(kb_graph *h) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL graph");
+        Graph &g = h->g;
+        use_device(g.device);
+        if (g.exch[0]) return;
+        g.exch_n = (size_t)g.n + 1;
+        for (int p = 0; p < 2; p++) {
+            KB_CUDA(cudaMalloc(&g.exch[p], g.exch_n * sizeof(double)));
+            KB_CUDA(cudaMemsetAsync(g.exch[p], 0, g.exch_n * sizeof(double), g.stream));
+        }
+        KB_CUDA(cudaStreamSynchronize(g.stream));
+    });
+}
+
+int kb_graph_exchange_ptr(kb_graph *h, int parity, void **ptr) {
+    return guarded([&] {
+        KB_REQUIRE(h && ptr && (parity == 0 || parity == 1), KB_EPARAM, "bad argument");
+        KB_REQUIRE(h->g.exch[parity], KB_ESTATE, "exchange buffers not allocated");
+        *ptr = h->g.exch[parity];
+    });
+}
+
+int kb_graph_exchange_handle(kb_graph *h, int parity, void *handle) {
+    return guarded([&] {
+        KB_REQUIRE(h && handle && (parity == 0 || parity == 1), KB_EPARAM, "bad argument");
+        KB_REQUIRE(h->g.exch[parity], KB_ESTATE, "exchange buffers not allocated");
+        use_device(h->g.device);
+        cudaIpcMemHandle_t m;
+        KB_CUDA(cudaIpcGetMemHandle(&m, h->g.exch[parity]));
+        memcpy(handle, &m, sizeof(m));
+    });
+}
+
+int kb_graph_exchange_add_peer(kb_graph *h, int parity, const void *handle, void *ptr) {
+    return guarded([&] {
+        KB_REQUIRE(h && (parity == 0 || parity == 1) && (handle || ptr), KB_EPARAM,
+                   "bad argument");
+        Graph &g = h->g;
+        KB_REQUIRE((int)g.exch_peer[parity].size() < KB_MAX_PEERS, KB_EPARAM,
+                   "too many exchange peers");
+        use_device(g.device);
+        double *p = (double *)ptr;
+        if (handle) {
+            cudaIpcMemHandle_t m;
+            memcpy(&m, handle, sizeof(m));
+            void *q = nullptr;
+            KB_CUDA(cudaIpcOpenMemHandle(&q, m, cudaIpcMemLazyEnablePeerAccess));
+            g.exch_opened.push_back(q);
+            p = (double *)q;
+        }
+        g.exch_peer[parity].push_back(p);
+    });
+}
+
+int kb_state_exchange(kb_state *h, int on) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL state");
+        State &s = h->s;
+        if (on) {
+            KB_REQUIRE(s.g->exch[0], KB_ESTATE, "exchange buffers not allocated");
+            KB_REQUIRE(!s.keep_all, KB_ESTATE, "the exchange keeps two levels: keep_levels=0");
+            KB_REQUIRE(s.r == 0, KB_ESTATE, "enable the exchange before the first iteration");
+        }
+        s.exch_on = on != 0;
+    });
+}
+
 int kb_graph_destroy(kb_graph *h) {
     return guarded([&] {
         if (!h) return;

@@ -81,12 +81,19 @@ template <typename T>
 struct DBuf {
     T *p = nullptr;
     size_t n = 0;
+    bool owned = true;  // false: a view of memory owned elsewhere (borrow)
     DBuf() = default;
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
-    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), owned(o.owned) {
+        o.p = nullptr; o.n = 0; o.owned = true;
+    }
     DBuf &operator=(DBuf &&o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; owned = o.owned;
+            o.p = nullptr; o.n = 0; o.owned = true;
+        }
         return *this;
     }
     ~DBuf() { release(); }
@@ -96,10 +103,17 @@ struct DBuf {
         p = (T *)dev_alloc(count * sizeof(T));
         n = count;
     }
+    void borrow(T *q, size_t count) {
+        release();
+        p = q;
+        n = count;
+        owned = false;
+    }
     void release() {
-        if (p) dev_free(p, n * sizeof(T));
+        if (p && owned) dev_free(p, n * sizeof(T));
         p = nullptr;
         n = 0;
+        owned = true;
     }
     size_t bytes() const { return n * sizeof(T); }
 };
@@ -174,10 +188,29 @@ struct Graph {
     DBuf<int32_t> orig_pos, orig_zero;
     DBuf<int32_t> seg_ptr;
     DBuf<int32_t> seg_list;
+    // fused omega exchange (shards): two full-length level buffers (ping-
+    // pong by level parity, cudaMalloc'd so they can be exported through
+    // CUDA IPC) and, per parity, the same buffers of the other ranks: K1's
+    // epilogue stores every owned row's w into all of them
+    double *exch[2] = {nullptr, nullptr};
+    size_t exch_n = 0;
+    std::vector<double *> exch_peer[2];
+    std::vector<void *> exch_opened;  // IPC mappings to close
     cudaStream_t stream = nullptr;
     int symmetric = -1;  // cached result of kb_graph_is_symmetric
     size_t device_bytes() const;
+    Graph() = default;
+    Graph(const Graph &) = delete;
+    Graph &operator=(const Graph &) = delete;
+    ~Graph() {
+        for (void *p : exch_opened) cudaIpcCloseMemHandle(p);
+        for (double *&p : exch)
+            if (p) { cudaFree(p); p = nullptr; }
+    }
 };
+
+// ranks a fused omega exchange stores to besides the local one (8 GPUs)
+constexpr int KB_MAX_PEERS = 7;
 
 // ---------------------------------------------------------------- state
 struct State {
@@ -229,6 +262,8 @@ struct State {
     // katz only); materialize_bounds recomputes them, bit for bit, before
     // anything reads them
     bool lazy_bounds = false, bounds_stale = false;
+    bool exch_on = false;     // levels live in the graph's exchange buffers
+    int exch_parity = 0;      // parity of the level being computed
     cudaEvent_t chk_ev = nullptr;
     const double *x_level() const { return levels.back().p; }
 };

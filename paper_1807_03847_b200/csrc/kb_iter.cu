@@ -65,6 +65,9 @@ struct IterArgs {
     int level_only;                 // write w only (dynamic level repair)
     int seg_only;                   // heavy-row segment sums only (no row epilogue)
     int lazy_bounds;                // leave lower/upper to materialize_bounds
+    // fused exchange: every w store also goes to the other ranks' buffers
+    int npeer;
+    double *peer[KB_MAX_PEERS];
     const int32_t *hrow, *vrow;     // explicit row maps (nullptr: implicit)
     int hot;
     // sharded graphs: the hot set is the head of every rank's block of the
@@ -105,6 +108,7 @@ __device__ __forceinline__ double fetch(const double *__restrict__ hot_s, const 
 
 __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s) {
     const double w = __dmul_rn(A.alpha, s);          // engine.py:306
+    for (int q = 0; q < A.npeer; q++) A.peer[q][v] = w;  // NVLink stores to the peers
     if (A.level_only) {
         A.w[v] = w;
         return;
@@ -133,6 +137,7 @@ __device__ __forceinline__ void gather8(const double *__restrict__ hot_s, const 
 // epilogue with katz already loaded (narrow-slice path)
 __device__ __forceinline__ void epilogue_k(const IterArgs &A, int64_t v, double s, double kv) {
     const double w = __dmul_rn(A.alpha, s);
+    for (int q = 0; q < A.npeer; q++) A.peer[q][v] = w;
     if (A.level_only) {
         A.w[v] = w;
         return;
@@ -283,6 +288,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
             else if (!A.seg_only) epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), sum);
         }
     }
+    if (A.npeer) __threadfence_system();  // peer stores visible before the next collective
 }
 
 // Graphs whose slices are all narrow (width <= 4: grids, meshes): no hot
@@ -299,6 +305,7 @@ __global__ void __launch_bounds__(1024, 2) k_sell_narrow(IterArgs A) {
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t gi = wid; gi < groups; gi += nw)
         narrow_group<0, false, Q>(A, gi * Q, lane, nullptr, hm, A.x, pol);
+    if (A.npeer) __threadfence_system();
 }
 
 // First iteration: x = levels[0] = ones, so every sequential row (or segment)
@@ -310,6 +317,7 @@ __global__ void k_ones_step(IterArgs A) {
     const double s = (double)A.vlen[vr];
     if (vr < A.nseg) A.seg_sum[vr] = s;
     else epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), s);
+    if (A.npeer) __threadfence_system();
 }
 
 // heavy row h = combine its segment sums in segment order, then epilogue
@@ -461,6 +469,12 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     A.counter = s.work_counter.p;
     A.abort = s.spec_abort ? s.abort_flag.p : nullptr;
     A.lazy_bounds = (s.lazy_bounds && !level_only) ? 1 : 0;
+    A.npeer = 0;
+    if (s.exch_on && w == g.exch[s.exch_parity]) {
+        const auto &pp = g.exch_peer[s.exch_parity];
+        A.npeer = (int)std::min<size_t>(pp.size(), KB_MAX_PEERS);
+        for (int q = 0; q < A.npeer; q++) A.peer[q] = pp[q];
+    }
     if (A.lazy_bounds) s.bounds_stale = true;
     if (s.seg_sum.n < (size_t)std::max<int64_t>(1, g.sell.nseg)) {
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
@@ -570,6 +584,7 @@ void run_segments(State &s, cudaStream_t st, const double *x) {
     A.level_only = 1;
     A.seg_only = 1;
     A.lazy_bounds = 0;
+    A.npeer = 0;
     A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
     A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
     A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), g.n);
@@ -619,7 +634,12 @@ void launch_iterate(State &s, cudaStream_t st) {
     Graph &g = *s.g;
     const int64_t n = g.n;
     DBuf<double> wnew;
-    wnew.alloc(n + 1);
+    if (s.exch_on) {           // the level goes to the exchange buffer of its parity
+        s.exch_parity = (int)((s.r + 1) & 1);
+        wnew.borrow(g.exch[s.exch_parity], g.exch_n);
+    } else {
+        wnew.alloc(n + 1);
+    }
     run_spmv(s, st, s.x_level(), wnew.p, false);
     s.levels.push_back(std::move(wnew));
     s.r += 1;

@@ -109,7 +109,7 @@ class CudaShard:
     def __init__(self, plan: ShardPlan, rank: int, indptr, indices, *, device: int,
                  alpha: float, gamma: float, crit: Criterion, undirected: bool,
                  max_iterations: int, symmetric: bool = True, split_threshold: int = 0,
-                 local_csr=None):
+                 local_csr=None, fused: bool = False):
         import torch
         self.torch = torch
         self.L = _lib.lib()
@@ -128,6 +128,11 @@ class CudaShard:
                                              _lib.ptr(ix), split_threshold, -1, flags,
                                              _lib.ptr(lab), lo, hi, ctypes.byref(h)))
         self.g = h
+        # fused exchange: K1 stores omega into every rank's level buffers
+        # (exchange_connect); no per-iteration all-gather
+        self.fused = bool(fused)
+        if self.fused:
+            _lib.check(self.L.kb_graph_exchange_alloc(h))
         self.reset(alpha=alpha, gamma=gamma, crit=crit, undirected=undirected,
                    max_iterations=max_iterations)
 
@@ -140,12 +145,42 @@ class CudaShard:
         kind = {RANKING: 0, TOPK: 1, SCORE: 2, PAIR: 3}[crit.kind]
         s = ctypes.c_void_p()
         _lib.check(self.L.kb_state_create(self.g, alpha, gamma, int(undirected), kind,
-                                          crit.epsilon, int(crit.k or 0), 0, 0, 1,
-                                          int(max_iterations), ctypes.byref(s)))
+                                          crit.epsilon, int(crit.k or 0), 0, 0,
+                                          0 if self.fused else 1, int(max_iterations),
+                                          ctypes.byref(s)))
         self.s = s
+        if self.fused:
+            _lib.check(self.L.kb_state_exchange(s, 1))
         lo, _ = self.plan.block(self.rank)
         _lib.check(self.L.kb_state_set_active_range(s, lo, lo + self.plan.owned(self.rank)))
         self.r = 0
+
+    def exchange_export(self):
+        """This rank's two exchange buffers: [(ipc handle bytes, device ptr)]."""
+        out = []
+        for parity in (0, 1):
+            hd = ctypes.create_string_buffer(64)
+            _lib.check(self.L.kb_graph_exchange_handle(self.g, parity, hd))
+            ptr = ctypes.c_void_p()
+            _lib.check(self.L.kb_graph_exchange_ptr(self.g, parity, ctypes.byref(ptr)))
+            out.append((bytes(hd.raw), int(ptr.value or 0)))
+        return out
+
+    def exchange_connect(self, exports, same_process: bool = False):
+        """Register every other rank's buffers (exports[q] from rank q's
+        exchange_export): opened through CUDA IPC, or used as device
+        pointers when the ranks share this process."""
+        for q, ex in enumerate(exports):
+            if q == self.rank:
+                continue
+            for parity in (0, 1):
+                hd, ptr = ex[parity]
+                if same_process:
+                    _lib.check(self.L.kb_graph_exchange_add_peer(self.g, parity, None,
+                                                                 ctypes.c_void_p(ptr)))
+                else:
+                    buf = ctypes.create_string_buffer(hd, 64)
+                    _lib.check(self.L.kb_graph_exchange_add_peer(self.g, parity, buf, None))
 
     def close(self):
         if getattr(self, "s", None):
@@ -346,7 +381,8 @@ class ShardedRun:
         while True:
             self.b.iterate()
             r += 1
-            _all_gather_flat(self.dist, self.b.level_tensor(), self.rank, P, n_per)
+            if not getattr(self.b, "fused", False):   # fused: K1 already stored it
+                _all_gather_flat(self.dist, self.b.level_tensor(), self.rank, P, n_per)
             if self._check():
                 break
             if r >= self.max_iterations:
@@ -373,9 +409,42 @@ class ShardedRun:
                              criterion=self.crit, separated_fraction=frac)
 
 
+def connect_shard(make_shard, dist, rank: int, world: int, device, fused: bool = True):
+    """This rank's CudaShard with the fused exchange (K1 stores omega into
+    every rank's level buffers through CUDA IPC mappings over NVLink) when
+    all ranks can map all peers' buffers; otherwise every rank falls back to
+    the per-iteration NCCL all-gather.  make_shard(fused) builds the shard.
+    Returns (shard, mode)."""
+    import torch
+    if world == 1 or not fused:
+        return make_shard(False), "nccl-allgather"
+    shard, mine, err = None, None, None
+    try:
+        shard = make_shard(True)
+        mine = shard.exchange_export()
+    except Exception as e:      # noqa: BLE001 -- any failure means fall back
+        err = e
+    exports = [None] * world
+    dist.all_gather_object(exports, mine)
+    ok = all(x is not None for x in exports)
+    if ok:
+        try:
+            shard.exchange_connect(exports)
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, e
+    flag = torch.tensor([1 if ok else 0], device=device, dtype=torch.int32)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 1:
+        return shard, "fused-nvlink-stores"
+    if shard is not None:
+        shard.close()
+    return make_shard(False), f"nccl-allgather (fused exchange unavailable: {err})"
+
+
 def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = True,
                 alpha: float | None = None, max_iterations: int | None = None,
-                device: int | None = None, backend_factory=None) -> RankingResult:
+                device: int | None = None, backend_factory=None,
+                fused: bool = True) -> RankingResult:
     """Certify `crit` on the graph (canonical CSR on every rank's host) with
     the current torch.distributed group, one GPU per rank."""
     import torch.distributed as dist
@@ -390,8 +459,12 @@ def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = True,
         max_iterations = default_iteration_cap(alpha, d, crit.epsilon)
     if backend_factory is None:
         dev = rank if device is None else device
-        backend = CudaShard(plan, rank, indptr, indices, device=dev, alpha=alpha, gamma=gamma,
-                            crit=crit, undirected=undirected, max_iterations=max_iterations)
+
+        def make(fz):
+            return CudaShard(plan, rank, indptr, indices, device=dev, alpha=alpha, gamma=gamma,
+                             crit=crit, undirected=undirected, max_iterations=max_iterations,
+                             fused=fz)
+        backend, _mode = connect_shard(make, dist, rank, world, f"cuda:{dev}", fused)
         backend.collective_device = f"cuda:{dev}"
     else:
         backend = backend_factory(plan, rank, alpha, gamma)
@@ -399,4 +472,4 @@ def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = True,
                       max_iterations=max_iterations).run()
 
 
-__all__ = ["ShardPlan", "CudaShard", "ShardedRun", "sharded_run", "fast_split"]
+__all__ = ["ShardPlan", "CudaShard", "ShardedRun", "sharded_run", "connect_shard", "fast_split"]

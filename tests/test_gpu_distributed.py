@@ -19,7 +19,7 @@ torch = pytest.importorskip("torch")
 from paper_1807_03847_b200 import distributed as D  # noqa: E402
 
 
-def _lockstep(g0, crit, world, protocol="device", split=0):
+def _lockstep(g0, crit, world, protocol="device", split=0, fused=False):
     plan = D.ShardPlan(g0.indptr, world)
     d = plan.max_degree
     alpha = 1.0 / (1.0 + d)
@@ -27,8 +27,12 @@ def _lockstep(g0, crit, world, protocol="device", split=0):
     cap = P.default_iteration_cap(alpha, d, crit.epsilon)
     shards = [D.CudaShard(plan, rk, g0.indptr, g0.indices, device=0, alpha=alpha,
                           gamma=gamma, crit=crit, undirected=True, max_iterations=cap,
-                          split_threshold=split)
+                          split_threshold=split, fused=fused)
               for rk in range(world)]
+    if fused:                                 # peers are buffers in this process
+        exports = [s.exchange_export() for s in shards]
+        for s in shards:
+            s.exchange_connect(exports, same_process=True)
     n_per = plan.n_per
     r = 0
     while True:
@@ -36,12 +40,13 @@ def _lockstep(g0, crit, world, protocol="device", split=0):
             s.iterate()
         torch.cuda.synchronize()
         r += 1
-        lv = [s.level_tensor() for s in shards]
-        for rk in range(world):               # all-gather by device copies
-            blk = lv[rk][rk * n_per:(rk + 1) * n_per].clone()
-            for other in range(world):
-                if other != rk:
-                    lv[other][rk * n_per:(rk + 1) * n_per].copy_(blk)
+        if not fused:
+            lv = [s.level_tensor() for s in shards]
+            for rk in range(world):           # all-gather by device copies
+                blk = lv[rk][rk * n_per:(rk + 1) * n_per].clone()
+                for other in range(world):
+                    if other != rk:
+                        lv[other][rk * n_per:(rk + 1) * n_per].copy_(blk)
         torch.cuda.synchronize()
         if crit.kind == "score":
             done = max(s.local_gap() for s in shards) < crit.epsilon
@@ -106,12 +111,15 @@ def _lockstep(g0, crit, world, protocol="device", split=0):
     return r, order, lower, upper, pairs
 
 
-@pytest.mark.parametrize("world,protocol", [(1, "device"), (2, "device"), (3, "device"),
-                                            (2, "host")])
-def test_cuda_shards_equal_single_gpu(world, protocol):
+@pytest.mark.parametrize("world,protocol,fused", [(1, "device", False), (2, "device", False),
+                                                  (3, "device", False), (2, "host", False),
+                                                  (2, "device", True), (3, "host", True)])
+def test_cuda_shards_equal_single_gpu(world, protocol, fused):
+    """fused: K1 stores omega straight into the other shards' level buffers
+    (the NVLink exchange), no all-gather."""
     g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
     crit = P.Criterion.top_k(100, 1e-6)
-    r, order, lower, upper, pairs = _lockstep(g0, crit, world, protocol)
+    r, order, lower, upper, pairs = _lockstep(g0, crit, world, protocol, fused=fused)
     g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
     res = P.run(P.init(g, crit, undirected=True), g)
     assert r == res.iterations_used
@@ -124,10 +132,11 @@ def test_cuda_shards_equal_single_gpu(world, protocol):
     assert ores.top(100) == [int(v) for v in order[:100]]
 
 
-def test_cuda_shards_score_criterion():
+@pytest.mark.parametrize("fused", [False, True])
+def test_cuda_shards_score_criterion(fused):
     g0 = O.rmat_graph(1 << 12, edge_factor=16, seed=3)
     crit = P.Criterion.score(1e-7)
-    r, order, lower, upper, _ = _lockstep(g0, crit, 2)
+    r, order, lower, upper, _ = _lockstep(g0, crit, 2, fused=fused)
     ost = O.OracleState(g0, O.Crit("score", 1e-7))
     ores = O.run(ost, g0)
     assert r == ores.iterations_used
@@ -147,3 +156,80 @@ def test_cuda_shards_fast_split_within_tolerance():
     np.testing.assert_array_equal(order[:100], res.order[:100])
     np.testing.assert_allclose(lower, res.lower, rtol=1e-12, atol=0)
     np.testing.assert_allclose(upper, res.upper, rtol=1e-12, atol=0)
+
+
+def _ipc_rank(rank, world, port, out_dir):
+    """One process of the two-process fused-exchange test (both on cuda:0;
+    host barriers only, so neither rank's kernels wait on the other)."""
+    import os
+    import pickle
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g0 = O.rmat_graph(1 << 12, edge_factor=16, seed=7)
+    crit = P.Criterion.top_k(50, 1e-6)
+    plan = D.ShardPlan(g0.indptr, world)
+    d = plan.max_degree
+    alpha = 1.0 / (1.0 + d)
+    sh = D.CudaShard(plan, rank, g0.indptr, g0.indices, device=0, alpha=alpha,
+                     gamma=P.tail_gamma(alpha, d), crit=crit, undirected=True,
+                     max_iterations=100, fused=True)
+    exports = [None] * world
+    dist.all_gather_object(exports, sh.exchange_export())
+    sh.exchange_connect(exports)              # CUDA IPC handles of the other process
+    r = 0
+    while True:
+        sh.iterate()
+        sh.sync()
+        dist.barrier()                        # every rank's stores have landed
+        r += 1
+        props = [None] * world
+        dist.all_gather_object(props, sh.local_topk(50))
+        keys = np.concatenate([p[0] for p in props])
+        labs = np.concatenate([p[1] for p in props])
+        ups = np.concatenate([p[2] for p in props])
+        kstar, istar, ok = sh.select_global(keys, labs, ups, 50, 1e-6)
+        m = [None] * world
+        dist.all_gather_object(m, sh.apply_cut(kstar, istar))
+        if sum(m) <= 50 and ok:
+            break
+    lo, up = sh.bounds_tensors()
+    a, b = plan.block(rank)
+    with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
+        pickle.dump((r, a, b, lo[a:b].cpu().numpy(), up[a:b].cpu().numpy()), fh)
+    sh.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fused_exchange_two_processes_ipc(tmp_path):
+    """Two processes exchange omega through CUDA IPC mappings of each other's
+    level buffers; the certified bounds equal the single-GPU engine's."""
+    import pickle
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.start_processes(_ipc_rank, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    g0 = O.rmat_graph(1 << 12, edge_factor=16, seed=7)
+    plan = D.ShardPlan(g0.indptr, 2)
+    lower = np.empty(plan.n)
+    upper = np.empty(plan.n)
+    node = plan.node_of_exch
+    rs = set()
+    for rank in range(2):
+        with open(tmp_path / f"rank{rank}.pkl", "rb") as fh:
+            r, a, b, lo, up = pickle.load(fh)
+        rs.add(r)
+        sel = node[a:b] >= 0
+        lower[node[a:b][sel]] = lo[sel]
+        upper[node[a:b][sel]] = up[sel]
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    res = P.run(P.init(g, P.Criterion.top_k(50, 1e-6), undirected=True), g)
+    assert rs == {res.iterations_used}
+    np.testing.assert_array_equal(lower, res.lower)
+    np.testing.assert_array_equal(upper, res.upper)
