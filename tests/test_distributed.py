@@ -216,3 +216,69 @@ def test_shard_plan_balances_and_is_a_bijection():
         row = ix[ip[lo]:ip[lo + 1]]
         np.testing.assert_array_equal(plan.node_of_exch[row],
                                       g.indices[g.indptr[v]:g.indptr[v + 1]])
+
+
+class _FakeFusedShard:
+    """Records what connect_shard asks of a shard (no device)."""
+
+    def __init__(self, rank, fused, fail_export, fail_connect):
+        self.rank, self.fused = rank, fused
+        self.fail_export, self.fail_connect = fail_export, fail_connect
+        self.closed = False
+        if fused and fail_export:
+            raise RuntimeError("cannot allocate exchange buffers")
+
+    def exchange_export(self):
+        return [(b"h%d" % self.rank, 1000 + self.rank), (b"g%d" % self.rank, 2000 + self.rank)]
+
+    def exchange_connect(self, exports):
+        if self.fail_connect:
+            raise RuntimeError("cudaIpcOpenMemHandle failed")
+        self.peers = [e for q, e in enumerate(exports) if q != self.rank]
+
+    def close(self):
+        self.closed = True
+
+
+def _connect_worker(rank, world, port, fail_rank, stage, q):
+    from paper_1807_03847_b200.distributed import connect_shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        made = []
+
+        def make(fused):
+            sh = _FakeFusedShard(rank, fused, fail_export=(stage == "export" and rank == fail_rank),
+                                 fail_connect=(stage == "connect" and rank == fail_rank))
+            made.append(sh)
+            return sh
+        sh, mode = connect_shard(make, dist, rank, world, "cpu", fused=True)
+        q.put((rank, sh.fused, mode.split(" ")[0], len(getattr(sh, "peers", []))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("stage", ["none", "export", "connect"])
+def test_connect_shard_ranks_agree_on_the_exchange(stage):
+    """Every rank uses the fused exchange, or -- when any rank cannot
+    allocate or map the buffers -- every rank falls back to the all-gather."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_connect_worker, args=(r, world, port, 1, stage, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    modes = {o[2] for o in out}
+    fused = {o[1] for o in out}
+    assert len(modes) == 1 and len(fused) == 1
+    if stage == "none":
+        assert fused == {True} and modes == {"fused-nvlink-stores"}
+        assert all(o[3] == world - 1 for o in out)
+    else:
+        assert fused == {False} and modes == {"nccl-allgather"}
