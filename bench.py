@@ -564,10 +564,24 @@ def main():
     peak, peak_src = measured_peaks()
     achieved = B / (k1_ms * 1e-3) / 1e9
     traffic = None
+    gather = None
     prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(prof) and a.scale == 24 and a.edge_factor == 16:
         with open(prof) as fh:
-            traffic = json.load(fh).get("traffic_bytes_per_launch")
+            pj = json.load(fh)
+        traffic = pj.get("traffic_bytes_per_launch")
+        # gather-sector efficiency from the same ncu capture: the 8-byte
+        # omega values the global gathers deliver over the 32-byte sectors
+        # they fetch (the column stream's sectors taken out)
+        sec = pj.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", {}).get("value")
+        if sec:
+            stream_sectors = 4 * nnz / 32
+            shared_gathers = pj.get("hot_set_gathers_per_launch", 0)
+            useful = 8 * (nnz - shared_gathers)
+            fetched = 32 * (sec - stream_sectors)
+            gather = {"sector_efficiency": useful / fetched if fetched > 0 else None,
+                      "global_gather_sectors": int(sec - stream_sectors),
+                      "source": "profiles/k1_traffic.json (ncu, one K1 launch)"}
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -652,7 +666,7 @@ def main():
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_sell_iterate (+k_heavy_combine)",
                          "bytes_per_launch": B, "avg_launch_ms": k1_ms,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src, "gather": gather},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(lc1.value - lc0.value),
