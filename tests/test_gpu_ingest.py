@@ -179,3 +179,22 @@ def test_pinned_host_arrays(chunk):
     finally:
         for a in (ip, ix):
             L.kb_host_unregister(_lib.ptr(a))
+
+
+@pytest.mark.parametrize("arcs", [1, 1 << 25])
+def test_degenerate_graphs(chunk, arcs):
+    """No rows, one row, rows that are all empty, self-loops only, and a
+    long run of empty rows between chunk boundaries."""
+    chunk(arcs)
+    assert device_sym(np.zeros(1, dtype=np.int64), np.zeros(0, dtype=np.int32))
+    assert device_sym(np.zeros(2, dtype=np.int64), np.zeros(0, dtype=np.int32))
+    ip, ix = csr_from_arcs(5, [(v, v) for v in range(5)])
+    assert device_sym(ip, ix)
+    ip, ix = csr_from_arcs(1000, [(0, 999), (999, 0), (1, 998)])
+    assert not device_sym(ip, ix)
+    ip, ix = csr_from_arcs(1000, [(0, 999), (999, 0), (1, 998), (998, 1)])
+    assert device_sym(ip, ix)
+    # a run on it: the two edges rank first, every other node has bound 0
+    g = P.Graph.from_csr(1000, ip, ix)
+    res = P.run(P.init(g, P.Criterion.top_k(4, 1e-9), undirected=True), g)
+    assert sorted(res.top(4)) == [0, 1, 998, 999]
