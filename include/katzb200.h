@@ -302,6 +302,12 @@ int kb_shard_propose(kb_state *s, int64_t k, void *block);
 int kb_shard_cut(kb_state *s, const void *blocks, int64_t nblocks, int64_t k,
                  void *word);
 int kb_shard_commit(kb_state *s, int64_t active);
+/* K1 of the next level queued behind a check's device word (after its
+ * all-reduce): it exits on the device if the word says converged, so the
+ * GPU does not idle through the host read; the caller then drops that
+ * level with kb_state_rollback */
+int kb_shard_iterate_spec(kb_state *s, const long long *word, int64_t k);
+int kb_state_rollback(kb_state *s);
 
 /* ranking_result of a sharded run: the state's lower/upper hold all shards'
  * blocks (exchange layout, after the all-gather) and the graph labels map

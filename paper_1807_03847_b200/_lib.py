@@ -119,6 +119,8 @@ SIGNATURES = {
     "kb_shard_propose": (i32, [vp, i64, vp]),
     "kb_shard_cut": (i32, [vp, vp, i64, i64, vp]),
     "kb_shard_commit": (i32, [vp, i64]),
+    "kb_shard_iterate_spec": (i32, [vp, vp, i64]),
+    "kb_state_rollback": (i32, [vp]),
     "kb_rank_gathered": (i32, [vp, i64, vp, vp, vp, ctypes.POINTER(i64)]),
     "kb_graph_exchange_alloc": (i32, [vp]),
     "kb_graph_exchange_ptr": (i32, [vp, i32, ctypes.POINTER(vp)]),

@@ -654,6 +654,50 @@ int kb_shard_commit(kb_state *h, int64_t active) {
     });
 }
 
+namespace kb {
+namespace {
+// converged iff |active| over all ranks <= k and the prefix is separated
+__global__ void k_shard_publish(const long long *word, int64_t k, unsigned long long *abort) {
+    abort[0] = (word[0] <= k && word[2] != 0) ? 1ull : 0ull;
+}
+}  // namespace
+}  // namespace kb
+
+int kb_shard_iterate_spec(kb_state *h, const long long *word, int64_t k) {
+    return guarded([&] {
+        KB_REQUIRE(h && word && k >= 1, KB_EPARAM, "bad argument");
+        State &s = h->s;
+        use_device(s.g->device);
+        KB_REQUIRE(s.g->version == s.graph_version, KB_ESTATE,
+                   "graph changed since init; static iteration would be unsound");
+        KB_REQUIRE(s.r < s.max_iter, KB_ECONVERGENCE, "iteration cap reached");
+        cudaStream_t st = s.g->stream;
+        if (!s.abort_flag.p) s.abort_flag.alloc(1);
+        k_shard_publish<<<1, 1, 0, st>>>(word, k, s.abort_flag.p);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+        s.spec_abort = true;
+        try {
+            launch_iterate(s, st);
+        } catch (...) {
+            s.spec_abort = false;
+            throw;
+        }
+        s.spec_abort = false;
+    });
+}
+
+int kb_state_rollback(kb_state *h) {
+    return guarded([&] {
+        KB_REQUIRE(h, KB_EPARAM, "NULL state");
+        State &s = h->s;
+        KB_REQUIRE(s.r >= 1 && s.levels.size() >= 2, KB_ESTATE, "no level to roll back");
+        s.levels.pop_back();
+        s.r -= 1;
+        if (s.k1_used >= 2) s.k1_used -= 2;
+    });
+}
+
 int kb_rank_gathered(kb_state *h, int64_t n, int64_t *order, double *lower, double *upper,
                      int64_t *separated_pairs) {
     return guarded([&] {

@@ -234,6 +234,16 @@ class CudaShard:
     def commit(self, active: int):
         _lib.check(self.L.kb_shard_commit(self.s, active))
 
+    def iterate_spec(self, word, k: int):
+        """K1 of the next level behind the check's all-reduced word; it
+        exits on the device if that word says converged (kb_shard_iterate_spec)."""
+        _lib.check(self.L.kb_shard_iterate_spec(self.s, word.data_ptr(), k))
+        self.r += 1
+
+    def rollback(self):
+        _lib.check(self.L.kb_state_rollback(self.s))
+        self.r -= 1
+
     def level_tensor(self):
         return self._view(_lib.KB_VEC_LEVEL, self.r)
 
@@ -346,11 +356,13 @@ class ShardedRun:
         self.dist.all_reduce(t, op=op)
         return t.item()
 
-    def _check(self) -> bool:
+    def _check(self, spec: bool = False):
+        """(converged, speculated): with spec, K1 of the next level is queued
+        behind the check's device word before the host reads it."""
         c = self.crit
         ops = self.dist.ReduceOp
         if c.kind == SCORE:
-            return self._allreduce(self.b.local_gap(), ops.MAX) < c.epsilon
+            return self._allreduce(self.b.local_gap(), ops.MAX) < c.epsilon, False
         # TOPK: fixed-size proposal blocks (count + k keys, labels, uppers as
         # 64-bit words) all-gathered on the device; every rank takes the same
         # global cut; |active| is all-reduced; one host read per check
@@ -363,9 +375,22 @@ class ShardedRun:
         self.dist.all_gather_into_tensor(self._blocks, self._blk)
         self.b.cut(self._blocks, self.world, k, self._word)
         self.dist.all_reduce(self._word[0:1], op=ops.SUM)
-        m_total, m_local, ok = (int(v) for v in self._word.tolist())
+        spec = spec and hasattr(self.b, "iterate_spec")
+        if spec:
+            torch = self.torch
+            if self._word_host is None:
+                self._word_host = torch.empty(3, dtype=torch.int64, pin_memory=True)
+                self._word_ev = torch.cuda.Event()
+            self._word_host.copy_(self._word, non_blocking=True)
+            self._word_ev.record()
+            self.b.iterate_spec(self._word, k)     # runs while the host waits
+            self._word_ev.synchronize()
+            words = self._word_host.tolist()
+        else:
+            words = self._word.tolist()
+        m_total, m_local, ok = (int(v) for v in words)
         self.b.commit(m_local)
-        return m_total <= k and bool(ok)
+        return m_total <= k and bool(ok), spec
 
     def run(self, host_result: bool = True, out=None):
         """engine.run for P ranks; every rank returns the same result.
@@ -377,13 +402,19 @@ class ShardedRun:
     def _run(self, host_result, out=None):
         P, n_per = self.plan.P, self.plan.n_per
         self._blocks = None
+        self._word_host = None
         r = 0
+        ahead = False                  # K1 of level r already queued
         while True:
-            self.b.iterate()
+            if not ahead:
+                self.b.iterate()
             r += 1
             if not getattr(self.b, "fused", False):   # fused: K1 already stored it
                 _all_gather_flat(self.dist, self.b.level_tensor(), self.rank, P, n_per)
-            if self._check():
+            done, ahead = self._check(spec=r < self.max_iterations)
+            if done:
+                if ahead:                  # the queued K1 exited on the device
+                    self.b.rollback()
                 break
             if r >= self.max_iterations:
                 gap = self._allreduce(self.b.local_gap(), self.dist.ReduceOp.MAX)

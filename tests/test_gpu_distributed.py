@@ -233,3 +233,30 @@ def test_fused_exchange_two_processes_ipc(tmp_path):
     assert rs == {res.iterations_used}
     np.testing.assert_array_equal(lower, res.lower)
     np.testing.assert_array_equal(upper, res.upper)
+
+
+def test_sharded_run_one_rank_nccl_speculative():
+    """sharded_run end to end on one rank over NCCL: the per-check host read
+    overlaps a speculative K1 of the next level (rolled back at
+    convergence); the result equals the single-GPU engine's bit for bit."""
+    import socket
+
+    import torch.distributed as dist
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
+        crit = P.Criterion.top_k(100, 1e-6)
+        res = D.sharded_run(g0.indptr, g0.indices, crit, device=0)
+    finally:
+        dist.destroy_process_group()
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    ref = P.run(P.init(g, crit, undirected=True), g)
+    assert res.iterations_used == ref.iterations_used
+    np.testing.assert_array_equal(res.order, ref.order)
+    np.testing.assert_array_equal(res.lower, ref.lower)
+    np.testing.assert_array_equal(res.upper, ref.upper)
+    assert res.separated_fraction == ref.separated_fraction
