@@ -1069,7 +1069,8 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         KB_CUDA(cudaEventCreate(&s.ev0));
         KB_CUDA(cudaEventCreate(&s.ev1));
         KB_CUDA(cudaGetLastError());
-        KB_CUDA(cudaStreamSynchronize(st));
+        // no sync: the fills are stream-ordered before any use of the state,
+        // and run() can queue its first K1 behind them
         *out = h;
     });
 }
