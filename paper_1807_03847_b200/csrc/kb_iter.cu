@@ -214,6 +214,30 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
             const int r = i / A.hot_per, j = i - r * A.hot_per;
             hot_s[i] = A.x[((int64_t)r << A.hot_shift) + j];
         }
+    } else if (A.hot > 0 && (A.hot & 1) == 0) {
+        // the hot set is one contiguous range: a single TMA bulk copy
+        // (global -> shared, completion on an mbarrier) while the CTA's
+        // threads only wait
+        __shared__ __align__(8) unsigned long long bar;
+        const unsigned sbar = (unsigned)__cvta_generic_to_shared(&bar);
+        const unsigned sdst = (unsigned)__cvta_generic_to_shared(hot_s);
+        const unsigned bytes = (unsigned)A.hot * 8u;
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(sbar), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                         "[%0], [%1], %2, [%3];"
+                         ::"r"(sdst), "l"(A.x), "r"(bytes), "r"(sbar) : "memory");
+        }
+        unsigned done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                         "  selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(sbar) : "memory");
     } else {
         for (int i = threadIdx.x; i < A.hot; i += blockDim.x) hot_s[i] = A.x[i];
     }
@@ -511,7 +535,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     const int kid = strided ? 9 + (depth - 1) : (depth - 1) * 3 + xl;
     if (!attr_done[g.device][kid]) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
+                                     227 * 1024 - 64));
         attr_done[g.device][kid] = true;
     }
     const size_t smem = (size_t)A.hot * sizeof(double);
@@ -597,7 +621,7 @@ void run_segments(State &s, cudaStream_t st, const double *x) {
     static bool attr_done[64] = {};
     if (!attr_done[g.device]) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
+                                     227 * 1024 - 64));
         attr_done[g.device] = true;
     }
     KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
