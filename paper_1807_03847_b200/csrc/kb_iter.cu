@@ -209,19 +209,16 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     if (aborted(A)) return;
     extern __shared__ double hot_s[];
     const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u};
-    if (ST) {
-        for (int i = threadIdx.x; i < A.hot; i += blockDim.x) {
-            const int r = i / A.hot_per, j = i - r * A.hot_per;
-            hot_s[i] = A.x[((int64_t)r << A.hot_shift) + j];
-        }
-    } else if (A.hot > 0 && (A.hot & 1) == 0) {
-        // the hot set is one contiguous range: a single TMA bulk copy
-        // (global -> shared, completion on an mbarrier) while the CTA's
-        // threads only wait
+    // The hot set is one contiguous range (or, for a shard, the head of
+    // every rank's block): TMA bulk copies global -> shared, completing on
+    // an mbarrier, while the CTA's threads only wait.
+    const int nseg_hot = ST ? (A.hot_per > 0 ? A.hot / A.hot_per : 0) : 1;
+    const int seg_len = ST ? A.hot_per : A.hot;
+    if (A.hot > 0 && (seg_len & 1) == 0 && nseg_hot >= 1) {
         __shared__ __align__(8) unsigned long long bar;
         const unsigned sbar = (unsigned)__cvta_generic_to_shared(&bar);
         const unsigned sdst = (unsigned)__cvta_generic_to_shared(hot_s);
-        const unsigned bytes = (unsigned)A.hot * 8u;
+        const unsigned bytes = (unsigned)seg_len * 8u;
         if (threadIdx.x == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -229,15 +226,24 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         __syncthreads();
         if (threadIdx.x == 0) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         ::"r"(sbar), "r"(bytes) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-                         "[%0], [%1], %2, [%3];"
-                         ::"r"(sdst), "l"(A.x), "r"(bytes), "r"(sbar) : "memory");
+                         ::"r"(sbar), "r"(bytes * (unsigned)nseg_hot) : "memory");
+            for (int r = 0; r < nseg_hot; r++) {
+                const double *src = ST ? A.x + ((int64_t)r << A.hot_shift) : A.x;
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                             "[%0], [%1], %2, [%3];"
+                             ::"r"(sdst + (unsigned)r * bytes), "l"(src), "r"(bytes), "r"(sbar)
+                             : "memory");
+            }
         }
         unsigned done = 0;
         while (!done)
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
                          "  selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(sbar) : "memory");
+    } else if (ST) {
+        for (int i = threadIdx.x; i < A.hot; i += blockDim.x) {
+            const int r = i / A.hot_per, j = i - r * A.hot_per;
+            hot_s[i] = A.x[((int64_t)r << A.hot_shift) + j];
+        }
     } else {
         for (int i = threadIdx.x; i < A.hot; i += blockDim.x) hot_s[i] = A.x[i];
     }
