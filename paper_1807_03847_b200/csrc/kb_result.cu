@@ -80,6 +80,64 @@ __global__ void k_sep_pairs_rank(const uint64_t *skeys, const int32_t *snids, in
     if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
 }
 
+// The same count with a search table for far answers (graphs with many
+// unseparated pairs, e.g. the grid, where galloping walks far): a few
+// galloping steps near t first (R-MAT's answers are near), then a bisection
+// of a shared-memory sample of every S-th sorted key, then one of the
+// S-long window it selects.
+constexpr int SEP_TAB = 4096;
+constexpr int SEP_GALLOP = 6;
+
+__global__ void k_sep_tab(const uint64_t *skeys, int64_t npos, int64_t S, uint64_t *tab) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < SEP_TAB) tab[i] = skeys[min(i * S, npos - 1)];
+}
+
+__global__ void __launch_bounds__(512) k_sep_pairs_tab(const uint64_t *skeys,
+                                                       const int32_t *snids, int64_t npos,
+                                                       const double *upper,
+                                                       const uint64_t *gtab, int64_t S,
+                                                       unsigned long long *total) {
+    typedef cub::BlockReduce<unsigned long long, 512> Red;
+    __shared__ typename Red::TempStorage tmp;
+    __shared__ uint64_t tab[SEP_TAB];
+    for (int i = threadIdx.x; i < SEP_TAB; i += blockDim.x) tab[i] = gtab[i];
+    __syncthreads();
+    unsigned long long acc = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npos;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        // lower(j) <= u  <=>  skeys[j] >= ~bits(u)  (keys ascend as lower descends)
+        const uint64_t ku = ~(uint64_t)__double_as_longlong(upper[snids[t]]);
+        int64_t hi = t, lo = -1, step = 1;
+        bool found = false;
+        for (int g = 0; g < SEP_GALLOP; g++) {
+            const int64_t c = hi - step;
+            if (c < 0) { lo = -1; found = true; break; }
+            if (skeys[c] < ku) { lo = c; found = true; break; }
+            hi = c;
+            step <<= 1;
+        }
+        if (!found) {
+            // first sample index i with tab[i] >= ku, over samples at or below hi
+            int a = 0, b = (int)min((int64_t)SEP_TAB, hi / S + 1);
+            while (a < b) {
+                const int mid = (a + b) >> 1;
+                if (tab[mid] >= ku) b = mid; else a = mid + 1;
+            }
+            // samples a-1 (< ku) and a (>= ku, or hi) bracket the answer
+            lo = a == 0 ? -1 : (int64_t)(a - 1) * S;
+            hi = min(hi, (int64_t)a * S);
+        }
+        while (hi - lo > 1) {            // keys[lo] < ku (or lo = -1), keys[hi] >= ku
+            const int64_t mid = (lo + hi) >> 1;
+            if (skeys[mid] < ku) lo = mid; else hi = mid;
+        }
+        acc += (unsigned long long)hi;
+    }
+    acc = Red(tmp).Sum(acc);
+    if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
+}
+
 __global__ void k_widen(const int32_t *src, int64_t n, int64_t *dst) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) dst[i] = src[i];
@@ -87,6 +145,26 @@ __global__ void k_widen(const int32_t *src, int64_t n, int64_t *dst) {
 
 }  // namespace
 
+
+// separated pairs of the sorted positive part (ties and zero bounds are
+// handled by the callers): galloping for near answers, a table for far ones
+static void sep_pairs(const uint64_t *skeys, const int32_t *snids, int64_t npos,
+                      const double *upper, unsigned long long *total, int sms,
+                      cudaStream_t st) {
+    if (npos <= 0) return;
+    if (!tune_get("result.sep_table", 1) || npos < 4 * SEP_TAB) {
+        k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(skeys, snids, npos, upper, total);
+        note_launch();
+        return;
+    }
+    const int64_t S = (npos + SEP_TAB - 1) / SEP_TAB;
+    DBuf<uint64_t> tab;
+    tab.alloc(SEP_TAB);
+    k_sep_tab<<<nblk(SEP_TAB, 256), 256, 0, st>>>(skeys, npos, S, tab.p);
+    k_sep_pairs_tab<<<4 * sms, 512, 0, st>>>(skeys, snids, npos, upper, tab.p, S, total);
+    note_launch(2);
+    KB_CUDA(cudaGetLastError());
+}
 
 namespace {
 template <typename F>
@@ -187,9 +265,7 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
         KB_CUDA(cudaMemcpyAsync(order.p + npos, zero_part.p, (n - npos) * sizeof(int32_t),
                                 cudaMemcpyDeviceToDevice, st));
     if (n >= 2 && npos) {
-        k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(kout.p, snids.p, npos, s.upper.p,
-                                                          u + 2);
-        note_launch();
+        sep_pairs(kout.p, snids.p, npos, s.upper.p, u + 2, g.sm_count, st);
     }
     if (order64) {
         order64->alloc(n);
@@ -323,8 +399,10 @@ static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const
         sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
         KB_CUDA(cudaMemcpyAsync(order.p, snids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
         if (n >= 2) {
-            k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(kout.p, snids.p, npos, up, u.p + 2);
-            note_launch();
+            int dev = 0, sms = 148;
+            KB_CUDA(cudaGetDevice(&dev));
+            KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            sep_pairs(kout.p, snids.p, npos, up, u.p + 2, sms, st);
         }
     }
     if (n > npos)
