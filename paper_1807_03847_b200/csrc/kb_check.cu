@@ -661,7 +661,8 @@ bool sorted_check(State &s, cudaStream_t st, int64_t k) {
 __global__ void k_pair_refutes_pub(const double *katz, const double *w, double alpha, double gamma,
                                    int undirected, const int32_t *perm, int32_t q, int32_t x,
                                    double eps, unsigned long long *out,
-                                   unsigned long long *abort) {
+                                   unsigned long long *abort, volatile unsigned long long *host,
+                                   unsigned long long *k1_counter) {
     // the two nodes' bounds from katz and the level, as the K1 epilogue forms them
     const double tq = __dmul_rn(alpha, w[q]), tx = __dmul_rn(alpha, w[x]);
     const double lq = undirected ? __dadd_rn(katz[q], tq) : katz[q];
@@ -671,6 +672,9 @@ __global__ void k_pair_refutes_pub(const double *katz, const double *w, double a
     const bool ref = above && lx <= __dsub_rn(uq, eps);
     out[0] = ref ? 1ull : 0ull;
     abort[0] = ref ? 0ull : 1ull;
+    k1_counter[0] = 0ull;      // the queued K1's work counter (no separate memset)
+    host[0] = ref ? 1ull : 0ull;  // straight into page-locked host memory
+    __threadfence_system();
 }
 
 // candidates: the NCAND block winners with the widest excess (ties: the
@@ -1000,10 +1004,10 @@ bool ranking_pair_enqueue(State &s, cudaStream_t st) {
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
     k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma, s.undirected,
                                         g.perm.p, s.rk_q, s.rk_x, s.eps, s.scratch_u64.p,
-                                        s.abort_flag.p);
+                                        s.abort_flag.p, s.h_flags, s.work_counter.p);
     note_launch();
     KB_CUDA(cudaGetLastError());
-    KB_CUDA(cudaMemcpyAsync(s.h_flags, s.scratch_u64.p, 8, cudaMemcpyDeviceToHost, st));
+    s.counter_zeroed = true;
     KB_CUDA(cudaEventRecord(s.chk_ev, st));
     return true;
 }
@@ -1027,8 +1031,17 @@ bool run_check(State &s, cudaStream_t st) {
 }
 
 namespace {
-__global__ void k_publish(const unsigned long long *src, unsigned long long *dst) {
-    *dst = *src;
+// the check's verdict: abort flag for a speculative K1 queued behind, that
+// K1's work counter reset, and the three result words written straight
+// into page-locked host memory (no separate copy)
+__global__ void k_publish(const unsigned long long *out, unsigned long long *abort,
+                          unsigned long long *k1_counter, volatile unsigned long long *host) {
+    *abort = out[1];
+    *k1_counter = 0ull;
+    host[0] = out[0];
+    host[1] = out[1];
+    host[2] = out[2];
+    __threadfence_system();
 }
 }  // namespace
 
@@ -1107,10 +1120,9 @@ int topk_check_enqueue(State &s, cudaStream_t st) {
     }
     // publish the verdict for a speculative K1 queued behind, then the one
     // host read of this check
-    k_publish<<<1, 1, 0, st>>>(out + 1, s.abort_flag.p);
+    k_publish<<<1, 1, 0, st>>>(out, s.abort_flag.p, s.work_counter.p, s.h_flags);
     note_launch();
-    KB_CUDA(cudaMemcpyAsync(s.h_flags, out, 3 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, st));
+    s.counter_zeroed = true;
     KB_CUDA(cudaEventRecord(s.chk_ev, st));
     return nxt;
 }

@@ -263,6 +263,7 @@ struct State {
     // anything reads them
     bool lazy_bounds = false, bounds_stale = false;
     bool exch_on = false;     // levels live in the graph's exchange buffers
+    bool counter_zeroed = false;  // the next K1's work counter was reset on the device
     int exch_parity = 0;      // parity of the level being computed
     cudaEvent_t chk_ev = nullptr;
     const double *x_level() const { return levels.back().p; }

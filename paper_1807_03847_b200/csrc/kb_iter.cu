@@ -545,8 +545,9 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         attr_done[g.device][kid] = true;
     }
     const size_t smem = (size_t)A.hot * sizeof(double);
-    if (A.nslices && !ones)
+    if (A.nslices && !ones && !s.counter_zeroed)
         KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
+    s.counter_zeroed = false;
     KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used], st));
     if (A.nslices && ones) {
         k_ones_step<<<(unsigned)((A.nvr + 255) / 256), 256, 0, st>>>(A);
