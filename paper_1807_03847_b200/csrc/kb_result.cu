@@ -93,19 +93,16 @@ __global__ void k_sep_tab(const uint64_t *skeys, int64_t npos, int64_t S, uint64
     if (i < SEP_TAB) tab[i] = skeys[min(i * S, npos - 1)];
 }
 
-__global__ void __launch_bounds__(512) k_sep_pairs_tab(const uint64_t *skeys,
+__global__ void __launch_bounds__(256) k_sep_pairs_tab(const uint64_t *skeys,
                                                        const int32_t *snids, int64_t npos,
                                                        const double *upper,
-                                                       const uint64_t *gtab, int64_t S,
+                                                       const uint64_t *__restrict__ tab, int64_t S,
                                                        unsigned long long *total) {
-    typedef cub::BlockReduce<unsigned long long, 512> Red;
+    typedef cub::BlockReduce<unsigned long long, 256> Red;
     __shared__ typename Red::TempStorage tmp;
-    __shared__ uint64_t tab[SEP_TAB];
-    for (int i = threadIdx.x; i < SEP_TAB; i += blockDim.x) tab[i] = gtab[i];
-    __syncthreads();
     unsigned long long acc = 0;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npos;
-         t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < npos) {
         // lower(j) <= u  <=>  skeys[j] >= ~bits(u)  (keys ascend as lower descends)
         const uint64_t ku = ~(uint64_t)__double_as_longlong(upper[snids[t]]);
         int64_t hi = t, lo = -1, step = 1;
@@ -118,13 +115,13 @@ __global__ void __launch_bounds__(512) k_sep_pairs_tab(const uint64_t *skeys,
             step <<= 1;
         }
         if (!found) {
-            // first sample index i with tab[i] >= ku, over samples at or below hi
+            // first sample i with tab[i] >= ku among samples at or below hi
+            // (the 32 KB table stays in L1/L2: every thread reads it)
             int a = 0, b = (int)min((int64_t)SEP_TAB, hi / S + 1);
             while (a < b) {
                 const int mid = (a + b) >> 1;
-                if (tab[mid] >= ku) b = mid; else a = mid + 1;
+                if (__ldg(tab + mid) >= ku) b = mid; else a = mid + 1;
             }
-            // samples a-1 (< ku) and a (>= ku, or hi) bracket the answer
             lo = a == 0 ? -1 : (int64_t)(a - 1) * S;
             hi = min(hi, (int64_t)a * S);
         }
@@ -132,7 +129,7 @@ __global__ void __launch_bounds__(512) k_sep_pairs_tab(const uint64_t *skeys,
             const int64_t mid = (lo + hi) >> 1;
             if (skeys[mid] < ku) lo = mid; else hi = mid;
         }
-        acc += (unsigned long long)hi;
+        acc = (unsigned long long)hi;
     }
     acc = Red(tmp).Sum(acc);
     if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
@@ -161,7 +158,8 @@ static void sep_pairs(const uint64_t *skeys, const int32_t *snids, int64_t npos,
     DBuf<uint64_t> tab;
     tab.alloc(SEP_TAB);
     k_sep_tab<<<nblk(SEP_TAB, 256), 256, 0, st>>>(skeys, npos, S, tab.p);
-    k_sep_pairs_tab<<<4 * sms, 512, 0, st>>>(skeys, snids, npos, upper, tab.p, S, total);
+    k_sep_pairs_tab<<<nblk(npos, 256), 256, 0, st>>>(skeys, snids, npos, upper, tab.p, S, total);
+    (void)sms;
     note_launch(2);
     KB_CUDA(cudaGetLastError());
 }
