@@ -1068,10 +1068,7 @@ void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
     g.indptr.alloc(n + 1);
     DBuf<int32_t> stage;  // the compact columns as uploaded
     stage.alloc(nnz);
-    cudaPointerAttributes pa{};
-    const bool pinned = cudaPointerGetAttributes(&pa, h_indices) == cudaSuccess &&
-                        pa.type == cudaMemoryTypeHost;
-    (void)cudaGetLastError();
+    const bool pinned = host_is_pinned(h_indices);
     // chunks of whole rows, ~chunk_arcs arcs each, processed from the top
     // rows down; the last ones (the bottom rows, processed after the final
     // byte lands) shrink geometrically so little work trails the upload
@@ -1101,9 +1098,7 @@ void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
     };
     auto copy_chunk = [&](int c) {
         const int64_t a = h_indptr[rb[c]], b = h_indptr[rb[c + 1]];
-        if (b > a)
-            KB_CUDA(cudaMemcpyAsync(stage.p + a, h_indices + a, (b - a) * sizeof(int32_t),
-                                    cudaMemcpyHostToDevice, cs));
+        if (b > a) upload_h2d(stage.p + a, h_indices + a, (b - a) * sizeof(int32_t), cs);
         KB_CUDA(cudaEventRecord(ev[c], cs));
     };
     try {
@@ -1111,8 +1106,7 @@ void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
         KB_CUDA(cudaEventRecord(ev[nch], st));
         KB_CUDA(cudaStreamWaitEvent(cs, ev[nch], 0));
         if (trace) KB_CUDA(cudaEventRecord(tev0, cs));
-        KB_CUDA(cudaMemcpyAsync(g.indptr.p, h_indptr, (n + 1) * sizeof(int64_t),
-                                cudaMemcpyHostToDevice, cs));
+        upload_h2d(g.indptr.p, h_indptr, (n + 1) * sizeof(int64_t), cs);
         KB_CUDA(cudaEventRecord(ev[nch + 1], cs));
         if (pinned)
             for (int c = nch - 1; c >= 0; c--) copy_chunk(c);

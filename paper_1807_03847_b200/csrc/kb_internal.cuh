@@ -72,6 +72,8 @@ struct PhaseTrace {
 // (one stream per device), so reuse needs no synchronisation.
 cudaStream_t device_stream();
 cudaStream_t copy_stream();
+bool host_is_pinned(const void *p);
+void upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t cs);
 constexpr size_t BIG_ALLOC = (size_t)64 << 20;
 void *dev_alloc(size_t bytes);
 void dev_free(void *p, size_t bytes);
