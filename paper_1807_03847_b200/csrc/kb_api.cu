@@ -607,7 +607,7 @@ int kb_ranking_read(kb_ranking *r, int which, int64_t offset, int64_t count, voi
                         : which == 1 ? (const void *)(r->lower.p + offset)
                                      : (const void *)(r->upper.p + offset);
         cudaStream_t st = device_stream();
-        KB_CUDA(cudaMemcpyAsync(host, src, count * 8, cudaMemcpyDeviceToHost, st));
+        download_d2h(host, src, count * 8, st);
         KB_CUDA(cudaStreamSynchronize(st));
     });
 }
@@ -846,12 +846,8 @@ int kb_graph_get_csr(kb_graph *h, int64_t *indptr, int32_t *indices) {
             ip = cip.p;
             ix = cix.p;
         }
-        if (indptr)
-            KB_CUDA(cudaMemcpyAsync(indptr, ip, (g.n + 1) * sizeof(int64_t),
-                                    cudaMemcpyDeviceToHost, g.stream));
-        if (indices && g.nnz)
-            KB_CUDA(cudaMemcpyAsync(indices, ix, g.nnz * sizeof(int32_t),
-                                    cudaMemcpyDeviceToHost, g.stream));
+        if (indptr) download_d2h(indptr, ip, (g.n + 1) * sizeof(int64_t), g.stream);
+        if (indices && g.nnz) download_d2h(indices, ix, g.nnz * sizeof(int32_t), g.stream);
         KB_CUDA(cudaStreamSynchronize(g.stream));
     });
 }
@@ -1322,7 +1318,7 @@ int kb_get_vector(kb_state *h, int which, int64_t level, double *out) {
         DBuf<double> tmp;
         tmp.alloc(s.g->n);
         gather_to_original(*s.g, src, tmp.p, st);
-        KB_CUDA(cudaMemcpyAsync(out, tmp.p, s.g->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        download_d2h(out, tmp.p, s.g->n * sizeof(double), st);
         KB_CUDA(cudaStreamSynchronize(st));
     });
 }

@@ -74,6 +74,7 @@ cudaStream_t device_stream();
 cudaStream_t copy_stream();
 bool host_is_pinned(const void *p);
 void upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t cs);
+void download_d2h(void *dst, const void *src, size_t bytes, cudaStream_t st);
 constexpr size_t BIG_ALLOC = (size_t)64 << 20;
 void *dev_alloc(size_t bytes);
 void dev_free(void *p, size_t bytes);

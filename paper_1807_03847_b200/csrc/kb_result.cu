@@ -324,10 +324,10 @@ void run_result(State &s, cudaStream_t st, int64_t *h_order, double *h_lower, do
     try {
         result_device(s, st, h_order ? &o : nullptr, (h_lower && !early) ? &lo : nullptr,
                       (h_upper && !early) ? &up : nullptr, h_pairs);
-        if (h_order) KB_CUDA(cudaMemcpyAsync(h_order, o.p, n * 8, cudaMemcpyDeviceToHost, st));
+        if (h_order) download_d2h(h_order, o.p, n * 8, st);
         if (!early) {
-            if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, st));
-            if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, st));
+            if (h_lower) download_d2h(h_lower, lo.p, n * 8, st);
+            if (h_upper) download_d2h(h_upper, up.p, n * 8, st);
         }
         KB_CUDA(cudaStreamSynchronize(st));
     } catch (...) {
@@ -411,7 +411,7 @@ static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const
         wide.alloc(n);
         k_widen<<<nblk(n, 256), 256, 0, st>>>(order.p, n, wide.p);
         note_launch();
-        KB_CUDA(cudaMemcpyAsync(h_order, wide.p, n * 8, cudaMemcpyDeviceToHost, st));
+        download_d2h(h_order, wide.p, n * 8, st);
     }
     unsigned long long pairs = 0;
     KB_CUDA(cudaMemcpyAsync(&pairs, u.p + 2, 8, cudaMemcpyDeviceToHost, st));
@@ -443,8 +443,8 @@ void rank_gathered(State &s, int64_t n, int64_t *h_order, double *h_lower, doubl
     k_scatter_by_label<<<nblk(g.n, 256), 256, 0, st>>>(s.lower.p, s.upper.p, g.labels(), g.n, n,
                                                       lo.p, up.p);
     note_launch();
-    if (h_lower) KB_CUDA(cudaMemcpyAsync(h_lower, lo.p, n * 8, cudaMemcpyDeviceToHost, st));
-    if (h_upper) KB_CUDA(cudaMemcpyAsync(h_upper, up.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (h_lower) download_d2h(h_lower, lo.p, n * 8, st);
+    if (h_upper) download_d2h(h_upper, up.p, n * 8, st);
     rank_bounds_core(st, n, lo.p, up.p, h_order, h_pairs);
 }
 

@@ -137,4 +137,38 @@ void upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t cs) {
     }
 }
 
+// host dst <- device src after the work queued on st.  Page-locked or small
+// destinations: a plain async copy (the caller synchronises).  Pageable
+// ones: up to RING slot copies in flight, each drained into dst by the host
+// threads as it lands; returns when dst is complete.
+void download_d2h(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    if (host_is_pinned(dst) || bytes < ((size_t)1 << 20) || !tune_get("upload.ring", 1)) {
+        KB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_up_mu);
+    int dev = 0;
+    KB_CUDA(cudaGetDevice(&dev));
+    Ring &R = ring(dev);
+    const size_t npieces = (bytes + SLOT - 1) / SLOT;
+    auto issue = [&](size_t k) {
+        const size_t off = k * SLOT, len = std::min(SLOT, bytes - off);
+        const int i = (int)(k % RING);
+        KB_CUDA(cudaMemcpyAsync(R.slot[i], (const char *)src + off, len, cudaMemcpyDeviceToHost,
+                                st));
+        KB_CUDA(cudaEventRecord(R.ev[i], st));
+    };
+    // the ring's slots may still feed an upload on another stream
+    for (int i = 0; i < RING; i++) KB_CUDA(cudaEventSynchronize(R.ev[i]));
+    for (size_t k = 0; k < std::min(npieces, (size_t)RING); k++) issue(k);
+    for (size_t k = 0; k < npieces; k++) {
+        const int i = (int)(k % RING);
+        const size_t off = k * SLOT, len = std::min(SLOT, bytes - off);
+        KB_CUDA(cudaEventSynchronize(R.ev[i]));
+        pool().copy((char *)dst + off, R.slot[i], len);
+        if (k + RING < npieces) issue(k + RING);
+    }
+}
+
 }  // namespace kb

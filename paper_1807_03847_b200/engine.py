@@ -449,6 +449,21 @@ class RankingResult:
 
 # ---------------------------------------------------------------- operations
 
+# Graph.is_symmetric on the host sorts every arc key (~12 s at C2); a large
+# graph is uploaded here anyway, and the pipelined ingest decides the same
+# question while its arcs stream in (kb_graph_is_symmetric).  Small graphs
+# keep the host test, so bad arguments are still rejected before any device
+# work.
+_HOST_SYMMETRY_ARCS = 1 << 22
+
+
+def _symmetric(g, device: int) -> bool:
+    arcs = getattr(g, "arc_count", None)
+    if arcs is None or arcs <= _HOST_SYMMETRY_ARCS:
+        return bool(g.is_symmetric())
+    return device_graph(g, device).is_symmetric()
+
+
 def init(g, criterion: Criterion, *, alpha: float | None = None,
          undirected: bool = False, keep_all_levels: bool = True,
          threads: int = 1, max_iterations: int | None = None,
@@ -471,7 +486,7 @@ def init(g, criterion: Criterion, *, alpha: float | None = None,
         raise ParameterError(f"topk k={criterion.k} exceeds node count {n}")
     if criterion.kind == PAIR and (criterion.u >= n or criterion.v >= n):
         raise ParameterError("pair criterion names a node outside the graph")
-    if undirected and not g.is_symmetric():
+    if undirected and not _symmetric(g, device):
         raise ParameterError("undirected mode requires a symmetric arc set")
     if threads < 1:
         raise ParameterError(f"threads must be >= 1, got {threads}")

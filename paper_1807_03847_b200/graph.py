@@ -245,8 +245,12 @@ class Graph:
         return np.diff(ip)
 
     def max_out_degree(self) -> int:
-        """graph.py:154-158."""
-        return int(self.out_degrees().max()) if self._n else 0
+        """graph.py:154-158 (cached per version: init asks twice)."""
+        c = self._cache.get("maxdeg")
+        if c is None or c[0] != self._version:
+            c = (self._version, int(self.out_degrees().max()) if self._n else 0)
+            self._cache["maxdeg"] = c
+        return c[1]
 
     def arcs(self) -> Iterator[Arc]:
         n = self._n

@@ -198,3 +198,26 @@ def test_degenerate_graphs(chunk, arcs):
     g = P.Graph.from_csr(1000, ip, ix)
     res = P.run(P.init(g, P.Criterion.top_k(4, 1e-9), undirected=True), g)
     assert sorted(res.top(4)) == [0, 1, 998, 999]
+
+
+def test_init_symmetry_from_the_device_copy_on_large_graphs():
+    """Above 4M arcs init takes the symmetry test from the ingest's device
+    result instead of sorting every arc key on the host; the verdict (and
+    the error for an asymmetric arc set) is the same."""
+    g0 = O.rmat_graph(1 << 18, edge_factor=16, seed=4)
+    assert g0.indptr[-1] > (1 << 22)
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    st = P.init(g, P.Criterion.top_k(10, 1e-6), undirected=True)
+    assert st.r == 0
+    ix = g0.indices.copy()
+    ip = g0.indptr
+    # drop one arc u -> v (keep v -> u): the arc set is no longer symmetric
+    u = int(np.argmax(np.diff(ip)))
+    keep = np.ones(ix.size, dtype=bool)
+    keep[ip[u]] = False
+    ip2 = ip.copy()
+    ip2[u + 1:] -= 1
+    gd = P.Graph.from_csr(g0.node_count, ip2, ix[keep])
+    assert not gd.is_symmetric()
+    with pytest.raises(P.ParameterError, match="symmetric"):
+        P.init(gd, P.Criterion.top_k(10, 1e-6), undirected=True)
