@@ -1117,6 +1117,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
                         HR.p, (int64_t)hh, w_cur, s.alpha, g.h_of_row.p, g.seg_ptr.p,
                         g.seg_list.p, s.seg_sum.p, C.p, cnt.p + 1);
                     note_launch();
+                    tr.mark("heavy rows (segment pass)");
                 } else if (hh) {
                     k_heavy_rows_fold<<<(unsigned)hh, 256, 0, st>>>(
                         HR.p, w_prev, w_cur, s.alpha, g.h_of_row.p, g.seg_ptr.p, g.seg_list.p,

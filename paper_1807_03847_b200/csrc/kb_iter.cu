@@ -632,6 +632,7 @@ void run_segments(State &s, cudaStream_t st, const double *x) {
         attr_done[g.device] = true;
     }
     KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
+    s.counter_zeroed = false;   // this launch leaves the counter non-zero
     kern<<<g.sm_count, 1024, (size_t)A.hot * sizeof(double), st>>>(A);
     note_launch();
     KB_CUDA(cudaGetLastError());

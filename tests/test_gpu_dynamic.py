@@ -325,5 +325,55 @@ def test_heavy_row_repair_routes_bitwise(heavy_dense):
             np.testing.assert_array_equal(mine, theirs)
         np.testing.assert_array_equal(st.lower, fresh.lower)
         np.testing.assert_array_equal(st.upper, fresh.upper)
+        # one more K1 pass after the repair: the dense heavy route's segment
+        # pass must leave the K1 work counter in a state K1 resets (it once
+        # kept a converged check's "already zeroed" mark, so this pass
+        # skipped rows)
+        P.iterate_once(st, g)
+        fresh = fresh_to_depth(g, st)
+        np.testing.assert_array_equal(st.levels[-1], fresh.levels[-1])
+        np.testing.assert_array_equal(st.lower, fresh.lower)
+    finally:
+        _lib.check(L.kb_tune(b"dyn.heavy_dense", 256))
+
+
+@pytest.mark.parametrize("seed", [5, 6, 7])
+def test_heavy_segment_pass_then_full_level_k1(seed):
+    """A converged check pre-zeroes K1's work counter; a dense heavy repair
+    (run_segments) at a local level then takes work from it, and the next
+    dense level runs K1 over every row.  That K1 must start from a reset
+    counter (it once skipped the reset and left rows unvisited): the levels
+    stay bit-identical to a fresh static run.  A few arcs between low-degree
+    nodes next to hubs put hubs in a local level."""
+    from paper_1807_03847_b200 import _lib
+    L = _lib.lib()
+    _lib.check(L.kb_tune(b"dyn.heavy_dense", 0))
+    try:
+        g0 = O.rmat_graph(65536, edge_factor=16, seed=42)
+        g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+        st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
+        P.run(st, g)
+        deg = np.diff(g0.indptr)
+        hub = deg > 2048
+        cand = [u for u in np.nonzero((deg >= 1) & (deg <= 3))[0]
+                if hub[g0.indices[g0.indptr[u]:g0.indptr[u + 1]]].any()]
+        rng = np.random.default_rng(seed)
+        rng.shuffle(cand)
+        ins = set()
+        for a, b in zip(cand[0:24:2], cand[1:24:2]):
+            if not g.has_arc(int(a), int(b)):
+                ins.add((min(int(a), int(b)), max(int(a), int(b))))
+        ins = sorted(ins)
+        # two batches: the first update's closing check is what leaves the
+        # counter pre-zeroed (P.run ends on a speculative K1 instead)
+        for part in (ins[:len(ins) // 2], ins[len(ins) // 2:]):
+            arcs = [a for uv in part for a in (uv, uv[::-1])]
+            P.update_batch(st, g, P.EdgeBatch(insertions=arcs))
+        fresh = fresh_to_depth(g, st)
+        assert len(st.levels) == len(fresh.levels)
+        for mine, theirs in zip(st.levels, fresh.levels):
+            np.testing.assert_array_equal(mine, theirs)
+        np.testing.assert_array_equal(st.lower, fresh.lower)
+        np.testing.assert_array_equal(st.upper, fresh.upper)
     finally:
         _lib.check(L.kb_tune(b"dyn.heavy_dense", 256))
