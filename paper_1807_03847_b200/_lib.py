@@ -147,6 +147,10 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        # KB_TUNE="name=value,...": tuning knobs for experiments (tools/)
+        for item in filter(None, os.environ.get("KB_TUNE", "").split(",")):
+            k, _, v = item.partition("=")
+            L.kb_tune(k.strip().encode(), int(v))
         _lib = L
     return _lib
 
