@@ -260,3 +260,26 @@ def test_sharded_run_one_rank_nccl_speculative():
     np.testing.assert_array_equal(res.lower, ref.lower)
     np.testing.assert_array_equal(res.upper, ref.upper)
     assert res.separated_fraction == ref.separated_fraction
+
+
+@pytest.mark.parametrize("world,fused", [(3, True), (4, False)])
+def test_cuda_shards_s20_match_reference_digests(world, fused):
+    """R-MAT s20 (31.4M arcs) on 3-4 lockstep shards with sequential rows:
+    r, order, bounds and separated fraction bit-identical to the reference's
+    own run (SURVEY.md §8(c) digests)."""
+    import hashlib
+
+    def h16(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+    g0 = O.rmat_graph(1 << 20, edge_factor=16, seed=42)
+    crit = P.Criterion.top_k(100, 1e-6)
+    r, order, lower, upper, pairs = _lockstep(g0, crit, world, split=1 << 30, fused=fused)
+    n = g0.node_count
+    assert r == 7
+    assert [int(v) for v in order[:10]] == [0, 2048, 32768, 131072, 4096, 4, 256, 524288,
+                                            1024, 32]
+    assert pairs / (n * (n - 1) // 2) == 0.8525977645781982
+    assert h16(np.asarray(order, dtype=np.int64)) == "85ea50d05c5dfd0e"
+    assert h16(lower) == "f13ddf321fb10751"
+    assert h16(upper) == "9db3105f69a9e233"
