@@ -110,3 +110,33 @@ def test_C4_grid_ranking_matches_reference_digests():
     assert h16(res.lower) == REF_C4["lower"]
     assert h16(res.upper) == REF_C4["upper"]
     assert h16(np.asarray(res.top(100), dtype=np.int64)) == REF_C4["top100"]
+
+
+def test_C5_batches_match_static_recompute_bitwise():
+    """C5 at full size: insertion batches on C2 (1e3 then 1e4 edges, the
+    second after the first update's closing check); after each, r, top-100
+    and the lower/upper bounds equal a fresh static run on the post-batch
+    graph bit for bit."""
+    n = 1 << 24
+    crit = P.Criterion.top_k(100, 1e-6)
+    g = G.rmat_graph(n, edge_factor=16, seed=42)
+    st = P.init(g, crit, undirected=True, max_iterations=200)
+    P.run(st, g)
+    deg = g.out_degrees()
+    dmax = int(deg.max())
+    rng = np.random.default_rng(7)
+    for b in (1000, 10000):
+        e = rng.integers(0, n, size=(3 * b, 2))
+        e = e[e[:, 0] != e[:, 1]]
+        e = np.unique(np.sort(e, axis=1), axis=0)
+        e = e[(deg[e[:, 0]] + 1 < dmax) & (deg[e[:, 1]] + 1 < dmax)][:b]
+        e = e[~g._present(e)]
+        arcs = np.concatenate([e, e[:, ::-1]])
+        P.update_batch(st, g, P.EdgeBatch(insertions=[tuple(x) for x in arcs.tolist()]))
+        np.add.at(deg, arcs[:, 0], 1)
+        dyn = P.ranking_result(st)
+        fresh = P.run(P.init(g, crit, undirected=True, max_iterations=200), g)
+        assert dyn.iterations_used == fresh.iterations_used
+        assert dyn.top(100) == fresh.top(100)
+        np.testing.assert_array_equal(dyn.lower, fresh.lower)
+        np.testing.assert_array_equal(dyn.upper, fresh.upper)
