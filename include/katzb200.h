@@ -81,8 +81,9 @@ typedef struct {
 typedef struct {
     int64_t batch_size, seeds, visited, reactivated, resumed_iterations;
     int64_t aborted_level;    /* -1 == None                                  */
-    int64_t n_level_sizes;
-    int64_t level_sizes[64];  /* UpdateStats.level_sizes (dynamic.py:35)     */
+    int64_t n_level_sizes;    /* the full count (may exceed 64)              */
+    int64_t level_sizes[64];  /* UpdateStats.level_sizes (dynamic.py:35):
+                                 the first 64; kb_update_level_sizes has all */
 } kb_update_stats;
 
 /* ---- library ---- */
@@ -122,6 +123,18 @@ int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr
                        const int32_t *indices, int64_t split_threshold,
                        int64_t hot_size, int flags, const int32_t *labels,
                        int64_t own_lo, int64_t own_hi, kb_graph **out);
+/* Rank `rank` of `nranks`' row shard of a device graph, built on that
+ * graph's device with no host round trip (the multi-GPU
+ * split of KatzState._matvec's rows, engine.py:181-208): rows are dealt by
+ * degree rank round-robin, the shard is a KB_GRAPH_NO_RELABEL graph over the
+ * exchange layout e(v) = (q mod P)*n_per + q div P whose non-owned rows are
+ * empty, each owned row keeps its arcs in ascending original-id order, and
+ * the tie-break labels are the node ids (padding: n, n+1, ...).  The shard
+ * inherits `full`'s symmetry flag.  Outputs n_per = ceil(n/P) and the number
+ * of rows this rank owns (its block's head). */
+int kb_graph_create_shard(kb_graph *full, int64_t nranks, int64_t rank,
+                          int64_t split_threshold, int64_t hot_size, kb_graph **out,
+                          int64_t *n_per, int64_t *owned);
 /* Device generators, bit-identical to katzbounds.generate (generate.py:38-103)
  * loaded with undirected=True: R-MAT on n = 2^scale nodes from numpy's PCG64
  * stream whose current state is pcg_state = {state_hi, state_lo, inc_hi,
@@ -317,6 +330,9 @@ int kb_rank_gathered(kb_state *s, int64_t n, int64_t *order, double *lower,
 
 /* dynamic.update_batch (dynamic.py:126-211): arcs as (src,dst) int64 pairs,
  * already validated by the caller against the host graph. */
+/* every entry of the last update's UpdateStats.level_sizes (dynamic.py:35),
+ * up to cap; *count receives the full length */
+int kb_update_level_sizes(kb_state *state, int64_t *out, int64_t cap, int64_t *count);
 int kb_update_batch(kb_state *s, const int64_t *ins, int64_t n_ins,
                     const int64_t *dels, int64_t n_dels, double theta,
                     double new_gamma, kb_update_stats *stats);

@@ -56,6 +56,13 @@ def lib():
         L.oracle_rmat_pairs.restype = i64
         L.oracle_csr_from_packed.argtypes = [i64, i64, dp, dp, dp]
         L.oracle_csr_from_packed.restype = ctypes.c_int
+        L.oracle_rmat_packed_lowmem.argtypes = [u64, u64, u64, u64, ctypes.c_int,
+                                                i64, ctypes.c_double,
+                                                ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_int, dp]
+        L.oracle_rmat_packed_lowmem.restype = i64
+        L.oracle_unique_sorted_inplace.argtypes = [i64, dp]
+        L.oracle_unique_sorted_inplace.restype = i64
         _lib = L
     return _lib
 
@@ -185,6 +192,36 @@ def rmat_graph(n: int, edge_factor: int = 8, seed: int = 0) -> CSRGraph:
     indices = np.empty(2 * packed.size, dtype=np.int32)
     lib().oracle_csr_from_packed(n, packed.size, _p(packed), _p(indptr),
                                  _p(indices))
+    return CSRGraph(n, indptr, indices, symmetric=True)
+
+
+def rmat_graph_lowmem(n: int, edge_factor: int = 8, seed: int = 0,
+                      threads: int | None = None) -> CSRGraph:
+    """rmat_graph with peak host memory ~ 8*m + 4*nnz bytes (scale 27 on a
+    64 GB host): the sampler writes packed keys directly (no src/dst
+    scratch), then an in-place sort + unique.  Same unique key set, hence
+    the same CSR, as rmat_graph / generate.py:55-81."""
+    if not (n >= 2 and (n & (n - 1)) == 0):
+        raise ValueError("rmat needs a power-of-two node count >= 2")
+    a, b, c, _ = (0.57, 0.19, 0.19, 0.05)
+    ab = a + b
+    abc = a + b + c
+    scale = n.bit_length() - 1
+    m = n * edge_factor
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    M = (1 << 64) - 1
+    packed = np.empty(m, dtype=np.int64)
+    t = threads or os.cpu_count() or 1
+    w = lib().oracle_rmat_packed_lowmem(s >> 64, s & M, inc >> 64, inc & M,
+                                        scale, m, a, ab, abc, t, _p(packed))
+    view = packed[:w]
+    view.sort()
+    w = lib().oracle_unique_sorted_inplace(w, _p(view))
+    indptr = np.empty(n + 1, dtype=np.int64)
+    indices = np.empty(2 * w, dtype=np.int32)
+    lib().oracle_csr_from_packed(n, w, _p(packed), _p(indptr), _p(indices))
+    del packed, view
     return CSRGraph(n, indptr, indices, symmetric=True)
 
 

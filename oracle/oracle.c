@@ -205,6 +205,87 @@ int64_t oracle_rmat_pairs(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
     return w;
 }
 
+/* Same draw stream as oracle_rmat_pairs, but without the two m-long src/dst
+ * scratch arrays: each thread walks its sample range in blocks of B samples,
+ * replays the `scale` per-bit draws of the block (jump-ahead per bit), and
+ * appends the block's non-loop packed keys to its own slice of `packed`.
+ * The slices are then compacted in thread order.  Peak memory is the m-long
+ * `packed` array alone, which is what makes scale 27 (m = 2^31) fit a 64 GB
+ * host.  Key ORDER differs from oracle_rmat_pairs (block-major per thread);
+ * the caller sorts, so the unique key set is identical. */
+typedef struct {
+    u128 state0, inc;
+    int scale;
+    int64_t m, e0, e1, n_out;
+    double a, ab, abc;
+    int64_t *packed;
+} rmat_lm_job;
+
+#define RMAT_BLOCK 65536
+
+static void *rmat_lm_worker(void *p) {
+    rmat_lm_job *j = (rmat_lm_job *)p;
+    int64_t src[RMAT_BLOCK], dst[RMAT_BLOCK];
+    int64_t w = j->e0, n = (int64_t)1 << j->scale;
+    for (int64_t b0 = j->e0; b0 < j->e1; b0 += RMAT_BLOCK) {
+        int64_t cnt = j->e1 - b0 < RMAT_BLOCK ? j->e1 - b0 : RMAT_BLOCK;
+        memset(src, 0, sizeof(int64_t) * cnt);
+        memset(dst, 0, sizeof(int64_t) * cnt);
+        for (int bit = 0; bit < j->scale; bit++) {
+            u128 s = pcg_advance(j->state0, (u128)((uint64_t)bit * (uint64_t)j->m + (uint64_t)b0),
+                                 PCG_MULT, j->inc);
+            for (int64_t e = 0; e < cnt; e++) {
+                s = s * PCG_MULT + j->inc;
+                double draw = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+                int64_t sb = draw >= j->ab;
+                int64_t db = ((draw >= j->a) & (draw < j->ab)) | (draw >= j->abc);
+                src[e] = (src[e] << 1) | sb;
+                dst[e] = (dst[e] << 1) | db;
+            }
+        }
+        for (int64_t e = 0; e < cnt; e++) {
+            int64_t s = src[e], d = dst[e];
+            if (s == d) continue;
+            int64_t lo = s < d ? s : d, hi = s < d ? d : s;
+            j->packed[w++] = lo * n + hi;
+        }
+    }
+    j->n_out = w - j->e0;
+    return NULL;
+}
+
+int64_t oracle_rmat_packed_lowmem(uint64_t state_hi, uint64_t state_lo,
+                                  uint64_t inc_hi, uint64_t inc_lo, int scale,
+                                  int64_t m, double a, double ab, double abc,
+                                  int threads, int64_t *packed) {
+    if (threads < 1) threads = 1;
+    pthread_t *tid = (pthread_t *)malloc(sizeof(pthread_t) * threads);
+    rmat_lm_job *jobs = (rmat_lm_job *)malloc(sizeof(rmat_lm_job) * threads);
+    for (int i = 0; i < threads; i++) {
+        jobs[i].state0 = mk128(state_hi, state_lo);
+        jobs[i].inc = mk128(inc_hi, inc_lo);
+        jobs[i].scale = scale;
+        jobs[i].m = m;
+        jobs[i].e0 = m * i / threads;
+        jobs[i].e1 = m * (i + 1) / threads;
+        jobs[i].a = a;
+        jobs[i].ab = ab;
+        jobs[i].abc = abc;
+        jobs[i].packed = packed;
+        pthread_create(&tid[i], NULL, rmat_lm_worker, &jobs[i]);
+    }
+    for (int i = 0; i < threads; i++) pthread_join(tid[i], NULL);
+    int64_t w = 0;
+    for (int i = 0; i < threads; i++) {
+        if (w != jobs[i].e0)
+            memmove(packed + w, packed + jobs[i].e0, sizeof(int64_t) * jobs[i].n_out);
+        w += jobs[i].n_out;
+    }
+    free(tid);
+    free(jobs);
+    return w;
+}
+
 /* ---------------- undirected CSR from sorted unique packed edges ----------
  * packed: sorted unique lo*n+hi with lo<hi. Builds the symmetric CSR with
  * each row sorted ascending (graph.py:191-192 canonical order). */
@@ -234,4 +315,14 @@ int oracle_csr_from_packed(int64_t n, int64_t ne, const int64_t *packed,
     }
     free(fill);
     return 0;
+}
+
+/* In-place np.unique of a sorted array (generate.py:80); returns the new
+ * length.  Used by the low-memory scale-27 golden build. */
+int64_t oracle_unique_sorted_inplace(int64_t cnt, int64_t *a) {
+    if (cnt == 0) return 0;
+    int64_t w = 1;
+    for (int64_t i = 1; i < cnt; i++)
+        if (a[i] != a[w - 1]) a[w++] = a[i];
+    return w;
 }

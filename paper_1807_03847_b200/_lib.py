@@ -68,6 +68,8 @@ SIGNATURES = {
     "kb_graph_create": (i32, [i32, i64, i64, vp, vp, i64, i64, ctypes.POINTER(vp)]),
     "kb_graph_create_ex": (i32, [i32, i64, i64, vp, vp, i64, i64, i32, vp, i64, i64,
                                  ctypes.POINTER(vp)]),
+    "kb_graph_create_shard": (i32, [vp, i64, i64, i64, i64, ctypes.POINTER(vp),
+                                    ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "kb_graph_create_rmat": (i32, [i32, i32, i64, vp, dbl, dbl, dbl, i64, i64,
                                    ctypes.POINTER(vp)]),
     "kb_graph_create_grid": (i32, [i32, i64, i64, i64, ctypes.POINTER(vp)]),
@@ -127,6 +129,7 @@ SIGNATURES = {
     "kb_graph_exchange_handle": (i32, [vp, i32, vp]),
     "kb_graph_exchange_add_peer": (i32, [vp, i32, vp, vp]),
     "kb_state_exchange": (i32, [vp, i32]),
+    "kb_update_level_sizes": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
     "kb_update_batch": (i32, [vp, vp, i64, vp, i64, dbl, dbl,
                               ctypes.POINTER(UpdateStatsC)]),
 }

@@ -405,6 +405,22 @@ int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr
     });
 }
 
+int kb_graph_create_shard(kb_graph *full, int64_t nranks, int64_t rank, int64_t split_threshold,
+                          int64_t hot_size, kb_graph **out, int64_t *n_per, int64_t *owned) {
+    return guarded([&] {
+        KB_REQUIRE(full && out && n_per && owned, KB_EPARAM, "NULL argument");
+        use_device(full->g.device);
+        kb_graph *h = new_graph(full->g.device, split_threshold, hot_size);
+        try {
+            build_shard(full->g, nranks, rank, h->g, n_per, owned);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
 int kb_state_set_active(kb_state *h, const int64_t *ids, int64_t m) {
     return guarded([&] {
         KB_REQUIRE(h && (m == 0 || ids), KB_EPARAM, "NULL argument");
@@ -1123,6 +1139,7 @@ int kb_iterate(kb_state *h, int64_t steps) {
         State &s = h->s;
         use_device(s.g->device);
         check_version(s);
+        if (steps > 0) materialize_rank_order(s, s.g->stream);
         for (int64_t i = 0; i < steps; i++) launch_iterate(s, s.g->stream);
         KB_CUDA(cudaGetLastError());
     });
@@ -1329,6 +1346,8 @@ int kb_get_active(kb_state *h, int64_t *out) {
         State &s = h->s;
         use_device(s.g->device);
         cudaStream_t st = s.g->stream;
+        materialize_bounds(s, st);
+        materialize_rank_order(s, st);
         const int64_t m = s.m_host;
         if (!m) return;
         DBuf<int64_t> tmp;
@@ -1337,6 +1356,15 @@ int kb_get_active(kb_state *h, int64_t *out) {
                                                        s.g->perm.p, tmp.p); note_launch();
         KB_CUDA(cudaMemcpyAsync(out, tmp.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kb_update_level_sizes(kb_state *h, int64_t *out, int64_t cap, int64_t *count) {
+    return guarded([&] {
+        KB_REQUIRE(h && count && (cap <= 0 || out), KB_EPARAM, "NULL argument");
+        const auto &v = h->s.level_sizes;
+        *count = (int64_t)v.size();
+        for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)v.size()); i++) out[i] = v[i];
     });
 }
 
@@ -1351,6 +1379,7 @@ int kb_update_batch(kb_state *h, const int64_t *ins, int64_t n_ins, const int64_
             KB_REQUIRE(ins[i] >= 0 && ins[i] < s.g->n, KB_ENODERANGE, "node id outside graph");
         for (int64_t i = 0; i < 2 * n_dels; i++)
             KB_REQUIRE(dels[i] >= 0 && dels[i] < s.g->n, KB_ENODERANGE, "node id outside graph");
+        materialize_rank_order(s, s.g->stream);
         update_batch(s, ins, n_ins, dels, n_dels, theta, new_gamma, stats);
     });
 }

@@ -653,6 +653,7 @@ bool sorted_check(State &s, cudaStream_t st, int64_t k) {
     s.cur = nxt;
     s.act_dense = false;
     s.m_host = (int64_t)s.h_flags[1];
+    s.rank_order_pending = false;
     return s.m_host <= k && s.h_flags[0] == 0;
 }
 
@@ -919,6 +920,11 @@ __global__ void __launch_bounds__(1024) k_pick_cands_fast(const unsigned long lo
 
 bool check_ranking(State &s, cudaStream_t st) {
     Graph &g = *s.g;
+    // the reference leaves active sorted by (-lower, id) after every ranking
+    // check (engine.py:362-372 with k = n); the certificates below decide
+    // without sorting, so the order is produced on demand
+    // (materialize_rank_order) unless the full sort runs anyway
+    s.rank_order_pending = true;
     const int64_t n = s.m_host;
     const int32_t *act = s.act[s.cur].p;
     const int dense = s.act_dense;
@@ -975,6 +981,12 @@ bool check_ranking(State &s, cudaStream_t st) {
 
 }  // namespace
 
+void materialize_rank_order(State &s, cudaStream_t st) {
+    if (!s.rank_order_pending || s.kind != KB_RANKING) return;
+    sorted_check(s, st, s.g->n);    // k = n: keeps every node, sorted
+    s.check_full_sorts--;           // not a check the certificates missed
+}
+
 void ensure_cub_tmp(State &s, size_t bytes) {
     if (s.cub_tmp.n < bytes) s.cub_tmp.alloc(bytes);
 }
@@ -999,6 +1011,7 @@ double run_gap(State &s, cudaStream_t st) {
 // (complete at chk_ev).  false: no pair cached.
 bool ranking_pair_enqueue(State &s, cudaStream_t st) {
     if (s.rk_q < 0 || !tune_get("check.pair_cache", 1)) return false;
+    s.rank_order_pending = true;
     Graph &g = *s.g;
     if (!s.abort_flag.p) s.abort_flag.alloc(1);
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));

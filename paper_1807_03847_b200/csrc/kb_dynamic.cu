@@ -930,6 +930,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
                "state does not belong to this graph revision");
     KB_REQUIRE(theta >= 0.0 && theta <= 1.0, KB_EPARAM, "theta must be in [0, 1]");
     kb_update_stats st_out{};
+    s.level_sizes.clear();
     st_out.batch_size = n_ins + n_dels;
     st_out.aborted_level = -1;
 
@@ -1019,7 +1020,9 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             tr.mark("level (full K1)");
             continue;
         }
-        if (st_out.n_level_sizes < 64) st_out.level_sizes[st_out.n_level_sizes++] = affected;
+        if (st_out.n_level_sizes < 64) st_out.level_sizes[st_out.n_level_sizes] = affected;
+        st_out.n_level_sizes++;
+        s.level_sizes.push_back(affected);
         bool dense = nchanged > n / 256;
         if (!dense && nchanged) {
             // a few hubs can carry most of the arcs: decide by the expansion's

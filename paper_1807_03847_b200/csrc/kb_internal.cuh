@@ -269,6 +269,8 @@ struct State {
     bool counter_zeroed = false;  // the next K1's work counter was reset on the device
     int exch_parity = 0;      // parity of the level being computed
     cudaEvent_t chk_ev = nullptr;
+    bool rank_order_pending = false;    // RANKING: active not yet in (-lower, id) order
+    std::vector<int64_t> level_sizes;   // UpdateStats.level_sizes of the last update
     const double *x_level() const { return levels.back().p; }
 };
 
@@ -303,6 +305,7 @@ bool run_check(State &s, cudaStream_t st);      // returns converged
 int topk_check_enqueue(State &s, cudaStream_t st);
 bool topk_check_finish(State &s, int nxt);
 bool ranking_pair_enqueue(State &s, cudaStream_t st);
+void materialize_rank_order(State &s, cudaStream_t st);
 double run_gap(State &s, cudaStream_t st);
 void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
                    DBuf<double> *upper, int64_t *h_pairs);
@@ -351,6 +354,8 @@ void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], do
 void grid_device_csr(int64_t n, DBuf<int64_t> &indptr, DBuf<int32_t> &indices,
                      int64_t &nnz_out);
 int graph_is_symmetric(Graph &g);
+void build_shard(Graph &full, int64_t P, int64_t rank, Graph &out, int64_t *n_per_out,
+                 int64_t *owned_out);
 void ensure_cub_tmp(State &s, size_t bytes);
 
 }  // namespace kb

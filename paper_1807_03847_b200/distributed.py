@@ -103,30 +103,62 @@ class ShardPlan:
         return ip, ix
 
 
-class CudaShard:
-    """Product backend: this rank's shard on its GPU through the C-ABI."""
+class DevicePlan:
+    """The partition of ShardPlan without its host arrays: the exchange
+    layout's block sizes.  The per-node maps live on the device
+    (kb_graph_create_shard)."""
 
-    def __init__(self, plan: ShardPlan, rank: int, indptr, indices, *, device: int,
+    def __init__(self, n: int, nranks: int, max_degree: int):
+        if nranks < 1:
+            raise ParameterError("nranks must be >= 1")
+        self.n, self.P = int(n), int(nranks)
+        self.n_per = max(1, -(-self.n // self.P))
+        self.max_degree = int(max_degree)
+
+    block = ShardPlan.block
+    owned = ShardPlan.owned
+
+
+class CudaShard:
+    """Product backend: this rank's shard on its GPU through the C-ABI.
+
+    Built on the device from a device graph (``full``: an
+    engine.DeviceGraph or generators.DeviceResidentGraph on this rank's GPU)
+    with kb_graph_create_shard, or -- the host protocol the lockstep tests
+    use -- from a ShardPlan's host CSR slice."""
+
+    def __init__(self, plan, rank: int, indptr=None, indices=None, *, device: int,
                  alpha: float, gamma: float, crit: Criterion, undirected: bool,
-                 max_iterations: int, symmetric: bool = True, split_threshold: int = 0,
-                 local_csr=None, fused: bool = False):
+                 max_iterations: int, symmetric: bool = False, split_threshold: int = 0,
+                 local_csr=None, fused: bool = False, full=None):
         import torch
         self.torch = torch
         self.L = _lib.lib()
         self.plan, self.rank, self.device = plan, rank, device
-        # local_csr: this rank's plan.local_csr(...) computed ahead (bench e2e)
-        ip, ix = local_csr if local_csr is not None else plan.local_csr(indptr, indices, rank)
-        lab = plan.labels()
-        lo, hi = plan.block(rank)
-        flags = _lib.KB_GRAPH_NO_RELABEL | (_lib.KB_GRAPH_SYMMETRIC if symmetric else 0)
         h = ctypes.c_void_p()
         # split_threshold 0 keeps the single-GPU segmentation (2048 arcs), so
         # the shards reproduce the one-GPU bounds bit for bit; a finer split
         # (fast_split(P)) shortens the kernel tail when the per-rank work is
         # small, at the cost of rounding-level (<= 1e-12) differences
-        _lib.check(self.L.kb_graph_create_ex(device, ip.size - 1, int(ip[-1]), _lib.ptr(ip),
-                                             _lib.ptr(ix), split_threshold, -1, flags,
-                                             _lib.ptr(lab), lo, hi, ctypes.byref(h)))
+        if full is not None:
+            fh = full.handle if hasattr(full, "handle") else full.device_graph.handle
+            n_per, owned = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(self.L.kb_graph_create_shard(fh, plan.P, rank, split_threshold, -1,
+                                                    ctypes.byref(h), ctypes.byref(n_per),
+                                                    ctypes.byref(owned)))
+            assert (int(n_per.value), int(owned.value)) == (plan.n_per, plan.owned(rank))
+        else:
+            # local_csr: this rank's plan.local_csr(...) computed ahead
+            ip, ix = (local_csr if local_csr is not None
+                      else plan.local_csr(indptr, indices, rank))
+            lab = plan.labels()
+            lo, hi = plan.block(rank)
+            # the symmetric flag is the caller's verified claim about the
+            # whole graph (sharded_run checks it before building shards)
+            flags = _lib.KB_GRAPH_NO_RELABEL | (_lib.KB_GRAPH_SYMMETRIC if symmetric else 0)
+            _lib.check(self.L.kb_graph_create_ex(device, ip.size - 1, int(ip[-1]), _lib.ptr(ip),
+                                                 _lib.ptr(ix), split_threshold, -1, flags,
+                                                 _lib.ptr(lab), lo, hi, ctypes.byref(h)))
         self.g = h
         # fused exchange: K1 stores omega into every rank's level buffers
         # (exchange_connect); no per-iteration all-gather
@@ -472,35 +504,80 @@ def connect_shard(make_shard, dist, rank: int, world: int, device, fused: bool =
     return make_shard(False), f"nccl-allgather (fused exchange unavailable: {err})"
 
 
-def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = True,
-                alpha: float | None = None, max_iterations: int | None = None,
-                device: int | None = None, backend_factory=None,
-                fused: bool = True) -> RankingResult:
-    """Certify `crit` on the graph (canonical CSR on every rank's host) with
-    the current torch.distributed group, one GPU per rank."""
-    import torch.distributed as dist
-    rank, world = dist.get_rank(), dist.get_world_size()
-    plan = ShardPlan(indptr, world)
-    d = plan.max_degree
+def _validate(n: int, d: int, crit: Criterion, alpha, max_iterations):
+    """engine.init's checks (engine.py:248-283) for a sharded run."""
+    if n < 1:
+        raise ParameterError("graph must have at least one node")
     if alpha is None:
         alpha = 1.0 / (1.0 + d) if d > 0 else 0.5      # engine.py:96-99
+    alpha = float(alpha)
     validate_alpha(alpha, d)
+    if crit.kind == TOPK and crit.k > n:
+        raise ParameterError(f"topk k={crit.k} exceeds node count {n}")
+    if crit.kind == PAIR and (crit.u >= n or crit.v >= n):
+        raise ParameterError("pair criterion names a node outside the graph")
     gamma = tail_gamma(alpha, d)
     if max_iterations is None:
         max_iterations = default_iteration_cap(alpha, d, crit.epsilon)
-    if backend_factory is None:
-        dev = rank if device is None else device
+    elif max_iterations < 1:
+        raise ParameterError("max_iterations must be >= 1")
+    return alpha, gamma, int(max_iterations)
 
-        def make(fz):
-            return CudaShard(plan, rank, indptr, indices, device=dev, alpha=alpha, gamma=gamma,
-                             crit=crit, undirected=undirected, max_iterations=max_iterations,
-                             fused=fz)
-        backend, _mode = connect_shard(make, dist, rank, world, f"cuda:{dev}", fused)
-        backend.collective_device = f"cuda:{dev}"
-    else:
+
+def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = False,
+                alpha: float | None = None, max_iterations: int | None = None,
+                device: int | None = None, backend_factory=None,
+                fused: bool = True, graph=None) -> RankingResult:
+    """engine.init + engine.run (engine.py:248-283, :382-396) of `crit` on the
+    graph with the current torch.distributed group, one GPU per rank.
+
+    The graph is the canonical CSR on every rank's host (uploaded to the
+    rank's GPU, where the symmetry test runs during the upload and the
+    rank's shard is cut out on the device), or ``graph``: a device graph
+    already on this rank's GPU (engine.DeviceGraph, or a generators graph).
+    undirected=True requires a symmetric arc set (ParameterError otherwise),
+    as in engine.init."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if backend_factory is not None:                  # host protocol (CPU tests)
+        plan = ShardPlan(indptr, world)
+        n, d = plan.n, plan.max_degree
+        if undirected:
+            ip = np.asarray(indptr, dtype=np.int64)
+            rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+            cols = np.asarray(indices, dtype=np.int64)
+            if not np.array_equal(np.sort(rows * n + cols), np.sort(cols * n + rows)):
+                raise ParameterError("undirected mode requires a symmetric arc set")
+        alpha, gamma, max_iterations = _validate(n, d, crit, alpha, max_iterations)
         backend = backend_factory(plan, rank, alpha, gamma)
+        return ShardedRun(backend, plan, crit, rank=rank, world=world,
+                          max_iterations=max_iterations).run()
+    from .engine import DeviceGraph
+    dev = rank if device is None else device
+    full = graph
+    own_full = full is None
+    if own_full:
+        full = DeviceGraph(indptr, indices, device=dev)
+    dg = full if hasattr(full, "handle") else full.device_graph
+    info = dg.info()
+    n, d = int(info.n), int(info.max_out_degree)
+    alpha, gamma, max_iterations = _validate(n, d, crit, alpha, max_iterations)
+    if undirected and not dg.is_symmetric():
+        raise ParameterError("undirected mode requires a symmetric arc set")
+    plan = DevicePlan(n, world, d)
+
+    def make(fz):
+        return CudaShard(plan, rank, device=dev, alpha=alpha, gamma=gamma, crit=crit,
+                         undirected=undirected, max_iterations=max_iterations, fused=fz,
+                         full=dg)
+    try:
+        backend, _mode = connect_shard(make, dist, rank, world, f"cuda:{dev}", fused)
+    finally:
+        if own_full:
+            full.close()
+    backend.collective_device = f"cuda:{dev}"
     return ShardedRun(backend, plan, crit, rank=rank, world=world,
                       max_iterations=max_iterations).run()
 
 
-__all__ = ["ShardPlan", "CudaShard", "ShardedRun", "sharded_run", "connect_shard", "fast_split"]
+__all__ = ["ShardPlan", "DevicePlan", "CudaShard", "ShardedRun", "sharded_run", "connect_shard", "fast_split"]

@@ -68,6 +68,7 @@ def update_batch(state: KatzState, g, batch: EdgeBatch, *, theta: float = 0.5) -
 
     ins, dels = (np.ascontiguousarray(a) for a in batch.arrays())
     stats_c = _lib.UpdateStatsC()
+    dev_version = state.device_graph.info().version
     state._touch()
     st = state._L.kb_update_batch(state._h, _lib.ptr(ins), ins.shape[0],
                                   _lib.ptr(dels), dels.shape[0], float(theta),
@@ -91,11 +92,46 @@ def update_batch(state: KatzState, g, batch: EdgeBatch, *, theta: float = 0.5) -
         stats = UpdateStats(
             batch_size=int(stats_c.batch_size), seeds=int(stats_c.seeds),
             visited=int(stats_c.visited),
-            level_sizes=[int(x) for x in stats_c.level_sizes[:stats_c.n_level_sizes]],
+            level_sizes=_level_sizes(state, stats_c),
             reactivated=int(stats_c.reactivated),
             aborted_level=None if stats_c.aborted_level < 0 else int(stats_c.aborted_level),
             resumed_iterations=int(stats_c.resumed_iterations))
         state.last_update_stats = stats
+    else:
+        # failed (out of memory, a CUDA error) possibly after the device had
+        # applied the batch to its CSR: the state's levels may be half
+        # repaired, so it refuses further use (StateError); a device copy
+        # that changed no longer matches the host graph's version and is
+        # dropped from every cache -- unless the device copy *is* the graph
+        # (generators.DeviceResidentGraph), which then records the new arcs
+        dg = state.device_graph
+        if dg.info().version != dev_version:
+            if hasattr(g, "_note_device_update"):
+                g._note_device_update()
+            else:
+                _forget_device_graph(g, dg)
+        state.graph_version = -1
     if st == _lib.KB_ECONVERGENCE:
         raise ConvergenceError(_lib.last_error(), iterations=state.r, gap=state.gap())
     _lib.check(st)
+
+
+def _level_sizes(state: KatzState, stats_c) -> list[int]:
+    """UpdateStats.level_sizes, all of it: the C struct carries the first 64."""
+    n = int(stats_c.n_level_sizes)
+    if n <= 64:
+        return [int(x) for x in stats_c.level_sizes[:n]]
+    out = np.empty(n, dtype=np.int64)
+    cnt = ctypes.c_int64()
+    _lib.check(state._L.kb_update_level_sizes(state._h, _lib.ptr(out), n, ctypes.byref(cnt)))
+    return [int(x) for x in out[:int(cnt.value)]]
+
+
+def _forget_device_graph(g, dg) -> None:
+    if hasattr(g, "_device"):
+        cached = g._device
+        if cached is not None and cached[1] is dg:
+            g._device = None
+        return
+    from .engine import _FOREIGN_CACHE
+    _FOREIGN_CACHE[:] = [e for e in _FOREIGN_CACHE if e[2] is not dg]

@@ -14,8 +14,8 @@ import numpy as np
 
 from . import _lib
 from .engine import DeviceGraph
-from .errors import BatchPreconditionError, NodeRangeError, ParameterError
-from .graph import EdgeBatch
+from .errors import NodeRangeError, ParameterError
+from .graph import EdgeBatch, check_batch_arcs
 
 
 class DeviceResidentGraph:
@@ -128,15 +128,9 @@ class DeviceResidentGraph:
 
     # ---- mutation (graph.py:201-237)
     def validate_batch(self, batch: EdgeBatch) -> None:
+        """graph.py:207-220 (presence tested on the device)."""
         batch.validate_shape()
-        i, d = (self._arcs(a) for a in batch.arrays())
-        pi, pd = self._present(i), self._present(d)
-        if pi.any():
-            u, v = batch.insertions[int(np.argmax(pi))]
-            raise BatchPreconditionError(f"cannot insert arc ({u}, {v}): already present")
-        if not pd.all():
-            u, v = batch.deletions[int(np.argmin(pd))]
-            raise BatchPreconditionError(f"cannot delete arc ({u}, {v}): not present")
+        check_batch_arcs(batch, self.node_count, self._check_node, self._present)
 
     def _apply(self, ins, dels):
         i, d = self._arcs(ins), self._arcs(dels)

@@ -26,6 +26,39 @@ Arc = tuple[int, int]
 MAX_NODE_ID = 2**31 - 1   # graph.py:27
 
 
+def check_batch_arcs(batch: "EdgeBatch", n: int, check_node, present) -> None:
+    """The per-arc checks of Graph.validate_batch (graph.py:207-220) in the
+    reference's order -- insertions, then deletions; per arc, the range of
+    u, of v, then presence -- vectorised: the first arc that fails any test
+    raises that test's error.  present((m, 2) int64 in-range arcs) -> bool[m]."""
+    try:
+        arrays = batch.arrays()
+    except OverflowError:
+        arrays = None
+    if arrays is None:              # ids beyond int64: the exact per-arc path
+        for u, v in batch.insertions + batch.deletions:
+            check_node(u)
+            check_node(v)
+        return
+    for a, arcs, want, msg in ((arrays[0], batch.insertions, False, "already present"),
+                               (arrays[1], batch.deletions, True, "not present")):
+        if not a.shape[0]:
+            continue
+        bad = ((a < 0) | (a >= n)).any(axis=1)
+        fault = bad.copy()
+        ok = ~bad
+        if ok.any():
+            fault[ok] = present(np.ascontiguousarray(a[ok])) != want
+        if fault.any():
+            i = int(np.argmax(fault))
+            u, v = arcs[i]
+            if bad[i]:
+                check_node(u)
+                check_node(v)
+            verb = "insert" if not want else "delete"
+            raise BatchPreconditionError(f"cannot {verb} arc ({u}, {v}): {msg}")
+
+
 @dataclass
 class EdgeBatch:
     """Arc insertions and deletions applied as one unit (graph.py:30-68)."""
@@ -284,32 +317,9 @@ class Graph:
     def validate_batch(self, batch: EdgeBatch) -> None:
         """graph.py:207-220."""
         batch.validate_shape()
-        try:
-            ia, da = batch.arrays()
-        except OverflowError:
-            ia = da = None
-        if ia is None:
-            for u, v in batch.insertions + batch.deletions:
-                self._check_node(u)
-                self._check_node(v)
-        else:
-            for a in (ia, da):      # first offending id in (u, v) order
-                bad = (a < 0) | (a >= self._n)
-                if bad.any():
-                    self._check_node(int(a[bad][0]))
         n = self._n
-        if batch.insertions:
-            present = self._has_keys(ia[:, 0] * n + ia[:, 1])
-            if present.any():
-                u, v = batch.insertions[int(np.argmax(present))]
-                raise BatchPreconditionError(
-                    f"cannot insert arc ({u}, {v}): already present")
-        if batch.deletions:
-            present = self._has_keys(da[:, 0] * n + da[:, 1])
-            if not present.all():
-                u, v = batch.deletions[int(np.argmin(present))]
-                raise BatchPreconditionError(
-                    f"cannot delete arc ({u}, {v}): not present")
+        check_batch_arcs(batch, n, self._check_node,
+                         lambda a: self._has_keys(a[:, 0] * n + a[:, 1]))
 
     def insert_arcs(self, arcs: Sequence[Arc], _validated: bool = False) -> None:
         if not _validated:

@@ -146,7 +146,8 @@ def _worker(rank, world, port, case, q):
         def factory(plan, rk, alpha, gamma):
             return OracleShard(plan, rk, g.indptr, g.indices, alpha, gamma, crit, True)
 
-        res = sharded_run(g.indptr, g.indices, crit, backend_factory=factory)
+        res = sharded_run(g.indptr, g.indices, crit, backend_factory=factory,
+                          undirected=True)
         q.put((rank, res.iterations_used, np.asarray(res.order), np.asarray(res.lower),
                np.asarray(res.upper), res.separated_fraction))
     finally:
@@ -282,3 +283,49 @@ def test_connect_shard_ranks_agree_on_the_exchange(stage):
         assert all(o[3] == world - 1 for o in out)
     else:
         assert fused == {False} and modes == {"nccl-allgather"}
+
+
+def _guard_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    try:
+        g = O.rmat_graph(1024, edge_factor=8, seed=5)
+        d = O.CSRGraph.from_edges(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5)])
+        crit = Criterion.top_k(3, 1e-9)
+
+        def factory(plan, rk, alpha, gamma):
+            raise AssertionError("no shard may be built for a rejected run")
+
+        for ip, ix, c, kw in [(d.indptr, d.indices, crit, dict(undirected=True)),
+                              (g.indptr, g.indices, Criterion.top_k(1025), {}),
+                              (g.indptr, g.indices, crit, dict(max_iterations=0))]:
+            try:
+                sharded_run(ip, ix, c, backend_factory=factory, **kw)
+                out.append("ran")
+            except Exception as e:          # noqa: BLE001
+                out.append(type(e).__name__ + ":" + str(e))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_run_applies_engine_init_guards():
+    """engine.init's guards (engine.py:257-283) on a sharded run, world 2:
+    undirected on an asymmetric arc set, k > n and max_iterations < 1 raise
+    ParameterError on every rank before any shard is built."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_guard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, out in outs:
+        assert out[0].startswith("ParameterError:") and "symmetric" in out[0]
+        assert out[1].startswith("ParameterError:") and "exceeds" in out[1]
+        assert out[2].startswith("ParameterError:") and "max_iterations" in out[2]

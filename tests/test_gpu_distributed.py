@@ -19,16 +19,21 @@ torch = pytest.importorskip("torch")
 from paper_1807_03847_b200 import distributed as D  # noqa: E402
 
 
-def _lockstep(g0, crit, world, protocol="device", split=0, fused=False):
+def _lockstep(g0, crit, world, protocol="device", split=0, fused=False, build="host"):
+    """build="device": every shard is cut out of one device graph on the GPU
+    (kb_graph_create_shard) instead of from the plan's host CSR slice."""
     plan = D.ShardPlan(g0.indptr, world)
     d = plan.max_degree
     alpha = 1.0 / (1.0 + d)
     gamma = P.tail_gamma(alpha, d)
     cap = P.default_iteration_cap(alpha, d, crit.epsilon)
+    full = P.DeviceGraph(g0.indptr, g0.indices, device=0) if build == "device" else None
     shards = [D.CudaShard(plan, rk, g0.indptr, g0.indices, device=0, alpha=alpha,
                           gamma=gamma, crit=crit, undirected=True, max_iterations=cap,
-                          split_threshold=split, fused=fused)
+                          split_threshold=split, fused=fused, full=full)
               for rk in range(world)]
+    if full is not None:
+        full.close()
     if fused:                                 # peers are buffers in this process
         exports = [s.exchange_export() for s in shards]
         for s in shards:
@@ -111,15 +116,20 @@ def _lockstep(g0, crit, world, protocol="device", split=0, fused=False):
     return r, order, lower, upper, pairs
 
 
-@pytest.mark.parametrize("world,protocol,fused", [(1, "device", False), (2, "device", False),
-                                                  (3, "device", False), (2, "host", False),
-                                                  (2, "device", True), (3, "host", True)])
-def test_cuda_shards_equal_single_gpu(world, protocol, fused):
+@pytest.mark.parametrize("world,protocol,fused,build",
+                         [(1, "device", False, "host"), (2, "device", False, "host"),
+                          (3, "device", False, "host"), (2, "host", False, "host"),
+                          (2, "device", True, "host"), (3, "host", True, "host"),
+                          (1, "device", False, "device"), (3, "device", False, "device"),
+                          (4, "device", True, "device")])
+def test_cuda_shards_equal_single_gpu(world, protocol, fused, build):
     """fused: K1 stores omega straight into the other shards' level buffers
-    (the NVLink exchange), no all-gather."""
+    (the NVLink exchange), no all-gather.  build="device": shards cut out of
+    a device graph on the GPU (kb_graph_create_shard)."""
     g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
     crit = P.Criterion.top_k(100, 1e-6)
-    r, order, lower, upper, pairs = _lockstep(g0, crit, world, protocol, fused=fused)
+    r, order, lower, upper, pairs = _lockstep(g0, crit, world, protocol, fused=fused,
+                                              build=build)
     g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
     res = P.run(P.init(g, crit, undirected=True), g)
     assert r == res.iterations_used
@@ -250,7 +260,21 @@ def test_sharded_run_one_rank_nccl_speculative():
     try:
         g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
         crit = P.Criterion.top_k(100, 1e-6)
-        res = D.sharded_run(g0.indptr, g0.indices, crit, device=0)
+        res = D.sharded_run(g0.indptr, g0.indices, crit, device=0, undirected=True)
+        # engine.init's guards (engine.py:257-283) hold for sharded runs too
+        # drop row 0's last arc: its reversal stays, so the set is asymmetric
+        cut = int(g0.indptr[1]) - 1
+        ix_bad = np.delete(g0.indices, cut)
+        ip_bad = g0.indptr.copy()
+        ip_bad[1:] -= 1
+        with pytest.raises(P.ParameterError, match="symmetric"):
+            D.sharded_run(ip_bad, ix_bad, crit, device=0, undirected=True)
+        with pytest.raises(P.ParameterError, match="exceeds"):
+            D.sharded_run(g0.indptr, g0.indices, P.Criterion.top_k(g0.node_count + 1),
+                          device=0, undirected=True)
+        with pytest.raises(P.ParameterError, match="max_iterations"):
+            D.sharded_run(g0.indptr, g0.indices, crit, device=0, undirected=True,
+                          max_iterations=0)
     finally:
         dist.destroy_process_group()
     g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
