@@ -1161,42 +1161,23 @@ int kb_run(kb_state *h, int *converged) {
         use_device(s.g->device);
         *converged = 0;
         cudaStream_t st = s.g->stream;
-        // TOPK: queue K1 of r+1 behind check r, so the GPU does not idle
-        // through the check's host read; that K1 exits at once on the device
-        // if check r converged, and the host then rolls the level back
+        // TOPK: the loop runs on the device (topk_run_device): levels of K1 +
+        // check are queued back to back, each check's count feeding the next,
+        // and a converged check stops everything queued behind it
         const bool spec = s.kind == KB_TOPK && s.k <= 4096 && s.keep_all &&
                           tune_get("run.speculate", 1);
         if (spec) {
             check_version(s);
-            launch_iterate(s, st);
-            for (;;) {
-                const int nxt = topk_check_enqueue(s, st);
-                const bool ahead = s.r < s.max_iter;
-                if (ahead) {
-                    s.spec_abort = true;
-                    launch_iterate(s, st);
-                    s.spec_abort = false;
-                }
-                KB_CUDA(cudaEventSynchronize(s.chk_ev));
-                if (topk_check_finish(s, nxt)) {
-                    if (ahead) {                      // the queued K1 did nothing
-                        s.levels.pop_back();
-                        s.r -= 1;
-                        if (s.k1_used >= 2) s.k1_used -= 2;
-                    }
-                    *converged = 1;
-                    break;
-                }
-                if (!ahead) {
-                    const double gap = run_gap(s, st);
-                    char buf[160];
-                    snprintf(buf, sizeof buf,
-                             "stopping rule still unmet after %lld iterations (widest bound "
-                             "interval %.3e)", (long long)s.r, gap);
-                    throw Error{KB_ECONVERGENCE, buf};
-                }
+            if (topk_run_device(s, st)) {
+                *converged = 1;
+                return;
             }
-            return;
+            const double gap = run_gap(s, st);
+            char buf[160];
+            snprintf(buf, sizeof buf,
+                     "stopping rule still unmet after %lld iterations (widest bound "
+                     "interval %.3e)", (long long)s.r, gap);
+            throw Error{KB_ECONVERGENCE, buf};
         }
         // RANKING: while a cached refuting pair still refutes (95 of C4's 99
         // checks) the check is one tiny kernel; K1 of r+1 is queued behind it

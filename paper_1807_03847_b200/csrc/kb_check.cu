@@ -59,8 +59,22 @@ struct TopkArgs {
     uint64_t *stK;                  // staged keys / uppers / ids (non-dense sets)
     double *stU;
     int32_t *stI;
-    unsigned long long *out;        // [0]=new m, [1]=converged, [2]=#prefix
+    unsigned long long *out;        // [0]=new m, [1]=converged, [2]=#prefix, [3]=kstar,
+                                    // [4]=istar, [5]=winners, [6]=survivors, [7]=m in
+    // device-driven runs: m is read from *m_dev (the previous check's count)
+    // and this launch only acts when m_lo < m <= m_hi (one launch per grid
+    // size; the others exit), and not at all once *abort (converged) is set
+    const unsigned long long *m_dev = nullptr;
+    int64_t m_lo = -1, m_hi = INT64_MAX;
+    const unsigned long long *abort = nullptr;
+    // fused split: winners -> prefix_buf, survivors -> act_out + k, in
+    // active-set order, counts into out[0], out[2], out[5], out[6]
+    int split = 0;
 };
+
+__device__ __forceinline__ bool flag_set(const unsigned long long *f) {
+    return f && *(const volatile unsigned long long *)f != 0;
+}
 
 // digit plan: two 12-bit digits over all elements, then the survivors of the
 // 24-bit prefix are compacted and five 8-bit digits finish on them; ties at
@@ -115,14 +129,40 @@ __device__ __forceinline__ void select_digit(unsigned int *sh, const unsigned in
 }
 
 constexpr int UNR = 4;  // elements per thread per tile (memory-level parallelism)
+constexpr int CSORT = 2048;  // candidate sets up to this size are sorted in shared memory
+
+// Block-wide bitonic sort of P (a power of two) (key, label) pairs ascending,
+// carrying x when given.  Callers pad with (~0, ~0).
+__device__ __forceinline__ void bitonic_kl(uint64_t *key, uint32_t *lab, int32_t *x, int P) {
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool gt = key[i] > key[j] || (key[i] == key[j] && lab[i] > lab[j]);
+                    if (gt == up) {
+                        const uint64_t tk = key[i]; key[i] = key[j]; key[j] = tk;
+                        const uint32_t tl = lab[i]; lab[i] = lab[j]; lab[j] = tl;
+                        if (x) { const int32_t tx = x[i]; x[i] = x[j]; x[j] = tx; }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
 
 __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
+    if (flag_set(A.abort)) return;
+    const int64_t m = A.m_dev ? (int64_t)*(const volatile unsigned long long *)A.m_dev : A.m;
+    if (m <= A.m_lo || m > A.m_hi) return;     // another launch's size class
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned int sh[4096];
     const int64_t G = gridDim.x;
     const int64_t TILE = (int64_t)CHK_THREADS * UNR;
-    const int64_t chunk = ((A.m + G - 1) / G + TILE - 1) / TILE * TILE;
-    const int64_t i0 = min(A.m, blockIdx.x * chunk), i1 = min(A.m, i0 + chunk);
+    const int64_t chunk = ((m + G - 1) / G + TILE - 1) / TILE * TILE;
+    const int64_t i0 = min(m, blockIdx.x * chunk), i1 = min(m, i0 + chunk);
     unsigned long long *ncand = A.blk + 2 * G;
     // Element views: dense -> lower/upper by position; otherwise the active
     // ids are first staged into contiguous key/upper/id arrays so that every
@@ -136,6 +176,11 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
     }
     grid.sync();
 
+    // with m <= k every element is a winner (engine.py:361-363): kstar = 0,
+    // istar = max admits every key >= +0
+    uint64_t kstar = 0;
+    uint32_t istar = 0xFFFFFFFFu;
+    if (m > A.k) {
     // ---- 1a. two 12-bit digits over the whole active set
     uint64_t prefix = 0, mask = 0;
     int64_t kk = A.k;
@@ -191,6 +236,30 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
     }
     grid.sync();
     const int64_t nc = (int64_t)*ncand;
+    if (nc <= CSORT) {
+        // few keys carry the 24-bit prefix (the usual case): every block
+        // sorts them by (-key, label) in shared memory and reads the cut at
+        // rank kk -- no further grid-wide digit passes
+        __shared__ uint64_t ck[CSORT];
+        __shared__ uint32_t cl[CSORT];
+        int P = 1;
+        while (P < nc) P <<= 1;
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+            if (i < nc) {
+                const int32_t id = id_at(A.cand[i]);
+                ck[i] = ~key_of(A.lower, id);
+                cl[i] = (uint32_t)A.perm[id];
+            } else {
+                ck[i] = ~0ull;
+                cl[i] = 0xFFFFFFFFu;
+            }
+        }
+        __syncthreads();
+        bitonic_kl(ck, cl, nullptr, P);
+        kstar = ~ck[kk - 1];
+        istar = cl[kk - 1];
+        __syncthreads();
+    } else {
     const int64_t cchunk = (nc + G - 1) / G;
     const int64_t c0 = min(nc, blockIdx.x * cchunk), c1 = min(nc, c0 + cchunk);
     // ---- 1c. five 8-bit digits over the candidates
@@ -216,11 +285,10 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
         prefix |= (uint64_t)sel << shift;
         mask |= (uint64_t)0xFF << shift;
     }
-    const uint64_t kstar = prefix;
+    kstar = prefix;
     const int64_t count_eq = A.hist[2 * 4096 + 4 * 256 + (int)(kstar & 255)];
 
     // ---- 2. ties at the cut: the kk smallest original ids among key == kstar
-    uint32_t istar = 0xFFFFFFFFu;
     if (kk < count_eq) {
         uint32_t ipre = 0, imask = 0;
         int64_t need = kk;
@@ -252,9 +320,107 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
         }
         istar = ipre;
     }
+    }   // nc > CSORT
+    }   // m > k
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         A.out[3] = kstar;
         A.out[4] = istar;
+    }
+    if (!A.split) return;
+
+    // ---- 3. the split (engine.py:359-373), fused: winners (the k best by
+    // (-lower, id)) to prefix_buf, survivors (the rest with fl(upper - eps) >=
+    // threshold) to act_out + k, both in active-set order.  Each warp owns a
+    // contiguous run of the block's chunk: pass A classifies its elements
+    // (loads kept in flight, one class byte each, reusing the candidate
+    // buffer) and counts them with ballots; one grid barrier publishes the
+    // block counts; pass B streams the class bytes and ids and writes every
+    // kept id at its rank (ballot + popc), so nothing is gathered twice.
+    const double thr = __longlong_as_double((long long)kstar);
+    uint8_t *cls = (uint8_t *)A.cand;
+    constexpr int NW = CHK_THREADS / 32;
+    __shared__ unsigned long long s_wcnt[NW];
+    __shared__ unsigned long long s_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t sub = ((i1 - i0 + NW - 1) / NW + 31) / 32 * 32;
+    const int64_t a_w = min(i1, i0 + warp * sub), b_w = min(i1, a_w + sub);
+    unsigned long long wc = 0;                 // (winners << 32) | survivors
+    for (int64_t t = a_w; t < b_w; t += 4 * 32) {
+        int32_t id[4];
+        uint64_t key[4];
+        double up[4];
+        bool in[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int64_t i = t + q * 32 + lane;
+            in[q] = i < b_w;
+            id[q] = in[q] ? id_at(i) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            key[q] = in[q] ? key_of(A.lower, id[q]) : 0;
+            up[q] = (in[q] && key[q] <= kstar) ? A.upper[id[q]] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint8_t c = 0;
+            if (in[q]) {
+                if (key[q] > kstar || (key[q] == kstar && (uint32_t)A.perm[id[q]] <= istar))
+                    c = 2;
+                else if (__dsub_rn(up[q], A.eps) >= thr)
+                    c = 1;
+                cls[t + q * 32 + lane] = c;
+            }
+            const unsigned bw = __ballot_sync(0xffffffffu, c == 2);
+            const unsigned bs = __ballot_sync(0xffffffffu, c == 1);
+            wc += ((unsigned long long)__popc(bw) << 32) + (unsigned long long)__popc(bs);
+        }
+    }
+    if (lane == 0) s_wcnt[warp] = wc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < NW; w++) tot += s_wcnt[w];
+        A.blk[blockIdx.x] = tot;
+    }
+    grid.sync();
+    if (threadIdx.x < 32) {                    // this block's base and the grid total
+        unsigned long long before = 0, total = 0;
+        for (int64_t b = threadIdx.x; b < G; b += 32) {
+            const unsigned long long c = A.blk[b];
+            total += c;
+            if (b < blockIdx.x) before += c;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            before += __shfl_down_sync(0xffffffffu, before, o);
+            total += __shfl_down_sync(0xffffffffu, total, o);
+        }
+        if (threadIdx.x == 0) {
+            s_base = before;
+            if (blockIdx.x == 0) {
+                const unsigned long long W = total >> 32, S = total & 0xFFFFFFFFull;
+                A.out[0] = W + S;       // |active| after the cut
+                A.out[2] = W;           // winners in the prefix buffer
+                A.out[5] = W;
+                A.out[6] = S;
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long base = s_base;
+    for (int w = 0; w < warp; w++) base += s_wcnt[w];
+    unsigned long long ow = base >> 32, os = base & 0xFFFFFFFFull;
+    for (int64_t t = a_w; t < b_w; t += 32) {
+        const int64_t i = t + lane;
+        const bool in = i < b_w;
+        const uint8_t c = in ? cls[i] : 0;
+        const unsigned bw = __ballot_sync(0xffffffffu, c == 2);
+        const unsigned bs = __ballot_sync(0xffffffffu, c == 1);
+        if (c == 2) A.prefix_buf[ow + __popc(bw & lt)] = id_at(i);
+        else if (c == 1) A.act_out[A.k + (int64_t)(os + __popc(bs & lt))] = id_at(i);
+        ow += __popc(bw);
+        os += __popc(bs);
     }
 }
 
@@ -280,18 +446,18 @@ struct IsSurvivor {
     }
 };
 
-__global__ void k_cut_counts(unsigned long long *out, int64_t k) {
-    out[0] = (unsigned long long)k + out[6];  // |active| after the cut
-    out[2] = (unsigned long long)k;           // winners in the prefix buffer
-}
-
 // Sort the prefix by (-lower, original id), write it to act_out[0..cnt), and
 // evaluate the stopping rule.  One block; cnt <= KMAX.
 __global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const double *upper,
                                                       const int32_t *perm, const int32_t *src,
                                                       int dense_src, int32_t *act_out,
                                                       unsigned long long *out, double eps,
-                                                      int64_t k) {
+                                                      int64_t k,
+                                                      const unsigned long long *abort = nullptr,
+                                                      const unsigned long long *m_dev = nullptr,
+                                                      int64_t m_min = -1) {
+    if (flag_set(abort)) return;
+    if (m_dev && (int64_t)*(const volatile unsigned long long *)m_dev <= m_min) return;
     extern __shared__ unsigned char smem[];
     const int64_t cnt = (int64_t)out[2];
     const int64_t mnew = (int64_t)out[0];
@@ -339,6 +505,90 @@ __global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const
     }
     __syncthreads();
     if (threadIdx.x == 0) out[1] = (mnew <= k) && !bad;
+}
+
+// The whole TOPK check for a small active set (m <= SMALL_M, the last
+// iterations of every R-MAT run: C2 ends at |active| 254 -> 100) in one
+// block: the set is sorted by (-lower, label) in shared memory, the first
+// min(m, k) are the sorted prefix (engine.py:359-366), the cut is read off,
+// survivors are compacted in active-set order (engine.py:367-373) and the
+// stopping rule is evaluated (engine.py:374-378).  Writes out[0..2] like
+// k_topk_select + k_topk_finish.
+__global__ void __launch_bounds__(1024) k_topk_small(const double *lower, const double *upper,
+                                                     const int32_t *perm, const int32_t *act_in,
+                                                     int dense, int64_t m_host,
+                                                     const unsigned long long *m_dev, int64_t m_max,
+                                                     int32_t *act_out, unsigned long long *out,
+                                                     double eps, int64_t k,
+                                                     const unsigned long long *abort) {
+    if (flag_set(abort)) return;
+    const int64_t m = m_dev ? (int64_t)*(const volatile unsigned long long *)m_dev : m_host;
+    if (m > m_max) return;
+    if (m == 0) {
+        if (threadIdx.x == 0) { out[0] = 0; out[1] = 1; out[2] = 0; }
+        return;
+    }
+    extern __shared__ unsigned char smem[];
+    int P = 1;
+    while (P < m) P <<= 1;
+    uint64_t *key = (uint64_t *)smem;
+    uint32_t *lab = (uint32_t *)(key + P);
+    int32_t *nid = (int32_t *)(lab + P);
+    __shared__ unsigned int s_cnt[32];
+    __shared__ int bad;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < m) {
+            const int32_t id = dense ? i : act_in[i];
+            key[i] = ~key_of(lower, id);
+            lab[i] = (uint32_t)perm[id];
+            nid[i] = id;
+        } else {
+            key[i] = ~0ull;
+            lab[i] = 0xFFFFFFFFu;
+            nid[i] = -1;
+        }
+    }
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    bitonic_kl(key, lab, nid, P);
+    const int64_t W = m < k ? m : k;
+    const uint64_t kstar = ~key[W - 1];
+    const uint32_t istar = lab[W - 1];
+    const double thr = __longlong_as_double((long long)kstar);
+    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) {
+        act_out[i] = nid[i];
+        if (i >= 1 && !(__dsub_rn(upper[nid[i]], eps) < lower[nid[i - 1]])) bad = 1;
+    }
+    // survivors, in active-set order
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t base = W;
+    for (int64_t t = 0; t < (m > k ? m : 0); t += blockDim.x) {
+        const int64_t i = t + threadIdx.x;
+        bool sv = false;
+        int32_t id = 0;
+        if (i < m) {
+            id = dense ? (int32_t)i : act_in[i];
+            const uint64_t kx = key_of(lower, id);
+            const bool win = kx > kstar || (kx == kstar && (uint32_t)perm[id] <= istar);
+            sv = !win && __dsub_rn(upper[id], eps) >= thr;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, sv);
+        if (lane == 0) s_cnt[warp] = __popc(b);
+        __syncthreads();
+        int64_t off = base;
+        for (int w = 0; w < warp; w++) off += s_cnt[w];
+        if (sv) act_out[off + __popc(b & ((1u << lane) - 1u))] = id;
+        int64_t tile = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) tile += s_cnt[w];
+        base += tile;
+        __syncthreads();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = (unsigned long long)base;          // |active| after the cut
+        out[1] = (base <= k) && !bad;
+        out[2] = (unsigned long long)W;
+    }
 }
 
 // ---------------------------------------------------------------- reductions
@@ -1044,98 +1294,135 @@ bool run_check(State &s, cudaStream_t st) {
 }
 
 namespace {
-// the check's verdict: abort flag for a speculative K1 queued behind, that
-// K1's work counter reset, and the three result words written straight
-// into page-locked host memory (no separate copy)
-__global__ void k_publish(const unsigned long long *out, unsigned long long *abort,
-                          unsigned long long *k1_counter, volatile unsigned long long *host) {
+// the check's verdict: abort flag for the K1s queued behind (they exit when
+// it is set), that K1's work counter reset, the new |active| as the next
+// check's input, and the result words written straight into page-locked
+// host memory (no separate copy).  A check behind a converged one does
+// nothing (its inputs are stale): the host words keep the converged check's.
+__global__ void k_publish(unsigned long long *out, unsigned long long *abort,
+                          unsigned long long *k1_counter, volatile unsigned long long *host,
+                          int64_t level) {
+    if (*(volatile unsigned long long *)abort) return;
     *abort = out[1];
     *k1_counter = 0ull;
+    out[7] = out[0];
     host[0] = out[0];
     host[1] = out[1];
     host[2] = out[2];
+    host[3] = (unsigned long long)level;
     __threadfence_system();
 }
+
+// size classes of the device-driven select: one cooperative launch each,
+// only the one whose class holds the runtime |active| does any work
+constexpr int64_t SMALL_M = 4096, MID_M = 1 << 18, MID_G = 32;
 }  // namespace
 
-int topk_check_enqueue(State &s, cudaStream_t st) {
+// Enqueue one TOPK check (engine.py:333-379) with no host read.  m_host >= 0:
+// |active| is known on the host (grid sized for it); m_host < 0: it is the
+// previous check's count, read on the device (device-driven run).  The
+// active set moves from act[cur] to act[cur ^ 1]; the verdict is published by
+// k_publish tagged with `level`.  Returns the new ping-pong index.
+int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense, int cur,
+                           int64_t level) {
     Graph &g = *s.g;
     const int64_t k = s.k;
-    const int64_t m = s.m_host;
-    unsigned long long *out = s.scratch_u64.p;  // [0..3)
-    const int nxt = s.cur ^ 1;
-    if (m <= k) {
-        // nothing to deactivate: sort the whole active set as the prefix
-        unsigned long long init[3] = {(unsigned long long)m, 0ull, (unsigned long long)m};
-        memcpy(s.h_flags, init, sizeof(init));
-        KB_CUDA(cudaMemcpyAsync(out, s.h_flags, sizeof(init), cudaMemcpyHostToDevice, st));
-        int P = 1;
-        while (P < m) P <<= 1;
-        const size_t smem = (size_t)P * 16;
+    unsigned long long *out = s.scratch_u64.p;  // [0..8)
+    const int nxt = cur ^ 1;
+    if (!s.abort_flag.p) {
+        s.abort_flag.alloc(1);
+        KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
+    }
+    TopkArgs A;
+    A.lower = s.lower.p;
+    A.upper = s.upper.p;
+    A.perm = g.labels();
+    A.act_in = s.act[cur].p;
+    A.dense = dense ? 1 : 0;
+    A.act_out = s.act[nxt].p;
+    A.k = k;
+    A.eps = s.eps;
+    A.hist = (unsigned int *)(s.scratch_u64.p + 8);
+    A.blk = s.scratch_u64.p + 8 + HIST_WORDS;
+    A.prefix_buf = s.scratch_i32.p;
+    A.cand = s.cand.p;
+    A.stK = s.stK.p;
+    A.stU = s.stU.p;
+    A.stI = s.stI.p;
+    A.out = out;
+    A.abort = s.abort_flag.p;
+    A.split = 1;
+    void *args[] = {&A};
+    const int Gmax = coop_grid(g.sm_count);
+    int P = 1;
+    while (P < k) P <<= 1;
+    const size_t smem = (size_t)P * 16;
+    static bool attr_done[64] = {};
+    static size_t attr_smem[64] = {};
+    if (!attr_done[g.device] || attr_smem[g.device] < smem) {
         KB_CUDA(cudaFuncSetAttribute(k_topk_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smem, 1)));
-        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), s.act[s.cur].p,
-                                             s.act_dense, s.act[nxt].p, out, s.eps, k); note_launch();
-        KB_CUDA(cudaGetLastError());
-    } else {
-        TopkArgs A;
-        A.lower = s.lower.p;
-        A.upper = s.upper.p;
-        A.perm = g.labels();
-        A.act_in = s.act[s.cur].p;
+        KB_CUDA(cudaFuncSetAttribute(k_topk_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(SMALL_M * 16)));
+        attr_done[g.device] = true;
+        attr_smem[g.device] = smem;
+    }
+    auto small = [&](int64_t mh, const unsigned long long *md) {
+        int Ps = 1;
+        while (Ps < (mh >= 0 ? mh : SMALL_M)) Ps <<= 1;
+        k_topk_small<<<1, 1024, (size_t)Ps * 16, st>>>(s.lower.p, s.upper.p, g.labels(),
+                                                       s.act[cur].p, dense ? 1 : 0, mh, md,
+                                                       SMALL_M, s.act[nxt].p, out, s.eps, k,
+                                                       s.abort_flag.p);
+        note_launch();
+    };
+    auto finish = [&](const unsigned long long *md) {
+        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), A.prefix_buf, 0,
+                                             s.act[nxt].p, out, s.eps, k, s.abort_flag.p, md,
+                                             SMALL_M);
+        note_launch();
+    };
+    if (m_host >= 0) {
         // in the dense first check, rows without out-arcs (new ids >= nv) have
         // lower == upper == 0 < every other lower: when k <= nv they can be
         // neither winners nor survivors, so they are dropped unread
-        A.m = (s.act_dense && k <= s.tail_zero_from) ? s.tail_zero_from : m;
-        A.dense = s.act_dense;
-        A.act_out = s.act[nxt].p;
-        A.k = k;
-        A.eps = s.eps;
-        A.hist = (unsigned int *)(s.scratch_u64.p + 8);
-        // small active sets run in one block (grid.sync degenerates)
-        const int G = (int)std::max<int64_t>(
-            1, std::min<int64_t>(coop_grid(g.sm_count), (A.m + 8191) / 8192));
-        A.blk = s.scratch_u64.p + 8 + HIST_WORDS;
-        A.prefix_buf = s.scratch_i32.p;
-        A.cand = s.cand.p;
-        A.stK = s.stK.p;
-        A.stU = s.stU.p;
-        A.stI = s.stI.p;
-        A.out = out;
-        void *args[] = {&A};
-        KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
-        note_launch();
-        IsWinner win{s.lower.p, g.labels(), out};
-        IsSurvivor sur{s.lower.p, s.upper.p, out, s.eps};
-        unsigned long long *nsel = out + 5;  // [5]=winners, [6]=survivors
-        int32_t *unsel = s.stI.p;
-        size_t tb = 0;
-        auto run_part = [&](auto in) {
-            KB_CUDA(cub::DevicePartition::If(nullptr, tb, in, A.prefix_buf, s.act[nxt].p + k, unsel,
-                                             nsel, (int)A.m, win, sur, st));
-            ensure_cub_tmp(s, tb);
-            KB_CUDA(cub::DevicePartition::If(s.cub_tmp.p, tb, in, A.prefix_buf, s.act[nxt].p + k,
-                                             unsel, nsel, (int)A.m, win, sur, st));
+        A.m = (dense && k <= s.tail_zero_from) ? s.tail_zero_from : m_host;
+        if (A.m <= SMALL_M) {
+            small(A.m, nullptr);
+        } else {
+            const int G = (int)std::max<int64_t>(1, std::min<int64_t>(Gmax, (A.m + 8191) / 8192));
+            KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0,
+                                                st));
             note_launch();
-        };
-        if (A.dense) run_part(cub::CountingInputIterator<int32_t>(0));
-        else run_part((const int32_t *)s.act[s.cur].p);
-        k_cut_counts<<<1, 1, 0, st>>>(out, k);
-        note_launch();
-        int P = 1;
-        while (P < k) P <<= 1;
-        const size_t smem = (size_t)P * 16;
-        KB_CUDA(cudaFuncSetAttribute(k_topk_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), A.prefix_buf, 0,
-                                             s.act[nxt].p, out, s.eps, k); note_launch();
-        KB_CUDA(cudaGetLastError());
+            finish(nullptr);
+        }
+    } else {
+        A.m_dev = out + 7;
+        small(-1, out + 7);
+        const int64_t lo[2] = {SMALL_M, MID_M}, hi[2] = {MID_M, INT64_MAX};
+        const int G[2] = {(int)std::min<int64_t>(MID_G, Gmax), Gmax};
+        for (int c = 0; c < 2; c++) {
+            A.m_lo = lo[c];
+            A.m_hi = hi[c];
+            KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G[c], CHK_THREADS, args,
+                                                0, st));
+            note_launch();
+        }
+        finish(out + 7);
     }
-    // publish the verdict for a speculative K1 queued behind, then the one
-    // host read of this check
-    k_publish<<<1, 1, 0, st>>>(out, s.abort_flag.p, s.work_counter.p, s.h_flags);
+    k_publish<<<1, 1, 0, st>>>(out, s.abort_flag.p, s.work_counter.p, s.h_flags, level);
     note_launch();
+    KB_CUDA(cudaGetLastError());
     s.counter_zeroed = true;
+    return nxt;
+}
+
+int topk_check_enqueue(State &s, cudaStream_t st) {
+    if (!s.abort_flag.p) s.abort_flag.alloc(1);
+    // a stand-alone check acts whatever an earlier run left in the flag
+    KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
+    const int nxt = topk_check_enqueue_dev(s, st, s.m_host, s.act_dense, s.cur, s.r);
+    if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
     KB_CUDA(cudaEventRecord(s.chk_ev, st));
     return nxt;
 }
@@ -1145,6 +1432,47 @@ bool topk_check_finish(State &s, int nxt) {
     s.act_dense = false;
     s.m_host = (int64_t)s.h_flags[0];
     return s.h_flags[1] != 0;
+}
+
+// engine.run (engine.py:382-396) for TOPK with the loop on the device: the
+// host queues up to `batch` levels of K1 + check back to back with no host
+// read in between -- each check's count feeds the next on the device, and a
+// converged check's flag makes every kernel queued behind it exit -- then
+// waits once.  C2 (r = 7) and C3 (r = 6) certify in one batch: one host
+// synchronisation per run.  Returns converged (false: the cap was reached).
+bool topk_run_device(State &s, cudaStream_t st) {
+    if (!s.abort_flag.p) s.abort_flag.alloc(1);
+    KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
+    if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
+    const int64_t batch = std::max<int64_t>(1, tune_get("run.batch", 8));
+    for (;;) {
+        const int64_t r0 = s.r, B = std::min<int64_t>(batch, s.max_iter - s.r);
+        const int cur0 = s.cur;
+        int cur = cur0;
+        for (int64_t j = 0; j < B; j++) {
+            s.spec_abort = true;      // exits once a check before it has converged
+            launch_iterate(s, st);
+            s.spec_abort = false;
+            cur = topk_check_enqueue_dev(s, st, j == 0 ? s.m_host : -1, j == 0 && s.act_dense,
+                                         cur, s.r);
+        }
+        KB_CUDA(cudaEventRecord(s.chk_ev, st));
+        KB_CUDA(cudaEventSynchronize(s.chk_ev));
+        const bool conv = s.h_flags[1] != 0;
+        const int64_t last = (int64_t)s.h_flags[3];   // level of the last check that ran
+        KB_REQUIRE(last > r0 && last <= r0 + B, KB_ECUDA, "device loop lost its verdict");
+        for (int64_t r = r0 + B; r > last; r--) {     // levels queued behind convergence
+            s.levels.pop_back();
+            s.r -= 1;
+            if (s.k1_used >= 2) s.k1_used -= 2;
+        }
+        s.cur = cur0 ^ (int)((last - r0) & 1);
+        s.act_dense = false;
+        s.m_host = (int64_t)s.h_flags[0];
+        (void)cur;
+        if (conv) return true;
+        if (s.r >= s.max_iter) return false;
+    }
 }
 
 

@@ -303,6 +303,7 @@ bool run_check(State &s, cudaStream_t st);      // returns converged
 // verdict to abort_flag, D2H into h_flags, record chk_ev) / finish (after
 // chk_ev: adopt the new active set, return converged); -1: not applicable
 int topk_check_enqueue(State &s, cudaStream_t st);
+bool topk_run_device(State &s, cudaStream_t st);  // TOPK loop, one host sync per batch
 bool topk_check_finish(State &s, int nxt);
 bool ranking_pair_enqueue(State &s, cudaStream_t st);
 void materialize_rank_order(State &s, cudaStream_t st);

@@ -192,3 +192,12 @@ def test_dynamic_oracle_matches_reference(golden_index, dynamic_cases):
             assert stats.aborted_level == step["aborted_level"], p
             assert stats.reactivated == step["reactivated"], p
             assert_same_active(st.active, dynamic_cases[p + "/active"], st.lower, p)
+
+
+def test_lowmem_rmat_generator_equals_pinned_generator():
+    """The scale-27 golden build (tests/golden/make_c3_golden.py) uses the
+    low-memory sampler: it must yield the same CSR as the pinned one."""
+    a = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
+    for t in (1, 3, 8):
+        b = O.rmat_graph_lowmem(1 << 14, edge_factor=16, seed=42, threads=t)
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
