@@ -44,6 +44,11 @@ def workload_name(a):
 METRIC = "time to certified top-100 Katz ranking (s); GTEPS/iter; HBM GB/s vs peak"
 
 
+def l2_note(nnz: int) -> str:
+    return (f"inputs larger than L2: {4 * nnz / 1e9:.1f} GB of column ids streamed per "
+            f"iteration (no flush needed)")
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -58,6 +63,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--launcher-selftest", nargs="?", const="gloo", default=None,
+                    help=argparse.SUPPRESS)
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded multi-GPU path even at one rank")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
@@ -138,25 +145,82 @@ def b_iter(n: int, nnz: int) -> int:
     return 4 * nnz + w_off * (n + 1) + 48 * n
 
 
-def cpu_leg(g0, k, eps, r_expected=None, reps=1):
-    """Oracle port on all host cores: one iterate+check on the full graph,
-    then ranking_result; returns (per-iteration seconds, result seconds)."""
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def port_tcert(g0, k, eps, threads):
+    """One certified run of the oracle port of the reference engine --
+    engine.init + engine.run (iterate_once + the reference's own
+    argpartition check until certified) + ranking_result -- on `threads`
+    host threads for the matvec (engine.py:181-219).  Returns (seconds,
+    iterations, top-10).  Nothing is projected or extrapolated."""
     from oracle import katz_oracle as O
-    threads = os.cpu_count() or 1
-    st = O.OracleState(g0, O.Crit("topk", eps, k=k), threads=threads)
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.iterate_once(st, g0)
-        O.check_converged(st)
-        times.append(time.perf_counter() - t0)
     t0 = time.perf_counter()
-    O.ranking_result(st)
-    t_res = time.perf_counter() - t0
-    return times, t_res, threads
+    st = O.OracleState(g0, O.Crit("topk", eps, k=k), threads=threads)
+    res = O.run_reference_path(st, g0)
+    return time.perf_counter() - t0, res.iterations_used, res.top(10)
+
+
+def reference_package_tcert(g0, k, eps, threads):
+    """The reference package itself (baseline/_ref, pip-installed from
+    /root/reference; it travels to the GPU box with the snapshot) through
+    the CSR shim of SURVEY.md 8(c): katzbounds.init + katzbounds.run, timed
+    as cli.py:212-214 times it.  None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "katzbounds")):
+        return None
+    import numpy as np
+    from scipy import sparse
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import katzbounds as K
+
+    class CSRShim:
+        """Duck-typed static graph (engine.py:98,189,257,263,270,302); the
+        arc set is the R-MAT generator's symmetric one (device-verified)."""
+        node_count = g0.node_count
+        version = 1
+
+        def max_out_degree(self):
+            return g0.max_out_degree()
+
+        def is_symmetric(self):
+            return True
+
+        def out_csr(self):
+            if not hasattr(self, "_csr"):
+                self._csr = sparse.csr_matrix((np.ones(g0.nnz), g0.indices, g0.indptr),
+                                              shape=(g0.node_count,) * 2)
+            return self._csr
+
+    g = CSRShim()
+    g.out_csr()                                  # the reference caches it per version
+    t0 = time.perf_counter()
+    st = K.init(g, K.Criterion.top_k(k, eps), undirected=True, threads=threads)
+    res = K.run(st, g)
+    dt = time.perf_counter() - t0
+    return {"value": dt, "unit": "s", "threads": threads, "iterations": res.iterations_used,
+            "top10": [int(v) for v in res.order[:10]],
+            "what": "katzbounds.init + katzbounds.run (incl. ranking_result) from baseline/_ref "
+                    "through the CSR shim, out_csr() built before timing"}
 
 
 def run_reference(a, rank, world):
+    """--impl reference: the reference's CPU path on this host's cores.  Each
+    step is one full certified run of the oracle port (r iterations of
+    iterate_once + the reference's argpartition check, then ranking_result)
+    with the matvec on every host thread -- measured, not projected.  Extra,
+    measured once after the timed steps: the same at threads=1, and the
+    reference package itself when baseline/_ref is present."""
     if rank != 0:
         return
     from oracle import katz_oracle as O
@@ -165,38 +229,38 @@ def run_reference(a, rank, world):
     g0 = O.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed)
     t_gen = time.perf_counter() - t0
     threads = os.cpu_count() or 1
-    # each step: one iterate_once + check_converged of the reference engine on
-    # the full graph; a fresh state every r_ref steps
-    r_ref = 7 if a.scale == 24 else None
-    st = O.OracleState(g0, O.Crit("topk", a.eps, k=a.k), threads=threads)
-    per = []
+    per, r_seen, top = [], None, None
     for i in range(a.warmup + a.steps):
-        if st.r >= 3:
-            st = O.OracleState(g0, O.Crit("topk", a.eps, k=a.k), threads=threads)
-        t0 = time.perf_counter()
-        O.iterate_once(st, g0)
-        O.check_converged(st)
-        dt = time.perf_counter() - t0
+        dt, r_seen, top = port_tcert(g0, a.k, a.eps, threads)
         if i >= a.warmup:
             per.append(dt)
-    t0 = time.perf_counter()
-    O.ranking_result(st)
-    t_res = time.perf_counter() - t0
-    it = sum(per) / len(per)
-    r = r_ref or 7
-    value = r * it + t_res
+    value = sum(per) / len(per)
+    one_thread = None
+    if not a.no_cpu:
+        dt1, _, _ = port_tcert(g0, a.k, a.eps, 1)
+        one_thread = {"value": dt1, "unit": "s", "cores": 1, "kind": "port",
+                      "sample": "one full certified run at threads=1"}
+    pkg = None
+    if not a.no_cpu and os.environ.get("KB_REF_PACKAGE", "1") == "1":
+        try:
+            pkg = reference_package_tcert(g0, a.k, a.eps, threads)
+        except Exception as e:          # noqa: BLE001 -- report, do not fail the arm
+            pkg = {"error": f"{type(e).__name__}: {e}"}
+    cfg = {"workload": workload_name(a), "n": n, "nnz": g0.nnz, "k": a.k, "eps": a.eps,
+           "seed": a.seed, "iterations": r_seen, "max_out_degree": g0.max_out_degree(),
+           "l2": l2_note(g0.nnz), "parallelism": "single"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(a), "n": n, "nnz": g0.nnz, "k": a.k, "eps": a.eps,
-                   "seed": a.seed, "r_assumed": r},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
-                         "sample": f"{a.steps} x (iterate_once+check_converged) on the full "
-                                   f"graph + 1 ranking_result; T_cert = r*iter + result"},
+                         "sample": f"{a.steps} full certified runs (init + run to the top-{a.k} "
+                                   f"certificate + ranking_result), each timed whole",
+                         "cpu_model": cpu_model(), "threads_1": one_thread,
+                         "reference_package": pkg},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gteps_per_iter": g0.nnz / it / 1e9, "generate_s": t_gen,
+        "gteps_per_iter": None, "top10": top, "generate_s": t_gen,
     }
     print(json.dumps(line), flush=True)
 
@@ -341,10 +405,36 @@ def run_dynamic(a, device):
                       "batches": rows}), flush=True)
 
 
+def shared_host_csr(g, rank, n, nnz, dist):
+    """The canonical CSR in host memory once per node: rank 0 downloads it
+    from its device graph into /dev/shm, the other ranks map the same pages."""
+    import numpy as np
+    tag = os.environ.get("MASTER_PORT", "0")
+    paths = [f"/dev/shm/kb_bench_{tag}_indptr", f"/dev/shm/kb_bench_{tag}_indices"]
+    if rank == 0:
+        ip, ix = g.csr_arrays()
+        for path, arr in zip(paths, (ip, ix)):
+            mm = np.lib.format.open_memmap(path, mode="w+", dtype=arr.dtype, shape=arr.shape)
+            mm[:] = arr
+            mm.flush()
+            del mm
+    dist.barrier()
+    ip = np.load(paths[0], mmap_mode="r+")
+    ix = np.load(paths[1], mmap_mode="r+")
+    assert ip.shape == (n + 1,) and ix.shape == (nnz,)
+    dist.barrier()
+    if rank == 0:
+        for path in paths:
+            os.unlink(path)        # the mappings stay valid until closed
+    return ip, ix
+
+
 def run_sharded(a, rank, world, local):
-    """C2 on N GPUs: rows sharded by degree rank, omega all-gathered with NCCL
-    every iteration (paper_1807_03847_b200.distributed).  Strong scaling: the
-    same graph at every N."""
+    """C2 (or --scale 27: C3) on N GPUs: rows dealt by degree rank, each
+    rank's shard cut out on its own GPU from the device graph
+    (kb_graph_create_shard), omega exchanged every iteration by K1's fused
+    NVLink stores (CUDA IPC) or an NCCL all-gather.  Strong scaling: the same
+    graph at every N."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -362,28 +452,33 @@ def run_sharded(a, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = _lib.lib()
     n = 1 << a.scale
+    crit = P.Criterion.top_k(a.k, a.eps)
+    fused = os.environ.get("KB_FUSED_EXCHANGE", "1") == "1"
+    # the synthetic input: the graph generated on this rank's device
     t0 = time.perf_counter()
     gfull = G.rmat_graph(n, edge_factor=a.edge_factor, seed=a.seed, device=local)
-    ip, ix = gfull.csr_arrays()
-    gfull.device_graph.close()
-    plan = D.ShardPlan(ip, world)
-    crit = P.Criterion.top_k(a.k, a.eps)
-    d = plan.max_degree
+    t_gen = time.perf_counter() - t0
+    info = gfull.device_graph.info()
+    nnz, d = int(info.nnz), int(info.max_out_degree)
     alpha = 1.0 / (1.0 + d)
     gamma = P.tail_gamma(alpha, d)
-    lcsr = tuple(np.ascontiguousarray(x) for x in plan.local_csr(ip, ix, rank))
-    shard_nnz = int(lcsr[0][-1])
-    fused = os.environ.get("KB_FUSED_EXCHANGE", "1") == "1"
+    plan = D.DevicePlan(n, world, d)
+    split = D.fast_split(world)
 
-    def make_shard(fz):
-        return D.CudaShard(plan, rank, None, None, device=local, alpha=alpha, gamma=gamma,
-                           crit=crit, undirected=True, max_iterations=200,
-                           split_threshold=D.fast_split(world), local_csr=lcsr, fused=fz)
-    shard, exch_mode = D.connect_shard(make_shard, dist, rank, world, f"cuda:{local}", fused)
+    def make_shard(fz, full):
+        return D.CudaShard(plan, rank, device=local, alpha=alpha, gamma=gamma, crit=crit,
+                           undirected=True, max_iterations=200, split_threshold=split,
+                           fused=fz, full=full)
+    t0 = time.perf_counter()
+    shard, exch_mode = D.connect_shard(lambda fz: make_shard(fz, gfull.device_graph), dist,
+                                       rank, world, f"cuda:{local}", fused)
     shard.collective_device = f"cuda:{local}"
-    nnz = int(ip[-1])
-    del ix
+    torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
+    shard_nnz = int(shard_info(shard).nnz)
+    host_csr = None if a.no_e2e else shared_host_csr(gfull, rank, n, nnz, dist)
+    gfull.device_graph.close()
+    del gfull
 
     def step(host):
         shard.reset(alpha=alpha, gamma=gamma, crit=crit, undirected=True, max_iterations=200)
@@ -414,52 +509,48 @@ def run_sharded(a, rank, world, local):
     ms_step = float(t.item()) / a.steps
 
     # roofline of this rank's K1 (its rows: n_per, its arcs)
-    nnz_r = int(shard_nnz)
-    w_off = 4 if nnz_r < 2**31 else 8
-    b_rank = 4 * nnz_r + w_off * (plan.n_per + 1) + 48 * plan.n_per
+    w_off = 4 if shard_nnz < 2**31 else 8
+    b_rank = 4 * shard_nnz + w_off * (plan.n_per + 1) + 48 * plan.n_per
     k1_avg = k1_ms / max(1, k1_n)
     peak, peak_src = measured_peaks()
     ach = b_rank / (k1_avg * 1e-3) / 1e9 if k1_avg > 0 else 0.0
     roof = torch.tensor([ach, k1_avg], device=f"cuda:{local}", dtype=torch.float64)
     dist.all_reduce(roof, op=dist.ReduceOp.MIN)   # the slowest rank's kernel
+    shard.close()
 
-    # e2e through the public API: this rank's host CSR shard (page-locked)
-    # -> CudaShard (upload + ingest) -> sharded run -> RankingResult on host
+    # e2e through the public API (distributed.sharded_run): every rank
+    # uploads the node's host CSR (page-locked) to its GPU -- ingest and
+    # symmetry check pipelined with the upload -- cuts its shard on the
+    # device, runs, and receives the ranked result on the host.  The
+    # partitioning is inside the timed region.
     e2e = None
-    if not a.no_e2e:
-        res_out = (np.empty(n, dtype=np.int64), np.empty(n, dtype=np.float64),
-                   np.empty(n, dtype=np.float64))
-        for arr in lcsr + res_out:
+    if host_csr is not None:
+        ip, ix = host_csr
+        for arr in (ip, ix):
             _lib.check(L.kb_host_register(_lib.ptr(arr), arr.nbytes))
 
         def e2e_step():
-            sh, _ = D.connect_shard(make_shard, dist, rank, world, f"cuda:{local}",
-                                    exch_mode.startswith("fused"))
-            sh.collective_device = f"cuda:{local}"
-            out = D.ShardedRun(sh, plan, crit, rank=rank, world=world,
-                               max_iterations=200).run(host_result=True, out=res_out)
-            sh.close()
-            return out
+            return D.sharded_run(ip, ix, crit, undirected=True, device=local,
+                                 fused=exch_mode.startswith("fused"), max_iterations=200)
 
         e2e_step()
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(a.e2e_steps):
-            e2e_step()
+            out = e2e_step()
         torch.cuda.synchronize()
         wall = torch.tensor([(time.perf_counter() - t0) / a.e2e_steps], device=f"cuda:{local}",
                             dtype=torch.float64)
         dist.all_reduce(wall, op=dist.ReduceOp.MAX)
-        hb = torch.tensor([float(lcsr[0].nbytes + lcsr[1].nbytes)], device=f"cuda:{local}",
-                          dtype=torch.float64)
-        dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+        assert out.top(10) == res.top(10)
         e2e = {"value": float(wall.item()), "unit": "s",
-               "h2d_bytes_per_step": int(hb.item()),
+               "h2d_bytes_per_step": int(world * (ip.nbytes + ix.nbytes)),
                "d2h_bytes_per_step": int(world * n * 24),
-               "timing": "host wall clock, max over ranks; each rank uploads its row shard "
-                         "from page-locked memory and every rank receives the ranked result"}
-        for arr in lcsr + res_out:
+               "timing": "host wall clock, max over ranks; every rank uploads the node's "
+                         "page-locked host CSR, cuts its shard on its GPU, runs, and receives "
+                         "the ranked result (order, lower, upper)"}
+        for arr in (ip, ix):
             L.kb_host_unregister(_lib.ptr(arr))
     if rank == 0:
         print(json.dumps({
@@ -469,11 +560,13 @@ def run_sharded(a, rank, world, local):
             "data": "synthetic",
             "config": {"workload": workload_name(a), "n": n, "nnz": nnz, "k": a.k, "eps": a.eps,
                        "seed": a.seed, "iterations": res.iterations_used,
-                       "parallelism": f"row-shard{world}, omega exchange: {exch_mode}",
+                       "max_out_degree": d, "l2": l2_note(nnz),
+                       "parallelism": f"row-shard{world}",
+                       "exchange": exch_mode, "nccl_ranks": world,
                        "top10": res.top(10)},
             "gteps_per_iter": nnz * res.iterations_used / (ms_step * 1e-3) / 1e9,
             "gpu_launches": int(lc1.value - lc0.value), "clocks": clk.summary(),
-            "setup_s": t_setup, "e2e": e2e, "cpu_baseline": None,
+            "generate_s": t_gen, "setup_s": t_setup, "e2e": e2e, "cpu_baseline": None,
             "roofline": {"bound": "hbm", "achieved": float(roof[0].item()), "peak": peak,
                          "unit": "GB/s", "frac": float(roof[0].item()) / peak, "traffic": None,
                          "kernel": "k_sell_iterate (+k_heavy_combine), per rank, slowest rank",
@@ -483,9 +576,61 @@ def run_sharded(a, rank, world, local):
     dist.destroy_process_group()
 
 
+def shard_info(shard):
+    import ctypes
+
+    from paper_1807_03847_b200 import _lib
+    info = _lib.GraphInfo()
+    _lib.check(shard.L.kb_graph_info_get(shard.g, ctypes.byref(info)))
+    return info
+
+
+def launch(a) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script as N ranks
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1).
+    Fails (exit 2) if fewer than N devices are visible."""
+    import socket
+    if a.launcher_selftest is None and a.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < a.gpus:
+            print(json.dumps({"error": f"--gpus {a.gpus} but only {have} CUDA devices "
+                                       "are visible"}), flush=True)
+            return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launcher_selftest(a, rank, world):
+    """The launcher's plumbing without GPUs (CPU tests): every rank joins a
+    gloo group, checks world == --gpus and all-reduces its rank."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank)])
+    dist.all_reduce(t)
+    ok = dist.get_world_size() == world == a.gpus
+    if rank == 0:
+        print(json.dumps({"launcher": "ok" if ok else "bad", "world": world,
+                          "rank_sum": float(t.item())}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     a = parse()
     rank, world, local = dist_env()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch(a))
+    if "WORLD_SIZE" in os.environ and world != a.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE={world} but --gpus {a.gpus}"}), flush=True)
+        sys.exit(2)
+    if a.launcher_selftest is not None:
+        return launcher_selftest(a, rank, world)
     if a.impl == "reference":
         return run_reference(a, rank, world)
     if a.workload == "c4":
@@ -565,23 +710,28 @@ def main():
     achieved = B / (k1_ms * 1e-3) / 1e9
     traffic = None
     gather = None
-    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(prof) and a.scale == 24 and a.edge_factor == 16:
+    name = "k1_traffic.json" if a.scale == 24 else f"k1_traffic_s{a.scale}.json"
+    prof = os.path.join(ROOT, "profiles", name)
+    if os.path.exists(prof) and a.edge_factor == 16:
         with open(prof) as fh:
             pj = json.load(fh)
         traffic = pj.get("traffic_bytes_per_launch")
         # gather-sector efficiency from the same ncu capture: the 8-byte
         # omega values the global gathers deliver over the 32-byte sectors
-        # they fetch (the column stream's sectors taken out)
+        # they fetch (the column stream's sectors taken out); gathers that
+        # hit K1's shared-memory hot set are the arcs into its `hot` hottest
+        # ids: the sum of the largest degrees
         sec = pj.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", {}).get("value")
         if sec:
             stream_sectors = 4 * nnz / 32
-            shared_gathers = pj.get("hot_set_gathers_per_launch", 0)
+            deg = np.sort(g.out_degrees())[::-1]
+            shared_gathers = int(deg[:int(info.hot_size)].sum())
             useful = 8 * (nnz - shared_gathers)
             fetched = 32 * (sec - stream_sectors)
             gather = {"sector_efficiency": useful / fetched if fetched > 0 else None,
                       "global_gather_sectors": int(sec - stream_sectors),
-                      "source": "profiles/k1_traffic.json (ncu, one K1 launch)"}
+                      "hot_set_gathers": shared_gathers,
+                      "source": f"profiles/{name} (ncu, one K1 launch)"}
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -627,18 +777,19 @@ def main():
         for arr in (indptr, indices, order, lo, up):
             L.kb_host_unregister(_lib.ptr(arr))
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): one full certified run of the
+    # reference path (oracle port) on every host core, measured whole
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         from oracle import katz_oracle as O
         ip, ix = g.csr_arrays()
         g0 = O.CSRGraph(n, ip, ix, symmetric=True)
-        it_times, t_res, threads = cpu_leg(g0, a.k, a.eps)
-        it = sum(it_times) / len(it_times)
-        cpu = {"value": r * it + t_res, "unit": "s", "cores": threads, "kind": "port",
-               "sample": f"1 x (iterate_once + check_converged) on the full C2 graph "
-                         f"({it:.2f}s) + ranking_result ({t_res:.2f}s); "
-                         f"T_cert projected as r*iter + result with r={r}"}
+        threads = os.cpu_count() or 1
+        t_cpu, r_cpu, _ = port_tcert(g0, a.k, a.eps, threads)
+        cpu = {"value": t_cpu, "unit": "s", "cores": threads, "kind": "port",
+               "sample": f"one full certified run (init + {r_cpu} x (iterate_once + "
+                         f"argpartition check) + ranking_result) on the whole graph",
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         clocks = clk.summary()
@@ -658,7 +809,7 @@ def main():
             "config": {"workload": workload_name(a), "n": n, "nnz": nnz, "k": a.k,
                        "eps": a.eps, "seed": a.seed, "iterations": r,
                        "max_out_degree": int(info.max_out_degree),
-                       "l2": "inputs larger than L2 (column stream 2.1 GB/iteration)",
+                       "l2": l2_note(nnz),
                        "parallelism": "replicas" if world > 1 else "single"},
             "gteps_per_iter": nnz / (k1_ms * 1e-3) / 1e9,
             "hbm_gbs": achieved,

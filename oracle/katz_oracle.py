@@ -364,6 +364,53 @@ def check_converged(st: OracleState) -> bool:
     return True
 
 
+def check_converged_reference(st: OracleState) -> bool:
+    """engine.py:333-379 exactly as the reference computes it (argpartition
+    for the cut, engine.py:359) -- the CPU *baseline* path, timed by
+    bench.py.  check_converged above is the checker's variant (the device's
+    deterministic tie rule); both give the same verdicts, thresholds and
+    prefixes whenever no exact tie straddles the k-th position (SURVEY.md
+    8(c) rule 4), as on every R-MAT config."""
+    kind = st.crit.kind
+    eps = st.epsilon
+    if kind in (SCORE, PAIR):
+        return check_converged(st)
+    k = st.n if kind == RANKING else st.crit.k
+    m = st.active
+    lowers = st.lower[m]
+    if m.size > k:
+        sel = np.argpartition(-lowers, k - 1)
+        top_pos, rest_pos = sel[:k], sel[k:]
+    else:
+        top_pos = np.arange(m.size)
+        rest_pos = np.empty(0, dtype=np.int64)
+    top_ids = m[top_pos]
+    prefix = top_ids[np.lexsort((top_ids, -st.lower[top_ids]))]
+    threshold = st.lower[prefix[-1]]
+    if rest_pos.size:
+        rest = m[rest_pos]
+        st.active = np.concatenate([prefix, rest[st.upper[rest] - eps >= threshold]])
+    else:
+        st.active = prefix
+    if st.active.size > k:
+        return False
+    if prefix.size >= 2:
+        return bool((st.upper[prefix[1:]] - eps < st.lower[prefix[:-1]]).all())
+    return True
+
+
+def run_reference_path(st: OracleState, g: CSRGraph) -> "OracleResult":
+    """engine.run (engine.py:382-396) with the reference's own check: the
+    timed CPU baseline (bench.py --impl reference and cpu_baseline)."""
+    while True:
+        iterate_once(st, g)
+        if check_converged_reference(st):
+            break
+        if st.r >= st.max_iterations:
+            raise OracleConvergenceError(st.r, st.gap())
+    return ranking_result(st)
+
+
 class OracleConvergenceError(Exception):
     def __init__(self, iterations, gap):
         super().__init__(f"unmet after {iterations} iterations")

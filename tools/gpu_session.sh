@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/g4_tests.log 2>&1; echo "tests $?"
-timeout 300 python tools/step_phases.py > gpurun_out/g4_phases.log 2>&1; echo "phases $?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/g4_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/g4_ncu.log 2>&1; echo "ncu $?"
+timeout 900 python -m pytest tests/test_gpu_distributed.py tests/test_gpu_parity.py -x -q > gpurun_out/g5_tests.log 2>&1; echo "tests $?"
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/g5_c2.log 2>&1; echo "c2 $?"
+timeout 900 python bench.py --steps 5 --warmup 3 --scale 27 > gpurun_out/g5_c3.log 2>&1; echo "c3 $?"
+timeout 900 python bench.py --steps 5 --warmup 3 --sharded --no-cpu > gpurun_out/g5_sh.log 2>&1; echo "sharded $?"
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/g5_ref.log 2>&1; echo "ref $?"
