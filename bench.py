@@ -371,7 +371,7 @@ def run_dynamic(a, device):
         pres = g._present(pk)
         pk = pk[~pres]
         arcs = np.concatenate([pk, pk[:, ::-1]])
-        batch = P.EdgeBatch(insertions=[tuple(x) for x in arcs.tolist()])
+        batch = P.EdgeBatch(insertions=arcs)          # (m, 2) int64, no tuples
         ms = P.engine.ctypes.c_double()
         _lib.check(L.kb_timer(device, 0, None))
         t0 = time.perf_counter()

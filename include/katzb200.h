@@ -76,6 +76,12 @@ typedef struct {
     double  spmv_ms;          /* summed device time of the K1 launches       */
     int64_t spmv_launches;    /* number of K1 iterations timed in spmv_ms    */
     int64_t check_full_sorts; /* ranking checks that needed the full sort    */
+    int64_t k_boundary_ties;  /* SURVEY 8(c) rule 4: nodes tied exactly with
+                                 the k-th lower bound and dropped with
+                                 gap < eps, summed over TOPK checks -- where
+                                 argpartition (engine.py:359) may choose
+                                 differently; 0 = active and r are the
+                                 reference's whatever its tie choice      */
 } kb_state_info;
 
 typedef struct {
@@ -132,6 +138,10 @@ int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr
  * the tie-break labels are the node ids (padding: n, n+1, ...).  The shard
  * inherits `full`'s symmetry flag.  Outputs n_per = ceil(n/P) and the number
  * of rows this rank owns (its block's head). */
+/* Device ids of the nodes whose tie-break label is labels[j] (-1: none),
+ * m <= 64: a shard's exchange ids of given node ids (sharded PAIR checks,
+ * engine.py:346-353). */
+int kb_graph_find_labels(kb_graph *g, const int64_t *labels, int64_t m, int64_t *ids);
 int kb_graph_create_shard(kb_graph *full, int64_t nranks, int64_t rank,
                           int64_t split_threshold, int64_t hot_size, kb_graph **out,
                           int64_t *n_per, int64_t *owned);

@@ -45,7 +45,8 @@ class StateInfo(ctypes.Structure):
     _fields_ = [("r", i64), ("active", i64), ("max_iterations", i64),
                 ("levels_kept", i64), ("alpha", dbl), ("gamma", dbl),
                 ("epsilon", dbl), ("last_check_ms", dbl), ("spmv_ms", dbl),
-                ("spmv_launches", i64), ("check_full_sorts", i64)]
+                ("spmv_launches", i64), ("check_full_sorts", i64),
+                ("k_boundary_ties", i64)]
 
 
 class UpdateStatsC(ctypes.Structure):
@@ -68,6 +69,7 @@ SIGNATURES = {
     "kb_graph_create": (i32, [i32, i64, i64, vp, vp, i64, i64, ctypes.POINTER(vp)]),
     "kb_graph_create_ex": (i32, [i32, i64, i64, vp, vp, i64, i64, i32, vp, i64, i64,
                                  ctypes.POINTER(vp)]),
+    "kb_graph_find_labels": (i32, [vp, vp, i64, vp]),
     "kb_graph_create_shard": (i32, [vp, i64, i64, i64, i64, ctypes.POINTER(vp),
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "kb_graph_create_rmat": (i32, [i32, i32, i64, vp, dbl, dbl, dbl, i64, i64,

@@ -421,6 +421,14 @@ int kb_graph_create_shard(kb_graph *full, int64_t nranks, int64_t rank, int64_t 
     });
 }
 
+int kb_graph_find_labels(kb_graph *h, const int64_t *labels, int64_t m, int64_t *ids) {
+    return guarded([&] {
+        KB_REQUIRE(h && (m == 0 || (labels && ids)), KB_EPARAM, "NULL argument");
+        use_device(h->g.device);
+        find_labels(h->g, labels, m, ids);
+    });
+}
+
 int kb_state_set_active(kb_state *h, const int64_t *ids, int64_t m) {
     return guarded([&] {
         KB_REQUIRE(h && (m == 0 || ids), KB_EPARAM, "NULL argument");
@@ -1076,6 +1084,8 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.work_counter.alloc(2);
         s.abort_flag.alloc(1);
         KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
+        s.tie_count.alloc(1);
+        KB_CUDA(cudaMemsetAsync(s.tie_count.p, 0, sizeof(unsigned long long), st));
         KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
         s.h_flags = pinned_flags();
         KB_CUDA(cudaEventCreate(&s.ev0));
@@ -1118,6 +1128,13 @@ int kb_state_info_get(const kb_state *h, kb_state_info *info) {
         info->spmv_ms = s.spmv_ms;
         info->spmv_launches = s.spmv_launches;
         info->check_full_sorts = s.check_full_sorts;
+        unsigned long long ties = 0;
+        if (s.tie_count.p) {
+            KB_CUDA(cudaMemcpyAsync(&ties, s.tie_count.p, sizeof(ties), cudaMemcpyDeviceToHost,
+                                    s.g->stream));
+            KB_CUDA(cudaStreamSynchronize(s.g->stream));
+        }
+        info->k_boundary_ties = (int64_t)ties;
     });
 }
 

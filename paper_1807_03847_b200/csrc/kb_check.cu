@@ -70,6 +70,10 @@ struct TopkArgs {
     // fused split: winners -> prefix_buf, survivors -> act_out + k, in
     // active-set order, counts into out[0], out[2], out[5], out[6]
     int split = 0;
+    // SURVEY.md 8(c) rule 4: losers that tie the k-th lower bound exactly and
+    // are dropped (gap < eps) -- where numpy's arbitrary argpartition choice
+    // (engine.py:359) could have kept them -- are counted here
+    unsigned long long *ties = nullptr;
 };
 
 __device__ __forceinline__ bool flag_set(const unsigned long long *f) {
@@ -370,6 +374,8 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
                     c = 2;
                 else if (__dsub_rn(up[q], A.eps) >= thr)
                     c = 1;
+                else if (key[q] == kstar && A.ties)
+                    atomicAdd(A.ties, 1ull);
                 cls[t + q * 32 + lane] = c;
             }
             const unsigned bw = __ballot_sync(0xffffffffu, c == 2);
@@ -520,7 +526,8 @@ __global__ void __launch_bounds__(1024) k_topk_small(const double *lower, const 
                                                      const unsigned long long *m_dev, int64_t m_max,
                                                      int32_t *act_out, unsigned long long *out,
                                                      double eps, int64_t k,
-                                                     const unsigned long long *abort) {
+                                                     const unsigned long long *abort,
+                                                     unsigned long long *ties) {
     if (flag_set(abort)) return;
     const int64_t m = m_dev ? (int64_t)*(const volatile unsigned long long *)m_dev : m_host;
     if (m > m_max) return;
@@ -571,6 +578,7 @@ __global__ void __launch_bounds__(1024) k_topk_small(const double *lower, const 
             const uint64_t kx = key_of(lower, id);
             const bool win = kx > kstar || (kx == kstar && (uint32_t)perm[id] <= istar);
             sv = !win && __dsub_rn(upper[id], eps) >= thr;
+            if (!win && !sv && kx == kstar && ties) atomicAdd(ties, 1ull);
         }
         const unsigned b = __ballot_sync(0xffffffffu, sv);
         if (lane == 0) s_cnt[warp] = __popc(b);
@@ -872,7 +880,7 @@ bool sorted_check(State &s, cudaStream_t st, int64_t k) {
     const int32_t *by_orig = id_in.p;
     size_t tb = 0;
     if (!s.act_dense) {
-        k_perm_keys<<<nblk(m, 256), 256, 0, st>>>(g.perm.p, id_in.p, m, ok_in.p); note_launch();
+        k_perm_keys<<<nblk(m, 256), 256, 0, st>>>(g.labels(), id_in.p, m, ok_in.p); note_launch();
         KB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ok_in.p, ok_out.p, id_in.p,
                                                 id_out.p, (int)m, 0, 32, st));
         ensure_cub_tmp(s, tb);
@@ -1186,7 +1194,7 @@ bool check_ranking(State &s, cudaStream_t st) {
     int32_t *cand = ids + nb;
     unsigned int *po = (unsigned int *)(cand + NCAND);
     if (s.rk_q >= 0 && tune_get("check.pair_cache", 1)) {
-        k_pair_refutes<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, s.rk_q, s.rk_x, s.eps, u);
+        k_pair_refutes<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, g.labels(), s.rk_q, s.rk_x, s.eps, u);
         note_launch();
         sync_read(s, st, u, 1);
         if (s.h_flags[0]) return false;          // still refuted: not converged
@@ -1194,11 +1202,11 @@ bool check_ranking(State &s, cudaStream_t st) {
     }
     KB_CUDA(cudaMemsetAsync(u, 0, 4 * sizeof(unsigned long long), st));
     KB_CUDA(cudaMemsetAsync(u + 3, 0xff, sizeof(unsigned long long), st));   // refuting pair
-    k_rank_violators<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, s.eps,
+    k_rank_violators<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.labels(), act, dense, n, s.eps,
                                          u, bkey, ids);
     if (tune_get("check.refute", 1) && nb <= 2048) {
-        k_pick_cands_fast<<<1, 1024, nb, st>>>(bkey, ids, nb, g.perm.p, cand, u + 1);
-        k_rank_refute<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.perm.p, act, dense, n, cand,
+        k_pick_cands_fast<<<1, 1024, nb, st>>>(bkey, ids, nb, g.labels(), cand, u + 1);
+        k_rank_refute<<<nb, 256, 0, st>>>(s.lower.p, s.upper.p, g.labels(), act, dense, n, cand,
                                           u + 1, s.eps, u + 2, u + 3);
         note_launch(3);
         KB_CUDA(cudaGetLastError());
@@ -1216,8 +1224,8 @@ bool check_ranking(State &s, cudaStream_t st) {
         if (nviol <= ncand) return true;         // every violator checked and passes
         return sorted_check(s, st, g.n);
     }
-    k_pick_cands<<<1, 256, 0, st>>>(bkey, ids, nb, g.perm.p, cand, u + 1);
-    k_rank_pred<<<nb, 256, 0, st>>>(s.lower.p, g.perm.p, act, dense, n, cand, NCAND, u + 1, pk,
+    k_pick_cands<<<1, 256, 0, st>>>(bkey, ids, nb, g.labels(), cand, u + 1);
+    k_rank_pred<<<nb, 256, 0, st>>>(s.lower.p, g.labels(), act, dense, n, cand, NCAND, u + 1, pk,
                                     po);
     k_rank_decide<<<1, 256, 0, st>>>(u, u + 1, cand, pk, po, nb, s.upper.p, s.eps, u + 2);
     note_launch(4);
@@ -1266,7 +1274,7 @@ bool ranking_pair_enqueue(State &s, cudaStream_t st) {
     if (!s.abort_flag.p) s.abort_flag.alloc(1);
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
     k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma, s.undirected,
-                                        g.perm.p, s.rk_q, s.rk_x, s.eps, s.scratch_u64.p,
+                                        g.labels(), s.rk_q, s.rk_x, s.eps, s.scratch_u64.p,
                                         s.abort_flag.p, s.h_flags, s.work_counter.p);
     note_launch();
     KB_CUDA(cudaGetLastError());
@@ -1352,6 +1360,7 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
     A.out = out;
     A.abort = s.abort_flag.p;
     A.split = 1;
+    A.ties = s.tie_count.p;
     void *args[] = {&A};
     const int Gmax = coop_grid(g.sm_count);
     int P = 1;
@@ -1373,7 +1382,7 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
         k_topk_small<<<1, 1024, (size_t)Ps * 16, st>>>(s.lower.p, s.upper.p, g.labels(),
                                                        s.act[cur].p, dense ? 1 : 0, mh, md,
                                                        SMALL_M, s.act[nxt].p, out, s.eps, k,
-                                                       s.abort_flag.p);
+                                                       s.abort_flag.p, s.tie_count.p);
         note_launch();
     };
     auto finish = [&](const unsigned long long *md) {

@@ -269,6 +269,7 @@ struct State {
     bool counter_zeroed = false;  // the next K1's work counter was reset on the device
     int exch_parity = 0;      // parity of the level being computed
     cudaEvent_t chk_ev = nullptr;
+    DBuf<unsigned long long> tie_count;  // k-boundary ties dropped with gap < eps (rule 4)
     bool rank_order_pending = false;    // RANKING: active not yet in (-lower, id) order
     std::vector<int64_t> level_sizes;   // UpdateStats.level_sizes of the last update
     const double *x_level() const { return levels.back().p; }
@@ -355,6 +356,7 @@ void rmat_device_csr(int scale, int64_t edge_factor, const uint64_t state[4], do
 void grid_device_csr(int64_t n, DBuf<int64_t> &indptr, DBuf<int32_t> &indices,
                      int64_t &nnz_out);
 int graph_is_symmetric(Graph &g);
+void find_labels(Graph &g, const int64_t *h_targets, int64_t m, int64_t *h_ids);
 void build_shard(Graph &full, int64_t P, int64_t rank, Graph &out, int64_t *n_per_out,
                  int64_t *owned_out);
 void ensure_cub_tmp(State &s, size_t bytes);

@@ -90,7 +90,35 @@ __global__ void k_local_cols(const int32_t *node_of_exch, const int64_t *ip_full
     for (int64_t j = lane; j < L; j += 32) ix_loc[dst + j] = exch_of_node[ix_full[src + j]];
 }
 
+// device ids whose tie-break label is one of the m targets (-1 if none)
+__global__ void k_find_labels(const int32_t *label, int64_t N, const int64_t *targets, int m,
+                              unsigned long long *out) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= N) return;
+    const int32_t l = label[e];
+    for (int j = 0; j < m; j++)
+        if ((int64_t)l == targets[j]) out[j] = (unsigned long long)e;
+}
+
 }  // namespace
+
+void find_labels(Graph &g, const int64_t *h_targets, int64_t m, int64_t *h_ids) {
+    cudaStream_t st = g.stream;
+    KB_REQUIRE(m >= 0 && m <= 64, KB_EPARAM, "at most 64 labels per call");
+    if (!m) return;
+    DBuf<int64_t> t;
+    DBuf<unsigned long long> o;
+    t.alloc(m);
+    o.alloc(m);
+    KB_CUDA(cudaMemcpyAsync(t.p, h_targets, m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    KB_CUDA(cudaMemsetAsync(o.p, 0xFF, m * sizeof(unsigned long long), st));
+    const int32_t *lab = g.labels();
+    if (g.n)
+        k_find_labels<<<nblk(g.n, 256), 256, 0, st>>>(lab, g.n, t.p, (int)m, o.p);
+    note_launch();
+    KB_CUDA(cudaMemcpyAsync(h_ids, o.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+}
 
 // Builds rank `rank`'s shard of `full` into `out` (fresh Graph: device,
 // stream, split and hot already set by the caller).  Returns n_per and the

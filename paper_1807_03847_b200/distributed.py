@@ -176,15 +176,22 @@ class CudaShard:
             self.s = None
         kind = {RANKING: 0, TOPK: 1, SCORE: 2, PAIR: 3}[crit.kind]
         s = ctypes.c_void_p()
+        # a PAIR state's (u, v) are device ids; the sharded check reads the
+        # two nodes' bounds itself (pair_values), so any distinct pair does
+        pu, pv = (0, 1) if crit.kind == PAIR else (0, 0)
         _lib.check(self.L.kb_state_create(self.g, alpha, gamma, int(undirected), kind,
-                                          crit.epsilon, int(crit.k or 0), 0, 0,
+                                          crit.epsilon, int(crit.k or 0), pu, pv,
                                           0 if self.fused else 1, int(max_iterations),
                                           ctypes.byref(s)))
         self.s = s
         if self.fused:
             _lib.check(self.L.kb_state_exchange(s, 1))
         lo, _ = self.plan.block(self.rank)
-        _lib.check(self.L.kb_state_set_active_range(s, lo, lo + self.plan.owned(self.rank)))
+        if crit.kind == RANKING:
+            # every rank certifies the whole ranking on the gathered bounds
+            _lib.check(self.L.kb_state_set_active_range(s, 0, self.plan.P * self.plan.n_per))
+        else:
+            _lib.check(self.L.kb_state_set_active_range(s, lo, lo + self.plan.owned(self.rank)))
         self.r = 0
 
     def exchange_export(self):
@@ -312,6 +319,29 @@ class CudaShard:
         _lib.check(self.L.kb_gap(self.s, ctypes.byref(out)))
         return float(out.value)
 
+    def pair_values(self, u: int, v: int):
+        """(lower[u], upper[u], lower[v], upper[v]) for the nodes this rank
+        owns, 0.0 for the others (an all-reduce SUM completes them)."""
+        if getattr(self, "_pair_ids", None) is None or self._pair_ids[0] != (u, v):
+            lab = np.array([u, v], dtype=np.int64)
+            ids = np.empty(2, dtype=np.int64)
+            _lib.check(self.L.kb_graph_find_labels(self.g, _lib.ptr(lab), 2, _lib.ptr(ids)))
+            self._pair_ids = ((u, v), [int(x) for x in ids])
+        lo, hi = self.plan.block(self.rank)
+        lo_t, up_t = self.bounds_tensors()
+        out = []
+        for e in self._pair_ids[1]:
+            own = lo <= e < hi
+            out += [float(lo_t[e]) if own else 0.0, float(up_t[e]) if own else 0.0]
+        return out[0], out[1], out[2], out[3]
+
+    def check_full(self) -> bool:
+        """check_converged on this rank's state, whose bounds hold every
+        block (gathered): the single-GPU RANKING certificates."""
+        out = ctypes.c_int()
+        _lib.check(self.L.kb_check(self.s, ctypes.byref(out)))
+        return bool(out.value)
+
     def rank_bounds(self, lower: np.ndarray, upper: np.ndarray):
         n = lower.size
         order = np.empty(n, dtype=np.int64)
@@ -378,9 +408,8 @@ class ShardedRun:
         self.b, self.plan, self.crit = backend, plan, crit
         self.rank, self.world = rank, world
         self.max_iterations = max_iterations
-        if crit.kind not in (TOPK, SCORE):
-            raise ParameterError(
-                f"sharded runs support the topk and score criteria (got {crit.kind!r})")
+        if crit.kind == TOPK and crit.k > 4096:
+            raise ParameterError("sharded top-k supports k <= 4096")
 
     def _allreduce(self, value, op):
         t = self.torch.tensor([value], dtype=self.torch.float64,
@@ -395,6 +424,24 @@ class ShardedRun:
         ops = self.dist.ReduceOp
         if c.kind == SCORE:
             return self._allreduce(self.b.local_gap(), ops.MAX) < c.epsilon, False
+        if c.kind == PAIR:
+            # the two nodes' bounds from their owners (engine.py:346-353)
+            t = self.torch.tensor(self.b.pair_values(int(c.u), int(c.v)),
+                                  dtype=self.torch.float64,
+                                  device=getattr(self.b, "collective_device", "cpu"))
+            self.dist.all_reduce(t, op=ops.SUM)
+            lu, uu, lv, uv = t.tolist()
+            u, v = int(c.u), int(c.v)
+            lw, ux = (lu, uv) if (lu, -u) >= (lv, -v) else (lv, uu)
+            return bool(lw > ux - c.epsilon), False
+        if c.kind == RANKING:
+            # every rank holds every block after the gather and runs the same
+            # O(n) certificates (engine.py:355-378 with k = n): same verdict
+            # on every rank, no further collective
+            lo_t, up_t = self.b.bounds_tensors()
+            _all_gather_flat(self.dist, lo_t, self.rank, self.plan.P, self.plan.n_per)
+            _all_gather_flat(self.dist, up_t, self.rank, self.plan.P, self.plan.n_per)
+            return self.b.check_full(), False
         # TOPK: fixed-size proposal blocks (count + k keys, labels, uppers as
         # 64-bit words) all-gathered on the device; every rank takes the same
         # global cut; |active| is all-reduced; one host read per check

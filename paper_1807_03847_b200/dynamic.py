@@ -36,10 +36,11 @@ class UpdateStats:
 def _post_batch_max_degree(g, batch: EdgeBatch) -> int:
     """dynamic.py:152-157: max out-degree after deletions and insertions."""
     degs = np.array(g.out_degrees(), dtype=np.int64, copy=True)
-    if batch.deletions:
-        np.subtract.at(degs, np.array([s for s, _ in batch.deletions]), 1)
-    if batch.insertions:
-        np.add.at(degs, np.array([s for s, _ in batch.insertions]), 1)
+    ins, dels = batch.arrays()
+    if dels.shape[0]:
+        np.subtract.at(degs, dels[:, 0], 1)
+    if ins.shape[0]:
+        np.add.at(degs, ins[:, 0], 1)
     return int(degs.max()) if degs.size else 0
 
 

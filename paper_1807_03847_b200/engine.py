@@ -335,6 +335,17 @@ class KatzState:
             self._cache["active"] = a
         return a
 
+    @property
+    def k_boundary_ties(self) -> int:
+        """SURVEY.md 8(c) rule 4: nodes that tied the k-th lower bound exactly
+        and were dropped from the active set with gap < eps, summed over this
+        state's TOPK checks.  The reference's argpartition (engine.py:359)
+        picks among such ties arbitrarily, so while this is 0 the active set
+        and r are the reference's whatever its choice; otherwise run() warns
+        (KBoundaryTieWarning) that they may differ (the certified order and
+        the bounds never do: ranking_result sorts every node)."""
+        return int(self._info().k_boundary_ties)
+
     def gap(self) -> float:
         """Widest remaining bound interval (engine.py:172-174)."""
         out = ctypes.c_double()
@@ -543,7 +554,20 @@ def run(state: KatzState, g) -> RankingResult:
         msg = _lib.last_error()
         raise ConvergenceError(msg, iterations=state.r, gap=state.gap())
     _lib.check(st)
+    if state.criterion.kind == TOPK:
+        ties = state.k_boundary_ties
+        if ties:
+            import warnings
+            warnings.warn(KBoundaryTieWarning(
+                f"{ties} node(s) tied the k-th lower bound exactly and were dropped with "
+                f"gap < epsilon: the reference's argpartition may keep a different active "
+                f"set (SURVEY.md 8(c) rule 4)"), stacklevel=2)
     return ranking_result(state)
+
+
+class KBoundaryTieWarning(UserWarning):
+    """An exact tie at the k-th position was resolved by node id where the
+    reference's np.argpartition (engine.py:359) resolves it arbitrarily."""
 
 
 def ranking_result(state: KatzState) -> RankingResult:

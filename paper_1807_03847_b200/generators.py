@@ -121,10 +121,14 @@ class DeviceResidentGraph:
                 yield (u, v)
 
     def out_csr(self):
-        from scipy import sparse
-        ip, ix = self.csr_arrays()
-        return sparse.csr_matrix((np.ones(ix.size), ix, ip),
-                                 shape=(self.node_count, self.node_count))
+        c = getattr(self, "_scipy", None)
+        if c is None or c[0] != self.version:     # cached per version (graph.py:184)
+            from scipy import sparse
+            ip, ix = self.csr_arrays()
+            c = (self.version, sparse.csr_matrix((np.ones(ix.size), ix, ip),
+                                                 shape=(self.node_count, self.node_count)))
+            self._scipy = c
+        return c[1]
 
     # ---- mutation (graph.py:201-237)
     def validate_batch(self, batch: EdgeBatch) -> None:

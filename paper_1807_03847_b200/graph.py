@@ -59,20 +59,79 @@ def check_batch_arcs(batch: "EdgeBatch", n: int, check_node, present) -> None:
             raise BatchPreconditionError(f"cannot {verb} arc ({u}, {v}): {msg}")
 
 
+class ArcArray(Sequence):
+    """An (m, 2) int64 arc array with the read-only list-of-tuples surface
+    EdgeBatch exposes (len, index, iterate, compare, concatenate): large
+    batches built from numpy arrays never become Python tuples unless a
+    caller walks them."""
+
+    def __init__(self, a: np.ndarray):
+        self.a = a
+
+    def __len__(self) -> int:
+        return self.a.shape[0]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [tuple(x) for x in self.a[i].tolist()]
+        u, v = self.a[i].tolist()
+        return (u, v)
+
+    def __iter__(self):
+        return iter(tuple(x) for x in self.a.tolist())
+
+    def __eq__(self, other) -> bool:
+        return list(self) == list(other)
+
+    def __add__(self, other):
+        return list(self) + list(other)
+
+    def __radd__(self, other):
+        return list(other) + list(self)
+
+    def __repr__(self) -> str:
+        return repr(list(self))
+
+
+def _arcs_in(x):
+    if isinstance(x, ArcArray):
+        return x
+    if isinstance(x, np.ndarray):
+        a = np.ascontiguousarray(x, dtype=np.int64)
+        if a.size == 0:
+            a = a.reshape(0, 2)
+        if a.ndim != 2 or a.shape[1] != 2:
+            raise ValueError("arc arrays must have shape (m, 2)")
+        if not np.array_equal(a, x):
+            raise ValueError("arc ids must be integers")
+        return ArcArray(a)
+    return [(int(u), int(v)) for u, v in x]
+
+
 @dataclass
 class EdgeBatch:
-    """Arc insertions and deletions applied as one unit (graph.py:30-68)."""
+    """Arc insertions and deletions applied as one unit (graph.py:30-68).
+
+    Besides lists of (u, v) pairs, either side may be an (m, 2) integer
+    numpy array (kept as an array: no per-arc Python objects)."""
 
     insertions: list[Arc] = field(default_factory=list)
     deletions: list[Arc] = field(default_factory=list)
 
     def __post_init__(self):
-        self.insertions = [(int(u), int(v)) for u, v in self.insertions]
-        self.deletions = [(int(u), int(v)) for u, v in self.deletions]
+        self.insertions = _arcs_in(self.insertions)
+        self.deletions = _arcs_in(self.deletions)
 
     def arrays(self) -> tuple[np.ndarray, np.ndarray]:
         """(insertions, deletions) as (m, 2) int64 arrays, cached per list
         object and length (the lists are the batch's public state)."""
+        if isinstance(self.insertions, ArcArray) and isinstance(self.deletions, ArcArray):
+            return self.insertions.a, self.deletions.a
+        if isinstance(self.insertions, ArcArray) or isinstance(self.deletions, ArcArray):
+            i, d = (x.a if isinstance(x, ArcArray) else
+                    np.array(x, dtype=np.int64).reshape(-1, 2)
+                    for x in (self.insertions, self.deletions))
+            return i, d
         key = (id(self.insertions), len(self.insertions), id(self.deletions),
                len(self.deletions))
         cached = self.__dict__.get("_arr")
@@ -221,10 +280,11 @@ class Graph:
         return bool(i < self._keys.size and self._keys[i] == k)
 
     def _has_keys(self, keys: np.ndarray) -> np.ndarray:
+        if not keys.size or not self._keys.size:
+            return np.zeros(keys.size, dtype=bool)
         i = np.searchsorted(self._keys, keys)
-        i = np.minimum(i, max(self._keys.size - 1, 0))
-        return (self._keys.size > 0) & (self._keys[i] == keys) if keys.size else \
-            np.zeros(0, dtype=bool)
+        i = np.minimum(i, self._keys.size - 1)
+        return self._keys[i] == keys
 
     def csr_arrays(self) -> tuple[np.ndarray, np.ndarray]:
         """(indptr int64[n+1], indices int32[nnz]), rows ascending."""
@@ -304,9 +364,14 @@ class Graph:
     def out_csr(self):
         """scipy view of the canonical CSR (graph.py:177-197), for callers
         that expect the reference's return type."""
-        from scipy import sparse
-        ip, ix = self.csr_arrays()
-        return sparse.csr_matrix((np.ones(ix.size), ix, ip), shape=(self._n, self._n))
+        c = self._cache.get("scipy_csr")
+        if c is None or c[0] != self._version:   # cached per version (graph.py:184)
+            from scipy import sparse
+            ip, ix = self.csr_arrays()
+            c = (self._version,
+                 sparse.csr_matrix((np.ones(ix.size), ix, ip), shape=(self._n, self._n)))
+            self._cache["scipy_csr"] = c
+        return c[1]
 
     # ---- mutation
     def apply_batch(self, batch: EdgeBatch) -> None:
@@ -321,19 +386,24 @@ class Graph:
         check_batch_arcs(batch, n, self._check_node,
                          lambda a: self._has_keys(a[:, 0] * n + a[:, 1]))
 
+    def _arc_keys(self, arcs) -> np.ndarray:
+        if isinstance(arcs, ArcArray):
+            return arcs.a[:, 0] * self._n + arcs.a[:, 1]
+        return np.array([u * self._n + v for u, v in arcs], dtype=np.int64)
+
     def insert_arcs(self, arcs: Sequence[Arc], _validated: bool = False) -> None:
         if not _validated:
-            self.validate_batch(EdgeBatch(insertions=list(arcs)))
+            self.validate_batch(EdgeBatch(insertions=_arcs_in(arcs)))
         if len(arcs):
-            k = np.sort(np.array([u * self._n + v for u, v in arcs], dtype=np.int64))
+            k = np.sort(self._arc_keys(arcs))
             self._keys = np.insert(self._keys, np.searchsorted(self._keys, k), k)
         self._version += 1
 
     def remove_arcs(self, arcs: Sequence[Arc], _validated: bool = False) -> None:
         if not _validated:
-            self.validate_batch(EdgeBatch(deletions=list(arcs)))
+            self.validate_batch(EdgeBatch(deletions=_arcs_in(arcs)))
         if len(arcs):
-            k = np.array([u * self._n + v for u, v in arcs], dtype=np.int64)
+            k = self._arc_keys(arcs)
             self._keys = np.delete(self._keys, np.searchsorted(self._keys, k))
         self._version += 1
 

@@ -114,6 +114,20 @@ class OracleShard:
         b = slice(self.lo, self.hi)
         return float(np.max(self.upper[b] - self.lower[b]))
 
+    def pair_values(self, u, v):
+        out = []
+        for x in (u, v):
+            e = int(self.plan.exch_of_node[x])
+            own = self.lo <= e < self.hi
+            out += [float(self.lower[e]) if own else 0.0, float(self.upper[e]) if own else 0.0]
+        return tuple(out)
+
+    def check_full(self):
+        """RANKING on the gathered bounds: every adjacent pair in (-lower,
+        label) order separated (engine.py:355-378 with k = n)."""
+        o = np.lexsort((self.labels, -self.lower))
+        return bool(np.all(self.upper[o[1:]] - self.eps < self.lower[o[:-1]]))
+
     def bounds_tensors(self):
         return torch.from_numpy(self.lower), torch.from_numpy(self.upper)
 
@@ -161,15 +175,22 @@ def _case(case):
         return O.rmat_graph(4096, edge_factor=16, seed=3), Criterion.score(1e-7)
     if case == "grid":
         return O.grid_graph(33 * 31), Criterion.top_k(7, 1e-8)
+    if case == "grid_ranking":
+        return O.grid_graph(24 * 24), Criterion.ranking(1e-9)
+    if case == "rmat12_ranking":
+        return O.rmat_graph(4096, edge_factor=16, seed=3), Criterion.ranking(1e-7)
+    if case == "rmat12_pair":
+        return O.rmat_graph(4096, edge_factor=16, seed=3), Criterion.pair(16, 256, 1e-9)
     raise KeyError(case)
 
 
 def _oracle_crit(c):
-    return O.Crit(c.kind, c.epsilon, k=c.k)
+    return O.Crit(c.kind, c.epsilon, k=c.k, u=c.u, v=c.v)
 
 
 @pytest.mark.parametrize("case,world", [("rmat12", 2), ("rmat12", 3), ("rmat12_score", 2),
-                                        ("grid", 2)])
+                                        ("grid", 2), ("grid_ranking", 2),
+                                        ("rmat12_ranking", 3), ("rmat12_pair", 2)])
 def test_sharded_run_equals_single_process(case, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -377,3 +377,43 @@ def test_heavy_segment_pass_then_full_level_k1(seed):
         np.testing.assert_array_equal(st.upper, fresh.upper)
     finally:
         _lib.check(L.kb_tune(b"dyn.heavy_dense", 256))
+
+
+@pytest.mark.parametrize("nb", [100, 1000, 10000])
+def test_rmat_s16_updates_match_oracle_update_batch(nb):
+    """C5's rule pinned against the oracle's update_batch (dynamic.py:126-211
+    restated; tests/test_oracle.py pins it to the reference's own golden
+    sequences): on R-MAT s16 ef16 with 1e2 / 1e3 / 1e4-edge insertion
+    batches, UpdateStats are identical field by field (level sizes, abort
+    level, visited, reactivated, resumed iterations) and the bounds agree
+    within 1e-12 (the reference's delta pushes vs the device's pull
+    recompute).  The batch comes in as an (m, 2) int64 array."""
+    n = 65536
+    g0 = O.rmat_graph(n, edge_factor=16, seed=42)
+    g = P.Graph.from_csr(n, g0.indptr, g0.indices)
+    crit = P.Criterion.top_k(100, 1e-6)
+    st = P.init(g, crit, undirected=True)
+    P.run(st, g)
+    deg = np.diff(g0.indptr)
+    dmax = int(deg.max())
+    rng = np.random.default_rng(7 + nb)
+    cand = rng.integers(0, n, size=(4 * nb, 2))
+    cand = np.sort(cand[cand[:, 0] != cand[:, 1]], axis=1)
+    cand = np.unique(cand, axis=0)
+    cand = cand[(deg[cand[:, 0]] + 1 < dmax) & (deg[cand[:, 1]] + 1 < dmax)]
+    cand = cand[~g._has_keys(cand[:, 0] * n + cand[:, 1])]
+    e = cand[rng.permutation(cand.shape[0])[:nb]]
+    arcs = np.concatenate([e, e[:, ::-1]])
+    P.update_batch(st, g, P.EdgeBatch(insertions=arcs))
+    stats = st.last_update_stats
+    og = O.AdjGraph.from_csr(g0)
+    ost = O.OracleState(og, O.Crit("topk", 1e-6, k=100))
+    O.run(ost, og)
+    ostats = O.update_batch(ost, og, [tuple(x) for x in arcs.tolist()], [])
+    for f in ("batch_size", "seeds", "visited", "level_sizes", "reactivated",
+              "aborted_level", "resumed_iterations"):
+        assert getattr(stats, f) == getattr(ostats, f), f
+    assert st.r == ost.r
+    np.testing.assert_allclose(st.lower, ost.lower, rtol=REL, atol=0)
+    np.testing.assert_allclose(st.upper, ost.upper, rtol=REL, atol=0)
+    assert P.ranking_result(st).top(100) == O.ranking_result(ost).top(100)

@@ -228,3 +228,26 @@ def test_stale_graph_rejected():
     st2 = P.init(g, P.Criterion.ranking(1e-6))
     with pytest.raises(P.StateError):
         P.check_converged(st2)
+
+
+def test_k_boundary_ties_are_detected_and_reported():
+    """SURVEY.md 8(c) rule 4: on a cycle every node ties every other, so the
+    top-2 cut drops tied nodes once their gap < eps -- where the reference's
+    argpartition (engine.py:359) picks arbitrarily.  The state counts them
+    and run() warns; the certified order is unaffected (node-id ties)."""
+    n = 12
+    g = P.Graph.from_edges(n, [(i, (i + 1) % n) for i in range(n)], undirected=True)
+    st = P.init(g, P.Criterion.top_k(2, 1e-6), undirected=True)
+    with pytest.warns(P.KBoundaryTieWarning):
+        res = P.run(st, g)
+    assert st.k_boundary_ties > 0
+    assert list(res.order) == list(range(n))
+    # R-MAT bounds never tie at the cut (SURVEY.md 8(c) margins)
+    g0 = O.rmat_graph(4096, edge_factor=16, seed=3)
+    g2 = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    st2 = P.init(g2, P.Criterion.top_k(50, 1e-9), undirected=True)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("error", P.KBoundaryTieWarning)
+        P.run(st2, g2)
+    assert st2.k_boundary_ties == 0

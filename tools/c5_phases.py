@@ -20,7 +20,7 @@ e = e[(deg[e[:, 0]] + 1 < deg.max()) & (deg[e[:, 1]] + 1 < deg.max())][:b]
 e = e[~g._present(e)]
 arcs = np.concatenate([e, e[:, ::-1]])
 t = [time.perf_counter()]
-batch = P.EdgeBatch(insertions=[tuple(x) for x in arcs.tolist()]); t.append(time.perf_counter())
+batch = P.EdgeBatch(insertions=arcs); t.append(time.perf_counter())
 batch.arrays(); t.append(time.perf_counter())
 g.validate_batch(batch); t.append(time.perf_counter())
 batch.is_symmetric(); t.append(time.perf_counter())
