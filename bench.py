@@ -732,6 +732,20 @@ def main():
                       "global_gather_sectors": int(sec - stream_sectors),
                       "hot_set_gathers": shared_gathers,
                       "source": f"profiles/{name} (ncu, one K1 launch)"}
+    floor = os.path.join(ROOT, "profiles", "r02_k1_c2_gather_floor.json")
+    if gather is not None and a.scale == 24 and os.path.exists(floor):
+        # the unit that binds K1: each 8-byte gather that misses L1 is one
+        # 32-byte sector request over the L1->XBAR interface (ncu source and
+        # raw pages, one K1 launch)
+        with open(floor) as fh:
+            fj = json.load(fh)
+        mt = fj["metrics"]
+        gather["binding_unit"] = {
+            "unit": "L1->XBAR sector requests per SM-cycle",
+            "achieved": fj["floor"]["miss_requests_per_sm_cycle"],
+            "busy_frac": float(mt["l1tex__m_l1tex2xbar_req_cycles_active.avg."
+                                  "pct_of_peak_sustained_elapsed"]) / 100.0,
+            "source": "profiles/r02_k1_c2_gather_floor.json"}
 
     # ---- e2e through the public API with host buffers
     e2e = None

@@ -70,6 +70,7 @@ struct IterArgs {
     double *peer[KB_MAX_PEERS];
     const int32_t *hrow, *vrow;     // explicit row maps (nullptr: implicit)
     int hot;
+    int warm;                       // XL 3/4 tier boundary (ids < warm: L1 evict_last)
     // sharded graphs: the hot set is the head of every rank's block of the
     // exchange layout (hot_per entries each, blocks of 2^hot_shift ids)
     int hot_per, hot_shift;
@@ -84,6 +85,7 @@ __device__ __forceinline__ bool aborted(const IterArgs &A) {
 struct HotMap {
     int hot, per, shift;
     uint32_t mask;
+    int warm;     // XL 3/4: ids in [hot, warm) are the L1-resident tier
 };
 
 // XL: 0 = ld.global.nc (read-only path, L1 allocate), 1 = ld.global.cg
@@ -98,9 +100,26 @@ __device__ __forceinline__ double ldx(const double *p) {
     return r;
 }
 
+// XL 3: ids in [hot, warm) load with L1::evict_last, colder ones with
+// L1::no_allocate (they never displace the warm tier); XL 4: evict_last /
+// evict_first
+template <int XL>
+__device__ __forceinline__ double ldx_tier(const double *p, bool warm) {
+    double r;
+    if (warm) {
+        asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    } else if (XL == 3) {
+        asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    } else {
+        asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    }
+    return r;
+}
+
 template <int XL, bool ST>
 __device__ __forceinline__ double fetch(const double *__restrict__ hot_s, const HotMap &hm,
                                         const double *__restrict__ x, int32_t c) {
+    if (XL >= 3 && !ST) return (c < hm.hot) ? hot_s[c] : ldx_tier<XL>(x + c, c < hm.warm);
     if (!ST) return (c < hm.hot) ? hot_s[c] : ldx<XL>(x + c);
     const int j = (int)((uint32_t)c & hm.mask);
     return (j < hm.per) ? hot_s[(c >> hm.shift) * hm.per + j] : ldx<XL>(x + c);
@@ -208,7 +227,7 @@ template <int DEPTH, int XL, bool ST = false>
 __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     if (aborted(A)) return;
     extern __shared__ double hot_s[];
-    const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u};
+    const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u, A.warm};
     // The hot set is one contiguous range (or, for a shard, the head of
     // every rank's block): TMA bulk copies global -> shared, completing on
     // an mbarrier, while the CTA's threads only wait.
@@ -329,7 +348,7 @@ __global__ void __launch_bounds__(1024, 2) k_sell_narrow(IterArgs A) {
     if (aborted(A)) return;
     const int lane = threadIdx.x & 31;
     const uint64_t pol = evict_first_policy();
-    const HotMap hm{0, 0, 0, 0u};
+    const HotMap hm{0, 0, 0, 0u, 0};
     const int64_t groups = (A.nslices + Q - 1) / Q;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -487,6 +506,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     A.hrow = g.implicit_rows ? nullptr : g.hrow.p;
     A.vrow = g.implicit_rows ? nullptr : g.vrow.p;
     A.hot = (int)std::min<int64_t>(tune_get("k1.hot", g.hot), n);
+    A.warm = (int)std::min<int64_t>(tune_get("k1.warm", 0), n);
     A.hot_per = 0;
     A.hot_shift = 0;
     const bool strided = g.hot_per > 0 && tune_get("k1.shard_hot", 1);
@@ -531,14 +551,17 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     const int threads = (int)tune_get("k1.threads", 1024);
     const int ctas = (int)tune_get("k1.ctas_per_sm", 1);
     auto kern = k_sell_iterate<2, 0>;
-    if (depth == 1) kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2> : k_sell_iterate<1, 0>;
+    if (depth == 1)
+        kern = xl == 1 ? k_sell_iterate<1, 1> : xl == 2 ? k_sell_iterate<1, 2>
+             : xl == 3 ? k_sell_iterate<1, 3> : xl == 4 ? k_sell_iterate<1, 4>
+                       : k_sell_iterate<1, 0>;
     else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
     else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
     if (strided)
         kern = depth == 3 ? k_sell_iterate<3, 0, true>
              : depth == 2 ? k_sell_iterate<2, 0, true> : k_sell_iterate<1, 0, true>;
-    static bool attr_done[64][12] = {};
-    const int kid = strided ? 9 + (depth - 1) : (depth - 1) * 3 + xl;
+    static bool attr_done[64][16] = {};
+    const int kid = strided ? 9 + (depth - 1) : xl >= 3 ? 12 + (xl - 3) : (depth - 1) * 3 + xl;
     if (!attr_done[g.device][kid]) {
         KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024 - 64));
