@@ -86,7 +86,14 @@ struct HotMap {
     int hot, per, shift;
     uint32_t mask;
     int warm;     // XL 3/4: ids in [hot, warm) are the L1-resident tier
+    int rank;     // ST >= 2 (cluster hot set): this CTA's rank in the cluster
+    uint32_t sbase;  // shared::cta address of hot_s
 };
+
+template <int ST>
+struct Log2 { static constexpr int v = ST <= 1 ? 0 : 1 + Log2<ST / 2>::v; };
+template <>
+struct Log2<1> { static constexpr int v = 0; };
 
 // XL: 0 = ld.global.nc (read-only path, L1 allocate), 1 = ld.global.cg
 // (L2 only), 2 = ld.global.ca with an L2 evict_last hint
@@ -116,9 +123,24 @@ __device__ __forceinline__ double ldx_tier(const double *p, bool warm) {
     return r;
 }
 
-template <int XL, bool ST>
+template <int XL, int ST>
 __device__ __forceinline__ double fetch(const double *__restrict__ hot_s, const HotMap &hm,
                                         const double *__restrict__ x, int32_t c) {
+    if (ST >= 2) {
+        // cluster hot set: the hm.hot hottest ids are dealt round-robin over
+        // the ST CTAs of the cluster (id c lives in CTA c mod ST, slot c / ST);
+        // a local slot is a shared-memory load, a remote one a DSMEM load
+        // over the cluster network -- off the L1->L2 request path
+        if (c >= hm.hot) return ldx<XL>(x + c);
+        const int owner = c & (ST - 1);
+        const uint32_t la = hm.sbase + ((uint32_t)(c >> Log2<ST>::v) << 3);
+        if (owner == hm.rank) return hot_s[c >> Log2<ST>::v];
+        uint32_t ra;
+        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(owner));
+        double r;
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(r) : "r"(ra));
+        return r;
+    }
     if (XL >= 3 && !ST) return (c < hm.hot) ? hot_s[c] : ldx_tier<XL>(x + c, c < hm.warm);
     if (!ST) return (c < hm.hot) ? hot_s[c] : ldx<XL>(x + c);
     const int j = (int)((uint32_t)c & hm.mask);
@@ -143,7 +165,7 @@ __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s)
 
 // Gather of one batch of 8 column slots (two int4 groups) of a lane's row;
 // slots at or beyond the row length read as +0.0 without touching memory.
-template <int XL, bool ST>
+template <int XL, int ST>
 __device__ __forceinline__ void gather8(const double *__restrict__ hot_s, const HotMap &hm,
                                         const double *__restrict__ x, int4 ca, int4 cb,
                                         int jb, int len, double v[8]) {
@@ -176,7 +198,7 @@ __device__ __forceinline__ void epilogue_k(const IterArgs &A, int64_t v, double 
 // the loads of batch i+1..i+DEPTH-1 are issued before batch i is folded, so
 // the in-order dependent add chain never waits on a single batch's latency.
 // four narrow slices (width <= 4) from slice s0 on, folded per lane
-template <int XL, bool ST, int Q = 4>
+template <int XL, int ST, int Q = 4>
 __device__ __forceinline__ void narrow_group(const IterArgs &A, int64_t s0, int lane,
                                              const double *__restrict__ hot_s,
                                              const HotMap &hm, const double *__restrict__ x,
@@ -223,17 +245,28 @@ __device__ __forceinline__ void narrow_group(const IterArgs &A, int64_t s0, int 
     }
 }
 
-template <int DEPTH, int XL, bool ST = false>
+template <int DEPTH, int XL, int ST = 0>
 __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
     if (aborted(A)) return;
     extern __shared__ double hot_s[];
-    const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u, A.warm};
+    unsigned crank = 0;
+    if (ST >= 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const HotMap hm{A.hot, A.hot_per, A.hot_shift, (1u << A.hot_shift) - 1u, A.warm, (int)crank,
+                    (uint32_t)__cvta_generic_to_shared(hot_s)};
     // The hot set is one contiguous range (or, for a shard, the head of
     // every rank's block): TMA bulk copies global -> shared, completing on
     // an mbarrier, while the CTA's threads only wait.
-    const int nseg_hot = ST ? (A.hot_per > 0 ? A.hot / A.hot_per : 0) : 1;
-    const int seg_len = ST ? A.hot_per : A.hot;
-    if (A.hot > 0 && (seg_len & 1) == 0 && nseg_hot >= 1) {
+    const int nseg_hot = ST == 1 ? (A.hot_per > 0 ? A.hot / A.hot_per : 0) : 1;
+    const int seg_len = ST == 1 ? A.hot_per : A.hot;
+    if (ST >= 2) {
+        // this CTA's share of the cluster hot set: ids crank, crank+ST, ...
+        constexpr int CS = ST >= 2 ? ST : 1;
+        for (int i = threadIdx.x; i < A.hot / CS; i += blockDim.x)
+            hot_s[i] = A.x[(int64_t)i * CS + crank];
+        // every CTA's share is in place before any remote read
+        asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                     "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (A.hot > 0 && (seg_len & 1) == 0 && nseg_hot >= 1) {
         __shared__ __align__(8) unsigned long long bar;
         const unsigned sbar = (unsigned)__cvta_generic_to_shared(&bar);
         const unsigned sdst = (unsigned)__cvta_generic_to_shared(hot_s);
@@ -247,7 +280,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                          ::"r"(sbar), "r"(bytes * (unsigned)nseg_hot) : "memory");
             for (int r = 0; r < nseg_hot; r++) {
-                const double *src = ST ? A.x + ((int64_t)r << A.hot_shift) : A.x;
+                const double *src = ST == 1 ? A.x + ((int64_t)r << A.hot_shift) : A.x;
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
                              "[%0], [%1], %2, [%3];"
                              ::"r"(sdst + (unsigned)r * bytes), "l"(src), "r"(bytes), "r"(sbar)
@@ -258,7 +291,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         while (!done)
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
                          "  selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(sbar) : "memory");
-    } else if (ST) {
+    } else if (ST == 1) {
         for (int i = threadIdx.x; i < A.hot; i += blockDim.x) {
             const int r = i / A.hot_per, j = i - r * A.hot_per;
             hot_s[i] = A.x[((int64_t)r << A.hot_shift) + j];
@@ -338,6 +371,9 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
         }
     }
     if (A.npeer) __threadfence_system();  // peer stores visible before the next collective
+    if (ST >= 2)   // no CTA leaves while the others may still read its share
+        asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                     "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Graphs whose slices are all narrow (width <= 4: grids, meshes): no hot
@@ -558,8 +594,8 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     else if (depth == 3) kern = xl == 1 ? k_sell_iterate<3, 1> : xl == 2 ? k_sell_iterate<3, 2> : k_sell_iterate<3, 0>;
     else kern = xl == 1 ? k_sell_iterate<2, 1> : xl == 2 ? k_sell_iterate<2, 2> : k_sell_iterate<2, 0>;
     if (strided)
-        kern = depth == 3 ? k_sell_iterate<3, 0, true>
-             : depth == 2 ? k_sell_iterate<2, 0, true> : k_sell_iterate<1, 0, true>;
+        kern = depth == 3 ? k_sell_iterate<3, 0, 1>
+             : depth == 2 ? k_sell_iterate<2, 0, 1> : k_sell_iterate<1, 0, 1>;
     static bool attr_done[64][16] = {};
     const int kid = strided ? 9 + (depth - 1) : xl >= 3 ? 12 + (xl - 3) : (depth - 1) * 3 + xl;
     if (!attr_done[g.device][kid]) {
@@ -568,6 +604,16 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         attr_done[g.device][kid] = true;
     }
     const size_t smem = (size_t)A.hot * sizeof(double);
+    // k1.cluster = 2/4/8: the hot set spans a thread-block cluster (DSMEM)
+    const int cl = strided ? 0 : (int)tune_get("k1.cluster", 0);
+    auto ckern = cl == 4 ? k_sell_iterate<1, 0, 4> : cl == 8 ? k_sell_iterate<1, 0, 8>
+                                                   : k_sell_iterate<1, 0, 2>;
+    size_t csmem = 0;
+    if (cl >= 2 && !ones) {
+        const int64_t per = std::min<int64_t>(tune_get("k1.hot", g.hot), n / cl);
+        A.hot = (int)(per * cl);
+        csmem = (size_t)per * sizeof(double);
+    }
     if (A.nslices && !ones && !s.counter_zeroed)
         KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
     s.counter_zeroed = false;
@@ -584,6 +630,42 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         else k_sell_narrow<2><<<g.sm_count * 2, 1024, 0, st>>>(A);
         note_launch();
         KB_CUDA(cudaGetLastError());
+    } else if (A.nslices && cl >= 2) {
+        // cluster hot set: cl CTAs share cl x hot ids over DSMEM
+        static int max_clusters[64][4] = {};
+        const int ci = cl == 2 ? 0 : cl == 4 ? 1 : 2;
+        if (!max_clusters[g.device][ci]) {
+            KB_CUDA(cudaFuncSetAttribute(ckern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024 - 64));
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((unsigned)(g.sm_count / cl * cl));
+            q.blockDim = dim3(1024);
+            q.dynamicSmemBytes = csmem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = (unsigned)cl;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int mc = 0;
+            KB_CUDA(cudaOccupancyMaxActiveClusters(&mc, ckern, &q));
+            max_clusters[g.device][ci] = std::max(1, mc);
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(max_clusters[g.device][ci] * cl));
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = csmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        KB_CUDA(cudaLaunchKernelEx(&cfg, ckern, A));
+        note_launch();
     } else if (A.nslices) {
         kern<<<g.sm_count * ctas, threads, smem, st>>>(A); note_launch();
         KB_CUDA(cudaGetLastError());

@@ -4,6 +4,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -27,7 +28,15 @@ __global__ void k_gather(const double *g, int64_t gsize, int H, int iters, doubl
         for (int q = 0; q < 8; q++) {
             st = hash32(st + q);
             if (MODE == 0) v[q] = sm[st % H];
-            else if (MODE == 1) {
+            else if (MODE >= 3 && (MODE == 3 ? (q & 1) : (q & 3) == 3)) {
+                // mixed: a share of the loads go to the cluster's DSMEM, the
+                // rest to the global array (both paths in flight together)
+                const uint32_t idx = st % (uint32_t)(H * csize);
+                const double *rp = cl.map_shared_rank(sm, idx / H);
+                v[q] = rp[idx % H];
+            } else if (MODE >= 3) {
+                v[q] = __ldg(g + (st % (uint32_t)gsize));
+            } else if (MODE == 1) {
                 const uint32_t idx = st % (uint32_t)(H * csize);
                 const double *rp = cl.map_shared_rank(sm, idx / H);
                 v[q] = rp[idx % H];
@@ -46,16 +55,17 @@ int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int H = 24576, threads = 1024, iters = 200;
-    int64_t gsize = 8 << 20;  // 64 MB: L2 resident
+    int64_t gsize = (int64_t)(getenv("GSIZE") ? atoll(getenv("GSIZE")) : (8 << 20));
     double *g, *out;
     unsigned long long *cyc;
     cudaMalloc(&g, gsize * 8);
     cudaMemset(g, 0, gsize * 8);
     cudaMalloc(&out, (size_t)sms * 2 * threads * 8);
     cudaMalloc(&cyc, 8);
-    for (int mode = 0; mode < 3; mode++) {
+    for (int mode = 0; mode < 5; mode++) {
         for (int cs : {1, 2, 4, 8}) {
-            if (mode != 1 && cs > 1) continue;
+            if ((mode == 0 || mode == 2) && cs > 1) continue;
+            if (mode >= 3 && cs == 1) continue;
             int grid = (sms / cs) * cs;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = grid;
@@ -68,7 +78,8 @@ int main() {
             at[0].val.clusterDim.z = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            auto kern = mode == 0 ? k_gather<0> : mode == 1 ? k_gather<1> : k_gather<2>;
+            auto kern = mode == 0 ? k_gather<0> : mode == 1 ? k_gather<1> : mode == 2 ? k_gather<2>
+                      : mode == 3 ? k_gather<3> : k_gather<4>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H * 8);
             cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             for (int rep = 0; rep < 2; rep++) {
@@ -87,7 +98,8 @@ int main() {
                 double cyc_per_block = (double)c / grid;
                 if (rep == 1)
                     printf("mode=%s cluster=%d err=%s time=%.3f ms gathers/SM-cycle=%.3f (Ggathers/s %.1f)\n",
-                           mode == 0 ? "local-smem" : mode == 1 ? "dsmem" : "global-L2", cs,
+                           mode == 0 ? "local-smem" : mode == 1 ? "dsmem" : mode == 2 ? "global"
+                           : mode == 3 ? "1:1 dsmem+global" : "1:3 dsmem+global", cs,
                            cudaGetErrorString(err), ms,
                            gathers / grid / cyc_per_block, gathers / (ms * 1e-3) / 1e9);
             }
