@@ -80,6 +80,29 @@ __device__ __forceinline__ bool flag_set(const unsigned long long *f) {
     return f && *(const volatile unsigned long long *)f != 0;
 }
 
+// The check's verdict, published by the kernel that finishes the check (one
+// thread, after the result words are final): the abort flag for the K1s
+// queued behind (they exit when it is set), that K1's work counter reset,
+// the new |active| as the next check's input, and the result words written
+// straight into page-locked host memory (no separate copy).
+struct Publish {
+    unsigned long long *abort, *k1_counter;
+    volatile unsigned long long *host;
+    int64_t level;
+};
+
+__device__ __forceinline__ void publish(const Publish &p, unsigned long long *out) {
+    if (!p.abort) return;
+    *p.abort = out[1];
+    if (p.k1_counter) *p.k1_counter = 0ull;
+    out[7] = out[0];
+    p.host[0] = out[0];
+    p.host[1] = out[1];
+    p.host[2] = out[2];
+    p.host[3] = (unsigned long long)p.level;
+    __threadfence_system();
+}
+
 // digit plan: two 12-bit digits over all elements, then the survivors of the
 // 24-bit prefix are compacted and five 8-bit digits finish on them; ties at
 // the cut take four 8-bit digits of the original id
@@ -461,7 +484,7 @@ __global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const
                                                       int64_t k,
                                                       const unsigned long long *abort = nullptr,
                                                       const unsigned long long *m_dev = nullptr,
-                                                      int64_t m_min = -1) {
+                                                      int64_t m_min = -1, Publish pub = {}) {
     if (flag_set(abort)) return;
     if (m_dev && (int64_t)*(const volatile unsigned long long *)m_dev <= m_min) return;
     extern __shared__ unsigned char smem[];
@@ -510,7 +533,10 @@ __global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const
         if (i >= 1 && !(__dsub_rn(upper[nid[i]], eps) < lower[nid[i - 1]])) bad = 1;
     }
     __syncthreads();
-    if (threadIdx.x == 0) out[1] = (mnew <= k) && !bad;
+    if (threadIdx.x == 0) {
+        out[1] = (mnew <= k) && !bad;
+        publish(pub, out);
+    }
 }
 
 // The whole TOPK check for a small active set (m <= SMALL_M, the last
@@ -527,12 +553,12 @@ __global__ void __launch_bounds__(1024) k_topk_small(const double *lower, const 
                                                      int32_t *act_out, unsigned long long *out,
                                                      double eps, int64_t k,
                                                      const unsigned long long *abort,
-                                                     unsigned long long *ties) {
+                                                     unsigned long long *ties, Publish pub) {
     if (flag_set(abort)) return;
     const int64_t m = m_dev ? (int64_t)*(const volatile unsigned long long *)m_dev : m_host;
     if (m > m_max) return;
     if (m == 0) {
-        if (threadIdx.x == 0) { out[0] = 0; out[1] = 1; out[2] = 0; }
+        if (threadIdx.x == 0) { out[0] = 0; out[1] = 1; out[2] = 0; publish(pub, out); }
         return;
     }
     extern __shared__ unsigned char smem[];
@@ -596,6 +622,7 @@ __global__ void __launch_bounds__(1024) k_topk_small(const double *lower, const 
         out[0] = (unsigned long long)base;          // |active| after the cut
         out[1] = (base <= k) && !bad;
         out[2] = (unsigned long long)W;
+        publish(pub, out);
     }
 }
 
@@ -1302,25 +1329,6 @@ bool run_check(State &s, cudaStream_t st) {
 }
 
 namespace {
-// the check's verdict: abort flag for the K1s queued behind (they exit when
-// it is set), that K1's work counter reset, the new |active| as the next
-// check's input, and the result words written straight into page-locked
-// host memory (no separate copy).  A check behind a converged one does
-// nothing (its inputs are stale): the host words keep the converged check's.
-__global__ void k_publish(unsigned long long *out, unsigned long long *abort,
-                          unsigned long long *k1_counter, volatile unsigned long long *host,
-                          int64_t level) {
-    if (*(volatile unsigned long long *)abort) return;
-    *abort = out[1];
-    *k1_counter = 0ull;
-    out[7] = out[0];
-    host[0] = out[0];
-    host[1] = out[1];
-    host[2] = out[2];
-    host[3] = (unsigned long long)level;
-    __threadfence_system();
-}
-
 // size classes of the device-driven select: one cooperative launch each,
 // only the one whose class holds the runtime |active| does any work
 constexpr int64_t SMALL_M = 4096, MID_M = 1 << 18, MID_G = 32;
@@ -1329,8 +1337,8 @@ constexpr int64_t SMALL_M = 4096, MID_M = 1 << 18, MID_G = 32;
 // Enqueue one TOPK check (engine.py:333-379) with no host read.  m_host >= 0:
 // |active| is known on the host (grid sized for it); m_host < 0: it is the
 // previous check's count, read on the device (device-driven run).  The
-// active set moves from act[cur] to act[cur ^ 1]; the verdict is published by
-// k_publish tagged with `level`.  Returns the new ping-pong index.
+// active set moves from act[cur] to act[cur ^ 1]; the kernel that finishes the
+// check publishes the verdict tagged with `level`.  Returns the new index.
 int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense, int cur,
                            int64_t level) {
     Graph &g = *s.g;
@@ -1376,19 +1384,20 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
         attr_done[g.device] = true;
         attr_smem[g.device] = smem;
     }
+    const Publish pub{s.abort_flag.p, s.work_counter.p, s.h_flags, level};
     auto small = [&](int64_t mh, const unsigned long long *md) {
         int Ps = 1;
         while (Ps < (mh >= 0 ? mh : SMALL_M)) Ps <<= 1;
         k_topk_small<<<1, 1024, (size_t)Ps * 16, st>>>(s.lower.p, s.upper.p, g.labels(),
                                                        s.act[cur].p, dense ? 1 : 0, mh, md,
                                                        SMALL_M, s.act[nxt].p, out, s.eps, k,
-                                                       s.abort_flag.p, s.tie_count.p);
+                                                       s.abort_flag.p, s.tie_count.p, pub);
         note_launch();
     };
     auto finish = [&](const unsigned long long *md) {
         k_topk_finish<<<1, 1024, smem, st>>>(s.lower.p, s.upper.p, g.labels(), A.prefix_buf, 0,
                                              s.act[nxt].p, out, s.eps, k, s.abort_flag.p, md,
-                                             SMALL_M);
+                                             SMALL_M, pub);
         note_launch();
     };
     if (m_host >= 0) {
@@ -1419,8 +1428,6 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
         }
         finish(out + 7);
     }
-    k_publish<<<1, 1, 0, st>>>(out, s.abort_flag.p, s.work_counter.p, s.h_flags, level);
-    note_launch();
     KB_CUDA(cudaGetLastError());
     s.counter_zeroed = true;
     return nxt;

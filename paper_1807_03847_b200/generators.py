@@ -75,7 +75,11 @@ class DeviceResidentGraph:
         return bool(self._present(self._arcs([(u, v)]))[0])
 
     def max_out_degree(self) -> int:
-        return self.max_degree_after(EdgeBatch())
+        c = getattr(self, "_maxdeg", None)
+        if c is None or c[0] != self.version:        # cached per version
+            c = (self.version, self.max_degree_after(EdgeBatch()))
+            self._maxdeg = c
+        return c[1]
 
     def max_degree_after(self, batch: EdgeBatch) -> int:
         """dynamic.py:151-157 evaluated on the device."""
