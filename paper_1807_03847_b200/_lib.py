@@ -12,7 +12,10 @@ import os
 from .errors import (BatchPreconditionError, ConvergenceError, DeviceError,
                      NodeRangeError, NumericError, ParameterError, StateError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+# KB_LIB=checked loads the checked build (device invariants polled after
+# every call; `make -C paper_1807_03847_b200/csrc checked`)
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        "_lib_checked" if os.environ.get("KB_LIB") == "checked" else "_lib",
                         "libkatzb200.so")
 
 KB_OK, KB_EPARAM, KB_ESTATE, KB_ECONVERGENCE, KB_ENUMERIC = 0, 1, 2, 3, 4

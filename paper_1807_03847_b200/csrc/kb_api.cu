@@ -50,6 +50,39 @@ void note_launch(int64_t k) { g_launches += k; }
 int64_t launch_count() { return g_launches.load(); }
 void set_error(const std::string &msg) { t_err = msg; }
 
+#ifdef KB_CHECKED
+namespace {
+struct DcheckReader {
+    void (*read)(unsigned long long *, int *);
+    const char *file;
+};
+std::vector<DcheckReader> &dcheck_readers() {
+    static std::vector<DcheckReader> v;
+    return v;
+}
+}  // namespace
+int dcheck_register(void (*read)(unsigned long long *, int *), const char *file) {
+    dcheck_readers().push_back({read, file});
+    return 1;
+}
+void dcheck_poll() {
+    if (cudaDeviceSynchronize() != cudaSuccess) return;   // the call's own error wins
+    for (auto &r : dcheck_readers()) {
+        unsigned long long f = 0;
+        int line = 0;
+        r.read(&f, &line);
+        if (f) {
+            char buf[256];
+            snprintf(buf, sizeof buf, "KB_DCHECK failed %llu time(s), last at %s:%d",
+                     f, r.file, line);
+            throw Error{KB_ECUDA, buf};
+        }
+    }
+}
+#else
+void dcheck_poll() {}
+#endif
+
 cudaStream_t device_stream() {
     static std::mutex mu;
     static cudaStream_t streams[64] = {};
@@ -219,6 +252,9 @@ __global__ void k_range32(int64_t lo, int64_t m, int32_t *out) {
     if (i < m) out[i] = (int32_t)(lo + i);
 }
 
+// checked build self-test: one failing KB_DCHECK (tests/test_checked_build.py)
+__global__ void k_dcheck_selftest(int v) { KB_DCHECK(v == 0); (void)v; }
+
 __global__ void k_sep_one(const double *lower, const double *upper, const int32_t *iperm,
                           int64_t w, int64_t v, double eps, unsigned long long *out) {
     out[0] = lower[iperm[w]] > __dsub_rn(upper[iperm[v]], eps);
@@ -239,6 +275,7 @@ int guarded(F &&f) {
     }
     try {
         f();
+        dcheck_poll();
         return KB_OK;
     } catch (const Error &e) {
         set_error(e.msg);
@@ -494,6 +531,10 @@ int kb_state_vector_ptr(kb_state *h, int which, int64_t level, void **ptr) {
 int kb_sync(int device) {
     return guarded([&] {
         use_device(device);
+        if (tune_get("dcheck.selftest", 0)) {
+            k_dcheck_selftest<<<1, 1, 0, device_stream()>>>(1);
+            note_launch();
+        }
         KB_CUDA(cudaStreamSynchronize(device_stream()));
     });
 }

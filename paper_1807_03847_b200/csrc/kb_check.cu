@@ -74,6 +74,7 @@ struct TopkArgs {
     // are dropped (gap < eps) -- where numpy's arbitrary argpartition choice
     // (engine.py:359) could have kept them -- are counted here
     unsigned long long *ties = nullptr;
+    int64_t act_cap = INT64_MAX;    // capacity of act_out (checked build)
 };
 
 __device__ __forceinline__ bool flag_set(const unsigned long long *f) {
@@ -446,6 +447,8 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
         const uint8_t c = in ? cls[i] : 0;
         const unsigned bw = __ballot_sync(0xffffffffu, c == 2);
         const unsigned bs = __ballot_sync(0xffffffffu, c == 1);
+        KB_DCHECK(c != 2 || ow + __popc(bw & lt) < (unsigned long long)A.k);
+        KB_DCHECK(c != 1 || A.k + (int64_t)(os + __popc(bs & lt)) < A.act_cap);
         if (c == 2) A.prefix_buf[ow + __popc(bw & lt)] = id_at(i);
         else if (c == 1) A.act_out[A.k + (int64_t)(os + __popc(bs & lt))] = id_at(i);
         ow += __popc(bw);
@@ -490,6 +493,7 @@ __global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const
     extern __shared__ unsigned char smem[];
     const int64_t cnt = (int64_t)out[2];
     const int64_t mnew = (int64_t)out[0];
+    KB_DCHECK(cnt >= 0 && cnt <= k);
     int P = 1;
     while (P < cnt) P <<= 1;
     uint64_t *hi = (uint64_t *)smem;            // ~key  (ascending = lower desc)
@@ -611,6 +615,7 @@ __global__ void __launch_bounds__(1024) k_topk_small(const double *lower, const 
         __syncthreads();
         int64_t off = base;
         for (int w = 0; w < warp; w++) off += s_cnt[w];
+        KB_DCHECK(!sv || off + __popc(b & ((1u << lane) - 1u)) < m);
         if (sv) act_out[off + __popc(b & ((1u << lane) - 1u))] = id;
         int64_t tile = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); w++) tile += s_cnt[w];
@@ -1369,6 +1374,7 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
     A.abort = s.abort_flag.p;
     A.split = 1;
     A.ties = s.tie_count.p;
+    A.act_cap = (int64_t)s.act[nxt].n;
     void *args[] = {&A};
     const int Gmax = coop_grid(g.sm_count);
     int P = 1;

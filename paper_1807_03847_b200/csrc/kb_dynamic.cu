@@ -239,7 +239,8 @@ __device__ __forceinline__ int64_t lower_bound32(const int32_t *a, int64_t n, in
 __global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dptr,
                               const int32_t *del, const int64_t *iptr, const int32_t *ins,
                               const int64_t *toff, int32_t *tmp, const int64_t *indptr,
-                              int32_t *indices, int32_t *rlen) {
+                              int32_t *indices, int32_t *rlen, const int32_t *rcap = nullptr,
+                              int64_t cap_total = INT64_MAX) {
     const int64_t e = blockIdx.x;  // a block per edited row (hub rows are long)
     const int t = threadIdx.x, nt = blockDim.x;
     if (e >= ne) return;
@@ -263,6 +264,9 @@ __global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dp
     }
     __syncthreads();
     const int64_t nl = L - nd + ni;
+    // the edited row fits its slot (capacity planned on the host) and the array
+    KB_DCHECK(nl >= 0 && (!rcap || nl <= rcap[v]) && indptr[v] + nl <= cap_total);
+    (void)rcap; (void)cap_total;
     for (int64_t j = t; j < nl; j += nt) indices[indptr[v] + j] = out[j];
     if (t == 0) rlen[v] = (int32_t)nl;
 }
@@ -868,7 +872,8 @@ void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int
     KB_CUDA(cudaMemcpyAsync(dtoff.p, toff.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
     k_apply_edits<<<(unsigned)ne, 128, 0, st>>>(drows.p, ne, ddptr.p, ddel.p, diptr.p,
                                                        dins.p, dtoff.p, tmp.p, g.indptr.p,
-                                                       g.indices.p, g.rlen.p);
+                                                       g.indices.p, g.rlen.p, g.rcap.p,
+                                                       (int64_t)g.indices.n);
     note_launch();
     KB_CUDA(cudaGetLastError());
     KB_CUDA(cudaStreamSynchronize(st));

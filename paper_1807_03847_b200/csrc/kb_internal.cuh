@@ -35,6 +35,45 @@ struct Error {
         if (!(cond)) throw ::kb::Error{(code), (msg)};                         \
     } while (0)
 
+// ---------------------------------------------------------------- checked build
+// `make checked` builds the library with -DKB_CHECKED (into _lib_checked/):
+// KB_DCHECK(cond) in a kernel counts a failed invariant (index in range,
+// count within capacity) in a per-translation-unit device word and records
+// the source line, without faulting the context; every C-ABI call ends by
+// reading all those words (dcheck_poll) and returns KB_ECUDA with the
+// file:line of the first failure.  This stands in for compute-sanitizer,
+// which is closed on the GPU pool.  In the normal build KB_DCHECK is empty.
+#ifdef KB_CHECKED
+int dcheck_register(void (*read)(unsigned long long *fails, int *line), const char *file);
+#define KB_DCHECK(c)                                                           \
+    do {                                                                       \
+        if (!(c)) {                                                            \
+            atomicAdd(&kb_dcheck_fail, 1ull);                                  \
+            kb_dcheck_line = __LINE__;                                         \
+        }                                                                      \
+    } while (0)
+namespace {
+__device__ unsigned long long kb_dcheck_fail;
+__device__ int kb_dcheck_line;
+void kb_dcheck_read(unsigned long long *fails, int *line) {
+    unsigned long long f = 0;
+    int l = 0;
+    cudaMemcpyFromSymbol(&f, kb_dcheck_fail, sizeof(f));
+    cudaMemcpyFromSymbol(&l, kb_dcheck_line, sizeof(l));
+    if (f) {                        // reported once, then re-armed
+        const unsigned long long zero = 0;
+        cudaMemcpyToSymbol(kb_dcheck_fail, &zero, sizeof(zero));
+    }
+    *fails = f;
+    *line = l;
+}
+const int kb_dcheck_registered = dcheck_register(kb_dcheck_read, __BASE_FILE__);
+}  // namespace
+#else
+#define KB_DCHECK(c) do { } while (0)
+#endif
+void dcheck_poll();   // throws Error{KB_ECUDA} if any KB_DCHECK failed (checked build)
+
 // named tuning knobs (kb_tune); default when unset
 int64_t tune_get(const char *name, int64_t dflt);
 

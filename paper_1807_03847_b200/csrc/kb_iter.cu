@@ -57,6 +57,7 @@ struct IterArgs {
     const int32_t *slice_w;
     const int32_t *vlen;
     int64_t nslices, nvr, nseg, nh;
+    int64_t ncols;                  // id space (columns < ncols; checked build)
     int64_t nwide;                  // slices >= nwide are narrow: 4 per grab
     const double *x;
     double *w, *katz, *lower, *upper, *seg_sum;
@@ -148,6 +149,7 @@ __device__ __forceinline__ double fetch(const double *__restrict__ hot_s, const 
 }
 
 __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s) {
+    KB_DCHECK(v >= 0 && v < A.ncols);
     const double w = __dmul_rn(A.alpha, s);          // engine.py:306
     for (int q = 0; q < A.npeer; q++) A.peer[q][v] = w;  // NVLink stores to the peers
     if (A.level_only) {
@@ -168,8 +170,11 @@ __device__ __forceinline__ void epilogue(const IterArgs &A, int64_t v, double s)
 template <int XL, int ST>
 __device__ __forceinline__ void gather8(const double *__restrict__ hot_s, const HotMap &hm,
                                         const double *__restrict__ x, int4 ca, int4 cb,
-                                        int jb, int len, double v[8]) {
+                                        int jb, int len, double v[8], int64_t ncols) {
     const int32_t c[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+    for (int q = 0; q < 8; q++) KB_DCHECK(jb + q >= len || (c[q] >= 0 && c[q] < ncols));
+    (void)ncols;
 #pragma unroll
     for (int q = 0; q < 8; q++)
         v[q] = (jb + q < len) ? fetch<XL, ST>(hot_s, hm, x, c[q]) : 0.0;
@@ -230,8 +235,10 @@ __device__ __forceinline__ void narrow_group(const IterArgs &A, int64_t s0, int 
 #pragma unroll
     for (int q = 0; q < Q; q++)
 #pragma unroll
-        for (int j = 0; j < 4; j++)
+        for (int j = 0; j < 4; j++) {
+            KB_DCHECK(j >= len[q] || (cc[q][j] >= 0 && cc[q][j] < A.ncols));
             v[q][j] = (j < len[q]) ? fetch<XL, ST>(hot_s, hm, x, cc[q][j]) : 0.0;
+        }
 #pragma unroll
     for (int q = 0; q < Q; q++) {
         double sum = 0.0;
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
                     const int4 ca = ld_stream_i4(p + (int64_t)g0 * 128, pol);
                     const int4 cb = (g0 + 1 < w4) ? ld_stream_i4(p + (int64_t)(g0 + 1) * 128, pol)
                                                   : zero4;
-                    gather8<XL, ST>(hot_s, hm, x, ca, cb, g0 * 4, len, v[d]);
+                    gather8<XL, ST>(hot_s, hm, x, ca, cb, g0 * 4, len, v[d], A.ncols);
                 }
             }
             for (int b = 0; b < nb; b += DEPTH) {
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(1024, 1) k_sell_iterate(IterArgs A) {
                             const int4 cb = (g0 + 1 < w4)
                                                 ? ld_stream_i4(p + (int64_t)(g0 + 1) * 128, pol)
                                                 : zero4;
-                            gather8<XL, ST>(hot_s, hm, x, ca, cb, g0 * 4, len, v[d]);
+                            gather8<XL, ST>(hot_s, hm, x, ca, cb, g0 * 4, len, v[d], A.ncols);
                         }
                     }
                 }
@@ -411,8 +418,10 @@ __global__ void k_heavy_combine(IterArgs A, const int32_t *seg_ptr,
     int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (h >= A.nh || aborted(A)) return;
     double s = 0.0;
-    for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++)
+    for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++) {
+        KB_DCHECK(seg_list[q] >= 0 && seg_list[q] < A.nseg);
         s = __dadd_rn(s, A.seg_sum[seg_list[q]]);
+    }
     epilogue(A, A.hrow ? A.hrow[h] : h, s);
 }
 
@@ -527,6 +536,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     A.nvr = g.sell.nvr;
     A.nseg = g.sell.nseg;
     A.nh = g.nh;
+    A.ncols = n;
     A.nwide = tune_get("k1.narrow4", 1) ? g.sell.nwide : g.sell.nslices;
     A.x = x;
     A.w = w;
@@ -714,6 +724,7 @@ void run_segments(State &s, cudaStream_t st, const double *x) {
     A.nvr = g.sell.nvr;
     A.nseg = g.sell.nseg;
     A.nh = g.nh;
+    A.ncols = g.n;
     A.nwide = std::min<int64_t>(g.sell.nwide, A.nslices);
     A.x = x;
     A.seg_sum = s.seg_sum.p;

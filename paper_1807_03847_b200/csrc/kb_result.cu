@@ -43,6 +43,7 @@ __global__ void k_sort_keys(const double *lower, const int32_t *iperm, const int
 
 __global__ void k_new_to_orig(const int32_t *perm, const int32_t *nids, int64_t n, int32_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) KB_DCHECK(nids[i] >= 0);
     if (i < n) out[i] = perm[nids[i]];
 }
 

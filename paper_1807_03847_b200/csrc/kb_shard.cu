@@ -79,7 +79,8 @@ __global__ void k_local_len(const int32_t *node_of_exch, const int32_t *rlen, in
 // order, mapped to exchange ids
 __global__ void k_local_cols(const int32_t *node_of_exch, const int64_t *ip_full,
                              const int32_t *ix_full, const int32_t *exch_of_node,
-                             const int64_t *ip_loc, int64_t lo, int64_t hi, int32_t *ix_loc) {
+                             const int64_t *ip_loc, int64_t lo, int64_t hi, int32_t *ix_loc,
+                             int64_t nnz_loc) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t e = lo + warp;
@@ -87,6 +88,8 @@ __global__ void k_local_cols(const int32_t *node_of_exch, const int64_t *ip_full
     const int32_t v = node_of_exch[e];
     if (v < 0) return;
     const int64_t src = ip_full[v], dst = ip_loc[e], L = ip_loc[e + 1] - dst;
+    KB_DCHECK(dst >= 0 && dst + L <= nnz_loc);
+    (void)nnz_loc;
     for (int64_t j = lane; j < L; j += 32) ix_loc[dst + j] = exch_of_node[ix_full[src + j]];
 }
 
@@ -184,7 +187,7 @@ void build_shard(Graph &full, int64_t P, int64_t rank, Graph &out, int64_t *n_pe
     if (n_per)
         k_local_cols<<<nblk(n_per * 32, 256), 256, 0, st>>>(noe.p, full.indptr.p, full.indices.p,
                                                             eon.p, out.indptr.p, lo, hi,
-                                                            out.indices.p);
+                                                            out.indices.p, nnz_loc);
     note_launch();
     out.n = N;
     out.nnz = nnz_loc;
