@@ -1256,30 +1256,21 @@ int kb_run(kb_state *h, int *converged) {
             } restore{s, st};
             launch_iterate(s, st);
             for (;;) {
-                if (ranking_pair_enqueue(s, st)) {
-                    const bool ahead = s.r < s.max_iter;
-                    if (ahead) {
-                        s.spec_abort = true;
+                if (s.rk_q >= 0 && tune_get("check.pair_cache", 1)) {
+                    if (ranking_pair_chain(s, st)) {     // still refuted at s.r
+                        if (s.r >= s.max_iter) {
+                            materialize_bounds(s, st);
+                            const double gap = run_gap(s, st);
+                            char buf[160];
+                            snprintf(buf, sizeof buf,
+                                     "stopping rule still unmet after %lld iterations (widest "
+                                     "bound interval %.3e)", (long long)s.r, gap);
+                            throw Error{KB_ECONVERGENCE, buf};
+                        }
                         launch_iterate(s, st);
-                        s.spec_abort = false;
+                        continue;
                     }
-                    KB_CUDA(cudaEventSynchronize(s.chk_ev));
-                    if (s.h_flags[0]) {              // still refuted: not converged
-                        if (ahead) continue;         // the queued K1 was the next level
-                        materialize_bounds(s, st);
-                        const double gap = run_gap(s, st);
-                        char buf[160];
-                        snprintf(buf, sizeof buf,
-                                 "stopping rule still unmet after %lld iterations (widest "
-                                 "bound interval %.3e)", (long long)s.r, gap);
-                        throw Error{KB_ECONVERGENCE, buf};
-                    }
-                    if (ahead) {                     // the queued K1 did nothing
-                        s.levels.pop_back();
-                        s.r -= 1;
-                        if (s.k1_used >= 2) s.k1_used -= 2;
-                    }
-                    s.rk_q = s.rk_x = -1;
+                    s.rk_q = s.rk_x = -1;                 // the full check decides at s.r
                 }
                 materialize_bounds(s, st);
                 if (run_check(s, st)) { *converged = 1; break; }

@@ -953,7 +953,9 @@ __global__ void k_pair_refutes_pub(const double *katz, const double *w, double a
                                    int undirected, const int32_t *perm, int32_t q, int32_t x,
                                    double eps, unsigned long long *out,
                                    unsigned long long *abort, volatile unsigned long long *host,
-                                   unsigned long long *k1_counter) {
+                                   unsigned long long *k1_counter, int64_t level = -1) {
+    // in a device-driven chain, a test behind a failed one does nothing
+    if (level >= 0 && *(volatile unsigned long long *)abort) return;
     // the two nodes' bounds from katz and the level, as the K1 epilogue forms them
     const double tq = __dmul_rn(alpha, w[q]), tx = __dmul_rn(alpha, w[x]);
     const double lq = undirected ? __dadd_rn(katz[q], tq) : katz[q];
@@ -965,6 +967,7 @@ __global__ void k_pair_refutes_pub(const double *katz, const double *w, double a
     abort[0] = ref ? 0ull : 1ull;
     k1_counter[0] = 0ull;      // the queued K1's work counter (no separate memset)
     host[0] = ref ? 1ull : 0ull;  // straight into page-locked host memory
+    if (level >= 0) host[3] = (unsigned long long)level;
     __threadfence_system();
 }
 
@@ -1296,23 +1299,45 @@ double run_gap(State &s, cudaStream_t st) {
     return g.n ? d : 0.0;
 }
 
-// RANKING with a cached refuting pair: enqueue its test, publish the abort
-// flag for a speculative K1 and start the 8-byte read into h_flags[0]
-// (complete at chk_ev).  false: no pair cached.
-bool ranking_pair_enqueue(State &s, cudaStream_t st) {
-    if (s.rk_q < 0 || !tune_get("check.pair_cache", 1)) return false;
-    s.rank_order_pending = true;
+// RANKING run with a cached refuting pair, the loop on the device: the test
+// of the pair at the current level, then up to `batch` - 1 more levels, each
+// a K1 (lazy bounds) followed by the pair's test, all queued with no host
+// read; a test that no longer refutes sets the abort flag and every kernel
+// behind it exits.  One host wait per chain; the levels queued past the
+// last test that ran are dropped.  Returns true while the pair still
+// refutes at s.r (not converged, caller iterates on), false when it stopped
+// refuting at s.r (the full check decides).  C4: 95 of 99 checks.
+bool ranking_pair_chain(State &s, cudaStream_t st) {
     Graph &g = *s.g;
+    s.rank_order_pending = true;
     if (!s.abort_flag.p) s.abort_flag.alloc(1);
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
-    k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma, s.undirected,
-                                        g.labels(), s.rk_q, s.rk_x, s.eps, s.scratch_u64.p,
-                                        s.abort_flag.p, s.h_flags, s.work_counter.p);
-    note_launch();
+    KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
+    const int64_t batch = std::max<int64_t>(1, tune_get("run.rank_batch", 16));
+    const int64_t r0 = s.r;
+    for (int64_t j = 0; j < batch; j++) {
+        k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma,
+                                            s.undirected, g.labels(), s.rk_q, s.rk_x, s.eps,
+                                            s.scratch_u64.p, s.abort_flag.p, s.h_flags,
+                                            s.work_counter.p, s.r);
+        note_launch();
+        s.counter_zeroed = true;
+        if (j + 1 == batch || s.r >= s.max_iter) break;
+        s.spec_abort = true;           // exits once a test before it stopped refuting
+        launch_iterate(s, st);
+        s.spec_abort = false;
+    }
     KB_CUDA(cudaGetLastError());
-    s.counter_zeroed = true;
     KB_CUDA(cudaEventRecord(s.chk_ev, st));
-    return true;
+    KB_CUDA(cudaEventSynchronize(s.chk_ev));
+    const int64_t last = (int64_t)s.h_flags[3];
+    KB_REQUIRE(last >= r0 && last <= s.r, KB_ECUDA, "device loop lost its verdict");
+    while (s.r > last) {               // levels queued behind a test that stopped refuting
+        s.levels.pop_back();
+        s.r -= 1;
+        if (s.k1_used >= 2) s.k1_used -= 2;
+    }
+    return s.h_flags[0] != 0;
 }
 
 bool run_check(State &s, cudaStream_t st) {

@@ -345,7 +345,7 @@ bool run_check(State &s, cudaStream_t st);      // returns converged
 int topk_check_enqueue(State &s, cudaStream_t st);
 bool topk_run_device(State &s, cudaStream_t st);  // TOPK loop, one host sync per batch
 bool topk_check_finish(State &s, int nxt);
-bool ranking_pair_enqueue(State &s, cudaStream_t st);
+bool ranking_pair_chain(State &s, cudaStream_t st);   // device-driven cached-pair levels
 void materialize_rank_order(State &s, cudaStream_t st);
 double run_gap(State &s, cudaStream_t st);
 void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
