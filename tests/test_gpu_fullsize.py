@@ -116,7 +116,8 @@ def test_C5_batches_match_static_recompute_bitwise():
     """C5 at full size: insertion batches on C2 (1e3 then 1e4 edges, the
     second after the first update's closing check); after each, r, top-100
     and the lower/upper bounds equal a fresh static run on the post-batch
-    graph bit for bit."""
+    graph bit for bit, and the CPU oracle's static run on the post-batch
+    arcs gives the same r, order and top-100 (bounds within 1e-12)."""
     n = 1 << 24
     crit = P.Criterion.top_k(100, 1e-6)
     g = G.rmat_graph(n, edge_factor=16, seed=42)
@@ -140,6 +141,20 @@ def test_C5_batches_match_static_recompute_bitwise():
         assert dyn.top(100) == fresh.top(100)
         np.testing.assert_array_equal(dyn.lower, fresh.lower)
         np.testing.assert_array_equal(dyn.upper, fresh.upper)
+        # ... and the post-batch graph pinned to the CPU oracle (scipy's
+        # order): same r, order and top-100, bounds within 1e-12
+        import os
+
+        from oracle import katz_oracle as O
+        ip, ix = g.csr_arrays()
+        og = O.CSRGraph(n, ip, ix, symmetric=True)
+        ores = O.run(O.OracleState(og, O.Crit("topk", 1e-6, k=100),
+                                   threads=os.cpu_count() or 1), og)
+        assert ores.iterations_used == dyn.iterations_used
+        assert ores.top(100) == dyn.top(100)
+        assert h16(np.asarray(dyn.order, dtype=np.int64)) == h16(ores.order.astype(np.int64))
+        np.testing.assert_allclose(dyn.lower, ores.lower, rtol=RTOL, atol=0)
+        np.testing.assert_allclose(dyn.upper, ores.upper, rtol=RTOL, atol=0)
 
 
 def _c3_golden():
