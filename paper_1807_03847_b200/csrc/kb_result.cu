@@ -189,23 +189,13 @@ void sort_keys_stable(const uint64_t *kin, const int32_t *nids, int64_t m, uint6
     });
 }
 
-// positive-bound nodes by ascending original id, and the rest: from the
-// flags of the current lower bounds (generic) -- or, when the state knows
-// that exactly the rows with out-arcs are positive (static runs), from the
-// lists precomputed at ingest (Graph::orig_pos / orig_zero)
+// positive-bound nodes by ascending original id, and the rest, from the
+// flags of the current lower bounds (after dynamic updates; static runs read
+// the lists precomputed at ingest, Graph::orig_pos / orig_zero, in place)
 static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_t *zero_out,
                            int64_t &npos) {
     Graph &g = *s.g;
     const int64_t n = g.n;
-    if (s.zero_tail_exact && g.orig_pos.p) {
-        npos = g.nv;
-        KB_CUDA(cudaMemcpyAsync(ids.p, g.orig_pos.p, npos * sizeof(int32_t),
-                                cudaMemcpyDeviceToDevice, st));
-        if (n > npos)
-            KB_CUDA(cudaMemcpyAsync(zero_out, g.orig_zero.p, (n - npos) * sizeof(int32_t),
-                                    cudaMemcpyDeviceToDevice, st));
-        return;
-    }
     DBuf<unsigned char> fpos, fzero;
     DBuf<int32_t> iota;
     fpos.alloc(n); fzero.alloc(n); iota.alloc(n);
@@ -239,30 +229,41 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
     KB_REQUIRE(s.r >= 1, KB_ESTATE, "separated_fraction needs at least one iteration");
     DBuf<int32_t> ids, order, nids, snids;
     DBuf<uint64_t> kin, kout;
-    ids.alloc(n); order.alloc(n);
+    order.alloc(n);
     int64_t npos = 0;
-    split_positive(s, st, ids, order.p, npos);  // zero part lands at order[0..)
-    // shift the zero part behind the positive one
-    DBuf<int32_t> zero_part;
-    if (n > npos) {
-        zero_part.alloc(n - npos);
-        KB_CUDA(cudaMemcpyAsync(zero_part.p, order.p, (n - npos) * sizeof(int32_t),
-                                cudaMemcpyDeviceToDevice, st));
+    const int32_t *pos_ids = nullptr;           // positive-bound nodes, ascending id
+    if (s.zero_tail_exact && g.orig_pos.p) {
+        // static runs: exactly the rows with out-arcs are positive, and their
+        // lists were laid out at ingest -- read in place, zero part copied once
+        npos = g.nv;
+        pos_ids = g.orig_pos.p;
+        if (n > npos)
+            KB_CUDA(cudaMemcpyAsync(order.p + npos, g.orig_zero.p, (n - npos) * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, st));
+    } else {
+        ids.alloc(n);
+        split_positive(s, st, ids, order.p, npos);  // zero part lands at order[0..)
+        pos_ids = ids.p;
+        if (n > npos) {                             // shift it behind the positive part
+            DBuf<int32_t> zero_part;
+            zero_part.alloc(n - npos);
+            KB_CUDA(cudaMemcpyAsync(zero_part.p, order.p, (n - npos) * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, st));
+            KB_CUDA(cudaMemcpyAsync(order.p + npos, zero_part.p,
+                                    (n - npos) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        }
     }
     unsigned long long *u = s.scratch_u64.p;  // [2]=pairs
     KB_CUDA(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), st));
     kin.alloc(npos); kout.alloc(npos); nids.alloc(npos); snids.alloc(npos);
     if (npos) {
-        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, ids.p, npos, kin.p,
+        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
                                                      nids.p);
         note_launch();
         sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
         k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order.p);
         note_launch();
     }
-    if (n > npos)
-        KB_CUDA(cudaMemcpyAsync(order.p + npos, zero_part.p, (n - npos) * sizeof(int32_t),
-                                cudaMemcpyDeviceToDevice, st));
     if (n >= 2 && npos) {
         sep_pairs(kout.p, snids.p, npos, s.upper.p, u + 2, g.sm_count, st);
     }

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -k C5 > gpurun_out/g19_c5.log 2>&1; echo "c5 $?"
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g21_tests.log 2>&1; echo "tests $?"
+timeout 300 python tools/step_phases.py > gpurun_out/g21_phases.log 2>&1; echo "phases $?"
