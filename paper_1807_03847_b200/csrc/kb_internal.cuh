@@ -399,5 +399,9 @@ void find_labels(Graph &g, const int64_t *h_targets, int64_t m, int64_t *h_ids);
 void build_shard(Graph &full, int64_t P, int64_t rank, Graph &out, int64_t *n_per_out,
                  int64_t *owned_out);
 void ensure_cub_tmp(State &s, size_t bytes);
+// stable (uint64 key, int32 value) radix sort (kb_sort.cu); input in (k0, v0),
+// scratch (k1, v1); returns true if the sorted pairs are in (k1, v1)
+bool radix_sort_pairs(uint64_t *k0, int32_t *v0, uint64_t *k1, int32_t *v1, int64_t n,
+                      int device, cudaStream_t st);
 
 }  // namespace kb

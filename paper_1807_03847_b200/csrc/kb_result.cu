@@ -260,7 +260,12 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
         k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
                                                      nids.p);
         note_launch();
-        sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
+        if (!tune_get("result.own_sort", 0)) {
+            sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
+        } else if (!radix_sort_pairs(kin.p, nids.p, kout.p, snids.p, npos, g.device, st)) {
+            std::swap(kin, kout);                       // sorted pairs ended in (kin, nids)
+            std::swap(nids, snids);
+        }
         k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order.p);
         note_launch();
     }

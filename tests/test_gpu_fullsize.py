@@ -204,3 +204,19 @@ def test_C3_rmat_s27_matches_oracle(layout):
         np.testing.assert_allclose(upper[ids], up_ref, rtol=RTOL, atol=0)
     # the certificate itself: the k-th lower bound beats the (k+1)-th upper
     assert lower[order[99]] > upper[order[100]] - 1e-6
+
+
+def test_own_radix_sort_gives_the_same_order():
+    """K3's hand-written LSD radix sort (kb_sort.cu, kb_tune result.own_sort)
+    produces the same full order and separated fraction as the default (CUB)
+    sort on s20: the reference's digests."""
+    from paper_1807_03847_b200 import _lib
+    L = _lib.lib()
+    cfg = REF["s20"]
+    L.kb_tune(b"result.own_sort", 1)
+    try:
+        g, st, res = _rmat_run(cfg, split=1 << 30)
+        assert h16(np.asarray(res.order, dtype=np.int64)) == cfg["order"]
+        assert res.separated_fraction == cfg["sepfrac"]
+    finally:
+        L.kb_tune(b"result.own_sort", 0)

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g21_tests.log 2>&1; echo "tests $?"
-timeout 300 python tools/step_phases.py > gpurun_out/g21_phases.log 2>&1; echo "phases $?"
+python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/g24_plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_rs_downsweep -s 2 -c 1 -o gpurun_out/r02_rs_down python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/g24_ncu.log 2>&1; echo "ncu $?"
