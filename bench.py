@@ -90,14 +90,35 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every ~2 ms from a thread (a C2 timed region is ~0.1-0.2 s), with
+    nvidia-smi -lms 20 as the fallback when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, device: int):
-        self.device = device
-        self.rows = []
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x for x in vis.split(",") if x.strip()]
+        self.device = int(ids[device]) if device < len(ids) and ids[device].isdigit() else device
+        self.rows = []          # (sm_mhz, max_mhz, set of reasons)
         self.proc = None
+        self.nvml = None
+        self.stop = False
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device),
@@ -112,11 +133,28 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        while not self.stop:
+            sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            reasons = {name for name, attr in self.REASONS if bits & getattr(nv, attr)}
+            self.rows.append((float(sm), float(mx), reasons))
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            if len(r) >= 7 and r[0].replace(".", "").isdigit():
+                reasons = {name for (name, _), v in zip(self.REASONS, r[3:7])
+                           if v.lower() == "active"}
+                self.rows.append((float(r[0]), float(r[1]), reasons))
 
     def __exit__(self, *a):
+        self.stop = True
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -125,19 +163,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        sm = sorted(r[0] for r in self.rows)
         reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in self.rows:
-            if len(r) >= 7:
-                for nm, val in zip(names, r[3:7]):
-                    if val.lower() == "active":
-                        reasons.add(nm)
-        sm.sort()
+            reasons |= r[2]
         return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "sm_max_mhz": max(r[1] for r in self.rows) if self.rows else None,
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def b_iter(n: int, nnz: int) -> int:
