@@ -440,18 +440,31 @@ def run_dynamic(a, device):
 
 def shared_host_csr(g, rank, n, nnz, dist):
     """The canonical CSR in host memory once per node: rank 0 downloads it
-    from its device graph into /dev/shm, the other ranks map the same pages."""
+    from its device graph into /dev/shm, the other ranks map the same pages.
+    If /dev/shm cannot hold it, every rank downloads its own copy."""
     import numpy as np
+    import torch
     tag = os.environ.get("MASTER_PORT", "0")
     paths = [f"/dev/shm/kb_bench_{tag}_indptr", f"/dev/shm/kb_bench_{tag}_indices"]
+    ok = 1
     if rank == 0:
-        ip, ix = g.csr_arrays()
-        for path, arr in zip(paths, (ip, ix)):
-            mm = np.lib.format.open_memmap(path, mode="w+", dtype=arr.dtype, shape=arr.shape)
-            mm[:] = arr
-            mm.flush()
-            del mm
-    dist.barrier()
+        try:
+            ip, ix = g.csr_arrays()
+            for path, arr in zip(paths, (ip, ix)):
+                mm = np.lib.format.open_memmap(path, mode="w+", dtype=arr.dtype, shape=arr.shape)
+                mm[:] = arr
+                mm.flush()
+                del mm
+        except OSError:
+            ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if not int(flag.item()):
+        if rank == 0:
+            for path in paths:
+                if os.path.exists(path):
+                    os.unlink(path)
+        return g.csr_arrays()
     ip = np.load(paths[0], mmap_mode="r+")
     ix = np.load(paths[1], mmap_mode="r+")
     assert ip.shape == (n + 1,) and ix.shape == (nnz,)
