@@ -335,8 +335,11 @@ __global__ void k_affect(const int32_t *list, int64_t m, unsigned int *aff_words
     if (i >= m) return;
     const int32_t v = list[i];
     const unsigned bit = 1u << (v & 31);
-    if (!(atomicOr(&aff_words[v >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
+    atomicOr(&aff_words[v >> 5], bit);
+    (void)affcount;
 }
+
+constexpr int EXPAND_SPLIT = 16;
 
 // in-neighbours of the changed rows (new ids) -> R (stamped) and affected
 __global__ void k_expand(const int32_t *changed, int64_t nc, const int64_t *in_ip,
@@ -344,21 +347,49 @@ __global__ void k_expand(const int32_t *changed, int64_t nc, const int64_t *in_i
                          const int32_t *iperm, int32_t *stamp, int32_t level, int32_t *R,
                          unsigned long long *rcount, unsigned int *aff_words,
                          unsigned long long *affcount, unsigned char *touched) {
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    // EXPAND_SPLIT warps per changed row, each taking every EXPAND_SPLIT-th
+    // 32-arc step: a hub's in-neighbours (10^5 arcs) do not serialise on one
+    // warp's atomics
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    const int64_t warp = gw / EXPAND_SPLIT;
+    const int part = (int)(gw % EXPAND_SPLIT);
     if (warp >= nc) return;
     const int32_t o = perm[changed[warp]];
     const int64_t a = in_ip[o];
     const int64_t L = in_len ? in_len[o] : in_ip[o + 1] - a;
-    for (int64_t j = lane; j < L; j += 32) {
-        const int32_t u = iperm[in_ix[a + j]];
-        const unsigned bit = 1u << (u & 31);
-        if (!(atomicOr(&aff_words[u >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
-        if (atomicExch(&stamp[u], level) != level) {
-            R[atomicAdd(rcount, 1ull)] = u;
-            touched[u] = 1;
+    (void)affcount;
+    for (int64_t j0 = (int64_t)part * 32; j0 < L; j0 += 32 * EXPAND_SPLIT) {
+        const int64_t j = j0 + lane;
+        bool fresh = false;
+        int32_t u = 0;
+        if (j < L) {
+            u = iperm[in_ix[a + j]];
+            atomicOr(&aff_words[u >> 5], 1u << (u & 31));
+            fresh = atomicExch(&stamp[u], level) != level;
+            if (fresh) touched[u] = 1;
+        }
+        // one counter update per warp step: the list position of each new row
+        const unsigned b = __ballot_sync(0xffffffffu, fresh);
+        if (b) {
+            unsigned long long base = 0;
+            if (lane == __ffs(b) - 1) base = atomicAdd(rcount, (unsigned long long)__popc(b));
+            base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+            if (fresh) R[base + __popc(b & ((1u << lane) - 1u))] = u;
         }
     }
+}
+
+// |affected| = population count of the bitmap (one pass over n/32 words;
+// the marking kernels set bits without counting)
+__global__ void k_popc_count(const unsigned int *words, int64_t nw, unsigned long long *count) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += __popc(words[i]);
+#pragma unroll
+    for (int k = 16; k; k >>= 1) c += __shfl_down_sync(0xffffffffu, c, k);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
 // total in-degree of the changed rows: the work an expansion would do
@@ -578,7 +609,8 @@ __global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const 
     for (int32_t j = 0; j < L; j++) {
         const int32_t c = __ldg(row + j);
         if ((__ldg(chg_bits + (c >> 5)) >> (c & 31)) & 1u) {
-            if (!(atomicOr(&aff_words[u >> 5], bit) & bit)) atomicAdd(affcount, 1ull);
+            atomicOr(&aff_words[u >> 5], bit);
+            (void)affcount;
             return;
         }
     }
@@ -1007,6 +1039,13 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         note_launch();
     }
     int64_t affected = ns;
+    const int64_t aff_words = (n + 31) / 32 + 1;
+    auto recount_affected = [&] {   // cnt[2] = |affected| from the bitmap
+        KB_CUDA(cudaMemsetAsync(cnt.p + 2, 0, 8, st));
+        k_popc_count<<<(unsigned)std::min<int64_t>(nblk(aff_words, 256), 4 * g.sm_count), 256, 0,
+                       st>>>(aff.p, aff_words, cnt.p + 2);
+        note_launch();
+    };
     bool aborted = false;
     bool all_touched = false;
     DBuf<unsigned int> chg_bits;
@@ -1059,6 +1098,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             run_spmv(s, st, w_prev, fresh.p, true);
             diff_changed(w_cur, fresh.p, n, C.p, cnt.p + 1, st);
             std::swap(s.levels[level - s.level_base], fresh);
+            recount_affected();
             unsigned long long hc[3];
             KB_CUDA(cudaMemcpyAsync(hc, cnt.p, 3 * 8, cudaMemcpyDeviceToHost, st));
             KB_CUDA(cudaStreamSynchronize(st));
@@ -1076,11 +1116,12 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             note_launch();
         }
         if (nchanged) {
-            k_expand<<<nblk(nchanged * 32, 256), 256, 0, st>>>(
+            k_expand<<<nblk(nchanged * 32 * EXPAND_SPLIT, 256), 256, 0, st>>>(
                 C.p, nchanged, in_ip, in_len, in_ix, g.perm.p, g.iperm.p, stamp.p, (int32_t)level,
                 R.p, cnt.p, aff.p, cnt.p + 2, touched.p);
             note_launch();
         }
+        recount_affected();
         unsigned long long hc[3];
         KB_CUDA(cudaMemcpyAsync(hc, cnt.p, 3 * 8, cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaStreamSynchronize(st));
@@ -1152,6 +1193,7 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
                 dt.p, (int64_t)targets.size(), aff.p, cnt.p + 2);
             note_launch();
         }
+        recount_affected();
         unsigned long long ha = 0;
         KB_CUDA(cudaMemcpyAsync(&ha, cnt.p + 2, 8, cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaStreamSynchronize(st));
