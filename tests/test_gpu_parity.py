@@ -251,3 +251,38 @@ def test_k_boundary_ties_are_detected_and_reported():
         warnings.simplefilter("error", P.KBoundaryTieWarning)
         P.run(st2, g2)
     assert st2.k_boundary_ties == 0
+
+
+@pytest.mark.parametrize("kind", ["topk", "ranking"])
+def test_device_loop_cap_rerun_and_state(kind):
+    """The device-driven run loops (TOPK batches of K1 + check, RANKING
+    cached-pair chains) against the oracle's engine.run on the same graph:
+    hitting max_iterations mid-batch raises ConvergenceError with the
+    reference's iteration count and leaves exactly r + 1 levels; a second
+    run on a converged state iterates once more and converges again, as
+    engine.py:382-396 does; the state afterwards answers check_converged."""
+    if kind == "topk":
+        g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
+        crit, ocrit = P.Criterion.top_k(100, 1e-6), O.Crit("topk", 1e-6, k=100)
+    else:
+        g0 = O.grid_graph(40 * 40)
+        crit, ocrit = P.Criterion.ranking(1e-9), O.Crit("ranking", 1e-9)
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    ref = O.run(O.OracleState(g0, ocrit), g0)
+    r = ref.iterations_used
+    assert r > 3
+    st = P.init(g, crit, undirected=True, max_iterations=r - 2)
+    with pytest.raises(P.ConvergenceError) as ei:
+        P.run(st, g)
+    assert ei.value.iterations == r - 2 and st.r == r - 2 and len(st.levels) == r - 1
+    st = P.init(g, crit, undirected=True)
+    res = P.run(st, g)
+    assert res.iterations_used == r and np.array_equal(res.order, ref.order)
+    assert P.check_converged(st)
+    res2 = P.run(st, g)
+    assert res2.iterations_used == r + 1 and st.r == r + 1
+    ost = O.OracleState(g0, ocrit)
+    O.run(ost, g0)
+    O.iterate_once(ost, g0)
+    assert O.check_converged(ost)
+    np.testing.assert_allclose(res2.lower, ost.lower, rtol=1e-12, atol=0)

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python bench.py --workload c5 > gpurun_out/g27_c5.log 2>&1; echo "c5 $?"
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k device_loop > gpurun_out/g28_tests.log 2>&1; echo "tests $?"
