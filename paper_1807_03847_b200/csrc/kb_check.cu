@@ -1212,6 +1212,7 @@ __global__ void __launch_bounds__(1024) k_pick_cands_fast(const unsigned long lo
 }
 
 bool check_ranking(State &s, cudaStream_t st) {
+    NvtxRange nv("K2 ranking check", (long long)s.r);
     Graph &g = *s.g;
     // the reference leaves active sorted by (-lower, id) after every ranking
     // check (engine.py:362-372 with k = n); the certificates below decide
@@ -1308,6 +1309,7 @@ double run_gap(State &s, cudaStream_t st) {
 // refutes at s.r (not converged, caller iterates on), false when it stopped
 // refuting at s.r (the full check decides).  C4: 95 of 99 checks.
 bool ranking_pair_chain(State &s, cudaStream_t st) {
+    NvtxRange nv("K2 ranking pair chain from level", (long long)s.r);
     Graph &g = *s.g;
     s.rank_order_pending = true;
     if (!s.abort_flag.p) s.abort_flag.alloc(1);
@@ -1371,6 +1373,7 @@ constexpr int64_t SMALL_M = 4096, MID_M = 1 << 18, MID_G = 32;
 // check publishes the verdict tagged with `level`.  Returns the new index.
 int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense, int cur,
                            int64_t level) {
+    NvtxRange nv("K2 topk check", (long long)level);
     Graph &g = *s.g;
     const int64_t k = s.k;
     unsigned long long *out = s.scratch_u64.p;  // [0..8)

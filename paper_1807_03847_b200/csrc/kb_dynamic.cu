@@ -958,6 +958,7 @@ static void sort_ids(std::vector<int32_t> &a) {
 
 void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                   int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats) {
+    NvtxRange nv("K4 update_batch");
     Graph &g = *s.g;
     cudaStream_t st = g.stream;
     const int64_t n = g.n;

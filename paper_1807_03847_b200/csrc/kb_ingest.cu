@@ -1062,6 +1062,7 @@ int graph_is_symmetric(Graph &g) {
 // is the bound (2.2 GB at C2); the graph and its symmetry flag are ready
 // one chunk after the last byte lands.
 void build_graph(Graph &g, const int64_t *h_indptr, const int32_t *h_indices) {
+    NvtxRange nv("ingest (upload + layout + symmetry)");
     cudaStream_t st = g.stream;
     cudaStream_t cs = copy_stream();
     const int64_t n = g.n, nnz = g.nnz;

@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/katzb200.h"
 
 namespace kb {
@@ -97,6 +99,21 @@ struct PhaseTrace {
                 std::chrono::duration<double, std::milli>(t1 - t0).count());
         t0 = t1;
     }
+};
+
+// NVTX ranges (SURVEY.md §5 tracing: nsys ranges per iteration): host-side
+// enqueue regions of every K1 level, check, result, update and ingest; the
+// header-only NVTX3 API costs nothing unless a tool is attached
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    NvtxRange(const char *what, long long level) {
+        char buf[64];
+        snprintf(buf, sizeof buf, "%s %lld", what, level);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
 };
 
 // ---------------------------------------------------------------- device buf

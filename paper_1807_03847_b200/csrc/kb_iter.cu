@@ -779,6 +779,7 @@ void materialize_bounds(State &s, cudaStream_t st) {
 }
 
 void launch_iterate(State &s, cudaStream_t st) {
+    NvtxRange nv("K1 level", (long long)s.r + 1);
     Graph &g = *s.g;
     const int64_t n = g.n;
     DBuf<double> wnew;

@@ -224,6 +224,7 @@ static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_
 // by original id, and the exact separated-pair count
 void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
                    DBuf<double> *upper, int64_t *h_pairs) {
+    NvtxRange nv("K3 ranking_result");
     Graph &g = *s.g;
     const int64_t n = g.n;
     KB_REQUIRE(s.r >= 1, KB_ESTATE, "separated_fraction needs at least one iteration");
