@@ -256,7 +256,8 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
     }
     unsigned long long *u = s.scratch_u64.p;  // [2]=pairs
     KB_CUDA(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), st));
-    kin.alloc(npos); kout.alloc(npos); nids.alloc(npos); snids.alloc(npos);
+    // +4: the own sort loads tiles in 16-byte chunks (kb_sort.cu)
+    kin.alloc(npos + 4); kout.alloc(npos + 4); nids.alloc(npos + 4); snids.alloc(npos + 4);
     if (npos) {
         k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
                                                      nids.p);
@@ -398,7 +399,8 @@ static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const
     KB_CUDA(cudaMemcpyAsync(hc, u.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
     const int64_t npos = (int64_t)hc[0];
-    kin.alloc(npos); kout.alloc(npos); nids.alloc(npos); snids.alloc(npos);
+    // +4: the own sort loads tiles in 16-byte chunks (kb_sort.cu)
+    kin.alloc(npos + 4); kout.alloc(npos + 4); nids.alloc(npos + 4); snids.alloc(npos + 4);
     if (npos) {
         k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(lo, iota.p, ids.p, npos, kin.p, nids.p);
         note_launch();

@@ -16,7 +16,10 @@
 // Measured at C2 (8.9M pairs, 8 passes): upsweep 39 us + offsets 7 us +
 // downsweep 111 us per pass, against 82 us for CUB's onesweep -- the
 // downsweep is latency-bound (3 blocks/SM, every warp waiting on its tile's
-// key loads before ranking).  A single-pass onesweep variant with decoupled
+// key loads before ranking).  A persistent variant loading the next tile
+// with cp.async while ranking the current one (one 256-thread CTA per SM)
+// measured 127 us: the per-warp ranking chain (16 items, each waiting on
+// the previous item's shared counter update) then binds.  A single-pass onesweep variant with decoupled
 // look-back measured 120-135 us per pass.  So K3 keeps CUB's sort by default
 // and this one runs with kb_tune("result.own_sort", 1) (bit-identical
 // order; tests/test_gpu_fullsize.py digests pass with either).
