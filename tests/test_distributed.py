@@ -350,3 +350,20 @@ def test_sharded_run_applies_engine_init_guards():
         assert out[0].startswith("ParameterError:") and "symmetric" in out[0]
         assert out[1].startswith("ParameterError:") and "exceeds" in out[1]
         assert out[2].startswith("ParameterError:") and "max_iterations" in out[2]
+
+
+def test_device_plan_matches_host_plan_blocks():
+    """DevicePlan (the device-built shards' block geometry) agrees with the
+    host ShardPlan on n_per, every rank's block and its owned-row count."""
+    from paper_1807_03847_b200.distributed import DevicePlan
+    g = O.rmat_graph(1 << 12, edge_factor=8, seed=11)
+    for P in (1, 2, 3, 5, 8):
+        hp = ShardPlan(g.indptr, P)
+        dp = DevicePlan(g.node_count, P, hp.max_degree)
+        assert dp.n_per == hp.n_per
+        for r in range(P):
+            assert dp.block(r) == hp.block(r) and dp.owned(r) == hp.owned(r)
+            # the owned rows are the block's head: exactly the valid exchange ids
+            lo, hi = hp.block(r)
+            assert (hp.node_of_exch[lo:lo + hp.owned(r)] >= 0).all()
+            assert (hp.node_of_exch[lo + hp.owned(r):hi] < 0).all()
