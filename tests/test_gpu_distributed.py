@@ -345,3 +345,45 @@ def test_cuda_shards_s20_match_reference_digests(world, fused):
     assert h16(np.asarray(order, dtype=np.int64)) == "85ea50d05c5dfd0e"
     assert h16(lower) == "f13ddf321fb10751"
     assert h16(upper) == "9db3105f69a9e233"
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_device_shard_csr_equals_host_plan(world):
+    """kb_graph_create_shard builds exactly the CSR the host ShardPlan
+    describes (exchange ids, owned rows only, original arc order), also from
+    a mutated device graph (degree order re-sorted on the device)."""
+    import ctypes
+
+    from paper_1807_03847_b200 import _lib
+    g0 = O.rmat_graph(1 << 13, edge_factor=16, seed=9)
+    L = _lib.lib()
+    for mutated in (False, True):
+        ip, ix = g0.indptr, g0.indices
+        dg = P.DeviceGraph(ip, ix, device=0)
+        if mutated:        # drop two arcs (u, v), (v, u) on the device
+            u, v = 0, int(ix[ip[0]])
+            dels = np.array([[u, v], [v, u]], dtype=np.int64)
+            _lib.check(L.kb_graph_apply_batch(dg.handle, None, 0, _lib.ptr(dels), 2))
+            keep = np.ones(ix.size, dtype=bool)
+            keep[ip[0]] = False
+            keep[ip[v] + np.searchsorted(ix[ip[v]:ip[v + 1]], u)] = False
+            ix = ix[keep]
+            ip = np.concatenate([[0], np.cumsum(np.diff(g0.indptr) - np.bincount(
+                [u, v], minlength=g0.node_count))]).astype(np.int64)
+        plan = D.ShardPlan(ip, world)
+        for rank in range(world):
+            h, n_per, owned = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(L.kb_graph_create_shard(dg.handle, world, rank, 0, -1, ctypes.byref(h),
+                                               ctypes.byref(n_per), ctypes.byref(owned)))
+            assert (n_per.value, owned.value) == (plan.n_per, plan.owned(rank))
+            N = world * plan.n_per
+            info = _lib.GraphInfo()
+            _lib.check(L.kb_graph_info_get(h, ctypes.byref(info)))
+            dip = np.empty(N + 1, dtype=np.int64)
+            dix = np.empty(int(info.nnz), dtype=np.int32)
+            _lib.check(L.kb_graph_get_csr(h, _lib.ptr(dip), _lib.ptr(dix)))
+            hip, hix = plan.local_csr(ip, ix, rank)
+            np.testing.assert_array_equal(dip, hip)
+            np.testing.assert_array_equal(dix, hix)
+            L.kb_graph_destroy(h)
+        dg.close()
