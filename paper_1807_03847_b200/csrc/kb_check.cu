@@ -360,12 +360,15 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
     // (-lower, id)) to prefix_buf, survivors (the rest with fl(upper - eps) >=
     // threshold) to act_out + k, both in active-set order.  Each warp owns a
     // contiguous run of the block's chunk: pass A classifies its elements
-    // (loads kept in flight, one class byte each, reusing the candidate
-    // buffer) and counts them with ballots; one grid barrier publishes the
-    // block counts; pass B streams the class bytes and ids and writes every
-    // kept id at its rank (ballot + popc), so nothing is gathered twice.
+    // (loads kept in flight, one class byte each in the staging buffer) and
+    // counts them with ballots; one grid barrier publishes the block counts;
+    // pass B streams the class bytes and ids and writes every kept id at its
+    // rank (ballot + popc), so nothing is gathered twice.
     const double thr = __longlong_as_double((long long)kstar);
-    uint8_t *cls = (uint8_t *)A.cand;
+    // class bytes go to the staging buffer, not the candidate list: in the
+    // shared-memory cut other blocks may still be reading the candidates
+    // (no grid barrier separates that read from this pass)
+    uint8_t *cls = (uint8_t *)A.stK;
     constexpr int NW = CHK_THREADS / 32;
     __shared__ unsigned long long s_wcnt[NW];
     __shared__ unsigned long long s_base;

@@ -632,7 +632,8 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         k_ones_step<<<(unsigned)((A.nvr + 255) / 256), 256, 0, st>>>(A);
         note_launch();
         KB_CUDA(cudaGetLastError());
-    } else if (A.nslices && g.sell.nwide == 0 && A.nseg == 0 && !A.lazy_bounds &&
+    } else if (A.nslices && g.sell.nwide == 0 && A.nseg == 0 &&
+               (!A.lazy_bounds || tune_get("k1.narrow_lazy", 0)) &&
                tune_get("k1.narrow_kernel", 1)) {
         // (without the bound stores the persistent kernel is faster on C4:
         // 0.18 vs 0.215 ms; with them the narrow one: 0.267 vs 0.37 ms)
