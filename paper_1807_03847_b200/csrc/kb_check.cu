@@ -1801,6 +1801,32 @@ __global__ void k_unpack_blocks(const unsigned long long *blocks, int64_t P, int
 
 // the global cut (k-th of the merged proposals) and the adjacent-separation
 // test of the merged top-k prefix; cut[3], cut[4] feed IsWinner/IsSurvivor
+// the P*k proposals ordered by (key desc, label asc) in one block (nc <=
+// 4096): a shared-memory bitonic sort instead of two device radix sorts
+__global__ void __launch_bounds__(1024) k_order_cands(const uint64_t *nk, const int64_t *labels,
+                                                      int64_t nc, int32_t *order) {
+    extern __shared__ unsigned char smem[];
+    int P = 1;
+    while (P < nc) P <<= 1;
+    uint64_t *key = (uint64_t *)smem;
+    uint32_t *lab = (uint32_t *)(key + P);
+    int32_t *idx = (int32_t *)(lab + P);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < nc) {
+            key[i] = nk[i];
+            lab[i] = labels[i] >= 0 && labels[i] < 0xFFFFFFFFll ? (uint32_t)labels[i] : 0xFFFFFFFFu;
+            idx[i] = i;
+        } else {
+            key[i] = ~0ull;
+            lab[i] = 0xFFFFFFFFu;
+            idx[i] = -1;
+        }
+    }
+    __syncthreads();
+    bitonic_kl(key, lab, idx, P);
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) order[i] = idx[i];
+}
+
 __global__ void k_global_cut_dev(const uint64_t *keys, const int64_t *labels,
                                  const double *uppers, const int32_t *order,
                                  const unsigned long long *blocks, int64_t P, int64_t k,
@@ -1875,19 +1901,14 @@ void shard_propose(State &s, cudaStream_t st, int64_t k, unsigned long long *blk
         A.stU = s.stU.p;
         A.stI = s.stI.p;
         A.out = s.scratch_u64.p;
+        // the fused split writes the k local winners (labels are unique, so
+        // exactly k) to the prefix buffer; its survivors land in the spare
+        // active buffer, which the cut overwrites
+        A.split = 1;
+        A.act_cap = (int64_t)s.act[s.cur ^ 1].n;
         void *args[] = {&A};
         KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
         note_launch();
-        // exactly k winners (labels are unique), so the count is known here
-        IsWinner win{s.lower.p, g.labels(), s.scratch_u64.p};
-        unsigned long long *nsel = s.scratch_u64.p + 5;
-        auto sel = [&](auto in) {
-            cub_go(&s, [&](void *t, size_t &b) {
-                return cub::DeviceSelect::If(t, b, in, s.scratch_i32.p, nsel, (int)m, win, st);
-            });
-        };
-        if (s.act_dense) sel(cub::CountingInputIterator<int32_t>(0));
-        else sel((const int32_t *)s.act[s.cur].p);
         src = s.scratch_i32.p;
         dense = 0;
     }
@@ -1915,15 +1936,28 @@ void shard_cut(State &s, cudaStream_t st, const unsigned long long *blocks, int6
     du.alloc(nc); i0.alloc(nc); i1.alloc(nc); i2.alloc(nc);
     k_unpack_blocks<<<nblk(nc, 256), 256, 0, st>>>(blocks, P, k, dk.p, dl.p, du.p, nk.p, i0.p);
     note_launch();
-    // (key desc, label asc): stable sort by label, then by inverted key
-    cub_go(nullptr, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, dl.p, l2.p, i0.p, i1.p, (int)nc, 0, 64, st);
-    });
-    k_gather_u64<<<nblk(nc, 256), 256, 0, st>>>(nk.p, i1.p, nc, nk2.p);
-    note_launch();
-    cub_go(nullptr, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, nk2.p, nk.p, i1.p, i2.p, (int)nc, 0, 64, st);
-    });
+    if (nc <= 4096) {
+        // (key desc, label asc) in one block
+        int Pp = 1;
+        while (Pp < nc) Pp <<= 1;
+        const size_t smem = (size_t)Pp * 16;
+        KB_CUDA(cudaFuncSetAttribute(k_order_cands, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 1)));
+        k_order_cands<<<1, 1024, smem, st>>>(nk.p, dl.p, nc, i2.p);
+        note_launch();
+    } else {
+        // (key desc, label asc): stable sort by label, then by inverted key
+        cub_go(nullptr, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, dl.p, l2.p, i0.p, i1.p, (int)nc, 0, 64,
+                                                   st);
+        });
+        k_gather_u64<<<nblk(nc, 256), 256, 0, st>>>(nk.p, i1.p, nc, nk2.p);
+        note_launch();
+        cub_go(nullptr, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, nk2.p, nk.p, i1.p, i2.p, (int)nc, 0, 64,
+                                                   st);
+        });
+    }
     unsigned long long *cut = s.scratch_u64.p;
     k_global_cut_dev<<<1, 256, 0, st>>>(dk.p, dl.p, du.p, i2.p, blocks, P, k, s.eps, cut);
     note_launch();
