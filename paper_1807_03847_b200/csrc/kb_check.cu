@@ -75,6 +75,11 @@ struct TopkArgs {
     // (engine.py:359) could have kept them -- are counted here
     unsigned long long *ties = nullptr;
     int64_t act_cap = INT64_MAX;    // capacity of act_out (checked build)
+    // sharded cut: the (global) cut is given in out[3], out[4] -- no
+    // selection, only the split; winners to win_out and survivors to
+    // surv_out when set (else prefix_buf and act_out + k)
+    int cut_given = 0;
+    int32_t *win_out = nullptr, *surv_out = nullptr;
 };
 
 __device__ __forceinline__ bool flag_set(const unsigned long long *f) {
@@ -208,7 +213,10 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
     // istar = max admits every key >= +0
     uint64_t kstar = 0;
     uint32_t istar = 0xFFFFFFFFu;
-    if (m > A.k) {
+    if (A.cut_given) {
+        kstar = A.out[3];
+        istar = (uint32_t)A.out[4];
+    } else if (m > A.k) {
     // ---- 1a. two 12-bit digits over the whole active set
     uint64_t prefix = 0, mask = 0;
     int64_t kk = A.k;
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
     }
     }   // nc > CSORT
     }   // m > k
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !A.cut_given) {
         A.out[3] = kstar;
         A.out[4] = istar;
     }
@@ -452,8 +460,12 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
         const unsigned bs = __ballot_sync(0xffffffffu, c == 1);
         KB_DCHECK(c != 2 || ow + __popc(bw & lt) < (unsigned long long)A.k);
         KB_DCHECK(c != 1 || A.k + (int64_t)(os + __popc(bs & lt)) < A.act_cap);
-        if (c == 2) A.prefix_buf[ow + __popc(bw & lt)] = id_at(i);
-        else if (c == 1) A.act_out[A.k + (int64_t)(os + __popc(bs & lt))] = id_at(i);
+        if (c == 2) (A.win_out ? A.win_out : A.prefix_buf)[ow + __popc(bw & lt)] = id_at(i);
+        else if (c == 1) {
+            const int64_t q = (int64_t)(os + __popc(bs & lt));
+            if (A.surv_out) A.surv_out[q] = id_at(i);
+            else A.act_out[A.k + q] = id_at(i);
+        }
         ow += __popc(bw);
         os += __popc(bs);
     }
@@ -1966,17 +1978,37 @@ void shard_cut(State &s, cudaStream_t st, const unsigned long long *blocks, int6
     const int64_t m = s.m_host;
     const int nxt = s.cur ^ 1;
     surv.alloc(std::max<int64_t>(1, m));
-    IsWinner win{s.lower.p, g.labels(), cut};
-    IsSurvivor sur{s.lower.p, s.upper.p, cut, s.eps};
     if (m) {
-        auto part = [&](auto in) {
-            cub_go(&s, [&](void *t, size_t &b) {
-                return cub::DevicePartition::If(t, b, in, s.act[nxt].p, surv.p, s.stI.p, cut + 5,
-                                                (int)m, win, sur, st);
-            });
-        };
-        if (s.act_dense) part(cub::CountingInputIterator<int32_t>(0));
-        else part((const int32_t *)s.act[s.cur].p);
+        // winners (under the global cut) to act[nxt], survivors to surv, both
+        // in active-set order: the select kernel's fused split with the cut
+        // given (counts into cut[5], cut[6])
+        TopkArgs A;
+        A.lower = s.lower.p;
+        A.upper = s.upper.p;
+        A.perm = g.labels();
+        A.act_in = s.act[s.cur].p;
+        A.m = m;
+        A.dense = s.act_dense;
+        A.act_out = s.act[nxt].p;
+        A.k = k;
+        A.eps = s.eps;
+        A.hist = (unsigned int *)(s.scratch_u64.p + 8);
+        A.blk = s.scratch_u64.p + 8 + HIST_WORDS;
+        A.prefix_buf = s.scratch_i32.p;
+        A.cand = s.cand.p;
+        A.stK = s.stK.p;
+        A.stU = s.stU.p;
+        A.stI = s.stI.p;
+        A.out = cut;
+        A.split = 1;
+        A.cut_given = 1;
+        A.win_out = s.act[nxt].p;
+        A.surv_out = surv.p;
+        const int G = (int)std::max<int64_t>(
+            1, std::min<int64_t>(coop_grid(g.sm_count), (m + 8191) / 8192));
+        void *args[] = {&A};
+        KB_CUDA(cudaLaunchCooperativeKernel((void *)k_topk_select, G, CHK_THREADS, args, 0, st));
+        note_launch();
     } else {
         KB_CUDA(cudaMemsetAsync(cut + 5, 0, 16, st));
     }
