@@ -138,6 +138,24 @@ int kb_graph_create_ex(int device, int64_t n, int64_t nnz, const int64_t *indptr
  * the tie-break labels are the node ids (padding: n, n+1, ...).  The shard
  * inherits `full`'s symmetry flag.  Outputs n_per = ceil(n/P) and the number
  * of rows this rank owns (its block's head). */
+/* The same shard straight from a host CSR (indptr n+1 int64, indices nnz
+ * int32, rows strictly ascending -- checked): only indptr (for the degree
+ * order) and this rank's own rows are uploaded to `device` (the rows
+ * gathered on the host into a page-locked ring), so graphs larger than one
+ * GPU shard too.  The shard's symmetry is decided across the ranks with
+ * kb_shard_symmetry_keys / kb_shard_symmetry_verify. */
+int kb_graph_create_shard_host(int device, int64_t n, int64_t nnz, const int64_t *indptr,
+                               const int32_t *indices, int64_t nranks, int64_t rank,
+                               int64_t split_threshold, int64_t hot_size, kb_graph **out,
+                               int64_t *n_per, int64_t *owned);
+/* Graph.is_symmetric (graph.py:168-175) of a sharded graph, exactly: every
+ * rank writes the reverse of each of its arcs as a device key, grouped by the
+ * rank owning the reversed arc's row (keys: nnz int64 device buffer;
+ * counts[q]: keys for rank q); after an all-to-all of those groups each rank
+ * verifies that the keys it received are exactly its own arcs (ok = 1); the
+ * graph is symmetric iff every rank says so. */
+int kb_shard_symmetry_keys(kb_graph *shard, int64_t nranks, int64_t *keys, int64_t *counts);
+int kb_shard_symmetry_verify(kb_graph *shard, const int64_t *recv, int64_t nrecv, int *ok);
 /* Device ids of the nodes whose tie-break label is labels[j] (-1: none),
  * m <= 64: a shard's exchange ids of given node ids (sharded PAIR checks,
  * engine.py:346-353). */

@@ -73,6 +73,11 @@ SIGNATURES = {
     "kb_graph_create_ex": (i32, [i32, i64, i64, vp, vp, i64, i64, i32, vp, i64, i64,
                                  ctypes.POINTER(vp)]),
     "kb_graph_find_labels": (i32, [vp, vp, i64, vp]),
+    "kb_graph_create_shard_host": (i32, [i32, i64, i64, vp, vp, i64, i64, i64, i64,
+                                         ctypes.POINTER(vp), ctypes.POINTER(i64),
+                                         ctypes.POINTER(i64)]),
+    "kb_shard_symmetry_keys": (i32, [vp, i64, vp, vp]),
+    "kb_shard_symmetry_verify": (i32, [vp, vp, i64, ctypes.POINTER(i32)]),
     "kb_graph_create_shard": (i32, [vp, i64, i64, i64, i64, ctypes.POINTER(vp),
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "kb_graph_create_rmat": (i32, [i32, i32, i64, vp, dbl, dbl, dbl, i64, i64,

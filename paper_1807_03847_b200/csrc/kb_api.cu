@@ -458,6 +458,41 @@ int kb_graph_create_shard(kb_graph *full, int64_t nranks, int64_t rank, int64_t 
     });
 }
 
+int kb_graph_create_shard_host(int device, int64_t n, int64_t nnz, const int64_t *indptr,
+                               const int32_t *indices, int64_t nranks, int64_t rank,
+                               int64_t split_threshold, int64_t hot_size, kb_graph **out,
+                               int64_t *n_per, int64_t *owned) {
+    return guarded([&] {
+        KB_REQUIRE(out && n_per && owned, KB_EPARAM, "NULL argument");
+        KB_REQUIRE(n >= 1 && n < ((int64_t)1 << 31), KB_ENODERANGE,
+                   "node ids must fit the 32-bit index type");
+        kb_graph *h = new_graph(device, split_threshold, hot_size);
+        try {
+            build_shard_host(h->g, n, nnz, indptr, indices, nranks, rank, n_per, owned);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int kb_shard_symmetry_keys(kb_graph *h, int64_t nranks, int64_t *keys, int64_t *counts) {
+    return guarded([&] {
+        KB_REQUIRE(h && counts && (keys || h->g.nnz == 0), KB_EPARAM, "NULL argument");
+        use_device(h->g.device);
+        shard_symmetry_keys(h->g, nranks, keys, counts);
+    });
+}
+
+int kb_shard_symmetry_verify(kb_graph *h, const int64_t *recv, int64_t nrecv, int *ok) {
+    return guarded([&] {
+        KB_REQUIRE(h && ok && (recv || nrecv == 0), KB_EPARAM, "NULL argument");
+        use_device(h->g.device);
+        *ok = shard_symmetry_verify(h->g, recv, nrecv);
+    });
+}
+
 int kb_graph_find_labels(kb_graph *h, const int64_t *labels, int64_t m, int64_t *ids) {
     return guarded([&] {
         KB_REQUIRE(h && (m == 0 || (labels && ids)), KB_EPARAM, "NULL argument");

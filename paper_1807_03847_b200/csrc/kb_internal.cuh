@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <chrono>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -131,6 +132,8 @@ cudaStream_t copy_stream();
 bool host_is_pinned(const void *p);
 void upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t cs);
 void download_d2h(void *dst, const void *src, size_t bytes, cudaStream_t st);
+void upload_gather_h2d(void *dst, size_t bytes, cudaStream_t cs,
+                       const std::function<void(char *, size_t, size_t, int, int)> &fill);
 constexpr size_t BIG_ALLOC = (size_t)64 << 20;
 void *dev_alloc(size_t bytes);
 void dev_free(void *p, size_t bytes);
@@ -257,6 +260,7 @@ struct Graph {
     std::vector<void *> exch_opened;  // IPC mappings to close
     cudaStream_t stream = nullptr;
     int symmetric = -1;  // cached result of kb_graph_is_symmetric
+    int64_t sym_n_per = 0;  // shards built from a host CSR (symmetry decided across ranks)
     size_t device_bytes() const;
     Graph() = default;
     Graph(const Graph &) = delete;
@@ -415,6 +419,11 @@ int graph_is_symmetric(Graph &g);
 void find_labels(Graph &g, const int64_t *h_targets, int64_t m, int64_t *h_ids);
 void build_shard(Graph &full, int64_t P, int64_t rank, Graph &out, int64_t *n_per_out,
                  int64_t *owned_out);
+void build_shard_host(Graph &out, int64_t n, int64_t nnz, const int64_t *h_ip,
+                      const int32_t *h_ix, int64_t P, int64_t rank, int64_t *n_per_out,
+                      int64_t *owned_out);
+void shard_symmetry_keys(Graph &g, int64_t P, int64_t *keys, int64_t *h_counts);
+int shard_symmetry_verify(Graph &g, const int64_t *recv, int64_t nrecv);
 void ensure_cub_tmp(State &s, size_t bytes);
 // stable (uint64 key, int32 value) radix sort (kb_sort.cu); input in (k0, v0),
 // scratch (k1, v1); returns true if the sorted pairs are in (k1, v1)

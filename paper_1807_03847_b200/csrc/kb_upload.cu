@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -34,11 +35,25 @@ class CopyPool {
             d_ = (char *)dst;
             s_ = (const char *)src;
             n_ = bytes;
+            fn_ = nullptr;
             pending_ = T_ - 1;
             gen_++;
         }
         cv_.notify_all();
         part(0, (char *)dst, (const char *)src, bytes);
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+    // fn(i, T) on every pool thread (i = 0 on the caller)
+    void parallel(const std::function<void(int, int)> &fn) {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            fn_ = &fn;
+            pending_ = T_ - 1;
+            gen_++;
+        }
+        cv_.notify_all();
+        fn(0, T_);
         std::unique_lock<std::mutex> lk(m_);
         done_.wait(lk, [&] { return pending_ == 0; });
     }
@@ -57,8 +72,10 @@ class CopyPool {
             char *d = d_;
             const char *s = s_;
             const size_t n = n_;
+            const std::function<void(int, int)> *fn = fn_;
             lk.unlock();
-            part(i, d, s, n);
+            if (fn) (*fn)(i, T_);
+            else part(i, d, s, n);
             lk.lock();
             if (--pending_ == 0) done_.notify_one();
         }
@@ -70,6 +87,7 @@ class CopyPool {
     char *d_ = nullptr;
     const char *s_ = nullptr;
     size_t n_ = 0;
+    const std::function<void(int, int)> *fn_ = nullptr;
     uint64_t gen_ = 0;
     int pending_ = 0;
 };
@@ -133,6 +151,29 @@ void upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t cs) {
         KB_CUDA(cudaEventSynchronize(R.ev[i]));   // the slot's previous copy is done
         pool().copy(R.slot[i], (const char *)src + off, len);
         KB_CUDA(cudaMemcpyAsync((char *)dst + off, R.slot[i], len, cudaMemcpyHostToDevice, cs));
+        KB_CUDA(cudaEventRecord(R.ev[i], cs));
+    }
+}
+
+// dst (device) <- a virtual host source of `bytes` bytes that fill(slot, off,
+// len, i, T) materialises piece by piece (part i of T on every pool thread)
+// into page-locked ring slots, each copied on stream cs while the next is
+// filled: a host-side gather (a rank's rows of a host CSR) at the PCIe rate
+void upload_gather_h2d(void *dst, size_t bytes, cudaStream_t cs,
+                       const std::function<void(char *, size_t, size_t, int, int)> &fill) {
+    if (!bytes) return;
+    std::lock_guard<std::mutex> lk(g_up_mu);
+    int dev = 0;
+    KB_CUDA(cudaGetDevice(&dev));
+    Ring &R = ring(dev);
+    for (size_t off = 0; off < bytes; off += SLOT) {
+        const size_t len = std::min(SLOT, bytes - off);
+        const int i = R.next;
+        R.next = (R.next + 1) % RING;
+        KB_CUDA(cudaEventSynchronize(R.ev[i]));
+        char *slot = (char *)R.slot[i];
+        pool().parallel([&](int t, int T) { fill(slot, off, len, t, T); });
+        KB_CUDA(cudaMemcpyAsync((char *)dst + off, slot, len, cudaMemcpyHostToDevice, cs));
         KB_CUDA(cudaEventRecord(R.ev[i], cs));
     }
 }

@@ -130,7 +130,7 @@ class CudaShard:
     def __init__(self, plan, rank: int, indptr=None, indices=None, *, device: int,
                  alpha: float, gamma: float, crit: Criterion, undirected: bool,
                  max_iterations: int, symmetric: bool = False, split_threshold: int = 0,
-                 local_csr=None, fused: bool = False, full=None):
+                 local_csr=None, fused: bool = False, full=None, host_build: bool = False):
         import torch
         self.torch = torch
         self.L = _lib.lib()
@@ -140,7 +140,16 @@ class CudaShard:
         # the shards reproduce the one-GPU bounds bit for bit; a finer split
         # (fast_split(P)) shortens the kernel tail when the per-rank work is
         # small, at the cost of rounding-level (<= 1e-12) differences
-        if full is not None:
+        if host_build:
+            # only indptr and this rank's rows travel to its GPU
+            ip = np.ascontiguousarray(indptr, dtype=np.int64)
+            ix = np.ascontiguousarray(indices, dtype=np.int32)
+            n_per, owned = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(self.L.kb_graph_create_shard_host(
+                device, ip.size - 1, int(ip[-1]), _lib.ptr(ip), _lib.ptr(ix), plan.P, rank,
+                split_threshold, -1, ctypes.byref(h), ctypes.byref(n_per), ctypes.byref(owned)))
+            assert (int(n_per.value), int(owned.value)) == (plan.n_per, plan.owned(rank))
+        elif full is not None:
             fh = full.handle if hasattr(full, "handle") else full.device_graph.handle
             n_per, owned = ctypes.c_int64(), ctypes.c_int64()
             _lib.check(self.L.kb_graph_create_shard(fh, plan.P, rank, split_threshold, -1,
@@ -193,6 +202,24 @@ class CudaShard:
         else:
             _lib.check(self.L.kb_state_set_active_range(s, lo, lo + self.plan.owned(self.rank)))
         self.r = 0
+
+    def symmetry_keys(self):
+        """(keys, counts): the reverse of every local arc as an int64 device
+        tensor grouped by destination rank, and the group sizes."""
+        info = _lib.GraphInfo()
+        _lib.check(self.L.kb_graph_info_get(self.g, ctypes.byref(info)))
+        keys = self.torch.empty(max(1, int(info.nnz)), dtype=self.torch.int64,
+                                device=f"cuda:{self.device}")
+        counts = np.zeros(self.plan.P, dtype=np.int64)
+        _lib.check(self.L.kb_shard_symmetry_keys(self.g, self.plan.P, keys.data_ptr(),
+                                                 _lib.ptr(counts)))
+        return keys[:int(counts.sum())], [int(c) for c in counts]
+
+    def symmetry_verify(self, recv) -> bool:
+        ok = ctypes.c_int()
+        _lib.check(self.L.kb_shard_symmetry_verify(self.g, recv.data_ptr(), int(recv.numel()),
+                                                   ctypes.byref(ok)))
+        return bool(ok.value)
 
     def exchange_export(self):
         """This rank's two exchange buffers: [(ipc handle bytes, device ptr)]."""
@@ -571,6 +598,25 @@ def _validate(n: int, d: int, crit: Criterion, alpha, max_iterations):
     return alpha, gamma, int(max_iterations)
 
 
+def shards_symmetric(shard, dist, world: int) -> bool:
+    """Graph.is_symmetric (graph.py:168-175) of the sharded arc set, exactly:
+    every rank sends the reverse of each of its arcs to the rank owning that
+    reversed arc's row (one all-to-all), and checks that what it receives is
+    exactly its own arc set; all-reduced."""
+    torch = shard.torch
+    dev = f"cuda:{shard.device}"
+    keys, counts = shard.symmetry_keys()
+    send = torch.tensor(counts, dtype=torch.int64, device=dev)
+    recv_counts = torch.empty_like(send)
+    dist.all_to_all_single(recv_counts, send)
+    rc = [int(x) for x in recv_counts.tolist()]
+    recv = torch.empty(max(1, sum(rc)), dtype=torch.int64, device=dev)[:sum(rc)]
+    dist.all_to_all_single(recv, keys, output_split_sizes=rc, input_split_sizes=counts)
+    ok = torch.tensor([1 if shard.symmetry_verify(recv) else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(ok.item())
+
+
 def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = False,
                 alpha: float | None = None, max_iterations: int | None = None,
                 device: int | None = None, backend_factory=None,
@@ -578,10 +624,12 @@ def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = False,
     """engine.init + engine.run (engine.py:248-283, :382-396) of `crit` on the
     graph with the current torch.distributed group, one GPU per rank.
 
-    The graph is the canonical CSR on every rank's host (uploaded to the
-    rank's GPU, where the symmetry test runs during the upload and the
-    rank's shard is cut out on the device), or ``graph``: a device graph
-    already on this rank's GPU (engine.DeviceGraph, or a generators graph).
+    The graph is the canonical CSR on every rank's host -- only indptr and
+    the rank's own rows are uploaded to its GPU (kb_graph_create_shard_host,
+    so graphs larger than one GPU shard too) and the arc set's symmetry is
+    decided across the ranks (shards_symmetric) -- or ``graph``: a device
+    graph already on this rank's GPU (engine.DeviceGraph, or a generators
+    graph), cut on the device.
     undirected=True requires a symmetric arc set (ParameterError otherwise),
     as in engine.init."""
     import torch.distributed as dist
@@ -599,32 +647,53 @@ def sharded_run(indptr, indices, crit: Criterion, *, undirected: bool = False,
         backend = backend_factory(plan, rank, alpha, gamma)
         return ShardedRun(backend, plan, crit, rank=rank, world=world,
                           max_iterations=max_iterations).run()
-    from .engine import DeviceGraph
     dev = rank if device is None else device
-    full = graph
-    own_full = full is None
-    if own_full:
-        full = DeviceGraph(indptr, indices, device=dev)
-    dg = full if hasattr(full, "handle") else full.device_graph
-    info = dg.info()
-    n, d = int(info.n), int(info.max_out_degree)
-    alpha, gamma, max_iterations = _validate(n, d, crit, alpha, max_iterations)
-    if undirected and not dg.is_symmetric():
-        raise ParameterError("undirected mode requires a symmetric arc set")
-    plan = DevicePlan(n, world, d)
+    own_graph = None
+    if graph is None and world == 1:
+        # one rank holds every row anyway: the pipelined full upload (symmetry
+        # decided while the columns land) beats a host-side row gather
+        from .engine import DeviceGraph
+        own_graph = graph = DeviceGraph(indptr, indices, device=dev)
+    if graph is not None:                           # a device graph on this rank's GPU
+        dg = graph if hasattr(graph, "handle") else graph.device_graph
+        info = dg.info()
+        n, d = int(info.n), int(info.max_out_degree)
+        alpha, gamma, max_iterations = _validate(n, d, crit, alpha, max_iterations)
+        if undirected and not dg.is_symmetric():
+            raise ParameterError("undirected mode requires a symmetric arc set")
+        plan = DevicePlan(n, world, d)
 
-    def make(fz):
-        return CudaShard(plan, rank, device=dev, alpha=alpha, gamma=gamma, crit=crit,
-                         undirected=undirected, max_iterations=max_iterations, fused=fz,
-                         full=dg)
-    try:
+        def make(fz):
+            return CudaShard(plan, rank, device=dev, alpha=alpha, gamma=gamma, crit=crit,
+                             undirected=undirected, max_iterations=max_iterations, fused=fz,
+                             full=dg)
+        try:
+            backend, _mode = connect_shard(make, dist, rank, world, f"cuda:{dev}", fused)
+        finally:
+            if own_graph is not None:
+                own_graph.close()
+    else:
+        # the host CSR: only indptr and this rank's rows go to its GPU; the
+        # arc set's symmetry is then decided across the ranks, exactly
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        n = ip.size - 1
+        d = int(np.diff(ip).max()) if n > 0 else 0
+        alpha, gamma, max_iterations = _validate(n, d, crit, alpha, max_iterations)
+        plan = DevicePlan(n, world, d)
+
+        def make(fz):
+            return CudaShard(plan, rank, ip, ix, device=dev, alpha=alpha, gamma=gamma,
+                             crit=crit, undirected=undirected, max_iterations=max_iterations,
+                             fused=fz, host_build=True)
         backend, _mode = connect_shard(make, dist, rank, world, f"cuda:{dev}", fused)
-    finally:
-        if own_full:
-            full.close()
+        if undirected and not shards_symmetric(backend, dist, world):
+            backend.close()
+            raise ParameterError("undirected mode requires a symmetric arc set")
     backend.collective_device = f"cuda:{dev}"
     return ShardedRun(backend, plan, crit, rank=rank, world=world,
                       max_iterations=max_iterations).run()
 
 
-__all__ = ["ShardPlan", "DevicePlan", "CudaShard", "ShardedRun", "sharded_run", "connect_shard", "fast_split"]
+__all__ = ["ShardPlan", "DevicePlan", "CudaShard", "ShardedRun", "sharded_run",
+           "shards_symmetric", "connect_shard", "fast_split"]

@@ -30,7 +30,8 @@ def _lockstep(g0, crit, world, protocol="device", split=0, fused=False, build="h
     full = P.DeviceGraph(g0.indptr, g0.indices, device=0) if build == "device" else None
     shards = [D.CudaShard(plan, rk, g0.indptr, g0.indices, device=0, alpha=alpha,
                           gamma=gamma, crit=crit, undirected=True, max_iterations=cap,
-                          split_threshold=split, fused=fused, full=full)
+                          split_threshold=split, fused=fused, full=full,
+                          host_build=build == "gather")
               for rk in range(world)]
     if full is not None:
         full.close()
@@ -138,11 +139,14 @@ def _lockstep(g0, crit, world, protocol="device", split=0, fused=False, build="h
                           (3, "device", False, "host"), (2, "host", False, "host"),
                           (2, "device", True, "host"), (3, "host", True, "host"),
                           (1, "device", False, "device"), (3, "device", False, "device"),
-                          (4, "device", True, "device")])
+                          (4, "device", True, "device"), (2, "device", False, "gather"),
+                          (5, "device", True, "gather")])
 def test_cuda_shards_equal_single_gpu(world, protocol, fused, build):
     """fused: K1 stores omega straight into the other shards' level buffers
     (the NVLink exchange), no all-gather.  build="device": shards cut out of
-    a device graph on the GPU (kb_graph_create_shard)."""
+    a device graph on the GPU (kb_graph_create_shard); build="gather": from the
+    host CSR, only indptr and the rank's rows uploaded
+    (kb_graph_create_shard_host)."""
     g0 = O.rmat_graph(1 << 14, edge_factor=16, seed=42)
     crit = P.Criterion.top_k(100, 1e-6)
     r, order, lower, upper, pairs = _lockstep(g0, crit, world, protocol, fused=fused,
@@ -292,6 +296,14 @@ def test_sharded_run_one_rank_nccl_speculative():
         with pytest.raises(P.ParameterError, match="max_iterations"):
             D.sharded_run(g0.indptr, g0.indices, crit, device=0, undirected=True,
                           max_iterations=0)
+        # the host-gather shard's distributed symmetry check through NCCL's
+        # all-to-all (the path sharded_run takes at more than one rank)
+        plan = D.DevicePlan(g0.node_count, 1, int(np.diff(g0.indptr).max()))
+        for ip, ix, sym in ((g0.indptr, g0.indices, True), (ip_bad, ix_bad, False)):
+            sh = D.CudaShard(plan, 0, ip, ix, device=0, alpha=1e-4, gamma=1.0, crit=crit,
+                             undirected=True, max_iterations=10, host_build=True)
+            assert D.shards_symmetric(sh, dist, 1) == sym
+            sh.close()
     finally:
         dist.destroy_process_group()
     g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
@@ -387,3 +399,51 @@ def test_device_shard_csr_equals_host_plan(world):
             np.testing.assert_array_equal(dix, hix)
             L.kb_graph_destroy(h)
         dg.close()
+
+
+def _exchange_symmetry(shards):
+    """shards_symmetric's all-to-all, by hand between lockstep shards."""
+    parts = [s.symmetry_keys() for s in shards]
+    oks = []
+    for q, s in enumerate(shards):
+        recv = []
+        for keys, counts in parts:
+            a = sum(counts[:q])
+            recv.append(keys[a:a + counts[q]])
+        oks.append(s.symmetry_verify(torch.cat(recv)))
+    return oks
+
+
+@pytest.mark.parametrize("world", [1, 2, 5])
+def test_host_gather_shards_decide_symmetry_exactly(world):
+    """kb_graph_create_shard_host + the distributed symmetry check: every
+    rank agrees on a symmetric R-MAT graph; dropping one arc (its reversal
+    kept) makes some rank refuse -- Graph.is_symmetric, exactly."""
+    g0 = O.rmat_graph(1 << 12, edge_factor=8, seed=4)
+    crit = P.Criterion.top_k(10, 1e-6)
+    cases = [(g0.indptr, g0.indices, True)]
+    cut = int(g0.indptr[7]) + 1                       # an arc of row 7
+    ip = g0.indptr.copy()
+    ip[8:] -= 1
+    cases.append((ip, np.delete(g0.indices, cut), False))
+    for ip, ix, sym in cases:
+        plan = D.DevicePlan(ip.size - 1, world, int(np.diff(ip).max()))
+        shards = [D.CudaShard(plan, rk, ip, ix, device=0, alpha=1e-4, gamma=1.0, crit=crit,
+                              undirected=True, max_iterations=10, host_build=True)
+                  for rk in range(world)]
+        oks = _exchange_symmetry(shards)
+        assert all(oks) == sym, (world, sym, oks)
+        for s in shards:
+            s.close()
+
+
+def test_host_gather_shard_rejects_bad_rows():
+    """Rows must hold strictly ascending ids in [0, n) (kb_graph_create's rule)."""
+    g0 = O.rmat_graph(1 << 10, edge_factor=8, seed=4)
+    ix = g0.indices.copy()
+    ix[g0.indptr[3]], ix[g0.indptr[3] + 1] = ix[g0.indptr[3] + 1], ix[g0.indptr[3]]
+    plan = D.DevicePlan(g0.node_count, 1, int(np.diff(g0.indptr).max()))
+    with pytest.raises(P.ParameterError, match="ascending"):
+        D.CudaShard(plan, 0, g0.indptr, ix, device=0, alpha=1e-4, gamma=1.0,
+                    crit=P.Criterion.top_k(5), undirected=True, max_iterations=5,
+                    host_build=True)
