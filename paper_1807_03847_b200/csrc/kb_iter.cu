@@ -400,6 +400,79 @@ __global__ void __launch_bounds__(1024, 2) k_sell_narrow(IterArgs A) {
     if (A.npeer) __threadfence_system();
 }
 
+
+// All-narrow graphs, software-pipelined: a static schedule of Q-slice groups
+// per warp where the next group's row metadata, katz and column ids are
+// loaded before the current group's gathers are consumed, so the three
+// dependent round trips of a group (metadata -> columns -> omega) overlap
+// with the previous group's.
+template <int Q>
+struct NarrowStage {
+    int len[Q];
+    int64_t row[Q];
+    double kz[Q];
+    int32_t cc[Q][4];
+};
+
+template <int Q>
+__device__ __forceinline__ void narrow_load(const IterArgs &A, int64_t s0, int lane, uint64_t pol,
+                                            NarrowStage<Q> &S) {
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        const int64_t sq = s0 + q;
+        const int64_t vq = sq * 32 + lane;
+        const bool ok = sq < A.nslices && vq < A.nvr;
+        S.len[q] = ok ? A.vlen[vq] : 0;
+        const int w = sq < A.nslices ? A.slice_w[sq] : 0;
+        const int32_t *base = A.cols + (sq < A.nslices ? A.slice_off[sq] : 0);
+        S.row[q] = -1;
+        if (ok && vq >= A.nseg) S.row[q] = A.vrow ? A.vrow[vq - A.nseg] : A.nh + (vq - A.nseg);
+        S.kz[q] = (S.row[q] >= 0 && !A.level_only) ? A.katz[S.row[q]] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) S.cc[q][j] = (j < w) ? ld_stream_i1(base + j * 32 + lane, pol) : 0;
+    }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(1024, 1) k_sell_narrow_pf(IterArgs A) {
+    if (aborted(A)) return;
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol = evict_first_policy();
+    const HotMap hm{0, 0, 0, 0u, 0, 0, 0u};
+    const int64_t groups = (A.nslices + Q - 1) / Q;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (wid >= groups) return;
+    NarrowStage<Q> cur;
+    narrow_load<Q>(A, wid * Q, lane, pol, cur);
+    for (int64_t gi = wid; gi < groups; gi += nw) {
+        NarrowStage<Q> nxt;
+        const int64_t gn = gi + nw;
+        if (gn < groups) narrow_load<Q>(A, gn * Q, lane, pol, nxt);
+        double v[Q][4];
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                KB_DCHECK(j >= cur.len[q] || (cur.cc[q][j] >= 0 && cur.cc[q][j] < A.ncols));
+                v[q][j] = (j < cur.len[q]) ? fetch<0, 0>(nullptr, hm, A.x, cur.cc[q][j]) : 0.0;
+            }
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+            double sum = 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) sum = __dadd_rn(sum, v[q][j]);
+            const int64_t vq = (gi * Q + q) * 32 + lane;
+            if (gi * Q + q < A.nslices && vq < A.nvr) {
+                if (vq < A.nseg) A.seg_sum[vq] = sum;
+                else if (!A.seg_only) epilogue_k(A, cur.row[q], sum, cur.kz[q]);
+            }
+        }
+        if (gn < groups) cur = nxt;
+    }
+    if (A.npeer) __threadfence_system();
+}
+
 // First iteration: x = levels[0] = ones, so every sequential row (or segment)
 // sum is exactly its length -- the same bits K1 would produce -- and no
 // gather is needed: w_1 = alpha * deg.
@@ -633,11 +706,16 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         note_launch();
         KB_CUDA(cudaGetLastError());
     } else if (A.nslices && g.sell.nwide == 0 && A.nseg == 0 &&
-               (!A.lazy_bounds || tune_get("k1.narrow_lazy", 0)) &&
+               (!A.lazy_bounds || tune_get("k1.narrow_lazy", 0) || tune_get("k1.narrow_pf", 2)) &&
                tune_get("k1.narrow_kernel", 1)) {
-        // (without the bound stores the persistent kernel is faster on C4:
-        // 0.18 vs 0.215 ms; with them the narrow one: 0.267 vs 0.37 ms)
-        if (tune_get("k1.narrow_q", 2) == 4) k_sell_narrow<4><<<g.sm_count * 2, 1024, 0, st>>>(A);
+        // C4 (4096^2 grid) per launch: pipelined narrow kernel 0.1825 ms with
+        // lazy bounds / 0.223 ms with the bound stores; the unpipelined one
+        // 0.1954 / 0.250; the persistent kernel 0.1929 / 0.37
+        const int pf = (int)tune_get("k1.narrow_pf", 2);
+        if (pf == 1) k_sell_narrow_pf<1><<<g.sm_count, 1024, 0, st>>>(A);
+        else if (pf == 2) k_sell_narrow_pf<2><<<g.sm_count, 1024, 0, st>>>(A);
+        else if (pf == 4) k_sell_narrow_pf<4><<<g.sm_count, 1024, 0, st>>>(A);
+        else if (tune_get("k1.narrow_q", 2) == 4) k_sell_narrow<4><<<g.sm_count * 2, 1024, 0, st>>>(A);
         else k_sell_narrow<2><<<g.sm_count * 2, 1024, 0, st>>>(A);
         note_launch();
         KB_CUDA(cudaGetLastError());
