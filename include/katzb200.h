@@ -64,6 +64,8 @@ typedef struct {
     int64_t hot_size;         /* leading (hottest) x entries staged in smem  */
     int64_t version;          /* bumped by kb_update_batch                   */
     int64_t device_bytes;     /* device memory held by the graph             */
+    int64_t overflow_rows;    /* rows edited past their SELL lane (batches)  */
+    int64_t overflow_long;    /* ... of which longer than 256 arcs           */
 } kb_graph_info;
 
 typedef struct {

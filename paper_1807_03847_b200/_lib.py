@@ -41,7 +41,7 @@ class GraphInfo(ctypes.Structure):
     _fields_ = [(name, i64) for name in (
         "n", "nnz", "max_out_degree", "nonisolated", "heavy_rows", "segments",
         "slices", "sell_elems", "split_threshold", "hot_size", "version",
-        "device_bytes")]
+        "device_bytes", "overflow_rows", "overflow_long")]
 
 
 class StateInfo(ctypes.Structure):

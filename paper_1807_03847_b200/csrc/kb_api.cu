@@ -1090,6 +1090,8 @@ int kb_graph_info_get(const kb_graph *h, kb_graph_info *info) {
         info->hot_size = std::min<int64_t>(g.hot, g.n);
         info->version = g.version;
         info->device_bytes = (int64_t)g.device_bytes();
+        info->overflow_rows = g.n_ovf;
+        info->overflow_long = g.n_ovf_long;
     });
 }
 

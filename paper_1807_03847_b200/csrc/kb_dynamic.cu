@@ -61,23 +61,6 @@ __global__ void k_cap32(const int64_t *cap, int64_t n, int32_t *rcap) {
     if (v < n) rcap[v] = (int32_t)min(cap[v], (int64_t)INT32_MAX);
 }
 
-// move row rows[e] (old content, rlen slots) to new_start[e], capacity new_cap[e]
-__global__ void k_relocate(const int32_t *rows, const int64_t *new_start,
-                           const int32_t *new_cap, int64_t ne, int64_t *indptr,
-                           const int32_t *rlen, int32_t *rcap, int32_t *indices) {
-    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (e >= ne) return;
-    const int32_t v = rows[e];
-    const int64_t a = indptr[v], b = new_start[e];
-    const int64_t L = rlen[v];
-    for (int64_t j = lane; j < L; j += 32) indices[b + j] = indices[a + j];
-    __syncwarp();
-    if (lane == 0) {
-        indptr[v] = b;
-        rcap[v] = new_cap[e];
-    }
-}
 
 // Row copy old -> new layout.  Short rows: a block takes 256 consecutive
 // rows, scans their lengths in shared memory and copies the concatenated
@@ -271,19 +254,7 @@ __global__ void k_apply_edits(const int32_t *rows, int64_t ne, const int64_t *dp
     if (t == 0) rlen[v] = (int32_t)nl;
 }
 
-__global__ void k_scatter_extra(const int32_t *rows, const int32_t *x, int64_t ne, int32_t *dst) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e < ne) dst[rows[e]] = x[e];
-}
 
-__global__ void k_gather_len(const int32_t *rlen, const int32_t *rcap, const int32_t *rows,
-                             int64_t ne, int64_t *len_cap) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= ne) return;
-    const int32_t v = rows[e];
-    len_cap[2 * e] = rlen[v];
-    len_cap[2 * e + 1] = rcap[v];
-}
 
 // ---------------------------------------------------------------- transpose
 
@@ -616,6 +587,17 @@ __global__ void k_pull_affect(const int64_t *indptr, const int32_t *rlen, const 
     }
 }
 
+// sources of every edit, then targets: ends[0..m) and ends[m..2m)
+__global__ void k_batch_ends(const int64_t *ins, int64_t ni, const int64_t *dels, int64_t nd,
+                             int32_t *ends) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t m = ni + nd;
+    if (i >= m) return;
+    const int64_t *a = i < ni ? ins + 2 * i : dels + 2 * (i - ni);
+    ends[i] = (int32_t)a[0];
+    ends[m + i] = (int32_t)a[1];
+}
+
 __global__ void k_map_new(const int32_t *orig, int64_t m, const int32_t *iperm, int32_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < m) out[i] = iperm[orig[i]];
@@ -792,129 +774,213 @@ static void build_transpose(Graph &g, DBuf<int64_t> &tip, DBuf<int32_t> &tix) {
     KB_CUDA(cudaStreamSynchronize(st));
 }
 
-void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
-                          int64_t n_dels) {
+namespace {
+
+// ---------------------------------------------------------------- edit grouping
+// One 64-bit key per edit: src << 33 | kind << 32 | dst (kind 0 delete,
+// 1 insert), so a plain integer sort groups the edits by row with the
+// deletions first and the dsts ascending (the order k_apply_edits merges in).
+__global__ void k_edit_keys(const int64_t *ins, int64_t ni, const int64_t *dels, int64_t nd,
+                            uint64_t *keys) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nd) {
+        keys[i] = ((uint64_t)(uint32_t)dels[2 * i] << 33) | (uint32_t)dels[2 * i + 1];
+    } else if (i < nd + ni) {
+        const int64_t j = i - nd;
+        keys[i] = ((uint64_t)(uint32_t)ins[2 * j] << 33) | (1ull << 32) | (uint32_t)ins[2 * j + 1];
+    }
+}
+
+// packed per-edit counters: (row head) << 32 | (is a deletion)
+__global__ void k_edit_flags(const uint64_t *k, int64_t m, uint64_t *fl) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const bool head = i == 0 || (k[i] >> 33) != (k[i - 1] >> 33);
+    fl[i] = ((uint64_t)head << 32) | (uint64_t)(((k[i] >> 32) & 1) == 0);
+}
+
+// from the exclusive scan of the flags: row e's id and its deletion and
+// insertion ranges; the dst lists split by kind (each ascending per row)
+__global__ void k_edit_scatter(const uint64_t *k, const uint64_t *sc, int64_t m, int32_t *rows,
+                               int64_t *dptr, int64_t *iptr, int32_t *del, int32_t *ins,
+                               int64_t *ne_out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const bool head = i == 0 || (k[i] >> 33) != (k[i - 1] >> 33);
+    const bool isdel = ((k[i] >> 32) & 1) == 0;
+    const int64_t e = (int64_t)(sc[i] >> 32), dc = (int64_t)(sc[i] & 0xffffffffu);
+    if (head) {
+        rows[e] = (int32_t)(k[i] >> 33);
+        dptr[e] = dc;
+        iptr[e] = i - dc;
+    }
+    if (isdel) del[dc] = (int32_t)(uint32_t)k[i];
+    else ins[i - dc] = (int32_t)(uint32_t)k[i];
+    if (i == m - 1) {
+        const int64_t ne = e + head, nd = dc + isdel;
+        dptr[ne] = nd;
+        iptr[ne] = m - nd;
+        *ne_out = ne;
+    }
+}
+
+// capacity plan per edited row: the merged length, the relocation capacity
+// when it outgrows its slack (0 if it fits) and its scratch size
+__global__ void k_cap_plan(const int32_t *rows, const int64_t *ne_p, const int64_t *dptr,
+                           const int64_t *iptr, const int32_t *rlen, const int32_t *rcap,
+                           int64_t *need, int64_t *tsz) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t ne = *ne_p;
+    if (e > ne) return;
+    if (e == ne) { need[e] = tsz[e] = 0; return; }
+    const int32_t v = rows[e];
+    const int64_t L = rlen[v];
+    const int64_t nl = L - (dptr[e + 1] - dptr[e]) + (iptr[e + 1] - iptr[e]);
+    need[e] = nl > rcap[v] ? nl + max((int64_t)2, nl / 8) : 0;
+    tsz[e] = max(nl, L);
+}
+
+// summary for the host: rows, relocation slots, relocated rows, scratch size
+__global__ void k_cap_summary(const int64_t *ne_p, const int64_t *need, const int64_t *need_off,
+                              const int64_t *toff, int64_t *out) {
+    __shared__ unsigned long long nover;
+    const int64_t ne = *ne_p;
+    if (threadIdx.x == 0) nover = 0;
+    __syncthreads();
+    unsigned long long c = 0;
+    for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) c += need[e] > 0;
+    atomicAdd(&nover, c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = ne;
+        out[1] = need_off[ne];
+        out[2] = (int64_t)nover;
+        out[3] = toff[ne];
+    }
+}
+
+// move every row that outgrew its slack to tail + need_off[e]
+__global__ void k_relocate_planned(const int32_t *rows, const int64_t *ne_p, const int64_t *need,
+                                   const int64_t *need_off, int64_t tail, int64_t *indptr,
+                                   const int32_t *rlen, int32_t *rcap, int32_t *indices) {
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= *ne_p || need[e] == 0) return;
+    const int32_t v = rows[e];
+    const int64_t a = indptr[v], b = tail + need_off[e];
+    const int64_t L = rlen[v];
+    for (int64_t j = lane; j < L; j += 32) indices[b + j] = indices[a + j];
+    __syncwarp();
+    if (lane == 0) {
+        indptr[v] = b;
+        rcap[v] = (int32_t)min(need[e], (int64_t)INT32_MAX);
+    }
+}
+
+// re-spread slack: each edited row gets room for its insertions
+__global__ void k_extra_from_edits(const int32_t *rows, const int64_t *ne_p, const int64_t *iptr,
+                                   int32_t *extra) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < *ne_p) extra[rows[e]] = (int32_t)(iptr[e + 1] - iptr[e]);
+}
+
+}  // namespace
+
+// Edits already on the device (ins / dels: (m, 2) int64 rows, validated):
+// grouped by source row, capacity planned, rows relocated and merged, SELL
+// patched -- one small host read (the plan's totals) in the whole call.
+void apply_batch_dev(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                     int64_t n_dels) {
     cudaStream_t st = g.stream;
-    // group the edits by source row (host; batches are small)
-    // one 64-bit key per edit: src | kind (0 delete, 1 insert) | dst, so a
-    // plain integer sort groups by row with deletions first, dsts ascending
-    std::vector<uint64_t> ed;
-    ed.reserve(n_ins + n_dels);
-    for (int64_t i = 0; i < n_dels; i++)
-        ed.push_back(((uint64_t)(uint32_t)dels[2 * i] << 33) | (uint32_t)dels[2 * i + 1]);
-    for (int64_t i = 0; i < n_ins; i++)
-        ed.push_back(((uint64_t)(uint32_t)ins[2 * i] << 33) | (1ull << 32) |
-                     (uint32_t)ins[2 * i + 1]);
-    if (ed.empty()) return;
+    const int64_t m = n_ins + n_dels;
+    if (m == 0) return;
     PhaseTrace tr(st);
-    if (ed.size() < 4096) {
-        std::sort(ed.begin(), ed.end());
-    } else {  // large batches: radix sort on the device
-        const int64_t m = (int64_t)ed.size();
-        DBuf<uint64_t> a, b;
-        a.alloc(m);
-        b.alloc(m);
-        KB_CUDA(cudaMemcpyAsync(a.p, ed.data(), m * 8, cudaMemcpyHostToDevice, st));
-        cub_run([&](void *t, size_t &bb) {
-            return cub::DeviceRadixSort::SortKeys(t, bb, a.p, b.p, (int)m, 0, 64, st);
-        });
-        KB_CUDA(cudaMemcpyAsync(ed.data(), b.p, m * 8, cudaMemcpyDeviceToHost, st));
-        KB_CUDA(cudaStreamSynchronize(st));
-    }
-    std::vector<int32_t> rows, dl, il;
-    std::vector<int64_t> dptr{0}, iptr{0};
-    for (size_t i = 0; i < ed.size();) {
-        const uint64_t src = ed[i] >> 33;
-        size_t j = i;
-        rows.push_back((int32_t)src);
-        for (; j < ed.size() && (ed[j] >> 33) == src; j++)
-            ((ed[j] >> 32) & 1 ? il : dl).push_back((int32_t)(uint32_t)ed[j]);
-        dptr.push_back((int64_t)dl.size());
-        iptr.push_back((int64_t)il.size());
-        i = j;
-    }
-    const int64_t ne = (int64_t)rows.size();
-    tr.mark("  host group edits");
+    DBuf<uint64_t> ka, kb, fl, sc;
+    ka.alloc(m); kb.alloc(m); fl.alloc(m); sc.alloc(m);
+    k_edit_keys<<<nblk(m, 256), 256, 0, st>>>(ins, n_ins, dels, n_dels, ka.p);
+    note_launch();
+    int hi = 1;
+    while (hi < 31 && ((int64_t)1 << hi) < g.n) hi++;
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, ka.p, kb.p, (int)m, 0, 33 + hi, st);
+    });
+    k_edit_flags<<<nblk(m, 256), 256, 0, st>>>(kb.p, m, fl.p);
+    note_launch();
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, fl.p, sc.p, (int)m, st);
+    });
     DBuf<int32_t> drows, ddel, dins;
-    DBuf<int64_t> ddptr, diptr, lc;
-    drows.alloc(ne); ddel.alloc(std::max<size_t>(1, dl.size()));
-    dins.alloc(std::max<size_t>(1, il.size())); ddptr.alloc(ne + 1); diptr.alloc(ne + 1);
-    lc.alloc(2 * ne);
-    KB_CUDA(cudaMemcpyAsync(drows.p, rows.data(), ne * 4, cudaMemcpyHostToDevice, st));
-    if (!dl.empty()) KB_CUDA(cudaMemcpyAsync(ddel.p, dl.data(), dl.size() * 4, cudaMemcpyHostToDevice, st));
-    if (!il.empty()) KB_CUDA(cudaMemcpyAsync(dins.p, il.data(), il.size() * 4, cudaMemcpyHostToDevice, st));
-    KB_CUDA(cudaMemcpyAsync(ddptr.p, dptr.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
-    KB_CUDA(cudaMemcpyAsync(diptr.p, iptr.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
+    DBuf<int64_t> ddptr, diptr, ne_d, need, need_off, tsz, toff, summ;
+    drows.alloc(m); ddel.alloc(std::max<int64_t>(1, n_dels)); dins.alloc(std::max<int64_t>(1, n_ins));
+    ddptr.alloc(m + 1); diptr.alloc(m + 1); ne_d.alloc(1);
+    need.alloc(m + 1); need_off.alloc(m + 1); tsz.alloc(m + 1); toff.alloc(m + 1); summ.alloc(4);
+    k_edit_scatter<<<nblk(m, 256), 256, 0, st>>>(kb.p, sc.p, m, drows.p, ddptr.p, diptr.p, ddel.p,
+                                                 dins.p, ne_d.p);
+    note_launch();
+    tr.mark("  group edits");
     // capacity check (slack CSR); re-spread once if any edited row overflows
     if (!g.slack) respread(g, nullptr);
-    k_gather_len<<<nblk(ne, 256), 256, 0, st>>>(g.rlen.p, g.rcap.p, drows.p, ne, lc.p);
+    k_cap_plan<<<nblk(m + 1, 256), 256, 0, st>>>(drows.p, ne_d.p, ddptr.p, diptr.p, g.rlen.p,
+                                                 g.rcap.p, need.p, tsz.p);
     note_launch();
-    std::vector<int64_t> hlc(2 * ne);
-    KB_CUDA(cudaMemcpyAsync(hlc.data(), lc.p, 2 * ne * 8, cudaMemcpyDeviceToHost, st));
+    // rows past ne hold garbage; the scans over m + 1 are read up to ne only
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, need.p, need_off.p, (int)(m + 1), st);
+    });
+    cub_run([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, tsz.p, toff.p, (int)(m + 1), st);
+    });
+    k_cap_summary<<<1, 1024, 0, st>>>(ne_d.p, need.p, need_off.p, toff.p, summ.p);
+    note_launch();
+    int64_t hs[4];
+    KB_CUDA(cudaMemcpyAsync(hs, summ.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    std::vector<int64_t> toff(ne + 1, 0);
-    std::vector<int32_t> ov_rows, ov_cap;
-    std::vector<int64_t> ov_start;
-    int64_t need = 0;
-    for (int64_t e = 0; e < ne; e++) {
-        const int64_t nl = hlc[2 * e] - (dptr[e + 1] - dptr[e]) + (iptr[e + 1] - iptr[e]);
-        if (nl > hlc[2 * e + 1]) {            // outgrows its slack: relocate
-            const int64_t cap = nl + std::max<int64_t>(2, nl / 8);
-            ov_rows.push_back(rows[e]);
-            ov_cap.push_back((int32_t)cap);
-            ov_start.push_back(g.tail + need);
-            need += cap;
-        }
-        toff[e + 1] = toff[e] + std::max<int64_t>(nl, hlc[2 * e]);
-    }
+    const int64_t ne = hs[0], need_total = hs[1], n_over = hs[2], tmp_total = hs[3];
     tr.mark("  capacity check");
-    if (!ov_rows.empty() && g.tail + need <= (int64_t)g.indices.n) {
-        const int64_t no = (int64_t)ov_rows.size();
-        DBuf<int32_t> r, c;
-        DBuf<int64_t> b;
-        r.alloc(no); c.alloc(no); b.alloc(no);
-        KB_CUDA(cudaMemcpyAsync(r.p, ov_rows.data(), no * 4, cudaMemcpyHostToDevice, st));
-        KB_CUDA(cudaMemcpyAsync(c.p, ov_cap.data(), no * 4, cudaMemcpyHostToDevice, st));
-        KB_CUDA(cudaMemcpyAsync(b.p, ov_start.data(), no * 8, cudaMemcpyHostToDevice, st));
-        k_relocate<<<nblk(no * 32, 256), 256, 0, st>>>(r.p, b.p, c.p, no, g.indptr.p, g.rlen.p,
-                                                      g.rcap.p, g.indices.p);
+    if (n_over && g.tail + need_total <= (int64_t)g.indices.n) {
+        k_relocate_planned<<<nblk(ne * 32, 256), 256, 0, st>>>(drows.p, ne_d.p, need.p,
+                                                               need_off.p, g.tail, g.indptr.p,
+                                                               g.rlen.p, g.rcap.p, g.indices.p);
         note_launch();
-        KB_CUDA(cudaStreamSynchronize(st));
-        g.tail += need;
+        g.tail += need_total;
         tr.mark("  relocate rows");
-    } else if (!ov_rows.empty()) {
+    } else if (n_over) {
         // the tail is full: re-spread everything (with fresh tail room)
-        std::vector<int32_t> extra(ne);
-        for (int64_t e = 0; e < ne; e++) extra[e] = (int32_t)(iptr[e + 1] - iptr[e]);
-        DBuf<int32_t> dex, dx;
+        DBuf<int32_t> dex;
         dex.alloc(g.n);
-        dx.alloc(ne);
         KB_CUDA(cudaMemsetAsync(dex.p, 0, g.n * 4, st));
-        KB_CUDA(cudaMemcpyAsync(dx.p, extra.data(), ne * 4, cudaMemcpyHostToDevice, st));
-        k_scatter_extra<<<nblk(ne, 256), 256, 0, st>>>(drows.p, dx.p, ne, dex.p);
+        k_extra_from_edits<<<nblk(ne, 256), 256, 0, st>>>(drows.p, ne_d.p, diptr.p, dex.p);
         note_launch();
         respread(g, dex.p);
         KB_CUDA(cudaStreamSynchronize(st));
         tr.mark("  respread");
     }
-    DBuf<int64_t> dtoff;
     DBuf<int32_t> tmp;
-    dtoff.alloc(ne + 1);
-    tmp.alloc(std::max<int64_t>(1, toff[ne]));
-    KB_CUDA(cudaMemcpyAsync(dtoff.p, toff.data(), (ne + 1) * 8, cudaMemcpyHostToDevice, st));
-    k_apply_edits<<<(unsigned)ne, 128, 0, st>>>(drows.p, ne, ddptr.p, ddel.p, diptr.p,
-                                                       dins.p, dtoff.p, tmp.p, g.indptr.p,
-                                                       g.indices.p, g.rlen.p, g.rcap.p,
-                                                       (int64_t)g.indices.n);
+    tmp.alloc(std::max<int64_t>(1, tmp_total));
+    k_apply_edits<<<(unsigned)ne, 128, 0, st>>>(drows.p, ne, ddptr.p, ddel.p, diptr.p, dins.p,
+                                                toff.p, tmp.p, g.indptr.p, g.indices.p, g.rlen.p,
+                                                g.rcap.p, (int64_t)g.indices.n);
     note_launch();
     KB_CUDA(cudaGetLastError());
-    KB_CUDA(cudaStreamSynchronize(st));
     tr.mark("  edit rows");
     g.nnz += n_ins - n_dels;
     patch_sell(g, drows.p, ne);
+    KB_CUDA(cudaStreamSynchronize(st));
     tr.mark("  patch SELL");
     g.mutated = true;
     g.version += 1;
+}
+
+void apply_batch_to_graph(Graph &g, const int64_t *ins, int64_t n_ins, const int64_t *dels,
+                          int64_t n_dels) {
+    if (n_ins + n_dels == 0) return;
+    cudaStream_t st = g.stream;
+    DBuf<int64_t> di, dd;
+    di.alloc(std::max<int64_t>(1, 2 * n_ins));
+    dd.alloc(std::max<int64_t>(1, 2 * n_dels));
+    if (n_ins) KB_CUDA(cudaMemcpyAsync(di.p, ins, n_ins * 16, cudaMemcpyHostToDevice, st));
+    if (n_dels) KB_CUDA(cudaMemcpyAsync(dd.p, dels, n_dels * 16, cudaMemcpyHostToDevice, st));
+    apply_batch_dev(g, di.p, n_ins, dd.p, n_dels);
 }
 
 namespace {
@@ -939,23 +1005,6 @@ static void diff_changed(const double *old, const double *nw, int64_t n, int32_t
     KB_CUDA(cudaMemcpyAsync(count, c64.p, 8, cudaMemcpyDeviceToDevice, st));
 }
 
-// ascending node ids (>= 0): two 16-bit LSD counting passes (batches of
-// 1e5 edges carry 2e5 ids; std::sort took ~5 ms per list here)
-static void sort_ids(std::vector<int32_t> &a) {
-    if (a.size() < 2048) {
-        std::sort(a.begin(), a.end());
-        return;
-    }
-    std::vector<int32_t> b(a.size());
-    for (int sh = 0; sh < 32; sh += 16) {
-        std::vector<size_t> cnt(65537, 0);
-        for (int32_t x : a) cnt[(((uint32_t)x >> sh) & 0xffffu) + 1]++;
-        for (size_t d = 1; d < cnt.size(); d++) cnt[d] += cnt[d - 1];
-        for (int32_t x : a) b[cnt[((uint32_t)x >> sh) & 0xffffu]++] = x;
-        a.swap(b);
-    }
-}
-
 void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *dels,
                   int64_t n_dels, double theta, double new_gamma, kb_update_stats *stats) {
     NvtxRange nv("K4 update_batch");
@@ -972,39 +1021,57 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     st_out.batch_size = n_ins + n_dels;
     st_out.aborted_level = -1;
 
-    // seeds (sources) and targets, as new ids
-    std::vector<int32_t> seeds_o, targets_o;
-    for (int64_t i = 0; i < n_ins; i++) { seeds_o.push_back((int32_t)ins[2 * i]); targets_o.push_back((int32_t)ins[2 * i + 1]); }
-    for (int64_t i = 0; i < n_dels; i++) { seeds_o.push_back((int32_t)dels[2 * i]); targets_o.push_back((int32_t)dels[2 * i + 1]); }
-    sort_ids(seeds_o);
-    seeds_o.erase(std::unique(seeds_o.begin(), seeds_o.end()), seeds_o.end());
-    sort_ids(targets_o);
-    targets_o.erase(std::unique(targets_o.begin(), targets_o.end()), targets_o.end());
-    st_out.seeds = (int64_t)seeds_o.size();
-    // seeds and targets as new ids (mapped on the device)
-    std::vector<int32_t> seeds(seeds_o.size()), targets(targets_o.size());
+    // the batch on the device once: seeds (sources) and targets, deduplicated
+    // in original-id order and mapped to new ids, and the edits themselves
+    const int64_t m = n_ins + n_dels;
+    DBuf<int64_t> d_ins, d_dels;
+    d_ins.alloc(std::max<int64_t>(1, 2 * n_ins));
+    d_dels.alloc(std::max<int64_t>(1, 2 * n_dels));
+    if (n_ins) KB_CUDA(cudaMemcpyAsync(d_ins.p, ins, n_ins * 16, cudaMemcpyHostToDevice, st));
+    if (n_dels) KB_CUDA(cudaMemcpyAsync(d_dels.p, dels, n_dels * 16, cudaMemcpyHostToDevice, st));
+    DBuf<int32_t> dseeds, dtargets;
+    int64_t ns = 0, nt = 0;
     {
-        DBuf<int32_t> a, b;
-        const int64_t m1 = (int64_t)seeds_o.size(), m2 = (int64_t)targets_o.size();
-        a.alloc(std::max<int64_t>(1, m1 + m2));
-        b.alloc(std::max<int64_t>(1, m1 + m2));
-        if (m1) KB_CUDA(cudaMemcpyAsync(a.p, seeds_o.data(), m1 * 4, cudaMemcpyHostToDevice, st));
-        if (m2)
-            KB_CUDA(cudaMemcpyAsync(a.p + m1, targets_o.data(), m2 * 4, cudaMemcpyHostToDevice, st));
-        if (m1 + m2) {
-            k_map_new<<<nblk(m1 + m2, 256), 256, 0, st>>>(a.p, m1 + m2, g.iperm.p, b.p);
+        DBuf<int32_t> ends, sorted, uniq;
+        DBuf<int64_t> cnt2;
+        ends.alloc(std::max<int64_t>(1, 2 * m));
+        sorted.alloc(std::max<int64_t>(1, 2 * m));
+        uniq.alloc(std::max<int64_t>(1, 2 * m));
+        cnt2.alloc(2);
+        dseeds.alloc(std::max<int64_t>(1, m));
+        dtargets.alloc(std::max<int64_t>(1, m));
+        KB_CUDA(cudaMemsetAsync(cnt2.p, 0, 16, st));
+        if (m) {
+            k_batch_ends<<<nblk(m, 256), 256, 0, st>>>(d_ins.p, n_ins, d_dels.p, n_dels, ends.p);
             note_launch();
+            int hi = 1;
+            while (hi < 31 && ((int64_t)1 << hi) < n) hi++;
+            for (int side = 0; side < 2; side++) {
+                cub_run([&](void *t, size_t &b) {
+                    return cub::DeviceRadixSort::SortKeys(t, b, ends.p + side * m,
+                                                          sorted.p + side * m, (int)m, 0, hi, st);
+                });
+                cub_run([&](void *t, size_t &b) {
+                    return cub::DeviceSelect::Unique(t, b, sorted.p + side * m, uniq.p + side * m,
+                                                     cnt2.p + side, (int)m, st);
+                });
+            }
         }
-        if (m1) KB_CUDA(cudaMemcpyAsync(seeds.data(), b.p, m1 * 4, cudaMemcpyDeviceToHost, st));
-        if (m2)
-            KB_CUDA(cudaMemcpyAsync(targets.data(), b.p + m1, m2 * 4, cudaMemcpyDeviceToHost, st));
+        int64_t hc[2];
+        KB_CUDA(cudaMemcpyAsync(hc, cnt2.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
         KB_CUDA(cudaStreamSynchronize(st));
+        ns = hc[0];
+        nt = hc[1];
+        if (ns) k_map_new<<<nblk(ns, 256), 256, 0, st>>>(uniq.p, ns, g.iperm.p, dseeds.p);
+        if (nt) k_map_new<<<nblk(nt, 256), 256, 0, st>>>(uniq.p + m, nt, g.iperm.p, dtargets.p);
+        note_launch(2);
     }
+    st_out.seeds = ns;
 
     PhaseTrace tr(st);
     // 1. the post-batch arc set on the device
     const bool was_sym = g.symmetric == 1;
-    apply_batch_to_graph(g, ins, n_ins, dels, n_dels);
+    apply_batch_dev(g, d_ins.p, n_ins, d_dels.p, n_dels);
     tr.mark("apply batch");
     if (!(was_sym && s.undirected)) g.symmetric = -1;
     // in-neighbours: the CSR itself when undirected (symmetric), else a transpose
@@ -1021,20 +1088,16 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     }
 
     // 2. level repair
-    DBuf<int32_t> stamp, R, C, dseeds, HR;
+    DBuf<int32_t> stamp, R, C, HR;
     DBuf<unsigned int> aff;
     DBuf<unsigned char> touched;
     DBuf<unsigned long long> cnt;  // [0]=|R|, [1]=|changed|, [2]=|affected|
     stamp.alloc(n); R.alloc(n); C.alloc(n); HR.alloc(std::max<int64_t>(1, g.nh)); aff.alloc((n + 31) / 32 + 1); touched.alloc(n);
     cnt.alloc(4);
-    dseeds.alloc(std::max<size_t>(1, seeds.size()));
     KB_CUDA(cudaMemsetAsync(stamp.p, 0xff, n * 4, st));
     KB_CUDA(cudaMemsetAsync(aff.p, 0, ((n + 31) / 32 + 1) * 4, st));
     KB_CUDA(cudaMemsetAsync(touched.p, 0, n, st));
     KB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * 8, st));
-    if (!seeds.empty())
-        KB_CUDA(cudaMemcpyAsync(dseeds.p, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice, st));
-    const int64_t ns = (int64_t)seeds.size();
     if (ns) {
         k_affect<<<nblk(ns, 256), 256, 0, st>>>(dseeds.p, ns, aff.p, cnt.p + 2);
         note_launch();
@@ -1079,7 +1142,9 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
             unsigned long long work = 0;
             KB_CUDA(cudaMemcpyAsync(&work, cnt.p + 3, 8, cudaMemcpyDeviceToHost, st));
             KB_CUDA(cudaStreamSynchronize(st));
-            dense = (int64_t)work > std::max<int64_t>(g.nnz / 64, 1 << 20);
+            dense = (int64_t)work > std::max<int64_t>(g.nnz / tune_get("dyn.dense_div", 64), 1 << 20);
+            if (tr.on) fprintf(stderr, "[kb]   level %lld: %lld changed rows, %llu in-arcs\n",
+                               (long long)level, (long long)nchanged, work);
         }
         if (dense) {
             // Dense level: the expansion would reach most rows, so recompute
@@ -1128,6 +1193,8 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
         KB_CUDA(cudaStreamSynchronize(st));
         const int64_t nr = (int64_t)hc[0];
         affected = (int64_t)hc[2];
+        if (tr.on) fprintf(stderr, "[kb]   level %lld: frontier %lld rows\n", (long long)level,
+                           (long long)nr);
         if (nr > n / 64) {
             // a wide frontier: one K1 level (same bits) is cheaper than a
             // warp per row; the changed rows come from the comparison
@@ -1185,13 +1252,8 @@ void update_batch(State &s, const int64_t *ins, int64_t n_ins, const int64_t *de
     }
     // visited = |affected U targets| (dynamic.py:176)
     {
-        DBuf<int32_t> dt;
-        dt.alloc(std::max<size_t>(1, targets.size()));
-        if (!targets.empty()) {
-            KB_CUDA(cudaMemcpyAsync(dt.p, targets.data(), targets.size() * 4,
-                                    cudaMemcpyHostToDevice, st));
-            k_affect<<<nblk((int64_t)targets.size(), 256), 256, 0, st>>>(
-                dt.p, (int64_t)targets.size(), aff.p, cnt.p + 2);
+        if (nt) {
+            k_affect<<<nblk(nt, 256), 256, 0, st>>>(dtargets.p, nt, aff.p, cnt.p + 2);
             note_launch();
         }
         recount_affected();

@@ -261,6 +261,23 @@ __global__ void k_patch_heavy(const int32_t *rows, const int32_t *perm, const in
     }
 }
 
+__global__ void k_ovf_long_list(const int32_t *ovf, int64_t n_ovf, const int32_t *perm,
+                                const int32_t *rlen, int32_t *out, unsigned long long *count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n_ovf && rlen[perm[ovf[i]]] > OVF_LONG) out[atomicAdd(count, 1ull)] = ovf[i];
+}
+
+// trace only: total and longest length of the overflow rows, rows > split
+__global__ void k_ovf_stats(const int32_t *ovf, int64_t n_ovf, const int32_t *perm,
+                            const int32_t *rlen, int64_t split, unsigned long long *out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_ovf) return;
+    const unsigned long long L = (unsigned long long)rlen[perm[ovf[i]]];
+    atomicAdd(&out[0], L);
+    atomicMax(&out[1], L);
+    if ((int64_t)L > split) atomicAdd(&out[2], 1ull);
+}
+
 __global__ void k_arc_flags(const int32_t *rlen, int64_t n, unsigned char *fl, int32_t *iota) {
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
@@ -557,6 +574,8 @@ void build_sell(Graph &g, bool fresh, bool fill) {
     g.ovf.release();
     g.ovf_flag.release();
     g.n_ovf = 0;
+    g.ovf_long.release();
+    g.n_ovf_long = 0;
     KB_CUDA(cudaStreamSynchronize(st));
     g.sell_dirty = false;
 }
@@ -597,6 +616,31 @@ void patch_sell(Graph &g, const int32_t *rows_orig, int64_t ne) {
             g.seg_ptr.p, g.seg_list.p, S.slice_w.p, S.slice_off.p, g.split, S.vlen.p, S.cols.p);
         note_launch();
         KB_CUDA(cudaGetLastError());
+    }
+    if (g.n_ovf) {
+        // long overflow rows get a block each in K1 (a warp's serial chain
+        // over thousands of arcs would be the level's tail)
+        g.ovf_long.alloc(g.n_ovf);
+        KB_CUDA(cudaMemsetAsync(hc.p, 0, 8, st));
+        k_ovf_long_list<<<blocks_for(g.n_ovf, 256), 256, 0, st>>>(g.ovf.p, g.n_ovf, g.perm.p,
+                                                                g.rlen.p, g.ovf_long.p, hc.p);
+        note_launch();
+        unsigned long long nl = 0;
+        KB_CUDA(cudaMemcpyAsync(&nl, hc.p, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        g.n_ovf_long = (int64_t)nl;
+    }
+    if (getenv("KB_TRACE") && g.n_ovf) {
+        DBuf<unsigned long long> lm;
+        lm.alloc(3);
+        KB_CUDA(cudaMemsetAsync(lm.p, 0, 24, st));
+        k_ovf_stats<<<blocks_for(g.n_ovf, 256), 256, 0, st>>>(g.ovf.p, g.n_ovf, g.perm.p,
+                                                            g.rlen.p, g.split, lm.p);
+        unsigned long long hl[3];
+        KB_CUDA(cudaMemcpyAsync(hl, lm.p, 24, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[kb]   overflow rows %lld: %llu arcs, longest %llu, %llu over the split\n",
+                (long long)g.n_ovf, hl[0], hl[1], hl[2]);
     }
     // the overflow pass is a warp per row: past a few percent of the rows a
     // rebuild of the layout is cheaper

@@ -85,6 +85,9 @@ void note_launch(int64_t k = 1);
 int64_t launch_count();
 
 // KB_TRACE=1: host-side phase times (syncing the stream at each mark)
+// overflow rows longer than this are summed by a block each (K1 tail)
+constexpr int OVF_LONG = 256;
+
 struct PhaseTrace {
     bool on;
     std::chrono::steady_clock::time_point t0;
@@ -243,6 +246,8 @@ struct Graph {
     DBuf<int32_t> ovf, ovf_flag;
     DBuf<unsigned long long> ovf_count;
     int64_t n_ovf = 0;
+    DBuf<int32_t> ovf_long;           // overflow rows longer than OVF_LONG arcs
+    int64_t n_ovf_long = 0;
     Sell sell;
     // heavy-row combine: segments of heavy row h are seg_list[seg_ptr[h] ..
     // seg_ptr[h+1]) in order (indices into the segment-sum buffer)

@@ -522,6 +522,7 @@ __global__ void k_ovf_rows(IterArgs A, const int32_t *rows, int64_t nr, const in
     const int32_t o = perm[v];
     const int32_t *row = indices + indptr[o];
     const int64_t L = rlen[o];
+    if (L > OVF_LONG) return;  // k_ovf_long
     const double *__restrict__ x = A.x;
     double s = 0.0;
     if (L <= split) {
@@ -551,6 +552,94 @@ __global__ void k_ovf_rows(IterArgs A, const int32_t *rows, int64_t nr, const in
         }
     }
     if (lane == 0) epilogue(A, v, s);
+}
+
+// Long overflow rows, a block each.  A row of at most split arcs is one
+// serial chain: warps 1.. gather the next 2048 values into shared memory
+// while thread 0 folds the current ones, so the chain never waits on a
+// gather.  A segmented row (> split arcs) folds up to 8 segments at once, a
+// warp each (lanes gather 256 values ahead while lane 0 folds), and thread
+// 0 combines the segment sums in order -- K1's order in both cases.
+constexpr int OVF_CHUNK = 2048;
+constexpr int OVF_WCHUNK = 256;
+
+__global__ void __launch_bounds__(256) k_ovf_long(IterArgs A, const int32_t *rows,
+                                                  const int32_t *perm, const int32_t *iperm,
+                                                  const int64_t *indptr, const int32_t *rlen,
+                                                  const int32_t *indices, int64_t split) {
+    if (aborted(A)) return;
+    __shared__ double buf[2][OVF_CHUNK];
+    __shared__ double segsum[8];
+    const int32_t v = rows[blockIdx.x];
+    const int32_t o = perm[v];
+    const int32_t *row = indices + indptr[o];
+    const int64_t L = rlen[o];
+    const double *__restrict__ x = A.x;
+    const int tid = threadIdx.x;
+    double s = 0.0;
+    if (L <= split) {
+        const int64_t nchunks = (L + OVF_CHUNK - 1) / OVF_CHUNK;
+        auto stage = [&](int64_t c, int nthreads, int t0) {
+            const int64_t a = c * OVF_CHUNK, b = min(L, a + OVF_CHUNK);
+            double *d = buf[c & 1];
+            for (int64_t j = a + (tid - t0); j < b; j += nthreads) d[j - a] = x[iperm[row[j]]];
+        };
+        stage(0, blockDim.x, 0);
+        __syncthreads();
+        for (int64_t c = 0; c < nchunks; c++) {
+            if (tid >= 32) {
+                if (c + 1 < nchunks) stage(c + 1, blockDim.x - 32, 32);
+            } else if (tid == 0) {
+                const int n = (int)(min(L, (c + 1) * OVF_CHUNK) - c * OVF_CHUNK);
+                const double *d = buf[c & 1];
+#pragma unroll 8
+                for (int j = 0; j < n; j++) s = __dadd_rn(s, d[j]);
+            }
+            __syncthreads();
+        }
+    } else {
+        const int warp = tid >> 5, lane = tid & 31;
+        double *wb = &buf[0][0] + warp * 2 * OVF_WCHUNK;   // 2 x 256 per warp
+        const int64_t nseg = (L + split - 1) / split;
+        for (int64_t g0 = 0; g0 < nseg; g0 += 8) {
+            const int64_t sg = g0 + warp;
+            if (sg < nseg) {
+                const int64_t a = sg * split, b = min(L, a + split);
+                const int64_t nch = (b - a + OVF_WCHUNK - 1) / OVF_WCHUNK;
+                double val[OVF_WCHUNK / 32];
+                auto gather = [&](int64_t c) {
+#pragma unroll
+                    for (int q = 0; q < OVF_WCHUNK / 32; q++) {
+                        const int64_t j = a + c * OVF_WCHUNK + q * 32 + lane;
+                        val[q] = j < b ? x[iperm[row[j]]] : 0.0;
+                    }
+                };
+                gather(0);
+                double ss = 0.0;
+                for (int64_t c = 0; c < nch; c++) {
+                    double *d = wb + (c & 1) * OVF_WCHUNK;
+#pragma unroll
+                    for (int q = 0; q < OVF_WCHUNK / 32; q++) d[q * 32 + lane] = val[q];
+                    __syncwarp();
+                    if (c + 1 < nch) gather(c + 1);   // in flight during the fold
+                    if (lane == 0) {
+                        const int n = (int)min((int64_t)OVF_WCHUNK, b - a - c * OVF_WCHUNK);
+#pragma unroll 8
+                        for (int j = 0; j < n; j++) ss = __dadd_rn(ss, d[j]);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) segsum[warp] = ss;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const int cnt = (int)min((int64_t)8, nseg - g0);
+                for (int q = 0; q < cnt; q++) s = __dadd_rn(s, segsum[q]);
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) epilogue(A, v, s);
 }
 
 // explicit empty rows (after updates): w = 0 and the bounds collapse to katz
@@ -780,6 +869,13 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         k_ovf_rows<<<(unsigned)((g.n_ovf * 32 + 255) / 256), 256, 0, st>>>(
             A, g.ovf.p, g.n_ovf, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p,
             g.split);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    if (g.n_ovf_long) {
+        k_ovf_long<<<(unsigned)g.n_ovf_long, 256, 0, st>>>(A, g.ovf_long.p, g.perm.p, g.iperm.p,
+                                                          g.indptr.p, g.rlen.p, g.indices.p,
+                                                          g.split);
         note_launch();
         KB_CUDA(cudaGetLastError());
     }

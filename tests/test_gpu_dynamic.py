@@ -417,3 +417,46 @@ def test_rmat_s16_updates_match_oracle_update_batch(nb):
     np.testing.assert_allclose(st.lower, ost.lower, rtol=REL, atol=0)
     np.testing.assert_allclose(st.upper, ost.upper, rtol=REL, atol=0)
     assert P.ranking_result(st).top(100) == O.ranking_result(ost).top(100)
+
+
+@pytest.mark.parametrize("split", [100, 2048])
+def test_long_overflow_rows_bitwise(split):
+    """Rows edited past their SELL lane are recomputed after K1 from the
+    canonical CSR; those longer than 256 arcs by a block each (k_ovf_long:
+    staged gathers, one serial chain, split-sized segments combined in
+    order, segment boundaries falling inside the 2048-value chunks when
+    split = 100).  Levels and bounds equal a fresh static layout's with the
+    same split bit for bit, after the update and after one more K1."""
+    from paper_1807_03847_b200 import generators as G
+    from paper_1807_03847_b200.engine import DeviceGraph
+    g = G.rmat_graph(65536, edge_factor=16, seed=42, split_threshold=split)
+    crit = P.Criterion.top_k(100, 1e-6)
+    st = P.init(g, crit, undirected=True)
+    P.run(st, g)
+    deg = g.out_degrees()
+    rng = np.random.default_rng(3)
+    long_rows = np.nonzero((deg > 300) & (deg + 40 < deg.max()))[0]
+    assert long_rows.size > 20
+    ins = set()
+    for u in long_rows[:60]:
+        k = 0
+        while k < 24:                      # enough to outgrow any lane
+            v = int(rng.integers(0, 65536))
+            if v != u and deg[v] + 30 < deg.max() and not g.has_arc(int(u), v):
+                ins.add((min(int(u), v), max(int(u), v)))
+                k += 1
+    e = np.array(sorted(ins), dtype=np.int64)
+    P.update_batch(st, g, P.EdgeBatch(insertions=np.concatenate([e, e[:, ::-1]])))
+    info = g.device_graph.info()
+    assert info.overflow_long > 0, (info.overflow_rows, info.overflow_long)
+    ip, ix = g.csr_arrays()
+    fg = G.DeviceResidentGraph(DeviceGraph(ip, ix, split_threshold=split))
+    fresh = fresh_to_depth(fg, st)
+    for mine, theirs in zip(st.levels, fresh.levels):
+        np.testing.assert_array_equal(mine, theirs)
+    np.testing.assert_array_equal(st.lower, fresh.lower)
+    np.testing.assert_array_equal(st.upper, fresh.upper)
+    P.iterate_once(st, g)
+    P.iterate_once(fresh, fg)
+    np.testing.assert_array_equal(st.levels[-1], fresh.levels[-1])
+    np.testing.assert_array_equal(st.lower, fresh.lower)
