@@ -101,7 +101,7 @@ __global__ void k_row_class(const int32_t *deg, int64_t n, int64_t split, unsign
     normal[v] = d > 0 && d <= split;
     zero[v] = d == 0 && v >= own_lo && v < own_hi;  // empty rows this device owns
     iota[v] = (int32_t)v;
-    key[v] = 0xFFFFFFFFu - (uint32_t)d;
+    key[v] = d <= split ? (uint32_t)(split - d) : 0u;  // normal rows: descending length
 }
 
 __global__ void k_gather_keys(const uint32_t *key, const int32_t *ids, int64_t m, uint32_t *out) {
@@ -157,11 +157,24 @@ __global__ void k_fill(const int64_t *indptr, const int32_t *indices, const int3
     }
     int w = slice_w[s];
     int32_t *base = cols + slice_off[s];
-    for (int j = 0; j < w; j++) {
-        int32_t c = (j < len) ? iperm[indices[src + j]] : 0;
-        int64_t pos = (w <= 4) ? ((int64_t)j * 32 + lane)
-                               : ((int64_t)(j >> 2) * 128 + lane * 4 + (j & 3));
-        base[pos] = c;
+    // eight columns per step with every load issued before the first use:
+    // the column ids, then their relabelled ids (a random gather), then the
+    // stores -- a step costs two memory latencies instead of sixteen
+    for (int j0 = 0; j0 < w; j0 += 8) {
+        int32_t r[8], c[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) r[q] = (j0 + q < len) ? indices[src + j0 + q] : -1;
+#pragma unroll
+        for (int q = 0; q < 8; q++) c[q] = r[q] >= 0 ? iperm[r[q]] : 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int j = j0 + q;
+            if (j < w) {
+                const int64_t pos = (w <= 4) ? ((int64_t)j * 32 + lane)
+                                             : ((int64_t)(j >> 2) * 128 + lane * 4 + (j & 3));
+                base[pos] = c[q];
+            }
+        }
     }
 }
 
@@ -428,9 +441,11 @@ void build_sell(Graph &g, bool fresh, bool fill) {
         if (nnorm) {
             k_gather_keys<<<blocks_for(nnorm, 256), 256, 0, st>>>(key.p, sel.p, nnorm, k2.p);
             note_launch();
+            int kbits = 1;
+            while (kbits < 32 && ((int64_t)1 << kbits) <= g.split) kbits++;
             cub_run([&](void *t, size_t &b) {
                 return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k3.p, sel.p, g.vrow.p,
-                                                       (int)nnorm, 0, 32, st);
+                                                       (int)nnorm, 0, kbits, st);
             });
         }
     }

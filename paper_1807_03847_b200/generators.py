@@ -56,7 +56,7 @@ class DeviceResidentGraph:
 
     def _arcs(self, arcs) -> np.ndarray:
         a = np.ascontiguousarray(np.asarray(arcs, dtype=np.int64).reshape(-1, 2))
-        if a.size:
+        if a.size and (a.min() < 0 or a.max() >= self.node_count):
             bad = (a < 0) | (a >= self.node_count)
             if bad.any():
                 self._check_node(int(a[bad][0]))

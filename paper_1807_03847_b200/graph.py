@@ -44,6 +44,14 @@ def check_batch_arcs(batch: "EdgeBatch", n: int, check_node, present) -> None:
                                (arrays[1], batch.deletions, True, "not present")):
         if not a.shape[0]:
             continue
+        if a.min() >= 0 and a.max() < n:        # the common case: no range fault
+            fault = present(np.ascontiguousarray(a)) != want
+            if fault.any():
+                i = int(np.argmax(fault))
+                u, v = arcs[i]
+                verb = "insert" if not want else "delete"
+                raise BatchPreconditionError(f"cannot {verb} arc ({u}, {v}): {msg}")
+            continue
         bad = ((a < 0) | (a >= n)).any(axis=1)
         fault = bad.copy()
         ok = ~bad
@@ -102,7 +110,7 @@ def _arcs_in(x):
             a = a.reshape(0, 2)
         if a.ndim != 2 or a.shape[1] != 2:
             raise ValueError("arc arrays must have shape (m, 2)")
-        if not np.array_equal(a, x):
+        if x.dtype != np.int64 and not np.array_equal(a, x):
             raise ValueError("arc ids must be integers")
         return ArcArray(a)
     return [(int(u), int(v)) for u, v in x]
@@ -123,25 +131,23 @@ class EdgeBatch:
         self.deletions = _arcs_in(self.deletions)
 
     def arrays(self) -> tuple[np.ndarray, np.ndarray]:
-        """(insertions, deletions) as (m, 2) int64 arrays, cached per list
-        object and length (the lists are the batch's public state)."""
-        if isinstance(self.insertions, ArcArray) and isinstance(self.deletions, ArcArray):
-            return self.insertions.a, self.deletions.a
-        if isinstance(self.insertions, ArcArray) or isinstance(self.deletions, ArcArray):
-            i, d = (x.a if isinstance(x, ArcArray) else
-                    np.array(x, dtype=np.int64).reshape(-1, 2)
-                    for x in (self.insertions, self.deletions))
-            return i, d
-        key = (id(self.insertions), len(self.insertions), id(self.deletions),
-               len(self.deletions))
-        cached = self.__dict__.get("_arr")
-        if cached is None or cached[0] != key:
-            i, d = (np.fromiter(itertools.chain.from_iterable(x), dtype=np.int64,
-                                count=2 * len(x)).reshape(-1, 2)
-                    for x in (self.insertions, self.deletions))
-            cached = (key, i, d)
-            self.__dict__["_arr"] = cached
-        return cached[1], cached[2]
+        """(insertions, deletions) as (m, 2) int64 arrays: an array side as
+        is, a list side converted once per list object and length (the lists
+        are the batch's public state)."""
+        return self._side_array(self.insertions, "_arr_i"), \
+            self._side_array(self.deletions, "_arr_d")
+
+    def _side_array(self, x, slot: str) -> np.ndarray:
+        if isinstance(x, ArcArray):
+            return x.a
+        key = (id(x), len(x))
+        cached = self.__dict__.get(slot)
+        if cached is None or cached[0] != key or cached[1] is not x:
+            a = np.fromiter(itertools.chain.from_iterable(x), dtype=np.int64,
+                            count=2 * len(x)).reshape(-1, 2)
+            cached = (key, x, a)
+            self.__dict__[slot] = cached
+        return cached[2]
 
     def _keys(self):
         """u << 32 | v keys when every id fits 31 bits, else None."""
@@ -154,13 +160,30 @@ class EdgeBatch:
                 return None
         return (i[:, 0] << 32) | i[:, 1], (d[:, 0] << 32) | d[:, 1]
 
+    def _sorted_keys(self):
+        """(sorted insertion keys, sorted deletion keys), or None when an id
+        does not fit 31 bits; cached while the batch's arrays are the same
+        objects (validate_shape and is_symmetric share one sort)."""
+        try:
+            i, d = self.arrays()
+        except OverflowError:
+            return None
+        c = self.__dict__.get("_skeys")
+        if c is not None and c[0] is i and c[1] is d:
+            return c[2]
+        k = self._keys()
+        out = None if k is None else (np.sort(k[0]), np.sort(k[1]))
+        self.__dict__["_skeys"] = (i, d, out)
+        return out
+
     def validate_shape(self) -> None:
         """Duplicates and overlap (graph.py:46-59)."""
-        k = self._keys()
-        if k is not None:           # vectorised test; messages from the exact path
-            ki, kd = np.sort(k[0]), np.sort(k[1])
+        sk = self._sorted_keys()
+        if sk is not None:          # vectorised test; messages from the exact path
+            ki, kd = sk
             if not ((ki[1:] == ki[:-1]).any() or (kd[1:] == kd[:-1]).any() or
-                    np.intersect1d(ki, kd, assume_unique=True).size):
+                    (ki.size and kd.size and
+                     np.intersect1d(ki, kd, assume_unique=True).size)):
                 return
         ins, dels = set(self.insertions), set(self.deletions)
         if len(ins) != len(self.insertions):
@@ -176,12 +199,12 @@ class EdgeBatch:
 
     def is_symmetric(self) -> bool:
         """Both lists closed under reversal (graph.py:61-65)."""
-        k = self._keys()
-        if k is not None:
+        sk = self._sorted_keys()
+        if sk is not None:
             # reversal is a bijection, so "closed under it" = equal key sets
-            return all(np.array_equal(sorted_unique(a),
+            return all(np.array_equal(_unique_of_sorted(a),
                                       sorted_unique(((a & 0xFFFFFFFF) << 32) | (a >> 32)))
-                       for a in k)
+                       for a in sk)
         ins, dels = set(self.insertions), set(self.deletions)
         return all((v, u) in ins for u, v in ins) and \
             all((v, u) in dels for u, v in dels)
@@ -202,7 +225,10 @@ def _first_duplicate(arcs: Sequence[Arc]) -> Arc:
 def sorted_unique(a: np.ndarray) -> np.ndarray:
     """np.unique for int64 keys as sort + run mask (same result, much faster
     than numpy 2.3's np.unique on large arrays)."""
-    a = np.sort(np.asarray(a, dtype=np.int64))
+    return _unique_of_sorted(np.sort(np.asarray(a, dtype=np.int64)))
+
+
+def _unique_of_sorted(a: np.ndarray) -> np.ndarray:
     if a.size > 1:
         keep = np.empty(a.size, dtype=bool)
         keep[0] = True
