@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 1200 python bench.py --workload c5 > gpurun_out/g50_c5.log 2>&1; echo "c5 $?"
+bash tools/round_check.sh
+bash tools/checked_suite.sh
