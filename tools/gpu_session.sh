@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-bash tools/round_check.sh
-bash tools/checked_suite.sh
+timeout 900 python tools/k3_runs.py > gpurun_out/g51_k3runs.log 2>&1; echo "k3 $?"
