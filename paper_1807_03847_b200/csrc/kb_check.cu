@@ -79,6 +79,7 @@ struct TopkArgs {
     // selection, only the split; winners to win_out and survivors to
     // surv_out when set (else prefix_buf and act_out + k)
     int cut_given = 0;
+    int early_cut = (int)tune_get("k2.early_cut", 1);  // compact after one digit when small
     int32_t *win_out = nullptr, *surv_out = nullptr;
 };
 
@@ -247,8 +248,12 @@ __global__ void __launch_bounds__(CHK_THREADS, 2) k_topk_select(TopkArgs A) {
         select_digit(sh, gh, 4096, kk, sel, true);
         prefix |= (uint64_t)sel << shift;
         mask |= (uint64_t)0xFFF << shift;
+        // the cut's bin after the first digit is already small (the usual
+        // case: it is the top exponent band): compact it now, skipping the
+        // second pass over the whole set (same decision in every block)
+        if (p == 0 && gh[sel] <= (unsigned)CSORT && A.early_cut) break;
     }
-    // ---- 1b. compact the positions carrying the 24-bit prefix
+    // ---- 1b. compact the positions carrying the 12- or 24-bit prefix
     for (int64_t t = i0; t < i1; t += TILE) {
         uint64_t key[UNR];
 #pragma unroll

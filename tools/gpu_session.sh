@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-for pf in 2 24 34 44; do
-  KB_TUNE="k1.narrow_pf=$pf" timeout 600 python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/g55_c4_pf$pf.log 2>&1; echo "c4 pf=$pf $?"
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q > gpurun_out/g56_tests.log 2>&1; echo "tests $?"
+for ec in 0 1; do
+  KB_TUNE="k2.early_cut=$ec" timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/g56_c2_ec$ec.log 2>&1; echo "c2 ec=$ec $?"
 done
-KB_TUNE="k1.narrow_pf=24" timeout 900 python -m pytest tests/test_gpu_fullsize.py -x -q -k C4 > gpurun_out/g55_c4_test.log 2>&1; echo "c4 test $?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_topk --csv --log-file gpurun_out/g56_k2.csv python tools/k2_one.py > gpurun_out/g56_ncu.log 2>&1; echo "ncu $?"
