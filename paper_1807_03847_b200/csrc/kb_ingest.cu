@@ -280,6 +280,14 @@ __global__ void k_ovf_long_list(const int32_t *ovf, int64_t n_ovf, const int32_t
     if (i < n_ovf && rlen[perm[ovf[i]]] > OVF_LONG) out[atomicAdd(count, 1ull)] = ovf[i];
 }
 
+__global__ void k_count_above(const int32_t *deg, int64_t m, int64_t thr,
+                              unsigned long long *count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool above = i < m && deg[i] > thr;
+    const unsigned b = __ballot_sync(0xffffffffu, above);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
+}
+
 // trace only: total and longest length of the overflow rows, rows > split
 __global__ void k_ovf_stats(const int32_t *ovf, int64_t n_ovf, const int32_t *perm,
                             const int32_t *rlen, int64_t split, unsigned long long *out) {
@@ -406,7 +414,22 @@ void build_sell(Graph &g, bool fresh, bool fill) {
         g.nv = hc[0];
         g.nh = hc[1];
         g.nzero = n - g.nv;
+        // heavy rows are [0, nh) by descending length: the leading ones with
+        // more than 8 segments get a warp each in the segment fold
+        {
+            DBuf<unsigned long long> c;
+            c.alloc(1);
+            KB_CUDA(cudaMemsetAsync(c.p, 0, 8, st));
+            if (g.nh)
+                k_count_above<<<blocks_for(g.nh, 256), 256, 0, st>>>(g.deg.p, g.nh, 8 * g.split,
+                                                                   c.p);
+            unsigned long long hl = 0;
+            KB_CUDA(cudaMemcpyAsync(&hl, c.p, 8, cudaMemcpyDeviceToHost, st));
+            KB_CUDA(cudaStreamSynchronize(st));
+            g.nh_long = (int64_t)hl;
+        }
     } else {
+        g.nh_long = -1;
         DBuf<unsigned char> fh, fn, fz;
         DBuf<int32_t> iota, sel;
         DBuf<uint32_t> key, k2, k3;

@@ -208,6 +208,7 @@ struct Graph {
     int device = 0;
     int sm_count = 0;
     int64_t n = 0, nnz = 0, nv = 0, nh = 0, nzero = 0, max_deg = 0;
+    int64_t nh_long = -1;  // leading heavy rows with > 8 segments (fresh layouts), else -1
     int64_t split = 0, hot = 0;
     // sharded graphs (KB_GRAPH_NO_RELABEL with an owned block of 2^k ids):
     // K1's shared-memory hot set takes the first hot_per ids of each block

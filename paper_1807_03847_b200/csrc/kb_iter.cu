@@ -498,6 +498,47 @@ __global__ void k_heavy_combine(IterArgs A, const int32_t *seg_ptr,
     epilogue(A, A.hrow ? A.hrow[h] : h, s);
 }
 
+// The same fold, a warp per heavy row: the lanes load 32 segment sums at a
+// time (independent loads in flight) and lane 0 adds them in segment order.
+// A thread per row left the hub rows' ~200 dependent load pairs as the tail
+// of every level (26 us at C2).
+// Rows [0, nwarp) take a warp each (the long ones: fresh layouts order heavy
+// rows by descending length), the rest a thread each.
+__global__ void k_heavy_combine_w(IterArgs A, const int32_t *seg_ptr, const int32_t *seg_list,
+                                  int64_t nwarp) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (aborted(A)) return;
+    if (t >= nwarp * 32) {
+        const int64_t h = nwarp + (t - nwarp * 32);
+        if (h >= A.nh) return;
+        double s = 0.0;
+        for (int q = seg_ptr[h]; q < seg_ptr[h + 1]; q++) {
+            KB_DCHECK(seg_list[q] >= 0 && seg_list[q] < A.nseg);
+            s = __dadd_rn(s, A.seg_sum[seg_list[q]]);
+        }
+        epilogue(A, A.hrow ? A.hrow[h] : h, s);
+        return;
+    }
+    const int64_t h = t >> 5;
+    const int lane = threadIdx.x & 31;
+    const int q0 = seg_ptr[h], q1 = seg_ptr[h + 1];
+    double s = 0.0;
+    for (int b = q0; b < q1; b += 32) {
+        const int q = b + lane;
+        double v = 0.0;
+        if (q < q1) {
+            KB_DCHECK(seg_list[q] >= 0 && seg_list[q] < A.nseg);
+            v = A.seg_sum[seg_list[q]];
+        }
+        const int cnt = min(32, q1 - b);
+        for (int j = 0; j < cnt; j++) {
+            const double t = __shfl_sync(0xffffffffu, v, j);
+            if (lane == 0) s = __dadd_rn(s, t);
+        }
+    }
+    if (lane == 0) epilogue(A, A.hrow ? A.hrow[h] : h, s);
+}
+
 // rows without out-arcs: w = 0, katz unchanged (0), bounds collapse to katz
 __global__ void k_empty_rows(double *upper, double *lower, const double *katz,
                              int64_t nv, int64_t n) {
@@ -849,8 +890,16 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         KB_CUDA(cudaGetLastError());
     }
     if (A.nslices && g.nh) {
-        k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
-            A, g.seg_ptr.p, g.seg_list.p); note_launch();
+        if (tune_get("k1.combine_warp", 1)) {
+            const int64_t nwarp = g.nh_long >= 0 && !A.hrow ? g.nh_long : g.nh;
+            const int64_t threads = nwarp * 32 + (g.nh - nwarp);
+            k_heavy_combine_w<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+                A, g.seg_ptr.p, g.seg_list.p, nwarp);
+        }
+        else
+            k_heavy_combine<<<(unsigned)((g.nh + 127) / 128), 128, 0, st>>>(
+                A, g.seg_ptr.p, g.seg_list.p);
+        note_launch();
         KB_CUDA(cudaGetLastError());
     }
     if (!g.implicit_rows && g.nzero) {
