@@ -92,10 +92,13 @@ __device__ __forceinline__ bool flag_set(const unsigned long long *f) {
 // queued behind (they exit when it is set), that K1's work counter reset,
 // the new |active| as the next check's input, and the result words written
 // straight into page-locked host memory (no separate copy).
+// (The host reads the published words only after an event synchronisation
+// on the stream: no system-scope fence is needed.)
 struct Publish {
     unsigned long long *abort, *k1_counter;
     volatile unsigned long long *host;
     int64_t level;
+    int fence = 0;   // kb_tune chk.sys_fence: the old fenced publish
 };
 
 __device__ __forceinline__ void publish(const Publish &p, unsigned long long *out) {
@@ -103,11 +106,11 @@ __device__ __forceinline__ void publish(const Publish &p, unsigned long long *ou
     *p.abort = out[1];
     if (p.k1_counter) *p.k1_counter = 0ull;
     out[7] = out[0];
-    p.host[0] = out[0];
+    p.host[0] = out[0];   // pub_words(): the device mirror or h_flags
     p.host[1] = out[1];
     p.host[2] = out[2];
     p.host[3] = (unsigned long long)p.level;
-    __threadfence_system();
+    if (p.fence) __threadfence_system();
 }
 
 // digit plan: two 12-bit digits over all elements, then the survivors of the
@@ -907,6 +910,23 @@ int coop_grid(int sm_count) {
     return sm_count * per_sm;
 }
 
+// Where device-driven checks publish their verdict words: a device mirror
+// copied to the page-locked h_flags once per batch (publish_copy) -- a
+// kernel that writes page-locked memory itself ends only after those PCIe
+// writes land (~3 us per check) -- or, with kb_tune chk.pub_host, h_flags
+// directly.
+unsigned long long *pub_words(State &s) {
+    if (tune_get("chk.pub_host", 0)) return s.h_flags;
+    if (!s.pub_dev.p) s.pub_dev.alloc(4);
+    return s.pub_dev.p;
+}
+
+void publish_copy(State &s, cudaStream_t st) {
+    if (tune_get("chk.pub_host", 0) || !s.pub_dev.p) return;
+    KB_CUDA(cudaMemcpyAsync(s.h_flags, s.pub_dev.p, 4 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+}
+
 void sync_read(State &s, cudaStream_t st, const unsigned long long *dev, int count) {
     KB_CUDA(cudaMemcpyAsync(s.h_flags, dev, count * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, st));
@@ -973,7 +993,8 @@ __global__ void k_pair_refutes_pub(const double *katz, const double *w, double a
                                    int undirected, const int32_t *perm, int32_t q, int32_t x,
                                    double eps, unsigned long long *out,
                                    unsigned long long *abort, volatile unsigned long long *host,
-                                   unsigned long long *k1_counter, int64_t level = -1) {
+                                   unsigned long long *k1_counter, int64_t level = -1,
+                                   int fence = 0) {
     // in a device-driven chain, a test behind a failed one does nothing
     if (level >= 0 && *(volatile unsigned long long *)abort) return;
     // the two nodes' bounds from katz and the level, as the K1 epilogue forms them
@@ -986,9 +1007,9 @@ __global__ void k_pair_refutes_pub(const double *katz, const double *w, double a
     out[0] = ref ? 1ull : 0ull;
     abort[0] = ref ? 0ull : 1ull;
     k1_counter[0] = 0ull;      // the queued K1's work counter (no separate memset)
-    host[0] = ref ? 1ull : 0ull;  // straight into page-locked host memory
+    host[0] = ref ? 1ull : 0ull;  // pub_words(): the device mirror or h_flags
     if (level >= 0) host[3] = (unsigned long long)level;
-    __threadfence_system();
+    if (fence) __threadfence_system();   // see Publish
 }
 
 // candidates: the NCAND block winners with the widest excess (ties: the
@@ -1340,8 +1361,9 @@ bool ranking_pair_chain(State &s, cudaStream_t st) {
     for (int64_t j = 0; j < batch; j++) {
         k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma,
                                             s.undirected, g.labels(), s.rk_q, s.rk_x, s.eps,
-                                            s.scratch_u64.p, s.abort_flag.p, s.h_flags,
-                                            s.work_counter.p, s.r);
+                                            s.scratch_u64.p, s.abort_flag.p, pub_words(s),
+                                            s.work_counter.p, s.r,
+                                            (int)tune_get("chk.sys_fence", 0));
         note_launch();
         s.counter_zeroed = true;
         if (j + 1 == batch || s.r >= s.max_iter) break;
@@ -1350,6 +1372,7 @@ bool ranking_pair_chain(State &s, cudaStream_t st) {
         s.spec_abort = false;
     }
     KB_CUDA(cudaGetLastError());
+    publish_copy(s, st);
     KB_CUDA(cudaEventRecord(s.chk_ev, st));
     KB_CUDA(cudaEventSynchronize(s.chk_ev));
     const int64_t last = (int64_t)s.h_flags[3];
@@ -1438,7 +1461,8 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
         attr_done[g.device] = true;
         attr_smem[g.device] = smem;
     }
-    const Publish pub{s.abort_flag.p, s.work_counter.p, s.h_flags, level};
+    const Publish pub{s.abort_flag.p, s.work_counter.p, pub_words(s), level,
+                      (int)tune_get("chk.sys_fence", 0)};
     auto small = [&](int64_t mh, const unsigned long long *md) {
         int Ps = 1;
         while (Ps < (mh >= 0 ? mh : SMALL_M)) Ps <<= 1;
@@ -1492,6 +1516,7 @@ int topk_check_enqueue(State &s, cudaStream_t st) {
     // a stand-alone check acts whatever an earlier run left in the flag
     KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
     const int nxt = topk_check_enqueue_dev(s, st, s.m_host, s.act_dense, s.cur, s.r);
+    publish_copy(s, st);
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
     KB_CUDA(cudaEventRecord(s.chk_ev, st));
     return nxt;
@@ -1526,6 +1551,7 @@ bool topk_run_device(State &s, cudaStream_t st) {
             cur = topk_check_enqueue_dev(s, st, j == 0 ? s.m_host : -1, j == 0 && s.act_dense,
                                          cur, s.r);
         }
+        publish_copy(s, st);
         KB_CUDA(cudaEventRecord(s.chk_ev, st));
         KB_CUDA(cudaEventSynchronize(s.chk_ev));
         const bool conv = s.h_flags[1] != 0;

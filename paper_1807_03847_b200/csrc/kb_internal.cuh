@@ -311,6 +311,7 @@ struct State {
     DBuf<unsigned char> cub_tmp;
     DBuf<unsigned long long> work_counter;
     unsigned long long *h_flags = nullptr;  // pinned host mirror
+    DBuf<unsigned long long> pub_dev;       // check verdict words, copied to h_flags per batch
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_check_ms = 0;
     // K1 launch timing: event pairs recorded around each SpMV+bounds step
