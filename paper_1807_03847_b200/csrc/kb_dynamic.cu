@@ -173,7 +173,7 @@ void slack_layout(Graph &g, const int32_t *extra, DBuf<int64_t> &nip, DBuf<int32
     total = 0;
     KB_CUDA(cudaMemcpyAsync(&total, nip.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
-    const int64_t room = std::max<int64_t>(total / 16, (int64_t)1 << 20);
+    const int64_t room = std::max<int64_t>(total / 16, tune_get("dyn.tail_room", 1 << 20));
     nix.alloc(total + room);
     g.rcap.alloc(std::max<int64_t>(1, n));
     k_cap32<<<nblk(n, 256), 256, 0, st>>>(cap.p, n, g.rcap.p);

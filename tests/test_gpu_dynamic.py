@@ -460,3 +460,61 @@ def test_long_overflow_rows_bitwise(split):
     P.iterate_once(fresh, fg)
     np.testing.assert_array_equal(st.levels[-1], fresh.levels[-1])
     np.testing.assert_array_equal(st.lower, fresh.lower)
+
+
+def test_mixed_batches_relocate_and_respread(capfd, monkeypatch):
+    """The device-side batch path end to end: edits grouped by row on the
+    device, rows that outgrow their slack relocated to the tail, then (tail
+    room made small with kb_tune dyn.tail_room) the tail exhausted and the
+    layout re-spread, with deletions of earlier insertions mixed in.  After
+    every batch the device arcs are exactly the expected set and the levels
+    and bounds equal a fresh static layout's bit for bit."""
+    from paper_1807_03847_b200 import _lib
+    from paper_1807_03847_b200 import generators as G
+    L = _lib.lib()
+    _lib.check(L.kb_tune(b"dyn.tail_room", 0))
+    try:
+        n = 4096
+        g = G.rmat_graph(n, edge_factor=8, seed=3)
+        crit = P.Criterion.top_k(20, 1e-6)
+        st = P.init(g, crit, undirected=True, alpha=1e-5, max_iterations=400)
+        P.run(st, g)
+        ip, ix = g.csr_arrays()
+        present = set(zip(np.repeat(np.arange(n), np.diff(ip)).tolist(), ix.tolist()))
+        rng = np.random.default_rng(5)
+        inserted = []
+        monkeypatch.setenv("KB_TRACE", "1")
+        for _ in range(6):
+            hubs = rng.choice(n, 24, replace=False)       # rows that grow fast
+            ins = set()
+            while len(ins) < 1500:
+                u = int(hubs[rng.integers(0, 24)]) if rng.random() < 0.6 else int(rng.integers(0, n))
+                v = int(rng.integers(0, n))
+                a = (min(u, v), max(u, v))
+                if u == v or a in ins or a in present:
+                    continue
+                ins.add(a)
+            dels, inserted = inserted[:500], inserted[500:]
+            ia = np.array(sorted(ins), dtype=np.int64)
+            da = np.array(dels, dtype=np.int64).reshape(-1, 2)
+            P.update_batch(st, g, P.EdgeBatch(insertions=np.concatenate([ia, ia[:, ::-1]]),
+                                              deletions=np.concatenate([da, da[:, ::-1]])))
+            for u, v in dels:
+                present.discard((u, v))
+                present.discard((v, u))
+            for u, v in ins:
+                present.add((u, v))
+                present.add((v, u))
+            inserted += sorted(ins)
+            ip, ix = g.csr_arrays()
+            got = set(zip(np.repeat(np.arange(n), np.diff(ip)).tolist(), ix.tolist()))
+            assert got == present
+            fresh = fresh_to_depth(P.Graph.from_csr(n, ip, ix), st)
+            for mine, theirs in zip(st.levels, fresh.levels):
+                np.testing.assert_array_equal(mine, theirs)
+            np.testing.assert_array_equal(st.lower, fresh.lower)
+            np.testing.assert_array_equal(st.upper, fresh.upper)
+        err = capfd.readouterr().err
+        assert "relocate rows" in err and "respread" in err, err[-2000:]
+    finally:
+        _lib.check(L.kb_tune(b"dyn.tail_room", 1 << 20))
