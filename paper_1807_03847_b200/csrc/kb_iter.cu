@@ -473,6 +473,161 @@ __global__ void __launch_bounds__(1024, 1) k_sell_narrow_pf(IterArgs A) {
     if (A.npeer) __threadfence_system();
 }
 
+// All-narrow graphs with the streams moved by TMA: one producer thread per
+// CTA bulk-copies chunks of NB_CH consecutive slices -- their column slots,
+// row lengths and katz rows, all contiguous -- into a ring of NB_ST
+// shared-memory stages (mbarrier complete_tx), and 31 consumer warps take
+// two slices of a landed chunk each: column ids come from shared memory, so
+// a slice's only global round trip is its omega gather, and the streams stay
+// in flight however long the gathers take.  Chunks go round-robin over the
+// CTAs; the slices past the last whole chunk are read directly.  Needs
+// implicit rows and no segments (nh = 0), which every all-narrow layout has.
+constexpr int NB_CH = 62;          // slices per chunk (two per consumer warp)
+constexpr int NB_ST = 3;           // stages
+constexpr int NB_COLS_B = NB_CH * 32 * 4 * 4;   // up to width 4
+constexpr int NB_VLEN_B = NB_CH * 32 * 4;
+constexpr int NB_KATZ_B = NB_CH * 32 * 8;
+constexpr int NB_STAGE_B = NB_COLS_B + NB_VLEN_B + NB_KATZ_B;
+constexpr size_t NB_SMEM = (size_t)NB_ST * NB_STAGE_B;
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     "  selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes,
+                                         unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1], %2, [%3];" ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+// one slice of a narrow layout, its column ids and lengths given
+__device__ __forceinline__ double narrow_slice_sum(const double *__restrict__ x, const int32_t c[4],
+                                                   int len) {
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) v[j] = (j < len) ? __ldg(x + c[j]) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) sum = __dadd_rn(sum, v[j]);
+    return sum;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_sell_narrow_tma(IterArgs A, int64_t nfull) {
+    if (aborted(A)) return;
+    extern __shared__ int4 nb_smem4[];                   // 16-byte aligned (bulk copies)
+    unsigned char *nb_smem = (unsigned char *)nb_smem4;
+    __shared__ __align__(8) unsigned long long full[NB_ST], empty[NB_ST];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncw = (int)(blockDim.x >> 5) - 1;          // consumer warps
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(nb_smem);
+    const unsigned fbar = (unsigned)__cvta_generic_to_shared(full);
+    const unsigned ebar = (unsigned)__cvta_generic_to_shared(empty);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NB_ST; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fbar + 8 * i));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ebar + 8 * i), "r"(ncw));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t G = gridDim.x;
+    const int64_t nmine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / G + 1 : 0;
+    const double *__restrict__ x = A.x;
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int64_t k = 0; k < nmine; k++) {
+                const int st = (int)(k % NB_ST);
+                const unsigned r = (unsigned)(k / NB_ST);
+                const int64_t s0 = (blockIdx.x + k * G) * NB_CH;
+                const int64_t off0 = A.slice_off[s0], off1 = A.slice_off[s0 + NB_CH];
+                const unsigned colsB = (unsigned)((off1 - off0) * 4);
+                const unsigned katzB = A.level_only ? 0u : (unsigned)NB_KATZ_B;
+                mbar_wait(ebar + 8 * st, (r & 1) ^ 1);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(fbar + 8 * st), "r"(colsB + NB_VLEN_B + katzB) : "memory");
+                const unsigned d = sbase + (unsigned)st * NB_STAGE_B;
+                if (colsB) bulk_g2s(d, A.cols + off0, colsB, fbar + 8 * st);
+                bulk_g2s(d + NB_COLS_B, A.vlen + s0 * 32, NB_VLEN_B, fbar + 8 * st);
+                if (katzB) bulk_g2s(d + NB_COLS_B + NB_VLEN_B, A.katz + s0 * 32, katzB,
+                                    fbar + 8 * st);
+            }
+        }
+    } else {
+        const int cw = warp - 1;
+        for (int64_t k = 0; k < nmine; k++) {
+            const int st = (int)(k % NB_ST);
+            const unsigned r = (unsigned)(k / NB_ST);
+            const int64_t s0 = (blockIdx.x + k * G) * NB_CH;
+            // this warp's two slices and their column offsets in the chunk
+            // (exclusive prefix of 32 * width over the chunk's slices)
+            const int qa = cw, qb = cw + ncw;
+            const int wa_l = lane < NB_CH ? A.slice_w[s0 + lane] : 0;
+            const int wb_l = lane + 32 < NB_CH ? A.slice_w[s0 + lane + 32] : 0;
+            int pa = wa_l, pb = wb_l;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int ta = __shfl_up_sync(0xffffffffu, pa, o);
+                const int tb = __shfl_up_sync(0xffffffffu, pb, o);
+                if (lane >= o) { pa += ta; pb += tb; }
+            }
+            const int tota = __shfl_sync(0xffffffffu, pa, 31);
+            pb += tota;                                   // inclusive over 0..lane+32
+            const int ea = (pa - wa_l) * 32, eb = (pb - wb_l) * 32;   // exclusive, in ints
+            const int w_a = __shfl_sync(0xffffffffu, qa < 32 ? wa_l : wb_l, qa & 31);
+            const int o_a = __shfl_sync(0xffffffffu, qa < 32 ? ea : eb, qa & 31);
+            const int w_b = __shfl_sync(0xffffffffu, qb < 32 ? wa_l : wb_l, qb & 31);
+            const int o_b = __shfl_sync(0xffffffffu, qb < 32 ? ea : eb, qb & 31);
+            mbar_wait(fbar + 8 * st, r & 1);
+            const unsigned char *stg = nb_smem + (size_t)st * NB_STAGE_B;
+            const int32_t *cs = (const int32_t *)stg;
+            const int32_t *vs = (const int32_t *)(stg + NB_COLS_B);
+            const double *ks = (const double *)(stg + NB_COLS_B + NB_VLEN_B);
+            const bool hb = qb < NB_CH;
+            int32_t ca[4], cb[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                ca[j] = j < w_a ? cs[o_a + j * 32 + lane] : 0;
+                cb[j] = (hb && j < w_b) ? cs[o_b + j * 32 + lane] : 0;
+            }
+            const int la = vs[qa * 32 + lane];
+            const int lb = hb ? vs[qb * 32 + lane] : 0;
+            const double ka = A.level_only ? 0.0 : ks[qa * 32 + lane];
+            const double kb2 = (hb && !A.level_only) ? ks[qb * 32 + lane] : 0.0;
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ebar + 8 * st)
+                             : "memory");
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                KB_DCHECK(j >= la || (ca[j] >= 0 && ca[j] < A.ncols));
+                KB_DCHECK(j >= lb || (cb[j] >= 0 && cb[j] < A.ncols));
+            }
+            const double sa = narrow_slice_sum(x, ca, la);
+            const double sb = narrow_slice_sum(x, cb, lb);
+            epilogue_k(A, (s0 + qa) * 32 + lane, sa, ka);
+            if (hb) epilogue_k(A, (s0 + qb) * 32 + lane, sb, kb2);
+        }
+        // the slices past the last whole chunk: direct loads
+        const int64_t gw = (int64_t)blockIdx.x * ncw + cw, nwarps = G * ncw;
+        const uint64_t pol = evict_first_policy();
+        for (int64_t s = nfull * NB_CH + gw; s < A.nslices; s += nwarps) {
+            const int64_t vq = s * 32 + lane;
+            const int w = A.slice_w[s];
+            const int32_t *base = A.cols + A.slice_off[s];
+            int32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) c[j] = j < w ? ld_stream_i1(base + j * 32 + lane, pol) : 0;
+            const int len = vq < A.nvr ? A.vlen[vq] : 0;
+            const double sum = narrow_slice_sum(x, c, len);
+            if (vq < A.nvr) epilogue_k(A, vq, sum, A.level_only ? 0.0 : A.katz[vq]);
+        }
+    }
+    if (A.npeer) __threadfence_system();
+}
+
 // First iteration: x = levels[0] = ones, so every sequential row (or segment)
 // sum is exactly its length -- the same bits K1 would produce -- and no
 // gather is needed: w_1 = alpha * deg.
@@ -836,14 +991,24 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         note_launch();
         KB_CUDA(cudaGetLastError());
     } else if (A.nslices && g.sell.nwide == 0 && A.nseg == 0 &&
-               (!A.lazy_bounds || tune_get("k1.narrow_lazy", 0) || tune_get("k1.narrow_pf", 2)) &&
+               (!A.lazy_bounds || tune_get("k1.narrow_lazy", 0) || tune_get("k1.narrow_pf", 9)) &&
                tune_get("k1.narrow_kernel", 1)) {
-        // C4 (4096^2 grid) per launch: pipelined narrow kernel 0.1825 ms with
-        // lazy bounds / 0.223 ms with the bound stores; the unpipelined one
-        // 0.1954 / 0.250; the persistent kernel 0.1929 / 0.37
-        const int pf = (int)tune_get("k1.narrow_pf", 2);
-        if (pf == 1) k_sell_narrow_pf<1><<<g.sm_count, 1024, 0, st>>>(A);
-        else if (pf == 2) k_sell_narrow_pf<2><<<g.sm_count, 1024, 0, st>>>(A);
+        // C4 (4096^2 grid) per launch with lazy bounds: TMA-staged narrow
+        // kernel 0.149 ms; register-pipelined 0.1825 (0.223 with the bound
+        // stores); unpipelined 0.1954 (0.250); the persistent kernel 0.1929
+        const int pf = (int)tune_get("k1.narrow_pf", 9);
+        if (pf == 9 && A.nh == 0 && !A.vrow && A.nseg == 0) {
+            static bool attr[64] = {};
+            if (!attr[g.device]) {
+                KB_CUDA(cudaFuncSetAttribute(k_sell_narrow_tma,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)NB_SMEM));
+                attr[g.device] = true;
+            }
+            const int64_t nfull = A.nvr / (32 * NB_CH);
+            k_sell_narrow_tma<<<g.sm_count, 1024, NB_SMEM, st>>>(A, nfull);
+        } else if (pf == 1) k_sell_narrow_pf<1><<<g.sm_count, 1024, 0, st>>>(A);
+        else if (pf == 2 || pf == 9) k_sell_narrow_pf<2><<<g.sm_count, 1024, 0, st>>>(A);
         else if (pf == 4) k_sell_narrow_pf<4><<<g.sm_count, 1024, 0, st>>>(A);
         else if (tune_get("k1.narrow_q", 2) == 4) k_sell_narrow<4><<<g.sm_count * 2, 1024, 0, st>>>(A);
         else k_sell_narrow<2><<<g.sm_count * 2, 1024, 0, st>>>(A);
