@@ -1185,6 +1185,7 @@ int kb_state_destroy(kb_state *h) {
         if (h->s.ev0) cudaEventDestroy(h->s.ev0);
         if (h->s.ev1) cudaEventDestroy(h->s.ev1);
         if (h->s.chk_ev) cudaEventDestroy(h->s.chk_ev);
+        if (h->s.chk_ev2) cudaEventDestroy(h->s.chk_ev2);
         for (cudaEvent_t e : h->s.k1_ev) cudaEventDestroy(e);
         delete h;
     });

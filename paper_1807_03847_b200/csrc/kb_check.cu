@@ -1355,34 +1355,98 @@ bool ranking_pair_chain(State &s, cudaStream_t st) {
     s.rank_order_pending = true;
     if (!s.abort_flag.p) s.abort_flag.alloc(1);
     if (!s.chk_ev) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev, cudaEventDisableTiming));
+    if (!s.chk_ev2) KB_CUDA(cudaEventCreateWithFlags(&s.chk_ev2, cudaEventDisableTiming));
     KB_CUDA(cudaMemsetAsync(s.abort_flag.p, 0, sizeof(unsigned long long), st));
-    const int64_t batch = std::max<int64_t>(1, tune_get("run.rank_batch", 16));
+    const int64_t batch = std::max<int64_t>(1, tune_get("run.rank_batch", 8));
+    const bool fuse = tune_get("chk.pair_fuse", 1) != 0;
+    const bool pub_host = tune_get("chk.pub_host", 0) != 0;
+    // two batches in flight: the next is queued before the host waits on the
+    // current one, so the GPU never idles through a host read; a batch
+    // queued behind a test that stopped refuting exits kernel by kernel on
+    // the abort flag, and its levels are dropped here
+    const bool pipe = tune_get("run.rank_pipe", 1) != 0 && !pub_host;
+    struct Inflight {
+        int64_t r_last;
+        const unsigned long long *words;
+        cudaEvent_t ev;
+    };
+    Inflight q[2];
+    int nq = 0, slot = 0;
+    cudaEvent_t evs[2] = {s.chk_ev, s.chk_ev2};
+    unsigned long long *hb[2] = {s.h_flags + 16, s.h_flags + 24};
+    bool first = true;
+    s.pair_fuse = State::PairFuse{};
+    auto enqueue = [&] {
+        for (int64_t j = 0; j < batch; j++) {
+            if (!(first && j == 0)) {
+                if (s.r >= s.max_iter) break;
+                if (fuse) {
+                    s.pair_fuse.want = true;
+                    s.pair_fuse.q = s.rk_q;
+                    s.pair_fuse.x = s.rk_x;
+                    s.pair_fuse.eps = s.eps;
+                    s.pair_fuse.perm = g.labels();
+                    s.pair_fuse.out = s.scratch_u64.p;
+                    s.pair_fuse.abort = s.abort_flag.p;
+                    s.pair_fuse.pub = pub_words(s);
+                    s.pair_fuse.k1c = s.work_counter.p;
+                }
+                s.spec_abort = true;   // exits once a test before it stopped refuting
+                launch_iterate(s, st);
+                s.spec_abort = false;
+                s.pair_fuse.want = false;
+            }
+            // the test of level s.r: already run by the tail of the K1 that
+            // produced it (the TMA-staged narrow kernel), else a one-thread
+            // launch
+            if (!s.pair_fuse.done) {
+                k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma,
+                                                    s.undirected, g.labels(), s.rk_q, s.rk_x,
+                                                    s.eps, s.scratch_u64.p, s.abort_flag.p,
+                                                    pub_words(s), s.work_counter.p, s.r,
+                                                    (int)tune_get("chk.sys_fence", 0));
+                note_launch();
+            }
+            s.pair_fuse = State::PairFuse{};
+            s.counter_zeroed = true;
+        }
+        first = false;
+        KB_CUDA(cudaGetLastError());
+        const unsigned long long *words = s.h_flags;
+        if (!pub_host) {      // this batch's closing words to its own host slot
+            KB_CUDA(cudaMemcpyAsync(hb[slot], s.pub_dev.p, 4 * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, st));
+            words = hb[slot];
+        }
+        KB_CUDA(cudaEventRecord(evs[slot], st));
+        q[nq++] = Inflight{s.r, words, evs[slot]};
+        slot ^= 1;
+    };
     const int64_t r0 = s.r;
-    for (int64_t j = 0; j < batch; j++) {
-        k_pair_refutes_pub<<<1, 1, 0, st>>>(s.katz.p, s.x_level(), s.alpha, s.gamma,
-                                            s.undirected, g.labels(), s.rk_q, s.rk_x, s.eps,
-                                            s.scratch_u64.p, s.abort_flag.p, pub_words(s),
-                                            s.work_counter.p, s.r,
-                                            (int)tune_get("chk.sys_fence", 0));
-        note_launch();
-        s.counter_zeroed = true;
-        if (j + 1 == batch || s.r >= s.max_iter) break;
-        s.spec_abort = true;           // exits once a test before it stopped refuting
-        launch_iterate(s, st);
-        s.spec_abort = false;
+    enqueue();
+    for (;;) {
+        if (pipe && nq < 2 && s.r < s.max_iter) enqueue();
+        const Inflight b = q[0];
+        q[0] = q[1];
+        nq -= 1;
+        KB_CUDA(cudaEventSynchronize(b.ev));
+        const bool refutes = b.words[0] != 0;
+        const int64_t last = (int64_t)b.words[3];   // level of the last test that ran
+        KB_REQUIRE(last >= r0 && last <= b.r_last, KB_ECUDA, "device loop lost its verdict");
+        if (!refutes) {
+            while (s.r > last) {      // levels queued behind the test that stopped refuting
+                s.levels.pop_back();
+                s.r -= 1;
+                if (s.k1_used >= 2) s.k1_used -= 2;
+            }
+            return false;
+        }
+        KB_REQUIRE(last == b.r_last, KB_ECUDA, "device loop lost its verdict");
+        if (nq == 0) {
+            if (s.r >= s.max_iter) return true;
+            enqueue();
+        }
     }
-    KB_CUDA(cudaGetLastError());
-    publish_copy(s, st);
-    KB_CUDA(cudaEventRecord(s.chk_ev, st));
-    KB_CUDA(cudaEventSynchronize(s.chk_ev));
-    const int64_t last = (int64_t)s.h_flags[3];
-    KB_REQUIRE(last >= r0 && last <= s.r, KB_ECUDA, "device loop lost its verdict");
-    while (s.r > last) {               // levels queued behind a test that stopped refuting
-        s.levels.pop_back();
-        s.r -= 1;
-        if (s.k1_used >= 2) s.k1_used -= 2;
-    }
-    return s.h_flags[0] != 0;
 }
 
 bool run_check(State &s, cudaStream_t st) {

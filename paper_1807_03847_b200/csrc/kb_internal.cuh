@@ -328,6 +328,16 @@ struct State {
     // and exits at once if that check converged (abort_flag, set on device)
     DBuf<unsigned long long> abort_flag;
     bool spec_abort = false;
+    // RANKING chain: the cached pair's test fused into the next K1's tail
+    // (k_sell_narrow_tma's last CTA), when that kernel runs the level
+    struct PairFuse {
+        bool want = false, done = false;
+        int32_t q = -1, x = -1;
+        double eps = 0;
+        const int32_t *perm = nullptr;
+        unsigned long long *out = nullptr, *abort = nullptr, *pub = nullptr, *k1c = nullptr;
+    } pair_fuse;
+    DBuf<unsigned long long> pair_done;     // arrival counter of the fused test
     // RANKING runs skip the per-iteration lower/upper stores (K1 writes w and
     // katz only); materialize_bounds recomputes them, bit for bit, before
     // anything reads them
@@ -336,6 +346,7 @@ struct State {
     bool counter_zeroed = false;  // the next K1's work counter was reset on the device
     int exch_parity = 0;      // parity of the level being computed
     cudaEvent_t chk_ev = nullptr;
+    cudaEvent_t chk_ev2 = nullptr;   // the second batch in flight (RANKING chain)
     DBuf<unsigned long long> tie_count;  // k-boundary ties dropped with gap < eps (rule 4)
     bool rank_order_pending = false;    // RANKING: active not yet in (-lower, id) order
     std::vector<int64_t> level_sizes;   // UpdateStats.level_sizes of the last update

@@ -77,6 +77,14 @@ struct IterArgs {
     int hot_per, hot_shift;
     unsigned long long *counter;
     const unsigned long long *abort;  // speculative launch: exit if set
+    // fused cached-pair test (RANKING chain, k_sell_narrow_tma): the last CTA
+    // evaluates k_pair_refutes_pub's rule on the level just written
+    unsigned long long *pair_done;
+    int32_t pair_q, pair_x;
+    double pair_eps;
+    const int32_t *pair_perm;
+    unsigned long long *pair_out, *pair_abort, *pair_pub, *pair_k1c;
+    int64_t pair_level;
 };
 
 __device__ __forceinline__ bool aborted(const IterArgs &A) {
@@ -515,6 +523,25 @@ __device__ __forceinline__ double narrow_slice_sum(const double *__restrict__ x,
     return sum;
 }
 
+// k_pair_refutes_pub's rule (kb_check.cu) on the level this launch wrote, by
+// the last CTA to finish (its stores fenced device-wide before it counts in)
+__device__ void fused_pair_test(const IterArgs &A) {
+    const int32_t q = A.pair_q, x = A.pair_x;
+    const double tq = __dmul_rn(A.alpha, __ldcg(A.w + q));
+    const double tx = __dmul_rn(A.alpha, __ldcg(A.w + x));
+    const double kq = __ldcg(A.katz + q), kx = __ldcg(A.katz + x);
+    const double lq = A.undirected ? __dadd_rn(kq, tq) : kq;
+    const double lx = A.undirected ? __dadd_rn(kx, tx) : kx;
+    const double uq = __dadd_rn(kq, __dmul_rn(tq, A.gamma));
+    const bool above = lx > lq || (lx == lq && A.pair_perm[x] < A.pair_perm[q]);
+    const bool ref = above && lx <= __dsub_rn(uq, A.pair_eps);
+    A.pair_out[0] = ref ? 1ull : 0ull;
+    A.pair_abort[0] = ref ? 0ull : 1ull;
+    A.pair_k1c[0] = 0ull;
+    A.pair_pub[0] = ref ? 1ull : 0ull;
+    A.pair_pub[3] = (unsigned long long)A.pair_level;
+}
+
 __global__ void __launch_bounds__(1024, 1) k_sell_narrow_tma(IterArgs A, int64_t nfull) {
     if (aborted(A)) return;
     extern __shared__ int4 nb_smem4[];                   // 16-byte aligned (bulk copies)
@@ -626,6 +653,15 @@ __global__ void __launch_bounds__(1024, 1) k_sell_narrow_tma(IterArgs A, int64_t
         }
     }
     if (A.npeer) __threadfence_system();
+    if (A.pair_done) {
+        __threadfence();                       // this thread's row stores
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(A.pair_done, 1ull) == gridDim.x - 1) {
+            __threadfence();
+            fused_pair_test(A);
+            *A.pair_done = 0ull;               // ready for the next launch
+        }
+    }
 }
 
 // First iteration: x = levels[0] = ones, so every sequential row (or segment)
@@ -922,6 +958,24 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     }
     A.counter = s.work_counter.p;
     A.abort = s.spec_abort ? s.abort_flag.p : nullptr;
+    A.pair_done = nullptr;
+    if (s.pair_fuse.want && !level_only) {
+        if (!s.pair_done.p) {
+            s.pair_done.alloc(1);
+            KB_CUDA(cudaMemsetAsync(s.pair_done.p, 0, sizeof(unsigned long long), st));
+        }
+        const auto &f = s.pair_fuse;
+        A.pair_done = s.pair_done.p;
+        A.pair_q = f.q;
+        A.pair_x = f.x;
+        A.pair_eps = f.eps;
+        A.pair_perm = f.perm;
+        A.pair_out = f.out;
+        A.pair_abort = f.abort;
+        A.pair_pub = f.pub;
+        A.pair_k1c = f.k1c;
+        A.pair_level = s.r + 1;
+    }
     A.lazy_bounds = (s.lazy_bounds && !level_only) ? 1 : 0;
     A.npeer = 0;
     if (s.exch_on && w == g.exch[s.exch_parity]) {
@@ -1007,6 +1061,7 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
             }
             const int64_t nfull = A.nvr / (32 * NB_CH);
             k_sell_narrow_tma<<<g.sm_count, 1024, NB_SMEM, st>>>(A, nfull);
+            if (A.pair_done) s.pair_fuse.done = true;
         } else if (pf == 1) k_sell_narrow_pf<1><<<g.sm_count, 1024, 0, st>>>(A);
         else if (pf == 2 || pf == 9) k_sell_narrow_pf<2><<<g.sm_count, 1024, 0, st>>>(A);
         else if (pf == 4) k_sell_narrow_pf<4><<<g.sm_count, 1024, 0, st>>>(A);
