@@ -249,6 +249,9 @@ struct Graph {
     int64_t n_ovf = 0;
     DBuf<int32_t> ovf_long;           // overflow rows longer than OVF_LONG arcs
     int64_t n_ovf_long = 0;
+    DBuf<double> ovf_sum;             // their sums, computed beside K1 (side stream)
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t side_fork = nullptr, side_join = nullptr;
     Sell sell;
     // heavy-row combine: segments of heavy row h are seg_list[seg_ptr[h] ..
     // seg_ptr[h+1]) in order (indices into the segment-sum buffer)
@@ -272,6 +275,12 @@ struct Graph {
     Graph(const Graph &) = delete;
     Graph &operator=(const Graph &) = delete;
     ~Graph() {
+        if (side_stream) {
+            cudaStreamSynchronize(side_stream);
+            cudaStreamDestroy(side_stream);
+            cudaEventDestroy(side_fork);
+            cudaEventDestroy(side_join);
+        }
         for (void *p : exch_opened) cudaIpcCloseMemHandle(p);
         for (double *&p : exch)
             if (p) { cudaFree(p); p = nullptr; }

@@ -745,7 +745,7 @@ __global__ void k_empty_rows(double *upper, double *lower, const double *katz,
 // One warp per row.
 __global__ void k_ovf_rows(IterArgs A, const int32_t *rows, int64_t nr, const int32_t *perm,
                            const int32_t *iperm, const int64_t *indptr, const int32_t *rlen,
-                           const int32_t *indices, int64_t split) {
+                           const int32_t *indices, int64_t split, double *sums = nullptr) {
     if (aborted(A)) return;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -783,7 +783,10 @@ __global__ void k_ovf_rows(IterArgs A, const int32_t *rows, int64_t nr, const in
             }
         }
     }
-    if (lane == 0) epilogue(A, v, s);
+    if (lane == 0) {
+        if (sums) sums[warp] = s;      // side-stream mode: k_ovf_merge applies it
+        else epilogue(A, v, s);
+    }
 }
 
 // Long overflow rows, a block each.  A row of at most split arcs is one
@@ -798,7 +801,8 @@ constexpr int OVF_WCHUNK = 256;
 __global__ void __launch_bounds__(256) k_ovf_long(IterArgs A, const int32_t *rows,
                                                   const int32_t *perm, const int32_t *iperm,
                                                   const int64_t *indptr, const int32_t *rlen,
-                                                  const int32_t *indices, int64_t split) {
+                                                  const int32_t *indices, int64_t split,
+                                                  double *sums = nullptr) {
     if (aborted(A)) return;
     __shared__ double buf[2][OVF_CHUNK];
     __shared__ double segsum[8];
@@ -871,7 +875,27 @@ __global__ void __launch_bounds__(256) k_ovf_long(IterArgs A, const int32_t *row
             __syncthreads();
         }
     }
-    if (tid == 0) epilogue(A, v, s);
+    if (tid == 0) {
+        if (sums) sums[blockIdx.x] = s;
+        else epilogue(A, v, s);
+    }
+}
+
+// Side-stream mode: the overflow rows' sums were computed concurrently with
+// K1 (which left those rows at +0 and katz unchanged: katz + 0.0 is katz);
+// applying the epilogue now gives the same bits as the serial passes.
+__global__ void k_ovf_merge(IterArgs A, const int32_t *rows, int64_t nr, const int32_t *perm,
+                            const int32_t *rlen, const double *sums,
+                            const int32_t *long_rows, int64_t nlong,
+                            const double *long_sums) {
+    if (aborted(A)) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nr) {
+        const int32_t v = rows[t];
+        if (rlen[perm[v]] <= OVF_LONG) epilogue(A, v, sums[t]);
+    } else if (t < nr + nlong) {
+        epilogue(A, long_rows[t - nr], long_sums[t - nr]);
+    }
 }
 
 // explicit empty rows (after updates): w = 0 and the bounds collapse to katz
@@ -1040,6 +1064,32 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         KB_CUDA(cudaMemsetAsync(s.work_counter.p, 0, sizeof(unsigned long long), st));
     s.counter_zeroed = false;
     KB_CUDA(cudaEventRecord(s.k1_ev[s.k1_used], st));
+    // overflow rows (dynamic batches): their sums on a side stream while K1
+    // runs, the epilogue applied after it (k_ovf_merge)
+    const bool ovf_side = g.n_ovf > 0 && !ones && tune_get("k1.ovf_side", 1);
+    if (ovf_side) {
+        if (!g.side_stream) {
+            KB_CUDA(cudaStreamCreateWithFlags(&g.side_stream, cudaStreamNonBlocking));
+            KB_CUDA(cudaEventCreateWithFlags(&g.side_fork, cudaEventDisableTiming));
+            KB_CUDA(cudaEventCreateWithFlags(&g.side_join, cudaEventDisableTiming));
+        }
+        if (g.ovf_sum.n < (size_t)(g.n_ovf + g.n_ovf_long))
+            g.ovf_sum.alloc(g.n_ovf + g.n_ovf_long);
+        KB_CUDA(cudaEventRecord(g.side_fork, st));
+        KB_CUDA(cudaStreamWaitEvent(g.side_stream, g.side_fork, 0));
+        k_ovf_rows<<<(unsigned)((g.n_ovf * 32 + 255) / 256), 256, 0, g.side_stream>>>(
+            A, g.ovf.p, g.n_ovf, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p,
+            g.split, g.ovf_sum.p);
+        note_launch();
+        if (g.n_ovf_long) {
+            k_ovf_long<<<(unsigned)g.n_ovf_long, 256, 0, g.side_stream>>>(
+                A, g.ovf_long.p, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p, g.split,
+                g.ovf_sum.p + g.n_ovf);
+            note_launch();
+        }
+        KB_CUDA(cudaGetLastError());
+        KB_CUDA(cudaEventRecord(g.side_join, g.side_stream));
+    }
     if (A.nslices && ones) {
         k_ones_step<<<(unsigned)((A.nvr + 255) / 256), 256, 0, st>>>(A);
         note_launch();
@@ -1134,14 +1184,21 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
             s.upper.p, s.lower.p, s.katz.p, g.nv, n); note_launch();
         KB_CUDA(cudaGetLastError());
     }
-    if (g.n_ovf) {
+    if (ovf_side) {
+        KB_CUDA(cudaStreamWaitEvent(st, g.side_join, 0));
+        k_ovf_merge<<<(unsigned)((g.n_ovf + g.n_ovf_long + 255) / 256), 256, 0, st>>>(
+            A, g.ovf.p, g.n_ovf, g.perm.p, g.rlen.p, g.ovf_sum.p, g.ovf_long.p, g.n_ovf_long,
+            g.ovf_sum.p + g.n_ovf);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    } else if (g.n_ovf) {
         k_ovf_rows<<<(unsigned)((g.n_ovf * 32 + 255) / 256), 256, 0, st>>>(
             A, g.ovf.p, g.n_ovf, g.perm.p, g.iperm.p, g.indptr.p, g.rlen.p, g.indices.p,
             g.split);
         note_launch();
         KB_CUDA(cudaGetLastError());
     }
-    if (g.n_ovf_long) {
+    if (g.n_ovf_long && !ovf_side) {
         k_ovf_long<<<(unsigned)g.n_ovf_long, 256, 0, st>>>(A, g.ovf_long.p, g.perm.p, g.iperm.p,
                                                           g.indptr.p, g.rlen.p, g.indices.p,
                                                           g.split);
