@@ -321,11 +321,14 @@ def run_grid(a, device):
     for _ in range(a.warmup):
         step()
     ms = P.engine.ctypes.c_double()
+    lc0, lc1 = P.engine.ctypes.c_int64(), P.engine.ctypes.c_int64()
     with ClockSampler(device) as clk:
+        _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc0)))
         _lib.check(L.kb_timer(device, 0, None))
         for _ in range(a.steps):
             step()
         _lib.check(L.kb_timer(device, 1, P.engine.ctypes.byref(ms)))
+        _lib.check(L.kb_launch_count(P.engine.ctypes.byref(lc1)))
     timed = infos[a.warmup:]
     r = int(timed[0][0].r)
     k1 = sum(i.spmv_ms for i, _ in timed) / max(1, sum(i.spmv_launches for i, _ in timed))
@@ -346,6 +349,7 @@ def run_grid(a, device):
                          "avg_launch_ms": k1, "bytes_per_launch": B, "peak_source": src,
                          "bytes_note": "4 nnz + 4 (n+1) + 32 n: the bound stores (16 n) are "
                                        "deferred to materialize_bounds (4 passes per run)"},
+            "gpu_launches": int(lc1.value - lc0.value),
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 

@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-bash tools/round_check.sh
-bash tools/checked_suite.sh
-timeout 900 python bench.py --workload c4 > gpurun_out/fin_c4.log 2>&1; echo "c4 $?"
-timeout 1500 python bench.py --scale 27 > gpurun_out/fin_c3.log 2>&1; echo "c3 $?"
-timeout 900 python bench.py --workload c5 > gpurun_out/fin_c5.log 2>&1; echo "c5 $?"
+timeout 900 python bench.py --steps 10 --warmup 3 --sharded --no-cpu --no-e2e > gpurun_out/g89_sh.log 2>&1; echo "sharded $?"
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29513 tools/sharded_breakdown.py > gpurun_out/g89_brk.log 2>&1; echo "brk $?"
