@@ -120,8 +120,11 @@ typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, voi
                              const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
-    const int64_t n = 1ll << 24, m = 1ll << 26;
+int main(int argc, char **argv) {
+    // log2 of the vector length (default 24: 128 MiB, DRAM-bound); 22 keeps
+    // it L2-resident like C2's hot columns; "mix" runs LDG and TMA gather4
+    // kernels concurrently on split index sets
+    const int64_t n = 1ll << (argc > 1 ? atoi(argv[1]) : 24), m = 1ll << 26;
     double *x;
     int32_t *idx;
     double *out;
@@ -182,6 +185,35 @@ int main() {
                 printf("TMA gather4 %d CTA/SM: %.3f ms, %.3f rows/SM/cycle\n", ctas, ms,
                        m / (ms * 1e-3) / sms / (clk * 1e3));
         }
+    }
+    // concurrent: LDG (768 threads/SM) on a fraction f of the indices, TMA
+    // gather4 (4 CTAs/SM) on the rest, on two streams
+    cudaStream_t s1, s2;
+    CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    for (double f : {1.0, 0.9, 0.8, 0.7, 0.6}) {
+        const int64_t ml = ((int64_t)(m * f) / 512) * 512, mt = m - ml;
+        float best = 1e9f;
+        for (int rep = 0; rep < 4; rep++) {
+            CK(cudaDeviceSynchronize());
+            cudaEventRecord(a);
+            CK(cudaStreamWaitEvent(s1, a, 0));
+            CK(cudaStreamWaitEvent(s2, a, 0));
+            if (mt) k_tma<<<sms * 4, 32 * (CONS + 1), 0, s2>>>(map, idx + ml, mt, out);
+            k_ldg<<<sms, 768, 0, s1>>>(x, idx, ml, out);
+            cudaEvent_t e1, e2;
+            cudaEventCreate(&e1); cudaEventCreate(&e2);
+            cudaEventRecord(e1, s1); cudaEventRecord(e2, s2);
+            CK(cudaStreamWaitEvent(0, e1, 0)); CK(cudaStreamWaitEvent(0, e2, 0));
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            CK(cudaGetLastError());
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep && ms < best) best = ms;
+        }
+        printf("mix LDG %.0f%% / TMA %.0f%%: %.3f ms, %.3f gathers/SM/cycle\n", f * 100,
+               (1 - f) * 100, best, m / (best * 1e-3) / sms / (clk * 1e3));
     }
     return 0;
 }
