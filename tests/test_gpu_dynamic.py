@@ -518,3 +518,53 @@ def test_mixed_batches_relocate_and_respread(capfd, monkeypatch):
         assert "relocate rows" in err and "respread" in err, err[-2000:]
     finally:
         _lib.check(L.kb_tune(b"dyn.tail_room", 1 << 20))
+
+
+def test_grid_updates_through_the_narrow_kernel_bitwise():
+    """An all-narrow graph (a grid) runs K1 as the TMA-staged narrow kernel,
+    also in the level repair (level-only launches, no katz stream) and with
+    the RANKING chain's fused pair test.  Insert and delete a few grid-local
+    arcs, keeping every degree <= 4: levels and bounds equal a fresh static
+    layout's bit for bit, and the ranking equals a fresh run's."""
+    from paper_1807_03847_b200 import generators as G
+    side = 96
+    n = side * side
+    g = G.grid_graph(n)
+    crit = P.Criterion.ranking(1e-9)
+    st = P.init(g, crit, undirected=True, max_iterations=400)
+    P.run(st, g)
+    deg = g.out_degrees()
+    rng = np.random.default_rng(2)
+    ins, dele = set(), set()
+    ip, ix = g.csr_arrays()
+    for _ in range(400):
+        u = int(rng.integers(0, n))
+        if deg[u] >= 4:
+            continue
+        for v in (u + 2, u + 2 * side):       # a short grid-local chord
+            if v < n and deg[v] < 4 and not g.has_arc(u, v) and (u, v) not in ins:
+                ins.add((u, v))
+                deg[u] += 1
+                deg[v] += 1
+                break
+        if len(ins) >= 30:
+            break
+    for u in range(0, n, 997):                # a few deletions of existing arcs
+        nb = ix[ip[u]:ip[u + 1]]
+        if nb.size:
+            v = int(nb[0])
+            dele.add((min(u, v), max(u, v)))
+    ia = np.array(sorted(ins), dtype=np.int64).reshape(-1, 2)
+    da = np.array(sorted(dele), dtype=np.int64).reshape(-1, 2)
+    P.update_batch(st, g, P.EdgeBatch(insertions=np.concatenate([ia, ia[:, ::-1]]),
+                                      deletions=np.concatenate([da, da[:, ::-1]])))
+    ip, ix = g.csr_arrays()
+    fg = P.Graph.from_csr(n, ip, ix)
+    fresh = fresh_to_depth(fg, st)
+    for mine, theirs in zip(st.levels, fresh.levels):
+        np.testing.assert_array_equal(mine, theirs)
+    np.testing.assert_array_equal(st.lower, fresh.lower)
+    np.testing.assert_array_equal(st.upper, fresh.upper)
+    res = P.ranking_result(st)
+    fres = P.run(P.init(fg, crit, undirected=True, alpha=st.alpha, max_iterations=400), fg)
+    np.testing.assert_array_equal(res.order, fres.order)

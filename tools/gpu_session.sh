@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-for b in 22 20; do timeout 300 ./tools/micro/tma_gather $b; done > gpurun_out/g90_mix.log 2>&1; echo "mix $?"
+timeout 900 python -m pytest tests/test_gpu_dynamic.py -x -q -k grid > gpurun_out/g91_test.log 2>&1; echo "test $?"
