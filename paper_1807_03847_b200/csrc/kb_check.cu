@@ -566,6 +566,65 @@ __global__ void __launch_bounds__(1024) k_topk_finish(const double *lower, const
     }
 }
 
+// The TOPK check at level 1 of a fresh degree-relabelled layout, in one
+// thread.  After the first iteration every bound is a function of the row
+// length alone -- lower_1 = fl(a*d) + fl(a*fl(a*d)) (undirected; katz_1 for
+// directed), upper_1 = fl(a*d) + fl(fl(a*fl(a*d))*gamma), both
+// non-decreasing in d and strictly increasing for distinct integer d < 2^52
+// -- and new ids order rows by (length desc, original id asc).  So the
+// order by (-lower, id) is the new-id order: the winners are [0, k), the
+// threshold is lower[k-1], and since upper is non-increasing in the new id
+// the survivors fl(upper - eps) >= threshold are [k, S), found by bisection.
+// The active set becomes exactly [0, S): the next check reads it densely.
+// Boundary ties (lower == threshold, dropped) are [S, end of the equal run).
+__global__ void k_topk_level1(const double *lower, const double *upper, int64_t nv, int64_t k,
+                              double eps, const int32_t *perm, int32_t *act_out,
+                              unsigned long long *out, unsigned long long *ties,
+                              Publish pub) {
+    if (flag_set(pub.abort)) return;
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const double T = lower[k - 1];
+    // warp-wide 32-ary searches for the first v in [k, nv) failing a monotone
+    // predicate (true on a prefix): five rounds at C2 instead of 24 probes
+    auto first_fail = [&](auto pred) {
+        int64_t lo = k, hi = nv;      // pred true on [k, lo), false on [hi, nv)
+        while (hi - lo > 0) {
+            const int64_t len = hi - lo;
+            const int64_t step = (len + 31) / 32;
+            const int64_t p = lo + (int64_t)lane * step;
+            const bool ok = p < hi ? pred(p) : false;
+            const unsigned bal = __ballot_sync(0xffffffffu, ok);
+            const int c = __popc(bal);        // lanes [0, c) pass (prefix)
+            const int64_t nlo = lo + (int64_t)c * step;
+            if (c == 0) { hi = lo; break; }
+            lo = c == 32 ? lo + 31 * step + 1 : lo + (int64_t)(c - 1) * step + 1;
+            hi = min(hi, nlo);
+            if (step == 1) { lo = hi = min(nlo, hi); break; }
+        }
+        return lo;
+    };
+    const int64_t S = first_fail([&](int64_t v) { return __dsub_rn(upper[v], eps) >= T; });
+    const int64_t a = first_fail([&](int64_t v) { return lower[v] >= T; });
+    if (lane != 0) return;
+    if (ties && a > S) atomicAdd(ties, (unsigned long long)(a - S));
+    bool conv = false;
+    if (S <= k) {                     // |active| <= k: the adjacent separations
+        bool bad = false;
+        for (int64_t i = 1; i < S && !bad; i++) bad = !(__dsub_rn(upper[i], eps) < lower[i - 1]);
+        conv = !bad;
+        for (int64_t i = 0; i < S; i++) act_out[i] = (int32_t)i;   // also as a list
+    }
+    out[0] = (unsigned long long)S;
+    out[1] = conv ? 1ull : 0ull;
+    out[2] = (unsigned long long)k;
+    out[3] = (unsigned long long)__double_as_longlong(T);
+    out[4] = (unsigned long long)(uint32_t)perm[k - 1];
+    out[5] = (unsigned long long)k;
+    out[6] = (unsigned long long)(S - k);
+    publish(pub, out);
+}
+
 // The whole TOPK check for a small active set (m <= SMALL_M, the last
 // iterations of every R-MAT run: C2 ends at |active| 254 -> 100) in one
 // block: the set is sorted by (-lower, label) in shared memory, the first
@@ -1479,7 +1538,7 @@ constexpr int64_t SMALL_M = 4096, MID_M = 1 << 18, MID_G = 32;
 // active set moves from act[cur] to act[cur ^ 1]; the kernel that finishes the
 // check publishes the verdict tagged with `level`.  Returns the new index.
 int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense, int cur,
-                           int64_t level) {
+                           int64_t level, bool level1 = false) {
     NvtxRange nv("K2 topk check", (long long)level);
     Graph &g = *s.g;
     const int64_t k = s.k;
@@ -1542,7 +1601,11 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
                                              SMALL_M, pub);
         note_launch();
     };
-    if (m_host >= 0) {
+    if (level1) {
+        k_topk_level1<<<1, 32, 0, st>>>(s.lower.p, s.upper.p, s.g->nv, k, s.eps, g.labels(),
+                                        s.act[nxt].p, out, s.tie_count.p, pub);
+        note_launch();
+    } else if (m_host >= 0) {
         // in the dense first check, rows without out-arcs (new ids >= nv) have
         // lower == upper == 0 < every other lower: when k <= nv they can be
         // neither winners nor survivors, so they are dropped unread
@@ -1573,6 +1636,16 @@ int topk_check_enqueue_dev(State &s, cudaStream_t st, int64_t m_host, bool dense
     KB_CUDA(cudaGetLastError());
     s.counter_zeroed = true;
     return nxt;
+}
+
+// k_topk_level1 applies: the check right after the first iteration of a
+// fresh single-GPU degree-relabelled layout, with the whole node set active
+bool level1_shortcut_ok(const State &s) {
+    const Graph &g = *s.g;
+    return tune_get("chk.level1", 1) && s.kind == KB_TOPK && s.r == 1 && s.act_dense &&
+           s.m_host == g.n && g.relabel && !g.mutated && g.implicit_rows && !s.exch_on &&
+           g.own_lo == 0 && (g.own_hi < 0 || g.own_hi == g.n) && s.k >= 1 && s.k <= g.nv &&
+           s.k <= KMAX && s.tail_zero_from == g.nv && s.level_base == 0;
 }
 
 int topk_check_enqueue(State &s, cudaStream_t st) {
@@ -1608,12 +1681,15 @@ bool topk_run_device(State &s, cudaStream_t st) {
         const int64_t r0 = s.r, B = std::min<int64_t>(batch, s.max_iter - s.r);
         const int cur0 = s.cur;
         int cur = cur0;
+        bool dense_next = false;
         for (int64_t j = 0; j < B; j++) {
             s.spec_abort = true;      // exits once a check before it has converged
             launch_iterate(s, st);
             s.spec_abort = false;
-            cur = topk_check_enqueue_dev(s, st, j == 0 ? s.m_host : -1, j == 0 && s.act_dense,
-                                         cur, s.r);
+            const bool l1 = j == 0 && level1_shortcut_ok(s);
+            cur = topk_check_enqueue_dev(s, st, j == 0 ? s.m_host : -1,
+                                         (j == 0 && s.act_dense) || dense_next, cur, s.r, l1);
+            dense_next = l1;          // the level-1 check leaves active = [0, S)
         }
         publish_copy(s, st);
         KB_CUDA(cudaEventRecord(s.chk_ev, st));

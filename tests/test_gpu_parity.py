@@ -286,3 +286,46 @@ def test_device_loop_cap_rerun_and_state(kind):
     O.iterate_once(ost, g0)
     assert O.check_converged(ost)
     np.testing.assert_allclose(res2.lower, ost.lower, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("case,k", [("rmat12", 100), ("rmat14", 100), ("star", 100),
+                                    ("rmat10", 600), ("rmat12", 1)])
+def test_level1_check_shortcut_matches_the_general_check(case, k):
+    """The TOPK check right after the first iteration of a fresh layout reads
+    the winners, threshold and survivors off the degree order
+    (k_topk_level1) and leaves the active set as the dense prefix [0, S)
+    for the next check.  Against the general select (kb_tune chk.level1 0):
+    the same r, active set (in order), bounds, order, separated fraction and
+    boundary-tie count, bit for bit (the star's leaves all tie at the cut)."""
+    from paper_1807_03847_b200 import _lib
+    L = _lib.lib()
+    if case.startswith("rmat"):
+        n = 1 << int(case[4:])
+        g0 = O.rmat_graph(n, edge_factor=8, seed=int(case[4:]))
+        ip, ix = g0.indptr, g0.indices
+    else:
+        n = 300
+        e = [(0, v) for v in range(1, n)]
+        a = np.array(e + [(v, u) for u, v in e], dtype=np.int64)
+        a = a[np.lexsort((a[:, 1], a[:, 0]))]
+        ip = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(ip, a[:, 0] + 1, 1)
+        ip = np.cumsum(ip)
+        ix = a[:, 1].astype(np.int32)
+    out = {}
+    for flag in (0, 1):
+        _lib.check(L.kb_tune(b"chk.level1", flag))
+        try:
+            g = P.Graph.from_csr(n, ip, ix)
+            st = P.init(g, P.Criterion.top_k(k, 1e-6), undirected=True, max_iterations=500)
+            res = P.run(st, g)
+            out[flag] = (st.r, np.asarray(st.active).copy(), np.asarray(st.lower).copy(),
+                         np.asarray(st.upper).copy(), np.asarray(res.order).copy(),
+                         res.separated_fraction, st.k_boundary_ties)
+        finally:
+            _lib.check(L.kb_tune(b"chk.level1", 1))
+    a0, a1 = out[0], out[1]
+    assert a0[0] == a1[0]
+    for x, y in zip(a0[1:5], a1[1:5]):
+        np.testing.assert_array_equal(x, y)
+    assert a0[5] == a1[5] and a0[6] == a1[6]
