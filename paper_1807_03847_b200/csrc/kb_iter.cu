@@ -714,17 +714,28 @@ __global__ void k_heavy_combine_w(IterArgs A, const int32_t *seg_ptr, const int3
     const int lane = threadIdx.x & 31;
     const int q0 = seg_ptr[h], q1 = seg_ptr[h + 1];
     double s = 0.0;
-    for (int b = q0; b < q1; b += 32) {
-        const int q = b + lane;
-        double v = 0.0;
-        if (q < q1) {
-            KB_DCHECK(seg_list[q] >= 0 && seg_list[q] < A.nseg);
-            v = A.seg_sum[seg_list[q]];
+    // up to 8 x 32 segment sums loaded at once (one round of latency for the
+    // hubs' ~200 segments), then folded in order by lane 0
+    constexpr int R = 8;
+    for (int b0 = q0; b0 < q1; b0 += 32 * R) {
+        double v[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int q = b0 + r * 32 + lane;
+            v[r] = 0.0;
+            if (q < q1) {
+                KB_DCHECK(seg_list[q] >= 0 && seg_list[q] < A.nseg);
+                v[r] = A.seg_sum[seg_list[q]];
+            }
         }
-        const int cnt = min(32, q1 - b);
-        for (int j = 0; j < cnt; j++) {
-            const double t = __shfl_sync(0xffffffffu, v, j);
-            if (lane == 0) s = __dadd_rn(s, t);
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int b = b0 + r * 32;
+            const int cnt = max(0, min(32, q1 - b));
+            for (int j = 0; j < cnt; j++) {
+                const double t = __shfl_sync(0xffffffffu, v[r], j);
+                if (lane == 0) s = __dadd_rn(s, t);
+            }
         }
     }
     if (lane == 0) epilogue(A, A.hrow ? A.hrow[h] : h, s);
