@@ -222,9 +222,14 @@ unsigned long long *pinned_flags() {
 
 namespace {
 
-__global__ void k_fill(double *p, int64_t n, double v) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
+__global__ void k_init_state(double *ones, double *katz, double *lower, double *upper,
+                             int64_t n, double ag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    ones[i] = i < n ? 1.0 : 0.0;
+    katz[i] = 0.0;
+    lower[i] = 0.0;
+    upper[i] = ag;
 }
 
 __global__ void k_active_to_orig(const int32_t *act, int dense, int64_t m, const int32_t *perm,
@@ -1138,14 +1143,14 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         cudaStream_t st = g.stream;
         s.levels.emplace_back();
         s.levels.back().alloc(n + 1);
-        k_fill<<<nblk(n + 1, 256), 256, 0, st>>>(s.levels.back().p, n, 1.0); note_launch();  // engine.py:147
-        KB_CUDA(cudaMemsetAsync(s.levels.back().p + n, 0, sizeof(double), st));
         s.katz.alloc(n + 1);
         s.lower.alloc(n + 1);
         s.upper.alloc(n + 1);
-        KB_CUDA(cudaMemsetAsync(s.katz.p, 0, (n + 1) * sizeof(double), st));   // :148
-        KB_CUDA(cudaMemsetAsync(s.lower.p, 0, (n + 1) * sizeof(double), st));  // :149
-        k_fill<<<nblk(n + 1, 256), 256, 0, st>>>(s.upper.p, n + 1, alpha * gamma); note_launch();  // :151
+        // levels[0] = ones (engine.py:147), katz = lower = 0 (:148-149),
+        // upper = alpha * gamma (:151): one pass over the four vectors
+        k_init_state<<<nblk(n + 1, 256), 256, 0, st>>>(s.levels.back().p, s.katz.p, s.lower.p,
+                                                       s.upper.p, n, alpha * gamma);
+        note_launch();
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
         s.act[0].alloc(n);
         s.act[1].alloc(n);
