@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g97_tests.log 2>&1; echo "tests $?"
-for i in 1 2; do timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/g97_c2_$i.log 2>&1; echo "c2 $?"; done
+timeout 1500 python bench.py --scale 27 > gpurun_out/g98_c3.log 2>&1; echo "c3 $?"
+timeout 900 python bench.py > gpurun_out/g98_c2.log 2>&1; echo "c2 $?"
