@@ -226,10 +226,12 @@ __global__ void k_init_state(double *ones, double *katz, double *lower, double *
                              int64_t n, double ag) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
-    ones[i] = i < n ? 1.0 : 0.0;
-    katz[i] = 0.0;
-    lower[i] = 0.0;
-    upper[i] = ag;
+    if (ones) ones[i] = i < n ? 1.0 : 0.0;
+    if (katz) {
+        katz[i] = 0.0;
+        lower[i] = 0.0;
+        upper[i] = ag;
+    }
 }
 
 __global__ void k_active_to_orig(const int32_t *act, int dense, int64_t m, const int32_t *perm,
@@ -298,6 +300,33 @@ int guarded(F &&f) {
 void use_device(int dev) { KB_CUDA(cudaSetDevice(dev)); }
 
 }  // namespace
+
+void ensure_init(State &s) {
+    // katz, lower, upper (and levels[0] with them) when nothing wrote them yet
+    if (!s.init_pending) return;
+    const int64_t n = s.g->n;
+    k_init_state<<<nblk(n + 1, 256), 256, 0, s.g->stream>>>(
+        s.ones_pending && s.level_base == 0 ? s.levels[0].p : nullptr, s.katz.p, s.lower.p,
+        s.upper.p, n, s.alpha * s.gamma);
+    note_launch();
+    KB_CUDA(cudaGetLastError());
+    s.init_pending = s.ones_pending = false;
+}
+
+void ensure_ones(State &s) {
+    // levels[0] (all ones), for the readers of that level only
+    ensure_init(s);
+    if (!s.ones_pending) return;
+    if (s.level_base == 0 && !s.levels.empty()) {
+        const int64_t n = s.g->n;
+        k_init_state<<<nblk(n + 1, 256), 256, 0, s.g->stream>>>(s.levels[0].p, nullptr, nullptr,
+                                                                nullptr, n, 0.0);
+        note_launch();
+        KB_CUDA(cudaGetLastError());
+    }
+    s.ones_pending = false;
+}
+
 }  // namespace kb
 
 using namespace kb;
@@ -512,6 +541,7 @@ int kb_state_set_active(kb_state *h, const int64_t *ids, int64_t m) {
         State &s = h->s;
         KB_REQUIRE(m >= 0 && m <= s.g->n, KB_EPARAM, "bad active size");
         use_device(s.g->device);
+        ensure_init(h->s);
         cudaStream_t st = s.g->stream;
         DBuf<int64_t> d;
         d.alloc(std::max<int64_t>(1, m));
@@ -538,6 +568,7 @@ int kb_state_set_active_range(kb_state *h, int64_t lo, int64_t hi) {
         KB_REQUIRE(0 <= lo && lo <= hi && hi <= s.g->n, KB_EPARAM, "bad active range");
         KB_REQUIRE(!s.g->relabel, KB_EPARAM, "active ranges need a KB_GRAPH_NO_RELABEL graph");
         use_device(s.g->device);
+        ensure_init(h->s);
         const int64_t m = hi - lo;
         if (m) {
             k_range32<<<nblk(m, 256), 256, 0, s.g->stream>>>(lo, m, s.act[s.cur].p);
@@ -552,6 +583,8 @@ int kb_state_vector_ptr(kb_state *h, int which, int64_t level, void **ptr) {
     return guarded([&] {
         KB_REQUIRE(h && ptr, KB_EPARAM, "NULL argument");
         State &s = h->s;
+        use_device(s.g->device);
+        ensure_ones(s);
         switch (which) {
             case KB_VEC_LEVEL: {
                 const int64_t idx = level - s.level_base;
@@ -586,6 +619,7 @@ int kb_check_local_topk(kb_state *h, int64_t k, uint64_t *keys, int64_t *labels,
         State &s = h->s;
         KB_REQUIRE(s.r >= 1, KB_ESTATE, "check_converged needs at least one iteration");
         use_device(s.g->device);
+        ensure_init(h->s);
         local_topk(s, s.g->stream, k, keys, labels, uppers, count);
     });
 }
@@ -595,6 +629,7 @@ int kb_check_apply_cut(kb_state *h, uint64_t kstar, int64_t istar, int64_t *acti
         KB_REQUIRE(h && active, KB_EPARAM, "NULL argument");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_init(h->s);
         apply_cut(s, s.g->stream, kstar, istar);
         *active = s.m_host;
     });
@@ -687,6 +722,7 @@ int kb_ranking_snapshot(kb_state *h, kb_ranking **out, int64_t *separated_pairs)
         KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_init(h->s);
         auto *r = new kb_ranking();
         try {
             r->device = s.g->device;
@@ -737,6 +773,7 @@ int kb_shard_propose(kb_state *h, int64_t k, void *block) {
     return guarded([&] {
         KB_REQUIRE(h && block, KB_EPARAM, "NULL argument");
         use_device(h->s.g->device);
+        ensure_init(h->s);
         shard_propose(h->s, h->s.g->stream, k, (unsigned long long *)block);
         KB_CUDA(cudaGetLastError());
     });
@@ -746,6 +783,7 @@ int kb_shard_cut(kb_state *h, const void *blocks, int64_t nblocks, int64_t k, vo
     return guarded([&] {
         KB_REQUIRE(h && blocks && word, KB_EPARAM, "NULL argument");
         use_device(h->s.g->device);
+        ensure_init(h->s);
         shard_cut(h->s, h->s.g->stream, (const unsigned long long *)blocks, nblocks, k,
                   (long long *)word);
         KB_CUDA(cudaGetLastError());
@@ -773,6 +811,7 @@ int kb_shard_iterate_spec(kb_state *h, const long long *word, int64_t k) {
         KB_REQUIRE(h && word && k >= 1, KB_EPARAM, "bad argument");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_init(h->s);
         KB_REQUIRE(s.g->version == s.graph_version, KB_ESTATE,
                    "graph changed since init; static iteration would be unsound");
         KB_REQUIRE(s.r < s.max_iter, KB_ECONVERGENCE, "iteration cap reached");
@@ -796,6 +835,8 @@ int kb_state_rollback(kb_state *h) {
     return guarded([&] {
         KB_REQUIRE(h, KB_EPARAM, "NULL state");
         State &s = h->s;
+        use_device(s.g->device);
+        ensure_init(s);
         KB_REQUIRE(s.r >= 1 && s.levels.size() >= 2, KB_ESTATE, "no level to roll back");
         s.levels.pop_back();
         s.r -= 1;
@@ -808,6 +849,7 @@ int kb_rank_gathered(kb_state *h, int64_t n, int64_t *order, double *lower, doub
     return guarded([&] {
         KB_REQUIRE(h && n >= 1, KB_EPARAM, "bad argument");
         use_device(h->s.g->device);
+        ensure_init(h->s);
         rank_gathered(h->s, n, order, lower, upper, separated_pairs);
     });
 }
@@ -1061,6 +1103,8 @@ int kb_state_exchange(kb_state *h, int on) {
     return guarded([&] {
         KB_REQUIRE(h, KB_EPARAM, "NULL state");
         State &s = h->s;
+        use_device(s.g->device);
+        ensure_init(s);
         if (on) {
             KB_REQUIRE(s.g->exch[0], KB_ESTATE, "exchange buffers not allocated");
             KB_REQUIRE(!s.keep_all, KB_ESTATE, "the exchange keeps two levels: keep_levels=0");
@@ -1147,10 +1191,17 @@ int kb_state_create(kb_graph *gh, double alpha, double gamma, int undirected, in
         s.lower.alloc(n + 1);
         s.upper.alloc(n + 1);
         // levels[0] = ones (engine.py:147), katz = lower = 0 (:148-149),
-        // upper = alpha * gamma (:151): one pass over the four vectors
-        k_init_state<<<nblk(n + 1, 256), 256, 0, st>>>(s.levels.back().p, s.katz.p, s.lower.p,
-                                                       s.upper.p, n, alpha * gamma);
-        note_launch();
+        // upper = alpha * gamma (:151): one pass over the four vectors -- or,
+        // on a fresh degree-relabelled layout, none: the first K1 (the ones
+        // step) writes katz, lower and upper itself, and every other entry
+        // point writes what it would read first (ensure_init / ensure_ones)
+        if (tune_get("init.lazy", 1) && g.implicit_rows && !g.mutated) {
+            s.init_pending = s.ones_pending = true;
+        } else {
+            k_init_state<<<nblk(n + 1, 256), 256, 0, st>>>(s.levels.back().p, s.katz.p, s.lower.p,
+                                                           s.upper.p, n, alpha * gamma);
+            note_launch();
+        }
         s.seg_sum.alloc(std::max<int64_t>(1, g.sell.nseg));
         s.act[0].alloc(n);
         s.act[1].alloc(n);
@@ -1251,6 +1302,7 @@ int kb_check(kb_state *h, int *converged) {
         KB_REQUIRE(h && converged, KB_EPARAM, "NULL argument");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_init(h->s);
         *converged = run_check(s, s.g->stream) ? 1 : 0;
     });
 }
@@ -1349,6 +1401,7 @@ int kb_gap(kb_state *h, double *gap) {
     return guarded([&] {
         KB_REQUIRE(h && gap, KB_EPARAM, "NULL argument");
         use_device(h->s.g->device);
+        ensure_init(h->s);
         *gap = run_gap(h->s, h->s.g->stream);
     });
 }
@@ -1360,6 +1413,7 @@ int kb_epsilon_separated(kb_state *h, int64_t w, int64_t v, int *sep) {
         KB_REQUIRE(w >= 0 && w < s.g->n, KB_EPARAM, "node id outside graph");
         KB_REQUIRE(v >= 0 && v < s.g->n, KB_EPARAM, "node id outside graph");
         use_device(s.g->device);
+        ensure_init(h->s);
         cudaStream_t st = s.g->stream;
         k_sep_one<<<1, 1, 0, st>>>(s.lower.p, s.upper.p, s.g->iperm.p, w, v, s.eps,
                                    s.scratch_u64.p); note_launch();
@@ -1373,6 +1427,7 @@ int kb_result(kb_state *h, int64_t *order, double *lower, double *upper, int64_t
     return guarded([&] {
         KB_REQUIRE(h, KB_EPARAM, "NULL state");
         use_device(h->s.g->device);
+        ensure_init(h->s);
         run_result(h->s, h->s.g->stream, order, lower, upper, pairs);
     });
 }
@@ -1381,6 +1436,7 @@ int kb_separated_pairs(kb_state *h, int64_t *pairs) {
     return guarded([&] {
         KB_REQUIRE(h && pairs, KB_EPARAM, "NULL argument");
         use_device(h->s.g->device);
+        ensure_init(h->s);
         run_result(h->s, h->s.g->stream, nullptr, nullptr, nullptr, pairs);
     });
 }
@@ -1390,6 +1446,7 @@ int kb_get_vector(kb_state *h, int which, int64_t level, double *out) {
         KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_ones(h->s);
         const double *src = nullptr;
         switch (which) {
             case KB_VEC_LEVEL: {
@@ -1418,6 +1475,7 @@ int kb_get_active(kb_state *h, int64_t *out) {
         KB_REQUIRE(h && out, KB_EPARAM, "NULL argument");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_init(h->s);
         cudaStream_t st = s.g->stream;
         materialize_bounds(s, st);
         materialize_rank_order(s, st);
@@ -1448,6 +1506,7 @@ int kb_update_batch(kb_state *h, const int64_t *ins, int64_t n_ins, const int64_
         KB_REQUIRE((n_ins == 0 || ins) && (n_dels == 0 || dels), KB_EPARAM, "NULL arc array");
         State &s = h->s;
         use_device(s.g->device);
+        ensure_ones(h->s);
         for (int64_t i = 0; i < 2 * n_ins; i++)
             KB_REQUIRE(ins[i] >= 0 && ins[i] < s.g->n, KB_ENODERANGE, "node id outside graph");
         for (int64_t i = 0; i < 2 * n_dels; i++)

@@ -308,6 +308,10 @@ struct State {
     bool act_dense = true;  // active == arange(n) (never materialised)
     int64_t tail_zero_from = 0;  // new ids >= this have lower == upper == 0
     bool zero_tail_exact = true; // and exactly those (no dynamic change yet)
+    // lazy initial vectors (engine.py:147-151): init_pending -- katz, lower,
+    // upper and levels[0] not written yet (the first K1's ones step writes
+    // the first three itself); ones_pending -- levels[0] (ones) not written
+    bool init_pending = false, ones_pending = false;
     DBuf<int32_t> cand;          // selection candidates (capacity n)
     DBuf<uint64_t> stK;          // staged keys/uppers/ids of the active set
     DBuf<double> stU;
@@ -382,6 +386,10 @@ void text_lines(TextScan &t, uint8_t *h_kind, int32_t *h_u, int32_t *h_v);
 void text_csr(TextScan &t, int64_t n, int undirected, const int64_t *h_extra, int64_t n_extra,
               DBuf<int64_t> &indptr, DBuf<int32_t> &indices, int64_t &nnz);
 void launch_iterate(State &s, cudaStream_t st);
+// write whatever initial vectors are still pending (ensure_init: all of
+// them; ensure_ones: levels[0]) -- before any read outside the first K1
+void ensure_init(State &s);
+void ensure_ones(State &s);
 void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_only);
 void collect_k1_times(State &s);
 void materialize_bounds(State &s, cudaStream_t st);

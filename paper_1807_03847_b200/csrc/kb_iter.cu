@@ -85,6 +85,7 @@ struct IterArgs {
     const int32_t *pair_perm;
     unsigned long long *pair_out, *pair_abort, *pair_pub, *pair_k1c;
     int64_t pair_level;
+    int fresh = 0;                  // ones step on a lazily initialised state: katz is 0
 };
 
 __device__ __forceinline__ bool aborted(const IterArgs &A) {
@@ -671,9 +672,25 @@ __global__ void k_ones_step(IterArgs A) {
     const int64_t vr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (vr >= A.nvr) return;
     const double s = (double)A.vlen[vr];
-    if (vr < A.nseg) A.seg_sum[vr] = s;
-    else epilogue(A, A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg), s);
+    if (vr < A.nseg) {
+        A.seg_sum[vr] = s;
+    } else {
+        const int64_t v = A.vrow ? A.vrow[vr - A.nseg] : A.nh + (vr - A.nseg);
+        if (A.fresh) epilogue_k(A, v, s, 0.0);   // katz_0 = 0 (not written yet)
+        else epilogue(A, v, s);
+    }
     if (A.npeer) __threadfence_system();
+}
+
+// the rows without arcs after the first step of a lazily initialised state:
+// katz = lower = upper = 0 (engine.py:148-149, then the collapse of :313-316)
+__global__ void k_fresh_tail(double *katz, double *lower, double *upper, int64_t nv,
+                             int64_t n) {
+    const int64_t i = nv + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    katz[i] = 0.0;
+    lower[i] = 0.0;
+    upper[i] = 0.0;
 }
 
 // heavy row h = combine its segment sums in segment order, then epilogue
@@ -1038,6 +1055,16 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
     }
     const bool ones = !s.levels.empty() && s.level_base == 0 && x == s.levels[0].p &&
                       tune_get("k1.ones_shortcut", 1);
+    // lazily initialised state: the ones step writes katz, lower and upper
+    // itself (katz_0 = 0); any other first K1 needs the initial vectors
+    const bool fresh = s.init_pending && ones && !level_only && g.implicit_rows && !s.exch_on;
+    if (s.init_pending && !fresh) ensure_init(s);
+    if (s.ones_pending && !ones && !s.levels.empty() && s.level_base == 0 &&
+        x == s.levels[0].p)
+        ensure_ones(s);
+    A.fresh = fresh ? 1 : 0;
+    if (fresh && g.nh)     // heavy rows fold in k_heavy_combine, which adds to katz
+        KB_CUDA(cudaMemsetAsync(s.katz.p, 0, g.nh * sizeof(double), st));
     // host-side setup first, so the events bracket only device work
     const int depth = (int)tune_get("k1.depth", 1);
     const int xl = (int)tune_get("k1.xload", 0);
@@ -1189,7 +1216,12 @@ void run_spmv(State &s, cudaStream_t st, const double *x, double *w, bool level_
         note_launch();
         KB_CUDA(cudaGetLastError());
     }
-    if (g.implicit_rows && s.r == 0 && !level_only && n > g.nv) {
+    if (fresh) {
+        k_fresh_tail<<<(unsigned)((n + 1 - g.nv + 255) / 256), 256, 0, st>>>(
+            s.katz.p, s.lower.p, s.upper.p, g.nv, n); note_launch();
+        KB_CUDA(cudaGetLastError());
+        s.init_pending = false;           // levels[0] stays pending (ones_pending)
+    } else if (g.implicit_rows && s.r == 0 && !level_only && n > g.nv) {
         // rows without arcs: bounds collapse to katz (= 0) after the first step
         k_empty_rows<<<(unsigned)((n - g.nv + 255) / 256), 256, 0, st>>>(
             s.upper.p, s.lower.p, s.katz.p, g.nv, n); note_launch();
