@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g99_tests.log 2>&1; echo "tests $?"
-bash tools/checked_suite.sh
-for l in 0 1; do
-  KB_TUNE="init.lazy=$l" timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/g99_c2_l$l.log 2>&1; echo "c2 l=$l $?"
-done
+timeout 900 python bench.py > gpurun_out/g100_c2.log 2>&1; echo "c2 $?"
+timeout 900 python bench.py --workload c5 > gpurun_out/g100_c5.log 2>&1; echo "c5 $?"
+timeout 900 python bench.py --workload c4 > gpurun_out/g100_c4.log 2>&1; echo "c4 $?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/g100_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/g100_ncu.log 2>&1; echo "ncu $?"
