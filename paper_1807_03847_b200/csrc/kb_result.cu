@@ -41,6 +41,155 @@ __global__ void k_sort_keys(const double *lower, const int32_t *iperm, const int
     nids[i] = v;
 }
 
+// the same, with each block's key range to part[2 * block] (a grid-wide
+// atomic pair per warp serialised at C2), reduced by k_range_reduce
+__global__ void k_sort_keys_range(const double *lower, const int32_t *iperm, const int32_t *ids,
+                                  int64_t npos, uint64_t *keys, int32_t *nids,
+                                  unsigned long long *part) {
+    __shared__ unsigned long long slo[32], shi[32];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    if (i < npos) {
+        const int32_t v = iperm[ids[i]];
+        const unsigned long long k = ~(uint64_t)__double_as_longlong(lower[v]);
+        keys[i] = k;
+        nids[i] = v;
+        lo = hi = k;
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) { slo[w] = lo; shi[w] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < nw; q++) { lo = min(lo, slo[q]); hi = max(hi, shi[q]); }
+        part[2 * blockIdx.x] = lo;
+        part[2 * blockIdx.x + 1] = hi;
+    }
+}
+
+__global__ void k_range_reduce(const unsigned long long *part, int64_t nb,
+                               unsigned long long *mm) {
+    __shared__ unsigned long long slo[32], shi[32];
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+        lo = min(lo, part[2 * b]);
+        hi = max(hi, part[2 * b + 1]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) { slo[w] = lo; shi[w] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < nw; q++) { lo = min(lo, slo[q]); hi = max(hi, shi[q]); }
+        mm[0] = lo;
+        mm[1] = hi;
+    }
+}
+
+__global__ void k_offset_keys(uint64_t *keys, int64_t n, const unsigned long long *mm) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) keys[i] -= mm[0];
+}
+
+// After a stable sort on bits [shift, 64) of the offset keys, a run of equal
+// prefixes is in input (ascending id) order, which is the final order unless
+// its low bits disagree.  Each run holding such a disagreement is found once
+// (by its first element), listed, and put in order by one thread: an
+// insertion sort on the full offset key that only moves past strictly
+// greater keys, so equal keys keep ascending ids.  Runs longer than FIX_MAX
+// (or walks past it) set the fallback flag.
+constexpr int FIX_MAX = 512;
+
+__global__ void k_fix_find(const uint64_t *k, int64_t n, int shift, unsigned int *claimed,
+                           int64_t *runs, int64_t cap, unsigned long long *nruns,
+                           unsigned long long *fallback) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < 1 || i >= n) return;
+    if ((k[i - 1] >> shift) != (k[i] >> shift) || k[i - 1] <= k[i]) return;
+    const uint64_t p = k[i] >> shift;
+    int64_t a = i - 1;
+    while (a > 0 && (k[a - 1] >> shift) == p) {
+        if (i - a > FIX_MAX) { atomicExch(fallback, 1ull); return; }
+        a--;
+    }
+    // claim the run by its first element (one flag bit per element)
+    const unsigned int bit = 1u << (a & 31);
+    if (atomicOr(&claimed[a >> 5], bit) & bit) return;
+    int64_t b = i + 1;
+    while (b < n && (k[b] >> shift) == p) {
+        if (b - a > FIX_MAX) { atomicExch(fallback, 1ull); return; }
+        b++;
+    }
+    const unsigned long long slot = atomicAdd(nruns, 1ull);
+    if ((int64_t)slot >= cap) { atomicExch(fallback, 1ull); return; }
+    runs[2 * slot] = a;
+    runs[2 * slot + 1] = b;
+}
+
+// one warp per listed run: (key, position) pairs into shared memory, a
+// bitonic sort there (the position keeps equal keys in input order), back
+constexpr int FIX_WARPS = 4;
+
+__global__ void __launch_bounds__(32 * FIX_WARPS) k_fix_runs(uint64_t *k, int32_t *ids,
+                                                             const int64_t *runs, int64_t cap,
+                                                             const unsigned long long *nruns) {
+    __shared__ uint64_t sk[FIX_WARPS][FIX_MAX];
+    __shared__ int32_t sp[FIX_WARPS][FIX_MAX];
+    __shared__ int32_t si[FIX_WARPS][FIX_MAX];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned long long nr = min(*nruns, (unsigned long long)cap);
+    for (unsigned long long r = (unsigned long long)blockIdx.x * FIX_WARPS + w; r < nr;
+         r += (unsigned long long)gridDim.x * FIX_WARPS) {
+        const int64_t a = runs[2 * r];
+        const int L = (int)(runs[2 * r + 1] - a);
+        int P = 1;
+        while (P < L) P <<= 1;
+        for (int i = lane; i < P; i += 32) {
+            sk[w][i] = i < L ? k[a + i] : ~0ull;
+            sp[w][i] = i < L ? i : 0x7fffffff;
+            si[w][i] = i < L ? ids[a + i] : 0;
+        }
+        __syncwarp();
+        for (int size = 2; size <= P; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = lane; i < P; i += 32) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const bool up = (i & size) == 0;
+                        const bool gt = sk[w][i] > sk[w][j] ||
+                                        (sk[w][i] == sk[w][j] && sp[w][i] > sp[w][j]);
+                        if (gt == up) {
+                            const uint64_t tk = sk[w][i]; sk[w][i] = sk[w][j]; sk[w][j] = tk;
+                            const int32_t tp = sp[w][i]; sp[w][i] = sp[w][j]; sp[w][j] = tp;
+                            const int32_t ti = si[w][i]; si[w][i] = si[w][j]; si[w][j] = ti;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int i = lane; i < L; i += 32) {
+            k[a + i] = sk[w][i];
+            ids[a + i] = si[w][i];
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_restore_orig(const uint64_t *ks, const unsigned long long *mm,
+                               const int32_t *snids, const int32_t *perm, int64_t n,
+                               uint64_t *kout, int32_t *order) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    kout[i] = ks[i] + mm[0];
+    order[i] = perm[snids[i]];
+}
+
 __global__ void k_new_to_orig(const int32_t *perm, const int32_t *nids, int64_t n, int32_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) KB_DCHECK(nids[i] >= 0);
@@ -222,6 +371,68 @@ static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_
 
 // ranking_result on the device: order (int64 original ids), lower and upper
 // by original id, and the exact separated-pair count
+// The ranking order with fewer radix passes (round 2): the keys are offset
+// by their minimum, so they vary in B low bits; a stable CUB sort on the top
+// min(B, 40) of them -- 5 onesweep passes instead of 8 at C2, where B = 57 --
+// is followed by the fix-up of the equal-prefix runs whose low bits disagree
+// (C2: ~12K runs of <= 97 keys).  B <= 56 (the grid) sorts every varying
+// bit, with no fix-up.  Writes kout (full keys, ascending), snids and the
+// order; false = not applicable / fall back (run too long, too many runs).
+static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64_t npos,
+                        DBuf<uint64_t> &kin, DBuf<int32_t> &nids, DBuf<uint64_t> &kout,
+                        DBuf<int32_t> &snids, int32_t *order) {
+    Graph &g = *s.g;
+    unsigned long long *mm = s.scratch_u64.p + 32;   // min, max, runs, fallback
+    KB_CUDA(cudaMemsetAsync(mm + 2, 0, 16, st));
+    const int64_t nb = (int64_t)nblk(npos, 256);
+    DBuf<unsigned long long> part;
+    part.alloc(2 * nb);
+    k_sort_keys_range<<<(unsigned)nb, 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
+                                                    nids.p, part.p);
+    k_range_reduce<<<1, 1024, 0, st>>>(part.p, nb, mm);
+    note_launch(2);
+    unsigned long long h[2];
+    KB_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, st));
+    KB_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long d = h[1] - h[0];
+    int B = 0;
+    while (B < 64 && (d >> B)) B++;
+    const int HB = (int)tune_get("result.prefix_bits", 40);
+    const int exact = (int)tune_get("result.prefix_exact_bits", 56);  // sort all bits up to this
+    const int shift = B <= exact ? 0 : std::max(0, B - HB);
+    k_offset_keys<<<nblk(npos, 256), 256, 0, st>>>(kin.p, npos, mm);
+    note_launch();
+    if (B == 0) {
+        KB_CUDA(cudaMemcpyAsync(kout.p, kin.p, npos * 8, cudaMemcpyDeviceToDevice, st));
+        KB_CUDA(cudaMemcpyAsync(snids.p, nids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+        cub_do([&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, kin.p, kout.p, nids.p, snids.p, npos,
+                                                   shift, B, st);
+        });
+    }
+    if (shift > 0) {
+        const int64_t cap = std::min<int64_t>(npos, (int64_t)1 << 20);
+        DBuf<unsigned int> claimed;
+        DBuf<int64_t> runs;
+        claimed.alloc((npos + 31) / 32);
+        runs.alloc(2 * cap);
+        KB_CUDA(cudaMemsetAsync(claimed.p, 0, claimed.bytes(), st));
+        k_fix_find<<<nblk(npos, 256), 256, 0, st>>>(kout.p, npos, shift, claimed.p, runs.p, cap,
+                                                    mm + 2, mm + 3);
+        k_fix_runs<<<8 * g.sm_count, 32 * FIX_WARPS, 0, st>>>(kout.p, snids.p, runs.p, cap,
+                                                              mm + 2);
+        note_launch(2);
+        // mm[3] (a run too long, too many runs) is read with the pair count;
+        // the caller then redoes the ranking with the full sort
+    }
+    k_restore_orig<<<nblk(npos, 256), 256, 0, st>>>(kout.p, mm, snids.p, g.perm.p, npos, kout.p,
+                                                    order);
+    note_launch();
+    KB_CUDA(cudaGetLastError());
+    return true;
+}
+
 void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<double> *lower,
                    DBuf<double> *upper, int64_t *h_pairs) {
     NvtxRange nv("K3 ranking_result");
@@ -258,7 +469,11 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
     KB_CUDA(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), st));
     // +4: the own sort loads tiles in 16-byte chunks (kb_sort.cu)
     kin.alloc(npos + 4); kout.alloc(npos + 4); nids.alloc(npos + 4); snids.alloc(npos + 4);
-    if (npos) {
+    bool sorted = false;
+    if (npos >= (1 << 16) && npos < ((int64_t)1 << 31) && tune_get("result.prefix_sort", 1) &&
+        !tune_get("result.own_sort", 0))
+        sorted = sort_prefix(s, st, pos_ids, npos, kin, nids, kout, snids, order.p);
+    if (npos && !sorted) {
         k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
                                                      nids.p);
         note_launch();
@@ -286,9 +501,25 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
         upper->alloc(n);
         gather_to_original(g, s.upper.p, upper->p, st);
     }
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, fallback = 0;
     KB_CUDA(cudaMemcpyAsync(&pairs, u + 2, sizeof(pairs), cudaMemcpyDeviceToHost, st));
+    if (sorted) KB_CUDA(cudaMemcpyAsync(&fallback, u + 35, 8, cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
+    if (fallback) {   // the prefix sort's fix-up gave up: the full sort, redone
+        k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
+                                                     nids.p);
+        note_launch();
+        sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
+        k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order.p);
+        note_launch();
+        KB_CUDA(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), st));
+        if (n >= 2) sep_pairs(kout.p, snids.p, npos, s.upper.p, u + 2, g.sm_count, st);
+        if (order64) {
+            k_widen<<<nblk(n, 256), 256, 0, st>>>(order.p, n, order64->p); note_launch();
+        }
+        KB_CUDA(cudaMemcpyAsync(&pairs, u + 2, sizeof(pairs), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    }
     // zero-bound nodes have upper == 0: every positive lower separates them
     pairs += (unsigned long long)(n - npos) * (unsigned long long)npos;
     if (h_pairs) *h_pairs = (int64_t)pairs;

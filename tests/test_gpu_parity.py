@@ -329,3 +329,32 @@ def test_level1_check_shortcut_matches_the_general_check(case, k):
     for x, y in zip(a0[1:5], a1[1:5]):
         np.testing.assert_array_equal(x, y)
     assert a0[5] == a1[5] and a0[6] == a1[6]
+
+
+@pytest.mark.parametrize("bits", [40, 24, 8])
+def test_prefix_result_sort_matches_the_full_sort(bits):
+    """K3's prefix sort (a stable radix sort of the top varying key bits,
+    then the out-of-order equal-prefix runs fixed; too many or too long runs
+    fall back to the full sort) gives the full sort's order, sorted keys and
+    separated-pair count bit for bit.  8 prefix bits force the fallback."""
+    from paper_1807_03847_b200 import _lib
+    L = _lib.lib()
+    g0 = O.rmat_graph(1 << 18, edge_factor=8, seed=5)
+    g = P.Graph.from_csr(g0.node_count, g0.indptr, g0.indices)
+    out = {}
+    for prefix in (0, 1):
+        _lib.check(L.kb_tune(b"result.prefix_sort", prefix))
+        _lib.check(L.kb_tune(b"result.prefix_bits", bits))
+        _lib.check(L.kb_tune(b"result.prefix_exact_bits", 0))   # always prefix + fix-up
+        try:
+            st = P.init(g, P.Criterion.top_k(100, 1e-6), undirected=True)
+            res = P.run(st, g)
+            out[prefix] = (np.asarray(res.order).copy(), res.separated_fraction,
+                           np.asarray(res.lower).copy())
+        finally:
+            _lib.check(L.kb_tune(b"result.prefix_sort", 1))
+            _lib.check(L.kb_tune(b"result.prefix_bits", 40))
+            _lib.check(L.kb_tune(b"result.prefix_exact_bits", 56))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+    np.testing.assert_array_equal(out[0][2], out[1][2])

@@ -20,7 +20,7 @@ for name, g, crit in (("c2", lambda: G.rmat_graph(1 << 24, edge_factor=16, seed=
     key = ~lo[pos].view(np.uint64)
     mn, mx = key.min(), key.max()
     d = int(mx - mn)
-    for hb in (32, 28, 24):
+    for hb in tuple(int(x) for x in os.environ.get('HBITS', '32,28,24').split(',')):
         s = max(0, d.bit_length() - hb)
         hi = ((key - mn) >> np.uint64(s)).astype(np.uint64)
         o = np.argsort(hi, kind="stable")
