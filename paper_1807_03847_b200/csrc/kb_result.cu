@@ -181,14 +181,7 @@ __global__ void __launch_bounds__(32 * FIX_WARPS) k_fix_runs(uint64_t *k, int32_
     }
 }
 
-__global__ void k_restore_orig(const uint64_t *ks, const unsigned long long *mm,
-                               const int32_t *snids, const int32_t *perm, int64_t n,
-                               uint64_t *kout, int32_t *order) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    kout[i] = ks[i] + mm[0];
-    order[i] = perm[snids[i]];
-}
+
 
 __global__ void k_new_to_orig(const int32_t *perm, const int32_t *nids, int64_t n, int32_t *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -202,14 +195,16 @@ __global__ void k_new_to_orig(const int32_t *perm, const int32_t *nids, int64_t 
 // tight, so j is found by galloping down from t inside a small window that
 // neighbouring threads share (coalesced, cache resident).
 __global__ void k_sep_pairs_rank(const uint64_t *skeys, const int32_t *snids, int64_t npos,
-                                 const double *upper, unsigned long long *total) {
+                                 const double *upper, unsigned long long *total,
+                                 const unsigned long long *koff) {
     typedef cub::BlockReduce<unsigned long long, 256> Red;
     __shared__ typename Red::TempStorage tmp;
     unsigned long long acc = 0;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t < npos) {
         const double u = upper[snids[t]];
-        auto val = [&](int64_t j) { return __longlong_as_double((long long)~skeys[j]); };
+        const unsigned long long off = koff ? *koff : 0ull;
+        auto val = [&](int64_t j) { return __longlong_as_double((long long)~(skeys[j] + off)); };
         // invariant: val(hi) <= u ; find smallest j in [0, hi] with val(j) <= u
         int64_t hi = t, step = 1, lo = t;
         while (true) {
@@ -247,14 +242,18 @@ __global__ void __launch_bounds__(256) k_sep_pairs_tab(const uint64_t *skeys,
                                                        const int32_t *snids, int64_t npos,
                                                        const double *upper,
                                                        const uint64_t *__restrict__ tab, int64_t S,
-                                                       unsigned long long *total) {
+                                                       unsigned long long *total,
+                                                       const unsigned long long *koff) {
     typedef cub::BlockReduce<unsigned long long, 256> Red;
     __shared__ typename Red::TempStorage tmp;
     unsigned long long acc = 0;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t < npos) {
-        // lower(j) <= u  <=>  skeys[j] >= ~bits(u)  (keys ascend as lower descends)
-        const uint64_t ku = ~(uint64_t)__double_as_longlong(upper[snids[t]]);
+        // lower(j) <= u  <=>  skeys[j] >= ~bits(u)  (keys ascend as lower descends);
+        // keys offset by koff (the prefix sort): compare against ku - koff,
+        // which is 0 -- below every key -- when ku < koff
+        uint64_t ku = ~(uint64_t)__double_as_longlong(upper[snids[t]]);
+        if (koff) ku = ku < *koff ? 0ull : ku - *koff;
         int64_t hi = t, lo = -1, step = 1;
         bool found = false;
         for (int g = 0; g < SEP_GALLOP; g++) {
@@ -297,10 +296,11 @@ __global__ void k_widen(const int32_t *src, int64_t n, int64_t *dst) {
 // handled by the callers): galloping for near answers, a table for far ones
 static void sep_pairs(const uint64_t *skeys, const int32_t *snids, int64_t npos,
                       const double *upper, unsigned long long *total, int sms,
-                      cudaStream_t st) {
+                      cudaStream_t st, const unsigned long long *koff = nullptr) {
     if (npos <= 0) return;
     if (!tune_get("result.sep_table", 1) || npos < 4 * SEP_TAB) {
-        k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(skeys, snids, npos, upper, total);
+        k_sep_pairs_rank<<<nblk(npos, 256), 256, 0, st>>>(skeys, snids, npos, upper, total,
+                                                          koff);
         note_launch();
         return;
     }
@@ -308,7 +308,8 @@ static void sep_pairs(const uint64_t *skeys, const int32_t *snids, int64_t npos,
     DBuf<uint64_t> tab;
     tab.alloc(SEP_TAB);
     k_sep_tab<<<nblk(SEP_TAB, 256), 256, 0, st>>>(skeys, npos, S, tab.p);
-    k_sep_pairs_tab<<<nblk(npos, 256), 256, 0, st>>>(skeys, snids, npos, upper, tab.p, S, total);
+    k_sep_pairs_tab<<<nblk(npos, 256), 256, 0, st>>>(skeys, snids, npos, upper, tab.p, S, total,
+                                                     koff);
     (void)sms;
     note_launch(2);
     KB_CUDA(cudaGetLastError());
@@ -426,8 +427,8 @@ static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64
         // mm[3] (a run too long, too many runs) is read with the pair count;
         // the caller then redoes the ranking with the full sort
     }
-    k_restore_orig<<<nblk(npos, 256), 256, 0, st>>>(kout.p, mm, snids.p, g.perm.p, npos, kout.p,
-                                                    order);
+    // kout stays offset by mm[0]: sep_pairs compares against ku - mm[0]
+    k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order);
     note_launch();
     KB_CUDA(cudaGetLastError());
     return true;
@@ -487,7 +488,8 @@ void result_device(State &s, cudaStream_t st, DBuf<int64_t> *order64, DBuf<doubl
         note_launch();
     }
     if (n >= 2 && npos) {
-        sep_pairs(kout.p, snids.p, npos, s.upper.p, u + 2, g.sm_count, st);
+        sep_pairs(kout.p, snids.p, npos, s.upper.p, u + 2, g.sm_count, st,
+                  sorted ? s.scratch_u64.p + 32 : nullptr);
     }
     if (order64) {
         order64->alloc(n);

@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k prefix > gpurun_out/g106_test.log 2>&1; echo "test $?"
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g107_tests.log 2>&1; echo "tests $?"
+for i in 1 2; do timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/g107_c2_$i.log 2>&1; echo "c2 $?"; done
+timeout 600 python bench.py --workload c4 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/g107_c4.log 2>&1; echo "c4 $?"
