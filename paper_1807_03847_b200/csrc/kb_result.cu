@@ -398,7 +398,13 @@ static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64
     const unsigned long long d = h[1] - h[0];
     int B = 0;
     while (B < 64 && (d >> B)) B++;
-    const int HB = (int)tune_get("result.prefix_bits", 40);
+    // prefix width: ~16 bits above log2(npos), in whole 8-bit passes (C2,
+    // 8.9M keys: 40 bits -- 12.5K short runs to fix; C3, 63M keys: 48 bits,
+    // where 40 would leave runs of 4K keys)
+    int lg = 1;
+    while (lg < 62 && ((int64_t)1 << lg) < npos) lg++;
+    int HB = (int)tune_get("result.prefix_bits", 0);        // <= 0: the default
+    if (HB <= 0) HB = std::min(56, (lg + 16 + 7) / 8 * 8);
     const int exact = (int)tune_get("result.prefix_exact_bits", 56);  // sort all bits up to this
     const int shift = B <= exact ? 0 : std::max(0, B - HB);
     k_offset_keys<<<nblk(npos, 256), 256, 0, st>>>(kin.p, npos, mm);

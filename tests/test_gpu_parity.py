@@ -353,7 +353,7 @@ def test_prefix_result_sort_matches_the_full_sort(bits):
                            np.asarray(res.lower).copy())
         finally:
             _lib.check(L.kb_tune(b"result.prefix_sort", 1))
-            _lib.check(L.kb_tune(b"result.prefix_bits", 40))
+            _lib.check(L.kb_tune(b"result.prefix_bits", -1))     # back to the default
             _lib.check(L.kb_tune(b"result.prefix_exact_bits", 56))
     np.testing.assert_array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g107_tests.log 2>&1; echo "tests $?"
-for i in 1 2; do timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/g107_c2_$i.log 2>&1; echo "c2 $?"; done
-timeout 600 python bench.py --workload c4 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/g107_c4.log 2>&1; echo "c4 $?"
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q > gpurun_out/g109_tests.log 2>&1; echo "tests $?"
+for p in 0 1; do
+  KB_TUNE="result.prefix_sort=$p" timeout 1500 python bench.py --scale 27 --steps 3 --warmup 2 --no-cpu --no-e2e > gpurun_out/g109_c3_p$p.log 2>&1; echo "c3 p=$p $?"
+  KB_TUNE="result.prefix_sort=$p" timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/g109_c2_p$p.log 2>&1; echo "c2 p=$p $?"
+done

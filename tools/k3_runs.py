@@ -9,7 +9,8 @@ import numpy as np  # noqa: E402
 import paper_1807_03847_b200 as P  # noqa: E402
 from paper_1807_03847_b200 import generators as G  # noqa: E402
 
-for name, g, crit in (("c2", lambda: G.rmat_graph(1 << 24, edge_factor=16, seed=42),
+SCALE = int(os.environ.get("SCALE", "24"))
+for name, g, crit in (("c%d" % (2 if SCALE == 24 else 3), lambda: G.rmat_graph(1 << SCALE, edge_factor=16, seed=42),
                        P.Criterion.top_k(100, 1e-6)),
                       ("c4", lambda: G.grid_graph(1 << 24), P.Criterion.ranking(1e-9))):
     g = g()
