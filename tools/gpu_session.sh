@@ -1,3 +1,5 @@
+# scratch driver for one gpurun call (edited per experiment); default: the
+# round-end self check plus the checked-build suite
 mkdir -p gpurun_out
-timeout 1500 python bench.py --scale 27 > gpurun_out/fin3_c3.log 2>&1; echo "c3 $?"
-timeout 900 python bench.py > gpurun_out/fin3_c2.log 2>&1; echo "c2 $?"
+bash tools/round_check.sh
+bash tools/checked_suite.sh
