@@ -1,5 +1,2 @@
-# scratch driver for one gpurun call (edited per experiment); default: the
-# round-end self check plus the checked-build suite
 mkdir -p gpurun_out
-bash tools/round_check.sh
-bash tools/checked_suite.sh
+timeout 600 python tools/step_phases.py > gpurun_out/g110_phases.log 2>&1; echo "ph $?"
