@@ -379,17 +379,17 @@ static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_
 // (C2: ~12K runs of <= 97 keys).  B <= 56 (the grid) sorts every varying
 // bit, with no fix-up.  Writes kout (full keys, ascending), snids and the
 // order; false = not applicable / fall back (run too long, too many runs).
-static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64_t npos,
-                        DBuf<uint64_t> &kin, DBuf<int32_t> &nids, DBuf<uint64_t> &kout,
-                        DBuf<int32_t> &snids, int32_t *order) {
-    Graph &g = *s.g;
-    unsigned long long *mm = s.scratch_u64.p + 32;   // min, max, runs, fallback
+static bool sort_prefix_core(const double *lower, const int32_t *iperm, const int32_t *pos_ids,
+                             int64_t npos, DBuf<uint64_t> &kin, DBuf<int32_t> &nids,
+                             DBuf<uint64_t> &kout, DBuf<int32_t> &snids, unsigned long long *mm,
+                             int sms, cudaStream_t st) {
+    // mm (device, 4 words): key minimum, maximum, fix-up run count, fallback
     KB_CUDA(cudaMemsetAsync(mm + 2, 0, 16, st));
     const int64_t nb = (int64_t)nblk(npos, 256);
     DBuf<unsigned long long> part;
     part.alloc(2 * nb);
-    k_sort_keys_range<<<(unsigned)nb, 256, 0, st>>>(s.lower.p, g.iperm.p, pos_ids, npos, kin.p,
-                                                    nids.p, part.p);
+    k_sort_keys_range<<<(unsigned)nb, 256, 0, st>>>(lower, iperm, pos_ids, npos, kin.p, nids.p,
+                                                    part.p);
     k_range_reduce<<<1, 1024, 0, st>>>(part.p, nb, mm);
     note_launch(2);
     unsigned long long h[2];
@@ -427,16 +427,28 @@ static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64
         KB_CUDA(cudaMemsetAsync(claimed.p, 0, claimed.bytes(), st));
         k_fix_find<<<nblk(npos, 256), 256, 0, st>>>(kout.p, npos, shift, claimed.p, runs.p, cap,
                                                     mm + 2, mm + 3);
-        k_fix_runs<<<8 * g.sm_count, 32 * FIX_WARPS, 0, st>>>(kout.p, snids.p, runs.p, cap,
-                                                              mm + 2);
+        k_fix_runs<<<8 * sms, 32 * FIX_WARPS, 0, st>>>(kout.p, snids.p, runs.p, cap, mm + 2);
         note_launch(2);
         // mm[3] (a run too long, too many runs) is read with the pair count;
         // the caller then redoes the ranking with the full sort
     }
-    // kout stays offset by mm[0]: sep_pairs compares against ku - mm[0]
+    KB_CUDA(cudaGetLastError());
+    return true;      // kout stays offset by mm[0]: sep_pairs compares against ku - mm[0]
+}
+
+// The ranking order with fewer radix passes (round 2): the keys are offset
+// by their minimum, so they vary in B low bits; a stable CUB sort on the top
+// ~log2(n) + 16 of them (whole 8-bit passes) is followed by the fix-up of
+// the equal-prefix runs whose low bits disagree.  Keys varying in <= 56 bits
+// (the grid) are sorted on all of them with no fix-up.
+static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64_t npos,
+                        DBuf<uint64_t> &kin, DBuf<int32_t> &nids, DBuf<uint64_t> &kout,
+                        DBuf<int32_t> &snids, int32_t *order) {
+    Graph &g = *s.g;
+    sort_prefix_core(s.lower.p, g.iperm.p, pos_ids, npos, kin, nids, kout, snids,
+                     s.scratch_u64.p + 32, g.sm_count, st);
     k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order);
     note_launch();
-    KB_CUDA(cudaGetLastError());
     return true;
 }
 
@@ -618,8 +630,8 @@ static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const
     DBuf<unsigned char> fpos, fzero;
     DBuf<uint64_t> kin, kout;
     DBuf<unsigned long long> u;
-    iota.alloc(n); ids.alloc(n); order.alloc(n); fpos.alloc(n); fzero.alloc(n); u.alloc(3);
-    KB_CUDA(cudaMemsetAsync(u.p, 0, 3 * 8, st));
+    iota.alloc(n); ids.alloc(n); order.alloc(n); fpos.alloc(n); fzero.alloc(n); u.alloc(8);
+    KB_CUDA(cudaMemsetAsync(u.p, 0, 8 * 8, st));
     k_iota32<<<nblk(n, 256), 256, 0, st>>>(n, iota.p);
     k_pos_flags<<<nblk(n, 256), 256, 0, st>>>(lo, iota.p, n, fpos.p, fzero.p, ids.p);
     note_launch(2);
@@ -640,17 +652,28 @@ static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const
     const int64_t npos = (int64_t)hc[0];
     // +4: the own sort loads tiles in 16-byte chunks (kb_sort.cu)
     kin.alloc(npos + 4); kout.alloc(npos + 4); nids.alloc(npos + 4); snids.alloc(npos + 4);
-    if (npos) {
+    int dev = 0, sms = 148;
+    KB_CUDA(cudaGetDevice(&dev));
+    KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // the prefix sort (sort_prefix_core) when large enough, as on one GPU
+    // (measured slower here than the full sort on the sharded C2 result,
+    // 13.4 vs 12.9 ms per step: kept behind result.prefix_gathered)
+    const bool prefix = npos >= (1 << 16) && npos < ((int64_t)1 << 31) &&
+                        tune_get("result.prefix_sort", 1) != 0 &&
+                        tune_get("result.prefix_gathered", 0) != 0;
+    auto full_sort = [&] {
         k_sort_keys<<<nblk(npos, 256), 256, 0, st>>>(lo, iota.p, ids.p, npos, kin.p, nids.p);
         note_launch();
         sort_keys_stable(kin.p, nids.p, npos, kout.p, snids.p, st);
         KB_CUDA(cudaMemcpyAsync(order.p, snids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
-        if (n >= 2) {
-            int dev = 0, sms = 148;
-            KB_CUDA(cudaGetDevice(&dev));
-            KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            sep_pairs(kout.p, snids.p, npos, up, u.p + 2, sms, st);
-        }
+        if (n >= 2) sep_pairs(kout.p, snids.p, npos, up, u.p + 2, sms, st);
+    };
+    if (npos && prefix) {
+        sort_prefix_core(lo, iota.p, ids.p, npos, kin, nids, kout, snids, u.p + 4, sms, st);
+        KB_CUDA(cudaMemcpyAsync(order.p, snids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
+        if (n >= 2) sep_pairs(kout.p, snids.p, npos, up, u.p + 2, sms, st, u.p + 4);
+    } else if (npos) {
+        full_sort();
     }
     if (n > npos)
         KB_CUDA(cudaMemcpyAsync(order.p + npos, zero_part.p, (n - npos) * 4,
@@ -662,9 +685,23 @@ static void rank_bounds_core(cudaStream_t st, int64_t n, const double *lo, const
         note_launch();
         download_d2h(h_order, wide.p, n * 8, st);
     }
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, fallback = 0;
     KB_CUDA(cudaMemcpyAsync(&pairs, u.p + 2, 8, cudaMemcpyDeviceToHost, st));
+    if (npos && prefix) KB_CUDA(cudaMemcpyAsync(&fallback, u.p + 7, 8, cudaMemcpyDeviceToHost, st));
     KB_CUDA(cudaStreamSynchronize(st));
+    if (fallback) {   // the prefix sort's fix-up gave up: the full sort, redone
+        KB_CUDA(cudaMemsetAsync(u.p + 2, 0, 8, st));
+        full_sort();
+        if (h_order) {
+            DBuf<int64_t> wide;
+            wide.alloc(n);
+            k_widen<<<nblk(n, 256), 256, 0, st>>>(order.p, n, wide.p);
+            note_launch();
+            download_d2h(h_order, wide.p, n * 8, st);
+        }
+        KB_CUDA(cudaMemcpyAsync(&pairs, u.p + 2, 8, cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+    }
     pairs += (unsigned long long)(n - npos) * (unsigned long long)npos;
     if (h_pairs) *h_pairs = (int64_t)pairs;
 }
