@@ -92,6 +92,23 @@ __global__ void k_range_reduce(const unsigned long long *part, int64_t nb,
     }
 }
 
+// keys already offset by a host-known floor K0 = ~bits(alpha * gamma): every
+// lower bound is <= the initial upper bound alpha * gamma (engine.py:151), so
+// every key is >= K0; a key below it (rounding at a bound that tight) sets
+// the fallback flag and the caller redoes the full sort
+__global__ void k_sort_keys_off(const double *lower, const int32_t *iperm, const int32_t *ids,
+                                int64_t npos, uint64_t *keys, int32_t *nids, uint64_t K0,
+                                uint64_t K1, unsigned long long *mm) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i == 0) mm[0] = K0;
+    if (i >= npos) return;
+    const int32_t v = iperm[ids[i]];
+    const uint64_t k = ~(uint64_t)__double_as_longlong(lower[v]);
+    if (k < K0 || k > K1) atomicOr(&mm[3], 1ull);   // outside the bounds: fall back
+    keys[i] = k - K0;
+    nids[i] = v;
+}
+
 __global__ void k_offset_keys(uint64_t *keys, int64_t n, const unsigned long long *mm) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) keys[i] -= mm[0];
@@ -382,20 +399,39 @@ static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_
 static bool sort_prefix_core(const double *lower, const int32_t *iperm, const int32_t *pos_ids,
                              int64_t npos, DBuf<uint64_t> &kin, DBuf<int32_t> &nids,
                              DBuf<uint64_t> &kout, DBuf<int32_t> &snids, unsigned long long *mm,
-                             int sms, cudaStream_t st) {
-    // mm (device, 4 words): key minimum, maximum, fix-up run count, fallback
+                             int sms, cudaStream_t st, double alpha = 0, double gamma = 0) {
+    // mm (device, 4 words): key offset (minimum), maximum, fix-up run count,
+    // fallback
     KB_CUDA(cudaMemsetAsync(mm + 2, 0, 16, st));
-    const int64_t nb = (int64_t)nblk(npos, 256);
-    DBuf<unsigned long long> part;
-    part.alloc(2 * nb);
-    k_sort_keys_range<<<(unsigned)nb, 256, 0, st>>>(lower, iperm, pos_ids, npos, kin.p, nids.p,
-                                                    part.p);
-    k_range_reduce<<<1, 1024, 0, st>>>(part.p, nb, mm);
-    note_launch(2);
-    unsigned long long h[2];
-    KB_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, st));
-    KB_CUDA(cudaStreamSynchronize(st));
-    const unsigned long long d = h[1] - h[0];
+    unsigned long long d;
+    const double ag = alpha * gamma;
+    if (alpha > 0 && ag >= alpha && tune_get("result.prefix_bound", 1)) {
+        // the key range from bounds the host knows, no device reduction, no
+        // host read: lower <= alpha * gamma (the initial upper bound) and
+        // every positive lower >= alpha (katz_1 of a row with an arc)
+        uint64_t bg, ba;
+        memcpy(&bg, &ag, 8);
+        memcpy(&ba, &alpha, 8);
+        const uint64_t K0 = ~bg, K1 = ~ba;
+        k_sort_keys_off<<<nblk(npos, 256), 256, 0, st>>>(lower, iperm, pos_ids, npos, kin.p,
+                                                         nids.p, K0, K1, mm);
+        note_launch();
+        d = K1 - K0;
+    } else {
+        const int64_t nb = (int64_t)nblk(npos, 256);
+        DBuf<unsigned long long> part;
+        part.alloc(2 * nb);
+        k_sort_keys_range<<<(unsigned)nb, 256, 0, st>>>(lower, iperm, pos_ids, npos, kin.p,
+                                                        nids.p, part.p);
+        k_range_reduce<<<1, 1024, 0, st>>>(part.p, nb, mm);
+        note_launch(2);
+        unsigned long long h[2];
+        KB_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, st));
+        KB_CUDA(cudaStreamSynchronize(st));
+        d = h[1] - h[0];
+        k_offset_keys<<<nblk(npos, 256), 256, 0, st>>>(kin.p, npos, mm);
+        note_launch();
+    }
     int B = 0;
     while (B < 64 && (d >> B)) B++;
     // prefix width: ~16 bits above log2(npos), in whole 8-bit passes (C2,
@@ -407,8 +443,6 @@ static bool sort_prefix_core(const double *lower, const int32_t *iperm, const in
     if (HB <= 0) HB = std::min(56, (lg + 16 + 7) / 8 * 8);
     const int exact = (int)tune_get("result.prefix_exact_bits", 56);  // sort all bits up to this
     const int shift = B <= exact ? 0 : std::max(0, B - HB);
-    k_offset_keys<<<nblk(npos, 256), 256, 0, st>>>(kin.p, npos, mm);
-    note_launch();
     if (B == 0) {
         KB_CUDA(cudaMemcpyAsync(kout.p, kin.p, npos * 8, cudaMemcpyDeviceToDevice, st));
         KB_CUDA(cudaMemcpyAsync(snids.p, nids.p, npos * 4, cudaMemcpyDeviceToDevice, st));
@@ -446,7 +480,7 @@ static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64
                         DBuf<int32_t> &snids, int32_t *order) {
     Graph &g = *s.g;
     sort_prefix_core(s.lower.p, g.iperm.p, pos_ids, npos, kin, nids, kout, snids,
-                     s.scratch_u64.p + 32, g.sm_count, st);
+                     s.scratch_u64.p + 32, g.sm_count, st, s.alpha, s.gamma);
     k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order);
     note_launch();
     return true;
