@@ -125,8 +125,10 @@ constexpr int FIX_MAX = 512;
 
 __global__ void k_fix_find(const uint64_t *k, int64_t n, int shift, unsigned int *claimed,
                            int64_t *runs, int64_t cap, unsigned long long *nruns,
-                           unsigned long long *fallback) {
+                           unsigned long long *fallback, const int32_t *ids = nullptr,
+                           const int32_t *perm = nullptr, int32_t *order = nullptr) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (order && i < n) order[i] = perm[ids[i]];   // the id map, fused (runs re-map theirs)
     if (i < 1 || i >= n) return;
     if ((k[i - 1] >> shift) != (k[i] >> shift) || k[i - 1] <= k[i]) return;
     const uint64_t p = k[i] >> shift;
@@ -155,7 +157,9 @@ constexpr int FIX_WARPS = 4;
 
 __global__ void __launch_bounds__(32 * FIX_WARPS) k_fix_runs(uint64_t *k, int32_t *ids,
                                                              const int64_t *runs, int64_t cap,
-                                                             const unsigned long long *nruns) {
+                                                             const unsigned long long *nruns,
+                                                             const int32_t *perm = nullptr,
+                                                             int32_t *order = nullptr) {
     __shared__ uint64_t sk[FIX_WARPS][FIX_MAX];
     __shared__ int32_t sp[FIX_WARPS][FIX_MAX];
     __shared__ int32_t si[FIX_WARPS][FIX_MAX];
@@ -193,6 +197,7 @@ __global__ void __launch_bounds__(32 * FIX_WARPS) k_fix_runs(uint64_t *k, int32_
         for (int i = lane; i < L; i += 32) {
             k[a + i] = sk[w][i];
             ids[a + i] = si[w][i];
+            if (order) order[a + i] = perm[si[w][i]];
         }
         __syncwarp();
     }
@@ -399,7 +404,10 @@ static void split_positive(State &s, cudaStream_t st, DBuf<int32_t> &ids, int32_
 static bool sort_prefix_core(const double *lower, const int32_t *iperm, const int32_t *pos_ids,
                              int64_t npos, DBuf<uint64_t> &kin, DBuf<int32_t> &nids,
                              DBuf<uint64_t> &kout, DBuf<int32_t> &snids, unsigned long long *mm,
-                             int sms, cudaStream_t st, double alpha = 0, double gamma = 0) {
+                             int sms, cudaStream_t st, double alpha = 0, double gamma = 0,
+                             const int32_t *perm = nullptr, int32_t *order = nullptr) {
+    // perm/order: also write order = perm[snids] (fused into the fix-up
+    // passes when there is one; returns whether it was written)
     // mm (device, 4 words): key offset (minimum), maximum, fix-up run count,
     // fallback
     KB_CUDA(cudaMemsetAsync(mm + 2, 0, 16, st));
@@ -460,14 +468,17 @@ static bool sort_prefix_core(const double *lower, const int32_t *iperm, const in
         runs.alloc(2 * cap);
         KB_CUDA(cudaMemsetAsync(claimed.p, 0, claimed.bytes(), st));
         k_fix_find<<<nblk(npos, 256), 256, 0, st>>>(kout.p, npos, shift, claimed.p, runs.p, cap,
-                                                    mm + 2, mm + 3);
-        k_fix_runs<<<8 * sms, 32 * FIX_WARPS, 0, st>>>(kout.p, snids.p, runs.p, cap, mm + 2);
+                                                    mm + 2, mm + 3, snids.p, perm, order);
+        k_fix_runs<<<8 * sms, 32 * FIX_WARPS, 0, st>>>(kout.p, snids.p, runs.p, cap, mm + 2,
+                                                      perm, order);
         note_launch(2);
         // mm[3] (a run too long, too many runs) is read with the pair count;
         // the caller then redoes the ranking with the full sort
+        KB_CUDA(cudaGetLastError());
+        return order != nullptr;
     }
     KB_CUDA(cudaGetLastError());
-    return true;      // kout stays offset by mm[0]: sep_pairs compares against ku - mm[0]
+    return false;     // kout stays offset by mm[0]: sep_pairs compares against ku - mm[0]
 }
 
 // The ranking order with fewer radix passes (round 2): the keys are offset
@@ -479,10 +490,12 @@ static bool sort_prefix(State &s, cudaStream_t st, const int32_t *pos_ids, int64
                         DBuf<uint64_t> &kin, DBuf<int32_t> &nids, DBuf<uint64_t> &kout,
                         DBuf<int32_t> &snids, int32_t *order) {
     Graph &g = *s.g;
-    sort_prefix_core(s.lower.p, g.iperm.p, pos_ids, npos, kin, nids, kout, snids,
-                     s.scratch_u64.p + 32, g.sm_count, st, s.alpha, s.gamma);
-    k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order);
-    note_launch();
+    if (!sort_prefix_core(s.lower.p, g.iperm.p, pos_ids, npos, kin, nids, kout, snids,
+                          s.scratch_u64.p + 32, g.sm_count, st, s.alpha, s.gamma, g.perm.p,
+                          order)) {
+        k_new_to_orig<<<nblk(npos, 256), 256, 0, st>>>(g.perm.p, snids.p, npos, order);
+        note_launch();
+    }
     return true;
 }
 
